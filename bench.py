@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 sketch engine on BASELINE.json's headline metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 2] [--kind countsketch]
+
+Workload (N=1): BASELINE config 2 -- dense fp64 A of 2^20 x 256
+(U diag(logspace(0,-8)) V^T, kappa = 1e8), b = A x + 1e-6 noise,
+CountSketch d = 2048.  A "step" is one pass of the hot path over one batch:
+S [A | b] by the CountSketch kernel (plus, for N > 1, the NCCL reduce of
+the d x (n+1) partials).  value = bytes of A and b sketched per second,
+whole job (weak scaling: every rank owns a 2^20-row block of an N*2^20-row
+problem).  Inputs are device-resident (2 GiB/step > 126 MB L2, so no L2
+flush is needed).  Reported beside it:
+
+* roofline  -- the CountSketch kernel's algorithmic bytes / CUDA-event time
+               against the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+* e2e       -- the same metric through the C-ABI host-buffer entry point
+               (skl_countsketch_dense_host: pinned host A/b in, host SA/Sb
+               out, H2D/D2H inside the timed call);
+* solves    -- full SAA solves/sec through the public API on device data
+               (operator build + sketch + QR + back-solve + residual), with
+               the QR time reported separately;
+* cpu_baseline -- the reference's algorithm (oracle port: scipy CSR @ A,
+               as sketch.py:209-212 does) timed on this host on a bounded
+               sample of the same workload.
+
+``--impl reference`` prints the reference arm: the same metric measured on
+the oracle port on the host cores (rank 0 only under torchrun).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        p = json.loads(PEAKS_FILE.read_text())
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    """dram bytes per launch of the CountSketch kernel from the committed
+    ncu --set full capture summary (profiles/*countsketch*_full.json)."""
+    best = None
+    for f in sorted((ROOT / "profiles").glob("*countsketch*full*.json")):
+        try:
+            best = json.loads(f.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    return best
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU arms
+def cpu_reference_sample(cfg, A_host: np.ndarray, b_host: np.ndarray, rows, signs, reps: int):
+    """Time the reference's algorithm (oracle port) on a row sample:
+    `sparse_map @ A` and `sparse_map @ b` as sketch.py:209-212 do.
+    Returns (GB/s, seconds per rep, sample description, cores)."""
+    from oracle import oracle as O
+
+    ms = A_host.shape[0]
+    smap = O.countsketch_map(rows[:ms].astype(np.int64), signs[:ms].astype(np.float64), cfg.d, ms)
+    bytes_ = 8 * A_host.size + 8 * b_host.size
+    smap @ A_host[: min(ms, 4096)]  # warm the code path
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        smap @ A_host
+        smap @ b_host
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return bytes_ / t / 1e9, t, times
+
+
+def run_reference_arm(args, cfg):
+    import torch
+
+    from paper_2409_14309_b200 import workloads as W
+    from paper_2409_14309_b200.rng import derive_seed
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # bounded sample of the same workload: the first ms rows of config 2
+    ms = 1 << 17
+    c = W.config(cfg.cfg, m=ms)
+    if torch.cuda.is_available():
+        A, b, _ = W.make_problem(c, backend="torch")
+        A_host = np.asfortranarray(A.cpu().numpy())
+        b_host = b.cpu().numpy()
+    else:
+        A_host, b_host, _ = W.make_problem(c)
+    from oracle import oracle as O
+
+    key = O.derive_seed(derive_seed(W.SEED, "saa"), "countsketch", cfg.m)
+    rows, signs = O.countsketch_draws(key, cfg.m, cfg.d)
+    times = []
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, A_host, b_host, rows, signs, 1)
+    for _ in range(args.steps):
+        _, t, _ = cpu_reference_sample(cfg, A_host, b_host, rows, signs, 1)
+        times.append(t)
+    t = statistics.median(times)
+    gbs = (8 * A_host.size + 8 * b_host.size) / t / 1e9
+    sample = (f"first {ms} of {cfg.m} rows of config {cfg.cfg} (A {ms}x{cfg.n} + b), "
+              f"scipy CSR @ A as sketch.py:209-212; median of {args.steps}")
+    line = {
+        "impl": "reference",
+        "metric": f"S·A sketch GB/s (config {cfg.cfg}: {cfg.kind} d={cfg.d}, dense {cfg.m}x{cfg.n} fp64)",
+        "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {cfg.cfg} CountSketch S[A|b], bounded host sample",
+                   "m_sample": ms, "n": cfg.n, "d": cfg.d},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2409_14309_b200 import workloads as W
+
+    cfg = W.config(args.config)
+    if cfg.kind != "countsketch" or cfg.gen == "csr":
+        cfg = W.config(args.config, kind="countsketch")
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_14309_b200 as E
+    from paper_2409_14309_b200 import _native
+    from paper_2409_14309_b200.distributed import ShardPlan, local_partial_device, shard_rows
+    from paper_2409_14309_b200.rng import derive_seed
+    from paper_2409_14309_b200.sketch import PLAN_CHUNK
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    # ---- data: every rank owns a full config-sized row block (weak scaling)
+    m_loc, n, d = cfg.m, cfg.n, cfg.d
+    m_total = m_loc * world
+    A, b, _ = W.make_problem(W.config(cfg.cfg, m=m_loc), seed=W.SEED + rank, backend="torch")
+    lda = int(A.stride(1))
+    spec = E.SketchSpec("countsketch", d, seed=derive_seed(W.SEED, "saa"))
+    t_build0 = time.perf_counter()
+    op = E.build_sketch(spec, m_total)
+    r0, r1 = shard_rows(m_total, world, rank)
+    assert r1 - r0 == m_loc
+    plan = ShardPlan(op, r0, r1)
+    plan.device_plan()
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build0
+
+    stream = torch.cuda.current_stream()
+    ld = (d + 1) // 2 * 2
+    out = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda").t()[:d]
+    ent, off = plan.device_plan()
+
+    def step():
+        _native.call("skl_countsketch_dense", A.data_ptr(), m_loc, n, lda, b.data_ptr(),
+                     ent.data_ptr(), off.data_ptr(), d, PLAN_CHUNK, out.data_ptr(), ld,
+                     out[:, n].data_ptr(), 1, 0, stream.cuda_stream)
+        if world > 1:
+            dist.reduce(out, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            k_ev[i][0].record(stream)
+            _native.call("skl_countsketch_dense", A.data_ptr(), m_loc, n, lda, b.data_ptr(),
+                         ent.data_ptr(), off.data_ptr(), d, PLAN_CHUNK, out.data_ptr(), ld,
+                         out[:, n].data_ptr(), 1, 0, stream.cuda_stream)
+            k_ev[i][1].record(stream)
+            if world > 1:
+                dist.reduce(out, dst=0)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    total_ms = start.elapsed_time(stop)
+    kern_ms = [a.elapsed_time(bb) for a, bb in k_ev]
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    bytes_local = W.algorithmic_bytes(W.config(cfg.cfg, m=m_loc))
+    value = bytes_local * world / (ms_per_step * 1e-3) / 1e9
+    kern_avg = statistics.mean(kern_ms)
+    achieved = bytes_local / (kern_avg * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+
+    # ---- full SAA solves through the public API (device data), QR separately
+    solve = None
+    if not args.no_solve and world == 1:
+        prob = E.LeastSquaresProblem(A=E.DenseMatrix(A), b=E.Vector(b))
+        sspec = E.SketchSpec("countsketch", 1, seed=W.SEED)
+        opts = E.SolverOptions(d_factor=d / n)
+        E.solve(prob, "saa", sspec, opts)  # warm (kernels, pools)
+        reps = 5
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            res = E.solve(prob, "saa", sspec, opts)
+        torch.cuda.synchronize()
+        solve_s = (time.perf_counter() - t0) / reps
+        # QR alone on the sketched matrix
+        from paper_2409_14309_b200.linalg import qr_solve_device
+
+        SAb = out
+        qa, qb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qr_solve_device(SAb[:, :n], ld, SAb[:, n], d, n)
+        torch.cuda.synchronize()
+        qa.record(stream)
+        for _ in range(reps):
+            qr_solve_device(SAb[:, :n], ld, SAb[:, n], d, n)
+        qb.record(stream)
+        torch.cuda.synchronize()
+        qr_ms = qa.elapsed_time(qb) / reps
+        solve = {"solves_per_sec": round(1.0 / solve_s, 3), "ms_per_solve": round(solve_s * 1e3, 3),
+                 "qr_solve_ms": round(qr_ms, 3), "residual": res.residual_norm,
+                 "operator_build_ms": round(build_s * 1e3, 2),
+                 "includes": "build_sketch (host RNG + plan upload), sketch, QR, back-solve, residual"}
+
+    # ---- e2e through the C-ABI host-buffer entry point
+    e2e = None
+    if not args.no_e2e:
+        from paper_2409_14309_b200._device import pinned_empty_f64
+
+        Ah = pinned_empty_f64((m_loc, n), fortran=True)
+        Ah[...] = A.cpu().numpy()
+        bh = pinned_empty_f64((m_loc,))
+        bh[...] = b.cpu().numpy()
+        SAh = np.empty((d, n), order="F")
+        Sbh = np.empty(d)
+
+        def e2e_call():
+            _native.call("skl_countsketch_dense_host", Ah.ctypes.data, m_loc, n, m_loc,
+                         bh.ctypes.data, ent.data_ptr(), off.data_ptr(), d, PLAN_CHUNK,
+                         SAh.ctypes.data, d, Sbh.ctypes.data, None, 0, None, stream.cuda_stream)
+
+        e2e_call()
+        reps = 3
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            e2e_call()
+            ts.append(time.perf_counter() - t0)
+        te = statistics.median(ts)
+        e2e = {"value": round(bytes_local / te / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": bytes_local, "d2h_bytes_per_step": 8 * d * (n + 1),
+               "ms_per_step": round(te * 1e3, 3),
+               "path": "skl_countsketch_dense_host (pinned host A,b -> host SA,Sb)"}
+        if world == 1:
+            # parity of the timed output against the device run (bitwise)
+            assert np.array_equal(SAh, out[:, :n].cpu().numpy())
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        ms = 1 << 17
+        Ah_s = np.asfortranarray(A[:ms].cpu().numpy())
+        bh_s = b[:ms].cpu().numpy()
+        gbs, t, _ = cpu_reference_sample(cfg, Ah_s, bh_s, op.rows, op.signs, 3)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"first {ms} rows x {n} (+b) of the config-{cfg.cfg} block, scipy CSR @ A "
+                         f"(the reference's csr_matvecs path), median of 3 = {t:.3f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": f"S·A sketch GB/s (config {cfg.cfg}: CountSketch d={d}, dense {m_loc}x{n} fp64 per GPU)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config {cfg.cfg}: dense {m_loc}x{n} fp64 (kappa=1e8) per GPU, "
+                                   f"CountSketch d={d}, one pass S[A|b]"
+                                   + (" + NCCL reduce of d x (n+1) partials" if world > 1 else ""),
+                       "m_per_gpu": m_loc, "n": n, "d": d, "m_total": m_total,
+                       "parallelism": f"rows sharded over {world} GPU(s)",
+                       "l2": "inputs larger than L2 (2 GiB of A per GPU per step); no flush"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": profiled_traffic(), "peak_source": peak_src,
+                         "kernel": "countsketch_dense_kernel<8,1>",
+                         "kernel_ms": round(kern_avg, 4),
+                         "algorithmic_bytes_per_launch": bytes_local,
+                         "frac_of_8TBps": round(achieved / 8000.0, 4)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps,
+        }
+        if solve:
+            line["solve"] = solve
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

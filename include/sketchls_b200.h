@@ -1,0 +1,181 @@
+/*
+ * sketchls_b200.h — C-ABI of the B200-native sketch-and-solve engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (`sketchls`, arxiv 2409.14309): the bodies of `build_sketch`,
+ * `_apply`, `economy_qr`, `_apply_inverse_r` and `_residual_norm`.
+ * Every entry point takes plain pointers and sizes (no torch types),
+ * returns an `int` status (SKL_OK == 0) and on failure leaves a message
+ * retrievable with skl_last_error() (thread-local, so the ABI is
+ * reentrant: inputs are borrowed read-only, outputs are caller-owned,
+ * each call runs on the caller's CUDA stream).
+ *
+ * Layout conventions follow the reference carriers
+ * (/root/reference/pkg/src/sketchls/linalg.py:31-53, 56-114, 117-133):
+ * dense matrices are fp64 column-major with a leading dimension,
+ * vectors are contiguous fp64, CSR uses int64 indptr/indices with
+ * strictly increasing columns per row.
+ *
+ * Pointers documented as "device" must be CUDA device pointers; "host"
+ * pointers are ordinary (preferably pinned) host memory.
+ */
+#ifndef SKETCHLS_B200_H
+#define SKETCHLS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python host maps them onto the reference's exception
+ * taxonomy (/root/reference/pkg/src/sketchls/errors.py:8-37). */
+enum {
+  SKL_OK = 0,
+  SKL_ERR_SHAPE = 1,     /* ShapeError            errors.py:12 */
+  SKL_ERR_SPEC = 2,      /* SpecError             errors.py:16 */
+  SKL_ERR_SINGULAR = 3,  /* SingularFactorError   errors.py:24 */
+  SKL_ERR_CAPACITY = 4,  /* CapacityError         errors.py:32 */
+  SKL_ERR_CUDA = 5,      /* device failure (SketchlsError) */
+  SKL_ERR_INVALID = 6,   /* bad argument / layout (ValueError) */
+  SKL_ERR_NCCL = 7       /* collective failure (SketchlsError) */
+};
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* skl_last_error(void);
+/* ABI version: bump on incompatible signature changes. */
+int skl_abi_version(void);
+
+/* ---------------------------------------------------------------------
+ * Seeds and the bit-exact host RNG (numpy 2.3.5 Philox4x64-10 streams).
+ * Replaces rng.py:19-45 and the draws in sketch.py:93-127.
+ * ------------------------------------------------------------------- */
+
+/* One splitmix64 step.  Replaces rng.py:19-24 (`splitmix64`). */
+uint64_t skl_splitmix64(uint64_t z);
+
+/* Raw u32 stream of Generator(Philox(key)) starting at u32 position
+ * `offset` (low half of each u64 first).  Test hook for the bit contract
+ * behind rng.py:43-45 (`stream`). */
+int skl_rng_u32(uint64_t key, uint64_t offset, int64_t count, uint32_t* out);
+/* Raw u64 stream (next_uint64 order) from u64 position `offset`. */
+int skl_rng_u64(uint64_t key, uint64_t offset, int64_t count, uint64_t* out);
+
+/* CountSketch hashes: rows[j] = integers(0, d, m)[j], signs[j] = +-1 from
+ * the following integers(0, 2, m).  Replaces sketch.py:97-99.
+ * host outputs; `threads` <= 0 means all hardware threads.
+ * *u32_consumed (optional) receives the number of u32 draws used. */
+int skl_rng_countsketch(uint64_t key, int64_t m, int64_t d, int32_t* rows, int8_t* signs,
+                        int threads, uint64_t* u32_consumed);
+
+/* SRHT sign diagonal over m_pad draws and row_sample = permutation(m_pad)[:d].
+ * Replaces sketch.py:116-127.  host outputs. */
+int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t* row_sample,
+                 int threads);
+
+/* Gaussian sketch entries G[i, j] = standard_normal((d, m))[i, j] / sqrt(d),
+ * written column-major into a device buffer (ld = ldg >= d), generated on
+ * device by a resynchronising parallel ziggurat over the Philox stream.
+ * Replaces sketch.py:94-96.  The ziggurat tables must have been installed
+ * once with skl_gaussian_set_tables (extracted from the installed numpy). */
+int skl_gaussian_set_tables(const uint64_t* ki, const double* wi, const double* fi);
+int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G_dev, int64_t ldg,
+                            void* stream);
+/* Host (sequential, glibc libm) reference generator of the same stream;
+ * used to patch the rare ziggurat tail draws and by tests. */
+int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);
+
+/* ---------------------------------------------------------------------
+ * CountSketch apply plan: per chunk of `chunk` rows, the row offsets
+ * sorted stably by bucket (bit 15 = negative sign) and the bucket
+ * offsets (stride skl_countsketch_plan_stride(d) uint16 per chunk).
+ * It is the chunked form of the reference's CSR sparse_map
+ * (sketch.py:100-102) and fixes the ascending-row fold order of
+ * scipy's csr_matvecs, so the device apply is bitwise-equal to it.
+ * ------------------------------------------------------------------- */
+int64_t skl_countsketch_plan_stride(int64_t d);
+int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
+                         int64_t chunk, uint16_t* entries, uint16_t* offsets, int threads);
+
+/* S*A and S*b for dense column-major A (device pointers).  b may be NULL
+ * (then Sb is ignored).  partitions: 0 = auto, 1 = single ordered pass
+ * (bitwise-equal to the reference), P>1 = P row partitions reduced in a
+ * fixed order (deterministic).  accumulate != 0 adds into SA/Sb (used for
+ * row-streamed applies).  workspace may be NULL (allocated from the
+ * stream-ordered pool).  Replaces sketch.py:209-212 (dense branch). */
+int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                          const uint16_t* entries, const uint16_t* offsets, int64_t d,
+                          int64_t chunk, double* SA, int64_t ldsa, double* Sb, int partitions,
+                          int accumulate, void* stream);
+
+/* Same apply with HOST A/b/SA/Sb: streams row blocks of A through the
+ * device with host-to-device copies overlapped with the kernel; if
+ * A_dev_keep != NULL the device copy of A (ld = m rounded up to 32) is
+ * left there for a later residual pass.  plan pointers are device. */
+int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
+                               const double* b_host, const uint16_t* entries,
+                               const uint16_t* offsets, int64_t d, int64_t chunk,
+                               double* SA_host, int64_t ldsa, double* Sb_host,
+                               double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
+                               void* stream);
+
+/* Bucket-sorted source rows of a CountSketch (host): bucket_rows[bucket_ptr[i]
+ * .. bucket_ptr[i+1]) are the rows j with rows[j] == i, ascending -- the CSR
+ * of S (sketch.py:100-102) without its values.  bucket_ptr has d+1 entries. */
+int skl_countsketch_buckets(const int32_t* rows, int64_t m, int64_t d, int32_t* bucket_rows,
+                            int64_t* bucket_ptr);
+
+/* S*A for CSR A (device pointers; int64 indptr/indices as SparseMatrix
+ * holds them, linalg.py:66-68).  bucket_rows/bucket_ptr from
+ * skl_countsketch_buckets and the int8 signs, all on the device.  SA is
+ * d x n column-major, fully overwritten (bitwise-equal to scipy's
+ * csr_matmat fold).  Replaces sketch.py:210-211. */
+int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices, const double* values,
+                        int64_t m, int64_t n, const int32_t* bucket_rows,
+                        const int64_t* bucket_ptr, const int8_t* signs, int64_t d, double* SA,
+                        int64_t ldsa, void* stream);
+
+/* SRHT: out = (P H D [A; 0]) / sqrt(d) for dense column-major A (device),
+ * H the unnormalised Sylvester-Hadamard of order m_pad.  signs (+-1 int8,
+ * m_pad) and row_sample (int64, d) are device arrays.  Replaces
+ * sketch.py:213-223 and fwht_inplace sketch.py:152-177. */
+int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda, const int8_t* signs,
+                   const int64_t* row_sample, int64_t m_pad, int64_t d, double* SA,
+                   int64_t ldsa, void* stream);
+
+/* In-place unnormalised FWHT of a device column-major m_pad x n array
+ * (lda >= m_pad), m_pad a power of two.  Replaces sketch.py:152-177. */
+int skl_fwht_device(double* X, int64_t m_pad, int64_t n, int64_t lda, void* stream);
+
+/* Gaussian apply SA = G * A with G d x m (ld ldg), A m x n (lda), column-
+ * major fp64, on the fp64 tensor cores (DMMA).  Replaces sketch.py:204-208. */
+int skl_gemm_f64(const double* G, int64_t ldg, const double* A, int64_t lda, double* C,
+                 int64_t ldc, int64_t d, int64_t n, int64_t m, int accumulate, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Reduced solve (device).  Householder QR of M = SA (d x n, d >= n) with
+ * the reference's conventions (linalg.py:166-192): diag(R) >= 0, rank
+ * check |R[c,c]| < 1e-14 * ||M||_F naming the first bad column, then
+ * x = R^{-1} Q^T Sb (solvers.py:309, linalg.py:214-218).
+ * R (n x n, ldr) and Q (d x n, ldq) are optional outputs (NULL to skip).
+ * x is device (n).  *bad_col receives -1 or the failing column and
+ * *bad_val |R[c,c]| for the error message.
+ * ------------------------------------------------------------------- */
+int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
+                 double* x, double* R, int64_t ldr, double* Q, int64_t ldq, int64_t* bad_col,
+                 double* bad_val, void* stream);
+
+/* ||A x - b||_2 for dense column-major A (device).  Replaces
+ * solvers.py:102-107.  *out is host. */
+int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
+                       const double* b, double* out, void* stream);
+/* ||A x - b||_2 for CSR A (device). */
+int skl_residual_csr(const int64_t* indptr, const int64_t* indices, const double* values,
+                     int64_t m, int64_t n, const double* x, const double* b, double* out,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHLS_B200_H */

@@ -1,0 +1,169 @@
+"""ctypes binding of the C-ABI in ``include/sketchls_b200.h``.
+
+The shared library ``_lib/libsketchls_b200.so`` is built in-tree by
+``_build.py`` (``__graft_entry__.build()``).  There is no fallback: if the
+library is missing or a call fails, the mapped exception is raised.
+Device buffers are passed as raw pointers (``torch.Tensor.data_ptr()``) and
+the caller's current CUDA stream as ``void*``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import (
+    CapacityError,
+    DeviceError,
+    ShapeError,
+    SingularFactorError,
+    SketchlsError,
+    SpecError,
+)
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsketchls_b200.so"
+
+_lib = None
+_lock = threading.Lock()
+
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_int = ctypes.c_int
+c_ptr = ctypes.c_void_p
+c_dbl_p = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes)
+SIGNATURES: dict[str, tuple] = {
+    "skl_last_error": (ctypes.c_char_p, []),
+    "skl_abi_version": (c_int, []),
+    "skl_splitmix64": (c_u64, [c_u64]),
+    "skl_rng_u32": (c_int, [c_u64, c_u64, c_i64, c_ptr]),
+    "skl_rng_u64": (c_int, [c_u64, c_u64, c_i64, c_ptr]),
+    "skl_rng_countsketch": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int, c_ptr]),
+    "skl_rng_srht": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
+    "skl_countsketch_plan_stride": (c_i64, [c_i64]),
+    "skl_countsketch_plan": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
+    "skl_countsketch_dense": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr,
+         c_int, c_int, c_ptr],
+    ),
+    "skl_countsketch_dense_host": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr,
+         c_ptr, c_i64, c_ptr, c_ptr],
+    ),
+    "skl_countsketch_buckets": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
+    "skl_countsketch_csr": (
+        c_int,
+        [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr],
+    ),
+    "skl_qr_solve": (
+        c_int,
+        [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
+         c_ptr],
+    ),
+    "skl_residual_dense": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_residual_csr": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+}
+
+_STATUS = {
+    1: ShapeError,
+    2: SpecError,
+    3: SingularFactorError,
+    4: CapacityError,
+    5: DeviceError,
+    6: ValueError,
+    7: DeviceError,
+}
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library (built on first use if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                from . import _build
+
+                _build.build()
+            if not LIB_PATH.exists():
+                raise DeviceError(f"native library missing: {LIB_PATH}")
+            handle = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().skl_last_error().decode("utf-8", "replace")
+    raise _STATUS.get(status, SketchlsError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def ptr(a) -> int | None:
+    """Raw address of a numpy array or torch tensor (None passes NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+# ----------------------------------------------------------------- host RNG
+def rng_u32(key: int, offset: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint32)
+    call("skl_rng_u32", key, offset, count, ptr(out))
+    return out
+
+
+def rng_u64(key: int, offset: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint64)
+    call("skl_rng_u64", key, offset, count, ptr(out))
+    return out
+
+
+def rng_countsketch(key: int, m: int, d: int, threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    rows = np.empty(m, dtype=np.int32)
+    signs = np.empty(m, dtype=np.int8)
+    call("skl_rng_countsketch", key, m, d, ptr(rows), ptr(signs), threads, None)
+    return rows, signs
+
+
+def rng_srht(key: int, m_pad: int, d: int, threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    signs = np.empty(m_pad, dtype=np.int8)
+    sample = np.empty(d, dtype=np.int64)
+    call("skl_rng_srht", key, m_pad, d, ptr(signs), ptr(sample), threads)
+    return signs, sample
+
+
+def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int,
+                     threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    m = rows.shape[0]
+    nch = (m + chunk - 1) // chunk
+    stride = int(lib().skl_countsketch_plan_stride(d))
+    ent = np.zeros(nch * chunk, dtype=np.uint16)
+    off = np.zeros(nch * stride, dtype=np.uint16)
+    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, ptr(ent), ptr(off), threads)
+    return ent, off
+
+
+def countsketch_buckets(rows: np.ndarray, d: int) -> tuple[np.ndarray, np.ndarray]:
+    m = rows.shape[0]
+    brow = np.empty(m, dtype=np.int32)
+    bptr = np.empty(d + 1, dtype=np.int64)
+    call("skl_countsketch_buckets", ptr(rows), m, d, ptr(brow), ptr(bptr))
+    return brow, bptr

@@ -1,0 +1,49 @@
+// Shared helpers of the sketchls_b200 native library: status/error plumbing
+// (thread-local message, see include/sketchls_b200.h) and CUDA checks.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/sketchls_b200.h"
+
+namespace skl {
+
+void set_error(const char* fmt, ...);
+void clear_error();
+
+// Number of host worker threads for `threads` <= 0 requests.
+int resolve_threads(int threads);
+
+}  // namespace skl
+
+#define SKL_FAIL(code, ...)          \
+  do {                               \
+    skl::set_error(__VA_ARGS__);     \
+    return (code);                   \
+  } while (0)
+
+#define SKL_REQUIRE(cond, code, ...) \
+  do {                               \
+    if (!(cond)) SKL_FAIL(code, __VA_ARGS__); \
+  } while (0)
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#define SKL_CUDA(call)                                                          \
+  do {                                                                          \
+    cudaError_t e__ = (call);                                                   \
+    if (e__ != cudaSuccess)                                                     \
+      SKL_FAIL(SKL_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e__), \
+               __FILE__, __LINE__);                                             \
+  } while (0)
+#define SKL_CUDA_LAUNCH()                                                       \
+  do {                                                                          \
+    cudaError_t e__ = cudaGetLastError();                                       \
+    if (e__ != cudaSuccess)                                                     \
+      SKL_FAIL(SKL_ERR_CUDA, "kernel launch failed: %s (%s:%d)",               \
+               cudaGetErrorString(e__), __FILE__, __LINE__);                    \
+  } while (0)
+#endif

@@ -1,0 +1,398 @@
+// CountSketch apply S*A, S*b for dense column-major fp64 A on sm_100a.
+//
+// Reference semantics (/root/reference/pkg/src/sketchls/sketch.py:209-212):
+// `op.sparse_map @ A` with the CSR map built at sketch.py:100-102; scipy's
+// csr_matvecs folds, for every bucket i and column c, the signed source rows
+// j with rows[j] == i in ascending j starting from +0.0.  Multiplying by a
+// sign is exact, so reproducing that fold order reproduces SA bit for bit.
+//
+// Design (B200): one CTA owns C columns of [A | b] and streams them once,
+// top to bottom, in chunks of T rows.  A dedicated producer warp issues 1-D
+// bulk copies (cp.async.bulk -> UBLKCP) of each chunk's column segments plus
+// the chunk's slice of the plan (bucket-sorted row offsets and bucket
+// offsets, L2-resident, shared by all CTAs) into an S-stage shared-memory
+// ring guarded by full/empty mbarriers.  Each consumer thread owns KPT
+// buckets (i = k*NT + t) whose running sums live in registers across chunks
+// and walks each bucket's entries in ascending row order, reading A from
+// shared memory.  No atomics; A is read from HBM exactly once with
+// evict-first L2 hints.  With P > 1 row partitions (small n), partial sums
+// go to a workspace and are reduced in fixed partition order
+// (deterministic, not bitwise).
+#include <algorithm>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "skl_common.h"
+#include "skl_ptx.cuh"
+
+namespace skl {
+
+constexpr int CS_NT = 256;     // consumer threads
+constexpr int CS_STAGES = 4;   // smem ring depth
+
+struct CsParams {
+  const double* A;
+  int64_t lda;
+  const double* b;
+  int64_t n;        // columns of A
+  int64_t ncols;    // n + (b != nullptr)
+  int64_t row_begin, row_end;  // rows handled by this launch (row_begin % T == 0)
+  const uint16_t* ent;
+  const uint16_t* off;
+  int d;
+  int T;
+  int stride;
+  int P;
+  double* out;      // SA (P == 1)
+  int64_t ldo;
+  double* outb;     // Sb (P == 1)
+  double* part;     // [P][ncols][d] (P > 1)
+  int accumulate;
+};
+
+__device__ __forceinline__ const double* cs_col(const CsParams& p, int64_t c) {
+  return c < p.n ? p.A + c * p.lda : p.b;
+}
+
+template <int KPT, int C>
+__global__ void __launch_bounds__(CS_NT + 32)
+    countsketch_dense_kernel(const CsParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + CS_STAGES;
+  unsigned char* ring = smem + 128;
+  const int T = p.T;
+  const size_t a_bytes = (size_t)C * T * sizeof(double);
+  const size_t e_bytes = (size_t)T * sizeof(uint16_t);
+  const size_t stage_bytes = a_bytes + e_bytes + (size_t)p.stride * sizeof(uint16_t);
+
+  const int tid = threadIdx.x;
+  const int64_t col0 = (int64_t)blockIdx.x * C;
+  const int ncol_here = (int)(p.ncols - col0 < C ? p.ncols - col0 : C);
+  const int64_t ch_first = p.row_begin / T;
+  const int64_t nch = (p.row_end - p.row_begin + T - 1) / T;
+  const int64_t it0 = nch * blockIdx.y / p.P, it1 = nch * (blockIdx.y + 1) / p.P;
+  const int64_t niter = it1 - it0;
+
+  if (tid == 0) {
+    for (int s = 0; s < CS_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CS_NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= CS_NT) {
+    // ------------------------------ producer warp
+    if (tid == CS_NT) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      for (int64_t it = 0; it < niter; ++it) {
+        const int s = (int)(it % CS_STAGES);
+        if (it >= CS_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / CS_STAGES) + 1) & 1));
+        const int64_t ch = ch_first + it0 + it;
+        const int64_t r0 = ch * T;
+        const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
+        const int len_even = len & ~1;
+        unsigned char* st = ring + s * stage_bytes;
+        double* As = reinterpret_cast<double*>(st);
+        uint16_t* Es = reinterpret_cast<uint16_t*>(st + a_bytes);
+        uint16_t* Os = reinterpret_cast<uint16_t*>(st + a_bytes + e_bytes);
+        const uint32_t ebytes = (uint32_t)(((len + 7) & ~7) * sizeof(uint16_t));
+        const uint32_t obytes = (uint32_t)(p.stride * sizeof(uint16_t));
+        if (len & 1) {
+          for (int c = 0; c < ncol_here; ++c)
+            As[c * T + len - 1] = __ldg(cs_col(p, col0 + c) + r0 + len - 1);
+        }
+        const uint32_t total =
+            (uint32_t)(ncol_here * len_even * sizeof(double)) + ebytes + obytes;
+        mbar_arrive_expect_tx(&full[s], total);
+        if (len_even) {
+          for (int c = 0; c < ncol_here; ++c)
+            bulk_g2s(As + c * T, cs_col(p, col0 + c) + r0, (uint32_t)(len_even * sizeof(double)),
+                     &full[s], pol_stream);
+        }
+        bulk_g2s(Es, p.ent + r0, ebytes, &full[s], pol_keep);
+        bulk_g2s(Os, p.off + ch * p.stride, obytes, &full[s], pol_keep);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers
+  double acc[C][KPT];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      acc[c][k] = 0.0;
+      const int i = k * CS_NT + tid;
+      if (p.P == 1 && p.accumulate && i < p.d && c < ncol_here) {
+        const int64_t col = col0 + c;
+        acc[c][k] = col < p.n ? p.out[col * p.ldo + i] : p.outb[i];
+      }
+    }
+
+  for (int64_t it = 0; it < niter; ++it) {
+    const int s = (int)(it % CS_STAGES);
+    mbar_wait(&full[s], (uint32_t)((it / CS_STAGES) & 1));
+    const unsigned char* st = ring + s * stage_bytes;
+    const double* As = reinterpret_cast<const double*>(st);
+    const uint16_t* Es = reinterpret_cast<const uint16_t*>(st + a_bytes);
+    const uint16_t* Os = reinterpret_cast<const uint16_t*>(st + a_bytes + e_bytes);
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int i = k * CS_NT + tid;
+      if (i < p.d) {
+        const int beg = Os[i], end = Os[i + 1];
+        for (int e = beg; e < end; ++e) {
+          const uint32_t v = Es[e];
+          const int row = v & 0x7fff;
+          const bool neg = v >> 15;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const double x = As[c * T + row];
+            acc[c][k] += neg ? -x : x;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (c >= ncol_here) break;
+    const int64_t col = col0 + c;
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int i = k * CS_NT + tid;
+      if (i >= p.d) continue;
+      if (p.P == 1) {
+        if (col < p.n)
+          p.out[col * p.ldo + i] = acc[c][k];
+        else
+          p.outb[i] = acc[c][k];
+      } else {
+        p.part[((int64_t)blockIdx.y * p.ncols + col) * p.d + i] = acc[c][k];
+      }
+    }
+  }
+}
+
+// Fixed-order reduction of the P partial sketches.
+__global__ void countsketch_reduce_kernel(const double* part, int P, int64_t ncols, int d,
+                                          int64_t n, double* out, int64_t ldo, double* outb,
+                                          int accumulate) {
+  const int64_t total = ncols * d;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / d;
+    const int i = (int)(idx % d);
+    double* dst = col < n ? out + col * ldo + i : outb + i;
+    double s = accumulate ? *dst : 0.0;
+    for (int q = 0; q < P; ++q) s += part[((int64_t)q * ncols + col) * d + i];
+    *dst = s;
+  }
+}
+
+static int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : 148;
+  }
+  return cached;
+}
+
+template <int KPT, int C>
+static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  auto kern = countsketch_dense_kernel<KPT, C>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, CS_NT + 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+static cudaError_t dispatch_cs(int kpt, int C, const CsParams& p, dim3 grid, size_t smem,
+                               cudaStream_t st) {
+#define SKL_CS_CASE(K, CC) \
+  if (kpt == K && C == CC) return launch_cs<K, CC>(p, grid, smem, st);
+  SKL_CS_CASE(1, 1) SKL_CS_CASE(1, 2) SKL_CS_CASE(1, 4)
+  SKL_CS_CASE(2, 1) SKL_CS_CASE(2, 2) SKL_CS_CASE(2, 4)
+  SKL_CS_CASE(4, 1) SKL_CS_CASE(4, 2) SKL_CS_CASE(4, 4)
+  SKL_CS_CASE(8, 1) SKL_CS_CASE(8, 2)
+  SKL_CS_CASE(16, 1) SKL_CS_CASE(32, 1)
+#undef SKL_CS_CASE
+  return cudaErrorInvalidValue;
+}
+
+static int kpt_for(int64_t d) {
+  int k = 1;
+  while ((int64_t)k * CS_NT < d) k <<= 1;
+  return k;
+}
+
+// Core launcher shared by the device and host-streaming entry points.
+static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                              const uint16_t* ent, const uint16_t* off, int64_t d, int64_t chunk,
+                              double* SA, int64_t ldsa, double* Sb, int partitions, int accumulate,
+                              int64_t row_begin, int64_t row_end, cudaStream_t st) {
+  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+              "countsketch: bad shape m=%lld n=%lld d=%lld lda=%lld ldsa=%lld", (long long)m,
+              (long long)n, (long long)d, (long long)lda, (long long)ldsa);
+  SKL_REQUIRE(d <= 32 * CS_NT, SKL_ERR_SPEC, "countsketch: embed_dim %lld > %d not supported",
+              (long long)d, 32 * CS_NT);
+  SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
+              "countsketch: bad plan chunk %lld", (long long)chunk);
+  SKL_REQUIRE(A && ent && off && SA && (!b || Sb), SKL_ERR_INVALID, "countsketch: null pointer");
+  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && (!b || ((uintptr_t)b & 15) == 0),
+              SKL_ERR_INVALID,
+              "countsketch: A/b must be 16-byte aligned with an even leading dimension");
+  SKL_REQUIRE(((uintptr_t)ent & 15) == 0 && ((uintptr_t)off & 15) == 0, SKL_ERR_INVALID,
+              "countsketch: plan arrays must be 16-byte aligned");
+  SKL_REQUIRE(row_begin % chunk == 0 && row_end > row_begin && row_end <= m, SKL_ERR_INVALID,
+              "countsketch: bad row range");
+
+  const int kpt = kpt_for(d);
+  const int64_t ncols = n + (b ? 1 : 0);
+  int C = 1;
+  const int T = (int)chunk;
+  const int stride = (int)skl_countsketch_plan_stride(d);
+  const size_t stage = (size_t)C * T * 8 + (size_t)T * 2 + (size_t)stride * 2;
+  const size_t smem = 128 + CS_STAGES * stage;
+  SKL_REQUIRE(smem <= 227 * 1024, SKL_ERR_INVALID, "countsketch: chunk %d too large for smem", T);
+
+  const int64_t groups = (ncols + C - 1) / C;
+  const int64_t nch = (row_end - row_begin + T - 1) / T;
+  int P = partitions;
+  if (P <= 0) {
+    const int sms = sm_count();
+    P = groups >= sms ? 1 : (int)((2 * sms + groups - 1) / groups);
+  }
+  P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nch));
+
+  CsParams p;
+  p.A = A; p.lda = lda; p.b = b; p.n = n; p.ncols = ncols;
+  p.row_begin = row_begin; p.row_end = row_end;
+  p.ent = ent; p.off = off; p.d = (int)d; p.T = T; p.stride = stride; p.P = P;
+  p.out = SA; p.ldo = ldsa; p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
+
+  double* part = nullptr;
+  if (P > 1) {
+    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * ncols * d * sizeof(double), st));
+    p.part = part;
+  }
+  dim3 grid((unsigned)groups, (unsigned)P);
+  cudaError_t e = dispatch_cs(kpt, C, p, grid, smem, st);
+  if (e != cudaSuccess) {
+    if (part) cudaFreeAsync(part, st);
+    SKL_FAIL(SKL_ERR_CUDA, "countsketch kernel launch failed: %s", cudaGetErrorString(e));
+  }
+  if (P > 1) {
+    const int64_t total = ncols * d;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * sm_count());
+    countsketch_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, ncols, (int)d, n, SA, ldsa, Sb,
+                                                      accumulate);
+    SKL_CUDA_LAUNCH();
+    SKL_CUDA(cudaFreeAsync(part, st));
+  }
+  return SKL_OK;
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,
+                                     const double* b, const uint16_t* entries,
+                                     const uint16_t* offsets, int64_t d, int64_t chunk, double* SA,
+                                     int64_t ldsa, double* Sb, int partitions, int accumulate,
+                                     void* stream) {
+  clear_error();
+  return countsketch_launch(A, m, n, lda, b, entries, offsets, d, chunk, SA, ldsa, Sb, partitions,
+                            accumulate, 0, m, (cudaStream_t)stream);
+}
+
+// Host-buffer entry point: row blocks of A are copied host->device on a
+// side stream while the kernel sketches the previous block (ordered pass,
+// accumulate across blocks, so the result stays bitwise-equal).
+extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
+                                          const double* b_host, const uint16_t* entries,
+                                          const uint16_t* offsets, int64_t d, int64_t chunk,
+                                          double* SA_host, int64_t ldsa, double* Sb_host,
+                                          double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
+                                          void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  SKL_REQUIRE(A_host && SA_host && m >= 1 && n >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+              "countsketch_host: bad arguments");
+  SKL_REQUIRE(!b_host || Sb_host, SKL_ERR_INVALID, "countsketch_host: Sb_host missing");
+  const int64_t ld_dev = A_dev_keep ? ld_keep : (m + 31) / 32 * 32;
+  SKL_REQUIRE(ld_dev >= m && ld_dev % 2 == 0, SKL_ERR_INVALID, "countsketch_host: bad ld_keep");
+  double* A_dev = A_dev_keep;
+  double* b_dev = b_dev_keep;
+  double *SA_dev = nullptr, *Sb_dev = nullptr;
+  if (!A_dev) SKL_CUDA(cudaMallocAsync(&A_dev, (size_t)ld_dev * n * sizeof(double), st));
+  if (b_host && !b_dev) SKL_CUDA(cudaMallocAsync(&b_dev, (size_t)m * sizeof(double), st));
+  SKL_CUDA(cudaMallocAsync(&SA_dev, (size_t)d * n * sizeof(double), st));
+  if (b_host) SKL_CUDA(cudaMallocAsync(&Sb_dev, (size_t)d * sizeof(double), st));
+
+  cudaStream_t cp;
+  SKL_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  cudaEvent_t ready;
+  SKL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  SKL_CUDA(cudaEventRecord(ready, st));  // allocations visible to the copy stream
+  SKL_CUDA(cudaStreamWaitEvent(cp, ready, 0));
+
+  // Blocks of whole plan chunks, ~256 MiB of A each.
+  int64_t rows_per_block = std::max<int64_t>(chunk, ((256LL << 20) / (8 * n)) / chunk * chunk);
+  const int64_t nblk = (m + rows_per_block - 1) / rows_per_block;
+  int rc = SKL_OK;
+  std::vector<cudaEvent_t> evs((size_t)nblk);
+  for (int64_t k = 0; k < nblk && rc == SKL_OK; ++k) {
+    const int64_t r0 = k * rows_per_block, r1 = std::min(m, r0 + rows_per_block);
+    cudaEventCreateWithFlags(&evs[(size_t)k], cudaEventDisableTiming);
+    cudaError_t e = cudaMemcpy2DAsync(A_dev + r0, ld_dev * sizeof(double), A_host + r0,
+                                      lda * sizeof(double), (r1 - r0) * sizeof(double), n,
+                                      cudaMemcpyHostToDevice, cp);
+    if (e == cudaSuccess && b_host)
+      e = cudaMemcpyAsync(b_dev + r0, b_host + r0, (r1 - r0) * sizeof(double),
+                          cudaMemcpyHostToDevice, cp);
+    if (e == cudaSuccess) e = cudaEventRecord(evs[(size_t)k], cp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, evs[(size_t)k], 0);
+    if (e != cudaSuccess) {
+      set_error("countsketch_host: copy failed: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, entries, offsets, d,
+                            chunk, SA_dev, d, Sb_dev, 1, k > 0 ? 1 : 0, r0, r1, st);
+  }
+  if (rc == SKL_OK) {
+    cudaError_t e = cudaMemcpy2DAsync(SA_host, ldsa * sizeof(double), SA_dev, d * sizeof(double),
+                                      d * sizeof(double), n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && b_host)
+      e = cudaMemcpyAsync(Sb_host, Sb_dev, d * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("countsketch_host: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+    }
+  }
+  for (auto& ev : evs)
+    if (ev) cudaEventDestroy(ev);
+  cudaEventDestroy(ready);
+  cudaStreamDestroy(cp);
+  if (!A_dev_keep) cudaFreeAsync(A_dev, st);
+  if (b_host && !b_dev_keep) cudaFreeAsync(b_dev, st);
+  cudaFreeAsync(SA_dev, st);
+  if (Sb_dev) cudaFreeAsync(Sb_dev, st);
+  return rc;
+}

@@ -1,0 +1,342 @@
+// Host side of sketchls_b200: error plumbing, the bit-exact Philox4x64-10
+// streams of numpy 2.3.5 (the generator behind sketchls/rng.py:43-45), the
+// CountSketch / SRHT draws of sketch.py:93-127 and the CountSketch plan.
+//
+// Bit contract (numpy 2.3.5, verified by tests/test_host_rng.py against
+// numpy itself): Generator(Philox(key=k)) runs Philox4x64-10 with key words
+// (k, 0); the 256-bit counter is incremented *before* each block, so block
+// q uses counter (q+1, 0, 0, 0) and yields u64 words 4q..4q+3 in order.
+// next_uint32 splits each u64 low half first; the leftover half persists
+// across `integers` calls.  integers(0, d) is Lemire's 32-bit method with
+// rejection threshold (2^32 - d) mod d; permutation(n) is a top-down
+// Fisher-Yates whose j comes from masked rejection on the u32 stream.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "skl_common.h"
+#include "skl_philox.h"
+
+namespace skl {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+void clear_error() { g_err.clear(); }
+
+int resolve_threads(int threads) {
+  if (threads > 0) return threads;
+  unsigned h = std::thread::hardware_concurrency();
+  return h ? (int)std::min(h, 64u) : 1;
+}
+
+template <class F>
+static void parallel_for(int64_t n, int threads, F&& f) {
+  // f(lo, hi) over [0, n) split in contiguous blocks.
+  threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / 4096 + 1));
+  if (threads == 1) {
+    f((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(threads);
+  for (int t = 0; t < threads; ++t) {
+    int64_t lo = n * t / threads, hi = n * (t + 1) / threads;
+    pool.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Fill out[i] = u32 at stream position pos0 + i.
+static void fill_u32(uint64_t key, uint64_t pos0, int64_t count, uint32_t* out) {
+  if (count <= 0) return;
+  uint64_t p = pos0;
+  int64_t i = 0;
+  while (i < count) {
+    uint64_t q = p >> 1;       // u64 index
+    uint64_t blk = q >> 2;     // Philox block
+    uint64_t w[4];
+    philox_block(key, blk, w);
+    // positions covered by this block: [blk*8, blk*8+8)
+    uint64_t end = (blk + 1) * 8;
+    while (p < end && i < count) {
+      uint64_t word = w[(p >> 1) & 3];
+      out[i++] = (p & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+      ++p;
+    }
+  }
+}
+
+static void fill_u32_par(uint64_t key, uint64_t pos0, int64_t count, uint32_t* out, int threads) {
+  parallel_for(count, threads, [&](int64_t lo, int64_t hi) { fill_u32(key, pos0 + lo, hi - lo, out + lo); });
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" {
+
+const char* skl_last_error(void) { return skl::g_err.c_str(); }
+int skl_abi_version(void) { return 1; }
+
+uint64_t skl_splitmix64(uint64_t z) { return splitmix64(z); }
+
+int skl_rng_u32(uint64_t key, uint64_t offset, int64_t count, uint32_t* out) {
+  SKL_REQUIRE(count >= 0 && (count == 0 || out), SKL_ERR_INVALID, "skl_rng_u32: bad arguments");
+  fill_u32(key, offset, count, out);
+  return SKL_OK;
+}
+
+int skl_rng_u64(uint64_t key, uint64_t offset, int64_t count, uint64_t* out) {
+  SKL_REQUIRE(count >= 0 && (count == 0 || out), SKL_ERR_INVALID, "skl_rng_u64: bad arguments");
+  int64_t i = 0;
+  uint64_t q = offset;
+  while (i < count) {
+    uint64_t w[4];
+    philox_block(key, q >> 2, w);
+    for (uint64_t k = q & 3; k < 4 && i < count; ++k, ++q) out[i++] = w[k];
+  }
+  return SKL_OK;
+}
+
+// CountSketch draws, sketch.py:98-99:
+//   rows  = rng.integers(0, d, size=m)      (Lemire u32, rejection-filtered)
+//   signs = 2 * rng.integers(0, 2, size=m) - 1   (u32 >> 31, never rejects)
+int skl_rng_countsketch(uint64_t key, int64_t m, int64_t d, int32_t* rows, int8_t* signs,
+                        int threads, uint64_t* u32_consumed) {
+  clear_error();
+  SKL_REQUIRE(m >= 1 && d >= 1 && rows && signs, SKL_ERR_INVALID,
+              "skl_rng_countsketch: bad arguments (m=%lld, d=%lld)", (long long)m, (long long)d);
+  SKL_REQUIRE(d <= 0x7fffffffLL, SKL_ERR_SPEC, "embed_dim %lld exceeds the 31-bit bucket range",
+              (long long)d);
+  threads = resolve_threads(threads);
+  uint64_t pos = 0;
+  if (d == 1) {
+    // integers(0, 1) draws nothing (rng == 0 branch of numpy's bounded fill).
+    std::fill(rows, rows + m, 0);
+  } else {
+    const uint64_t dd = (uint64_t)d;
+    const uint32_t threshold = (uint32_t)((0x100000000ULL - dd) % dd);
+    // Pass 1: accept-test every candidate position in [0, m) in parallel.
+    std::atomic<int64_t> rejections{0};
+    parallel_for(m, threads, [&](int64_t lo, int64_t hi) {
+      std::vector<uint32_t> buf(8192);
+      int64_t local_rej = 0;
+      for (int64_t s = lo; s < hi; s += 8192) {
+        int64_t cnt = std::min<int64_t>(8192, hi - s);
+        fill_u32(key, (uint64_t)s, cnt, buf.data());
+        for (int64_t i = 0; i < cnt; ++i) {
+          uint64_t prod = (uint64_t)buf[i] * dd;
+          uint32_t left = (uint32_t)prod;
+          if (left < threshold) {
+            ++local_rej;
+            rows[s + i] = -1;
+          } else {
+            rows[s + i] = (int32_t)(prod >> 32);
+          }
+        }
+      }
+      rejections += local_rej;
+    });
+    pos = (uint64_t)m;
+    if (rejections.load() > 0) {
+      // Rare (probability threshold / 2^32 per draw): compact the accepted
+      // draws in stream order and keep drawing until m are accepted.
+      int64_t w = 0;
+      for (int64_t i = 0; i < m; ++i)
+        if (rows[i] >= 0) rows[w++] = rows[i];
+      while (w < m) {
+        uint32_t u;
+        fill_u32(key, pos++, 1, &u);
+        uint64_t prod = (uint64_t)u * dd;
+        if ((uint32_t)prod >= threshold) rows[w++] = (int32_t)(prod >> 32);
+      }
+    }
+  }
+  const uint64_t sign_pos = pos;
+  parallel_for(m, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<uint32_t> buf(8192);
+    for (int64_t s = lo; s < hi; s += 8192) {
+      int64_t cnt = std::min<int64_t>(8192, hi - s);
+      fill_u32(key, sign_pos + (uint64_t)s, cnt, buf.data());
+      for (int64_t i = 0; i < cnt; ++i) signs[s + i] = (buf[i] >> 31) ? 1 : -1;
+    }
+  });
+  if (u32_consumed) *u32_consumed = sign_pos + (uint64_t)m;
+  return SKL_OK;
+}
+
+// SRHT draws, sketch.py:117-119:
+//   sign_diag  = 2 * rng.integers(0, 2, size=m_pad) - 1
+//   row_sample = rng.permutation(m_pad)[:d]
+// The permutation is numpy's top-down Fisher-Yates (swap a[i], a[j_i] for
+// i = n-1 .. 1).  Only a[:d] is needed, so instead of materialising the
+// n-element array we record the j_i sequence and trace the final positions
+// 0..d-1 backwards through the swaps with a small open-addressing table.
+int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t* row_sample,
+                 int threads) {
+  clear_error();
+  SKL_REQUIRE(m_pad >= 1 && d >= 1 && d <= m_pad && signs && row_sample, SKL_ERR_INVALID,
+              "skl_rng_srht: bad arguments");
+  SKL_REQUIRE(m_pad <= 0x100000000LL, SKL_ERR_SPEC, "padded dimension %lld exceeds 2^32",
+              (long long)m_pad);
+  threads = resolve_threads(threads);
+  parallel_for(m_pad, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<uint32_t> buf(8192);
+    for (int64_t s = lo; s < hi; s += 8192) {
+      int64_t cnt = std::min<int64_t>(8192, hi - s);
+      fill_u32(key, (uint64_t)s, cnt, buf.data());
+      for (int64_t i = 0; i < cnt; ++i) signs[s + i] = (buf[i] >> 31) ? 1 : -1;
+    }
+  });
+  const int64_t n = m_pad;
+  if (n == 1) {
+    row_sample[0] = 0;
+    return SKL_OK;
+  }
+  // Forward pass: draw j_i for i = n-1 .. 1 (sequential rejection).
+  std::vector<uint32_t> js((size_t)(n - 1));  // js[i-1] = j_i
+  uint64_t pos = (uint64_t)n;
+  const int64_t BUF = 1 << 16;
+  std::vector<uint32_t> buf(BUF);
+  int64_t bi = BUF;
+  auto next32 = [&]() -> uint32_t {
+    if (bi == BUF) {
+      fill_u32_par(key, pos, BUF, buf.data(), std::min(threads, 4));
+      pos += BUF;
+      bi = 0;
+    }
+    return buf[bi++];
+  };
+  for (int64_t i = n - 1; i >= 1; --i) {
+    uint64_t mask = (uint64_t)i;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4;
+    mask |= mask >> 8; mask |= mask >> 16; mask |= mask >> 32;
+    uint64_t v;
+    do {
+      v = next32() & mask;
+    } while (v > (uint64_t)i);
+    js[(size_t)(i - 1)] = (uint32_t)v;
+  }
+  // Backward trace: position p at the end came from position pos(p) at the
+  // start; walk the swaps in reverse (i = 1 .. n-1).
+  size_t cap = 1;
+  while (cap < (size_t)d * 4) cap <<= 1;
+  std::vector<int64_t> hkey(cap, -1);
+  std::vector<int64_t> hval(cap, -1);
+  // Table: current position -> tracked item (final position p), with
+  // tombstones for moved keys.  Undoing swap (i, j): if both positions are
+  // tracked their items trade places, otherwise the one item moves.
+  const int64_t TOMB = -2;
+  auto find = [&](int64_t k) -> size_t {
+    size_t h = (size_t)(splitmix64((uint64_t)k) & (cap - 1));
+    while (hkey[h] != -1) {
+      if (hkey[h] == k) return h;
+      h = (h + 1) & (cap - 1);
+    }
+    return (size_t)-1;
+  };
+  auto insert = [&](int64_t k, int64_t v) {
+    size_t h = (size_t)(splitmix64((uint64_t)k) & (cap - 1));
+    while (hkey[h] != -1 && hkey[h] != TOMB) h = (h + 1) & (cap - 1);
+    hkey[h] = k;
+    hval[h] = v;
+  };
+  for (int64_t p = 0; p < d; ++p) insert(p, p);
+  int64_t tombs = 0;
+  for (int64_t i = 1; i <= n - 1; ++i) {
+    int64_t j = js[(size_t)(i - 1)];
+    if (j == i) continue;
+    size_t hi_ = find(i), hj = find(j);
+    bool ti = hi_ != (size_t)-1, tj = hj != (size_t)-1;
+    if (ti && tj) {
+      std::swap(hval[hi_], hval[hj]);
+    } else if (ti) {
+      int64_t item = hval[hi_];
+      hkey[hi_] = TOMB;
+      ++tombs;
+      insert(j, item);
+    } else if (tj) {
+      int64_t item = hval[hj];
+      hkey[hj] = TOMB;
+      ++tombs;
+      insert(i, item);
+    }
+    if (tombs > (int64_t)cap / 4) {
+      // rebuild without tombstones
+      std::vector<std::pair<int64_t, int64_t>> live;
+      live.reserve(d);
+      for (size_t h = 0; h < cap; ++h)
+        if (hkey[h] >= 0) live.emplace_back(hkey[h], hval[h]);
+      std::fill(hkey.begin(), hkey.end(), -1);
+      for (auto& kv : live) insert(kv.first, kv.second);
+      tombs = 0;
+    }
+  }
+  for (size_t h = 0; h < cap; ++h)
+    if (hkey[h] >= 0) row_sample[hval[h]] = hkey[h];
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CountSketch plan (see header).  Chunk k covers rows [k*chunk, ...); its
+// entries are the local row offsets sorted stably by bucket, bit 15 set for
+// a negative sign; offsets[k*stride + i] is the first entry of bucket i and
+// offsets[k*stride + d] the chunk length.
+int64_t skl_countsketch_plan_stride(int64_t d) { return ((d + 1) + 7) / 8 * 8; }
+
+int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
+                         int64_t chunk, uint16_t* entries, uint16_t* offsets, int threads) {
+  clear_error();
+  SKL_REQUIRE(rows && signs && entries && offsets && m >= 1 && d >= 1, SKL_ERR_INVALID,
+              "skl_countsketch_plan: bad arguments");
+  SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
+              "plan chunk must be a multiple of 8 in [8, 32768], got %lld", (long long)chunk);
+  const int64_t stride = skl_countsketch_plan_stride(d);
+  const int64_t nch = (m + chunk - 1) / chunk;
+  threads = resolve_threads(threads);
+  std::atomic<int> bad{0};
+  parallel_for(nch, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<uint32_t> cnt((size_t)d + 1);
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t r0 = k * chunk, len = std::min<int64_t>(chunk, m - r0);
+      std::fill(cnt.begin(), cnt.end(), 0u);
+      for (int64_t j = 0; j < len; ++j) {
+        int32_t r = rows[r0 + j];
+        if (r < 0 || r >= d) {
+          bad = 1;
+          return;
+        }
+        ++cnt[(size_t)r + 1];
+      }
+      uint16_t* off = offsets + k * stride;
+      uint32_t run = 0;
+      for (int64_t i = 0; i < d; ++i) {
+        run += cnt[(size_t)i + 1];
+        cnt[(size_t)i + 1] = run;
+      }
+      for (int64_t i = 0; i <= d; ++i) off[i] = (uint16_t)cnt[(size_t)i];
+      for (int64_t i = d + 1; i < stride; ++i) off[i] = (uint16_t)len;
+      uint16_t* ent = entries + r0;
+      for (int64_t j = 0; j < len; ++j) {
+        int32_t r = rows[r0 + j];
+        ent[cnt[(size_t)r]++] = (uint16_t)(j | (signs[r0 + j] < 0 ? 0x8000 : 0));
+      }
+    }
+  });
+  SKL_REQUIRE(!bad.load(), SKL_ERR_INVALID, "bucket index out of range [0, %lld)", (long long)d);
+  return SKL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,342 @@
+// Reduced solve on device: Householder QR of M = [SA | Sb] (d x (n+1)) and
+// back substitution, with the reference's conventions
+// (/root/reference/pkg/src/sketchls/linalg.py:166-192, 214-218;
+// solvers.py:309):
+//   * reflectors follow LAPACK dlarfg/dgeqr2 (beta = -sign(alpha)*||x||,
+//     tau = (beta-alpha)/beta, v = x/(alpha-beta));
+//   * diag(R) is normalised to be >= 0 (row sign flips of R and Q^T Sb,
+//     which leave x unchanged);
+//   * rank check |R[c,c]| < RANK_TOL * ||M||_F (RANK_TOL = 1e-14) reports
+//     the first offending column;
+//   * x = R^{-1} (Q^T Sb), the triangular solve in the column order of
+//     LAPACK dtrsv ('U','N').
+// Q^T Sb is obtained by applying the reflectors to the Sb column as the
+// (n+1)-th trailing column; Q itself is only formed when requested
+// (economy_qr), by backward accumulation of the reflectors into I.
+//
+// Execution: one persistent cooperative kernel; step k is split across all
+// CTAs (each owns trailing columns round-robin) with one grid barrier per
+// step.  The CTA that updates column k+1 also computes its norm and
+// publishes (alpha, ||x||) so the next step starts without a reduction.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "skl_common.h"
+
+namespace cg = cooperative_groups;
+
+namespace skl {
+
+constexpr int QR_NT = 256;
+constexpr double RANK_TOL = 1e-14;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // deterministic: fixed shuffle tree, then warp 0 folds the warp sums
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+struct QrParams {
+  double* M;        // d x (n+1), ld = d (working copy, destroyed)
+  int64_t d, n;
+  double* tau;      // n
+  double* beta;     // n   (diag of R before sign normalisation)
+  double* colinfo;  // 2*(n+1): alpha, xnorm of the current pivot column
+};
+
+// Norm of column j below row k (rows k+1..d-1) and alpha = M[k, j].
+__device__ void publish_column(const QrParams& p, int64_t k, int64_t j, double* red) {
+  const double* col = p.M + j * p.d;
+  double s = 0.0;
+  for (int64_t i = k + 1 + threadIdx.x; i < p.d; i += QR_NT) s += col[i] * col[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    p.colinfo[2 * k] = col[k];
+    p.colinfo[2 * k + 1] = sqrt(s);
+  }
+}
+
+__global__ void __launch_bounds__(QR_NT) qr_householder_kernel(QrParams p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[33];
+  const int64_t d = p.d, n = p.n;
+  if (blockIdx.x == 0) publish_column(p, 0, 0, red);
+  grid.sync();
+  for (int64_t k = 0; k < n; ++k) {
+    const double alpha = p.colinfo[2 * k];
+    const double xnorm = p.colinfo[2 * k + 1];
+    double tau, beta, scale;
+    if (xnorm == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+      scale = 0.0;
+    } else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.tau[k] = tau;
+      p.beta[k] = beta;
+    }
+    const double* vk = p.M + k * d;
+    // trailing columns j = k+1 .. n (n is the Sb column)
+    for (int64_t j = k + 1 + blockIdx.x; j <= n; j += gridDim.x) {
+      double* cj = p.M + j * d;
+      if (tau != 0.0) {
+        double s = 0.0;
+        for (int64_t i = k + 1 + threadIdx.x; i < d; i += QR_NT) s += (vk[i] * scale) * cj[i];
+        s = block_sum(s, red);
+        const double w = tau * (cj[k] + s);
+        for (int64_t i = k + 1 + threadIdx.x; i < d; i += QR_NT) cj[i] -= (vk[i] * scale) * w;
+        __syncthreads();
+        if (threadIdx.x == 0) cj[k] -= w;
+      }
+      __syncthreads();
+      if (j == k + 1 && k + 1 < n) publish_column(p, k + 1, j, red);
+    }
+    grid.sync();
+  }
+}
+
+// Store v (scaled reflector, implicit unit head) below the diagonal so Q can
+// be formed: v_i = M[i,k] / (alpha_k - beta_k).  alpha_k is lost after the
+// step, recover it from beta and tau: alpha - beta = -beta*tau... (tau =
+// (beta-alpha)/beta  =>  alpha - beta = -tau*beta).
+__global__ void qr_scale_reflectors(double* M, int64_t d, int64_t n, const double* tau,
+                                    const double* beta) {
+  for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+    const double t = tau[k];
+    const double scale = t != 0.0 ? 1.0 / (-t * beta[k]) : 0.0;
+    for (int64_t i = k + 1 + threadIdx.x; i < d; i += blockDim.x) M[k * d + i] *= scale;
+  }
+}
+
+// Rank check + R output with nonnegative diagonal, y = sign-fixed Q^T Sb.
+// One CTA.  fro2 = ||SA||_F^2 computed beforehand.
+__global__ void qr_finish_kernel(const double* M, int64_t d, int64_t n, const double* beta,
+                                 const double* fro2, double* R, int64_t ldr, double* y,
+                                 int64_t* bad_col, double* bad_val) {
+  __shared__ int64_t first_bad;
+  if (threadIdx.x == 0) first_bad = -1;
+  __syncthreads();
+  const double fro = sqrt(*fro2);
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const double dg = fabs(beta[c]);
+    const bool bad = fro > 0.0 ? (dg < RANK_TOL * fro) : true;
+    if (bad) atomicMin((unsigned long long*)&first_bad, (unsigned long long)c);
+  }
+  // atomicMin on -1 (all ones) works as "no bad column yet"
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *bad_col = first_bad == (int64_t)-1 ? -1 : first_bad;
+    *bad_val = (first_bad >= 0 && fro > 0.0) ? fabs(beta[first_bad]) : 0.0;
+  }
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+    const double sg = beta[r] < 0.0 ? -1.0 : 1.0;
+    y[r] = sg * M[n * d + r];
+    if (R) {
+      for (int64_t c = 0; c < n; ++c) {
+        double v = 0.0;
+        if (c > r) v = sg * M[c * d + r];
+        else if (c == r) v = sg * beta[r];
+        R[c * ldr + r] = v;
+      }
+    }
+  }
+}
+
+// Column-oriented back substitution (dtrsv 'U','N' order):
+// for j = n-1..0: x_j = y_j / R_jj; y_i -= x_j * R_ij (i < j).
+// R is read from the factored M (upper part) with the sign-normalised
+// diagonal; one CTA, y in shared memory when it fits.
+__global__ void __launch_bounds__(1024) qr_backsolve_kernel(const double* M, int64_t d, int64_t n,
+                                                            const double* beta, const double* y_in,
+                                                            double* x) {
+  extern __shared__ double ys[];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y_in[i];
+  __syncthreads();
+  for (int64_t j = n - 1; j >= 0; --j) {
+    const double sgj = beta[j] < 0.0 ? -1.0 : 1.0;
+    const double xj = ys[j] / fabs(beta[j]);
+    __syncthreads();
+    if (threadIdx.x == 0) x[j] = xj;
+    for (int64_t i = threadIdx.x; i < j; i += blockDim.x) {
+      const double sgi = beta[i] < 0.0 ? -1.0 : 1.0;
+      ys[i] -= xj * (sgi * M[j * d + i]);
+    }
+    (void)sgj;
+    __syncthreads();
+  }
+}
+
+// Q = H_0 H_1 ... H_{n-1} [I; 0] by backward accumulation (dorg2r), one
+// cooperative kernel, then column sign normalisation.
+__global__ void __launch_bounds__(QR_NT) qr_form_q_kernel(const double* V, int64_t d, int64_t n,
+                                                          const double* tau, const double* beta,
+                                                          double* Q, int64_t ldq) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[33];
+  // Q = [I; 0]
+  for (int64_t c = blockIdx.x; c < n; c += gridDim.x)
+    for (int64_t i = threadIdx.x; i < d; i += QR_NT) Q[c * ldq + i] = (i == c) ? 1.0 : 0.0;
+  grid.sync();
+  for (int64_t k = n - 1; k >= 0; --k) {
+    const double t = tau[k];
+    if (t != 0.0) {
+      const double* v = V + k * d;  // v_k = 1, v_i (i>k) stored
+      for (int64_t j = k + blockIdx.x; j < n; j += gridDim.x) {
+        double* qj = Q + j * ldq;
+        double s = 0.0;
+        for (int64_t i = k + 1 + threadIdx.x; i < d; i += QR_NT) s += v[i] * qj[i];
+        s = block_sum(s, red);
+        const double w = t * (qj[k] + s);
+        for (int64_t i = k + 1 + threadIdx.x; i < d; i += QR_NT) qj[i] -= v[i] * w;
+        __syncthreads();
+        if (threadIdx.x == 0) qj[k] -= w;
+        __syncthreads();
+      }
+    }
+    grid.sync();
+  }
+  for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+    if (beta[c] < 0.0)
+      for (int64_t i = threadIdx.x; i < d; i += QR_NT) Q[c * ldq + i] = -Q[c * ldq + i];
+  }
+}
+
+__global__ void copy_aug_kernel(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
+                                int64_t n, double* M, double* fro_part) {
+  // M[:, :n] = SA, M[:, n] = Sb; per-block partial of ||SA||_F^2
+  __shared__ double red[33];
+  double s = 0.0;
+  const int64_t total = d * (n + 1);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / d, i = idx % d;
+    double v;
+    if (c < n) {
+      v = SA[c * ldsa + i];
+      s += v * v;
+    } else {
+      v = Sb ? Sb[i] : 0.0;
+    }
+    M[idx] = v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) fro_part[blockIdx.x] = s;
+}
+
+__global__ void sum_parts_kernel(const double* part, int nparts, double* out) {
+  __shared__ double red[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
+                            int64_t n, double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
+                            int64_t* bad_col, double* bad_val, void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  SKL_REQUIRE(d >= n && n >= 1, SKL_ERR_SHAPE,
+              "economy_qr requires rows >= cols, got %lldx%lld", (long long)d, (long long)n);
+  SKL_REQUIRE(SA && ldsa >= d && bad_col && bad_val, SKL_ERR_INVALID, "qr_solve: bad arguments");
+  SKL_REQUIRE(!R || ldr >= n, SKL_ERR_INVALID, "qr_solve: ldr < n");
+  SKL_REQUIRE(!Q || ldq >= d, SKL_ERR_INVALID, "qr_solve: ldq < d");
+  SKL_REQUIRE(n <= (48 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
+
+  const int fro_blocks = 256;
+  // workspace: M, tau, beta, colinfo, y, fro parts, fro2, bad (int64), badval
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t oM = take((size_t)d * (n + 1) * 8), oTau = take(n * 8), oBeta = take(n * 8),
+               oInfo = take(2 * (n + 1) * 8), oY = take(n * 8), oPart = take(fro_blocks * 8),
+               oFro = take(8), oBad = take(8), oBadV = take(8), oX = take(n * 8);
+  unsigned char* ws = nullptr;
+  SKL_CUDA(cudaMallocAsync(&ws, off, st));
+  double* M = (double*)(ws + oM);
+  double* tau = (double*)(ws + oTau);
+  double* beta = (double*)(ws + oBeta);
+  double* info = (double*)(ws + oInfo);
+  double* y = (double*)(ws + oY);
+  double* part = (double*)(ws + oPart);
+  double* fro2 = (double*)(ws + oFro);
+  int64_t* badc = (int64_t*)(ws + oBad);
+  double* badv = (double*)(ws + oBadV);
+  double* xd = x ? x : (double*)(ws + oX);
+
+  int rc = SKL_OK;
+  do {
+    copy_aug_kernel<<<fro_blocks, 256, 0, st>>>(SA, ldsa, Sb, d, n, M, part);
+    sum_parts_kernel<<<1, 256, 0, st>>>(part, fro_blocks, fro2);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_householder_kernel, QR_NT, 0);
+    int grid = (int)std::min<int64_t>((int64_t)sms * std::max(1, per_sm), n + 1);
+    QrParams p{M, d, n, tau, beta, info};
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)qr_householder_kernel, grid, QR_NT, args, 0, st);
+    if (e != cudaSuccess) {
+      set_error("qr kernel launch failed: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    qr_finish_kernel<<<1, 256, 0, st>>>(M, d, n, beta, fro2, R, ldr, y, badc, badv);
+    qr_backsolve_kernel<<<1, 1024, n * sizeof(double), st>>>(M, d, n, beta, y, xd);
+    if (Q) {
+      qr_scale_reflectors<<<(int)std::min<int64_t>(n, 1024), 256, 0, st>>>(M, d, n, tau, beta);
+      int gq = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gq, qr_form_q_kernel, QR_NT, 0);
+      int gridq = (int)std::min<int64_t>((int64_t)sms * std::max(1, gq), n);
+      void* qargs[] = {&M, &d, &n, &tau, &beta, &Q, &ldq};
+      e = cudaLaunchCooperativeKernel((void*)qr_form_q_kernel, gridq, QR_NT, qargs, 0, st);
+      if (e != cudaSuccess) {
+        set_error("form-Q kernel launch failed: %s", cudaGetErrorString(e));
+        rc = SKL_ERR_CUDA;
+        break;
+      }
+    }
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_col, badc, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_val, badv, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("qr_solve: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+    }
+  } while (0);
+  cudaFreeAsync(ws, st);
+  if (rc == SKL_OK && *bad_col >= 0) {
+    set_error("input is numerically rank deficient at column %lld (|R[%lld,%lld]| = %.3e)",
+              (long long)*bad_col, (long long)*bad_col, (long long)*bad_col, *bad_val);
+    return SKL_ERR_SINGULAR;
+  }
+  return rc;
+}

@@ -1,0 +1,259 @@
+"""Carriers and the device reduced-solve kernels.
+
+Carriers keep the reference's conventions
+(/root/reference/pkg/src/sketchls/linalg.py:31-133): dense matrices are
+fp64 column-major, sparse matrices are CSR with int64 indices and strictly
+increasing columns, every carrier is immutable after construction.  A
+carrier may additionally hold a CUDA tensor (device-resident data, the
+engine's native habitat); host numpy data is moved to the device by the
+kernels that consume it.
+
+``economy_qr`` (linalg.py:166-192) and the inverse-R solve
+(linalg.py:214-218) run on the device through ``skl_qr_solve``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse
+
+from . import _native
+from ._device import current_stream, device_f64, require_cuda, to_device, torch
+from .errors import ShapeError, SingularFactorError
+
+# Relative threshold below which a diagonal entry of R marks the input as
+# rank deficient (linalg.py:23).
+RANK_TOL = 1e-14
+
+
+def _freeze(a: np.ndarray) -> np.ndarray:
+    a.flags.writeable = False
+    return a
+
+
+def _is_tensor(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+@dataclass(frozen=True)
+class DenseMatrix:
+    """Column-major float64 matrix with at least one row and column.
+
+    ``data`` is a read-only Fortran-ordered numpy array (host) or a CUDA
+    float64 tensor with column-major strides (device)."""
+
+    data: object
+
+    def __post_init__(self) -> None:
+        if _is_tensor(self.data):
+            t = self.data
+            if t.dtype != torch.float64 or not t.is_cuda:
+                raise ValueError("device dense matrix must be a CUDA float64 tensor")
+            if t.dim() != 2:
+                raise ShapeError(f"dense matrix must be 2-d, got ndim={t.dim()}")
+            if t.shape[0] < 1 or t.shape[1] < 1:
+                raise ShapeError(f"dense matrix must be nonempty, got shape {tuple(t.shape)}")
+            if not (t.stride(0) == 1 and (t.shape[1] == 1 or t.stride(1) >= t.shape[0])):
+                t = t.t().contiguous().t()
+            if not bool(torch.isfinite(t).all()):
+                raise ValueError("dense matrix entries must be finite")
+            object.__setattr__(self, "data", t)
+            return
+        a = np.asfortranarray(self.data, dtype=np.float64)
+        if a.ndim != 2:
+            raise ShapeError(f"dense matrix must be 2-d, got ndim={a.ndim}")
+        if a.shape[0] < 1 or a.shape[1] < 1:
+            raise ShapeError(f"dense matrix must be nonempty, got shape {a.shape}")
+        if not np.all(np.isfinite(a)):
+            raise ValueError("dense matrix entries must be finite")
+        object.__setattr__(self, "data", _freeze(a))
+
+    @property
+    def rows(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def cols(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def on_device(self) -> bool:
+        return _is_tensor(self.data)
+
+    @property
+    def ld(self) -> int:
+        if self.on_device:
+            return int(self.data.stride(1)) if self.cols > 1 else self.rows
+        return self.rows
+
+    def to_numpy(self) -> np.ndarray:
+        if self.on_device:
+            return np.asfortranarray(self.data.cpu().numpy())
+        return self.data
+
+
+@dataclass(frozen=True)
+class SparseMatrix:
+    """Compressed-row float64 matrix with strictly increasing column indices
+    per row (linalg.py:56-114).  Host arrays; a device copy is cached on
+    first use by the kernels."""
+
+    rows: int
+    cols: int
+    indptr: np.ndarray
+    indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self) -> None:
+        if self.rows < 1 or self.cols < 1:
+            raise ShapeError(f"sparse matrix must be nonempty, got {self.rows}x{self.cols}")
+        indptr = np.ascontiguousarray(self.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(self.indices, dtype=np.int64)
+        values = np.ascontiguousarray(self.values, dtype=np.float64)
+        if indptr.ndim != 1 or indptr.shape[0] != self.rows + 1:
+            raise ShapeError("row pointers must have length rows+1")
+        if indptr[0] != 0 or np.any(np.diff(indptr) < 0):
+            raise ValueError("row pointers must start at 0 and be nondecreasing")
+        nnz = int(indptr[-1])
+        if indices.shape[0] != nnz or values.shape[0] != nnz:
+            raise ShapeError("index/value arrays must match the final row pointer")
+        if nnz and (indices.min() < 0 or indices.max() >= self.cols):
+            raise ValueError("column indices out of range")
+        if nnz > 1:
+            diffs = np.diff(indices)
+            row_starts = np.zeros(nnz - 1, dtype=bool)
+            interior = indptr[1:-1]
+            interior = interior[(interior > 0) & (interior < nnz)]
+            row_starts[interior - 1] = True
+            if np.any((diffs <= 0) & ~row_starts):
+                raise ValueError("column indices must be strictly increasing within each row")
+        if not np.all(np.isfinite(values)):
+            raise ValueError("sparse matrix values must be finite")
+        object.__setattr__(self, "indptr", _freeze(indptr))
+        object.__setattr__(self, "indices", _freeze(indices))
+        object.__setattr__(self, "values", _freeze(values))
+        object.__setattr__(self, "_dev", {})
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indptr[-1])
+
+    def to_scipy(self) -> scipy.sparse.csr_matrix:
+        return scipy.sparse.csr_matrix(
+            (self.values, self.indices, self.indptr), shape=(self.rows, self.cols)
+        )
+
+    @classmethod
+    def from_scipy(cls, mat) -> "SparseMatrix":
+        csr = scipy.sparse.csr_matrix(mat)
+        csr.sort_indices()
+        csr.sum_duplicates()
+        return cls(csr.shape[0], csr.shape[1], csr.indptr, csr.indices, csr.data)
+
+    def densify(self) -> DenseMatrix:
+        return DenseMatrix(self.to_scipy().toarray())
+
+    def device_arrays(self):
+        """(indptr, indices, values) as CUDA tensors, uploaded once."""
+        require_cuda()
+        dev = torch.cuda.current_device()
+        cache = self._dev
+        if dev not in cache:
+            cache[dev] = (to_device(self.indptr), to_device(self.indices),
+                          to_device(self.values))
+        return cache[dev]
+
+
+@dataclass(frozen=True)
+class Vector:
+    """Contiguous float64 vector (linalg.py:117-133); host numpy or CUDA tensor."""
+
+    data: object
+
+    def __post_init__(self) -> None:
+        if _is_tensor(self.data):
+            t = self.data
+            if t.dtype != torch.float64 or not t.is_cuda:
+                raise ValueError("device vector must be a CUDA float64 tensor")
+            if t.dim() != 1:
+                raise ShapeError(f"vector must be 1-d, got ndim={t.dim()}")
+            t = t.contiguous()
+            if not bool(torch.isfinite(t).all()):
+                raise ValueError("vector entries must be finite")
+            object.__setattr__(self, "data", t)
+            return
+        a = np.ascontiguousarray(self.data, dtype=np.float64)
+        if a.ndim != 1:
+            raise ShapeError(f"vector must be 1-d, got ndim={a.ndim}")
+        if not np.all(np.isfinite(a)):
+            raise ValueError("vector entries must be finite")
+        object.__setattr__(self, "data", _freeze(a))
+
+    @property
+    def len(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return _is_tensor(self.data)
+
+    def to_numpy(self) -> np.ndarray:
+        return self.data.cpu().numpy() if self.on_device else self.data
+
+
+@dataclass(frozen=True)
+class QRFactors:
+    """Economy QR factors: Q has orthonormal columns, R is upper triangular
+    with nonnegative diagonal (linalg.py:136-142)."""
+
+    Q: DenseMatrix
+    R: DenseMatrix
+
+
+Matrix = DenseMatrix | SparseMatrix
+
+
+def _as_device_matrix(M: DenseMatrix):
+    """(tensor, ld) of M on the current CUDA device (column-major)."""
+    if M.on_device:
+        return M.data, M.ld
+    return to_device(M.data), M.rows
+
+
+def qr_solve_device(SA, ldsa: int, Sb, d: int, n: int, want_q: bool = False,
+                    want_r: bool = False):
+    """Device Householder QR + back substitution.  SA: column-major tensor
+    (d x n, ld ldsa); Sb: tensor (d) or None.  Returns (x, R, Q) tensors
+    (R, Q None unless requested).  Raises SingularFactorError with the
+    reference's message (linalg.py:186-191)."""
+    x = device_f64((n,))
+    R = device_f64((n, n), fortran=True) if want_r else None
+    Q = device_f64((d, n), fortran=True) if want_q else None
+    bad_col = np.zeros(1, dtype=np.int64)
+    bad_val = np.zeros(1, dtype=np.float64)
+    _native.call(
+        "skl_qr_solve", _native.ptr(SA), ldsa, _native.ptr(Sb), d, n, _native.ptr(x),
+        _native.ptr(R), n, _native.ptr(Q), d, _native.ptr(bad_col), _native.ptr(bad_val),
+        current_stream())
+    return x, R, Q
+
+
+def economy_qr(M: DenseMatrix) -> QRFactors:
+    """Householder QR of a tall matrix on the device, M = Q R, diag(R) >= 0
+    (linalg.py:166-192).  Factors come back on the side M lives on."""
+    if M.rows < M.cols:
+        raise ShapeError(f"economy_qr requires rows >= cols, got {M.rows}x{M.cols}")
+    require_cuda()
+    t, ld = _as_device_matrix(M)
+    _, R, Q = qr_solve_device(t, ld, None, M.rows, M.cols, want_q=True, want_r=True)
+    if M.on_device:
+        return QRFactors(Q=DenseMatrix(Q), R=DenseMatrix(R))
+    return QRFactors(Q=DenseMatrix(Q.cpu().numpy()), R=DenseMatrix(R.cpu().numpy()))
+
+
+def _check_diagonal(r: np.ndarray) -> None:
+    zero = np.flatnonzero(np.diagonal(r) == 0.0)
+    if zero.size:
+        raise SingularFactorError(f"zero diagonal entry at index {int(zero[0])}")

@@ -1,0 +1,362 @@
+"""Sketching operators on the B200 engine.
+
+Public surface and semantics follow /root/reference/pkg/src/sketchls/sketch.py
+(`KINDS` :31-32, `default_embed_dim` :41-45, `SketchSpec` :48-63,
+`SketchOperator` :66-81, `build_sketch` :84-127, `apply_to_matrix` :180-188,
+`apply_to_vector` :191-195, `_apply` :198-223, `materialize` :226-242).
+
+What changes is where the work runs:
+
+* the seeded draws (bucket hashes, signs, SRHT sign diagonal and row sample)
+  come from the native bit-exact Philox generator (``_native``), identical
+  to what numpy 2.3.5 produces for the reference;
+* a CountSketch operator keeps its hashes (not a scipy CSR) plus a chunked,
+  bucket-sorted *plan* cached on the device; the apply is the
+  ``skl_countsketch_dense`` kernel (bitwise-equal to scipy's
+  ``csr_matvecs`` fold) or the CSR scatter kernel;
+* SRHT and Gaussian applies run in their own sm_100a kernels.
+
+There is no host fallback: without the CUDA library the applies raise.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse
+
+from . import _native
+from ._device import current_stream, device_f64, require_cuda, to_device, torch
+from .errors import CapacityError, ShapeError, SpecError
+from .linalg import DenseMatrix, Matrix, SparseMatrix, Vector, _freeze
+from .rng import derive_seed
+
+KINDS = ("gaussian", "srht", "countsketch", "sparsesign", "identity")
+DEFAULT_KIND = "countsketch"
+# Kinds with a native implementation in this engine (sparsesign is "next").
+ENGINE_KINDS = ("gaussian", "srht", "countsketch", "identity")
+
+_MATERIALIZE_GUARD = 10**7
+
+# Rows per plan chunk of the CountSketch apply (multiple of 8, <= 32768).
+PLAN_CHUNK = 2048
+
+
+def default_embed_dim(m: int, n: int, d_factor: float = 4.0) -> int:
+    """ceil(d_factor*n) clamped to [n, m] (sketch.py:41-45)."""
+    return min(m, max(n, math.ceil(d_factor * n)))
+
+
+@dataclass(frozen=True)
+class SketchSpec:
+    """Declarative description of a sketching map (sketch.py:48-63)."""
+
+    kind: str
+    embed_dim: int
+    seed: int = 0
+    sparsity: int = 8
+
+    def __post_init__(self) -> None:
+        if self.kind not in KINDS:
+            raise SpecError(f"unknown sketch kind {self.kind!r}, expected one of {KINDS}")
+        if self.embed_dim < 1:
+            raise SpecError(f"embed_dim must be >= 1, got {self.embed_dim}")
+        if self.kind == "sparsesign" and self.sparsity < 1:
+            raise SpecError(f"sparsity must be >= 1, got {self.sparsity}")
+
+
+class SketchOperator:
+    """A seeded realisation of a sketch for one source dimension.
+
+    Immutable; rebuilding with the same (spec, m) reproduces it bitwise.
+    Besides the reference's fields it keeps the raw CountSketch hashes
+    (``rows`` int32, ``signs`` int8) and per-device caches of what the
+    kernels consume.  ``sparse_map`` / ``gaussian_entries`` are built on
+    demand for compatibility with code that inspects them."""
+
+    __slots__ = ("kind", "source_dim", "target_dim", "rows", "signs", "sign_diag",
+                 "row_sample", "padded_dim", "key", "_dev", "_host")
+
+    def __init__(self, kind, source_dim, target_dim, rows=None, signs=None, sign_diag=None,
+                 row_sample=None, padded_dim=None, key=None):
+        for name, val in (("kind", kind), ("source_dim", source_dim),
+                          ("target_dim", target_dim), ("rows", rows), ("signs", signs),
+                          ("sign_diag", sign_diag), ("row_sample", row_sample),
+                          ("padded_dim", padded_dim), ("key", key)):
+            object.__setattr__(self, name, val)
+        object.__setattr__(self, "_dev", {})
+        object.__setattr__(self, "_host", {})
+
+    def __setattr__(self, name, value):
+        raise AttributeError("SketchOperator is immutable")
+
+    def __repr__(self) -> str:
+        return (f"SketchOperator(kind={self.kind!r}, source_dim={self.source_dim}, "
+                f"target_dim={self.target_dim})")
+
+    # ------------------------------------------------ reference-compatible views
+    @property
+    def sparse_map(self):
+        """d x m scipy CSR of a CountSketch (sketch.py:100-102), built lazily."""
+        if self.kind != "countsketch":
+            return None
+        if "csr" not in self._host:
+            m, d = self.source_dim, self.target_dim
+            self._host["csr"] = scipy.sparse.csr_matrix(
+                (self.signs.astype(np.float64), (self.rows.astype(np.int64), np.arange(m))),
+                shape=(d, m), dtype=np.float64)
+        return self._host["csr"]
+
+    @property
+    def gaussian_entries(self):
+        """d x m Gaussian entries (sketch.py:94-96), copied back from the device."""
+        if self.kind != "gaussian":
+            return None
+        if "g" not in self._host:
+            G, ldg = self.device_gaussian()
+            host = G[:, : self.source_dim].cpu().numpy() if ldg != self.source_dim else G.cpu().numpy()
+            self._host["g"] = _freeze(np.ascontiguousarray(host))
+        return self._host["g"]
+
+    # ------------------------------------------------------------ device caches
+    def _cache(self):
+        dev = torch.cuda.current_device()
+        return self._dev.setdefault(dev, {})
+
+    def device_plan(self):
+        """(entries, offsets) of the CountSketch plan on the current device."""
+        require_cuda()
+        c = self._cache()
+        if "plan" not in c:
+            ent, off = _native.countsketch_plan(self.rows, self.signs, self.target_dim, PLAN_CHUNK)
+            c["plan"] = (to_device(ent), to_device(off))
+        return c["plan"]
+
+    def device_buckets(self):
+        """(bucket_rows int32, bucket_ptr int64, signs int8) on the current
+        device: the CSR of S consumed by the CSR-operand kernel."""
+        require_cuda()
+        c = self._cache()
+        if "buckets" not in c:
+            brow, bptr = _native.countsketch_buckets(self.rows, self.target_dim)
+            c["buckets"] = (to_device(brow), to_device(bptr), to_device(self.signs))
+        return c["buckets"]
+
+    def device_srht(self):
+        require_cuda()
+        c = self._cache()
+        if "srht" not in c:
+            signs8 = np.where(self.sign_diag > 0, 1, -1).astype(np.int8)
+            c["srht"] = (to_device(signs8), to_device(self.row_sample))
+        return c["srht"]
+
+    def device_gaussian(self):
+        """G (d x m, row-major like numpy's C order, ld = ldg) on the device."""
+        require_cuda()
+        c = self._cache()
+        if "gauss" not in c:
+            d, m = self.target_dim, self.source_dim
+            ldg = (m + 31) // 32 * 32
+            G = torch.empty((d, ldg), dtype=torch.float64, device="cuda")
+            _native.call("skl_rng_gaussian_device", self.key, d, m, _native.ptr(G), ldg,
+                         current_stream())
+            c["gauss"] = (G, ldg)
+        return c["gauss"]
+
+
+def build_sketch(spec: SketchSpec, m: int) -> SketchOperator:
+    """Realise ``spec`` for source dimension ``m`` (sketch.py:84-127)."""
+    if m < 1:
+        raise SpecError(f"source dimension must be >= 1, got {m}")
+    if spec.kind == "identity":
+        return SketchOperator(kind="identity", source_dim=m, target_dim=m)
+    d = spec.embed_dim
+    if d > m:
+        raise SpecError(f"embed_dim {d} exceeds source dimension {m} for kind {spec.kind!r}")
+    key = derive_seed(spec.seed, spec.kind, m)
+    if spec.kind == "gaussian":
+        return SketchOperator("gaussian", m, d, key=key)
+    if spec.kind == "countsketch":
+        rows, signs = _native.rng_countsketch(key, m, d)
+        return SketchOperator("countsketch", m, d, rows=_freeze(rows), signs=_freeze(signs),
+                              key=key)
+    if spec.kind == "sparsesign":
+        raise SpecError("sparsesign is not implemented by the B200 engine yet "
+                        f"(engine kinds: {ENGINE_KINDS})")
+    m_pad = 1 << (m - 1).bit_length()
+    signs8, sample = _native.rng_srht(key, m_pad, d)
+    return SketchOperator("srht", m, d, sign_diag=_freeze(signs8.astype(np.float64)),
+                          row_sample=_freeze(sample), padded_dim=m_pad, key=key)
+
+
+# ------------------------------------------------------------------ applies
+def _aligned(t, ld: int, cols: int):
+    """Return (tensor, ld) satisfying the kernels' 16-byte alignment rules,
+    copying on the device when the caller's layout does not."""
+    if t.data_ptr() % 16 == 0 and (ld % 2 == 0 or cols == 1):
+        return t, ld
+    rows = t.shape[0]
+    ld2 = (rows + 1) // 2 * 2
+    out = device_f64((rows, cols), fortran=True, ld=ld2)
+    out.copy_(t)
+    return out, ld2
+
+
+def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
+    """SA (d x n column-major tensor) and Sb (d) or None, all on device."""
+    ent, off = op.device_plan()
+    d, m = op.target_dim, op.source_dim
+    A, lda = _aligned(A, lda, n)
+    if b is not None and b.data_ptr() % 16:
+        b = b.clone()
+    SA = device_f64((d, n), fortran=True)
+    Sb = device_f64((d,)) if b is not None else None
+    _native.call("skl_countsketch_dense", _native.ptr(A), m, n, lda, _native.ptr(b),
+                 _native.ptr(ent), _native.ptr(off), d, PLAN_CHUNK, _native.ptr(SA), d,
+                 _native.ptr(Sb), 0, 0, current_stream())
+    return SA, Sb
+
+
+def _countsketch_dense_host(op: SketchOperator, A: np.ndarray, n: int,
+                            b: np.ndarray | None = None):
+    """Host buffers in, host SA/Sb out; H2D streamed under the kernel."""
+    ent, off = op.device_plan()
+    d, m = op.target_dim, op.source_dim
+    A = np.asfortranarray(A)
+    SA = np.empty((d, n), dtype=np.float64, order="F")
+    Sb = np.empty(d, dtype=np.float64) if b is not None else None
+    _native.call("skl_countsketch_dense_host", _native.ptr(A), m, n, A.shape[0] if A.ndim == 2
+                 else m, _native.ptr(b), _native.ptr(ent), _native.ptr(off), d, PLAN_CHUNK,
+                 _native.ptr(SA), d, _native.ptr(Sb), None, 0, None, current_stream())
+    return SA, Sb
+
+
+def _countsketch_csr_device(op: SketchOperator, A: SparseMatrix):
+    require_cuda()
+    indptr, indices, values = A.device_arrays()
+    brow, bptr, signs = op.device_buckets()
+    d, n = op.target_dim, A.cols
+    SA = device_f64((d, n), fortran=True)
+    _native.call("skl_countsketch_csr", _native.ptr(indptr), _native.ptr(indices),
+                 _native.ptr(values), A.rows, n, _native.ptr(brow), _native.ptr(bptr),
+                 _native.ptr(signs), d, _native.ptr(SA), d, current_stream())
+    return SA
+
+
+def _srht_device(op: SketchOperator, A, lda: int, n: int):
+    signs, sample = op.device_srht()
+    A, lda = _aligned(A, lda, n)
+    d = op.target_dim
+    SA = device_f64((d, n), fortran=True)
+    _native.call("skl_srht_dense", _native.ptr(A), op.source_dim, n, lda, _native.ptr(signs),
+                 _native.ptr(sample), op.padded_dim, d, _native.ptr(SA), d, current_stream())
+    return SA
+
+
+def _gaussian_device(op: SketchOperator, A, lda: int, n: int):
+    G, ldg = op.device_gaussian()
+    A, lda = _aligned(A, lda, n)
+    d = op.target_dim
+    SA = device_f64((d, n), fortran=True)
+    _native.call("skl_gemm_f64", _native.ptr(G), ldg, _native.ptr(A), lda, _native.ptr(SA), d,
+                 d, n, op.source_dim, 0, current_stream())
+    return SA
+
+
+def _apply_device(op: SketchOperator, operand):
+    """S @ operand on the device.  operand: DenseMatrix | SparseMatrix | Vector.
+    Returns a column-major tensor (d x n) or a vector tensor (d)."""
+    require_cuda()
+    if isinstance(operand, SparseMatrix):
+        if op.kind == "countsketch":
+            return _countsketch_csr_device(op, operand)
+        if op.kind == "identity":
+            return to_device(operand.to_scipy().toarray(order="F"))
+        # srht / gaussian: the reference densifies the CSR input
+        # (sketch.py:205-206, 214) -- do the same on the device.
+        dense = to_device(np.asfortranarray(operand.to_scipy().toarray()))
+        return _apply_dense_tensor(op, dense, operand.rows, operand.cols)
+    if isinstance(operand, Vector):
+        v = operand.data if operand.on_device else to_device(operand.data)
+        out = _apply_dense_tensor(op, v.reshape(-1, 1), operand.len, 1, lda=operand.len)
+        return out.reshape(-1)
+    t = operand.data if operand.on_device else to_device(operand.data)
+    return _apply_dense_tensor(op, t, operand.rows, operand.cols, lda=operand.ld)
+
+
+def _apply_dense_tensor(op: SketchOperator, t, m: int, n: int, lda: int | None = None):
+    lda = lda if lda is not None else (int(t.stride(1)) if n > 1 else m)
+    if op.kind == "identity":
+        return t.clone()
+    if op.kind == "countsketch":
+        SA, _ = _countsketch_dense_device(op, t, lda, n)
+        return SA
+    if op.kind == "srht":
+        return _srht_device(op, t, lda, n)
+    if op.kind == "gaussian":
+        return _gaussian_device(op, t, lda, n)
+    raise SpecError(f"kind {op.kind!r} is not implemented by the B200 engine")
+
+
+def apply_to_matrix(op: SketchOperator, A: Matrix) -> DenseMatrix:
+    """S A as a dense d x n matrix (sketch.py:180-188).  Host carriers give a
+    host result, device carriers a device result."""
+    if A.rows != op.source_dim:
+        raise ShapeError(f"operator expects {op.source_dim} rows, matrix has {A.rows}")
+    if isinstance(A, DenseMatrix) and not A.on_device and op.kind == "countsketch":
+        SA, _ = _countsketch_dense_host(op, A.data, A.cols)
+        return DenseMatrix(SA)
+    out = _apply_device(op, A)
+    if isinstance(A, DenseMatrix) and A.on_device:
+        return DenseMatrix(out)
+    return DenseMatrix(out.cpu().numpy())
+
+
+def apply_to_vector(op: SketchOperator, b: Vector) -> Vector:
+    """S b as a length-d vector (sketch.py:191-195)."""
+    if b.len != op.source_dim:
+        raise ShapeError(f"operator expects length {op.source_dim}, vector has {b.len}")
+    out = _apply_device(op, b)
+    return Vector(out if b.on_device else out.cpu().numpy())
+
+
+def fwht_inplace(x):
+    """In-place unnormalised FWHT along the leading dimension (sketch.py:152-177),
+    computed on the device.  Same argument checks as the reference."""
+    a = x if isinstance(x, np.ndarray) else np.asarray(x)
+    if a.dtype != np.float64:
+        raise ValueError("fwht_inplace requires a float64 array")
+    if a.ndim not in (1, 2):
+        raise ShapeError("fwht_inplace expects a 1-d or 2-d array")
+    n = a.shape[0]
+    if n < 1 or (n & (n - 1)) != 0:
+        raise ShapeError(f"fwht_inplace requires a power-of-two length, got {n}")
+    if not (a.flags.c_contiguous and a.flags.writeable):
+        raise ValueError("fwht_inplace requires a writable C-contiguous array")
+    cols = 1 if a.ndim == 1 else a.shape[1]
+    dev = to_device(np.asfortranarray(a.reshape(n, cols)))
+    _native.call("skl_fwht_device", _native.ptr(dev), n, cols, n, current_stream())
+    a.reshape(n, cols)[...] = dev.cpu().numpy()
+    return x
+
+
+def materialize(op: SketchOperator) -> DenseMatrix:
+    """Explicit d x m matrix equal to the operator (sketch.py:226-242).
+    Test/inspection helper, guarded at d*m <= 1e7 entries."""
+    d, m = op.target_dim, op.source_dim
+    if d * m > _MATERIALIZE_GUARD:
+        raise CapacityError(f"materialize guard exceeded: {d}x{m} > {_MATERIALIZE_GUARD} entries")
+    if op.kind == "identity":
+        return DenseMatrix(np.eye(m))
+    if op.kind == "gaussian":
+        return DenseMatrix(op.gaussian_entries.copy())
+    if op.kind == "countsketch":
+        out = np.zeros((d, m))
+        out[op.rows, np.arange(m)] = op.signs
+        return DenseMatrix(out)
+    cols = np.arange(m, dtype=np.int64)
+    parity = np.bitwise_count(op.row_sample[:, None] & cols[None, :]) & 1
+    h_rows = 1.0 - 2.0 * parity.astype(np.float64)
+    return DenseMatrix(h_rows * op.sign_diag[:m][None, :] / math.sqrt(d))

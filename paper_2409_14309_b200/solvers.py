@@ -1,0 +1,180 @@
+"""Sketch-and-apply least squares on the B200 engine.
+
+Mirrors /root/reference/pkg/src/sketchls/solvers.py: `LeastSquaresProblem`
+:43-60, `SolverOptions` :63-87, `SolveResult` :90-99, `_operator_spec`
+:273-279, `_sketch_qr` :282-293, `sketch_and_apply` :296-320 and the
+dispatcher `solve` :364-398.  The SAA path keeps everything on the device:
+operator build (host RNG, cached plan) -> one sketch pass over [A | b] ->
+Householder QR + back substitution -> a second pass for ||Ax - b||.
+
+Methods other than "saa" (LSQR, sketch-and-precondition, direct) are
+outside this engine's hot path and raise ``SpecError``.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native
+from ._device import current_stream, device_f64, require_cuda, to_device, torch
+from .errors import ShapeError, SingularFactorError, SpecError
+from .linalg import DenseMatrix, Matrix, SparseMatrix, Vector, qr_solve_device
+from .rng import derive_seed
+from .sketch import (
+    DEFAULT_KIND,
+    SketchSpec,
+    _apply_dense_tensor,
+    _countsketch_csr_device,
+    _countsketch_dense_device,
+    build_sketch,
+    default_embed_dim,
+)
+
+METHODS = ("lsqr", "saa", "sap", "direct")
+ENGINE_METHODS = ("saa",)
+
+
+@dataclass(frozen=True)
+class LeastSquaresProblem:
+    """min_x ||A x - b|| (solvers.py:43-60)."""
+
+    A: Matrix
+    b: Vector
+    x_star: Vector | None = None
+    beta: float | None = None
+
+    def __post_init__(self) -> None:
+        if self.b.len != self.A.rows:
+            raise ShapeError(f"A is {self.A.rows}x{self.A.cols} but b has length {self.b.len}")
+        if self.x_star is not None and self.x_star.len != self.A.cols:
+            raise ShapeError(f"x_star has length {self.x_star.len}, expected {self.A.cols}")
+        if self.beta is not None and not (self.beta >= 0 and math.isfinite(self.beta)):
+            raise SpecError(f"beta must be finite and >= 0, got {self.beta}")
+
+
+@dataclass(frozen=True)
+class SolverOptions:
+    """Tolerances and sizing knobs (solvers.py:63-87).  Only d_factor matters
+    to sketch-and-apply."""
+
+    atol: float = 1e-10
+    btol: float = 1e-10
+    max_iter: int | None = None
+    d_factor: float = 4.0
+    warm_start: bool = True
+
+    def __post_init__(self) -> None:
+        if not (self.atol > 0 and self.btol > 0):
+            raise SpecError("tolerances must be positive")
+        if self.max_iter is not None and self.max_iter < 1:
+            raise SpecError("max_iter must be >= 1")
+        if self.d_factor < 1:
+            raise SpecError("d_factor must be >= 1")
+
+    def resolve_max_iter(self, n: int) -> int:
+        return 4 * n if self.max_iter is None else self.max_iter
+
+
+@dataclass(frozen=True)
+class SolveResult:
+    x: Vector
+    method: str
+    sketch: str | None
+    d: int | None
+    iterations: int
+    residual_norm: float
+    termination: str
+    wall_time_s: float
+
+
+def _operator_spec(spec: SketchSpec | None, method: str, m: int, n: int,
+                   d_factor: float) -> SketchSpec:
+    """d from d_factor, seed mixed with the method tag (solvers.py:273-279)."""
+    if spec is None:
+        spec = SketchSpec(kind=DEFAULT_KIND, embed_dim=1)
+    d = default_embed_dim(m, n, d_factor)
+    return replace(spec, embed_dim=d, seed=derive_seed(spec.seed, method))
+
+
+def _residual_device(A: Matrix, A_dev, lda: int, b_dev, x_dev) -> float:
+    out = np.zeros(1, dtype=np.float64)
+    if isinstance(A, SparseMatrix):
+        indptr, indices, values = A.device_arrays()
+        _native.call("skl_residual_csr", _native.ptr(indptr), _native.ptr(indices),
+                     _native.ptr(values), A.rows, A.cols, _native.ptr(x_dev), _native.ptr(b_dev),
+                     _native.ptr(out), current_stream())
+    else:
+        _native.call("skl_residual_dense", _native.ptr(A_dev), A.rows, A.cols, lda,
+                     _native.ptr(x_dev), _native.ptr(b_dev), _native.ptr(out), current_stream())
+    return float(out[0])
+
+
+def sketch_operands_device(op, A: Matrix, b: Vector):
+    """(SA, Sb, A_dev, lda, b_dev) on the device for one SAA solve; A and b
+    are uploaded once when host-resident and reused for the residual."""
+    b_dev = b.data if b.on_device else to_device(b.data)
+    if isinstance(A, SparseMatrix):
+        if op.kind == "countsketch":
+            SA = _countsketch_csr_device(op, A)
+            Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
+            return SA, Sb, None, 0, b_dev
+        dense = to_device(np.asfortranarray(A.to_scipy().toarray()))
+        SA = _apply_dense_tensor(op, dense, A.rows, A.cols, lda=A.rows)
+        Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
+        return SA, Sb, None, 0, b_dev
+    A_dev = A.data if A.on_device else to_device(A.data)
+    lda = A.ld if A.on_device else A.rows
+    if op.kind == "countsketch":
+        SA, Sb = _countsketch_dense_device(op, A_dev, lda, A.cols, b=b_dev)
+    else:
+        SA = _apply_dense_tensor(op, A_dev, A.rows, A.cols, lda=lda)
+        Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
+    return SA, Sb, A_dev, lda, b_dev
+
+
+def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = None,
+                     opts: SolverOptions | None = None) -> SolveResult:
+    """Solve min ||S A x - S b|| by QR, one shot (solvers.py:296-320)."""
+    A, b = problem.A, problem.b
+    if A.rows < A.cols:
+        raise ShapeError(f"need rows >= cols, got {A.rows}x{A.cols}")
+    require_cuda()
+    opts = opts or SolverOptions()
+    op_spec = _operator_spec(spec, "saa", A.rows, A.cols, opts.d_factor)
+    t0 = time.perf_counter()
+    op = build_sketch(op_spec, A.rows)
+    SA, Sb, A_dev, lda, b_dev = sketch_operands_device(op, A, b)
+    d = op.target_dim
+    try:
+        x_dev, _, _ = qr_solve_device(SA, d, Sb, d, A.cols)
+    except SingularFactorError as exc:
+        raise SingularFactorError(
+            f"sketched matrix ({op_spec.kind}, d={d}) is rank deficient: {exc}; "
+            f"a larger embedding dimension may help") from exc
+    wall = time.perf_counter() - t0
+    rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
+    x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
+    return SolveResult(x=Vector(x), method="saa", sketch=op_spec.kind, d=d, iterations=0,
+                       residual_norm=rnorm, termination="direct", wall_time_s=wall)
+
+
+def solve(problem: LeastSquaresProblem, method: str = "saa", spec: SketchSpec | None = None,
+          opts: SolverOptions | None = None) -> SolveResult:
+    """Dispatch (solvers.py:364-398); wall_time_s covers the full path.
+
+    Note: the reference defaults to ``method="lsqr"``; this engine implements
+    the sketch-and-apply path only, so ``"saa"`` is the default here and the
+    other reference methods raise ``SpecError``."""
+    if method not in METHODS:
+        raise SpecError(f"unknown method {method!r}, expected one of {METHODS}")
+    if method not in ENGINE_METHODS:
+        raise SpecError(f"method {method!r} is outside the B200 engine's scope "
+                        f"(implemented: {ENGINE_METHODS})")
+    t0 = time.perf_counter()
+    result = sketch_and_apply(problem, spec, opts)
+    wall = time.perf_counter() - t0
+    return replace(result, wall_time_s=wall)

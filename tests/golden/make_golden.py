@@ -1,0 +1,168 @@
+"""Generate the golden fixtures from the REFERENCE implementation itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package from /root/reference/pkg/src
+(`sketchls`), runs its public API on seeded inputs from
+paper_2409_14309_b200.workloads (numpy backend) and writes
+tests/golden/golden.npz.  The fixtures pin (a) the oracle restatement
+(tests/test_oracle_golden.py, CPU) and (b) the CUDA engine
+(tests/test_gpu_parity.py).  /root/reference is never read at test time.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import scipy
+import scipy.sparse
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+
+import sketchls as ref  # noqa: E402
+from sketchls.rng import derive_seed, stream  # noqa: E402
+
+from paper_2409_14309_b200 import workloads as W  # noqa: E402
+
+OUT = Path(__file__).resolve().parent / "golden.npz"
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def cs_hashes(op):
+    coo = op.sparse_map.tocoo()
+    order = np.argsort(coo.col, kind="stable")
+    return coo.row[order].astype(np.int32), coo.data[order].astype(np.int8)
+
+
+def main() -> None:
+    g: dict[str, np.ndarray] = {}
+    meta: dict[str, object] = {"numpy": np.__version__, "scipy": scipy.__version__}
+
+    # --- seeds (rng.py:27-40)
+    seed_cases = [(0, ()), (5, ("countsketch", 100)), (2**64 - 1, ("saa",)), (123, ("srht", 64)),
+                  (9, ("A", 3, "noise"))]
+    meta["derive_seed"] = [[s, list(t), derive_seed(s, *t)] for s, t in seed_cases]
+
+    # --- CountSketch hashes/signs (sketch.py:97-99)
+    for m, d, seed in [(100, 4, 5), (20_000, 800, 0), (4097, 16, 3)]:
+        op = ref.build_sketch(ref.SketchSpec("countsketch", d, seed=seed), m)
+        rows, signs = cs_hashes(op)
+        g[f"cs_rows_{m}_{d}_{seed}"] = rows
+        g[f"cs_signs_{m}_{d}_{seed}"] = signs
+    for m, d, seed in [(1 << 20, 2048, 7), (1 << 22, 8192, 11)]:
+        op = ref.build_sketch(ref.SketchSpec("countsketch", d, seed=seed), m)
+        rows, signs = cs_hashes(op)
+        meta[f"cs_sha_{m}_{d}_{seed}"] = sha(rows, signs)
+        g[f"cs_rows_head_{m}_{d}_{seed}"] = rows[:4096]
+        g[f"cs_rows_tail_{m}_{d}_{seed}"] = rows[-4096:]
+
+    # --- SRHT signs and row samples (sketch.py:116-127)
+    for m, d, seed in [(50, 16, 2), (1000, 64, 3), (20_000, 800, 4)]:
+        op = ref.build_sketch(ref.SketchSpec("srht", d, seed=seed), m)
+        g[f"srht_signs_{m}_{d}_{seed}"] = op.sign_diag.astype(np.int8)
+        g[f"srht_sample_{m}_{d}_{seed}"] = op.row_sample
+        meta[f"srht_pad_{m}_{d}_{seed}"] = op.padded_dim
+    op = ref.build_sketch(ref.SketchSpec("srht", 2048, seed=5), 1 << 20)
+    meta["srht_sha_1048576_2048_5"] = sha(op.sign_diag.astype(np.int8))
+    g["srht_sample_1048576_2048_5"] = op.row_sample
+
+    # --- Gaussian entries (sketch.py:94-96)
+    op = ref.build_sketch(ref.SketchSpec("gaussian", 16, seed=1), 64)
+    g["gauss_16_64_1"] = op.gaussian_entries
+    op = ref.build_sketch(ref.SketchSpec("gaussian", 2048, seed=3), 262_144)
+    G = op.gaussian_entries
+    g["gauss_cfg3_head"] = G.ravel()[:4096].copy()
+    g["gauss_cfg3_tail"] = G.ravel()[-4096:].copy()
+    g["gauss_cfg3_rowsums"] = G.sum(axis=1)
+    del G, op
+
+    # --- FWHT known answers (test_sketch.py:29-36)
+    for i, v in enumerate(([1.0, 0, 0, 0], [1.0, 1, 1, 1], [1.0, 2, 3, 4])):
+        g[f"fwht_in_{i}"] = np.array(v)
+        g[f"fwht_out_{i}"] = ref.fwht_inplace(np.array(v))
+    x = stream(4).standard_normal((1024, 3))
+    g["fwht_in_1024x3"] = x
+    g["fwht_out_1024x3"] = ref.fwht_inplace(x.copy())
+
+    # --- small applies of every engine kind (test_sketch.py:159-166 shapes)
+    a = stream(7).standard_normal((64, 5))
+    g["small_A"] = a
+    for kind in ("gaussian", "srht", "countsketch", "identity"):
+        op = ref.build_sketch(ref.SketchSpec(kind, 16, seed=42), 64)
+        g[f"small_SA_{kind}"] = ref.apply_to_matrix(op, ref.DenseMatrix(a)).data
+        g[f"small_Sb_{kind}"] = ref.apply_to_vector(op, ref.Vector(a[:, 0].copy())).data
+
+    # --- QR conventions (linalg.py:166-192)
+    for m, n, seed in [(5, 3, 0), (20, 5, 1), (100, 40, 2)]:
+        M = stream(seed).standard_normal((m, n))
+        f = ref.economy_qr(ref.DenseMatrix(M))
+        g[f"qr_M_{m}_{n}"] = M
+        g[f"qr_Q_{m}_{n}"] = f.Q.data
+        g[f"qr_R_{m}_{n}"] = f.R.data
+
+    # --- SAA solves on the configs (full cfg1, reduced cfg2-5)
+    saa_cases = {
+        "cfg1": (W.config(1), "countsketch"),
+        "cfg2r": (W.config(2, m=1 << 14), "countsketch"),
+        "cfg3r": (W.config(3, m=8192, n=64, d=256), "gaussian"),
+        "cfg4r": (W.config(4, m=1 << 16, n=256, d=2048), "countsketch"),
+        "cfg5r": (W.config(5, m=6000, n=32, d=256), "srht"),
+        "cfg5r_cs": (W.config(5, m=6000, n=32, d=256), "countsketch"),
+    }
+    for name, (c, kind) in saa_cases.items():
+        A, b, _ = W.make_problem(c)
+        Ac = ref.SparseMatrix.from_scipy(A) if scipy.sparse.issparse(A) else ref.DenseMatrix(A)
+        prob = ref.LeastSquaresProblem(A=Ac, b=ref.Vector(b))
+        spec = ref.SketchSpec(kind, 1, seed=W.SEED)
+        opts = ref.SolverOptions(d_factor=c.d / c.n)
+        res = ref.solve(prob, "saa", spec, opts)
+        assert res.d == c.d, (name, res.d, c.d)
+        op = ref.build_sketch(ref.SketchSpec(kind, c.d, seed=derive_seed(W.SEED, "saa")), c.m)
+        SA = ref.apply_to_matrix(op, Ac).data
+        Sb = ref.apply_to_vector(op, ref.Vector(b)).data
+        g[f"{name}_x"] = res.x.data
+        g[f"{name}_Sb"] = Sb
+        meta[f"{name}_residual"] = res.residual_norm
+        meta[f"{name}_SA_sha"] = sha(np.asfortranarray(SA))
+        meta[f"{name}_SA_fro"] = float(np.linalg.norm(SA))
+        if SA.size <= 300_000:
+            g[f"{name}_SA"] = SA
+        else:
+            g[f"{name}_SA_cols"] = SA[:, :4].copy()
+        meta[f"{name}_shape"] = [c.m, c.n, c.d]
+
+    # --- rank-deficient sketch message (test_solvers.py:121-127)
+    rng = stream(15)
+    a = rng.standard_normal((50, 4))
+    a[:, 3] = a[:, 0]
+    bb = rng.standard_normal(50)
+    g["rankdef_A"] = a
+    g["rankdef_b"] = bb
+    try:
+        ref.sketch_and_apply(ref.LeastSquaresProblem(A=ref.DenseMatrix(a), b=ref.Vector(bb)),
+                             ref.SketchSpec("countsketch", 1, seed=16))
+        meta["rankdef_msg"] = None
+    except ref.SingularFactorError as exc:
+        meta["rankdef_msg"] = str(exc)
+
+    g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB)")
+
+
+if __name__ == "__main__":
+    main()
