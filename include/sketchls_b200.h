@@ -87,27 +87,38 @@ int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G_dev, i
 int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);
 
 /* ---------------------------------------------------------------------
- * CountSketch apply plan: per chunk of `chunk` rows, the row offsets
- * sorted stably by bucket (bit 15 = negative sign) and the bucket
- * offsets (stride skl_countsketch_plan_stride(d) uint16 per chunk).
- * It is the chunked form of the reference's CSR sparse_map
- * (sketch.py:100-102) and fixes the ascending-row fold order of
- * scipy's csr_matvecs, so the device apply is bitwise-equal to it.
+ * CountSketch apply plan.  The rows are cut into chunks of `chunk` rows.
+ * Bucket b belongs to warp group w(b) = b / ceil(d / warps) of the consuming
+ * CTA (contiguous ranges keep a warp's lanes on different smem banks);
+ * per chunk the non-empty buckets of each group become "tasks" ordered by
+ * descending entry count (ties by bucket id).  Per chunk k the task block
+ * tasks[k*stride ...] holds
+ *   [0, H)        H = round4(warps+1): first task index of each group
+ *                 (relative to the task list), group `warps` = end;
+ *   [H, H+ntask)  (bucket << 16) | first entry of the task;
+ * and entries[k*chunk + e] = local row (bits 0..14) | negative sign (bit
+ * 15), grouped by task, ascending row inside a task.  It is the chunked
+ * form of the reference's CSR sparse_map (sketch.py:100-102) and keeps
+ * scipy csr_matvecs' ascending-row fold order per bucket, so the device
+ * apply is bitwise-equal to it; a bucket always lands in the same warp and
+ * the count ordering gives the lanes of a warp equal work.
+ * Limits: d <= 65536, chunk a multiple of 8 in [8, 32768], warps in {4,8,16}.
  * ------------------------------------------------------------------- */
-int64_t skl_countsketch_plan_stride(int64_t d);
+int64_t skl_countsketch_plan_stride(int64_t d, int warps);
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
-                         int64_t chunk, uint16_t* entries, uint16_t* offsets, int threads);
+                         int64_t chunk, int warps, uint16_t* entries, uint32_t* tasks,
+                         int32_t* ntask, int threads);
 
-/* S*A and S*b for dense column-major A (device pointers).  b may be NULL
- * (then Sb is ignored).  partitions: 0 = auto, 1 = single ordered pass
- * (bitwise-equal to the reference), P>1 = P row partitions reduced in a
- * fixed order (deterministic).  accumulate != 0 adds into SA/Sb (used for
- * row-streamed applies).  workspace may be NULL (allocated from the
- * stream-ordered pool).  Replaces sketch.py:209-212 (dense branch). */
+/* S*A and S*b for dense column-major A (device pointers, plan on device).
+ * b may be NULL (then Sb is ignored).  partitions: 0 = auto, 1 = single
+ * ordered pass (bitwise-equal to the reference), P>1 = P row partitions
+ * reduced in a fixed order (deterministic).  accumulate != 0 adds into
+ * SA/Sb (used for row-streamed applies).  Replaces sketch.py:209-212
+ * (dense branch). */
 int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
-                          const uint16_t* entries, const uint16_t* offsets, int64_t d,
-                          int64_t chunk, double* SA, int64_t ldsa, double* Sb, int partitions,
-                          int accumulate, void* stream);
+                          const uint16_t* entries, const uint32_t* tasks, const int32_t* ntask,
+                          int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
+                          double* Sb, int partitions, int accumulate, void* stream);
 
 /* Same apply with HOST A/b/SA/Sb: streams row blocks of A through the
  * device with host-to-device copies overlapped with the kernel; if
@@ -115,8 +126,8 @@ int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, co
  * left there for a later residual pass.  plan pointers are device. */
 int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
                                const double* b_host, const uint16_t* entries,
-                               const uint16_t* offsets, int64_t d, int64_t chunk,
-                               double* SA_host, int64_t ldsa, double* Sb_host,
+                               const uint32_t* tasks, const int32_t* ntask, int64_t d,
+                               int64_t chunk, int warps, double* SA_host, int64_t ldsa, double* Sb_host,
                                double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                void* stream);
 

@@ -44,18 +44,30 @@ SIGNATURES: dict[str, tuple] = {
     "skl_rng_u64": (c_int, [c_u64, c_u64, c_i64, c_ptr]),
     "skl_rng_countsketch": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int, c_ptr]),
     "skl_rng_srht": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
-    "skl_countsketch_plan_stride": (c_i64, [c_i64]),
-    "skl_countsketch_plan": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
+    "skl_countsketch_plan_stride": (c_i64, [c_i64, c_int]),
+    "skl_countsketch_plan": (
+        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_int]),
     "skl_countsketch_dense": (
         c_int,
-        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr,
-         c_int, c_int, c_ptr],
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr,
+         c_i64, c_ptr, c_int, c_int, c_ptr],
     ),
     "skl_countsketch_dense_host": (
         c_int,
-        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr,
-         c_ptr, c_i64, c_ptr, c_ptr],
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr,
+         c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     ),
+    "skl_srht_dense": (
+        c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_srht_dense_shard": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_fwht_device": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr]),
+    "skl_gaussian_set_tables": (c_int, [c_ptr, c_ptr, c_ptr]),
+    "skl_rng_gaussian_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_rng_gaussian_host": (c_int, [c_u64, c_i64, c_ptr]),
+    "skl_gemm_f64": (
+        c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_i64, c_int, c_ptr]),
     "skl_countsketch_buckets": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
     "skl_countsketch_csr": (
         c_int,
@@ -79,6 +91,30 @@ _STATUS = {
     6: ValueError,
     7: DeviceError,
 }
+
+
+_tables_installed = False
+
+
+def install_gaussian_tables() -> None:
+    """Hand numpy's ziggurat tables (read from the installed library) to the
+    native generator once per process."""
+    global _tables_installed
+    if _tables_installed:
+        return
+    from ._ziggurat import tables
+
+    ki, wi, fi = tables()
+    call("skl_gaussian_set_tables", ptr(ki), ptr(wi), ptr(fi))
+    _tables_installed = True
+
+
+def rng_gaussian_host(key: int, count: int) -> np.ndarray:
+    """First `count` standard normals of Generator(Philox(key)) (host, libm)."""
+    install_gaussian_tables()
+    out = np.empty(count, dtype=np.float64)
+    call("skl_rng_gaussian_host", key, count, ptr(out))
+    return out
 
 
 def lib() -> ctypes.CDLL:
@@ -150,15 +186,23 @@ def rng_srht(key: int, m_pad: int, d: int, threads: int = 0) -> tuple[np.ndarray
     return signs, sample
 
 
-def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int,
-                     threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+def plan_geometry(d: int) -> tuple[int, int]:
+    """(chunk rows, consumer warps) of the CountSketch plan for embed_dim d."""
+    return 2048, (16 if d >= 1024 else 8)
+
+
+def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
+                     threads: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """(entries u16 [nch*chunk], tasks u32 [nch*stride], ntask i32 [nch])."""
     m = rows.shape[0]
     nch = (m + chunk - 1) // chunk
-    stride = int(lib().skl_countsketch_plan_stride(d))
+    stride = int(lib().skl_countsketch_plan_stride(d, warps))
     ent = np.zeros(nch * chunk, dtype=np.uint16)
-    off = np.zeros(nch * stride, dtype=np.uint16)
-    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, ptr(ent), ptr(off), threads)
-    return ent, off
+    tasks = np.zeros(nch * stride, dtype=np.uint32)
+    ntask = np.zeros(nch, dtype=np.int32)
+    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(ent), ptr(tasks),
+         ptr(ntask), threads)
+    return ent, tasks, ntask
 
 
 def countsketch_buckets(rows: np.ndarray, d: int) -> tuple[np.ndarray, np.ndarray]:

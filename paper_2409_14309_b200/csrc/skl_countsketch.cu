@@ -7,17 +7,20 @@
 // sign is exact, so reproducing that fold order reproduces SA bit for bit.
 //
 // Design (B200): one CTA owns C columns of [A | b] and streams them once,
-// top to bottom, in chunks of T rows.  A dedicated producer warp issues 1-D
-// bulk copies (cp.async.bulk -> UBLKCP) of each chunk's column segments plus
-// the chunk's slice of the plan (bucket-sorted row offsets and bucket
-// offsets, L2-resident, shared by all CTAs) into an S-stage shared-memory
-// ring guarded by full/empty mbarriers.  Each consumer thread owns KPT
-// buckets (i = k*NT + t) whose running sums live in registers across chunks
-// and walks each bucket's entries in ascending row order, reading A from
-// shared memory.  No atomics; A is read from HBM exactly once with
-// evict-first L2 hints.  With P > 1 row partitions (small n), partial sums
-// go to a workspace and are reduced in fixed partition order
-// (deterministic, not bitwise).
+// top to bottom, in chunks of T rows.  A producer warp issues 1-D bulk
+// copies (cp.async.bulk -> UBLKCP) of each chunk's column segments and the
+// chunk's slice of the plan (L2-resident, shared by all CTAs) into an
+// S-stage shared-memory ring guarded by full/empty mbarriers.  The running
+// bucket sums live in shared memory (C x d doubles).  Bucket b always
+// belongs to warp b / ceil(d/W) (contiguous ranges: random smem banks); per chunk the plan lists each warp's non-empty
+// buckets as tasks sorted by entry count, so the 32 lanes of a warp walk
+// buckets of (nearly) equal length: each lane loads its bucket's sum, adds
+// the bucket's rows in ascending order and stores it back.  Because a
+// bucket never changes warp, __syncwarp orders its updates across chunks
+// and no CTA-wide barrier is needed per chunk.  No atomics; A is
+// read from HBM exactly once with evict-first L2 hints.  With P > 1 row
+// partitions (few columns, long input), partial sums go to a workspace and
+// are reduced in fixed partition order (deterministic, not bitwise).
 #include <algorithm>
 #include <vector>
 
@@ -28,8 +31,7 @@
 
 namespace skl {
 
-constexpr int CS_NT = 256;     // consumer threads
-constexpr int CS_STAGES = 4;   // smem ring depth
+constexpr int CS_STAGES = 3;   // smem ring depth
 
 struct CsParams {
   const double* A;
@@ -39,10 +41,12 @@ struct CsParams {
   int64_t ncols;    // n + (b != nullptr)
   int64_t row_begin, row_end;  // rows handled by this launch (row_begin % T == 0)
   const uint16_t* ent;
-  const uint16_t* off;
+  const uint32_t* tasks;
+  const int32_t* ntask;
   int d;
   int T;
   int stride;
+  int head;         // per-chunk warp-offset header (u32 words)
   int P;
   double* out;      // SA (P == 1)
   int64_t ldo;
@@ -55,17 +59,24 @@ __device__ __forceinline__ const double* cs_col(const CsParams& p, int64_t c) {
   return c < p.n ? p.A + c * p.lda : p.b;
 }
 
-template <int KPT, int C>
-__global__ void __launch_bounds__(CS_NT + 32)
+template <int NT>
+__device__ __forceinline__ void cs_consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+template <int NT, int C>
+__global__ void __launch_bounds__(NT + 32)
     countsketch_dense_kernel(const CsParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + CS_STAGES;
-  unsigned char* ring = smem + 128;
-  const int T = p.T;
+  int* nt_s = reinterpret_cast<int*>(empty + CS_STAGES);
+  const int T = p.T, d = p.d;
+  double* acc_s = reinterpret_cast<double*>(smem + 128);
+  unsigned char* ring = smem + 128 + (((size_t)C * d * sizeof(double) + 127) & ~(size_t)127);
   const size_t a_bytes = (size_t)C * T * sizeof(double);
   const size_t e_bytes = (size_t)T * sizeof(uint16_t);
-  const size_t stage_bytes = a_bytes + e_bytes + (size_t)p.stride * sizeof(uint16_t);
+  const size_t stage_bytes = a_bytes + e_bytes + (size_t)p.stride * sizeof(uint32_t);
 
   const int tid = threadIdx.x;
   const int64_t col0 = (int64_t)blockIdx.x * C;
@@ -78,15 +89,15 @@ __global__ void __launch_bounds__(CS_NT + 32)
   if (tid == 0) {
     for (int s = 0; s < CS_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS_NT / 32);
+      mbar_init(&empty[s], NT / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (tid >= CS_NT) {
+  if (tid >= NT) {
     // ------------------------------ producer warp
-    if (tid == CS_NT) {
+    if (tid == NT) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
       for (int64_t it = 0; it < niter; ++it) {
@@ -96,18 +107,20 @@ __global__ void __launch_bounds__(CS_NT + 32)
         const int64_t r0 = ch * T;
         const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
         const int len_even = len & ~1;
+        const int nt = __ldg(p.ntask + ch);
         unsigned char* st = ring + s * stage_bytes;
         double* As = reinterpret_cast<double*>(st);
         uint16_t* Es = reinterpret_cast<uint16_t*>(st + a_bytes);
-        uint16_t* Os = reinterpret_cast<uint16_t*>(st + a_bytes + e_bytes);
+        uint32_t* Ts = reinterpret_cast<uint32_t*>(st + a_bytes + e_bytes);
         const uint32_t ebytes = (uint32_t)(((len + 7) & ~7) * sizeof(uint16_t));
-        const uint32_t obytes = (uint32_t)(p.stride * sizeof(uint16_t));
+        const uint32_t tbytes = (uint32_t)((p.head + ((nt + 3) & ~3)) * sizeof(uint32_t));
         if (len & 1) {
           for (int c = 0; c < ncol_here; ++c)
             As[c * T + len - 1] = __ldg(cs_col(p, col0 + c) + r0 + len - 1);
         }
+        nt_s[s] = nt;
         const uint32_t total =
-            (uint32_t)(ncol_here * len_even * sizeof(double)) + ebytes + obytes;
+            (uint32_t)(ncol_here * len_even * sizeof(double)) + ebytes + tbytes;
         mbar_arrive_expect_tx(&full[s], total);
         if (len_even) {
           for (int c = 0; c < ncol_here; ++c)
@@ -115,69 +128,76 @@ __global__ void __launch_bounds__(CS_NT + 32)
                      &full[s], pol_stream);
         }
         bulk_g2s(Es, p.ent + r0, ebytes, &full[s], pol_keep);
-        bulk_g2s(Os, p.off + ch * p.stride, obytes, &full[s], pol_keep);
+        bulk_g2s(Ts, p.tasks + ch * p.stride, tbytes, &full[s], pol_keep);
       }
     }
     return;
   }
 
   // -------------------------------- consumers
-  double acc[C][KPT];
+  for (int i = tid; i < d; i += NT) {
 #pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      acc[c][k] = 0.0;
-      const int i = k * CS_NT + tid;
-      if (p.P == 1 && p.accumulate && i < p.d && c < ncol_here) {
-        const int64_t col = col0 + c;
-        acc[c][k] = col < p.n ? p.out[col * p.ldo + i] : p.outb[i];
-      }
+    for (int c = 0; c < C; ++c) {
+      double v = 0.0;
+      const int64_t col = col0 + c;
+      if (p.P == 1 && p.accumulate && c < ncol_here) v = col < p.n ? p.out[col * p.ldo + i] : p.outb[i];
+      acc_s[c * d + i] = v;
     }
+  }
+  cs_consumer_bar<NT>();
 
   for (int64_t it = 0; it < niter; ++it) {
     const int s = (int)(it % CS_STAGES);
     mbar_wait(&full[s], (uint32_t)((it / CS_STAGES) & 1));
+    const int64_t r0 = (ch_first + it0 + it) * T;
+    const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
     const unsigned char* st = ring + s * stage_bytes;
     const double* As = reinterpret_cast<const double*>(st);
     const uint16_t* Es = reinterpret_cast<const uint16_t*>(st + a_bytes);
-    const uint16_t* Os = reinterpret_cast<const uint16_t*>(st + a_bytes + e_bytes);
+    const uint32_t* Ts = reinterpret_cast<const uint32_t*>(st + a_bytes + e_bytes);
+    const uint32_t* Ks = Ts + p.head;
+    const int nt = nt_s[s];
+    const int wid = tid >> 5, lane = tid & 31;
+    const int lo = (int)Ts[wid], hi = (int)Ts[wid + 1];
+    for (int i = lo + lane; i < hi; i += 32) {
+      const uint32_t tv = Ks[i];
+      const int bkt = (int)(tv >> 16);
+      const int e0 = (int)(tv & 0xffff);
+      const int e1 = i + 1 < nt ? (int)(Ks[i + 1] & 0xffff) : len;
+      double a[C];
 #pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int i = k * CS_NT + tid;
-      if (i < p.d) {
-        const int beg = Os[i], end = Os[i + 1];
-        for (int e = beg; e < end; ++e) {
-          const uint32_t v = Es[e];
-          const int row = v & 0x7fff;
-          const bool neg = v >> 15;
+      for (int c = 0; c < C; ++c) a[c] = acc_s[c * d + bkt];
+      for (int e = e0; e < e1; ++e) {
+        const uint32_t v = Es[e];
+        const int row = v & 0x7fff;
+        const bool neg = v >> 15;
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const double x = As[c * T + row];
-            acc[c][k] += neg ? -x : x;
-          }
+        for (int c = 0; c < C; ++c) {
+          const double x = As[c * T + row];
+          a[c] += neg ? -x : x;
         }
       }
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc_s[c * d + bkt] = a[c];
     }
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
+  cs_consumer_bar<NT>();
 
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     if (c >= ncol_here) break;
     const int64_t col = col0 + c;
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int i = k * CS_NT + tid;
-      if (i >= p.d) continue;
+    for (int i = tid; i < d; i += NT) {
+      const double v = acc_s[c * d + i];
       if (p.P == 1) {
         if (col < p.n)
-          p.out[col * p.ldo + i] = acc[c][k];
+          p.out[col * p.ldo + i] = v;
         else
-          p.outb[i] = acc[c][k];
+          p.outb[i] = v;
       } else {
-        p.part[((int64_t)blockIdx.y * p.ncols + col) * p.d + i] = acc[c][k];
+        p.part[((int64_t)blockIdx.y * p.ncols + col) * d + i] = v;
       }
     }
   }
@@ -211,77 +231,76 @@ static int sm_count() {
   return cached;
 }
 
-template <int KPT, int C>
+template <int NT, int C>
 static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kern = countsketch_dense_kernel<KPT, C>;
+  auto kern = countsketch_dense_kernel<NT, C>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, CS_NT + 32, smem, st>>>(p);
+  kern<<<grid, NT + 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-static cudaError_t dispatch_cs(int kpt, int C, const CsParams& p, dim3 grid, size_t smem,
+static cudaError_t dispatch_cs(int nt, int C, const CsParams& p, dim3 grid, size_t smem,
                                cudaStream_t st) {
-#define SKL_CS_CASE(K, CC) \
-  if (kpt == K && C == CC) return launch_cs<K, CC>(p, grid, smem, st);
-  SKL_CS_CASE(1, 1) SKL_CS_CASE(1, 2) SKL_CS_CASE(1, 4)
-  SKL_CS_CASE(2, 1) SKL_CS_CASE(2, 2) SKL_CS_CASE(2, 4)
-  SKL_CS_CASE(4, 1) SKL_CS_CASE(4, 2) SKL_CS_CASE(4, 4)
-  SKL_CS_CASE(8, 1) SKL_CS_CASE(8, 2)
-  SKL_CS_CASE(16, 1) SKL_CS_CASE(32, 1)
-#undef SKL_CS_CASE
+  if (nt == 256 && C == 1) return launch_cs<256, 1>(p, grid, smem, st);
+  if (nt == 512 && C == 1) return launch_cs<512, 1>(p, grid, smem, st);
+  if (nt == 256 && C == 2) return launch_cs<256, 2>(p, grid, smem, st);
+  if (nt == 512 && C == 2) return launch_cs<512, 2>(p, grid, smem, st);
   return cudaErrorInvalidValue;
-}
-
-static int kpt_for(int64_t d) {
-  int k = 1;
-  while ((int64_t)k * CS_NT < d) k <<= 1;
-  return k;
 }
 
 // Core launcher shared by the device and host-streaming entry points.
 static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
-                              const uint16_t* ent, const uint16_t* off, int64_t d, int64_t chunk,
-                              double* SA, int64_t ldsa, double* Sb, int partitions, int accumulate,
-                              int64_t row_begin, int64_t row_end, cudaStream_t st) {
+                              const uint16_t* ent, const uint32_t* tasks, const int32_t* ntask,
+                              int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
+                              double* Sb, int partitions, int accumulate, int64_t row_begin,
+                              int64_t row_end, cudaStream_t st) {
   SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld lda=%lld ldsa=%lld", (long long)m,
               (long long)n, (long long)d, (long long)lda, (long long)ldsa);
-  SKL_REQUIRE(d <= 32 * CS_NT, SKL_ERR_SPEC, "countsketch: embed_dim %lld > %d not supported",
-              (long long)d, 32 * CS_NT);
+  SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch: embed_dim %lld > 65536 not supported",
+              (long long)d);
   SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
               "countsketch: bad plan chunk %lld", (long long)chunk);
-  SKL_REQUIRE(A && ent && off && SA && (!b || Sb), SKL_ERR_INVALID, "countsketch: null pointer");
+  SKL_REQUIRE(A && ent && tasks && ntask && SA && (!b || Sb), SKL_ERR_INVALID,
+              "countsketch: null pointer");
   SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && (!b || ((uintptr_t)b & 15) == 0),
               SKL_ERR_INVALID,
               "countsketch: A/b must be 16-byte aligned with an even leading dimension");
-  SKL_REQUIRE(((uintptr_t)ent & 15) == 0 && ((uintptr_t)off & 15) == 0, SKL_ERR_INVALID,
+  SKL_REQUIRE(((uintptr_t)ent & 15) == 0 && ((uintptr_t)tasks & 15) == 0, SKL_ERR_INVALID,
               "countsketch: plan arrays must be 16-byte aligned");
   SKL_REQUIRE(row_begin % chunk == 0 && row_end > row_begin && row_end <= m, SKL_ERR_INVALID,
               "countsketch: bad row range");
 
-  const int kpt = kpt_for(d);
+  SKL_REQUIRE(warps == 8 || warps == 16, SKL_ERR_INVALID,
+              "countsketch: plan built for %d warps; kernels exist for 8 and 16", warps);
+  const int nthr = 32 * warps;
   const int64_t ncols = n + (b ? 1 : 0);
   int C = 1;
   const int T = (int)chunk;
-  const int stride = (int)skl_countsketch_plan_stride(d);
-  const size_t stage = (size_t)C * T * 8 + (size_t)T * 2 + (size_t)stride * 2;
-  const size_t smem = 128 + CS_STAGES * stage;
-  SKL_REQUIRE(smem <= 227 * 1024, SKL_ERR_INVALID, "countsketch: chunk %d too large for smem", T);
+  const int stride = (int)skl_countsketch_plan_stride(d, warps);
+  const size_t stage = (size_t)C * T * 8 + (size_t)T * 2 + (size_t)stride * 4;
+  const size_t smem = 128 + (((size_t)C * d * 8 + 127) & ~(size_t)127) + CS_STAGES * stage;
+  SKL_REQUIRE(smem <= 227 * 1024, SKL_ERR_INVALID,
+              "countsketch: chunk %d / embed_dim %lld too large for shared memory", T, (long long)d);
 
   const int64_t groups = (ncols + C - 1) / C;
   const int64_t nch = (row_end - row_begin + T - 1) / T;
   int P = partitions;
   if (P <= 0) {
+    // Ordered single pass (bitwise-equal to the reference) unless the
+    // column count leaves most SMs idle on a long input.
     const int sms = sm_count();
-    P = groups >= sms ? 1 : (int)((2 * sms + groups - 1) / groups);
+    const bool ordered = groups * 2 >= sms || (row_end - row_begin) <= (1 << 18);
+    P = ordered ? 1 : (int)((2 * sms + groups - 1) / groups);
   }
   P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nch));
 
   CsParams p;
   p.A = A; p.lda = lda; p.b = b; p.n = n; p.ncols = ncols;
   p.row_begin = row_begin; p.row_end = row_end;
-  p.ent = ent; p.off = off; p.d = (int)d; p.T = T; p.stride = stride; p.P = P;
+  p.ent = ent; p.tasks = tasks; p.ntask = ntask; p.d = (int)d; p.T = T; p.stride = stride; p.P = P;
+  p.head = (warps + 1 + 3) / 4 * 4;
   p.out = SA; p.ldo = ldsa; p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
 
   double* part = nullptr;
@@ -290,7 +309,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
     p.part = part;
   }
   dim3 grid((unsigned)groups, (unsigned)P);
-  cudaError_t e = dispatch_cs(kpt, C, p, grid, smem, st);
+  cudaError_t e = dispatch_cs(nthr, C, p, grid, smem, st);
   if (e != cudaSuccess) {
     if (part) cudaFreeAsync(part, st);
     SKL_FAIL(SKL_ERR_CUDA, "countsketch kernel launch failed: %s", cudaGetErrorString(e));
@@ -312,11 +331,13 @@ using namespace skl;
 
 extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,
                                      const double* b, const uint16_t* entries,
-                                     const uint16_t* offsets, int64_t d, int64_t chunk, double* SA,
+                                     const uint32_t* tasks, const int32_t* ntask, int64_t d,
+                                     int64_t chunk, int warps, double* SA,
                                      int64_t ldsa, double* Sb, int partitions, int accumulate,
                                      void* stream) {
   clear_error();
-  return countsketch_launch(A, m, n, lda, b, entries, offsets, d, chunk, SA, ldsa, Sb, partitions,
+  return countsketch_launch(A, m, n, lda, b, entries, tasks, ntask, d, chunk, warps, SA, ldsa, Sb,
+                            partitions,
                             accumulate, 0, m, (cudaStream_t)stream);
 }
 
@@ -325,7 +346,8 @@ extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int6
 // accumulate across blocks, so the result stays bitwise-equal).
 extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
                                           const double* b_host, const uint16_t* entries,
-                                          const uint16_t* offsets, int64_t d, int64_t chunk,
+                                          const uint32_t* tasks, const int32_t* ntask,
+                                          int64_t d, int64_t chunk, int warps,
                                           double* SA_host, int64_t ldsa, double* Sb_host,
                                           double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                           void* stream) {
@@ -372,8 +394,8 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
       rc = SKL_ERR_CUDA;
       break;
     }
-    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, entries, offsets, d,
-                            chunk, SA_dev, d, Sb_dev, 1, k > 0 ? 1 : 0, r0, r1, st);
+    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, entries, tasks, ntask, d,
+                            chunk, warps, SA_dev, d, Sb_dev, 1, k > 0 ? 1 : 0, r0, r1, st);
   }
   if (rc == SKL_OK) {
     cudaError_t e = cudaMemcpy2DAsync(SA_host, ldsa * sizeof(double), SA_dev, d * sizeof(double),

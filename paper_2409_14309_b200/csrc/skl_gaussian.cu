@@ -1,0 +1,385 @@
+// Gaussian sketch entries on device, bit-exact to the reference's
+// `stream(key).standard_normal((d, m)) / sqrt(d)`
+// (/root/reference/pkg/src/sketchls/sketch.py:94-96; generator rng.py:43-45).
+//
+// numpy 2.3.5's standard_normal is a 256-strip ziggurat over full 64-bit
+// Philox words: the fast path consumes one word, the wedge test one more
+// word per attempt, the tail (strip 0) two words per attempt, so the i-th
+// normal sits at a data-dependent stream position.  Parallel generation:
+//   A. the stream is cut into segments of S words; every segment is parsed
+//      speculatively as if a normal started at its first word, recording
+//      the start positions it finds (bitmask) and where it exits;
+//   B. the true entry of segment k is the exit of segment k-1; parsing from
+//      there re-synchronises with the speculative parse at the first shared
+//      start (almost always within a word or two), which gives the true
+//      number of normals starting in the segment;
+//   C. an exclusive scan gives each segment its output offset and the
+//      segment is parsed again, writing G[i, j] (row-major, ld ldg).
+// Strip-0 tail values depend on log1p; the device computes them, records
+// their positions, and the host recomputes those (~2.5e-4 of all draws)
+// with the same libm numpy uses and patches them in.  Arithmetic follows
+// numpy's C expression order with explicit _rn intrinsics (no FMA
+// contraction).  The tables come from the installed numpy (_ziggurat.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+#include "skl_common.h"
+#include "skl_philox.h"
+
+namespace skl {
+
+constexpr double ZIG_R = 3.6541528853610087963519472518;
+constexpr double ZIG_INV_R = 0.27366123732975827203338247596;
+constexpr int ZIG_S = 4096;  // words per segment
+constexpr int ZIG_MASKW = ZIG_S / 32;
+
+__constant__ uint64_t c_ki[256];
+__constant__ double c_wi[256];
+__constant__ double c_fi[256];
+
+static std::mutex g_tab_mu;
+static bool g_tab_set = false;
+static uint64_t h_ki[256];
+static double h_wi[256], h_fi[256];
+
+struct WordStream {
+  uint64_t key, blk, w0, w1, w2, w3;
+  __host__ __device__ WordStream(uint64_t k) : key(k), blk(~0ULL), w0(0), w1(0), w2(0), w3(0) {}
+  __host__ __device__ __forceinline__ uint64_t at(uint64_t pos) {
+    const uint64_t b = pos >> 2;
+    if (b != blk) {
+      uint64_t w[4];
+      philox_block(key, b, w);
+      w0 = w[0]; w1 = w[1]; w2 = w[2]; w3 = w[3];
+      blk = b;
+    }
+    const int q = (int)(pos & 3);
+    return q == 0 ? w0 : q == 1 ? w1 : q == 2 ? w2 : w3;
+  }
+};
+
+__host__ __device__ __forceinline__ double next_double_of(uint64_t w) {
+  return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+#ifdef __CUDA_ARCH__
+#define ZMUL(a, b) __dmul_rn((a), (b))
+#define ZADD(a, b) __dadd_rn((a), (b))
+#define ZSUB(a, b) __dsub_rn((a), (b))
+#define ZKI c_ki
+#define ZWI c_wi
+#define ZFI c_fi
+#else
+#define ZMUL(a, b) ((a) * (b))
+#define ZADD(a, b) ((a) + (b))
+#define ZSUB(a, b) ((a) - (b))
+#define ZKI h_ki
+#define ZWI h_wi
+#define ZFI h_fi
+#endif
+
+// One standard normal starting at word `pos` (numpy random_standard_normal).
+// Returns the position after it; *tail is set when the strip-0 tail (log1p)
+// produced the value.
+__host__ __device__ __forceinline__ uint64_t zig_parse(WordStream& ws, uint64_t pos, double* val,
+                                                       bool* tail) {
+  *tail = false;
+  for (;;) {
+    uint64_t r = ws.at(pos++);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = ZMUL((double)rabs, ZWI[idx]);
+    if (sign) x = -x;
+    if (rabs < ZKI[idx]) {
+      *val = x;
+      return pos;
+    }
+    if (idx == 0) {
+      *tail = true;
+      for (;;) {
+        const double xx = ZMUL(-ZIG_INV_R, log1p(-next_double_of(ws.at(pos++))));
+        const double yy = -log1p(-next_double_of(ws.at(pos++)));
+        if (ZADD(yy, yy) > ZMUL(xx, xx)) {
+          *val = ((rabs >> 8) & 1) ? -(ZADD(ZIG_R, xx)) : ZADD(ZIG_R, xx);
+          return pos;
+        }
+      }
+    }
+    const double u = next_double_of(ws.at(pos++));
+    const double lhs = ZADD(ZMUL(ZSUB(ZFI[idx - 1], ZFI[idx]), u), ZFI[idx]);
+    if (lhs < exp(ZMUL(ZMUL(-0.5, x), x))) {
+      *val = x;
+      return pos;
+    }
+  }
+}
+
+// A: speculative parse of each segment.
+__global__ void zig_spec_kernel(uint64_t key, int64_t nseg, uint32_t* mask, uint64_t* exitpos) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nseg) return;
+  WordStream ws(key);
+  const uint64_t s0 = (uint64_t)k * ZIG_S;
+  uint64_t pos = s0;
+  uint32_t* mk = mask + k * ZIG_MASKW;
+  int cur = 0;
+  uint32_t bits = 0;
+  while (pos < s0 + ZIG_S) {
+    const int off = (int)(pos - s0);
+    const int w = off >> 5;
+    while (cur < w) {
+      mk[cur++] = bits;
+      bits = 0;
+    }
+    bits |= 1u << (off & 31);
+    double v;
+    bool t;
+    pos = zig_parse(ws, pos, &v, &t);
+  }
+  while (cur < ZIG_MASKW) {
+    mk[cur++] = bits;
+    bits = 0;
+  }
+  exitpos[k] = pos;
+}
+
+__device__ __forceinline__ int zig_count_from(const uint32_t* mk, int off) {
+  int c = __popc(mk[off >> 5] & (0xffffffffu << (off & 31)));
+  for (int w = (off >> 5) + 1; w < ZIG_MASKW; ++w) c += __popc(mk[w]);
+  return c;
+}
+
+// B: true per-segment counts from the true entries; flags a broken chain.
+__global__ void zig_count_kernel(uint64_t key, int64_t nseg, const uint32_t* mask,
+                                 const uint64_t* exitpos, int64_t* count, int* bad) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nseg) return;
+  const uint64_t s0 = (uint64_t)k * ZIG_S;
+  const uint64_t entry = k == 0 ? 0 : exitpos[k - 1];
+  const uint32_t* mk = mask + k * ZIG_MASKW;
+  int64_t cnt = 0;
+  uint64_t pos = entry;
+  bool synced = false;
+  WordStream ws(key);
+  while (pos < s0 + ZIG_S) {
+    const int off = (int)(pos - s0);
+    if ((mk[off >> 5] >> (off & 31)) & 1u) {
+      cnt += zig_count_from(mk, off);
+      synced = true;
+      break;
+    }
+    double v;
+    bool t;
+    pos = zig_parse(ws, pos, &v, &t);
+    ++cnt;
+  }
+  if (!synced && pos != exitpos[k]) atomicExch(bad, 1);
+  count[k] = cnt;
+}
+
+// Single-block exclusive scan of the counts (nseg is O(1e5)).
+__global__ void zig_scan_kernel(const int64_t* count, int64_t nseg, int64_t* offset,
+                                int64_t* total) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nseg + 1023) / 1024;
+  const int64_t lo = t * per, hi = min(nseg, lo + per);
+  int64_t s = 0;
+  for (int64_t k = lo; k < hi; ++k) s += count[k];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  int64_t run = part[t];
+  for (int64_t k = lo; k < hi; ++k) {
+    offset[k] = run;
+    run += count[k];
+  }
+}
+
+// C: write the normals of each segment; record strip-0 tail positions.
+__global__ void zig_write_kernel(uint64_t key, int64_t nseg, const uint64_t* exitpos,
+                                 const int64_t* count, const int64_t* offset, int64_t N,
+                                 int64_t m, double* G, int64_t ldg, double sqrt_d,
+                                 int64_t* tail_t, uint64_t* tail_pos, int* tail_n, int tail_cap) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nseg) return;
+  int64_t t = offset[k];
+  const int64_t cnt = count[k];
+  if (t >= N || cnt == 0) return;
+  uint64_t pos = k == 0 ? 0 : exitpos[k - 1];
+  WordStream ws(key);
+  int64_t i = t / m, j = t % m;
+  for (int64_t q = 0; q < cnt && t < N; ++q, ++t) {
+    double v;
+    bool tail;
+    const uint64_t start = pos;
+    pos = zig_parse(ws, pos, &v, &tail);
+    G[i * ldg + j] = v / sqrt_d;
+    if (tail) {
+      const int slot = atomicAdd(tail_n, 1);
+      if (slot < tail_cap) {
+        tail_t[slot] = t;
+        tail_pos[slot] = start;
+      }
+    }
+    if (++j == m) {
+      j = 0;
+      ++i;
+    }
+  }
+}
+
+__global__ void zig_patch_kernel(const int64_t* tail_t, const double* vals, int n, int64_t m,
+                                 double* G, int64_t ldg) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int64_t t = tail_t[q];
+  G[(t / m) * ldg + t % m] = vals[q];
+}
+
+static int upload_tables(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  SKL_REQUIRE(g_tab_set, SKL_ERR_INVALID,
+              "ziggurat tables not installed (call skl_gaussian_set_tables first)");
+  SKL_CUDA(cudaMemcpyToSymbolAsync(c_ki, h_ki, sizeof(h_ki), 0, cudaMemcpyHostToDevice, st));
+  SKL_CUDA(cudaMemcpyToSymbolAsync(c_wi, h_wi, sizeof(h_wi), 0, cudaMemcpyHostToDevice, st));
+  SKL_CUDA(cudaMemcpyToSymbolAsync(c_fi, h_fi, sizeof(h_fi), 0, cudaMemcpyHostToDevice, st));
+  return SKL_OK;
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" int skl_gaussian_set_tables(const uint64_t* ki, const double* wi, const double* fi) {
+  clear_error();
+  SKL_REQUIRE(ki && wi && fi, SKL_ERR_INVALID, "gaussian tables: null pointer");
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  std::copy(ki, ki + 256, h_ki);
+  std::copy(wi, wi + 256, h_wi);
+  std::copy(fi, fi + 256, h_fi);
+  g_tab_set = true;
+  return SKL_OK;
+}
+
+extern "C" int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out) {
+  clear_error();
+  SKL_REQUIRE(count >= 0 && (count == 0 || out), SKL_ERR_INVALID, "gaussian_host: bad arguments");
+  {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    SKL_REQUIRE(g_tab_set, SKL_ERR_INVALID, "ziggurat tables not installed");
+  }
+  WordStream ws(key);
+  uint64_t pos = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    bool tail;
+    pos = zig_parse(ws, pos, &out[i], &tail);
+  }
+  return SKL_OK;
+}
+
+extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G, int64_t ldg,
+                                       void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  SKL_REQUIRE(d >= 1 && m >= 1 && ldg >= m && G, SKL_ERR_SHAPE, "gaussian: bad arguments");
+  int rc = upload_tables(st);
+  if (rc) return rc;
+  const int64_t N = d * m;
+  // expected words per normal ~1.025; start with 3% slack
+  int64_t nseg = (int64_t)((double)N * 1.03 / ZIG_S) + 8;
+  const double sqrt_d = std::sqrt((double)d);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    uint32_t* mask = nullptr;
+    uint64_t* exitpos = nullptr;
+    int64_t *count = nullptr, *offset = nullptr, *total = nullptr;
+    int* flags = nullptr;  // [0] bad chain, [1] tail count
+    const int tail_cap = (int)std::min<int64_t>(N / 256 + 4096, 1 << 26);
+    int64_t* tail_t = nullptr;
+    uint64_t* tail_pos = nullptr;
+    SKL_CUDA(cudaMallocAsync(&mask, (size_t)nseg * ZIG_MASKW * 4, st));
+    SKL_CUDA(cudaMallocAsync(&exitpos, (size_t)nseg * 8, st));
+    SKL_CUDA(cudaMallocAsync(&count, (size_t)nseg * 8, st));
+    SKL_CUDA(cudaMallocAsync(&offset, (size_t)nseg * 8, st));
+    SKL_CUDA(cudaMallocAsync(&total, 8, st));
+    SKL_CUDA(cudaMallocAsync(&flags, 8, st));
+    SKL_CUDA(cudaMallocAsync(&tail_t, (size_t)tail_cap * 8, st));
+    SKL_CUDA(cudaMallocAsync(&tail_pos, (size_t)tail_cap * 8, st));
+    SKL_CUDA(cudaMemsetAsync(flags, 0, 8, st));
+    const int tb = 128;
+    const int blocks = (int)((nseg + tb - 1) / tb);
+    zig_spec_kernel<<<blocks, tb, 0, st>>>(key, nseg, mask, exitpos);
+    zig_count_kernel<<<blocks, tb, 0, st>>>(key, nseg, mask, exitpos, count, flags);
+    zig_scan_kernel<<<1, 1024, 0, st>>>(count, nseg, offset, total);
+    int64_t h_total = 0;
+    int h_flags[2] = {0, 0};
+    SKL_CUDA(cudaMemcpyAsync(&h_total, total, 8, cudaMemcpyDeviceToHost, st));
+    SKL_CUDA(cudaMemcpyAsync(h_flags, flags, 8, cudaMemcpyDeviceToHost, st));
+    SKL_CUDA(cudaStreamSynchronize(st));
+    auto release = [&]() {
+      cudaFreeAsync(mask, st); cudaFreeAsync(exitpos, st); cudaFreeAsync(count, st);
+      cudaFreeAsync(offset, st); cudaFreeAsync(total, st); cudaFreeAsync(flags, st);
+      cudaFreeAsync(tail_t, st); cudaFreeAsync(tail_pos, st);
+    };
+    if (h_flags[0]) {
+      release();
+      SKL_FAIL(SKL_ERR_CUDA, "gaussian: ziggurat segment chain failed to resynchronise");
+    }
+    if (h_total < N) {  // not enough words drawn: retry with more segments
+      release();
+      nseg = nseg + nseg / 8 + 16;
+      continue;
+    }
+    zig_write_kernel<<<blocks, tb, 0, st>>>(key, nseg, exitpos, count, offset, N, m, G, ldg,
+                                             sqrt_d, tail_t, tail_pos, flags + 1, tail_cap);
+    SKL_CUDA_LAUNCH();
+    SKL_CUDA(cudaMemcpyAsync(h_flags, flags, 8, cudaMemcpyDeviceToHost, st));
+    SKL_CUDA(cudaStreamSynchronize(st));
+    const int ntail = h_flags[1];
+    if (ntail > tail_cap) {
+      release();
+      SKL_FAIL(SKL_ERR_CUDA, "gaussian: tail record overflow (%d > %d)", ntail, tail_cap);
+    }
+    if (ntail > 0) {
+      // host recomputation of the strip-0 tail values with the host libm
+      std::vector<int64_t> ht((size_t)ntail);
+      std::vector<uint64_t> hp((size_t)ntail);
+      std::vector<double> hv((size_t)ntail);
+      SKL_CUDA(cudaMemcpyAsync(ht.data(), tail_t, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st));
+      SKL_CUDA(cudaMemcpyAsync(hp.data(), tail_pos, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st));
+      SKL_CUDA(cudaStreamSynchronize(st));
+      for (int q = 0; q < ntail; ++q) {
+        WordStream ws(key);
+        bool tl;
+        double v;
+        zig_parse(ws, hp[(size_t)q], &v, &tl);
+        hv[(size_t)q] = v / sqrt_d;
+      }
+      double* dv = nullptr;
+      SKL_CUDA(cudaMallocAsync(&dv, (size_t)ntail * 8, st));
+      SKL_CUDA(cudaMemcpyAsync(dv, hv.data(), (size_t)ntail * 8, cudaMemcpyHostToDevice, st));
+      zig_patch_kernel<<<(ntail + 255) / 256, 256, 0, st>>>(tail_t, dv, ntail, m, G, ldg);
+      SKL_CUDA_LAUNCH();
+      SKL_CUDA(cudaFreeAsync(dv, st));
+      SKL_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    }
+    release();
+    return SKL_OK;
+  }
+  SKL_FAIL(SKL_ERR_CUDA, "gaussian: stream segmentation did not converge");
+}

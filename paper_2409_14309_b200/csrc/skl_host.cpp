@@ -41,9 +41,9 @@ int resolve_threads(int threads) {
 }
 
 template <class F>
-static void parallel_for(int64_t n, int threads, F&& f) {
-  // f(lo, hi) over [0, n) split in contiguous blocks.
-  threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / 4096 + 1));
+static void parallel_for(int64_t n, int threads, F&& f, int64_t grain = 4096) {
+  // f(lo, hi) over [0, n) split in contiguous blocks of at least `grain`.
+  threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / grain + 1));
   if (threads == 1) {
     f((int64_t)0, n);
     return;
@@ -290,51 +290,97 @@ int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t*
 }
 
 // ---------------------------------------------------------------------------
-// CountSketch plan (see header).  Chunk k covers rows [k*chunk, ...); its
-// entries are the local row offsets sorted stably by bucket, bit 15 set for
-// a negative sign; offsets[k*stride + i] is the first entry of bucket i and
-// offsets[k*stride + d] the chunk length.
-int64_t skl_countsketch_plan_stride(int64_t d) { return ((d + 1) + 7) / 8 * 8; }
+// CountSketch plan (see the header).  Per chunk: a stable counting sort of
+// the rows by bucket, then per warp group the non-empty buckets ordered by
+// descending count (ties by bucket id) become the tasks.
+static int64_t plan_head(int warps) { return (warps + 1 + 3) / 4 * 4; }
+
+int64_t skl_countsketch_plan_stride(int64_t d, int warps) {
+  return plan_head(warps) + (d + 3) / 4 * 4;
+}
 
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
-                         int64_t chunk, uint16_t* entries, uint16_t* offsets, int threads) {
+                         int64_t chunk, int warps, uint16_t* entries, uint32_t* tasks,
+                         int32_t* ntask, int threads) {
   clear_error();
-  SKL_REQUIRE(rows && signs && entries && offsets && m >= 1 && d >= 1, SKL_ERR_INVALID,
+  SKL_REQUIRE(rows && signs && entries && tasks && ntask && m >= 1 && d >= 1, SKL_ERR_INVALID,
               "skl_countsketch_plan: bad arguments");
+  SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch plan: embed_dim %lld > 65536",
+              (long long)d);
   SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
               "plan chunk must be a multiple of 8 in [8, 32768], got %lld", (long long)chunk);
-  const int64_t stride = skl_countsketch_plan_stride(d);
+  SKL_REQUIRE(warps == 4 || warps == 8 || warps == 16, SKL_ERR_INVALID,
+              "plan warps must be 4, 8 or 16, got %d", warps);
+  const int64_t stride = skl_countsketch_plan_stride(d, warps);
+  const int64_t head = plan_head(warps);
   const int64_t nch = (m + chunk - 1) / chunk;
   threads = resolve_threads(threads);
   std::atomic<int> bad{0};
   parallel_for(nch, threads, [&](int64_t lo, int64_t hi) {
-    std::vector<uint32_t> cnt((size_t)d + 1);
+    std::vector<uint32_t> cnt((size_t)d), start((size_t)d), order((size_t)d), pos((size_t)d);
+    std::vector<uint16_t> sorted((size_t)chunk);
+    std::vector<uint32_t> byc(64);
     for (int64_t k = lo; k < hi; ++k) {
-      const int64_t r0 = k * chunk, len = std::min<int64_t>(chunk, m - r0);
+      const int64_t r0 = k * chunk;
+      const int len = (int)std::min<int64_t>(chunk, m - r0);
       std::fill(cnt.begin(), cnt.end(), 0u);
-      for (int64_t j = 0; j < len; ++j) {
-        int32_t r = rows[r0 + j];
+      for (int j = 0; j < len; ++j) {
+        const int32_t r = rows[r0 + j];
         if (r < 0 || r >= d) {
           bad = 1;
           return;
         }
-        ++cnt[(size_t)r + 1];
+        ++cnt[(size_t)r];
       }
-      uint16_t* off = offsets + k * stride;
       uint32_t run = 0;
       for (int64_t i = 0; i < d; ++i) {
-        run += cnt[(size_t)i + 1];
-        cnt[(size_t)i + 1] = run;
+        start[(size_t)i] = run;
+        pos[(size_t)i] = run;
+        run += cnt[(size_t)i];
       }
-      for (int64_t i = 0; i <= d; ++i) off[i] = (uint16_t)cnt[(size_t)i];
-      for (int64_t i = d + 1; i < stride; ++i) off[i] = (uint16_t)len;
+      for (int j = 0; j < len; ++j) {
+        const int32_t r = rows[r0 + j];
+        sorted[pos[(size_t)r]++] = (uint16_t)(j | (signs[r0 + j] < 0 ? 0x8000 : 0));
+      }
+      // tasks: group by warp (contiguous bucket ranges), then count desc,
+      // then bucket id (counting sort on the count inside each group)
+      uint32_t nt = 0;
+      uint32_t* tk = tasks + k * stride;
+      const int64_t gsize = (d + warps - 1) / warps;
+      for (int w = 0; w < warps; ++w) {
+        tk[w] = nt;
+        const int64_t b0 = std::min<int64_t>(d, w * gsize), b1 = std::min<int64_t>(d, b0 + gsize);
+        uint32_t maxc = 0;
+        for (int64_t b = b0; b < b1; ++b) maxc = std::max(maxc, cnt[(size_t)b]);
+        if (maxc == 0) continue;
+        if (byc.size() < (size_t)maxc + 2) byc.resize((size_t)maxc + 2);
+        std::fill(byc.begin(), byc.begin() + maxc + 2, 0u);
+        for (int64_t b = b0; b < b1; ++b) ++byc[cnt[(size_t)b]];
+        uint32_t acc = nt;  // slot of count c = nt + #buckets with count > c
+        for (int64_t c = (int64_t)maxc; c >= 1; --c) {
+          const uint32_t h = byc[(size_t)c];
+          byc[(size_t)c] = acc;
+          acc += h;
+        }
+        for (int64_t b = b0; b < b1; ++b) {
+          const uint32_t c = cnt[(size_t)b];
+          if (c) order[byc[c]++] = (uint32_t)b;
+        }
+        nt = acc;
+      }
+      for (int64_t w = warps; w < head; ++w) tk[w] = nt;
       uint16_t* ent = entries + r0;
-      for (int64_t j = 0; j < len; ++j) {
-        int32_t r = rows[r0 + j];
-        ent[cnt[(size_t)r]++] = (uint16_t)(j | (signs[r0 + j] < 0 ? 0x8000 : 0));
+      uint32_t e = 0;
+      for (uint32_t t = 0; t < nt; ++t) {
+        const uint32_t bkt = order[t];
+        tk[head + t] = (bkt << 16) | e;
+        const uint32_t s0 = start[bkt], c = cnt[bkt];
+        for (uint32_t q = 0; q < c; ++q) ent[e++] = sorted[s0 + q];
       }
+      for (int64_t t = head + nt; t < stride; ++t) tk[t] = 0;
+      ntask[k] = (int32_t)nt;
     }
-  });
+  }, 4);
   SKL_REQUIRE(!bad.load(), SKL_ERR_INVALID, "bucket index out of range [0, %lld)", (long long)d);
   return SKL_OK;
 }

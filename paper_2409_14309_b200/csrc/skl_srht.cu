@@ -1,0 +1,385 @@
+// SRHT apply and device FWHT.
+//
+// Reference (/root/reference/pkg/src/sketchls/sketch.py:213-223, fwht
+// :152-177): pad A to m_pad = 2^L rows, multiply row j by sign_diag[j], run
+// an unnormalised Sylvester-order FWHT down the rows, keep rows row_sample
+// and divide by sqrt(d).  That is O(m_pad n log m_pad) flops over a padded
+// m_pad x n copy of A.
+//
+// B200 design (fused, one pass over A): with H[p, j] = (-1)^popc(p & j) and
+// j = (j_hi, j_lo) split at B = 2^b rows,
+//     out[k, c] = sum_{j_hi} (-1)^popc(p_hi(k) & j_hi) * Y_{j_hi}[p_lo(k), c],
+//     Y_{j_hi} = FWHT_B(sign .* A[j_hi*B : (j_hi+1)*B, c]).
+// A CTA owns one column of A and streams it top to bottom in blocks of
+// B = 4096 rows: a producer warp bulk-copies (cp.async.bulk) each block and
+// its signs into a 2-stage smem ring; the consumers apply the signs and the
+// 12 in-block butterfly stages as three register passes of 4 stages each
+// (16 elements per thread, XOR-swizzled smem work buffer: conflict-free),
+// then every thread gathers its KPT sampled rows p_lo(k) and accumulates them
+// with the sign (-1)^popc(p_hi(k) & j_hi) in registers.  A is read from HBM
+// once; nothing of size m_pad is ever written.  Row sharding across GPUs is a
+// block offset (j_hi of the first local block).
+//
+// The butterfly here is (a+b, a-b) and the high stages are a direct signed
+// sum, so results agree with the reference to rounding (~1e-15 relative),
+// not bitwise.  skl_fwht_device (the fwht_inplace API) instead reproduces
+// the reference's butterfly (a+b, (a+b)-2b) in its ascending stage order and
+// is bitwise-equal.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "skl_common.h"
+#include "skl_ptx.cuh"
+
+namespace skl {
+
+constexpr int SR_NT = 256;
+constexpr int SR_STAGES = 2;
+constexpr int SR_BMAX = 4096;
+
+__device__ __forceinline__ int sr_swz(int e) { return e ^ ((e >> 4) & 15); }
+
+struct SrParams {
+  const double* A;
+  int64_t lda;
+  int64_t m;          // local rows
+  int64_t n;
+  const int8_t* signs;  // local rows' signs (padded to a multiple of 16)
+  const int64_t* sample;
+  int64_t d;
+  int b;              // log2 B
+  int64_t jhi0;       // j_hi of the first local block
+  int P;
+  double* out;
+  int64_t ldo;
+  double* part;       // [P][n][d]
+  double inv_scale_div;  // sqrt(d) (division at the end)
+};
+
+// One pass of NB butterfly stages at bits [lo, lo+NB).  FIRST reads the
+// natural-layout stage buffer (applying signs and the tail mask) and writes
+// the swizzled work buffer; later passes work in place on `work`.
+template <int NB, bool FIRST>
+__device__ __forceinline__ void sr_pass(const double* __restrict__ in,
+                                        const int8_t* __restrict__ sg, int len,
+                                        double* __restrict__ work, int lo, int B) {
+  constexpr int CNT = 1 << NB;
+  const int ntask = B >> NB;
+  for (int task = threadIdx.x; task < ntask; task += SR_NT) {
+    const int base = ((task >> lo) << (lo + NB)) | (task & ((1 << lo) - 1));
+    double v[CNT];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      const int e = base + (i << lo);
+      if (FIRST) {
+        v[i] = e < len ? (sg[e] < 0 ? -in[e] : in[e]) : 0.0;
+      } else {
+        v[i] = work[sr_swz(e)];
+      }
+    }
+#pragma unroll
+    for (int h = 1; h < CNT; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        if (!(i & h)) {
+          const double a = v[i], c = v[i + h];
+          v[i] = a + c;
+          v[i + h] = a - c;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) work[sr_swz(base + (i << lo))] = v[i];
+  }
+}
+
+template <bool FIRST>
+__device__ __forceinline__ void sr_pass_any(int nb, const double* in, const int8_t* sg, int len,
+                                            double* work, int lo, int B) {
+  switch (nb) {
+    case 0: sr_pass<0, FIRST>(in, sg, len, work, lo, B); break;
+    case 1: sr_pass<1, FIRST>(in, sg, len, work, lo, B); break;
+    case 2: sr_pass<2, FIRST>(in, sg, len, work, lo, B); break;
+    case 3: sr_pass<3, FIRST>(in, sg, len, work, lo, B); break;
+    default: sr_pass<4, FIRST>(in, sg, len, work, lo, B); break;
+  }
+}
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(SR_NT) : "memory");
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(SR_NT + 32) srht_dense_kernel(const SrParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + SR_STAGES;
+  const int B = 1 << p.b;
+  const size_t soff = ((size_t)B * 8 + 15) & ~(size_t)15;  // signs offset (16-byte aligned)
+  const size_t stage_bytes = (soff + (size_t)std::max(B, 16) + 127) & ~(size_t)127;
+  unsigned char* ring = smem + 128;
+  double* work = reinterpret_cast<double*>(ring + SR_STAGES * stage_bytes);
+
+  const int tid = threadIdx.x;
+  const int64_t col = blockIdx.x;
+  const int64_t nblk = (p.m + B - 1) / B;
+  const int64_t q0 = nblk * blockIdx.y / p.P, q1 = nblk * (blockIdx.y + 1) / p.P;
+  const int64_t niter = q1 - q0;
+
+  if (tid == 0) {
+    for (int s = 0; s < SR_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SR_NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= SR_NT) {
+    if (tid == SR_NT) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      const double* colp = p.A + col * p.lda;
+      for (int64_t it = 0; it < niter; ++it) {
+        const int s = (int)(it % SR_STAGES);
+        if (it >= SR_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / SR_STAGES) + 1) & 1));
+        const int64_t r0 = (q0 + it) * (int64_t)B;
+        const int len = (int)min((int64_t)B, p.m - r0);
+        const int len_even = len & ~1;
+        unsigned char* st = ring + s * stage_bytes;
+        double* As = reinterpret_cast<double*>(st);
+        int8_t* Ss = reinterpret_cast<int8_t*>(st + soff);
+        const uint32_t sbytes = (uint32_t)((len + 15) & ~15);
+        if (len & 1) As[len - 1] = __ldg(colp + r0 + len - 1);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(len_even * 8) + sbytes);
+        if (len_even) bulk_g2s(As, colp + r0, (uint32_t)(len_even * 8), &full[s], pol_stream);
+        bulk_g2s(Ss, p.signs + r0, sbytes, &full[s], pol_keep);
+      }
+    }
+    return;
+  }
+
+  // sampled rows owned by this thread
+  double acc[KPT];
+  int plo[KPT];
+  int64_t phi[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    acc[k] = 0.0;
+    const int64_t i = (int64_t)k * SR_NT + tid;
+    const int64_t ps = i < p.d ? p.sample[i] : 0;
+    plo[k] = (int)(ps & (B - 1));
+    phi[k] = ps >> p.b;
+  }
+  // pass plan: first pass = highest bit group (natural-layout friendly)
+  const int nb_hi = p.b > 8 ? p.b - 8 : 0;
+  const int nb_mid = p.b > 4 ? std::min(p.b, 8) - 4 : 0;
+  const int nb_lo = std::min(p.b, 4);
+
+  for (int64_t it = 0; it < niter; ++it) {
+    const int s = (int)(it % SR_STAGES);
+    mbar_wait(&full[s], (uint32_t)((it / SR_STAGES) & 1));
+    const int64_t q = q0 + it;
+    const int64_t r0 = q * (int64_t)B;
+    const int len = (int)min((int64_t)B, p.m - r0);
+    const unsigned char* st = ring + s * stage_bytes;
+    const double* As = reinterpret_cast<const double*>(st);
+    const int8_t* Ss = reinterpret_cast<const int8_t*>(st + soff);
+    if (nb_hi) {
+      sr_pass_any<true>(nb_hi, As, Ss, len, work, 8, B);
+    } else if (nb_mid) {
+      sr_pass_any<true>(nb_mid, As, Ss, len, work, 4, B);
+    } else {
+      sr_pass_any<true>(nb_lo, As, Ss, len, work, 0, B);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    consumer_bar();
+    if (nb_hi && nb_mid) {
+      sr_pass_any<false>(nb_mid, nullptr, nullptr, 0, work, 4, B);
+      consumer_bar();
+    }
+    if (nb_hi || nb_mid) {
+      sr_pass_any<false>(nb_lo, nullptr, nullptr, 0, work, 0, B);
+      consumer_bar();
+    }
+    const int64_t jhi = p.jhi0 + q;
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int64_t i = (int64_t)k * SR_NT + tid;
+      if (i < p.d) {
+        const double y = work[sr_swz(plo[k])];
+        acc[k] += (__popcll(phi[k] & jhi) & 1) ? -y : y;
+      }
+    }
+    consumer_bar();
+  }
+
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int64_t i = (int64_t)k * SR_NT + tid;
+    if (i >= p.d) continue;
+    if (p.P == 1)
+      p.out[col * p.ldo + i] = acc[k] / p.inv_scale_div;
+    else
+      p.part[((int64_t)blockIdx.y * p.n + col) * p.d + i] = acc[k];
+  }
+}
+
+__global__ void srht_reduce_kernel(const double* part, int P, int64_t n, int64_t d, double* out,
+                                   int64_t ldo, double div) {
+  const int64_t total = n * d;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / d, i = idx % d;
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += part[((int64_t)q * n + col) * d + i];
+    out[col * ldo + i] = s / div;
+  }
+}
+
+template <int KPT>
+static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  auto kern = srht_dense_kernel<KPT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, SR_NT + 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const int8_t* signs,
+                const int64_t* sample, int64_t m_pad, int64_t d, double* SA, int64_t ldsa,
+                int64_t row_offset, int partitions, cudaStream_t st) {
+  SKL_REQUIRE(A && signs && sample && SA && m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d,
+              SKL_ERR_SHAPE, "srht: bad arguments");
+  SKL_REQUIRE(m_pad >= 1 && (m_pad & (m_pad - 1)) == 0, SKL_ERR_SHAPE,
+              "srht: padded dimension %lld is not a power of two", (long long)m_pad);
+  SKL_REQUIRE(d <= 32 * SR_NT, SKL_ERR_SPEC, "srht: embed_dim %lld > %d not supported",
+              (long long)d, 32 * SR_NT);
+  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && ((uintptr_t)signs & 15) == 0,
+              SKL_ERR_INVALID, "srht: A/signs must be 16-byte aligned with an even leading dimension");
+  int b = 0;
+  while ((1LL << (b + 1)) <= std::min<int64_t>(m_pad, SR_BMAX)) ++b;
+  const int64_t B = 1LL << b;
+  SKL_REQUIRE(row_offset % B == 0, SKL_ERR_INVALID, "srht: row offset not block aligned");
+  int kpt = 1;
+  while ((int64_t)kpt * SR_NT < d) kpt <<= 1;
+  const size_t stage = ((((size_t)B * 8 + 15) & ~(size_t)15) + (size_t)std::max<int64_t>(B, 16) + 127) & ~(size_t)127;
+  const size_t smem = 128 + SR_STAGES * stage + (size_t)B * 8;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nblk = (m + B - 1) / B;
+  int P = partitions;
+  if (P <= 0) P = n * 2 >= sms ? 1 : (int)((2 * sms + n - 1) / n);
+  P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nblk));
+  SrParams p;
+  p.A = A; p.lda = lda; p.m = m; p.n = n; p.signs = signs; p.sample = sample; p.d = d; p.b = b;
+  p.jhi0 = row_offset >> b; p.P = P; p.out = SA; p.ldo = ldsa; p.part = nullptr;
+  p.inv_scale_div = std::sqrt((double)d);
+  double* part = nullptr;
+  if (P > 1) {
+    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * n * d * sizeof(double), st));
+    p.part = part;
+  }
+  dim3 grid((unsigned)n, (unsigned)P);
+  cudaError_t e;
+  switch (kpt) {
+    case 1: e = launch_srht<1>(p, grid, smem, st); break;
+    case 2: e = launch_srht<2>(p, grid, smem, st); break;
+    case 4: e = launch_srht<4>(p, grid, smem, st); break;
+    case 8: e = launch_srht<8>(p, grid, smem, st); break;
+    case 16: e = launch_srht<16>(p, grid, smem, st); break;
+    default: e = launch_srht<32>(p, grid, smem, st); break;
+  }
+  if (e != cudaSuccess) {
+    if (part) cudaFreeAsync(part, st);
+    SKL_FAIL(SKL_ERR_CUDA, "srht kernel launch failed: %s", cudaGetErrorString(e));
+  }
+  if (P > 1) {
+    const int64_t total = n * d;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4LL * sms);
+    srht_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, n, d, SA, ldsa, std::sqrt((double)d));
+    SKL_CUDA_LAUNCH();
+    SKL_CUDA(cudaFreeAsync(part, st));
+  }
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------- fwht_inplace
+// Stages [lo, lo+nb) of the reference's FWHT, in ascending order, with its
+// butterfly x' = x + y, y' = x' - 2y (sketch.py:172-175).
+template <int NB>
+__global__ void fwht_ref_pass_kernel(double* X, int64_t m_pad, int64_t n, int64_t lda, int lo) {
+  constexpr int CNT = 1 << NB;
+  const int64_t ntask = (m_pad >> NB) * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntask;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = t / (m_pad >> NB), task = t % (m_pad >> NB);
+    const int64_t base = ((task >> lo) << (lo + NB)) | (task & ((1LL << lo) - 1));
+    double* x = X + col * lda;
+    double v[CNT];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) v[i] = x[base + ((int64_t)i << lo)];
+#pragma unroll
+    for (int h = 1; h < CNT; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        if (!(i & h)) {
+          const double s = v[i] + v[i + h];
+          v[i + h] = s + (-2.0 * v[i + h]);
+          v[i] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) x[base + ((int64_t)i << lo)] = v[i];
+  }
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda,
+                              const int8_t* signs, const int64_t* row_sample, int64_t m_pad,
+                              int64_t d, double* SA, int64_t ldsa, void* stream) {
+  clear_error();
+  return srht_launch(A, m, n, lda, signs, row_sample, m_pad, d, SA, ldsa, 0, 0,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int skl_srht_dense_shard(const double* A, int64_t m_local, int64_t n, int64_t lda,
+                                    const int8_t* signs_local, const int64_t* row_sample,
+                                    int64_t m_pad, int64_t d, int64_t row_offset, double* partial,
+                                    int64_t ldp, void* stream) {
+  clear_error();
+  // partial sums of one row block; the caller sums partials across ranks.
+  // Scaling by 1/sqrt(d) is applied here as well (it is linear).
+  return srht_launch(A, m_local, n, lda, signs_local, row_sample, m_pad, d, partial, ldp,
+                     row_offset, 1, (cudaStream_t)stream);
+}
+
+extern "C" int skl_fwht_device(double* X, int64_t m_pad, int64_t n, int64_t lda, void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  SKL_REQUIRE(X && n >= 1 && lda >= m_pad && m_pad >= 1 && (m_pad & (m_pad - 1)) == 0,
+              SKL_ERR_SHAPE, "fwht requires a power-of-two length, got %lld", (long long)m_pad);
+  int L = 0;
+  while ((1LL << L) < m_pad) ++L;
+  for (int lo = 0; lo < L; lo += 4) {
+    const int nb = std::min(4, L - lo);
+    const int64_t ntask = (m_pad >> nb) * n;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ntask + 255) / 256, 4096));
+    switch (nb) {
+      case 1: fwht_ref_pass_kernel<1><<<blocks, 256, 0, st>>>(X, m_pad, n, lda, lo); break;
+      case 2: fwht_ref_pass_kernel<2><<<blocks, 256, 0, st>>>(X, m_pad, n, lda, lo); break;
+      case 3: fwht_ref_pass_kernel<3><<<blocks, 256, 0, st>>>(X, m_pad, n, lda, lo); break;
+      default: fwht_ref_pass_kernel<4><<<blocks, 256, 0, st>>>(X, m_pad, n, lda, lo); break;
+    }
+    SKL_CUDA_LAUNCH();
+  }
+  return SKL_OK;
+}

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native
 from ._device import current_stream, device_f64, require_cuda, to_device, torch
-from .sketch import PLAN_CHUNK, SketchOperator, build_sketch
+from .sketch import PLAN_CHUNK, SketchOperator, build_sketch, plan_warps
 
 
 def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
@@ -53,8 +53,9 @@ class ShardPlan:
 
     def device_plan(self):
         if self._plan is None:
-            ent, off = _native.countsketch_plan(self.rows, self.signs, self.d, PLAN_CHUNK)
-            self._plan = (to_device(ent), to_device(off))
+            plan = _native.countsketch_plan(self.rows, self.signs, self.d, PLAN_CHUNK,
+                                            plan_warps(self.d))
+            self._plan = tuple(to_device(a) for a in plan)
         return self._plan
 
 
@@ -64,12 +65,13 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
     require_cuda()
     m_loc = plan.r1 - plan.r0
     n = A_local.shape[1]
-    ent, off = plan.device_plan()
+    ent, tasks, ntask = plan.device_plan()
     d = plan.d
     ld = (d + 1) // 2 * 2  # keeps the Sb column 16-byte aligned
     out = device_f64((d, n + 1), fortran=True, ld=ld)
     _native.call("skl_countsketch_dense", _native.ptr(A_local), m_loc, n, lda,
-                 _native.ptr(b_local), _native.ptr(ent), _native.ptr(off), d, PLAN_CHUNK,
+                 _native.ptr(b_local), _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask),
+                 d, PLAN_CHUNK, plan_warps(d),
                  _native.ptr(out), ld, _native.ptr(out[:, n]), 1, 0, current_stream())
     return out
 

@@ -40,8 +40,13 @@ ENGINE_KINDS = ("gaussian", "srht", "countsketch", "identity")
 
 _MATERIALIZE_GUARD = 10**7
 
-# Rows per plan chunk of the CountSketch apply (multiple of 8, <= 32768).
+# Rows per plan chunk of the CountSketch apply (multiple of 8, <= 32768);
+# the consumer warp count follows d (_native.plan_geometry).
 PLAN_CHUNK = 2048
+
+
+def plan_warps(d: int) -> int:
+    return _native.plan_geometry(d)[1]
 
 
 def default_embed_dim(m: int, n: int, d_factor: float = 4.0) -> int:
@@ -126,12 +131,13 @@ class SketchOperator:
         return self._dev.setdefault(dev, {})
 
     def device_plan(self):
-        """(entries, offsets) of the CountSketch plan on the current device."""
+        """(entries, tasks, ntask) of the CountSketch plan on the current device."""
         require_cuda()
         c = self._cache()
         if "plan" not in c:
-            ent, off = _native.countsketch_plan(self.rows, self.signs, self.target_dim, PLAN_CHUNK)
-            c["plan"] = (to_device(ent), to_device(off))
+            plan = _native.countsketch_plan(self.rows, self.signs, self.target_dim, PLAN_CHUNK,
+                                            plan_warps(self.target_dim))
+            c["plan"] = tuple(to_device(a) for a in plan)
         return c["plan"]
 
     def device_buckets(self):
@@ -148,7 +154,10 @@ class SketchOperator:
         require_cuda()
         c = self._cache()
         if "srht" not in c:
-            signs8 = np.where(self.sign_diag > 0, 1, -1).astype(np.int8)
+            # int8 signs, padded so 16-byte bulk copies never run past the end
+            pad = (self.padded_dim + 15) // 16 * 16
+            signs8 = np.ones(max(pad, 16), dtype=np.int8)
+            signs8[: self.padded_dim] = np.where(self.sign_diag > 0, 1, -1)
             c["srht"] = (to_device(signs8), to_device(self.row_sample))
         return c["srht"]
 
@@ -160,6 +169,7 @@ class SketchOperator:
             d, m = self.target_dim, self.source_dim
             ldg = (m + 31) // 32 * 32
             G = torch.empty((d, ldg), dtype=torch.float64, device="cuda")
+            _native.install_gaussian_tables()
             _native.call("skl_rng_gaussian_device", self.key, d, m, _native.ptr(G), ldg,
                          current_stream())
             c["gauss"] = (G, ldg)
@@ -206,7 +216,7 @@ def _aligned(t, ld: int, cols: int):
 
 def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     """SA (d x n column-major tensor) and Sb (d) or None, all on device."""
-    ent, off = op.device_plan()
+    ent, tasks, ntask = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A, lda = _aligned(A, lda, n)
     if b is not None and b.data_ptr() % 16:
@@ -214,22 +224,23 @@ def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     SA = device_f64((d, n), fortran=True)
     Sb = device_f64((d,)) if b is not None else None
     _native.call("skl_countsketch_dense", _native.ptr(A), m, n, lda, _native.ptr(b),
-                 _native.ptr(ent), _native.ptr(off), d, PLAN_CHUNK, _native.ptr(SA), d,
-                 _native.ptr(Sb), 0, 0, current_stream())
+                 _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask), d, PLAN_CHUNK,
+                 plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), 0, 0, current_stream())
     return SA, Sb
 
 
 def _countsketch_dense_host(op: SketchOperator, A: np.ndarray, n: int,
                             b: np.ndarray | None = None):
     """Host buffers in, host SA/Sb out; H2D streamed under the kernel."""
-    ent, off = op.device_plan()
+    ent, tasks, ntask = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A = np.asfortranarray(A)
     SA = np.empty((d, n), dtype=np.float64, order="F")
     Sb = np.empty(d, dtype=np.float64) if b is not None else None
     _native.call("skl_countsketch_dense_host", _native.ptr(A), m, n, A.shape[0] if A.ndim == 2
-                 else m, _native.ptr(b), _native.ptr(ent), _native.ptr(off), d, PLAN_CHUNK,
-                 _native.ptr(SA), d, _native.ptr(Sb), None, 0, None, current_stream())
+                 else m, _native.ptr(b), _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask),
+                 d, PLAN_CHUNK, plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), None, 0, None,
+                 current_stream())
     return SA, Sb
 
 
@@ -248,6 +259,8 @@ def _countsketch_csr_device(op: SketchOperator, A: SparseMatrix):
 def _srht_device(op: SketchOperator, A, lda: int, n: int):
     signs, sample = op.device_srht()
     A, lda = _aligned(A, lda, n)
+    if lda % 2 and n > 1:
+        A, lda = _aligned(A.clone(), lda, n)
     d = op.target_dim
     SA = device_f64((d, n), fortran=True)
     _native.call("skl_srht_dense", _native.ptr(A), op.source_dim, n, lda, _native.ptr(signs),

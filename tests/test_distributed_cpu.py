@@ -1,0 +1,127 @@
+"""Multi-rank row sharding on CPU (gloo, world_size 2).
+
+Exercises the host-side logic of paper_2409_14309_b200.distributed -- shard
+boundaries, per-rank slices of the global operator, the reduce of the
+d x (n+1) partials, broadcast of x and the residual all-reduce -- with the
+per-rank compute supplied by the CPU oracle (the CUDA kernels need a GPU;
+their parity is covered by tests/test_gpu_parity.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2409_14309_b200 import SketchSpec, build_sketch
+from paper_2409_14309_b200.distributed import ShardPlan, shard_rows, sharded_sketch_and_apply
+from paper_2409_14309_b200.sketch import PLAN_CHUNK
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(m, n, seed=5):
+    rng = np.random.default_rng(seed)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = A @ rng.standard_normal(n) + 1e-3 * rng.standard_normal(m)
+    return A, b
+
+
+def _oracle_partial(plan, A_local, b_local):
+    a = A_local.numpy()
+    bb = b_local.numpy()
+    rows, signs = plan.rows.astype(np.int64), plan.signs.astype(np.float64)
+    SA = O.countsketch_apply(rows, signs, plan.d, a)
+    Sb = O.countsketch_apply(rows, signs, plan.d, bb)
+    return torch.from_numpy(np.asfortranarray(np.column_stack([SA, Sb])))
+
+
+def _oracle_solve(partial):
+    p = partial.numpy()
+    q, r = O.economy_qr(p[:, :-1])
+    import scipy.linalg
+
+    x = scipy.linalg.solve_triangular(r, q.T @ p[:, -1], lower=False)
+    return torch.from_numpy(x)
+
+
+def _oracle_r2(A_local, b_local, x):
+    r = A_local.numpy() @ x.numpy() - b_local.numpy()
+    return torch.tensor([float(r @ r)], dtype=torch.float64)
+
+
+def _worker(rank, world, port, m, n, d, seed, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, b = _problem(m, n)
+        r0, r1 = shard_rows(m, world, rank)
+        spec = SketchSpec("countsketch", d, seed=seed)
+        x, rnorm, dd = sharded_sketch_and_apply(
+            torch.from_numpy(np.asfortranarray(A[r0:r1])), torch.from_numpy(b[r0:r1].copy()), m,
+            spec, dist, local_apply=_oracle_partial, solve_reduced=_oracle_solve,
+            residual_local=_oracle_r2)
+        out[rank] = (x.numpy().copy(), rnorm, dd)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_rows_cover_and_align():
+    for m in (1, 2047, 2048, 2049, 10_000, 1 << 20):
+        for world in (1, 2, 3, 8):
+            spans = [shard_rows(m, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0
+            assert all(s0 % PLAN_CHUNK == 0 for s0, _ in spans)
+
+
+def test_shard_plan_slices_global_hashes():
+    op = build_sketch(SketchSpec("countsketch", 64, seed=3), 10_000)
+    plan = ShardPlan(op, 4096, 8192)
+    assert np.array_equal(plan.rows, op.rows[4096:8192])
+    assert np.array_equal(plan.signs, op.signs[4096:8192])
+
+
+def test_partials_sum_to_global_sketch():
+    m, n, d = 9000, 5, 64
+    A, b = _problem(m, n)
+    op = build_sketch(SketchSpec("countsketch", d, seed=11), m)
+    total = 0
+    for rank in range(3):
+        r0, r1 = shard_rows(m, 3, rank)
+        total = total + _oracle_partial(ShardPlan(op, r0, r1), torch.from_numpy(A[r0:r1]),
+                                        torch.from_numpy(b[r0:r1].copy())).numpy()
+    full = O.countsketch_apply(op.rows.astype(np.int64), op.signs.astype(np.float64), d, A)
+    assert np.linalg.norm(total[:, :n] - full) <= 1e-15 * np.linalg.norm(full)
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_matches_single_process():
+    m, n, d, seed = 8192, 6, 96, 21
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(2, port, m, n, d, seed, out), nprocs=2, join=True)
+    A, b = _problem(m, n)
+    key = O.derive_seed(seed, "countsketch", m)
+    rows, signs = O.countsketch_draws(key, m, d)
+    SA = O.countsketch_apply(rows, signs, d, A)
+    Sb = O.countsketch_apply(rows, signs, d, b)
+    q, r = O.economy_qr(SA)
+    import scipy.linalg
+
+    x_ref = scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False)
+    r_ref = np.linalg.norm(A @ x_ref - b)
+    for rank in range(2):
+        x, rnorm, dd = out[rank]
+        assert dd == d
+        assert np.linalg.norm(x - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
+        assert abs(rnorm - r_ref) <= 1e-12 * r_ref
