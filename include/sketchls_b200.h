@@ -96,13 +96,14 @@ int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);
  *   [0, H)        H = round4(warps+1): first task index of each group
  *                 (relative to the task list), group `warps` = end;
  *   [H, H+ntask)  (bucket << 16) | first entry of the task;
- * and entries[k*chunk + e] = local row (bits 0..14) | negative sign (bit
- * 15), grouped by task, ascending row inside a task.  It is the chunked
+ * and entries[k*chunk + e] = 8 * local row | negative sign (bit 0) -- the
+ * row's byte offset in the staged column chunk with the sign folded in --
+ * grouped by task, ascending row inside a task.  It is the chunked
  * form of the reference's CSR sparse_map (sketch.py:100-102) and keeps
  * scipy csr_matvecs' ascending-row fold order per bucket, so the device
  * apply is bitwise-equal to it; a bucket always lands in the same warp and
  * the count ordering gives the lanes of a warp equal work.
- * Limits: d <= 65536, chunk a multiple of 8 in [8, 32768], warps in {4,8,16}.
+ * Limits: d <= 65536, chunk a multiple of 8 in [8, 8192], warps in {4,8,16}.
  * ------------------------------------------------------------------- */
 int64_t skl_countsketch_plan_stride(int64_t d, int warps);
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,

@@ -159,24 +159,30 @@ __global__ void __launch_bounds__(NT + 32)
     const int nt = nt_s[s];
     const int wid = tid >> 5, lane = tid & 31;
     const int lo = (int)Ts[wid], hi = (int)Ts[wid + 1];
+    // Per task (= one bucket of this chunk): load the running sum, fold the
+    // bucket's rows in ascending order, store it back.  An entry is the
+    // row's byte offset in the staged column with the sign in bit 0, which
+    // is moved into the sign bit of the loaded double (exact negation).
+    const unsigned char* Ab = reinterpret_cast<const unsigned char*>(As);
     for (int i = lo + lane; i < hi; i += 32) {
       const uint32_t tv = Ks[i];
       const int bkt = (int)(tv >> 16);
-      const int e0 = (int)(tv & 0xffff);
+      int e = (int)(tv & 0xffff);
       const int e1 = i + 1 < nt ? (int)(Ks[i + 1] & 0xffff) : len;
       double a[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) a[c] = acc_s[c * d + bkt];
-      for (int e = e0; e < e1; ++e) {
+#pragma unroll 1
+      do {
         const uint32_t v = Es[e];
-        const int row = v & 0x7fff;
-        const bool neg = v >> 15;
+        const uint32_t flip = v << 31;
+        const unsigned char* src = Ab + (v & 0xfff8u);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const double x = As[c * T + row];
-          a[c] += neg ? -x : x;
+          const uint2 w = *reinterpret_cast<const uint2*>(src + (size_t)c * T * 8);
+          a[c] += __hiloint2double((int)(w.y ^ flip), (int)w.x);
         }
-      }
+      } while (++e < e1);
 #pragma unroll
       for (int c = 0; c < C; ++c) acc_s[c * d + bkt] = a[c];
     }
@@ -260,7 +266,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
               (long long)n, (long long)d, (long long)lda, (long long)ldsa);
   SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch: embed_dim %lld > 65536 not supported",
               (long long)d);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
+  SKL_REQUIRE(chunk >= 8 && chunk <= 8192 && chunk % 8 == 0, SKL_ERR_INVALID,
               "countsketch: bad plan chunk %lld", (long long)chunk);
   SKL_REQUIRE(A && ent && tasks && ntask && SA && (!b || Sb), SKL_ERR_INVALID,
               "countsketch: null pointer");

@@ -307,8 +307,8 @@ int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, in
               "skl_countsketch_plan: bad arguments");
   SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch plan: embed_dim %lld > 65536",
               (long long)d);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 32768 && chunk % 8 == 0, SKL_ERR_INVALID,
-              "plan chunk must be a multiple of 8 in [8, 32768], got %lld", (long long)chunk);
+  SKL_REQUIRE(chunk >= 8 && chunk <= 8192 && chunk % 8 == 0, SKL_ERR_INVALID,
+              "plan chunk must be a multiple of 8 in [8, 8192], got %lld", (long long)chunk);
   SKL_REQUIRE(warps == 4 || warps == 8 || warps == 16, SKL_ERR_INVALID,
               "plan warps must be 4, 8 or 16, got %d", warps);
   const int64_t stride = skl_countsketch_plan_stride(d, warps);
@@ -340,7 +340,7 @@ int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, in
       }
       for (int j = 0; j < len; ++j) {
         const int32_t r = rows[r0 + j];
-        sorted[pos[(size_t)r]++] = (uint16_t)(j | (signs[r0 + j] < 0 ? 0x8000 : 0));
+        sorted[pos[(size_t)r]++] = (uint16_t)((j << 3) | (signs[r0 + j] < 0 ? 1 : 0));
       }
       // tasks: group by warp (contiguous bucket ranges), then count desc,
       // then bucket id (counting sort on the count inside each group)

@@ -107,7 +107,7 @@ def test_srht_draws_match_numpy(m_pad, d):
 
 
 @pytest.mark.parametrize("m,d,chunk,warps", [(1, 1, 8, 8), (100, 4, 8, 4), (20_000, 800, 2048, 8),
-                                             (65_537, 2048, 2048, 16), (10_000, 8192, 4096, 16),
+                                             (65_537, 2048, 2048, 16), (10_000, 8192, 8192, 16),
                                              (9_000, 3, 1024, 8)])
 def test_countsketch_plan_structure(m, d, chunk, warps):
     key = O.derive_seed(1, "countsketch", m)
@@ -137,7 +137,7 @@ def test_countsketch_plan_structure(m, d, chunk, warps):
             ties = np.diff(cnts[g]) == 0
             assert np.all(np.diff(bkt[g])[ties] > 0)         # ties by bucket id
         e = ent[r0: r0 + length].astype(np.int64)
-        local, neg = e & 0x7FFF, (e >> 15).astype(bool)
+        local, neg = e >> 3, (e & 1).astype(bool)
         assert np.array_equal(np.sort(local), np.arange(length))
         owner = np.repeat(bkt, cnts)
         assert np.array_equal(rows[r0 + local], owner)
