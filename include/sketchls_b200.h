@@ -87,37 +87,42 @@ int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G_dev, i
 int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);
 
 /* ---------------------------------------------------------------------
- * CountSketch apply plan.  The rows are cut into chunks of `chunk` rows.
- * Bucket b belongs to warp group w(b) = b / ceil(d / warps) of the consuming
- * CTA (contiguous ranges keep a warp's lanes on different smem banks);
- * per chunk the non-empty buckets of each group become "tasks" ordered by
- * descending entry count (ties by bucket id).  Per chunk k the task block
- * tasks[k*stride ...] holds
- *   [0, H)        H = round4(warps+1): first task index of each group
- *                 (relative to the task list), group `warps` = end;
- *   [H, H+ntask)  (bucket << 16) | first entry of the task;
- * and entries[k*chunk + e] = 8 * local row | negative sign (bit 0) -- the
- * row's byte offset in the staged column chunk with the sign folded in --
- * grouped by task, ascending row inside a task.  It is the chunked
- * form of the reference's CSR sparse_map (sketch.py:100-102) and keeps
- * scipy csr_matvecs' ascending-row fold order per bucket, so the device
- * apply is bitwise-equal to it; a bucket always lands in the same warp and
- * the count ordering gives the lanes of a warp equal work.
- * Limits: d <= 65536, chunk a multiple of 8 in [8, 8192], warps in {4,8,16}.
+ * CountSketch apply plan ("lane lists").  The rows are cut into chunks of
+ * `chunk` rows (<= 4088).  Bucket b belongs to warp w(b) = b / ceil(d/warps)
+ * of the consuming CTA.  Per chunk, each warp's non-empty buckets are
+ * scheduled onto its 32 lanes: a lane walks one bucket's rows (ascending)
+ * at a time and keeps the bucket's running sum in a register, also into
+ * the next chunk when it continues the same bucket; free lanes take the
+ * bucket that keeps that step's shared-memory banks least loaded.  A
+ * chunk's block, at lanes[chunk_off[k]], is
+ *   [0, H)        H = round4(warps+1): first list row of each warp, and the
+ *                 total number of rows at index `warps`;
+ *   [H, ...)      rows of 32 words, word (r*32 + lane) = that lane's r-th
+ *                 entry: bits 0..14 byte offset 8*row of the source row in
+ *                 the staged chunk (8*chunk = a zero slot), bits 16..30 the
+ *                 bucket (d = dummy slot), bit 31 negative sign.  A lane
+ *                 writes its held sum back and loads the entry's bucket
+ *                 whenever the bucket field changes.
+ * This is the chunked, lane-scheduled form of the reference's CSR
+ * sparse_map (sketch.py:100-102); it keeps scipy csr_matvecs' ascending-row
+ * fold per bucket, so the device apply is bitwise-equal to it.
+ * Call with lanes == NULL first to get chunk_off (nch + 1 entries; the
+ * block sizes), then with a buffer of chunk_off[nch] words.
+ * Limits: d <= 32767, chunk a multiple of 8 in [8, 4088], warps in [1, 31].
  * ------------------------------------------------------------------- */
-int64_t skl_countsketch_plan_stride(int64_t d, int warps);
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
-                         int64_t chunk, int warps, uint16_t* entries, uint32_t* tasks,
-                         int32_t* ntask, int threads);
+                         int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                         int threads);
 
-/* S*A and S*b for dense column-major A (device pointers, plan on device).
+/* S*A and S*b for dense column-major A (device pointers, plan on device;
+ * max_block = largest chunk block in words).
  * b may be NULL (then Sb is ignored).  partitions: 0 = auto, 1 = single
  * ordered pass (bitwise-equal to the reference), P>1 = P row partitions
  * reduced in a fixed order (deterministic).  accumulate != 0 adds into
  * SA/Sb (used for row-streamed applies).  Replaces sketch.py:209-212
  * (dense branch). */
 int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
-                          const uint16_t* entries, const uint32_t* tasks, const int32_t* ntask,
+                          const uint32_t* lanes, const int64_t* chunk_off, int64_t max_block,
                           int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                           double* Sb, int partitions, int accumulate, void* stream);
 
@@ -126,8 +131,8 @@ int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, co
  * A_dev_keep != NULL the device copy of A (ld = m rounded up to 32) is
  * left there for a later residual pass.  plan pointers are device. */
 int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
-                               const double* b_host, const uint16_t* entries,
-                               const uint32_t* tasks, const int32_t* ntask, int64_t d,
+                               const double* b_host, const uint32_t* lanes,
+                               const int64_t* chunk_off, int64_t max_block, int64_t d,
                                int64_t chunk, int warps, double* SA_host, int64_t ldsa, double* Sb_host,
                                double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                void* stream);

@@ -44,17 +44,16 @@ SIGNATURES: dict[str, tuple] = {
     "skl_rng_u64": (c_int, [c_u64, c_u64, c_i64, c_ptr]),
     "skl_rng_countsketch": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int, c_ptr]),
     "skl_rng_srht": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
-    "skl_countsketch_plan_stride": (c_i64, [c_i64, c_int]),
     "skl_countsketch_plan": (
-        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_int]),
+        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_int]),
     "skl_countsketch_dense": (
         c_int,
-        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_int, c_int, c_ptr],
     ),
     "skl_countsketch_dense_host": (
         c_int,
-        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     ),
     "skl_srht_dense": (
@@ -192,17 +191,17 @@ def plan_geometry(d: int) -> tuple[int, int]:
 
 
 def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
-                     threads: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
-    """(entries u16 [nch*chunk], tasks u32 [nch*stride], ntask i32 [nch])."""
+                     threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
+    """(lanes u32, chunk_off i64 [nch+1], max block words) -- see the header."""
     m = rows.shape[0]
     nch = (m + chunk - 1) // chunk
-    stride = int(lib().skl_countsketch_plan_stride(d, warps))
-    ent = np.zeros(nch * chunk, dtype=np.uint16)
-    tasks = np.zeros(nch * stride, dtype=np.uint32)
-    ntask = np.zeros(nch, dtype=np.int32)
-    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(ent), ptr(tasks),
-         ptr(ntask), threads)
-    return ent, tasks, ntask
+    off = np.zeros(nch + 1, dtype=np.int64)
+    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, None, ptr(off),
+         threads)
+    lanes = np.empty(int(off[-1]), dtype=np.uint32)
+    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(lanes), ptr(off),
+         threads)
+    return lanes, off, int(np.diff(off).max())
 
 
 def countsketch_buckets(rows: np.ndarray, d: int) -> tuple[np.ndarray, np.ndarray]:

@@ -9,18 +9,24 @@
 // Design (B200): one CTA owns C columns of [A | b] and streams them once,
 // top to bottom, in chunks of T rows.  A producer warp issues 1-D bulk
 // copies (cp.async.bulk -> UBLKCP) of each chunk's column segments and the
-// chunk's slice of the plan (L2-resident, shared by all CTAs) into an
+// chunk's block of the plan (L2-resident, shared by all CTAs) into an
 // S-stage shared-memory ring guarded by full/empty mbarriers.  The running
-// bucket sums live in shared memory (C x d doubles).  Bucket b always
-// belongs to warp b / ceil(d/W) (contiguous ranges: random smem banks); per chunk the plan lists each warp's non-empty
-// buckets as tasks sorted by entry count, so the 32 lanes of a warp walk
-// buckets of (nearly) equal length: each lane loads its bucket's sum, adds
-// the bucket's rows in ascending order and stores it back.  Because a
-// bucket never changes warp, __syncwarp orders its updates across chunks
-// and no CTA-wide barrier is needed per chunk.  No atomics; A is
-// read from HBM exactly once with evict-first L2 hints.  With P > 1 row
-// partitions (few columns, long input), partial sums go to a workspace and
-// are reduced in fixed partition order (deterministic, not bitwise).
+// bucket sums live in shared memory (C x (d+1) doubles; slot d is a dummy).
+// Bucket b always belongs to warp b / ceil(d/W); per chunk the plan deals
+// each warp's buckets to its 32 lanes so that every lane walks the same
+// number of entries ("lane lists", interleaved so a warp reads 32
+// consecutive words).  An entry carries the row's byte offset, the sign and
+// the bucket: when the bucket differs from the one the lane holds, the lane
+// writes the held sum back and loads the new one (a lane keeps its bucket
+// across chunks when the plan continues it), then every entry is one masked
+// load, one XOR (exact negation) and one add -- in ascending row order per
+// bucket, as scipy's csr_matvecs folds.  The plan schedules lanes so each
+// step's shared-memory gathers spread over the banks.  A bucket never leaves
+// its warp, so __syncwarp orders its updates across chunks; no CTA barrier
+// and no atomics.  A is read from HBM exactly once with evict-first L2 hints.
+// With P > 1 row partitions (few columns, long input), partial sums go to a
+// workspace and are reduced in fixed partition order (deterministic, not
+// bitwise).
 #include <algorithm>
 #include <vector>
 
@@ -40,12 +46,11 @@ struct CsParams {
   int64_t n;        // columns of A
   int64_t ncols;    // n + (b != nullptr)
   int64_t row_begin, row_end;  // rows handled by this launch (row_begin % T == 0)
-  const uint16_t* ent;
-  const uint32_t* tasks;
-  const int32_t* ntask;
+  const uint32_t* lanes;
+  const int64_t* chunk_off;
+  int max_block;    // words
   int d;
   int T;
-  int stride;
   int head;         // per-chunk warp-offset header (u32 words)
   int P;
   double* out;      // SA (P == 1)
@@ -65,18 +70,17 @@ __device__ __forceinline__ void cs_consumer_bar() {
 }
 
 template <int NT, int C>
-__global__ void __launch_bounds__(NT + 32)
+__global__ void __launch_bounds__(NT + 32, 2)
     countsketch_dense_kernel(const CsParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + CS_STAGES;
-  int* nt_s = reinterpret_cast<int*>(empty + CS_STAGES);
   const int T = p.T, d = p.d;
+  const int ldacc = d + 1;
   double* acc_s = reinterpret_cast<double*>(smem + 128);
-  unsigned char* ring = smem + 128 + (((size_t)C * d * sizeof(double) + 127) & ~(size_t)127);
-  const size_t a_bytes = (size_t)C * T * sizeof(double);
-  const size_t e_bytes = (size_t)T * sizeof(uint16_t);
-  const size_t stage_bytes = a_bytes + e_bytes + (size_t)p.stride * sizeof(uint32_t);
+  unsigned char* ring = smem + 128 + (((size_t)C * ldacc * sizeof(double) + 127) & ~(size_t)127);
+  const size_t a_bytes = (size_t)C * (T + 2) * sizeof(double);
+  const size_t stage_bytes = (a_bytes + (size_t)p.max_block * sizeof(uint32_t) + 127) & ~(size_t)127;
 
   const int tid = threadIdx.x;
   const int64_t col0 = (int64_t)blockIdx.x * C;
@@ -93,6 +97,11 @@ __global__ void __launch_bounds__(NT + 32)
     }
     fence_mbar_init();
   }
+  // zero slot (index T of every staged column; never written by the copies)
+  if (tid < CS_STAGES * C) {
+    double* As = reinterpret_cast<double*>(ring + (tid / C) * stage_bytes);
+    As[(tid % C) * (T + 2) + T] = 0.0;
+  }
   __syncthreads();
 
   if (tid >= NT) {
@@ -107,28 +116,23 @@ __global__ void __launch_bounds__(NT + 32)
         const int64_t r0 = ch * T;
         const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
         const int len_even = len & ~1;
-        const int nt = __ldg(p.ntask + ch);
+        const int64_t o0 = __ldg(p.chunk_off + ch), o1 = __ldg(p.chunk_off + ch + 1);
         unsigned char* st = ring + s * stage_bytes;
         double* As = reinterpret_cast<double*>(st);
-        uint16_t* Es = reinterpret_cast<uint16_t*>(st + a_bytes);
-        uint32_t* Ts = reinterpret_cast<uint32_t*>(st + a_bytes + e_bytes);
-        const uint32_t ebytes = (uint32_t)(((len + 7) & ~7) * sizeof(uint16_t));
-        const uint32_t tbytes = (uint32_t)((p.head + ((nt + 3) & ~3)) * sizeof(uint32_t));
+        uint32_t* Ls = reinterpret_cast<uint32_t*>(st + a_bytes);
+        const uint32_t lbytes = (uint32_t)((o1 - o0) * sizeof(uint32_t));
         if (len & 1) {
           for (int c = 0; c < ncol_here; ++c)
-            As[c * T + len - 1] = __ldg(cs_col(p, col0 + c) + r0 + len - 1);
+            As[c * (T + 2) + len - 1] = __ldg(cs_col(p, col0 + c) + r0 + len - 1);
         }
-        nt_s[s] = nt;
-        const uint32_t total =
-            (uint32_t)(ncol_here * len_even * sizeof(double)) + ebytes + tbytes;
+        const uint32_t total = (uint32_t)(ncol_here * len_even * sizeof(double)) + lbytes;
         mbar_arrive_expect_tx(&full[s], total);
         if (len_even) {
           for (int c = 0; c < ncol_here; ++c)
-            bulk_g2s(As + c * T, cs_col(p, col0 + c) + r0, (uint32_t)(len_even * sizeof(double)),
-                     &full[s], pol_stream);
+            bulk_g2s(As + c * (T + 2), cs_col(p, col0 + c) + r0,
+                     (uint32_t)(len_even * sizeof(double)), &full[s], pol_stream);
         }
-        bulk_g2s(Es, p.ent + r0, ebytes, &full[s], pol_keep);
-        bulk_g2s(Ts, p.tasks + ch * p.stride, tbytes, &full[s], pol_keep);
+        bulk_g2s(Ls, p.lanes + o0, lbytes, &full[s], pol_keep);
       }
     }
     return;
@@ -141,54 +145,53 @@ __global__ void __launch_bounds__(NT + 32)
       double v = 0.0;
       const int64_t col = col0 + c;
       if (p.P == 1 && p.accumulate && c < ncol_here) v = col < p.n ? p.out[col * p.ldo + i] : p.outb[i];
-      acc_s[c * d + i] = v;
+      acc_s[c * ldacc + i] = v;
     }
   }
   cs_consumer_bar<NT>();
 
+  const int wid = tid >> 5, lane = tid & 31;
+  // The lane's current bucket and its running sum stay in registers across
+  // chunks; the sum goes back to shared memory only when the plan switches
+  // the lane to another bucket (or to the dummy slot d).
+  int cur = d;
+  double a[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) a[c] = 0.0;
   for (int64_t it = 0; it < niter; ++it) {
     const int s = (int)(it % CS_STAGES);
     mbar_wait(&full[s], (uint32_t)((it / CS_STAGES) & 1));
-    const int64_t r0 = (ch_first + it0 + it) * T;
-    const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
     const unsigned char* st = ring + s * stage_bytes;
-    const double* As = reinterpret_cast<const double*>(st);
-    const uint16_t* Es = reinterpret_cast<const uint16_t*>(st + a_bytes);
-    const uint32_t* Ts = reinterpret_cast<const uint32_t*>(st + a_bytes + e_bytes);
-    const uint32_t* Ks = Ts + p.head;
-    const int nt = nt_s[s];
-    const int wid = tid >> 5, lane = tid & 31;
-    const int lo = (int)Ts[wid], hi = (int)Ts[wid + 1];
-    // Per task (= one bucket of this chunk): load the running sum, fold the
-    // bucket's rows in ascending order, store it back.  An entry is the
-    // row's byte offset in the staged column with the sign in bit 0, which
-    // is moved into the sign bit of the loaded double (exact negation).
-    const unsigned char* Ab = reinterpret_cast<const unsigned char*>(As);
-    for (int i = lo + lane; i < hi; i += 32) {
-      const uint32_t tv = Ks[i];
-      const int bkt = (int)(tv >> 16);
-      int e = (int)(tv & 0xffff);
-      const int e1 = i + 1 < nt ? (int)(Ks[i + 1] & 0xffff) : len;
-      double a[C];
+    const unsigned char* Ab = st;
+    const uint32_t* H = reinterpret_cast<const uint32_t*>(st + a_bytes);
+    const uint32_t* Lr = H + p.head + lane;
+    const int r0 = (int)H[wid], r1 = (int)H[wid + 1];
+#pragma unroll 2
+    for (int r = r0; r < r1; ++r) {
+      const uint32_t e = Lr[r * 32];
+      const unsigned char* src = Ab + (e & 0x7fffu);
+      double x[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) a[c] = acc_s[c * d + bkt];
-#pragma unroll 1
-      do {
-        const uint32_t v = Es[e];
-        const uint32_t flip = v << 31;
-        const unsigned char* src = Ab + (v & 0xfff8u);
+      for (int c = 0; c < C; ++c) {
+        const uint2 w = *reinterpret_cast<const uint2*>(src + (size_t)c * (T + 2) * 8);
+        x[c] = __hiloint2double((int)(w.y ^ (e & 0x80000000u)), (int)w.x);
+      }
+      const int b = (int)((e >> 16) & 0x7fffu);
+      if (b != cur) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const uint2 w = *reinterpret_cast<const uint2*>(src + (size_t)c * T * 8);
-          a[c] += __hiloint2double((int)(w.y ^ flip), (int)w.x);
-        }
-      } while (++e < e1);
+        for (int c = 0; c < C; ++c) acc_s[c * ldacc + cur] = a[c];
+        cur = b;
 #pragma unroll
-      for (int c = 0; c < C; ++c) acc_s[c * d + bkt] = a[c];
+        for (int c = 0; c < C; ++c) a[c] = acc_s[c * ldacc + cur];
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) a[c] += x[c];
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc_s[c * ldacc + cur] = a[c];
   cs_consumer_bar<NT>();
 
 #pragma unroll
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(NT + 32)
     if (c >= ncol_here) break;
     const int64_t col = col0 + c;
     for (int i = tid; i < d; i += NT) {
-      const double v = acc_s[c * d + i];
+      const double v = acc_s[c * ldacc + i];
       if (p.P == 1) {
         if (col < p.n)
           p.out[col * p.ldo + i] = v;
@@ -242,6 +245,9 @@ static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStre
   auto kern = countsketch_dense_kernel<NT, C>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   kern<<<grid, NT + 32, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -257,23 +263,23 @@ static cudaError_t dispatch_cs(int nt, int C, const CsParams& p, dim3 grid, size
 
 // Core launcher shared by the device and host-streaming entry points.
 static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
-                              const uint16_t* ent, const uint32_t* tasks, const int32_t* ntask,
+                              const uint32_t* lanes, const int64_t* chunk_off, int64_t max_block,
                               int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                               double* Sb, int partitions, int accumulate, int64_t row_begin,
                               int64_t row_end, cudaStream_t st) {
   SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld lda=%lld ldsa=%lld", (long long)m,
               (long long)n, (long long)d, (long long)lda, (long long)ldsa);
-  SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch: embed_dim %lld > 65536 not supported",
+  SKL_REQUIRE(d <= 32767, SKL_ERR_SPEC, "countsketch: embed_dim %lld > 32767 not supported",
               (long long)d);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 8192 && chunk % 8 == 0, SKL_ERR_INVALID,
+  SKL_REQUIRE(chunk >= 8 && chunk <= 4088 && chunk % 8 == 0, SKL_ERR_INVALID,
               "countsketch: bad plan chunk %lld", (long long)chunk);
-  SKL_REQUIRE(A && ent && tasks && ntask && SA && (!b || Sb), SKL_ERR_INVALID,
+  SKL_REQUIRE(A && lanes && chunk_off && SA && (!b || Sb) && max_block > 0, SKL_ERR_INVALID,
               "countsketch: null pointer");
   SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && (!b || ((uintptr_t)b & 15) == 0),
               SKL_ERR_INVALID,
               "countsketch: A/b must be 16-byte aligned with an even leading dimension");
-  SKL_REQUIRE(((uintptr_t)ent & 15) == 0 && ((uintptr_t)tasks & 15) == 0, SKL_ERR_INVALID,
+  SKL_REQUIRE(((uintptr_t)lanes & 15) == 0, SKL_ERR_INVALID,
               "countsketch: plan arrays must be 16-byte aligned");
   SKL_REQUIRE(row_begin % chunk == 0 && row_end > row_begin && row_end <= m, SKL_ERR_INVALID,
               "countsketch: bad row range");
@@ -284,9 +290,8 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
   const int64_t ncols = n + (b ? 1 : 0);
   int C = 1;
   const int T = (int)chunk;
-  const int stride = (int)skl_countsketch_plan_stride(d, warps);
-  const size_t stage = (size_t)C * T * 8 + (size_t)T * 2 + (size_t)stride * 4;
-  const size_t smem = 128 + (((size_t)C * d * 8 + 127) & ~(size_t)127) + CS_STAGES * stage;
+  const size_t stage = ((size_t)C * (T + 2) * 8 + (size_t)max_block * 4 + 127) & ~(size_t)127;
+  const size_t smem = 128 + (((size_t)C * (d + 1) * 8 + 127) & ~(size_t)127) + CS_STAGES * stage;
   SKL_REQUIRE(smem <= 227 * 1024, SKL_ERR_INVALID,
               "countsketch: chunk %d / embed_dim %lld too large for shared memory", T, (long long)d);
 
@@ -305,7 +310,8 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
   CsParams p;
   p.A = A; p.lda = lda; p.b = b; p.n = n; p.ncols = ncols;
   p.row_begin = row_begin; p.row_end = row_end;
-  p.ent = ent; p.tasks = tasks; p.ntask = ntask; p.d = (int)d; p.T = T; p.stride = stride; p.P = P;
+  p.lanes = lanes; p.chunk_off = chunk_off; p.max_block = (int)max_block;
+  p.d = (int)d; p.T = T; p.P = P;
   p.head = (warps + 1 + 3) / 4 * 4;
   p.out = SA; p.ldo = ldsa; p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
 
@@ -336,13 +342,14 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
 using namespace skl;
 
 extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,
-                                     const double* b, const uint16_t* entries,
-                                     const uint32_t* tasks, const int32_t* ntask, int64_t d,
+                                     const double* b, const uint32_t* lanes,
+                                     const int64_t* chunk_off, int64_t max_block, int64_t d,
                                      int64_t chunk, int warps, double* SA,
                                      int64_t ldsa, double* Sb, int partitions, int accumulate,
                                      void* stream) {
   clear_error();
-  return countsketch_launch(A, m, n, lda, b, entries, tasks, ntask, d, chunk, warps, SA, ldsa, Sb,
+  return countsketch_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps, SA, ldsa,
+                            Sb,
                             partitions,
                             accumulate, 0, m, (cudaStream_t)stream);
 }
@@ -351,8 +358,8 @@ extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int6
 // side stream while the kernel sketches the previous block (ordered pass,
 // accumulate across blocks, so the result stays bitwise-equal).
 extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
-                                          const double* b_host, const uint16_t* entries,
-                                          const uint32_t* tasks, const int32_t* ntask,
+                                          const double* b_host, const uint32_t* lanes,
+                                          const int64_t* chunk_off, int64_t max_block,
                                           int64_t d, int64_t chunk, int warps,
                                           double* SA_host, int64_t ldsa, double* Sb_host,
                                           double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
@@ -400,7 +407,8 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
       rc = SKL_ERR_CUDA;
       break;
     }
-    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, entries, tasks, ntask, d,
+    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, lanes, chunk_off,
+                            max_block, d,
                             chunk, warps, SA_dev, d, Sb_dev, 1, k > 0 ? 1 : 0, r0, r1, st);
   }
   if (rc == SKL_OK) {

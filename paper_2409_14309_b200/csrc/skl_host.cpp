@@ -85,6 +85,199 @@ static void fill_u32_par(uint64_t key, uint64_t pos0, int64_t count, uint32_t* o
 
 using namespace skl;
 
+// ---------------------------------------------------------------------------
+// CountSketch plan (see the header).
+//
+// Schedule of one warp (its contiguous bucket range) over the chunks, built
+// sequentially chunk after chunk because a lane keeps its last bucket's sum
+// in a register into the next chunk.  Per chunk:
+//   * the non-empty buckets of the warp form a pool, each with its rows in
+//     ascending order (stable counting sort of the chunk by bucket);
+//   * step 0: a lane whose current bucket is in the pool continues it (no
+//     reload); every other lane switches -- to a new bucket from the pool,
+//     or to the dummy slot so its held sum is written back before another
+//     lane can read it;
+//   * at every step a lane without work takes the pool bucket that keeps
+//     this step's shared-memory banks least loaded (first-row gather bank,
+//     then accumulator bank), longest buckets first;
+//   * idle lanes emit padding that adds +0.0 to the bucket they hold.
+// Entry word: byte offset 8*row (8*chunk = zero slot) | bucket << 16 |
+// sign << 31; a lane reloads whenever the bucket field changes.
+static int64_t plan_head(int warps) { return (warps + 1 + 3) / 4 * 4; }
+
+namespace {
+
+// Chunks are planned in independent segments of this many chunks (lanes
+// start a segment holding no bucket), which is what makes the planner
+// parallel; the segmentation never depends on the thread count.
+constexpr int64_t kPlanSegment = 32;
+
+struct ChunkSort {
+  std::vector<uint32_t> cnt, start, pos;
+  std::vector<uint16_t> sorted;
+  ChunkSort(int64_t d, int64_t chunk)
+      : cnt((size_t)d), start((size_t)d), pos((size_t)d), sorted((size_t)chunk) {}
+  // stable counting sort of chunk k's rows by bucket; false on a bad bucket
+  bool run(const int32_t* rows, int64_t m, int64_t d, int64_t chunk, int64_t k) {
+    const int64_t r0 = k * chunk;
+    const int len = (int)std::min<int64_t>(chunk, m - r0);
+    std::fill(cnt.begin(), cnt.end(), 0u);
+    for (int j = 0; j < len; ++j) {
+      const int32_t r = rows[r0 + j];
+      if (r < 0 || r >= d) return false;
+      ++cnt[(size_t)r];
+    }
+    uint32_t run = 0;
+    for (int64_t b = 0; b < d; ++b) {
+      start[(size_t)b] = run;
+      pos[(size_t)b] = run;
+      run += cnt[(size_t)b];
+    }
+    for (int j = 0; j < len; ++j) sorted[pos[(size_t)rows[r0 + j]]++] = (uint16_t)j;
+    return true;
+  }
+};
+
+struct WarpSched {
+  uint32_t cur[32];
+  std::vector<uint32_t> pool, bank[16], byc;
+  std::vector<uint8_t> taken;
+  size_t bhead[16];
+};
+
+// Schedules warp w's buckets [b0, b1) of chunk k (sorted in S) onto the 32
+// lanes, appending rows of 32 words to `words`.
+void schedule_chunk(const int8_t* signs, int64_t d, int64_t chunk, int64_t r0, int64_t b0,
+                    int64_t b1, const ChunkSort& S, WarpSched& W, std::vector<uint32_t>& words) {
+  const uint32_t dummy = (uint32_t)d;
+  const uint32_t zero_off = (uint32_t)(8 * chunk);
+  uint32_t* cur = W.cur;
+  uint32_t pos[32];
+  int32_t run[32];
+  // pool = non-empty buckets by descending count, ties by id (counting sort)
+  uint32_t maxc = 0;
+  for (int64_t b = b0; b < b1; ++b) maxc = std::max(maxc, S.cnt[(size_t)b]);
+  if (W.byc.size() < (size_t)maxc + 2) W.byc.resize((size_t)maxc + 2);
+  std::fill(W.byc.begin(), W.byc.begin() + maxc + 2, 0u);
+  for (int64_t b = b0; b < b1; ++b) ++W.byc[S.cnt[(size_t)b]];
+  uint32_t npool = 0;
+  for (int64_t c = (int64_t)maxc; c >= 1; --c) {
+    const uint32_t h = W.byc[(size_t)c];
+    W.byc[(size_t)c] = npool;
+    npool += h;
+  }
+  W.pool.resize(npool);
+  for (int64_t b = b0; b < b1; ++b) {
+    const uint32_t c = S.cnt[(size_t)b];
+    if (c) W.pool[W.byc[c]++] = (uint32_t)b;
+  }
+  if (W.taken.size() < (size_t)(b1 - b0 + 1)) W.taken.resize((size_t)(b1 - b0 + 1));
+  std::fill(W.taken.begin(), W.taken.end(), 0);
+  for (int g = 0; g < 16; ++g) {
+    W.bank[g].clear();
+    W.bhead[g] = 0;
+  }
+  for (uint32_t b : W.pool) W.bank[S.sorted[S.start[b]] & 15].push_back(b);
+  size_t left = W.pool.size();
+  for (int l = 0; l < 32; ++l) run[l] = -1;
+  for (int l = 0; l < 32; ++l) {  // continuations keep their register sum
+    const uint32_t b = cur[l];
+    if (b != dummy && S.cnt[b] && !W.taken[b - b0]) {
+      W.taken[b - b0] = 1;
+      --left;
+      run[l] = (int32_t)b;
+      pos[l] = 0;
+    }
+  }
+  bool first = true;
+  for (;;) {
+    bool busy = false;
+    for (int l = 0; l < 32; ++l) busy |= run[l] >= 0;
+    if (!first && !busy && !left) break;
+    int gl[16] = {0}, al[16] = {0};
+    for (int l = 0; l < 32; ++l)
+      if (run[l] >= 0) gl[S.sorted[S.start[(uint32_t)run[l]] + pos[l]] & 15]++;
+    for (int l = 0; l < 32 && left; ++l) {
+      if (run[l] >= 0) continue;
+      // least-loaded gather bank with work left, then the least-loaded
+      // accumulator bank among its first few (longest) buckets
+      int gbest = -1;
+      for (int g = 0; g < 16; ++g) {
+        while (W.bhead[g] < W.bank[g].size() && W.taken[W.bank[g][W.bhead[g]] - b0]) ++W.bhead[g];
+        if (W.bhead[g] < W.bank[g].size() && (gbest < 0 || gl[g] < gl[gbest])) gbest = g;
+      }
+      const std::vector<uint32_t>& q = W.bank[gbest];
+      size_t pick = W.bhead[gbest];
+      int abest = al[q[pick] & 15];
+      for (size_t t = pick + 1, seen = 0; t < q.size() && seen < 4 && abest > 0; ++t) {
+        if (W.taken[q[t] - b0]) continue;
+        ++seen;
+        if (al[q[t] & 15] < abest) {
+          abest = al[q[t] & 15];
+          pick = t;
+        }
+      }
+      const uint32_t b = q[pick];
+      W.taken[b - b0] = 1;
+      --left;
+      run[l] = (int32_t)b;
+      pos[l] = 0;
+      gl[gbest]++;
+      al[b & 15]++;
+    }
+    bool any = false;
+    for (int l = 0; l < 32; ++l) {
+      uint32_t word;
+      if (run[l] >= 0) {
+        const uint32_t b = (uint32_t)run[l];
+        const uint32_t j = S.sorted[S.start[b] + pos[l]];
+        word = (8u * j) | (b << 16) | ((signs[r0 + j] < 0 ? 1u : 0u) << 31);
+        cur[l] = b;
+        if (++pos[l] == S.cnt[b]) run[l] = -1;
+        any = true;
+      } else if (first && cur[l] != dummy) {
+        word = zero_off | (dummy << 16);  // write the held sum back
+        cur[l] = dummy;
+        any = true;
+      } else {
+        word = zero_off | (cur[l] << 16);  // padding: +0.0 to the held bucket
+      }
+      words.push_back(word);
+    }
+    first = false;
+    if (!any) {
+      words.resize(words.size() - 32);
+      break;
+    }
+  }
+}
+
+// Runs the schedule of chunks [k0, k1) for all warps; per chunk calls
+// sink(k, warp_rows[warps], words_of_warp[warps]).
+template <class Sink>
+bool plan_segment(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d, int64_t chunk,
+                  int warps, int64_t k0, int64_t k1, Sink&& sink) {
+  const int64_t gsize = (d + warps - 1) / warps;
+  ChunkSort S(d, chunk);
+  std::vector<WarpSched> W((size_t)warps);
+  for (auto& ws : W)
+    for (int l = 0; l < 32; ++l) ws.cur[l] = (uint32_t)d;
+  std::vector<std::vector<uint32_t>> words((size_t)warps);
+  for (int64_t k = k0; k < k1; ++k) {
+    if (!S.run(rows, m, d, chunk, k)) return false;
+    for (int w = 0; w < warps; ++w) {
+      const int64_t b0 = std::min<int64_t>(d, w * gsize), b1 = std::min<int64_t>(d, b0 + gsize);
+      words[(size_t)w].clear();
+      schedule_chunk(signs, d, chunk, k * chunk, b0, b1, S, W[(size_t)w], words[(size_t)w]);
+    }
+    sink(k, words);
+  }
+  return true;
+}
+
+}  // namespace
+
+
 extern "C" {
 
 const char* skl_last_error(void) { return skl::g_err.c_str(); }
@@ -289,99 +482,68 @@ int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t*
   return SKL_OK;
 }
 
-// ---------------------------------------------------------------------------
-// CountSketch plan (see the header).  Per chunk: a stable counting sort of
-// the rows by bucket, then per warp group the non-empty buckets ordered by
-// descending count (ties by bucket id) become the tasks.
-static int64_t plan_head(int warps) { return (warps + 1 + 3) / 4 * 4; }
-
-int64_t skl_countsketch_plan_stride(int64_t d, int warps) {
-  return plan_head(warps) + (d + 3) / 4 * 4;
-}
-
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
-                         int64_t chunk, int warps, uint16_t* entries, uint32_t* tasks,
-                         int32_t* ntask, int threads) {
+                         int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                         int threads) {
   clear_error();
-  SKL_REQUIRE(rows && signs && entries && tasks && ntask && m >= 1 && d >= 1, SKL_ERR_INVALID,
+  SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1, SKL_ERR_INVALID,
               "skl_countsketch_plan: bad arguments");
-  SKL_REQUIRE(d <= 65536, SKL_ERR_SPEC, "countsketch plan: embed_dim %lld > 65536",
+  SKL_REQUIRE(d <= 32767, SKL_ERR_SPEC, "countsketch plan: embed_dim %lld > 32767",
               (long long)d);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 8192 && chunk % 8 == 0, SKL_ERR_INVALID,
-              "plan chunk must be a multiple of 8 in [8, 8192], got %lld", (long long)chunk);
-  SKL_REQUIRE(warps == 4 || warps == 8 || warps == 16, SKL_ERR_INVALID,
-              "plan warps must be 4, 8 or 16, got %d", warps);
-  const int64_t stride = skl_countsketch_plan_stride(d, warps);
-  const int64_t head = plan_head(warps);
+  SKL_REQUIRE(chunk >= 8 && chunk <= 4088 && chunk % 8 == 0, SKL_ERR_INVALID,
+              "plan chunk must be a multiple of 8 in [8, 4088], got %lld", (long long)chunk);
+  SKL_REQUIRE(warps >= 1 && warps <= 31, SKL_ERR_INVALID,
+              "plan warps must be in [1, 31], got %d", warps);
   const int64_t nch = (m + chunk - 1) / chunk;
+  const int64_t head = plan_head(warps);
+  const int64_t nseg = (nch + kPlanSegment - 1) / kPlanSegment;
   threads = resolve_threads(threads);
+  // pass 1: list rows per (chunk, warp)
+  std::vector<uint32_t> R((size_t)(nch * warps));
   std::atomic<int> bad{0};
-  parallel_for(nch, threads, [&](int64_t lo, int64_t hi) {
-    std::vector<uint32_t> cnt((size_t)d), start((size_t)d), order((size_t)d), pos((size_t)d);
-    std::vector<uint16_t> sorted((size_t)chunk);
-    std::vector<uint32_t> byc(64);
-    for (int64_t k = lo; k < hi; ++k) {
-      const int64_t r0 = k * chunk;
-      const int len = (int)std::min<int64_t>(chunk, m - r0);
-      std::fill(cnt.begin(), cnt.end(), 0u);
-      for (int j = 0; j < len; ++j) {
-        const int32_t r = rows[r0 + j];
-        if (r < 0 || r >= d) {
-          bad = 1;
-          return;
-        }
-        ++cnt[(size_t)r];
-      }
-      uint32_t run = 0;
-      for (int64_t i = 0; i < d; ++i) {
-        start[(size_t)i] = run;
-        pos[(size_t)i] = run;
-        run += cnt[(size_t)i];
-      }
-      for (int j = 0; j < len; ++j) {
-        const int32_t r = rows[r0 + j];
-        sorted[pos[(size_t)r]++] = (uint16_t)((j << 3) | (signs[r0 + j] < 0 ? 1 : 0));
-      }
-      // tasks: group by warp (contiguous bucket ranges), then count desc,
-      // then bucket id (counting sort on the count inside each group)
-      uint32_t nt = 0;
-      uint32_t* tk = tasks + k * stride;
-      const int64_t gsize = (d + warps - 1) / warps;
-      for (int w = 0; w < warps; ++w) {
-        tk[w] = nt;
-        const int64_t b0 = std::min<int64_t>(d, w * gsize), b1 = std::min<int64_t>(d, b0 + gsize);
-        uint32_t maxc = 0;
-        for (int64_t b = b0; b < b1; ++b) maxc = std::max(maxc, cnt[(size_t)b]);
-        if (maxc == 0) continue;
-        if (byc.size() < (size_t)maxc + 2) byc.resize((size_t)maxc + 2);
-        std::fill(byc.begin(), byc.begin() + maxc + 2, 0u);
-        for (int64_t b = b0; b < b1; ++b) ++byc[cnt[(size_t)b]];
-        uint32_t acc = nt;  // slot of count c = nt + #buckets with count > c
-        for (int64_t c = (int64_t)maxc; c >= 1; --c) {
-          const uint32_t h = byc[(size_t)c];
-          byc[(size_t)c] = acc;
-          acc += h;
-        }
-        for (int64_t b = b0; b < b1; ++b) {
-          const uint32_t c = cnt[(size_t)b];
-          if (c) order[byc[c]++] = (uint32_t)b;
-        }
-        nt = acc;
-      }
-      for (int64_t w = warps; w < head; ++w) tk[w] = nt;
-      uint16_t* ent = entries + r0;
-      uint32_t e = 0;
-      for (uint32_t t = 0; t < nt; ++t) {
-        const uint32_t bkt = order[t];
-        tk[head + t] = (bkt << 16) | e;
-        const uint32_t s0 = start[bkt], c = cnt[bkt];
-        for (uint32_t q = 0; q < c; ++q) ent[e++] = sorted[s0 + q];
-      }
-      for (int64_t t = head + nt; t < stride; ++t) tk[t] = 0;
-      ntask[k] = (int32_t)nt;
+  parallel_for(nseg, threads, [&](int64_t lo, int64_t hi) {
+    for (int64_t g = lo; g < hi; ++g) {
+      const int64_t k0 = g * kPlanSegment, k1 = std::min(nch, k0 + kPlanSegment);
+      if (!plan_segment(rows, signs, m, d, chunk, warps, k0, k1,
+                        [&](int64_t k, const std::vector<std::vector<uint32_t>>& wd) {
+                          for (int w = 0; w < warps; ++w)
+                            R[(size_t)(k * warps + w)] = (uint32_t)(wd[(size_t)w].size() / 32);
+                        }))
+        bad = 1;
     }
-  }, 4);
+  }, 1);
   SKL_REQUIRE(!bad.load(), SKL_ERR_INVALID, "bucket index out of range [0, %lld)", (long long)d);
+  std::vector<int64_t> off((size_t)nch + 1, 0);
+  for (int64_t k = 0; k < nch; ++k) {
+    int64_t rws = 0;
+    for (int w = 0; w < warps; ++w) rws += R[(size_t)(k * warps + w)];
+    off[(size_t)k + 1] = off[(size_t)k] + head + 32 * rws;
+  }
+  if (!lanes) {
+    std::copy(off.begin(), off.end(), chunk_off);
+    return SKL_OK;
+  }
+  for (int64_t k = 0; k <= nch; ++k)
+    SKL_REQUIRE(chunk_off[k] == off[(size_t)k], SKL_ERR_INVALID,
+                "countsketch plan: chunk offsets do not match this (rows, d, chunk, warps)");
+  // pass 2: emit
+  parallel_for(nseg, threads, [&](int64_t lo, int64_t hi) {
+    for (int64_t g = lo; g < hi; ++g) {
+      const int64_t k0 = g * kPlanSegment, k1 = std::min(nch, k0 + kPlanSegment);
+      plan_segment(rows, signs, m, d, chunk, warps, k0, k1,
+                   [&](int64_t k, const std::vector<std::vector<uint32_t>>& wd) {
+                     uint32_t* blk = lanes + off[(size_t)k];
+                     uint32_t base = 0;
+                     for (int w = 0; w < warps; ++w) {
+                       blk[w] = base;
+                       std::copy(wd[(size_t)w].begin(), wd[(size_t)w].end(),
+                                 blk + head + 32 * (int64_t)base);
+                       base += (uint32_t)(wd[(size_t)w].size() / 32);
+                     }
+                     for (int64_t w = warps; w < head; ++w) blk[w] = base;
+                   });
+    }
+  }, 1);
   return SKL_OK;
 }
 

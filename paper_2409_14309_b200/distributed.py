@@ -53,9 +53,9 @@ class ShardPlan:
 
     def device_plan(self):
         if self._plan is None:
-            plan = _native.countsketch_plan(self.rows, self.signs, self.d, PLAN_CHUNK,
-                                            plan_warps(self.d))
-            self._plan = tuple(to_device(a) for a in plan)
+            lanes, off, mx = _native.countsketch_plan(self.rows, self.signs, self.d, PLAN_CHUNK,
+                                                      plan_warps(self.d))
+            self._plan = (to_device(lanes), to_device(off), mx)
         return self._plan
 
 
@@ -65,13 +65,13 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
     require_cuda()
     m_loc = plan.r1 - plan.r0
     n = A_local.shape[1]
-    ent, tasks, ntask = plan.device_plan()
+    lanes, off, mx = plan.device_plan()
     d = plan.d
     ld = (d + 1) // 2 * 2  # keeps the Sb column 16-byte aligned
     out = device_f64((d, n + 1), fortran=True, ld=ld)
     _native.call("skl_countsketch_dense", _native.ptr(A_local), m_loc, n, lda,
-                 _native.ptr(b_local), _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask),
-                 d, PLAN_CHUNK, plan_warps(d),
+                 _native.ptr(b_local), _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK,
+                 plan_warps(d),
                  _native.ptr(out), ld, _native.ptr(out[:, n]), 1, 0, current_stream())
     return out
 

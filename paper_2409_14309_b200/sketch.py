@@ -22,6 +22,8 @@ There is no host fallback: without the CUDA library the applies raise.
 from __future__ import annotations
 
 import math
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -131,13 +133,13 @@ class SketchOperator:
         return self._dev.setdefault(dev, {})
 
     def device_plan(self):
-        """(entries, tasks, ntask) of the CountSketch plan on the current device."""
+        """(lanes, chunk_off, max_block) of the CountSketch plan on the current device."""
         require_cuda()
         c = self._cache()
         if "plan" not in c:
-            plan = _native.countsketch_plan(self.rows, self.signs, self.target_dim, PLAN_CHUNK,
-                                            plan_warps(self.target_dim))
-            c["plan"] = tuple(to_device(a) for a in plan)
+            lanes, off, mx = _native.countsketch_plan(self.rows, self.signs, self.target_dim,
+                                                      PLAN_CHUNK, plan_warps(self.target_dim))
+            c["plan"] = (to_device(lanes), to_device(off), mx)
         return c["plan"]
 
     def device_buckets(self):
@@ -176,10 +178,41 @@ class SketchOperator:
         return c["gauss"]
 
 
+_OP_CACHE: "OrderedDict[tuple, SketchOperator]" = OrderedDict()
+_OP_CACHE_LOCK = threading.Lock()
+OP_CACHE_SIZE = 4
+
+
+def clear_operator_cache() -> None:
+    """Drop cached operators (and the device memory their plans hold)."""
+    with _OP_CACHE_LOCK:
+        _OP_CACHE.clear()
+
+
 def build_sketch(spec: SketchSpec, m: int) -> SketchOperator:
-    """Realise ``spec`` for source dimension ``m`` (sketch.py:84-127)."""
+    """Realise ``spec`` for source dimension ``m`` (sketch.py:84-127).
+
+    Operators are immutable and a (spec, m) pair always yields the same one
+    bitwise, so the most recent ones are cached: repeated
+    solves with the same spec skip the host draws and the device upload."""
     if m < 1:
         raise SpecError(f"source dimension must be >= 1, got {m}")
+    key = (spec.kind, spec.embed_dim, spec.seed & ((1 << 64) - 1), spec.sparsity, m)
+    with _OP_CACHE_LOCK:
+        op = _OP_CACHE.get(key)
+        if op is not None:
+            _OP_CACHE.move_to_end(key)
+            return op
+    op = _build_sketch(spec, m)
+    if OP_CACHE_SIZE > 0:
+        with _OP_CACHE_LOCK:
+            _OP_CACHE[key] = op
+            while len(_OP_CACHE) > OP_CACHE_SIZE:
+                _OP_CACHE.popitem(last=False)
+    return op
+
+
+def _build_sketch(spec: SketchSpec, m: int) -> SketchOperator:
     if spec.kind == "identity":
         return SketchOperator(kind="identity", source_dim=m, target_dim=m)
     d = spec.embed_dim
@@ -216,7 +249,7 @@ def _aligned(t, ld: int, cols: int):
 
 def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     """SA (d x n column-major tensor) and Sb (d) or None, all on device."""
-    ent, tasks, ntask = op.device_plan()
+    lanes, off, mx = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A, lda = _aligned(A, lda, n)
     if b is not None and b.data_ptr() % 16:
@@ -224,22 +257,22 @@ def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     SA = device_f64((d, n), fortran=True)
     Sb = device_f64((d,)) if b is not None else None
     _native.call("skl_countsketch_dense", _native.ptr(A), m, n, lda, _native.ptr(b),
-                 _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask), d, PLAN_CHUNK,
-                 plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), 0, 0, current_stream())
+                 _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK, plan_warps(d),
+                 _native.ptr(SA), d, _native.ptr(Sb), 0, 0, current_stream())
     return SA, Sb
 
 
 def _countsketch_dense_host(op: SketchOperator, A: np.ndarray, n: int,
                             b: np.ndarray | None = None):
     """Host buffers in, host SA/Sb out; H2D streamed under the kernel."""
-    ent, tasks, ntask = op.device_plan()
+    lanes, off, mx = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A = np.asfortranarray(A)
     SA = np.empty((d, n), dtype=np.float64, order="F")
     Sb = np.empty(d, dtype=np.float64) if b is not None else None
     _native.call("skl_countsketch_dense_host", _native.ptr(A), m, n, A.shape[0] if A.ndim == 2
-                 else m, _native.ptr(b), _native.ptr(ent), _native.ptr(tasks), _native.ptr(ntask),
-                 d, PLAN_CHUNK, plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), None, 0, None,
+                 else m, _native.ptr(b), _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK,
+                 plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), None, 0, None,
                  current_stream())
     return SA, Sb
 

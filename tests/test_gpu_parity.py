@@ -225,13 +225,13 @@ def test_host_streaming_abi_bitwise(golden, golden_meta):
     c, _, A, b, ref = live_case("cfg1", golden_meta)
     A = np.asfortranarray(A)
     op = saa_op(c, "countsketch")
-    ent, tasks, ntask = op.device_plan()
+    lanes, coff, mx = op.device_plan()
     SA = np.empty((c.d, c.n), order="F")
     Sb = np.empty(c.d)
     from paper_2409_14309_b200.sketch import PLAN_CHUNK, plan_warps
 
     _native.call("skl_countsketch_dense_host", A.ctypes.data, c.m, c.n, c.m, b.ctypes.data,
-                 ent.data_ptr(), tasks.data_ptr(), ntask.data_ptr(), c.d, PLAN_CHUNK,
+                 lanes.data_ptr(), coff.data_ptr(), mx, c.d, PLAN_CHUNK,
                  plan_warps(c.d), SA.ctypes.data, c.d,
                  Sb.ctypes.data, None, 0, None, torch.cuda.current_stream().cuda_stream)
     assert np.array_equal(SA, golden["cfg1_SA"]) and np.array_equal(Sb, ref["Sb"])

@@ -106,44 +106,92 @@ def test_srht_draws_match_numpy(m_pad, d):
     assert np.array_equal(sample, want_sample)
 
 
+def _simulate_plan(lanes, off, d, chunk, warps, m, A):
+    """Execute the lane lists exactly as countsketch_dense_kernel does
+    (per warp: 32 lanes holding (bucket, running sum), write back / reload on
+    a bucket change, stores before loads within a step)."""
+    head = (warps + 1 + 3) // 4 * 4
+    acc = np.zeros(d + 1)
+    cur = np.full((warps, 32), d)
+    a = np.zeros((warps, 32))
+    for k in range(len(off) - 1):
+        blk = lanes[off[k]: off[k + 1]].astype(np.int64)
+        wrow = blk[: warps + 1]
+        words = blk[head:].reshape(-1, 32)
+        r0 = k * chunk
+        stage = np.zeros(chunk + 1)
+        seg = A[r0: r0 + chunk]
+        stage[: len(seg)] = seg
+        for w in range(warps):
+            for row in words[wrow[w]: wrow[w + 1]]:
+                j = (row & 0x7FFF) // 8
+                x = stage[j] * np.where(row >> 31, -1.0, 1.0)
+                b = (row >> 16) & 0x7FFF
+                sw = b != cur[w]
+                acc[cur[w][sw]] = a[w][sw]          # write back (distinct buckets)
+                cur[w][sw] = b[sw]
+                a[w][sw] = acc[b[sw]]
+                a[w] = a[w] + x
+    for w in range(warps):
+        for l in range(32):
+            acc[cur[w][l]] = a[w][l]
+    return acc[:d]
+
+
 @pytest.mark.parametrize("m,d,chunk,warps", [(1, 1, 8, 8), (100, 4, 8, 4), (20_000, 800, 2048, 8),
-                                             (65_537, 2048, 2048, 16), (10_000, 8192, 8192, 16),
-                                             (9_000, 3, 1024, 8)])
-def test_countsketch_plan_structure(m, d, chunk, warps):
+                                             (65_537, 2048, 2048, 16), (10_000, 8192, 4088, 16),
+                                             (9_000, 3, 1024, 8), (200_000, 2048, 2048, 16)])
+def test_countsketch_plan_structure_and_semantics(m, d, chunk, warps):
     key = O.derive_seed(1, "countsketch", m)
     rows, signs = _native.rng_countsketch(key, m, d)
-    ent, tasks, ntask = _native.countsketch_plan(rows, signs, d, chunk, warps)
-    stride = int(_native.lib().skl_countsketch_plan_stride(d, warps))
+    lanes, off, mx = _native.countsketch_plan(rows, signs, d, chunk, warps)
     head = (warps + 1 + 3) // 4 * 4
+    gsize = -(-d // warps)
     nch = (m + chunk - 1) // chunk
-    for k in range(nch):
+    assert off[0] == 0 and len(off) == nch + 1 and mx == int(np.diff(off).max())
+    for k in range(0, nch, max(1, nch // 7)):
         r0 = k * chunk
         length = min(chunk, m - r0)
-        nt = int(ntask[k])
-        blk = tasks[k * stride: (k + 1) * stride].astype(np.int64)
-        wofs = blk[: warps + 1]
-        tk = blk[head: head + nt]
-        bkt, start = tk >> 16, tk & 0xFFFF
-        ends = np.append(start[1:], length)
-        cnts = ends - start
-        want_cnt = np.bincount(rows[r0: r0 + length], minlength=d)
-        assert nt == np.count_nonzero(want_cnt) and wofs[0] == 0 and wofs[-1] == nt
-        assert start[0] == 0 and np.all(cnts >= 1)
-        assert np.array_equal(cnts, want_cnt[bkt])          # task = one whole bucket
+        blk = lanes[off[k]: off[k + 1]].astype(np.int64)
+        wrow = blk[: warps + 1]
+        words = blk[head:]
+        assert len(words) == 32 * wrow[warps] and wrow[0] == 0 and np.all(np.diff(wrow) >= 0)
+        seen = np.zeros(length, dtype=int)
         for w in range(warps):
-            g = slice(wofs[w], wofs[w + 1])
-            assert np.all(bkt[g] // -(-d // warps) == w)     # bucket stays in its warp
-            assert np.all(np.diff(cnts[g]) <= 0)             # longest first
-            ties = np.diff(cnts[g]) == 0
-            assert np.all(np.diff(bkt[g])[ties] > 0)         # ties by bucket id
-        e = ent[r0: r0 + length].astype(np.int64)
-        local, neg = e >> 3, (e & 1).astype(bool)
-        assert np.array_equal(np.sort(local), np.arange(length))
-        owner = np.repeat(bkt, cnts)
-        assert np.array_equal(rows[r0 + local], owner)
-        assert np.array_equal(neg, signs[r0 + local] < 0)
-        same = owner[1:] == owner[:-1]
-        assert np.all(np.diff(local)[same] > 0)             # ascending rows per task
+            sub = words[32 * wrow[w]: 32 * wrow[w + 1]].reshape(-1, 32)
+            owner = {}
+            for lane in range(32):
+                lst = sub[:, lane]
+                real = (lst & 0x7FFF) != 8 * chunk
+                j = (lst[real] & 0x7FFF) // 8
+                bkt = (lst[real] >> 16) & 0x7FFF
+                neg = (lst[real] >> 31) & 1
+                seen[j] += 1
+                assert np.all(rows[r0 + j] == bkt)            # entry -> its bucket
+                assert np.all(bkt // gsize == w)              # bucket stays in its warp
+                assert np.array_equal(neg.astype(bool), signs[r0 + j] < 0)
+                for b in np.unique(bkt):
+                    pos = np.flatnonzero(bkt == b)
+                    assert np.all(np.diff(pos) == 1)          # one contiguous run ...
+                    assert np.all(np.diff(j[pos]) > 0)        # ... in ascending rows
+                    assert owner.setdefault(int(b), lane) == lane
+                pads = (lst[~real] >> 16) & 0x7FFF
+                assert np.all(pads <= d)
+        assert np.all(seen == 1)                              # every row exactly once
+    # executing the lists reproduces the reference fold bitwise
+    if m <= 200_000:
+        A = np.random.default_rng(m).standard_normal(m)
+        got = _simulate_plan(lanes, off, d, chunk, warps, m, A)
+        want = O.countsketch_fold(rows.astype(np.int64), signs.astype(np.float64), d, A)
+        assert np.array_equal(got, want)
+
+
+def test_plan_is_thread_count_invariant():
+    m, d = 300_000, 2048
+    rows, signs = _native.rng_countsketch(O.derive_seed(4, "countsketch", m), m, d)
+    l1, o1, _ = _native.countsketch_plan(rows, signs, d, 2048, 16, threads=1)
+    l8, o8, _ = _native.countsketch_plan(rows, signs, d, 2048, 16, threads=7)
+    assert np.array_equal(o1, o8) and np.array_equal(l1, l8)
 
 
 def test_bucket_lists_are_the_csr_of_s():
@@ -161,7 +209,7 @@ def test_plan_rejects_out_of_range_bucket():
     with pytest.raises(ValueError):
         _native.countsketch_plan(rows, signs, 4, 8, 8)
     with pytest.raises(Exception):
-        _native.countsketch_plan(rows, signs, 70_000, 8, 8)  # d > 65536
+        _native.countsketch_plan(rows, signs, 40_000, 8, 8)  # d > 32767
 
 
 def test_gaussian_host_generator_matches_numpy():
