@@ -14,10 +14,12 @@
 // (n+1)-th trailing column; Q itself is only formed when requested
 // (economy_qr), by backward accumulation of the reflectors into I.
 //
-// Execution: one persistent cooperative kernel; step k is split across all
-// CTAs (each owns trailing columns round-robin) with one grid barrier per
-// step.  The CTA that updates column k+1 also computes its norm and
-// publishes (alpha, ||x||) so the next step starts without a reduction.
+// Execution: the blocked factorisation in skl_qr_blocked.cu (cluster panel
+// + GEMM-shaped trailing updates) for n >= 384 when a panel fits a
+// thread-block cluster (d <= 10880); otherwise this file's unblocked fallback: one
+// persistent cooperative kernel, step k split across all CTAs (each owns
+// trailing columns round-robin) with one grid barrier per step, the CTA that
+// updates column k+1 publishing its norm for the next step.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -186,6 +188,53 @@ __global__ void __launch_bounds__(1024) qr_backsolve_kernel(const double* M, int
   }
 }
 
+// Blocked back substitution for large n: 32 x 32 diagonal blocks solved by
+// one warp (x_j broadcast by shuffles), the rows above updated by the whole
+// CTA with one 32-term dot product per row.  R = sign-normalised upper
+// triangle of the factored M (ld ldm).
+__global__ void __launch_bounds__(1024) qr_backsolve_blocked_kernel(const double* M, int64_t ldm,
+                                                                    int64_t n, const double* beta,
+                                                                    const double* y_in, double* x) {
+  extern __shared__ double ys[];
+  __shared__ double xb[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t i = tid; i < n; i += blockDim.x) ys[i] = y_in[i];
+  __syncthreads();
+  for (int64_t hi = n; hi > 0; hi -= 32) {
+    const int64_t lo = hi > 32 ? hi - 32 : 0;
+    const int w = (int)(hi - lo);
+    if (warp == 0) {
+      // lane r holds row lo + r of the diagonal block
+      const int64_t row = lo + lane;
+      const double sgr = (lane < w && beta[row] < 0.0) ? -1.0 : 1.0;
+      double yr = lane < w ? ys[row] : 0.0;
+      double xr = 0.0;
+      for (int j = w - 1; j >= 0; --j) {
+        const int64_t col = lo + j;
+        double rij = 0.0;
+        if (lane < j) rij = sgr * M[col * ldm + row];
+        const double rjj = fabs(beta[col]);
+        const double yj = __shfl_sync(0xffffffffu, yr, j);
+        const double xj = yj / rjj;
+        if (lane == j) xr = xj;
+        if (lane < j) yr -= xj * rij;
+      }
+      if (lane < w) {
+        x[lo + lane] = xr;
+        xb[lane] = xr;
+      }
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < lo; i += blockDim.x) {
+      const double sgi = beta[i] < 0.0 ? -1.0 : 1.0;
+      double t = 0.0;
+      for (int j = 0; j < w; ++j) t = fma(sgi * M[(lo + j) * ldm + i], xb[j], t);
+      ys[i] -= t;
+    }
+    __syncthreads();
+  }
+}
+
 // Q = H_0 H_1 ... H_{n-1} [I; 0] by backward accumulation (dorg2r), one
 // cooperative kernel, then column sign normalisation.
 __global__ void __launch_bounds__(QR_NT) qr_form_q_kernel(const double* V, int64_t d, int64_t n,
@@ -222,7 +271,7 @@ __global__ void __launch_bounds__(QR_NT) qr_form_q_kernel(const double* V, int64
 }
 
 __global__ void copy_aug_kernel(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
-                                int64_t n, double* M, double* fro_part) {
+                                int64_t n, double* M, int64_t ldm, double* fro_part) {
   // M[:, :n] = SA, M[:, n] = Sb; per-block partial of ||SA||_F^2
   __shared__ double red[33];
   double s = 0.0;
@@ -237,7 +286,7 @@ __global__ void copy_aug_kernel(const double* SA, int64_t ldsa, const double* Sb
     } else {
       v = Sb ? Sb[i] : 0.0;
     }
-    M[idx] = v;
+    M[c * ldm + i] = v;
   }
   s = block_sum(s, red);
   if (threadIdx.x == 0) fro_part[blockIdx.x] = s;
@@ -250,6 +299,36 @@ __global__ void sum_parts_kernel(const double* part, int nparts, double* out) {
   s = block_sum(s, red);
   if (threadIdx.x == 0) *out = s;
 }
+
+// Q workspace = [I; 0]
+__global__ void eye_kernel(double* Q, int64_t ldq, int64_t d, int64_t n) {
+  const int64_t total = d * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / d, i = idx % d;
+    Q[c * ldq + i] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
+// Q_out = Qw with columns of negative beta negated (diag(R) >= 0 convention)
+__global__ void q_signfix_copy_kernel(const double* Qw, int64_t ldw, const double* beta, int64_t d,
+                                      int64_t n, double* Q, int64_t ldq) {
+  const int64_t total = d * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / d, i = idx % d;
+    const double v = Qw[c * ldw + i];
+    Q[c * ldq + i] = beta[c] < 0.0 ? -v : v;
+  }
+}
+
+bool qr_blocked_supported(int64_t d);
+int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau, double* beta,
+                      double* V, double* Tall, double* W, double* W2, double* part,
+                      int64_t part_cap, cudaStream_t st);
+int qr_blocked_form_q(double* Q, int64_t ldq, int64_t d, int64_t n, const double* V, int64_t ldv,
+                      const double* Tall, double* W, double* W2, double* part, int64_t part_cap,
+                      cudaStream_t st);
 
 }  // namespace skl
 
@@ -268,16 +347,27 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   SKL_REQUIRE(n <= (48 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
 
   const int fro_blocks = 256;
-  // workspace: M, tau, beta, colinfo, y, fro parts, fro2, bad (int64), badval
+  // the cluster-panel factorisation wins from n ~ 384 columns on (panel
+  // steps are latency-bound); narrower systems use the unblocked kernel
+  const bool blocked = n >= 384 && qr_blocked_supported(d);
+  const int64_t ldm = blocked ? (d + 1) / 2 * 2 : d;
+  const int64_t npan = (n + 31) / 32;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off += (bytes + 255) / 256 * 256;
     return o;
   };
-  const size_t oM = take((size_t)d * (n + 1) * 8), oTau = take(n * 8), oBeta = take(n * 8),
+  const size_t oM = take((size_t)ldm * (n + 1) * 8), oTau = take(n * 8), oBeta = take(n * 8),
                oInfo = take(2 * (n + 1) * 8), oY = take(n * 8), oPart = take(fro_blocks * 8),
-               oFro = take(8), oBad = take(8), oBadV = take(8), oX = take(n * 8);
+               oFro = take(8), oBad = take(8), oBadV = take(8), oX = take(n * 8),
+               oV = blocked ? take((size_t)ldm * n * 8) : 0,
+               oT = blocked ? take((size_t)npan * 32 * 32 * 8) : 0,
+               oW = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
+               oW2 = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
+               oQ = (blocked && Q) ? take((size_t)ldm * n * 8) : 0;
+  const int64_t part_cap = blocked ? 32 * (n + 1) * 320 : 0;  // up to 320 row splits
+  const size_t oP = blocked ? take((size_t)part_cap * 8) : 0;
   unsigned char* ws = nullptr;
   SKL_CUDA(cudaMallocAsync(&ws, off, st));
   double* M = (double*)(ws + oM);
@@ -293,34 +383,57 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
 
   int rc = SKL_OK;
   do {
-    copy_aug_kernel<<<fro_blocks, 256, 0, st>>>(SA, ldsa, Sb, d, n, M, part);
+    copy_aug_kernel<<<fro_blocks, 256, 0, st>>>(SA, ldsa, Sb, d, n, M, ldm, part);
     sum_parts_kernel<<<1, 256, 0, st>>>(part, fro_blocks, fro2);
-    int dev = 0, sms = 148, per_sm = 1;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_householder_kernel, QR_NT, 0);
-    int grid = (int)std::min<int64_t>((int64_t)sms * std::max(1, per_sm), n + 1);
-    QrParams p{M, d, n, tau, beta, info};
-    void* args[] = {&p};
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)qr_householder_kernel, grid, QR_NT, args, 0, st);
-    if (e != cudaSuccess) {
-      set_error("qr kernel launch failed: %s", cudaGetErrorString(e));
-      rc = SKL_ERR_CUDA;
-      break;
-    }
-    qr_finish_kernel<<<1, 256, 0, st>>>(M, d, n, beta, fro2, R, ldr, y, badc, badv);
-    qr_backsolve_kernel<<<1, 1024, n * sizeof(double), st>>>(M, d, n, beta, y, xd);
-    if (Q) {
-      qr_scale_reflectors<<<(int)std::min<int64_t>(n, 1024), 256, 0, st>>>(M, d, n, tau, beta);
-      int gq = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gq, qr_form_q_kernel, QR_NT, 0);
-      int gridq = (int)std::min<int64_t>((int64_t)sms * std::max(1, gq), n);
-      void* qargs[] = {&M, &d, &n, &tau, &beta, &Q, &ldq};
-      e = cudaLaunchCooperativeKernel((void*)qr_form_q_kernel, gridq, QR_NT, qargs, 0, st);
+    cudaError_t e = cudaSuccess;
+    if (blocked) {
+      double* V = (double*)(ws + oV);
+      double* T = (double*)(ws + oT);
+      double* W = (double*)(ws + oW);
+      double* W2 = (double*)(ws + oW2);
+      double* Pw = (double*)(ws + oP);
+      rc = qr_blocked_factor(M, ldm, d, n, tau, beta, V, T, W, W2, Pw, part_cap, st);
+      if (rc) break;
+      qr_finish_kernel<<<1, 256, 0, st>>>(M, ldm, n, beta, fro2, R, ldr, y, badc, badv);
+      qr_backsolve_blocked_kernel<<<1, 1024, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
+      if (Q) {
+        double* Qw = (double*)(ws + oQ);
+        const int64_t tot = d * n;
+        const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 8LL * sms);
+        eye_kernel<<<blocks, 256, 0, st>>>(Qw, ldm, d, n);
+        rc = qr_blocked_form_q(Qw, ldm, d, n, V, ldm, T, W, W2, Pw, part_cap, st);
+        if (rc) break;
+        q_signfix_copy_kernel<<<blocks, 256, 0, st>>>(Qw, ldm, beta, d, n, Q, ldq);
+      }
+    } else {
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_householder_kernel, QR_NT, 0);
+      int grid = (int)std::min<int64_t>((int64_t)sms * std::max(1, per_sm), n + 1);
+      QrParams p{M, d, n, tau, beta, info};
+      void* args[] = {&p};
+      e = cudaLaunchCooperativeKernel((void*)qr_householder_kernel, grid, QR_NT, args, 0, st);
       if (e != cudaSuccess) {
-        set_error("form-Q kernel launch failed: %s", cudaGetErrorString(e));
+        set_error("qr kernel launch failed: %s", cudaGetErrorString(e));
         rc = SKL_ERR_CUDA;
         break;
+      }
+      qr_finish_kernel<<<1, 256, 0, st>>>(M, d, n, beta, fro2, R, ldr, y, badc, badv);
+      qr_backsolve_kernel<<<1, 1024, n * sizeof(double), st>>>(M, d, n, beta, y, xd);
+      if (Q) {
+        qr_scale_reflectors<<<(int)std::min<int64_t>(n, 1024), 256, 0, st>>>(M, d, n, tau, beta);
+        int gq = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gq, qr_form_q_kernel, QR_NT, 0);
+        int gridq = (int)std::min<int64_t>((int64_t)sms * std::max(1, gq), n);
+        void* qargs[] = {&M, &d, &n, &tau, &beta, &Q, &ldq};
+        e = cudaLaunchCooperativeKernel((void*)qr_form_q_kernel, gridq, QR_NT, qargs, 0, st);
+        if (e != cudaSuccess) {
+          set_error("form-Q kernel launch failed: %s", cudaGetErrorString(e));
+          rc = SKL_ERR_CUDA;
+          break;
+        }
       }
     }
     e = cudaGetLastError();

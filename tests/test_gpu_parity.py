@@ -361,3 +361,25 @@ def test_saa_gaussian_cfg3_reduced(golden, golden_meta):
     assert rel_fro(res.x.data, ref["x"]) <= 1e-9
     assert abs(res.residual_norm - ref["residual"]) <= 1e-10 * ref["residual"]
     assert rel_fro(res.x.data, golden["cfg3r_x"]) <= 1e-9
+
+
+# ------------------------------------------------------------ reduced solve
+@pytest.mark.parametrize("d,n", [(64, 31), (64, 33), (300, 100), (2048, 256), (1500, 400),
+                                 (2048, 513), (8192, 1024), (12_000, 64), (20_000, 40)])
+def test_qr_solve_matches_lapack(d, n):
+    rng = np.random.default_rng(d + n)
+    M = rng.standard_normal((d, n)) @ np.diag(np.logspace(0, -6, n))
+    y = rng.standard_normal(d)
+    from paper_2409_14309_b200.linalg import qr_solve_device
+
+    Md = torch.from_numpy(np.asfortranarray(M)).cuda()
+    yd = torch.from_numpy(y).cuda()
+    x, R, Q = qr_solve_device(Md, d, yd, d, n, want_q=True, want_r=True)
+    R, Q, x = R.cpu().numpy(), Q.cpu().numpy(), x.cpu().numpy()
+    q_ref, r_ref = O.economy_qr(M)
+    assert np.all(np.diagonal(R) >= 0) and np.array_equal(np.tril(R, -1), np.zeros((n, n)))
+    assert rel_fro(R, r_ref) <= 1e-12
+    assert np.abs(Q.T @ Q - np.eye(n)).max() <= 1e-12
+    assert rel_fro(Q @ R, M) <= 1e-13
+    x_ref = np.linalg.lstsq(M, y, rcond=None)[0]
+    assert rel_fro(x, x_ref) <= 1e-8

@@ -1,0 +1,25 @@
+"""Profiling driver for the reduced solve: QR + back-solve of a d x n
+sketched system (default: config 4's 8192 x 1024, and config 2's 2048 x 256)."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2409_14309_b200.linalg import qr_solve_device  # noqa: E402
+
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+M = torch.randn((n, d), dtype=torch.float64, device="cuda").t()
+y = torch.randn((d,), dtype=torch.float64, device="cuda")
+for _ in range(reps):
+    qr_solve_device(M, d, y, d, n)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+qr_solve_device(M, d, y, d, n)
+e.record()
+torch.cuda.synchronize()
+print(f"qr_solve {d}x{n}: {s.elapsed_time(e):.3f} ms")
