@@ -154,12 +154,25 @@ int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices, const dou
                         int64_t ldsa, void* stream);
 
 /* SRHT: out = (P H D [A; 0]) / sqrt(d) for dense column-major A (device),
- * H the unnormalised Sylvester-Hadamard of order m_pad.  signs (+-1 int8,
- * m_pad) and row_sample (int64, d) are device arrays.  Replaces
- * sketch.py:213-223 and fwht_inplace sketch.py:152-177. */
-int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda, const int8_t* signs,
+ * H the unnormalised Sylvester-Hadamard of order m_pad.  sign_bits are the
+ * +-1 sign diagonal packed by skl_srht_pack_signs (device copy);
+ * row_sample (int64, d) is device.  Replaces sketch.py:213-223 and
+ * fwht_inplace sketch.py:152-177. */
+int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda, const uint16_t* sign_bits,
                    const int64_t* row_sample, int64_t m_pad, int64_t d, double* SA,
                    int64_t ldsa, void* stream);
+/* Row block [row_offset, row_offset + m_local) of the same apply (row_offset
+ * a multiple of min(m_pad, 4096)); sign_bits of that block; the caller sums
+ * the per-block partials (the multi-GPU reduce). */
+int skl_srht_dense_shard(const double* A, int64_t m_local, int64_t n, int64_t lda,
+                         const uint16_t* sign_bits, const int64_t* row_sample, int64_t m_pad,
+                         int64_t d, int64_t row_offset, double* partial, int64_t ldp,
+                         void* stream);
+/* Sign packing (host): per block of B = min(m_pad, 4096) rows,
+ * skl_srht_sign_words(B) 16-bit words; bit i of word t is the sign of the
+ * i-th element the kernel's first butterfly pass gives task t. */
+int64_t skl_srht_sign_words(int64_t B);
+int skl_srht_pack_signs(const int8_t* signs, int64_t m_pad, uint16_t* packed);
 
 /* In-place unnormalised FWHT of a device column-major m_pad x n array
  * (lda >= m_pad), m_pad a power of two.  Replaces sketch.py:152-177. */

@@ -62,6 +62,8 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_fwht_device": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr]),
+    "skl_srht_sign_words": (c_i64, [c_i64]),
+    "skl_srht_pack_signs": (c_int, [c_ptr, c_i64, c_ptr]),
     "skl_gaussian_set_tables": (c_int, [c_ptr, c_ptr, c_ptr]),
     "skl_rng_gaussian_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_rng_gaussian_host": (c_int, [c_u64, c_i64, c_ptr]),
@@ -210,3 +212,13 @@ def countsketch_buckets(rows: np.ndarray, d: int) -> tuple[np.ndarray, np.ndarra
     bptr = np.empty(d + 1, dtype=np.int64)
     call("skl_countsketch_buckets", ptr(rows), m, d, ptr(brow), ptr(bptr))
     return brow, bptr
+
+
+def srht_pack_signs(signs: np.ndarray) -> np.ndarray:
+    """Packed sign words of an SRHT sign diagonal (int8 +-1, length m_pad)."""
+    m_pad = signs.shape[0]
+    B = min(m_pad, 4096)
+    words = int(lib().skl_srht_sign_words(B)) * (m_pad // B)
+    out = np.zeros(max(words, 8), dtype=np.uint16)
+    call("skl_srht_pack_signs", ptr(np.ascontiguousarray(signs, dtype=np.int8)), m_pad, ptr(out))
+    return out

@@ -33,6 +33,8 @@
 #include "skl_common.h"
 #include "skl_ptx.cuh"
 
+extern "C" int64_t skl_srht_sign_words(int64_t B);
+
 namespace skl {
 
 constexpr int SR_NT = 256;
@@ -46,7 +48,7 @@ struct SrParams {
   int64_t lda;
   int64_t m;          // local rows
   int64_t n;
-  const int8_t* signs;  // local rows' signs (padded to a multiple of 16)
+  const uint16_t* sbits;  // packed signs: per block, one word per first-pass task
   const int64_t* sample;
   int64_t d;
   int b;              // log2 B
@@ -56,25 +58,30 @@ struct SrParams {
   int64_t ldo;
   double* part;       // [P][n][d]
   double inv_scale_div;  // sqrt(d) (division at the end)
+  int sw_block;         // packed sign words per block (multiple of 8)
 };
 
 // One pass of NB butterfly stages at bits [lo, lo+NB).  FIRST reads the
-// natural-layout stage buffer (applying signs and the tail mask) and writes
-// the swizzled work buffer; later passes work in place on `work`.
+// natural-layout stage buffer, applies the signs (bit i of the task's packed
+// word flips element i: an XOR into the sign bit, exact) and the tail mask,
+// and writes the swizzled work buffer; later passes work in place.
 template <int NB, bool FIRST>
 __device__ __forceinline__ void sr_pass(const double* __restrict__ in,
-                                        const int8_t* __restrict__ sg, int len,
+                                        const uint16_t* __restrict__ sw, int len,
                                         double* __restrict__ work, int lo, int B) {
   constexpr int CNT = 1 << NB;
   const int ntask = B >> NB;
   for (int task = threadIdx.x; task < ntask; task += SR_NT) {
     const int base = ((task >> lo) << (lo + NB)) | (task & ((1 << lo) - 1));
+    const uint32_t mask = FIRST ? (uint32_t)sw[task] : 0u;
     double v[CNT];
 #pragma unroll
     for (int i = 0; i < CNT; ++i) {
       const int e = base + (i << lo);
       if (FIRST) {
-        v[i] = e < len ? (sg[e] < 0 ? -in[e] : in[e]) : 0.0;
+        const uint2 w = *reinterpret_cast<const uint2*>(in + e);
+        const double x = __hiloint2double((int)(w.y ^ (((mask >> i) & 1u) << 31)), (int)w.x);
+        v[i] = e < len ? x : 0.0;
       } else {
         v[i] = work[sr_swz(e)];
       }
@@ -96,14 +103,14 @@ __device__ __forceinline__ void sr_pass(const double* __restrict__ in,
 }
 
 template <bool FIRST>
-__device__ __forceinline__ void sr_pass_any(int nb, const double* in, const int8_t* sg, int len,
+__device__ __forceinline__ void sr_pass_any(int nb, const double* in, const uint16_t* sw, int len,
                                             double* work, int lo, int B) {
   switch (nb) {
-    case 0: sr_pass<0, FIRST>(in, sg, len, work, lo, B); break;
-    case 1: sr_pass<1, FIRST>(in, sg, len, work, lo, B); break;
-    case 2: sr_pass<2, FIRST>(in, sg, len, work, lo, B); break;
-    case 3: sr_pass<3, FIRST>(in, sg, len, work, lo, B); break;
-    default: sr_pass<4, FIRST>(in, sg, len, work, lo, B); break;
+    case 0: sr_pass<0, FIRST>(in, sw, len, work, lo, B); break;
+    case 1: sr_pass<1, FIRST>(in, sw, len, work, lo, B); break;
+    case 2: sr_pass<2, FIRST>(in, sw, len, work, lo, B); break;
+    case 3: sr_pass<3, FIRST>(in, sw, len, work, lo, B); break;
+    default: sr_pass<4, FIRST>(in, sw, len, work, lo, B); break;
   }
 }
 
@@ -111,14 +118,16 @@ __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(SR_NT) : "memory");
 }
 
-template <int KPT>
-__global__ void __launch_bounds__(SR_NT + 32) srht_dense_kernel(const SrParams p) {
+// FULL: B = 4096, three passes of 4 stages at bits 8, 4, 0 (compile-time);
+// otherwise the generic pass plan for small m_pad.
+template <int KPT, bool FULL>
+__global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + SR_STAGES;
   const int B = 1 << p.b;
-  const size_t soff = ((size_t)B * 8 + 15) & ~(size_t)15;  // signs offset (16-byte aligned)
-  const size_t stage_bytes = (soff + (size_t)std::max(B, 16) + 127) & ~(size_t)127;
+  const size_t soff = ((size_t)B * 8 + 15) & ~(size_t)15;  // sign words (16-byte aligned)
+  const size_t stage_bytes = (soff + (size_t)p.sw_block * 2 + 127) & ~(size_t)127;
   unsigned char* ring = smem + 128;
   double* work = reinterpret_cast<double*>(ring + SR_STAGES * stage_bytes);
 
@@ -150,28 +159,25 @@ __global__ void __launch_bounds__(SR_NT + 32) srht_dense_kernel(const SrParams p
         const int len_even = len & ~1;
         unsigned char* st = ring + s * stage_bytes;
         double* As = reinterpret_cast<double*>(st);
-        int8_t* Ss = reinterpret_cast<int8_t*>(st + soff);
-        const uint32_t sbytes = (uint32_t)((len + 15) & ~15);
+        uint16_t* Ss = reinterpret_cast<uint16_t*>(st + soff);
+        const uint32_t sbytes = (uint32_t)(p.sw_block * 2);
         if (len & 1) As[len - 1] = __ldg(colp + r0 + len - 1);
         mbar_arrive_expect_tx(&full[s], (uint32_t)(len_even * 8) + sbytes);
         if (len_even) bulk_g2s(As, colp + r0, (uint32_t)(len_even * 8), &full[s], pol_stream);
-        bulk_g2s(Ss, p.signs + r0, sbytes, &full[s], pol_keep);
+        bulk_g2s(Ss, p.sbits + (q0 + it) * (int64_t)p.sw_block, sbytes, &full[s], pol_keep);
       }
     }
     return;
   }
 
-  // sampled rows owned by this thread
+  // sampled rows owned by this thread (row index < m_pad <= 2^32)
   double acc[KPT];
-  int plo[KPT];
-  int64_t phi[KPT];
+  uint32_t ps[KPT];
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     acc[k] = 0.0;
     const int64_t i = (int64_t)k * SR_NT + tid;
-    const int64_t ps = i < p.d ? p.sample[i] : 0;
-    plo[k] = (int)(ps & (B - 1));
-    phi[k] = ps >> p.b;
+    ps[k] = i < p.d ? (uint32_t)p.sample[i] : 0u;
   }
   // pass plan: first pass = highest bit group (natural-layout friendly)
   const int nb_hi = p.b > 8 ? p.b - 8 : 0;
@@ -186,8 +192,10 @@ __global__ void __launch_bounds__(SR_NT + 32) srht_dense_kernel(const SrParams p
     const int len = (int)min((int64_t)B, p.m - r0);
     const unsigned char* st = ring + s * stage_bytes;
     const double* As = reinterpret_cast<const double*>(st);
-    const int8_t* Ss = reinterpret_cast<const int8_t*>(st + soff);
-    if (nb_hi) {
+    const uint16_t* Ss = reinterpret_cast<const uint16_t*>(st + soff);
+    if (FULL) {
+      sr_pass<4, true>(As, Ss, len, work, 8, SR_BMAX);
+    } else if (nb_hi) {
       sr_pass_any<true>(nb_hi, As, Ss, len, work, 8, B);
     } else if (nb_mid) {
       sr_pass_any<true>(nb_mid, As, Ss, len, work, 4, B);
@@ -197,22 +205,25 @@ __global__ void __launch_bounds__(SR_NT + 32) srht_dense_kernel(const SrParams p
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     consumer_bar();
-    if (nb_hi && nb_mid) {
+    if (FULL) {
+      sr_pass<4, false>(nullptr, nullptr, 0, work, 4, SR_BMAX);
+      consumer_bar();
+      sr_pass<4, false>(nullptr, nullptr, 0, work, 0, SR_BMAX);
+      consumer_bar();
+    } else if (nb_hi && nb_mid) {
       sr_pass_any<false>(nb_mid, nullptr, nullptr, 0, work, 4, B);
       consumer_bar();
     }
-    if (nb_hi || nb_mid) {
+    if (!FULL && (nb_hi || nb_mid)) {
       sr_pass_any<false>(nb_lo, nullptr, nullptr, 0, work, 0, B);
       consumer_bar();
     }
-    const int64_t jhi = p.jhi0 + q;
+    const uint32_t jhi = (uint32_t)(p.jhi0 + q);
 #pragma unroll
     for (int k = 0; k < KPT; ++k) {
-      const int64_t i = (int64_t)k * SR_NT + tid;
-      if (i < p.d) {
-        const double y = work[sr_swz(plo[k])];
-        acc[k] += (__popcll(phi[k] & jhi) & 1) ? -y : y;
-      }
+      const uint2 w = *reinterpret_cast<const uint2*>(work + sr_swz((int)(ps[k] & (B - 1))));
+      const uint32_t flip = (uint32_t)(__popc((ps[k] >> p.b) & jhi) & 1) << 31;
+      acc[k] += __hiloint2double((int)(w.y ^ flip), (int)w.x);
     }
     consumer_bar();
   }
@@ -240,33 +251,56 @@ __global__ void srht_reduce_kernel(const double* part, int P, int64_t n, int64_t
   }
 }
 
+// First-pass geometry for a block of B = 2^b rows: (lo bit, stages).
+static void first_pass(int b, int* lo, int* nb) {
+  if (b > 8) {
+    *lo = 8;
+    *nb = b - 8;
+  } else if (b > 4) {
+    *lo = 4;
+    *nb = b - 4;
+  } else {
+    *lo = 0;
+    *nb = b;
+  }
+}
+
+static int block_log2(int64_t m_pad) {
+  int b = 0;
+  while ((1LL << (b + 1)) <= std::min<int64_t>(m_pad, SR_BMAX)) ++b;
+  return b;
+}
+
 template <int KPT>
 static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kern = srht_dense_kernel<KPT>;
+  auto kern = p.b == 12 ? srht_dense_kernel<KPT, true> : srht_dense_kernel<KPT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SR_NT + 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const int8_t* signs,
+int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16_t* sbits,
                 const int64_t* sample, int64_t m_pad, int64_t d, double* SA, int64_t ldsa,
                 int64_t row_offset, int partitions, cudaStream_t st) {
-  SKL_REQUIRE(A && signs && sample && SA && m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d,
+  const int64_t* sample_ = sample;
+  SKL_REQUIRE(A && sbits && sample && SA && m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d,
               SKL_ERR_SHAPE, "srht: bad arguments");
   SKL_REQUIRE(m_pad >= 1 && (m_pad & (m_pad - 1)) == 0, SKL_ERR_SHAPE,
               "srht: padded dimension %lld is not a power of two", (long long)m_pad);
   SKL_REQUIRE(d <= 32 * SR_NT, SKL_ERR_SPEC, "srht: embed_dim %lld > %d not supported",
               (long long)d, 32 * SR_NT);
-  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && ((uintptr_t)signs & 15) == 0,
+  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && ((uintptr_t)sbits & 15) == 0,
               SKL_ERR_INVALID, "srht: A/signs must be 16-byte aligned with an even leading dimension");
-  int b = 0;
-  while ((1LL << (b + 1)) <= std::min<int64_t>(m_pad, SR_BMAX)) ++b;
+  SKL_REQUIRE(m_pad <= 0x100000000LL, SKL_ERR_SPEC, "srht: padded dimension > 2^32");
+  (void)sample_;
+  const int b = block_log2(m_pad);
   const int64_t B = 1LL << b;
   SKL_REQUIRE(row_offset % B == 0, SKL_ERR_INVALID, "srht: row offset not block aligned");
   int kpt = 1;
   while ((int64_t)kpt * SR_NT < d) kpt <<= 1;
-  const size_t stage = ((((size_t)B * 8 + 15) & ~(size_t)15) + (size_t)std::max<int64_t>(B, 16) + 127) & ~(size_t)127;
+  const int sw_block = (int)skl_srht_sign_words(B);
+  const size_t stage = ((((size_t)B * 8 + 15) & ~(size_t)15) + (size_t)sw_block * 2 + 127) & ~(size_t)127;
   const size_t smem = 128 + SR_STAGES * stage + (size_t)B * 8;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -276,7 +310,8 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const int8_t
   if (P <= 0) P = n * 2 >= sms ? 1 : (int)((2 * sms + n - 1) / n);
   P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nblk));
   SrParams p;
-  p.A = A; p.lda = lda; p.m = m; p.n = n; p.signs = signs; p.sample = sample; p.d = d; p.b = b;
+  p.A = A; p.lda = lda; p.m = m; p.n = n; p.sbits = sbits; p.sample = sample; p.d = d; p.b = b;
+  p.sw_block = sw_block;
   p.jhi0 = row_offset >> b; p.P = P; p.out = SA; p.ldo = ldsa; p.part = nullptr;
   p.inv_scale_div = std::sqrt((double)d);
   double* part = nullptr;
@@ -344,15 +379,15 @@ __global__ void fwht_ref_pass_kernel(double* X, int64_t m_pad, int64_t n, int64_
 using namespace skl;
 
 extern "C" int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda,
-                              const int8_t* signs, const int64_t* row_sample, int64_t m_pad,
+                              const uint16_t* sign_bits, const int64_t* row_sample, int64_t m_pad,
                               int64_t d, double* SA, int64_t ldsa, void* stream) {
   clear_error();
-  return srht_launch(A, m, n, lda, signs, row_sample, m_pad, d, SA, ldsa, 0, 0,
+  return srht_launch(A, m, n, lda, sign_bits, row_sample, m_pad, d, SA, ldsa, 0, 0,
                      (cudaStream_t)stream);
 }
 
 extern "C" int skl_srht_dense_shard(const double* A, int64_t m_local, int64_t n, int64_t lda,
-                                    const int8_t* signs_local, const int64_t* row_sample,
+                                    const uint16_t* signs_local, const int64_t* row_sample,
                                     int64_t m_pad, int64_t d, int64_t row_offset, double* partial,
                                     int64_t ldp, void* stream) {
   clear_error();
@@ -380,6 +415,42 @@ extern "C" int skl_fwht_device(double* X, int64_t m_pad, int64_t n, int64_t lda,
       default: fwht_ref_pass_kernel<4><<<blocks, 256, 0, st>>>(X, m_pad, n, lda, lo); break;
     }
     SKL_CUDA_LAUNCH();
+  }
+  return SKL_OK;
+}
+
+// Packed signs for the SRHT kernel (host): per block of B = min(m_pad, 4096)
+// rows, one 16-bit word per first-pass task whose bit i is the sign of that
+// task's element i (1 = negative), padded to a multiple of 8 words.
+extern "C" int64_t skl_srht_sign_words(int64_t B) {
+  int b = 0;
+  while ((1LL << (b + 1)) <= B) ++b;
+  int lo, nb;
+  first_pass(b, &lo, &nb);
+  const int64_t tasks = B >> nb;
+  return (tasks + 7) / 8 * 8;
+}
+
+extern "C" int skl_srht_pack_signs(const int8_t* signs, int64_t m_pad, uint16_t* packed) {
+  clear_error();
+  SKL_REQUIRE(signs && packed && m_pad >= 1 && (m_pad & (m_pad - 1)) == 0, SKL_ERR_INVALID,
+              "srht_pack_signs: bad arguments");
+  const int b = block_log2(m_pad);
+  const int64_t B = 1LL << b;
+  int lo, nb;
+  first_pass(b, &lo, &nb);
+  const int64_t tasks = B >> nb, words = skl_srht_sign_words(B);
+  for (int64_t blk = 0; blk < m_pad / B; ++blk) {
+    uint16_t* w = packed + blk * words;
+    for (int64_t t = 0; t < words; ++t) {
+      uint32_t mask = 0;
+      if (t < tasks) {
+        const int64_t base = ((t >> lo) << (lo + nb)) | (t & ((1LL << lo) - 1));
+        for (int i = 0; i < (1 << nb); ++i)
+          if (signs[blk * B + base + ((int64_t)i << lo)] < 0) mask |= 1u << i;
+      }
+      w[t] = (uint16_t)mask;
+    }
   }
   return SKL_OK;
 }

@@ -156,11 +156,8 @@ class SketchOperator:
         require_cuda()
         c = self._cache()
         if "srht" not in c:
-            # int8 signs, padded so 16-byte bulk copies never run past the end
-            pad = (self.padded_dim + 15) // 16 * 16
-            signs8 = np.ones(max(pad, 16), dtype=np.int8)
-            signs8[: self.padded_dim] = np.where(self.sign_diag > 0, 1, -1)
-            c["srht"] = (to_device(signs8), to_device(self.row_sample))
+            signs8 = np.where(self.sign_diag > 0, 1, -1).astype(np.int8)
+            c["srht"] = (to_device(_native.srht_pack_signs(signs8)), to_device(self.row_sample))
         return c["srht"]
 
     def device_gaussian(self):
