@@ -71,60 +71,66 @@ def profiled_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
 
-    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML is polled from a thread every ~1 ms (nvidia-smi's fastest loop is
+    far slower than a short timed region); samples are kept only between
+    __enter__ and __exit__ (none when NVML is unavailable)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4, "hw_power_brake": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.out = []
+        self.samples = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
+        self.stop_ev = threading.Event()
+        self.th = None
+        self.source = "nvml"
+
+    def _poll(self):
+        import pynvml
+
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.ready.set()
+        while True:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(smax), int(rs)))
+            except Exception:
+                pass
+            if self.stop_ev.wait(0.001):
+                break
 
     def __enter__(self):
+        self.ready = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.th = threading.Thread(target=self._poll, daemon=True)
             self.th.start()
+            self.ready.wait(2.0)
         except Exception:
-            self.proc = None
+            self.th = None
+            self.source = "unavailable"
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.out.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop_ev.set()
+        if self.th is not None:
+            self.th.join(timeout=2)
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.out:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[3:7]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": self.source}
+        reasons = sorted(name for name, bit in self.REASONS.items()
+                         if any(r & bit for _, _, r in self.samples))
+        return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
+                "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml (1 ms poll)"}
 
 
 # ----------------------------------------------------------------- CPU arms
@@ -201,7 +207,7 @@ def run_reference_arm(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2)
@@ -227,7 +233,6 @@ def main():
     from paper_2409_14309_b200 import _native
     from paper_2409_14309_b200.distributed import ShardPlan, local_partial_device, shard_rows
     from paper_2409_14309_b200.rng import derive_seed
-    from paper_2409_14309_b200.sketch import PLAN_CHUNK, plan_warps
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -254,14 +259,14 @@ def main():
     stream = torch.cuda.current_stream()
     ld = (d + 1) // 2 * 2
     out = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda").t()[:d]
-    lanes, coff, mx = plan.device_plan()
-    pw = plan_warps(d)
+    cs_plan = plan.device_plan()
+
+    def apply():
+        cs_plan.apply(A, m_loc, n, lda, b, out, ld, out[:, n], partitions=1,
+                      stream=stream.cuda_stream)
 
     def step():
-        _native.call("skl_countsketch_dense", A.data_ptr(), m_loc, n, lda, b.data_ptr(),
-                     lanes.data_ptr(), coff.data_ptr(), mx, d, PLAN_CHUNK, pw,
-                     out.data_ptr(), ld,
-                     out[:, n].data_ptr(), 1, 0, stream.cuda_stream)
+        apply()
         if world > 1:
             dist.reduce(out, dst=0)
 
@@ -280,10 +285,7 @@ def main():
         start.record(stream)
         for i in range(args.steps):
             k_ev[i][0].record(stream)
-            _native.call("skl_countsketch_dense", A.data_ptr(), m_loc, n, lda, b.data_ptr(),
-                         lanes.data_ptr(), coff.data_ptr(), mx, d, PLAN_CHUNK, pw,
-                         out.data_ptr(), ld,
-                         out[:, n].data_ptr(), 1, 0, stream.cuda_stream)
+            apply()
             k_ev[i][1].record(stream)
             if world > 1:
                 dist.reduce(out, dst=0)
@@ -363,10 +365,7 @@ def main():
         Sbh = np.empty(d)
 
         def e2e_call():
-            _native.call("skl_countsketch_dense_host", Ah.ctypes.data, m_loc, n, m_loc,
-                         bh.ctypes.data, lanes.data_ptr(), coff.data_ptr(), mx, d,
-                         PLAN_CHUNK, pw,
-                         SAh.ctypes.data, d, Sbh.ctypes.data, None, 0, None, stream.cuda_stream)
+            cs_plan.apply_host(Ah, m_loc, n, m_loc, bh, SAh, d, Sbh, stream=stream.cuda_stream)
 
         e2e_call()
         reps = 3
@@ -379,7 +378,8 @@ def main():
         e2e = {"value": round(bytes_local / te / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": bytes_local, "d2h_bytes_per_step": 8 * d * (n + 1),
                "ms_per_step": round(te * 1e3, 3),
-               "path": "skl_countsketch_dense_host (pinned host A,b -> host SA,Sb)"}
+               "path": f"{'skl_countsketch_dense_owned_host' if cs_plan.kind == 'owned' else 'skl_countsketch_dense_host'}"
+                       " (pinned host A,b -> host SA,Sb)"}
         if world == 1:
             # parity of the timed output against the device run (bitwise)
             assert np.array_equal(SAh, out[:, :n].cpu().numpy())
@@ -410,7 +410,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": profiled_traffic(), "peak_source": peak_src,
-                         "kernel": "countsketch_dense_kernel<512,1>",
+                         "kernel": (f"countsketch_owned_kernel<{32 * cs_plan.warps}>" if cs_plan.kind == "owned"
+                           else f"countsketch_dense_kernel<{32 * cs_plan.warps},1>"),
                          "kernel_ms": round(kern_avg, 4),
                          "algorithmic_bytes_per_launch": bytes_local,
                          "frac_of_8TBps": round(achieved / 8000.0, 4)},

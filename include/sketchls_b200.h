@@ -126,6 +126,27 @@ int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, co
                           int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                           double* Sb, int partitions, int accumulate, void* stream);
 
+/* Register-owned plan for d <= 128 * warps (the common case): bucket b is
+ * held for the whole apply in a register of consumer thread b % (32*warps),
+ * slot b / (32*warps).  Per chunk, each lane's list is the union of its four
+ * buckets' rows (ascending inside a bucket, the four streams interleaved to
+ * spread shared-memory banks), padded to the longest lane.  Block (u16
+ * words) at lanes[chunk_off[k]]: H = round8(warps+1) words of per-warp first
+ * list rows (index `warps` = total), then rows of 32 words: bits 0..12 row
+ * in the chunk (chunk = zero slot), bits 13..14 slot, bit 15 negative sign.
+ * Call with lanes == NULL first to get chunk_off, as for the lane lists.
+ * Limits: chunk a multiple of 8 in [8, 8184]. */
+int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
+                               int64_t chunk, int warps, uint16_t* lanes, int64_t* chunk_off,
+                               int threads);
+/* S*A, S*b with a register-owned plan (warps 8 or 16); otherwise as
+ * skl_countsketch_dense (bitwise-equal to the reference for partitions 1). */
+int skl_countsketch_dense_owned(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* b, const uint16_t* lanes, const int64_t* chunk_off,
+                                int64_t max_block, int64_t d, int64_t chunk, int warps, double* SA,
+                                int64_t ldsa, double* Sb, int partitions, int accumulate,
+                                void* stream);
+
 /* Same apply with HOST A/b/SA/Sb: streams row blocks of A through the
  * device with host-to-device copies overlapped with the kernel; if
  * A_dev_keep != NULL the device copy of A (ld = m rounded up to 32) is
@@ -136,6 +157,13 @@ int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64
                                int64_t chunk, int warps, double* SA_host, int64_t ldsa, double* Sb_host,
                                double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                void* stream);
+/* skl_countsketch_dense_host with a register-owned plan. */
+int skl_countsketch_dense_owned_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
+                                     const double* b_host, const uint16_t* lanes,
+                                     const int64_t* chunk_off, int64_t max_block, int64_t d,
+                                     int64_t chunk, int warps, double* SA_host, int64_t ldsa,
+                                     double* Sb_host, double* A_dev_keep, int64_t ld_keep,
+                                     double* b_dev_keep, void* stream);
 
 /* Bucket-sorted source rows of a CountSketch (host): bucket_rows[bucket_ptr[i]
  * .. bucket_ptr[i+1]) are the rows j with rows[j] == i, ascending -- the CSR

@@ -51,7 +51,19 @@ SIGNATURES: dict[str, tuple] = {
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_int, c_int, c_ptr],
     ),
+    "skl_countsketch_plan_owned": (
+        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_int]),
+    "skl_countsketch_dense_owned": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
+         c_i64, c_ptr, c_int, c_int, c_ptr],
+    ),
     "skl_countsketch_dense_host": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
+         c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    ),
+    "skl_countsketch_dense_owned_host": (
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
@@ -187,9 +199,25 @@ def rng_srht(key: int, m_pad: int, d: int, threads: int = 0) -> tuple[np.ndarray
     return signs, sample
 
 
-def plan_geometry(d: int) -> tuple[int, int]:
-    """(chunk rows, consumer warps) of the CountSketch plan for embed_dim d."""
-    return 2048, (16 if d >= 1024 else 8)
+# Register-owned plans cover d <= 128 * 16; larger embeddings use lane lists.
+OWNED_MAX_D = 2048
+OWNED_CHUNK = 8184   # rows per chunk (<= 8184: 13-bit row field incl. the zero slot)
+LANES_CHUNK = 2048
+
+
+def plan_geometry(d: int, kind: str | None = None) -> tuple[str, int, int]:
+    """(plan kind, chunk rows, consumer warps) of the CountSketch plan for
+    embed_dim d: "owned" (register-owned buckets) when d <= 2048, else
+    "lanes" (shared-memory accumulators, lane lists).  ``kind`` forces one
+    (tests exercise both kernels on the same operator)."""
+    kind = kind or ("owned" if d <= OWNED_MAX_D else "lanes")
+    if kind == "owned":
+        if d > OWNED_MAX_D:
+            raise ValueError(f"owned plan needs d <= {OWNED_MAX_D}, got {d}")
+        return "owned", OWNED_CHUNK, (8 if d <= 1024 else 16)
+    if kind != "lanes":
+        raise ValueError(f"unknown plan kind {kind!r}")
+    return "lanes", LANES_CHUNK, (16 if d >= 1024 else 8)
 
 
 def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
@@ -203,6 +231,20 @@ def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, wa
     lanes = np.empty(int(off[-1]), dtype=np.uint32)
     call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(lanes), ptr(off),
          threads)
+    return lanes, off, int(np.diff(off).max())
+
+
+def countsketch_plan_owned(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
+                           threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
+    """(lanes u16, chunk_off i64 [nch+1], max block words) of the register-owned plan."""
+    m = rows.shape[0]
+    nch = (m + chunk - 1) // chunk
+    off = np.zeros(nch + 1, dtype=np.int64)
+    call("skl_countsketch_plan_owned", ptr(rows), ptr(signs), m, d, chunk, warps, None, ptr(off),
+         threads)
+    lanes = np.empty(int(off[-1]), dtype=np.uint16)
+    call("skl_countsketch_plan_owned", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(lanes),
+         ptr(off), threads)
     return lanes, off, int(np.diff(off).max())
 
 

@@ -27,6 +27,7 @@
 // With P > 1 row partitions (few columns, long input), partial sums go to a
 // workspace and are reduced in fixed partition order (deterministic, not
 // bitwise).
+#include <cstdlib>
 #include <algorithm>
 #include <vector>
 
@@ -212,6 +213,148 @@ __global__ void __launch_bounds__(NT + 32, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-owned variant (d <= 128 * warps): bucket b lives for the whole
+// apply in a register of lane (b/4) % 32 of warp b/128 (slot b % 4), so no
+// accumulator ever touches shared memory; per chunk each lane walks the
+// union of its four buckets' rows (skl_countsketch_plan_owned), one masked
+// gather + XOR + predicated add per entry.  Same fold order per bucket ->
+// bitwise-equal to the reference.
+constexpr int OW_MAX_STAGES = 6;  // ring depth: as many as fit in shared memory
+
+struct OwParams {
+  const double* A;
+  int64_t lda;
+  const double* b;
+  int64_t n, ncols;
+  int64_t row_begin, row_end;
+  const uint16_t* lanes;
+  const int64_t* chunk_off;
+  int max_block;  // u16 words
+  int d, T, head, P, stages;
+  double* out;
+  int64_t ldo;
+  double* outb;
+  double* part;
+  int accumulate;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + OW_MAX_STAGES;
+  const int NS = p.stages;
+  const int T = p.T;
+  unsigned char* ring = smem + 128;
+  const size_t a_bytes = (size_t)(T + 2) * sizeof(double);
+  const size_t stage_bytes = (a_bytes + (size_t)p.max_block * 2 + 127) & ~(size_t)127;
+  const int tid = threadIdx.x;
+  const int64_t col = blockIdx.x;
+  const double* colp = col < p.n ? p.A + col * p.lda : p.b;
+  const int64_t ch_first = p.row_begin / T;
+  const int64_t nch = (p.row_end - p.row_begin + T - 1) / T;
+  const int64_t it0 = nch * blockIdx.y / p.P, it1 = nch * (blockIdx.y + 1) / p.P;
+  const int64_t niter = it1 - it0;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  if (tid < NS) reinterpret_cast<double*>(ring + tid * stage_bytes)[T] = 0.0;
+  __syncthreads();
+
+  if (tid >= NT) {
+    if (tid == NT) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      int s = 0;
+      uint32_t ph = 1;  // phase of empty[s] to wait for (first pass: none)
+      for (int64_t it = 0; it < niter; ++it) {
+        if (it >= NS) mbar_wait(&empty[s], ph);
+        const int64_t ch = ch_first + it0 + it;
+        const int64_t r0 = ch * T;
+        const int len = (int)(p.row_end - r0 < T ? p.row_end - r0 : T);
+        const int len_even = len & ~1;
+        const int64_t o0 = __ldg(p.chunk_off + ch), o1 = __ldg(p.chunk_off + ch + 1);
+        unsigned char* st = ring + s * stage_bytes;
+        double* As = reinterpret_cast<double*>(st);
+        const uint32_t lbytes = (uint32_t)((o1 - o0) * 2);
+        if (len & 1) As[len - 1] = __ldg(colp + r0 + len - 1);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(len_even * sizeof(double)) + lbytes);
+        if (len_even)
+          bulk_g2s(As, colp + r0, (uint32_t)(len_even * sizeof(double)), &full[s], pol_stream);
+        bulk_g2s(st + a_bytes, p.lanes + o0, lbytes, &full[s], pol_keep);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  const int wid = tid >> 5, lane = tid & 31;
+  // slot q of this thread owns bucket tid + q * NT
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (p.P == 1 && p.accumulate) {
+    const double* src = col < p.n ? p.out + col * p.ldo : p.outb;
+    if (tid + 0 * NT < p.d) a0 = src[tid + 0 * NT];
+    if (tid + 1 * NT < p.d) a1 = src[tid + 1 * NT];
+    if (tid + 2 * NT < p.d) a2 = src[tid + 2 * NT];
+    if (tid + 3 * NT < p.d) a3 = src[tid + 3 * NT];
+  }
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t it = 0; it < niter; ++it) {
+    mbar_wait(&full[s], ph);
+    const unsigned char* st = ring + s * stage_bytes;
+    const uint16_t* L = reinterpret_cast<const uint16_t*>(st + a_bytes);
+    const int r0 = L[wid], r1 = L[wid + 1];
+    const uint16_t* Lr = L + p.head + lane;
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+      const uint32_t e = Lr[r * 32];
+      const uint2 w = *reinterpret_cast<const uint2*>(st + (e & 0x1fffu) * 8);
+      const double x = __hiloint2double((int)(w.y ^ ((e & 0x8000u) << 16)), (int)w.x);
+      // Exactly one slot accumulates.  Written as branches around each add
+      // so ptxas emits four predicated DADDs (a C if-chain or predicated PTX
+      // adds come out as DADD + FSEL select chains, 3x the issue slots).
+      const uint32_t slot = e & 0x6000u;
+      asm("{\n\t.reg .pred q;\n\t"
+          "setp.ne.u32 q, %4, 0x0000;\n\t@q bra SK0%=;\n\tadd.rn.f64 %0, %0, %5;\n\tSK0%=:\n\t"
+          "setp.ne.u32 q, %4, 0x2000;\n\t@q bra SK1%=;\n\tadd.rn.f64 %1, %1, %5;\n\tSK1%=:\n\t"
+          "setp.ne.u32 q, %4, 0x4000;\n\t@q bra SK2%=;\n\tadd.rn.f64 %2, %2, %5;\n\tSK2%=:\n\t"
+          "setp.ne.u32 q, %4, 0x6000;\n\t@q bra SK3%=;\n\tadd.rn.f64 %3, %3, %5;\n\tSK3%=:\n\t}"
+          : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3)
+          : "r"(slot), "d"(x));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+  const double av[4] = {a0, a1, a2, a3};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int bkt = tid + q * NT;
+    if (bkt >= p.d) continue;
+    if (p.P == 1) {
+      if (col < p.n)
+        p.out[col * p.ldo + bkt] = av[q];
+      else
+        p.outb[bkt] = av[q];
+    } else {
+      p.part[((int64_t)blockIdx.y * p.ncols + col) * p.d + bkt] = av[q];
+    }
+  }
+}
+
 // Fixed-order reduction of the P partial sketches.
 __global__ void countsketch_reduce_kernel(const double* part, int P, int64_t ncols, int d,
                                           int64_t n, double* out, int64_t ldo, double* outb,
@@ -337,9 +480,107 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
   return SKL_OK;
 }
 
+static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64_t lda,
+                                    const double* b, const uint16_t* lanes,
+                                    const int64_t* chunk_off, int64_t max_block, int64_t d,
+                                    int64_t chunk, int warps, double* SA, int64_t ldsa, double* Sb,
+                                    int partitions, int accumulate, int64_t row_begin,
+                                    int64_t row_end, cudaStream_t st) {
+  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+              "countsketch: bad shape m=%lld n=%lld d=%lld", (long long)m, (long long)n,
+              (long long)d);
+  SKL_REQUIRE((warps == 8 || warps == 16) && d <= (int64_t)warps * 128, SKL_ERR_SPEC,
+              "countsketch (owned): d=%lld does not fit %d warps", (long long)d, warps);
+  SKL_REQUIRE(chunk >= 8 && chunk <= 8184 && chunk % 8 == 0, SKL_ERR_INVALID,
+              "countsketch: bad plan chunk %lld", (long long)chunk);
+  SKL_REQUIRE(A && lanes && chunk_off && SA && (!b || Sb) && max_block > 0, SKL_ERR_INVALID,
+              "countsketch: null pointer");
+  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) &&
+                  (!b || ((uintptr_t)b & 15) == 0) && ((uintptr_t)lanes & 15) == 0,
+              SKL_ERR_INVALID,
+              "countsketch: A/b/plan must be 16-byte aligned with an even leading dimension");
+  SKL_REQUIRE(row_begin % chunk == 0 && row_end > row_begin && row_end <= m, SKL_ERR_INVALID,
+              "countsketch: bad row range");
+  const int64_t ncols = n + (b ? 1 : 0);
+  const int T = (int)chunk;
+  const size_t stage = ((size_t)(T + 2) * 8 + (size_t)max_block * 2 + 127) & ~(size_t)127;
+  // Deepest ring that fits; with 16 warps two CTAs share an SM when the
+  // ring fits half the shared memory.
+  const size_t budget = 227 * 1024 - 128;
+  int stages = (int)std::min<size_t>(OW_MAX_STAGES, budget / stage);
+  SKL_REQUIRE(stages >= 2, SKL_ERR_INVALID, "countsketch: plan blocks too large");
+  if (const char* env = getenv("SKL_OWNED_STAGES")) stages = std::max(2, std::min(stages, atoi(env)));
+  const size_t smem = 128 + stages * stage;
+  const int64_t nch = (row_end - row_begin + T - 1) / T;
+  int P = partitions;
+  if (P <= 0) {
+    const int sms = sm_count();
+    const bool ordered = ncols * 2 >= sms || (row_end - row_begin) <= (1 << 18);
+    P = ordered ? 1 : (int)((2 * sms + ncols - 1) / ncols);
+  }
+  P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nch));
+  OwParams p;
+  p.A = A; p.lda = lda; p.b = b; p.n = n; p.ncols = ncols; p.row_begin = row_begin;
+  p.row_end = row_end; p.lanes = lanes; p.chunk_off = chunk_off; p.max_block = (int)max_block;
+  p.d = (int)d; p.T = T; p.head = (warps + 1 + 7) / 8 * 8; p.P = P; p.stages = stages; p.out = SA; p.ldo = ldsa;
+  p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
+  double* part = nullptr;
+  if (P > 1) {
+    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * ncols * d * sizeof(double), st));
+    p.part = part;
+  }
+  dim3 grid((unsigned)ncols, (unsigned)P);
+  cudaError_t e;
+  if (warps == 16) {
+    auto k = countsketch_owned_kernel<512>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) {
+      k<<<grid, 512 + 32, smem, st>>>(p);
+      e = cudaGetLastError();
+    }
+  } else {
+    auto k = countsketch_owned_kernel<256>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) {
+      k<<<grid, 256 + 32, smem, st>>>(p);
+      e = cudaGetLastError();
+    }
+  }
+  if (e != cudaSuccess) {
+    if (part) cudaFreeAsync(part, st);
+    SKL_FAIL(SKL_ERR_CUDA, "countsketch (owned) launch failed: %s", cudaGetErrorString(e));
+  }
+  if (P > 1) {
+    const int64_t total = ncols * d;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * sm_count());
+    countsketch_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, ncols, (int)d, n, SA, ldsa, Sb,
+                                                      accumulate);
+    SKL_CUDA_LAUNCH();
+    SKL_CUDA(cudaFreeAsync(part, st));
+  }
+  return SKL_OK;
+}
+
 }  // namespace skl
 
 using namespace skl;
+
+extern "C" int skl_countsketch_dense_owned(const double* A, int64_t m, int64_t n, int64_t lda,
+                                           const double* b, const uint16_t* lanes,
+                                           const int64_t* chunk_off, int64_t max_block, int64_t d,
+                                           int64_t chunk, int warps, double* SA, int64_t ldsa,
+                                           double* Sb, int partitions, int accumulate,
+                                           void* stream) {
+  clear_error();
+  return countsketch_owned_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps,
+                                  SA, ldsa, Sb, partitions, accumulate, 0, m, (cudaStream_t)stream);
+}
 
 extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,
                                      const double* b, const uint32_t* lanes,
@@ -354,18 +595,15 @@ extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int6
                             accumulate, 0, m, (cudaStream_t)stream);
 }
 
-// Host-buffer entry point: row blocks of A are copied host->device on a
-// side stream while the kernel sketches the previous block (ordered pass,
+// Host-buffer apply: row blocks of A are copied host->device on a side
+// stream while the kernel sketches the previous block (ordered pass,
 // accumulate across blocks, so the result stays bitwise-equal).
-extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
-                                          const double* b_host, const uint32_t* lanes,
-                                          const int64_t* chunk_off, int64_t max_block,
-                                          int64_t d, int64_t chunk, int warps,
-                                          double* SA_host, int64_t ldsa, double* Sb_host,
-                                          double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
-                                          void* stream) {
-  clear_error();
-  cudaStream_t st = (cudaStream_t)stream;
+template <class Launch>
+static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, int64_t lda,
+                                   const double* b_host, int64_t d, int64_t chunk,
+                                   double* SA_host, int64_t ldsa, double* Sb_host,
+                                   double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
+                                   cudaStream_t st, Launch&& launch) {
   SKL_REQUIRE(A_host && SA_host && m >= 1 && n >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch_host: bad arguments");
   SKL_REQUIRE(!b_host || Sb_host, SKL_ERR_INVALID, "countsketch_host: Sb_host missing");
@@ -407,9 +645,7 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
       rc = SKL_ERR_CUDA;
       break;
     }
-    rc = countsketch_launch(A_dev, m, n, ld_dev, b_host ? b_dev : nullptr, lanes, chunk_off,
-                            max_block, d,
-                            chunk, warps, SA_dev, d, Sb_dev, 1, k > 0 ? 1 : 0, r0, r1, st);
+    rc = launch(A_dev, ld_dev, b_host ? b_dev : nullptr, SA_dev, Sb_dev, k > 0 ? 1 : 0, r0, r1);
   }
   if (rc == SKL_OK) {
     cudaError_t e = cudaMemcpy2DAsync(SA_host, ldsa * sizeof(double), SA_dev, d * sizeof(double),
@@ -431,4 +667,40 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
   cudaFreeAsync(SA_dev, st);
   if (Sb_dev) cudaFreeAsync(Sb_dev, st);
   return rc;
+}
+
+extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
+                                          const double* b_host, const uint32_t* lanes,
+                                          const int64_t* chunk_off, int64_t max_block,
+                                          int64_t d, int64_t chunk, int warps,
+                                          double* SA_host, int64_t ldsa, double* Sb_host,
+                                          double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
+                                          void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  return countsketch_host_stream(
+      A_host, m, n, lda, b_host, d, chunk, SA_host, ldsa, Sb_host, A_dev_keep, ld_keep,
+      b_dev_keep, st,
+      [&](const double* A_dev, int64_t ld_dev, const double* b_dev, double* SA_dev, double* Sb_dev,
+          int acc, int64_t r0, int64_t r1) {
+        return countsketch_launch(A_dev, m, n, ld_dev, b_dev, lanes, chunk_off, max_block, d,
+                                  chunk, warps, SA_dev, d, Sb_dev, 1, acc, r0, r1, st);
+      });
+}
+
+extern "C" int skl_countsketch_dense_owned_host(
+    const double* A_host, int64_t m, int64_t n, int64_t lda, const double* b_host,
+    const uint16_t* lanes, const int64_t* chunk_off, int64_t max_block, int64_t d, int64_t chunk,
+    int warps, double* SA_host, int64_t ldsa, double* Sb_host, double* A_dev_keep,
+    int64_t ld_keep, double* b_dev_keep, void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  return countsketch_host_stream(
+      A_host, m, n, lda, b_host, d, chunk, SA_host, ldsa, Sb_host, A_dev_keep, ld_keep,
+      b_dev_keep, st,
+      [&](const double* A_dev, int64_t ld_dev, const double* b_dev, double* SA_dev, double* Sb_dev,
+          int acc, int64_t r0, int64_t r1) {
+        return countsketch_owned_launch(A_dev, m, n, ld_dev, b_dev, lanes, chunk_off, max_block,
+                                        d, chunk, warps, SA_dev, d, Sb_dev, 1, acc, r0, r1, st);
+      });
 }

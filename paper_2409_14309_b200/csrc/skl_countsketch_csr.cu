@@ -5,16 +5,16 @@
 // column c; densifying keeps those sums.  Reproducing that per-(i, c) fold
 // order makes the device result bitwise-equal.
 //
-// Design (B200): a CTA owns B buckets x Cw output columns held as a dense
-// tile in shared memory; one warp per bucket walks the bucket's source rows
-// (the operator's bucket-sorted row list, i.e. the CSR of S) 32 rows at a
-// time.  The warp flattens those rows' nonzeros in (row, position) order,
-// lanes load one nonzero each (coalesced over the CSR arrays of
-// consecutive... rows of the bucket are scattered, so each row's entries are
-// one short gather), and commit into the tile in flattened order: lanes hitting
-// the same column are serialised by lane rank (__match_any_sync), distinct
-// columns commit together.  The tile is then written once, coalesced; the
-// output needs no memset and no atomics.
+// Design (B200): a CTA owns 8 buckets x Cw output columns held as a dense
+// tile in shared memory (bucket-major, odd row stride); one warp per bucket
+// walks the bucket's source rows (the operator's bucket-sorted row list, i.e.
+// the CSR of S) 32 rows at a time, fetching the next 32 rows' CSR extents
+// while committing the current ones.  The warp flattens those rows'
+// nonzeros in (row, position) order, lanes gather one nonzero each, and
+// commit into the tile in flattened order: lanes hitting the same column are
+// serialised by lane rank (__match_any_sync), distinct columns commit
+// together.  The tile is then written once; the output needs no memset and
+// no atomics.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,7 +24,7 @@
 
 namespace skl {
 
-constexpr int CSR_B = 16;  // buckets (warps) per CTA
+constexpr int CSR_B = 8;   // buckets (warps) per CTA
 
 __global__ void __launch_bounds__(CSR_B * 32)
     countsketch_csr_kernel(const int64_t* __restrict__ indptr, const int64_t* __restrict__ indices,
@@ -32,27 +32,46 @@ __global__ void __launch_bounds__(CSR_B * 32)
                            const int64_t* __restrict__ bptr, const int8_t* __restrict__ signs,
                            int64_t d, int64_t n, int64_t Cw, double* __restrict__ SA,
                            int64_t ldsa) {
-  extern __shared__ double tile[];  // [Cw][CSR_B]
+  extern __shared__ double tile[];  // [CSR_B][cw + 1] (bucket-major, odd stride)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)blockIdx.x * CSR_B;
   const int64_t c0 = (int64_t)blockIdx.y * Cw;
   const int64_t cw = min(Cw, n - c0);
-  for (int64_t k = threadIdx.x; k < cw * CSR_B; k += blockDim.x) tile[k] = 0.0;
+  const int64_t ldt = cw + 1;
+  for (int64_t k = threadIdx.x; k < ldt * CSR_B; k += blockDim.x) tile[k] = 0.0;
   __syncthreads();
 
   const int64_t i = i0 + warp;
   if (i < d) {
     const int64_t r_beg = bptr[i], r_end = bptr[i + 1];
-    double* my = tile + warp;  // column c at my[(c - c0) * CSR_B]
-    for (int64_t base = r_beg; base < r_end; base += 32) {
-      const int64_t r = base + lane;
-      int64_t p0 = 0, cnt = 0;
-      double s = 0.0;
+    double* my = tile + warp * ldt;  // column c at my[c - c0]
+    // Row metadata of round r+1 is fetched while round r is committed
+    // (two dependent loads: bucket row -> its CSR extent).
+    int64_t np0 = 0, ncnt = 0;
+    double ns = 0.0;
+    {
+      const int64_t r = r_beg + lane;
       if (r < r_end) {
         const int32_t j = brow[r];
-        p0 = indptr[j];
-        cnt = indptr[j + 1] - p0;
-        s = (double)signs[j];
+        np0 = indptr[j];
+        ncnt = indptr[j + 1] - np0;
+        ns = (double)signs[j];
+      }
+    }
+    for (int64_t base = r_beg; base < r_end; base += 32) {
+      const int64_t p0 = np0, cnt = ncnt;
+      const double s = ns;
+      np0 = 0;
+      ncnt = 0;
+      ns = 0.0;
+      if (base + 32 < r_end) {
+        const int64_t r = base + 32 + lane;
+        if (r < r_end) {
+          const int32_t j = brow[r];
+          np0 = indptr[j];
+          ncnt = indptr[j + 1] - np0;
+          ns = (double)signs[j];
+        }
       }
       // exclusive scan of counts over the warp (lane order == ascending j)
       int64_t incl = cnt;
@@ -91,7 +110,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
         const int rank = __popc(grp & ((1u << lane) - 1));
         const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
         for (int q = 0; q < rounds; ++q) {
-          if (valid && rank == q) my[(c - c0) * CSR_B] += s_o * v;
+          if (valid && rank == q) my[c - c0] += s_o * v;
           __syncwarp();
         }
       }
@@ -102,7 +121,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
   const int64_t nb = min((int64_t)CSR_B, d - i0);
   for (int64_t k = threadIdx.x; k < cw * CSR_B; k += blockDim.x) {
     const int64_t cc = k / CSR_B, b = k % CSR_B;
-    if (b < nb) SA[(c0 + cc) * ldsa + i0 + b] = tile[k];
+    if (b < nb) SA[(c0 + cc) * ldsa + i0 + b] = tile[b * ldt + cc];
   }
 }
 
@@ -139,9 +158,9 @@ extern "C" int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices
                   ldsa >= d,
               SKL_ERR_SHAPE, "countsketch_csr: bad arguments");
   // shared tile budget: up to 192 KiB
-  const int64_t max_cw = (192 * 1024) / (CSR_B * 8);
+  const int64_t max_cw = (192 * 1024) / (CSR_B * 8) - 1;
   const int64_t Cw = std::min<int64_t>(n, max_cw);
-  const size_t smem = (size_t)Cw * CSR_B * sizeof(double);
+  const size_t smem = (size_t)(Cw + 1) * CSR_B * sizeof(double);
   SKL_CUDA(cudaFuncSetAttribute(countsketch_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   dim3 grid((unsigned)((d + CSR_B - 1) / CSR_B), (unsigned)((n + Cw - 1) / Cw));

@@ -24,18 +24,19 @@ import numpy as np
 
 from . import _native
 from ._device import current_stream, device_f64, require_cuda, to_device, torch
-from .sketch import PLAN_CHUNK, SketchOperator, build_sketch, plan_warps
+from .sketch import SHARD_ALIGN, CountSketchPlan, SketchOperator, build_sketch
 
 
 def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous row block [r0, r1) of rank ``rank``; blocks start on plan
-    chunk boundaries so each rank's plan is chunk-aligned."""
+    """Contiguous row block [r0, r1) of rank ``rank``; blocks start on
+    multiples of SHARD_ALIGN rows (keeps row blocks of a shared array
+    16-byte aligned and the shards near-equal)."""
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad rank {rank} of {world}")
-    chunks = math.ceil(m / PLAN_CHUNK)
+    chunks = math.ceil(m / SHARD_ALIGN)
     c0 = chunks * rank // world
     c1 = chunks * (rank + 1) // world
-    return min(m, c0 * PLAN_CHUNK), min(m, c1 * PLAN_CHUNK)
+    return min(m, c0 * SHARD_ALIGN), min(m, c1 * SHARD_ALIGN)
 
 
 class ShardPlan:
@@ -51,11 +52,9 @@ class ShardPlan:
         self.signs = np.ascontiguousarray(op.signs[r0:r1])
         self._plan = None
 
-    def device_plan(self):
+    def device_plan(self) -> CountSketchPlan:
         if self._plan is None:
-            lanes, off, mx = _native.countsketch_plan(self.rows, self.signs, self.d, PLAN_CHUNK,
-                                                      plan_warps(self.d))
-            self._plan = (to_device(lanes), to_device(off), mx)
+            self._plan = CountSketchPlan(self.rows, self.signs, self.d)
         return self._plan
 
 
@@ -65,14 +64,10 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
     require_cuda()
     m_loc = plan.r1 - plan.r0
     n = A_local.shape[1]
-    lanes, off, mx = plan.device_plan()
     d = plan.d
     ld = (d + 1) // 2 * 2  # keeps the Sb column 16-byte aligned
     out = device_f64((d, n + 1), fortran=True, ld=ld)
-    _native.call("skl_countsketch_dense", _native.ptr(A_local), m_loc, n, lda,
-                 _native.ptr(b_local), _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK,
-                 plan_warps(d),
-                 _native.ptr(out), ld, _native.ptr(out[:, n]), 1, 0, current_stream())
+    plan.device_plan().apply(A_local, m_loc, n, lda, b_local, out, ld, out[:, n], partitions=1)
     return out
 
 

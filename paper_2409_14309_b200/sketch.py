@@ -42,13 +42,61 @@ ENGINE_KINDS = ("gaussian", "srht", "countsketch", "identity")
 
 _MATERIALIZE_GUARD = 10**7
 
-# Rows per plan chunk of the CountSketch apply (multiple of 8, <= 32768);
-# the consumer warp count follows d (_native.plan_geometry).
-PLAN_CHUNK = 2048
+# Row-shard boundaries (distributed.shard_rows) are multiples of this.
+SHARD_ALIGN = 8192
+# Shared memory per CTA available to the apply kernels' rings.
+_SMEM_BUDGET = 226 * 1024
 
 
-def plan_warps(d: int) -> int:
-    return _native.plan_geometry(d)[1]
+class CountSketchPlan:
+    """Device form of a CountSketch's hashes for the dense apply kernels.
+
+    kind "owned" (d <= 2048): each bucket's running sum lives in a register
+    of one lane for the whole apply (skl_countsketch_dense_owned);
+    kind "lanes" (larger d): shared-memory accumulators fed by per-lane
+    lists (skl_countsketch_dense).  Either way the per-bucket fold order is
+    ascending source row, so the ordered apply is bitwise-equal to scipy."""
+
+    def __init__(self, rows: np.ndarray, signs: np.ndarray, d: int, kind: str | None = None):
+        self.d = int(d)
+        self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, kind)
+        # The kernels' ring stages (A chunk + plan block) must fit shared
+        # memory: shrink the chunk when few buckets make per-lane lists long.
+        while True:
+            if self.kind == "owned":
+                lanes, off, mx = _native.countsketch_plan_owned(rows, signs, self.d, self.chunk,
+                                                                self.warps)
+                need = 2 * ((self.chunk + 2) * 8 + 2 * mx + 127)
+            else:
+                lanes, off, mx = _native.countsketch_plan(rows, signs, self.d, self.chunk,
+                                                          self.warps)
+                need = 3 * ((self.chunk + 2) * 8 + 4 * mx + 127) + (self.d + 1) * 8 + 256
+            if need <= _SMEM_BUDGET or self.chunk <= 8:
+                break
+            self.chunk = max(8, int(self.chunk * 0.9 * _SMEM_BUDGET / need) // 8 * 8)
+        self.lanes = to_device(lanes.view(np.int16 if self.kind == "owned" else np.int32))
+        self.off = to_device(off)
+        self.max_block = mx
+        self.plan_bytes = int(lanes.nbytes + off.nbytes)
+
+    def apply(self, A, m: int, n: int, lda: int, b, out, ldo: int, outb,
+              partitions: int = 0, accumulate: int = 0, stream=None) -> None:
+        """out[:, :n] (+)= S A, outb (+)= S b on the device (raw pointers or tensors)."""
+        fn = "skl_countsketch_dense_owned" if self.kind == "owned" else "skl_countsketch_dense"
+        _native.call(fn, _native.ptr(A), m, n, lda, _native.ptr(b), _native.ptr(self.lanes),
+                     _native.ptr(self.off), self.max_block, self.d, self.chunk, self.warps,
+                     _native.ptr(out), ldo, _native.ptr(outb), partitions, accumulate,
+                     current_stream() if stream is None else stream)
+
+    def apply_host(self, A, m: int, n: int, lda: int, b, SA, ldsa: int, Sb,
+                   A_keep=None, ld_keep: int = 0, b_keep=None, stream=None) -> None:
+        """Host A/b in, host SA/Sb out; H2D streamed under the kernel."""
+        fn = ("skl_countsketch_dense_owned_host" if self.kind == "owned"
+              else "skl_countsketch_dense_host")
+        _native.call(fn, _native.ptr(A), m, n, lda, _native.ptr(b), _native.ptr(self.lanes),
+                     _native.ptr(self.off), self.max_block, self.d, self.chunk, self.warps,
+                     _native.ptr(SA), ldsa, _native.ptr(Sb), _native.ptr(A_keep), ld_keep,
+                     _native.ptr(b_keep), current_stream() if stream is None else stream)
 
 
 def default_embed_dim(m: int, n: int, d_factor: float = 4.0) -> int:
@@ -132,14 +180,12 @@ class SketchOperator:
         dev = torch.cuda.current_device()
         return self._dev.setdefault(dev, {})
 
-    def device_plan(self):
-        """(lanes, chunk_off, max_block) of the CountSketch plan on the current device."""
+    def device_plan(self) -> CountSketchPlan:
+        """The CountSketch apply plan on the current device (built once)."""
         require_cuda()
         c = self._cache()
         if "plan" not in c:
-            lanes, off, mx = _native.countsketch_plan(self.rows, self.signs, self.target_dim,
-                                                      PLAN_CHUNK, plan_warps(self.target_dim))
-            c["plan"] = (to_device(lanes), to_device(off), mx)
+            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim)
         return c["plan"]
 
     def device_buckets(self):
@@ -246,31 +292,26 @@ def _aligned(t, ld: int, cols: int):
 
 def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     """SA (d x n column-major tensor) and Sb (d) or None, all on device."""
-    lanes, off, mx = op.device_plan()
+    plan = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A, lda = _aligned(A, lda, n)
     if b is not None and b.data_ptr() % 16:
         b = b.clone()
     SA = device_f64((d, n), fortran=True)
     Sb = device_f64((d,)) if b is not None else None
-    _native.call("skl_countsketch_dense", _native.ptr(A), m, n, lda, _native.ptr(b),
-                 _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK, plan_warps(d),
-                 _native.ptr(SA), d, _native.ptr(Sb), 0, 0, current_stream())
+    plan.apply(A, m, n, lda, b, SA, d, Sb)
     return SA, Sb
 
 
 def _countsketch_dense_host(op: SketchOperator, A: np.ndarray, n: int,
                             b: np.ndarray | None = None):
     """Host buffers in, host SA/Sb out; H2D streamed under the kernel."""
-    lanes, off, mx = op.device_plan()
+    plan = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A = np.asfortranarray(A)
     SA = np.empty((d, n), dtype=np.float64, order="F")
     Sb = np.empty(d, dtype=np.float64) if b is not None else None
-    _native.call("skl_countsketch_dense_host", _native.ptr(A), m, n, A.shape[0] if A.ndim == 2
-                 else m, _native.ptr(b), _native.ptr(lanes), _native.ptr(off), mx, d, PLAN_CHUNK,
-                 plan_warps(d), _native.ptr(SA), d, _native.ptr(Sb), None, 0, None,
-                 current_stream())
+    plan.apply_host(A, m, n, A.shape[0] if A.ndim == 2 else m, b, SA, d, Sb)
     return SA, Sb
 
 

@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 from oracle import oracle as O
 from paper_2409_14309_b200 import SketchSpec, build_sketch
 from paper_2409_14309_b200.distributed import ShardPlan, shard_rows, sharded_sketch_and_apply
-from paper_2409_14309_b200.sketch import PLAN_CHUNK
+from paper_2409_14309_b200.sketch import SHARD_ALIGN
 
 
 def _free_port():
@@ -80,7 +80,7 @@ def test_shard_rows_cover_and_align():
             assert spans[0][0] == 0 and spans[-1][1] == m
             for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
                 assert a1 == b0
-            assert all(s0 % PLAN_CHUNK == 0 for s0, _ in spans)
+            assert all(s0 % SHARD_ALIGN == 0 for s0, _ in spans)
 
 
 def test_shard_plan_slices_global_hashes():

@@ -220,21 +220,45 @@ def test_residual_kernel():
     assert abs(got - want) <= 1e-12 * want
 
 
-def test_host_streaming_abi_bitwise(golden, golden_meta):
-    """skl_countsketch_dense_host: host buffers in/out, H2D streamed."""
+@pytest.mark.parametrize("kind", ["owned", "lanes"])
+def test_host_streaming_abi_bitwise(golden, golden_meta, kind):
+    """skl_countsketch_dense{_owned}_host: host buffers in/out, H2D streamed."""
+    from paper_2409_14309_b200.sketch import CountSketchPlan
+
     c, _, A, b, ref = live_case("cfg1", golden_meta)
     A = np.asfortranarray(A)
     op = saa_op(c, "countsketch")
-    lanes, coff, mx = op.device_plan()
+    plan = CountSketchPlan(op.rows, op.signs, c.d, kind=kind)
     SA = np.empty((c.d, c.n), order="F")
     Sb = np.empty(c.d)
-    from paper_2409_14309_b200.sketch import PLAN_CHUNK, plan_warps
-
-    _native.call("skl_countsketch_dense_host", A.ctypes.data, c.m, c.n, c.m, b.ctypes.data,
-                 lanes.data_ptr(), coff.data_ptr(), mx, c.d, PLAN_CHUNK,
-                 plan_warps(c.d), SA.ctypes.data, c.d,
-                 Sb.ctypes.data, None, 0, None, torch.cuda.current_stream().cuda_stream)
+    plan.apply_host(A, c.m, c.n, c.m, b, SA, c.d, Sb)
     assert np.array_equal(SA, golden["cfg1_SA"]) and np.array_equal(Sb, ref["Sb"])
+
+
+@pytest.mark.parametrize("kind", ["owned", "lanes"])
+@pytest.mark.parametrize("m,n,d", [(1, 1, 1), (9, 2, 3), (8184, 3, 5), (8185, 2, 2048),
+                                   (50_000, 5, 1024), (50_001, 3, 1025), (100_000, 2, 17)])
+def test_countsketch_both_plans_bitwise(m, n, d, kind):
+    """Both dense kernels (register-owned and lane-list) on the same
+    operator: bitwise-equal to the oracle's scipy fold, ragged chunk tails,
+    one-bucket and many-bucket lanes."""
+    from paper_2409_14309_b200.sketch import CountSketchPlan
+
+    rng = np.random.default_rng(m + 7 * d)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec("countsketch", d, seed=m ^ d), m)
+    plan = CountSketchPlan(op.rows, op.signs, d, kind=kind)
+    lda = (m + 1) // 2 * 2  # kernels need an even leading dimension
+    Ad = torch.zeros((n, lda), dtype=torch.float64, device="cuda").t()
+    Ad[:m] = torch.from_numpy(A).cuda()
+    bd = torch.from_numpy(b).cuda()
+    SA = torch.full((n, d), float("nan"), dtype=torch.float64, device="cuda").t()
+    Sb = torch.full((d,), float("nan"), dtype=torch.float64, device="cuda")
+    plan.apply(Ad, m, n, lda, bd, SA, d, Sb, partitions=1)
+    want = O.countsketch_apply(op.rows, op.signs, d, np.column_stack([A, b]))
+    got = np.column_stack([SA.cpu().numpy(), Sb.cpu().numpy()])
+    assert np.array_equal(got, want)
 
 
 # ---------------------------------------------------------------------- SRHT

@@ -186,6 +186,84 @@ def test_countsketch_plan_structure_and_semantics(m, d, chunk, warps):
         assert np.array_equal(got, want)
 
 
+def _simulate_owned(lanes, off, d, chunk, warps, m, x):
+    """Execute a register-owned plan the way the kernel does: every lane
+    folds its list in order into the register of the entry's slot."""
+    head = (warps + 1 + 7) // 8 * 8
+    acc = np.zeros((warps, 32, 4))
+    for k in range(len(off) - 1):
+        r0 = k * chunk
+        xs = np.zeros(chunk + 1)
+        seg = x[r0: r0 + chunk]
+        xs[: len(seg)] = seg
+        blk = lanes[off[k]: off[k + 1]].astype(np.int64)
+        for w in range(warps):
+            sub = blk[head + 32 * blk[w]: head + 32 * blk[w + 1]].reshape(-1, 32)
+            for step in sub:
+                v = np.where(step >> 15, -1.0, 1.0) * xs[step & 0x1FFF]
+                acc[w, np.arange(32), (step >> 13) & 3] += v
+    # slot q of thread t owns bucket t + q * 32 * warps
+    return acc.reshape(32 * warps, 4).T.reshape(-1)[:d]
+
+
+@pytest.mark.parametrize("m,d,chunk,warps", [(1, 1, 8, 8), (100, 4, 8, 8), (20_000, 800, 8184, 8),
+                                             (65_537, 2048, 8184, 16), (9_000, 3, 1024, 8),
+                                             (50_000, 1024, 4096, 8), (30_001, 1025, 8184, 16)])
+def test_owned_plan_structure_and_semantics(m, d, chunk, warps):
+    """Register-owned plan (skl_countsketch_plan_owned): every row exactly
+    once, in the lane/slot that owns its bucket, ascending within a bucket,
+    and executing it reproduces the scipy fold bitwise."""
+    key = O.derive_seed(5, "countsketch", m)
+    rows, signs = _native.rng_countsketch(key, m, d)
+    lanes, off, mx = _native.countsketch_plan_owned(rows, signs, d, chunk, warps)
+    head = (warps + 1 + 7) // 8 * 8
+    nch = (m + chunk - 1) // chunk
+    assert lanes.dtype == np.uint16 and off[0] == 0 and len(off) == nch + 1
+    assert mx == int(np.diff(off).max()) and np.all(np.diff(off) % 8 == 0)
+    for k in range(0, nch, max(1, nch // 5)):
+        r0 = k * chunk
+        length = min(chunk, m - r0)
+        blk = lanes[off[k]: off[k + 1]].astype(np.int64)
+        wrow = blk[: warps + 1]
+        assert wrow[0] == 0 and np.all(np.diff(wrow) >= 0)
+        assert len(blk) == head + 32 * wrow[warps]
+        seen = np.zeros(length, dtype=int)
+        for w in range(warps):
+            sub = blk[head + 32 * wrow[w]: head + 32 * wrow[w + 1]].reshape(-1, 32)
+            for lane in range(32):
+                lst = sub[:, lane]
+                j = lst & 0x1FFF
+                real = j != chunk
+                jr, slot = j[real], (lst[real] >> 13) & 3
+                assert np.all((lst[~real] >> 13) == 0)          # pads: slot 0, +, zero row
+                seen[jr] += 1
+                assert np.all(rows[r0 + jr] == w * 32 + lane + slot * 32 * warps)
+                assert np.array_equal(((lst[real] >> 15) & 1).astype(bool), signs[r0 + jr] < 0)
+                for s_ in range(4):
+                    assert np.all(np.diff(jr[slot == s_]) > 0)  # ascending per bucket
+        assert np.all(seen == 1)
+    x = np.random.default_rng(m).standard_normal(m)
+    got = _simulate_owned(lanes, off, d, chunk, warps, m, x)
+    want = O.countsketch_fold(rows.astype(np.int64), signs.astype(np.float64), d, x)
+    assert np.array_equal(got, want)
+
+
+def test_owned_plan_limits_and_thread_invariance():
+    m, d = 100_000, 2048
+    rows, signs = _native.rng_countsketch(O.derive_seed(6, "countsketch", m), m, d)
+    l1, o1, _ = _native.countsketch_plan_owned(rows, signs, d, 8184, 16, threads=1)
+    l7, o7, _ = _native.countsketch_plan_owned(rows, signs, d, 8184, 16, threads=7)
+    assert np.array_equal(o1, o7) and np.array_equal(l1, l7)
+    with pytest.raises(Exception):
+        _native.countsketch_plan_owned(rows, signs, d, 8184, 8)     # 2048 > 8 warps x 128
+    with pytest.raises(Exception):
+        _native.countsketch_plan_owned(rows, signs, d, 8192, 16)    # row field is 13 bits
+    bad = rows.copy()
+    bad[7] = d
+    with pytest.raises(ValueError):
+        _native.countsketch_plan_owned(bad, signs, d, 8184, 16)
+
+
 def test_plan_is_thread_count_invariant():
     m, d = 300_000, 2048
     rows, signs = _native.rng_countsketch(O.derive_seed(4, "countsketch", m), m, d)
