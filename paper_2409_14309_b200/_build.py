@@ -43,7 +43,9 @@ def _stale() -> bool:
 
 
 def _compile(src: Path, obj: Path, verbose: bool) -> None:
-    cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    # SKL_NVCC_DEFINES: extra flags for instrumented builds (e.g. -DSKL_QR_PROBE)
+    extra = os.environ.get("SKL_NVCC_DEFINES", "").split()
+    cmd = [NVCC, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd += ["-Xptxas", "-v"] if verbose else []
     else:

@@ -46,4 +46,26 @@ int resolve_threads(int threads);
       SKL_FAIL(SKL_ERR_CUDA, "kernel launch failed: %s (%s:%d)",               \
                cudaGetErrorString(e__), __FILE__, __LINE__);                    \
   } while (0)
+
+namespace skl {
+// Stream-ordered workspace allocation.  The first call on a device raises
+// the default memory pool's release threshold so freed workspaces stay
+// mapped across stream synchronisations (the default threshold of 0 unmaps
+// them at every sync and the next call pays the remap, milliseconds for the
+// QR's workspaces).
+template <class T>
+inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
+  static bool retained[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !retained[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    retained[dev] = true;
+  }
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+}
+}  // namespace skl
 #endif

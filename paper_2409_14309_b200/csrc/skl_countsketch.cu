@@ -460,7 +460,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
 
   double* part = nullptr;
   if (P > 1) {
-    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * ncols * d * sizeof(double), st));
+    SKL_CUDA(malloc_async(&part, (size_t)P * ncols * d * sizeof(double), st));
     p.part = part;
   }
   dim3 grid((unsigned)groups, (unsigned)P);
@@ -526,7 +526,7 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
   double* part = nullptr;
   if (P > 1) {
-    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * ncols * d * sizeof(double), st));
+    SKL_CUDA(malloc_async(&part, (size_t)P * ncols * d * sizeof(double), st));
     p.part = part;
   }
   dim3 grid((unsigned)ncols, (unsigned)P);
@@ -612,10 +612,10 @@ static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, i
   double* A_dev = A_dev_keep;
   double* b_dev = b_dev_keep;
   double *SA_dev = nullptr, *Sb_dev = nullptr;
-  if (!A_dev) SKL_CUDA(cudaMallocAsync(&A_dev, (size_t)ld_dev * n * sizeof(double), st));
-  if (b_host && !b_dev) SKL_CUDA(cudaMallocAsync(&b_dev, (size_t)m * sizeof(double), st));
-  SKL_CUDA(cudaMallocAsync(&SA_dev, (size_t)d * n * sizeof(double), st));
-  if (b_host) SKL_CUDA(cudaMallocAsync(&Sb_dev, (size_t)d * sizeof(double), st));
+  if (!A_dev) SKL_CUDA(malloc_async(&A_dev, (size_t)ld_dev * n * sizeof(double), st));
+  if (b_host && !b_dev) SKL_CUDA(malloc_async(&b_dev, (size_t)m * sizeof(double), st));
+  SKL_CUDA(malloc_async(&SA_dev, (size_t)d * n * sizeof(double), st));
+  if (b_host) SKL_CUDA(malloc_async(&Sb_dev, (size_t)d * sizeof(double), st));
 
   cudaStream_t cp;
   SKL_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));

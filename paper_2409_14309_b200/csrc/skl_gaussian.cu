@@ -312,14 +312,14 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
     const int tail_cap = (int)std::min<int64_t>(N / 256 + 4096, 1 << 26);
     int64_t* tail_t = nullptr;
     uint64_t* tail_pos = nullptr;
-    SKL_CUDA(cudaMallocAsync(&mask, (size_t)nseg * ZIG_MASKW * 4, st));
-    SKL_CUDA(cudaMallocAsync(&exitpos, (size_t)nseg * 8, st));
-    SKL_CUDA(cudaMallocAsync(&count, (size_t)nseg * 8, st));
-    SKL_CUDA(cudaMallocAsync(&offset, (size_t)nseg * 8, st));
-    SKL_CUDA(cudaMallocAsync(&total, 8, st));
-    SKL_CUDA(cudaMallocAsync(&flags, 8, st));
-    SKL_CUDA(cudaMallocAsync(&tail_t, (size_t)tail_cap * 8, st));
-    SKL_CUDA(cudaMallocAsync(&tail_pos, (size_t)tail_cap * 8, st));
+    SKL_CUDA(malloc_async(&mask, (size_t)nseg * ZIG_MASKW * 4, st));
+    SKL_CUDA(malloc_async(&exitpos, (size_t)nseg * 8, st));
+    SKL_CUDA(malloc_async(&count, (size_t)nseg * 8, st));
+    SKL_CUDA(malloc_async(&offset, (size_t)nseg * 8, st));
+    SKL_CUDA(malloc_async(&total, 8, st));
+    SKL_CUDA(malloc_async(&flags, 8, st));
+    SKL_CUDA(malloc_async(&tail_t, (size_t)tail_cap * 8, st));
+    SKL_CUDA(malloc_async(&tail_pos, (size_t)tail_cap * 8, st));
     SKL_CUDA(cudaMemsetAsync(flags, 0, 8, st));
     const int tb = 128;
     const int blocks = (int)((nseg + tb - 1) / tb);
@@ -371,7 +371,7 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
         hv[(size_t)q] = v / sqrt_d;
       }
       double* dv = nullptr;
-      SKL_CUDA(cudaMallocAsync(&dv, (size_t)ntail * 8, st));
+      SKL_CUDA(malloc_async(&dv, (size_t)ntail * 8, st));
       SKL_CUDA(cudaMemcpyAsync(dv, hv.data(), (size_t)ntail * 8, cudaMemcpyHostToDevice, st));
       zig_patch_kernel<<<(ntail + 255) / 256, 256, 0, st>>>(tail_t, dv, ntail, m, G, ldg);
       SKL_CUDA_LAUNCH();

@@ -205,7 +205,7 @@ extern "C" int skl_gemm_f64(const double* G, int64_t ldg, const double* A, int64
   p.nkb = nkb; p.accumulate = accumulate; p.ldc = ldc;
   double* part = nullptr;
   if (S > 1) {
-    SKL_CUDA(cudaMallocAsync(&part, (size_t)S * d * n * sizeof(double), st));
+    SKL_CUDA(malloc_async(&part, (size_t)S * d * n * sizeof(double), st));
     p.C = part;
   } else {
     p.C = C;

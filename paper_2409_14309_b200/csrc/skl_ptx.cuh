@@ -60,4 +60,47 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// --- cluster (DSMEM) helpers -------------------------------------------
+// Address of the same shared-memory offset in CTA `cta` of the cluster.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t smem_addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(cta));
+  return r;
+}
+
+// Make this thread's generic-proxy shared-memory writes visible to
+// subsequent async-proxy (bulk copy) reads.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Local shared -> (remote) cluster shared bulk copy; completes `bytes` on the
+// destination CTA's mbarrier (both cluster addresses from mapa_u32).
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cl, const void* src, uint32_t bytes,
+                                               uint32_t mbar_cl) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst_cl), "r"(smem_u32(src)), "r"(bytes), "r"(mbar_cl)
+      : "memory");
+}
+
+// 8-byte store into (remote) cluster shared memory completing 8 bytes on the
+// destination CTA's mbarrier (cluster addresses from mapa_u32).
+__device__ __forceinline__ void st_async_f64(uint32_t dst_cl, double v, uint32_t mbar_cl) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               ::"r"(dst_cl), "d"(v), "r"(mbar_cl)
+               : "memory");
+}
+
+// Phase wait with cluster-scope acquire (data delivered by other CTAs).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 }  // namespace skl

@@ -15,7 +15,7 @@
 // (economy_qr), by backward accumulation of the reflectors into I.
 //
 // Execution: the blocked factorisation in skl_qr_blocked.cu (cluster panel
-// + GEMM-shaped trailing updates) for n >= 384 when a panel fits a
+// + GEMM-shaped trailing updates) for n >= 64 when a panel fits a
 // thread-block cluster (d <= 10880); otherwise this file's unblocked fallback: one
 // persistent cooperative kernel, step k split across all CTAs (each owns
 // trailing columns round-robin) with one grid barrier per step, the CTA that
@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "skl_common.h"
 
@@ -347,9 +348,11 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   SKL_REQUIRE(n <= (48 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
 
   const int fro_blocks = 256;
-  // the cluster-panel factorisation wins from n ~ 384 columns on (panel
-  // steps are latency-bound); narrower systems use the unblocked kernel
-  const bool blocked = n >= 384 && qr_blocked_supported(d);
+  // the blocked factorisation (register cluster panels + GEMM-shaped
+  // trailing updates) wins from a few panels on; very narrow systems use the
+  // unblocked kernel (SKL_QR_BLOCKED_MIN_N overrides the cut-over)
+  static const int64_t min_n = getenv("SKL_QR_BLOCKED_MIN_N") ? atoll(getenv("SKL_QR_BLOCKED_MIN_N")) : 64;
+  const bool blocked = n >= min_n && qr_blocked_supported(d);
   const int64_t ldm = blocked ? (d + 1) / 2 * 2 : d;
   const int64_t npan = (n + 31) / 32;
   size_t off = 0;
@@ -369,7 +372,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   const int64_t part_cap = blocked ? 32 * (n + 1) * 320 : 0;  // up to 320 row splits
   const size_t oP = blocked ? take((size_t)part_cap * 8) : 0;
   unsigned char* ws = nullptr;
-  SKL_CUDA(cudaMallocAsync(&ws, off, st));
+  SKL_CUDA(malloc_async(&ws, off, st));
   double* M = (double*)(ws + oM);
   double* tau = (double*)(ws + oTau);
   double* beta = (double*)(ws + oBeta);

@@ -23,8 +23,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "skl_common.h"
+#include "skl_ptx.cuh"
 
 namespace skl {
 
@@ -34,8 +36,8 @@ constexpr int QB_NT = 1024;      // threads per CTA (32 warps)
 constexpr int QB_NW = QB_NT / 32;
 constexpr int QB_MAXCL = 16;     // max cluster size (non-portable)
 constexpr int QB_MAXROWS = 680;  // rows per CTA that fit in shared memory
-// pub[2][64] + red[32][32] + gram[32][32] + allp[17][32] + gsum[32][32]
-constexpr int QB_SMEM_EXTRA = 128 + 1024 + 1024 + (QB_MAXCL + 1) * 32 + 1024;
+// pub[2][64] + red[32][32] + G[32][32] + sc[2][64] + Ts[32][32]
+constexpr int QB_SMEM_EXTRA = 128 + 1024 + 1024 + 128 + 1024;
 
 __device__ __forceinline__ uint32_t cta_rank_in_cluster() {
   uint32_t r;
@@ -58,6 +60,20 @@ __device__ __forceinline__ double ld_dsmem(const double* local, uint32_t cta) {
   return v;
 }
 
+// Instrumented builds (SKL_NVCC_DEFINES=-DSKL_QR_PROBE): CTA 0 thread 0 of
+// the panel kernel accumulates clock64 cycles per phase; the host prints the
+// totals after each factorisation.
+#ifdef SKL_QR_PROBE
+__device__ unsigned long long g_qr_probe[12];
+#define QR_PROBE_INIT long long pr_[12] = {}; long long t0_ = clock64();
+#define QR_PROBE(i) do { if (rank == 0 && tid == 0) { long long t_ = clock64(); pr_[i] += t_ - t0_; t0_ = t_; } } while (0)
+#define QR_PROBE_FLUSH do { if (rank == 0 && tid == 0) for (int q_ = 0; q_ < 12; ++q_) atomicAdd(&g_qr_probe[q_], (unsigned long long)pr_[q_]); } while (0)
+#else
+#define QR_PROBE_INIT
+#define QR_PROBE(i) do {} while (0)
+#define QR_PROBE_FLUSH do {} while (0)
+#endif
+
 struct PanelParams {
   double* M;        // ld ldm, the whole augmented matrix
   int64_t ldm, d;
@@ -74,16 +90,17 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
   extern __shared__ __align__(16) double qsm[];
   const uint32_t rank = cta_rank_in_cluster();
   const uint32_t ncta = gridDim.x;  // one cluster spans the grid
-  double* P = qsm;                                  // [rows_per][32]
-  double* pub = P + (size_t)p.rows_per * QB_PLD;    // [2][64]
-  double* red = pub + 128;                          // [32][32]
-  double* gram = red + 1024;                        // [32][32]
-  double* allp = gram + 1024;                       // [QB_MAXCL + 1][32]
-  double* gsum = allp + (QB_MAXCL + 1) * 32;        // [32][32]
+  double* P = qsm;                                  // [rows_per][QB_PLD]
+  double* pub = P + (size_t)p.rows_per * QB_PLD;    // [2][64]: column sums, pivot row
+  double* red = pub + 128;                          // [32 warps][32]
+  double* G = red + 1024;                           // [32][32]: column k = V^T v_k
+  double* sc = G + 1024;                            // [2][64]: w_j, scale, beta
+  double* Ts = sc + 128;                            // [32][32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t rbeg = p.j0 + (int64_t)rank * p.rows_per;
   const int nloc = (int)std::max<int64_t>(0, std::min<int64_t>(p.rows_per, p.d - rbeg));
   const int jb = p.jb;
+  QR_PROBE_INIT
 
   // load the panel slice (column-major source -> row-major smem)
   for (int idx = tid; idx < nloc * QB_NB; idx += QB_NT) {
@@ -91,135 +108,123 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
     P[i * QB_PLD + j] = j < jb ? p.M[(p.j0 + j) * p.ldm + rbeg + i] : 0.0;
   }
   __syncthreads();
+  QR_PROBE(0);
 
+  // Per column k (pivot row g): warps own local rows i = warp (mod 32) in
+  // both the dot-product and the update loop, so P needs no barrier between
+  // steps; two CTA barriers and one cluster barrier per column.  Warp 0 does
+  // the scalar work (sums over warps and CTAs, dlarfg) once and publishes
+  // w_j and the reflector scale.
   for (int k = 0; k < jb; ++k) {
     const int64_t g = p.j0 + k;
-    const double* pubr = pub + (k & 1) * 64;
-    double* pubw = pub + (k & 1) * 64;
-    // partial sums s_j = sum_{i > g, local} P[i][k] * P[i][j]
-    double s0 = 0.0;
-    for (int i = warp; i < nloc; i += QB_NW)
-      if (rbeg + i > g) s0 = fma(P[i * QB_PLD + k], P[i * QB_PLD + lane], s0);
-    red[warp * 32 + lane] = s0;
-    __syncthreads();
-    if (warp == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < QB_NW; ++w) t += red[w * 32 + lane];
-      pubw[lane] = t;
-      const int64_t gl = g - rbeg;
-      if (gl >= 0 && gl < nloc) pubw[32 + lane] = P[gl * QB_PLD + lane];
+    double* pb = pub + (k & 1) * 64;
+    double* sk = sc + (k & 1) * 64;
+    const int gl = (int)std::max<int64_t>(-1, std::min<int64_t>(g - rbeg, nloc));
+    // first local row > gl owned by this warp
+    const int i0 = gl + 1 + ((warp - (gl + 1)) % 32 + 32) % 32;
+    // s_j = sum_{i > g} P[i][k] P[i][j]  (j > k: trailing dots; j < k: V^T v)
+    double s0 = 0.0, s1 = 0.0;
+    int i = i0;
+    for (; i + 32 < nloc; i += 64) {
+      s0 = fma(P[i * QB_PLD + k], P[i * QB_PLD + lane], s0);
+      s1 = fma(P[(i + 32) * QB_PLD + k], P[(i + 32) * QB_PLD + lane], s1);
     }
+    if (i < nloc) s0 = fma(P[i * QB_PLD + k], P[i * QB_PLD + lane], s0);
+    QR_PROBE(1);
+    red[warp * 32 + lane] = s0 + s1;
+    __syncthreads();
+    QR_PROBE(2);
+    if (warp == 0) {
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+      for (int w = 0; w < QB_NW; w += 4) {
+        t0 += red[w * 32 + lane];
+        t1 += red[(w + 1) * 32 + lane];
+        t2 += red[(w + 2) * 32 + lane];
+        t3 += red[(w + 3) * 32 + lane];
+      }
+      pb[lane] = (t0 + t1) + (t2 + t3);
+      if (gl >= 0 && gl < nloc) pb[32 + lane] = P[gl * QB_PLD + lane];
+    }
+    QR_PROBE(3);
     cluster_sync_all();
-    // gather every CTA's partials (one remote load per thread), then every
-    // thread sums them in fixed CTA order from local shared memory
-    const uint32_t owner = (uint32_t)((g - p.j0) / p.rows_per);
-    for (int e = tid; e < (int)ncta * 32; e += QB_NT) {
-      const uint32_t q = (uint32_t)(e >> 5);
-      allp[e] = ld_dsmem(pubr + (e & 31), q);
-    }
-    if (tid < 32) allp[QB_MAXCL * 32 + tid] = ld_dsmem(pubr + 32 + tid, owner);
-    __syncthreads();
-    double Sj = 0.0, Sk = 0.0;
-    for (uint32_t q = 0; q < ncta; ++q) {
-      Sj += allp[q * 32 + lane];
-      Sk += allp[q * 32 + k];
-    }
-    const double alpha = allp[QB_MAXCL * 32 + k];
-    const double pj = allp[QB_MAXCL * 32 + lane];
-    const double xnorm = sqrt(Sk);
-    double tau, beta, scale;
-    if (xnorm == 0.0) {
-      tau = 0.0;
-      beta = alpha;
-      scale = 0.0;
-    } else {
-      beta = -copysign(hypot(alpha, xnorm), alpha);
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-    const double wj = (lane > k && lane < jb) ? tau * (pj + scale * Sj) : 0.0;
-    // update local rows below the pivot; column k becomes v
-    for (int i = warp; i < nloc; i += QB_NW) {
-      const int64_t gi = rbeg + i;
-      if (gi > g) {
-        const double v = scale * P[i * QB_PLD + k];
-        if (lane == k)
-          P[i * QB_PLD + k] = v;
-        else if (lane > k)
-          P[i * QB_PLD + lane] -= wj * v;
-      } else if (gi == g) {
-        if (lane == k)
-          P[i * QB_PLD + k] = beta;
-        else if (lane > k)
-          P[i * QB_PLD + lane] -= wj;
-      }
-    }
-    if (rank == 0 && tid == 0) {
-      p.tau[g] = tau;
-      p.beta[g] = beta;
-    }
-    __syncthreads();
-  }
-
-  // V^T V partials (explicit V: 1 at its pivot, 0 above) for T: lane b,
-  // 32 register accumulators over a; warps split the rows, then reduce.
-  for (int half = 0; half < 2; ++half) {
-    double ga[16];
-#pragma unroll
-    for (int a = 0; a < 16; ++a) ga[a] = 0.0;
-    for (int i = warp; i < nloc; i += QB_NW) {
-      const int64_t rel = rbeg + i - p.j0;  // row index inside the panel
-      const double vb = rel < lane ? 0.0 : (rel == lane ? 1.0 : P[i * QB_PLD + lane]);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int a = half * 16 + q;
-        const double va = rel < a ? 0.0 : (rel == a ? 1.0 : P[i * QB_PLD + a]);
-        ga[q] = fma(va, vb, ga[q]);
-      }
-    }
-    // fixed-order reduction over warps through shared memory
-    for (int q = 0; q < 16; ++q) {
-      const int a = half * 16 + q;
-      red[warp * 32 + lane] = ga[q];
-      __syncthreads();
-      if (warp == 0) {
-        double t = 0.0;
-        for (int w = 0; w < QB_NW; ++w) t += red[w * 32 + lane];
-        gram[a * QB_NB + lane] = (a < jb && lane < jb) ? t : 0.0;
-      }
-      __syncthreads();
-    }
-  }
-  cluster_sync_all();
-  if (rank == 0) {
-    // G = sum of all CTAs' V^T V partials (parallel remote loads, fixed
-    // CTA order), then dlarft: T[k][k] = tau_k,
-    // T[0:k, k] = -tau_k * T[0:k, 0:k] * G[0:k, k]   (one warp)
-    for (int e = tid; e < QB_NB * QB_NB; e += QB_NT) {
-      double v = 0.0;
-      if ((e / QB_NB) < (e % QB_NB))
-        for (uint32_t q = 0; q < ncta; ++q) v += ld_dsmem(gram + e, q);
-      gsum[e] = v;
-    }
-    __syncthreads();
+    QR_PROBE(4);
     if (warp == 0) {
-      double* T = p.T;
-      for (int k = 0; k < jb; ++k) {
-        const double tk = p.tau[p.j0 + k];
-        double t = 0.0;
-        if (lane < k) {
-          for (int pp = lane; pp < k; ++pp) t = fma(T[pp * 32 + lane], gsum[pp * QB_NB + k], t);
-          t = -tk * t;
+      // sum the CTAs' partials in fixed CTA order (remote loads issued together)
+      const uint32_t owner = (uint32_t)((g - p.j0) / p.rows_per);
+      double part[QB_MAXCL];
+#pragma unroll
+      for (int q = 0; q < QB_MAXCL; ++q) part[q] = q < (int)ncta ? ld_dsmem(pb + lane, q) : 0.0;
+      const double pj = ld_dsmem(pb + 32 + lane, owner);
+      double Sj = 0.0;
+#pragma unroll
+      for (int q = 0; q < QB_MAXCL; ++q) Sj += part[q];
+      const double Sk = __shfl_sync(0xffffffffu, Sj, k);
+      const double alpha = __shfl_sync(0xffffffffu, pj, k);
+      const double xnorm = sqrt(Sk);
+      double tau, beta, scale;
+      if (xnorm == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      sk[lane] = (lane > k && lane < jb) ? tau * (pj + scale * Sj) : 0.0;
+      // V_j^T v_k = V_j[g] + scale * sum_{i>g} V_j[i] x_i  (j < k)
+      G[k * 32 + lane] = lane < k ? pj + scale * Sj : 0.0;
+      if (lane == 0) {
+        sk[32] = scale;
+        sk[33] = beta;
+        if (rank == 0) {
+          p.tau[g] = tau;
+          p.beta[g] = beta;
         }
-        __syncwarp();
-        if (lane < k) T[k * 32 + lane] = t;
-        if (lane == k) T[k * 32 + k] = tk;
-        if (lane > k) T[k * 32 + lane] = 0.0;
-        __syncwarp();
+        Ts[k * 32 + k] = tau;
       }
     }
+    QR_PROBE(5);
+    __syncthreads();
+    QR_PROBE(6);
+    const double wj = sk[lane], scale = sk[32];
+    // update local rows below the pivot; column k becomes v
+    for (int r = i0; r < nloc; r += 32) {
+      const double v = scale * P[r * QB_PLD + k];
+      const double o = P[r * QB_PLD + lane];
+      P[r * QB_PLD + lane] = lane == k ? v : fma(-wj, v, o);
+    }
+    if (gl >= 0 && gl < nloc && warp == (gl & 31)) {
+      const double o = P[gl * QB_PLD + lane];
+      P[gl * QB_PLD + lane] = lane == k ? sk[33] : o - wj;
+    }
+    QR_PROBE(7);
   }
+  __syncthreads();
+
+  // T (dlarft, forward columnwise): T[k][k] = tau_k,
+  // T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k]; one warp, T in shared memory.
+  if (warp == 0) {
+    for (int k = 0; k < jb; ++k) {
+      const double tk = Ts[k * 32 + k];
+      double a0 = 0.0, a1 = 0.0;
+      if (lane < k) {
+        int l = lane;
+        for (; l + 1 < k; l += 2) {
+          a0 = fma(Ts[l * 32 + lane], G[k * 32 + l], a0);
+          a1 = fma(Ts[(l + 1) * 32 + lane], G[k * 32 + l + 1], a1);
+        }
+        if (l < k) a0 = fma(Ts[l * 32 + lane], G[k * 32 + l], a0);
+      }
+      __syncwarp();
+      if (lane != k) Ts[k * 32 + lane] = lane < k ? -tk * (a0 + a1) : 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (rank == 0)
+    for (int e = tid; e < QB_NB * QB_NB; e += QB_NT) p.T[e] = (e / 32) < jb ? Ts[e] : 0.0;
   // write back the panel and the explicit V
   for (int idx = tid; idx < nloc * QB_NB; idx += QB_NT) {
     const int j = idx / nloc, i = idx % nloc;
@@ -229,7 +234,284 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
     p.M[gj * p.ldm + gi] = val;
     p.V[gj * p.ldm + gi] = gi < gj ? 0.0 : (gi == gj ? 1.0 : val);
   }
+  QR_PROBE(8);
   cluster_sync_all();  // keep shared memory alive for remote readers
+  QR_PROBE(9);
+  QR_PROBE_FLUSH;
+}
+
+// Register-resident panel factorisation: the production panel kernel.
+//
+// Rows of the panel [j0, d) x [j0, j0 + jb) are split into the HEAD (rows
+// j0 .. j0+jb-1, which hold every pivot of the panel; CTA 0, two rows per
+// warp) and the TAIL (rows below, spread over the cluster's CTAs, RPW rows
+// per warp).  Thread (warp w, lane j) keeps column j of its rows in
+// registers for the whole panel, so the per-column dot products and updates
+// never touch shared memory; the pivot-column value of a row comes from lane
+// k by a shuffle.  Tail rows lie below every pivot, so their updates carry
+// no row predicates: P <- P - w_j (scale * x).  Column k itself is left
+// unscaled (w_j = 0 for j <= k) and scaled by scale_k at write-back; the
+// V^T v products the T factor needs come from the same dot products
+// (lanes j < k), corrected by scale_j.
+//
+// Per column the only cross-CTA exchange is a push: each CTA reduces its 16
+// warp partials and bulk-copies the 32 column sums into every CTA's inbox
+// (cp.async.bulk shared::cta -> shared::cluster, completing on the
+// receiver's mbarrier); CTA 0 also pushes the pivot row.  No cluster-wide
+// barrier per column.  Double-buffered by column parity (see the ordering
+// argument at the buffers).
+constexpr int QR_NT2 = 512;
+constexpr int QR_NW2 = QR_NT2 / 32;
+// extra shared memory of the register panel (doubles): inbox[2][16][32],
+// inrow[2][32], red[16][32], G[32][32], Ts[32][32], colscale[32],
+// sc[2][128], mbarriers
+constexpr int QR2_SMEM_EXTRA = 2 * QB_MAXCL * 32 + 64 + 512 + 1024 + 1024 + 32 + 256 + 8;
+
+// staging doubles, even so the buffers after it stay 16-byte aligned
+__host__ __device__ inline size_t qr2_staging(int rows_per) {
+  return ((size_t)(rows_per > 32 ? rows_per : 32) * QB_PLD + 1) & ~(size_t)1;
+}
+
+template <int RPW>
+__global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams p) {
+  constexpr bool KEEPX = RPW <= 16;
+  extern __shared__ __align__(16) double qsm[];
+  const uint32_t rank = cta_rank_in_cluster();
+  const uint32_t ncta = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jb = p.jb;
+  const int64_t tail0 = p.j0 + jb;                         // first tail row
+  const int64_t tbeg = tail0 + (int64_t)rank * p.rows_per;
+  const int nt = (int)std::max<int64_t>(0, std::min<int64_t>(p.rows_per, p.d - tbeg));
+  const bool head = rank == 0;
+
+  double* S = qsm;                                         // staging [max(rows_per, 32)][QB_PLD]
+  double* inbox = S + qr2_staging(p.rows_per);             // [2][16][32]
+  double* inrow = inbox + 2 * QB_MAXCL * 32;               // [2][32]
+  double* red = inrow + 64;                                // [16][32]
+  double* G = red + 512;                                   // [32][32]: column k = V^T v_k
+  double* Ts = G + 1024;                                   // [32][32]
+  double* colscale = Ts + 1024;                            // [32]
+  double* sc = colscale + 32;                              // [2][128]: w_j scale, w_j, beta
+  uint64_t* mb = reinterpret_cast<uint64_t*>(sc + 256);    // [2]
+  QR_PROBE_INIT
+
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    fence_mbar_init();
+  }
+  // stage tail rows (coalesced along rows), then the head rows
+  for (int idx = tid; idx < nt * QB_NB; idx += QR_NT2) {
+    const int j = idx / nt, i = idx % nt;
+    S[i * QB_PLD + j] = j < jb ? p.M[(p.j0 + j) * p.ldm + tbeg + i] : 0.0;
+  }
+  __syncthreads();
+  double P[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int li = r * QR_NW2 + warp;
+    P[r] = li < nt ? S[li * QB_PLD + lane] : 0.0;
+  }
+  __syncthreads();
+  double H0 = 0.0, H1 = 0.0;  // head rows warp and warp + 16 (CTA 0)
+  if (head) {
+    for (int idx = tid; idx < 32 * QB_NB; idx += QR_NT2) {
+      const int j = idx / 32, i = idx % 32;
+      S[i * QB_PLD + j] = (j < jb && i < jb) ? p.M[(p.j0 + j) * p.ldm + p.j0 + i] : 0.0;
+    }
+    __syncthreads();
+    H0 = S[warp * QB_PLD + lane];
+    H1 = S[(warp + 16) * QB_PLD + lane];
+  }
+  cluster_sync_all();  // barriers initialised everywhere before any push
+  // pivot row of column 0 -> every CTA's inrow[0]
+  if (head && warp == 0)
+    for (uint32_t q = 0; q < ncta; ++q)
+      st_async_f64(mapa_u32(smem_u32(inrow + lane), q), H0, mapa_u32(smem_u32(&mb[0]), q));
+  QR_PROBE(0);
+  double myscale = 0.0;  // warp 0: scale of column `lane`
+
+  for (int k = 0; k < jb; ++k) {
+    const int b = k & 1;
+    // ---- dot products s_j = sum_{i > pivot} x_i P_i[j]
+    double xs[KEEPX ? RPW : 1];
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const double x = __shfl_sync(0xffffffffu, P[r], k);
+      if (KEEPX) xs[r & (KEEPX ? RPW - 1 : 0)] = x;
+      if (r & 1)
+        s1 = fma(x, P[r], s1);
+      else
+        s0 = fma(x, P[r], s0);
+    }
+    double xh0 = 0.0, xh1 = 0.0;
+    if (head) {
+      xh0 = __shfl_sync(0xffffffffu, H0, k);
+      xh1 = __shfl_sync(0xffffffffu, H1, k);
+      if (warp > k) s0 = fma(xh0, H0, s0);
+      if (warp + 16 > k) s1 = fma(xh1, H1, s1);
+    }
+    QR_PROBE(1);
+    red[warp * 32 + lane] = s0 + s1;
+    __syncthreads();
+    QR_PROBE(2);
+    if (warp == 0) {
+      // Buffers of parity b are rewritten only at column k + 2: by then this
+      // CTA has received every CTA's column-(k+1) push, each sent after that
+      // CTA finished column k, i.e. after our column-k copies into it landed
+      // and after it read its column-k inbox.
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+      for (int w = 0; w < QR_NW2; w += 4) {
+        t0 += red[w * 32 + lane];
+        t1 += red[(w + 1) * 32 + lane];
+        t2 += red[(w + 2) * 32 + lane];
+        t3 += red[(w + 3) * 32 + lane];
+      }
+      const double tot = (t0 + t1) + (t2 + t3);
+      if (lane == 0) mbar_arrive_expect_tx(&mb[b], (ncta + 1) * 256);
+      // push the column sums: lane j stores s_j into every CTA's inbox
+      const uint32_t dst = smem_u32(inbox + (b * QB_MAXCL + rank) * 32 + lane);
+      const uint32_t mbl = smem_u32(&mb[b]);
+      for (uint32_t q = 0; q < ncta; ++q) st_async_f64(mapa_u32(dst, q), tot, mapa_u32(mbl, q));
+      QR_PROBE(3);
+      mbar_wait_cluster(&mb[b], (uint32_t)((k >> 1) & 1));
+      QR_PROBE(4);
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+      const double* ib = inbox + b * QB_MAXCL * 32 + lane;
+      uint32_t q = 0;
+      for (; q + 3 < ncta; q += 4) {
+        u0 += ib[q * 32];
+        u1 += ib[(q + 1) * 32];
+        u2 += ib[(q + 2) * 32];
+        u3 += ib[(q + 3) * 32];
+      }
+      for (; q < ncta; ++q) u0 += ib[q * 32];
+      const double Sj = (u0 + u1) + (u2 + u3);
+      const double pj = inrow[b * 32 + lane];
+      const double Sk = __shfl_sync(0xffffffffu, Sj, k);
+      const double alpha = __shfl_sync(0xffffffffu, pj, k);
+      double tau, beta, scale;
+      if (Sk == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        beta = -copysign(sqrt(fma(alpha, alpha, Sk)), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      if (lane == k) myscale = scale;
+      // rows below the pivot: P_i[j] -= (w_j scale) x_i; the pivot row: -= w_j
+      const double wv = (lane > k && lane < jb) ? tau * (pj + scale * Sj) : 0.0;
+      sc[b * 128 + lane] = wv * scale;
+      sc[b * 128 + 32 + lane] = wv;
+      // V_j^T v_k = scale_j (U_j[g] + scale_k sum_{i>g} U_j[i] x_i), U unscaled
+      G[k * 32 + lane] = lane < k ? myscale * (pj + scale * Sj) : 0.0;
+      if (lane == 0) {
+        sc[b * 128 + 64] = beta;
+        colscale[k] = scale;
+        Ts[k * 32 + k] = tau;
+        if (head) {
+          p.tau[p.j0 + k] = tau;
+          p.beta[p.j0 + k] = beta;
+        }
+      }
+    }
+    QR_PROBE(5);
+    __syncthreads();
+    QR_PROBE(6);
+    const double ws = sc[b * 128 + lane];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const double x = KEEPX ? xs[r & (KEEPX ? RPW - 1 : 0)] : __shfl_sync(0xffffffffu, P[r], k);
+      P[r] = fma(-ws, x, P[r]);
+    }
+    if (head) {
+      const double wj = sc[b * 128 + 32 + lane], beta = sc[b * 128 + 64];
+      if (warp > k) H0 = fma(-ws, xh0, H0);
+      else if (warp == k) H0 = lane == k ? beta : H0 - wj;
+      if (warp + 16 > k) H1 = fma(-ws, xh1, H1);
+      else if (warp + 16 == k) H1 = lane == k ? beta : H1 - wj;
+      // push the next pivot row into every CTA's inrow (its mbarrier for
+      // column k + 1 is in that phase: its column k - 1 wait completed before
+      // it sent the column-k sums this CTA has received)
+      if (k + 1 < jb && warp == ((k + 1) & 15)) {
+        const int bn = (k + 1) & 1;
+        const double rv = (k + 1) < 16 ? H0 : H1;
+        const uint32_t dst = smem_u32(inrow + bn * 32 + lane), mbl = smem_u32(&mb[bn]);
+        for (uint32_t q = 0; q < ncta; ++q) st_async_f64(mapa_u32(dst, q), rv, mapa_u32(mbl, q));
+      }
+    }
+    QR_PROBE(7);
+  }
+
+  // ---- write back: column j rows below its pivot are scale_j * stored
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int li = r * QR_NW2 + warp;
+    if (li < nt) S[li * QB_PLD + lane] = P[r];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nt * QB_NB; idx += QR_NT2) {
+    const int j = idx / nt, i = idx % nt;
+    if (j >= jb) continue;
+    const int64_t gi = tbeg + i, gj = p.j0 + j;
+    const double val = colscale[j] * S[i * QB_PLD + j];
+    p.M[gj * p.ldm + gi] = val;
+    p.V[gj * p.ldm + gi] = val;
+  }
+  QR_PROBE(10);
+  if (head) {
+    __syncthreads();
+    S[warp * QB_PLD + lane] = H0;
+    S[(warp + 16) * QB_PLD + lane] = H1;
+    __syncthreads();
+    for (int idx = tid; idx < jb * QB_NB; idx += QR_NT2) {
+      const int j = idx / jb, i = idx % jb;
+      if (j >= jb) continue;
+      const int64_t gi = p.j0 + i, gj = p.j0 + j;
+      const double raw = S[i * QB_PLD + j];
+      const double val = i > j ? colscale[j] * raw : raw;
+      p.M[gj * p.ldm + gi] = val;
+      p.V[gj * p.ldm + gi] = i < j ? 0.0 : (i == j ? 1.0 : val);
+    }
+    // T (dlarft, forward columnwise): T[k][k] = tau_k,
+    // T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k].  One warp; lane j keeps row
+    // j of T in registers, G[., k] is read by broadcast.
+    if (warp == 0) {
+      double Trow[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) Trow[l] = 0.0;
+      for (int k = 0; k < jb; ++k) {
+        const double tk = Ts[k * 32 + k];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 32; l += 4) {
+          a0 = fma(Trow[l], G[k * 32 + l], a0);      // G[l][k] = 0 for l >= k
+          a1 = fma(Trow[l + 1], G[k * 32 + l + 1], a1);
+          a2 = fma(Trow[l + 2], G[k * 32 + l + 2], a2);
+          a3 = fma(Trow[l + 3], G[k * 32 + l + 3], a3);
+        }
+        const double t = lane < k ? -tk * ((a0 + a1) + (a2 + a3)) : (lane == k ? tk : 0.0);
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+          if (l == k) Trow[l] = t;
+      }
+#pragma unroll
+      for (int l = 0; l < 32; ++l) Ts[l * 32 + lane] = Trow[l];
+    }
+    QR_PROBE(11);
+    __syncthreads();
+    for (int e = tid; e < QB_NB * QB_NB; e += QR_NT2) p.T[e] = (e / 32) < jb ? Ts[e] : 0.0;
+  }
+  QR_PROBE(8);
+  cluster_sync_all();  // every push into this CTA has landed and been read
+  QR_PROBE(9);
+  QR_PROBE_FLUSH;
 }
 
 // Partial W = V^T C over a row range: part[s][c][k] = sum_i V[i][k] C[i][c]
@@ -372,31 +654,57 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
                       double* V, double* Tall, double* W, double* W2, double* part,
                       int64_t part_cap, cudaStream_t st) {
   static bool attr_set = false;
+  const int smem_max = (int)(QB_SMEM_EXTRA + QB_MAXROWS * QB_PLD) * (int)sizeof(double);
   if (!attr_set) {
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SKL_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(QB_SMEM_EXTRA + QB_MAXROWS * QB_PLD) * (int)sizeof(double)));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     attr_set = true;
   }
+  static const bool smem_panel = getenv("SKL_QR_SMEM_PANEL") != nullptr;
   for (int64_t j0 = 0; j0 < n; j0 += QB_NB) {
     const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
-    int rows_per = 0;
-    const int cl = panel_cluster(d - j0, &rows_per);
-    SKL_REQUIRE(cl > 0, SKL_ERR_INVALID, "qr panel does not fit the cluster");
-    PanelParams pp{M, ldm, d, j0, jb, rows_per, V, Tall + (j0 / QB_NB) * 32 * 32, tau, beta};
+    const int64_t tail = d - j0 - jb;
+    // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
+    int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + 127) / 128));
+    const int rows2 = (int)((tail + cl2 - 1) / cl2);
+    const int rpw = (rows2 + QR_NW2 - 1) / QR_NW2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(QB_NT);
-    cfg.dynamicSmemBytes = (size_t)(rows_per * QB_PLD + QB_SMEM_EXTRA) * sizeof(double);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, pp));
+    if (!smem_panel && rpw <= 32) {
+      PanelParams pp{M, ldm, d, j0, jb, rows2, V, Tall + (j0 / QB_NB) * 32 * 32, tau, beta};
+      cfg.gridDim = dim3(cl2);
+      cfg.blockDim = dim3(QR_NT2);
+      cfg.dynamicSmemBytes = (qr2_staging(rows2) + QR2_SMEM_EXTRA) * sizeof(double);
+      attr[0].val.clusterDim.x = cl2;
+      if (rpw <= 8)
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<8>, pp));
+      else if (rpw <= 16)
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<16>, pp));
+      else
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<32>, pp));
+    } else {
+      int rows_per = 0;
+      const int cl = panel_cluster(d - j0, &rows_per);
+      SKL_REQUIRE(cl > 0, SKL_ERR_INVALID, "qr panel does not fit the cluster");
+      PanelParams pp{M, ldm, d, j0, jb, rows_per, V, Tall + (j0 / QB_NB) * 32 * 32, tau, beta};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(QB_NT);
+      cfg.dynamicSmemBytes = (size_t)(rows_per * QB_PLD + QB_SMEM_EXTRA) * sizeof(double);
+      attr[0].val.clusterDim.x = cl;
+      SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, pp));
+    }
     const int64_t c0 = j0 + jb;
     const int64_t nc = (n + 1) - c0;  // trailing columns incl. Sb
     if (nc <= 0) continue;
@@ -413,6 +721,18 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
                                         rows, nc);
     SKL_CUDA_LAUNCH();
   }
+#ifdef SKL_QR_PROBE
+  {
+    unsigned long long h[12] = {}, z[12] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_qr_probe, sizeof(h));
+    cudaMemcpyToSymbol(g_qr_probe, z, sizeof(z));
+    fprintf(stderr, "qr panel probe d=%lld n=%lld (cycles, CTA 0 thread 0, all panels):",
+            (long long)d, (long long)n);
+    for (int i = 0; i < 12; ++i) fprintf(stderr, " %llu", h[i]);
+    fprintf(stderr, "\n");
+  }
+#endif
   return SKL_OK;
 }
 

@@ -154,7 +154,7 @@ extern "C" int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t
   const bool vec = ((uintptr_t)A & 15) == 0 && lda % 2 == 0;
   const int blocks = rs_grid(vec ? (m + 1) / 2 : m);
   double* part = nullptr;
-  SKL_CUDA(cudaMallocAsync(&part, (blocks + 1) * sizeof(double), st));
+  SKL_CUDA(malloc_async(&part, (blocks + 1) * sizeof(double), st));
   if (vec) {
     const size_t smem = n <= RS_XMAX ? n * sizeof(double) : 0;
     if (smem > 48 * 1024)
@@ -183,7 +183,7 @@ extern "C" int skl_residual_csr(const int64_t* indptr, const int64_t* indices,
               "residual_csr: bad arguments");
   const int blocks = rs_grid(m);
   double* part = nullptr;
-  SKL_CUDA(cudaMallocAsync(&part, (blocks + 1) * sizeof(double), st));
+  SKL_CUDA(malloc_async(&part, (blocks + 1) * sizeof(double), st));
   residual_csr_kernel<<<blocks, RS_NT, 0, st>>>(indptr, indices, values, m, x, b, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

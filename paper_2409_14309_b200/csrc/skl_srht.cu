@@ -316,7 +316,7 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   p.inv_scale_div = std::sqrt((double)d);
   double* part = nullptr;
   if (P > 1) {
-    SKL_CUDA(cudaMallocAsync(&part, (size_t)P * n * d * sizeof(double), st));
+    SKL_CUDA(malloc_async(&part, (size_t)P * n * d * sizeof(double), st));
     p.part = part;
   }
   dim3 grid((unsigned)n, (unsigned)P);
