@@ -189,51 +189,85 @@ __global__ void __launch_bounds__(1024) qr_backsolve_kernel(const double* M, int
   }
 }
 
-// Blocked back substitution for large n: 32 x 32 diagonal blocks solved by
-// one warp (x_j broadcast by shuffles), the rows above updated by the whole
-// CTA with one 32-term dot product per row.  R = sign-normalised upper
-// triangle of the factored M (ld ldm).
-__global__ void __launch_bounds__(1024) qr_backsolve_blocked_kernel(const double* M, int64_t ldm,
+// Blocked back substitution: 32 x 32 diagonal blocks from the bottom.  Warp
+// 0 preloads the block (lane r holds row r of R in registers) and solves it
+// with shuffles (x_j = y_j * (1 / R_jj) in dtrsv's column order); then every
+// thread updates one row above the block with a 32-term dot product whose
+// loads are all in flight together.  R = sign-normalised upper triangle of
+// the factored M (ld ldm): R_ij = sign(beta_i) M_ij, R_ii = |beta_i|.
+__global__ void __launch_bounds__(512) qr_backsolve_blocked_kernel(const double* M, int64_t ldm,
                                                                     int64_t n, const double* beta,
                                                                     const double* y_in, double* x) {
   extern __shared__ double ys[];
   __shared__ double xb[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef SKL_QR_PROBE
+  long long pb0 = 0, pb1 = 0, pb2 = 0, tq = clock64();
+#endif
   for (int64_t i = tid; i < n; i += blockDim.x) ys[i] = y_in[i];
   __syncthreads();
   for (int64_t hi = n; hi > 0; hi -= 32) {
     const int64_t lo = hi > 32 ? hi - 32 : 0;
     const int w = (int)(hi - lo);
     if (warp == 0) {
-      // lane r holds row lo + r of the diagonal block
       const int64_t row = lo + lane;
-      const double sgr = (lane < w && beta[row] < 0.0) ? -1.0 : 1.0;
-      double yr = lane < w ? ys[row] : 0.0;
+      const bool live = lane < w;
+      const double sgr = (live && beta[row] < 0.0) ? -1.0 : 1.0;
+      double Rr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        Rr[j] = (live && j > lane && j < w) ? sgr * M[(lo + j) * ldm + row] : 0.0;
+      // reciprocals of the diagonal in parallel; the solve chain is then a
+      // multiply, a shuffle and an FMA per column
+      const double rinv = live ? 1.0 / fabs(beta[row]) : 1.0;
+      double yr = live ? ys[row] : 0.0;
       double xr = 0.0;
-      for (int j = w - 1; j >= 0; --j) {
-        const int64_t col = lo + j;
-        double rij = 0.0;
-        if (lane < j) rij = sgr * M[col * ldm + row];
-        const double rjj = fabs(beta[col]);
-        const double yj = __shfl_sync(0xffffffffu, yr, j);
-        const double xj = yj / rjj;
-        if (lane == j) xr = xj;
-        if (lane < j) yr -= xj * rij;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < w) {
+          if (lane == j) xr = yr * rinv;
+          const double xj = __shfl_sync(0xffffffffu, xr, j);
+          yr = fma(-xj, Rr[j], yr);  // Rr[j] = 0 unless lane < j
+        }
       }
-      if (lane < w) {
-        x[lo + lane] = xr;
+      if (live) {
+        x[row] = xr;
         xb[lane] = xr;
       }
     }
+#ifdef SKL_QR_PROBE
+    if (tid == 0) { long long t = clock64(); pb0 += t - tq; tq = t; }
+#endif
     __syncthreads();
+#ifdef SKL_QR_PROBE
+    if (tid == 0) { long long t = clock64(); pb1 += t - tq; tq = t; }
+#endif
     for (int64_t i = tid; i < lo; i += blockDim.x) {
       const double sgi = beta[i] < 0.0 ? -1.0 : 1.0;
-      double t = 0.0;
-      for (int j = 0; j < w; ++j) t = fma(sgi * M[(lo + j) * ldm + i], xb[j], t);
-      ys[i] -= t;
+      // 16 loads in flight per group (one column stride apart)
+      const double* mp = M + lo * ldm + i;
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll 1
+      for (int g = 0; g < 32; g += 16) {
+        double mv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mv[j] = (g + j) < w ? mp[(g + j) * ldm] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          t0 = fma(mv[j], xb[g + j], t0);
+          t1 = fma(mv[j + 1], xb[g + j + 1], t1);
+        }
+      }
+      ys[i] -= sgi * (t0 + t1);
     }
     __syncthreads();
+#ifdef SKL_QR_PROBE
+    if (tid == 0) { long long t = clock64(); pb2 += t - tq; tq = t; }
+#endif
   }
+#ifdef SKL_QR_PROBE
+  if (tid == 0) printf("backsolve n=%lld cycles: diag %lld sync %lld update %lld\n", (long long)n, pb0, pb1, pb2);
+#endif
 }
 
 // Q = H_0 H_1 ... H_{n-1} [I; 0] by backward accumulation (dorg2r), one
@@ -369,7 +403,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
                oW = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oW2 = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oQ = (blocked && Q) ? take((size_t)ldm * n * 8) : 0;
-  const int64_t part_cap = blocked ? 32 * (n + 1) * 320 : 0;  // up to 320 row splits
+  const int64_t part_cap = blocked ? 32 * (n + 1) * ((d + 63) / 64) : 0;  // 64-row splits
   const size_t oP = blocked ? take((size_t)part_cap * 8) : 0;
   unsigned char* ws = nullptr;
   SKL_CUDA(malloc_async(&ws, off, st));
@@ -401,7 +435,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
       rc = qr_blocked_factor(M, ldm, d, n, tau, beta, V, T, W, W2, Pw, part_cap, st);
       if (rc) break;
       qr_finish_kernel<<<1, 256, 0, st>>>(M, ldm, n, beta, fro2, R, ldr, y, badc, badv);
-      qr_backsolve_blocked_kernel<<<1, 1024, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
+      qr_backsolve_blocked_kernel<<<1, 512, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
       if (Q) {
         double* Qw = (double*)(ws + oQ);
         const int64_t tot = d * n;

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "skl_common.h"
 #include "skl_ptx.cuh"
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
   QR_PROBE_INIT
 
   // load the panel slice (column-major source -> row-major smem)
+  #pragma unroll 8
   for (int idx = tid; idx < nloc * QB_NB; idx += QB_NT) {
     const int j = idx / nloc, i = idx % nloc;  // coalesced along rows
     P[i * QB_PLD + j] = j < jb ? p.M[(p.j0 + j) * p.ldm + rbeg + i] : 0.0;
@@ -224,8 +226,10 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
   }
   __syncthreads();
   if (rank == 0)
+    #pragma unroll 8
     for (int e = tid; e < QB_NB * QB_NB; e += QB_NT) p.T[e] = (e / 32) < jb ? Ts[e] : 0.0;
   // write back the panel and the explicit V
+  #pragma unroll 8
   for (int idx = tid; idx < nloc * QB_NB; idx += QB_NT) {
     const int j = idx / nloc, i = idx % nloc;
     if (j >= jb) continue;
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     fence_mbar_init();
   }
   // stage tail rows (coalesced along rows), then the head rows
+  #pragma unroll 8
   for (int idx = tid; idx < nt * QB_NB; idx += QR_NT2) {
     const int j = idx / nt, i = idx % nt;
     S[i * QB_PLD + j] = j < jb ? p.M[(p.j0 + j) * p.ldm + tbeg + i] : 0.0;
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   __syncthreads();
   double H0 = 0.0, H1 = 0.0;  // head rows warp and warp + 16 (CTA 0)
   if (head) {
+    #pragma unroll 8
     for (int idx = tid; idx < 32 * QB_NB; idx += QR_NT2) {
       const int j = idx / 32, i = idx % 32;
       S[i * QB_PLD + j] = (j < jb && i < jb) ? p.M[(p.j0 + j) * p.ldm + p.j0 + i] : 0.0;
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     if (li < nt) S[li * QB_PLD + lane] = P[r];
   }
   __syncthreads();
+  #pragma unroll 8
   for (int idx = tid; idx < nt * QB_NB; idx += QR_NT2) {
     const int j = idx / nt, i = idx % nt;
     if (j >= jb) continue;
@@ -470,6 +477,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     S[warp * QB_PLD + lane] = H0;
     S[(warp + 16) * QB_PLD + lane] = H1;
     __syncthreads();
+    #pragma unroll 8
     for (int idx = tid; idx < jb * QB_NB; idx += QR_NT2) {
       const int j = idx / jb, i = idx % jb;
       if (j >= jb) continue;
@@ -506,6 +514,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     }
     QR_PROBE(11);
     __syncthreads();
+    #pragma unroll 8
     for (int e = tid; e < QB_NB * QB_NB; e += QR_NT2) p.T[e] = (e / 32) < jb ? Ts[e] : 0.0;
   }
   QR_PROBE(8);
@@ -514,103 +523,32 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   QR_PROBE_FLUSH;
 }
 
-// Partial W = V^T C over a row range: part[s][c][k] = sum_i V[i][k] C[i][c]
-// for the rows of split s.  Grid (ceil(nc/32), S); one CTA = 32 columns.
-__global__ void __launch_bounds__(256) qr_vtc_kernel(const double* V, int64_t ldv, const double* C,
-                                                     int64_t ldc, int jb, int64_t rows, int64_t nc,
-                                                     int S, double* part) {
-  __shared__ double Vs[32][33];
-  __shared__ double Cs[32][33];
-  const int64_t c0 = (int64_t)blockIdx.x * 32;
-  const int s = blockIdx.y;
-  const int64_t ib = rows * s / S, ie = rows * (s + 1) / S;
-  const int tid = threadIdx.x, k = tid & 31, cq = (tid >> 5) * 4;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t i0 = ib; i0 < ie; i0 += 32) {
-    for (int e = tid; e < 1024; e += 256) {
-      const int col = e >> 5, r = e & 31;
-      const int64_t i = i0 + r;
-      Vs[r][col] = (i < ie && col < jb) ? V[col * ldv + i] : 0.0;
-      Cs[r][col] = (i < ie && c0 + col < nc) ? C[(c0 + col) * ldc + i] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) {
-      const double v = Vs[r][k];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(v, Cs[r][cq + q], acc[q]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (c0 + cq + q < nc) part[((int64_t)s * nc + c0 + cq + q) * 32 + k] = acc[q];
-}
-
-// W[c][k] = sum_s part[s][c][k] in fixed split order
-__global__ void qr_vtc_reduce_kernel(const double* part, int S, int64_t nc, double* W) {
-  const int64_t total = nc * 32;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    double v = 0.0;
-    for (int q = 0; q < S; ++q) v += part[(int64_t)q * total + idx];
-    W[idx] = v;
-  }
-}
-
-// W = V^T C for the block reflector (rows x jb times rows x nc)
-static int qr_vtc(const double* V, int64_t ldv, const double* C, int64_t ldc, int jb, int64_t rows,
-                  int64_t nc, double* W, double* part, int64_t part_cap, cudaStream_t st) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tiles = (nc + 31) / 32;
-  int64_t S = std::max<int64_t>(1, std::min<int64_t>(rows / 256, (2 * sms + tiles - 1) / tiles));
-  S = std::min<int64_t>(S, part_cap / (nc * 32));
-  S = std::max<int64_t>(S, 1);
-  qr_vtc_kernel<<<dim3((unsigned)tiles, (unsigned)S), 256, 0, st>>>(V, ldv, C, ldc, jb, rows, nc,
-                                                                    (int)S, part);
-  SKL_CUDA_LAUNCH();
-  const int64_t tot = nc * 32;
-  qr_vtc_reduce_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(
-      part, (int)S, nc, W);
-  SKL_CUDA_LAUNCH();
-  return SKL_OK;
-}
-
-// W2 = T^T W  (T upper, jb x jb, ld 32; W jb x nc, ld 32)
-__global__ void qr_apply_tt_kernel(const double* T, const double* W, double* W2, int jb, int64_t nc,
-                                   int transpose) {
-  const int64_t total = (int64_t)jb * nc;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = idx / jb;
-    const int k = (int)(idx % jb);
-    double s = 0.0;
-    if (transpose) {  // (T^T W)[k] = sum_{l <= k} T[l][k] W[l]
-      for (int l = 0; l <= k; ++l) s = fma(T[k * 32 + l], W[c * 32 + l], s);
-    } else {          // (T W)[k] = sum_{l >= k} T[k][l] W[l]
-      for (int l = k; l < jb; ++l) s = fma(T[l * 32 + k], W[c * 32 + l], s);
-    }
-    W2[c * 32 + k] = s;
-  }
-}
-
 // C[rows x nc] -= V[rows x jb] * W2[jb x nc]; 64 x 64 tiles, 4 x 4 per thread.
-__global__ void __launch_bounds__(256) qr_update_kernel(double* C, int64_t ldc, const double* V,
-                                                        int64_t ldv, const double* W2, int jb,
+__global__ void __launch_bounds__(256) qr_update_kernel(double* __restrict__ C, int64_t ldc,
+                                                        const double* __restrict__ V, int64_t ldv,
+                                                        const double* __restrict__ W2, int jb,
                                                         int64_t rows, int64_t nc) {
   __shared__ double Vs[32][64 + 1];
   __shared__ double Ws[32][64 + 1];
   const int64_t i0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
   const int tid = threadIdx.x;
+  const int tr = tid % 16, tc = tid / 16;  // rows tr + 16a, cols tc + 16b
+  // the 16 outputs are fetched first: their latency overlaps the staging
+  double cv[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + tr + 16 * a, c = c0 + tc + 16 * b;
+      cv[a][b] = (i < rows && c < nc) ? C[c * ldc + i] : 0.0;
+    }
+#pragma unroll
   for (int e = tid; e < 32 * 64; e += 256) {
     const int k = e / 64, r = e % 64;
     Vs[k][r] = (k < jb && i0 + r < rows) ? V[(int64_t)k * ldv + i0 + r] : 0.0;
     Ws[k][r] = (k < jb && c0 + r < nc) ? W2[(c0 + r) * 32 + k] : 0.0;
   }
   __syncthreads();
-  const int tr = tid % 16, tc = tid / 16;  // rows tr + 16a, cols tc + 16b
   double acc[4][4] = {};
 #pragma unroll 8
   for (int k = 0; k < 32; ++k) {
@@ -629,8 +567,97 @@ __global__ void __launch_bounds__(256) qr_update_kernel(double* C, int64_t ldc, 
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t i = i0 + tr + 16 * a, c = c0 + tc + 16 * b;
-      if (i < rows && c < nc) C[c * ldc + i] -= acc[a][b];
+      if (i < rows && c < nc) C[c * ldc + i] = cv[a][b] - acc[a][b];
     }
+}
+
+// Trailing update, pass 1: partial W = V^T C over 64-row splits.  Each CTA
+// loads its whole 64 x 32 slice of V and of C (one 32-column tile) at once,
+// so a split costs one memory latency; grid (column tiles, splits).
+constexpr int QV_ROWS = 64;
+__global__ void __launch_bounds__(256) qr_vtc64_kernel(const double* __restrict__ V, int64_t ldv,
+                                                       const double* __restrict__ C, int64_t ldc,
+                                                       int jb, int64_t rows, int64_t nc,
+                                                       double* __restrict__ part) {
+  __shared__ double Vs[QV_ROWS][33];
+  __shared__ double Cs[QV_ROWS][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int s = blockIdx.y;
+  const int64_t ib = (int64_t)s * QV_ROWS;
+  const int nr = (int)std::min<int64_t>(QV_ROWS, rows - ib);
+  const int tid = threadIdx.x;
+  #pragma unroll
+  for (int e = tid; e < QV_ROWS * 32; e += 256) {
+    const int col = e / QV_ROWS, r = e % QV_ROWS;
+    Vs[r][col] = (r < nr && col < jb) ? V[col * ldv + ib + r] : 0.0;
+    Cs[r][col] = (r < nr && c0 + col < nc) ? C[(c0 + col) * ldc + ib + r] : 0.0;
+  }
+  __syncthreads();
+  const int k = tid & 31, cq = (tid >> 5) * 4;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 16
+  for (int r = 0; r < QV_ROWS; ++r) {
+    const double v = Vs[r][k];
+    a0 = fma(v, Cs[r][cq], a0);
+    a1 = fma(v, Cs[r][cq + 1], a1);
+    a2 = fma(v, Cs[r][cq + 2], a2);
+    a3 = fma(v, Cs[r][cq + 3], a3);
+  }
+  double* out = part + ((int64_t)s * nc + c0) * 32;
+  if (c0 + cq < nc) out[(cq + 0) * 32 + k] = a0;
+  if (c0 + cq + 1 < nc) out[(cq + 1) * 32 + k] = a1;
+  if (c0 + cq + 2 < nc) out[(cq + 2) * 32 + k] = a2;
+  if (c0 + cq + 3 < nc) out[(cq + 3) * 32 + k] = a3;
+}
+
+// Pass 2: W = sum of the S partials (fixed split order), W2 = T' W
+// (T' = T^T when factoring, T when forming Q).  8 columns per CTA.
+__global__ void __launch_bounds__(256) qr_reduce_tt_kernel(const double* __restrict__ part, int S,
+                                                           int64_t nc, const double* __restrict__ T,
+                                                           int jb, int transpose,
+                                                           double* __restrict__ W2) {
+  __shared__ double Tsm[32][33];
+  __shared__ double Wsm[8][33];
+  const int tid = threadIdx.x, k = tid & 31, cl = tid >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 8 + cl;
+  #pragma unroll
+  for (int e = tid; e < 1024; e += 256) Tsm[e & 31][e >> 5] = T[e];  // Tsm[row][col]
+  double w0 = 0.0, w1 = 0.0;
+  if (c < nc) {
+    int q = 0;
+#pragma unroll 8
+    for (; q + 1 < S; q += 2) {
+      w0 += part[((int64_t)q * nc + c) * 32 + k];
+      w1 += part[((int64_t)(q + 1) * nc + c) * 32 + k];
+    }
+    if (q < S) w0 += part[((int64_t)q * nc + c) * 32 + k];
+  }
+  Wsm[cl][k] = w0 + w1;
+  __syncthreads();
+  if (c >= nc) return;
+  double u = 0.0;
+  if (k < jb) {
+    if (transpose)
+      for (int l = 0; l <= k; ++l) u = fma(Tsm[l][k], Wsm[cl][l], u);
+    else
+      for (int l = k; l < jb; ++l) u = fma(Tsm[k][l], Wsm[cl][l], u);
+  }
+  W2[c * 32 + k] = u;
+}
+
+// W2 = T' V^T C for the block reflector (rows x jb, rows x nc)
+static int qr_wt(const double* V, int64_t ldv, const double* C, int64_t ldc, int jb, int64_t rows,
+                 int64_t nc, const double* T, int transpose, double* W2, double* part,
+                 int64_t part_cap, cudaStream_t st) {
+  const int64_t S = (rows + QV_ROWS - 1) / QV_ROWS;
+  SKL_REQUIRE(S * nc * 32 <= part_cap, SKL_ERR_INVALID, "qr: partial buffer too small");
+  qr_vtc64_kernel<<<dim3((unsigned)((nc + 31) / 32), (unsigned)S), 256, 0, st>>>(V, ldv, C, ldc,
+                                                                              jb, rows, nc, part);
+  SKL_CUDA_LAUNCH();
+  qr_reduce_tt_kernel<<<(unsigned)((nc + 7) / 8), 256, 0, st>>>(part, (int)S, nc, T, jb, transpose,
+                                                                W2);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
 }
 
 // cluster size for the panel factorisation of rows [j0, d)
@@ -709,12 +736,9 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
     const int64_t nc = (n + 1) - c0;  // trailing columns incl. Sb
     if (nc <= 0) continue;
     const int64_t rows = d - j0;
-    int rc = qr_vtc(V + j0 * ldm + j0, ldm, M + c0 * ldm + j0, ldm, jb, rows, nc, W, part,
-                    part_cap, st);
+    int rc = qr_wt(V + j0 * ldm + j0, ldm, M + c0 * ldm + j0, ldm, jb, rows, nc,
+                   Tall + (j0 / QB_NB) * 32 * 32, 1, W2, part, part_cap, st);
     if (rc) return rc;
-    const int64_t tot = (int64_t)jb * nc;
-    qr_apply_tt_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(
-        Tall + (j0 / QB_NB) * 32 * 32, W, W2, jb, nc, 1);
     SKL_CUDA_LAUNCH();
     dim3 g((unsigned)((rows + 63) / 64), (unsigned)((nc + 63) / 64));
     qr_update_kernel<<<g, 256, 0, st>>>(M + c0 * ldm + j0, ldm, V + j0 * ldm + j0, ldm, W2, jb,
@@ -743,12 +767,9 @@ int qr_blocked_form_q(double* Q, int64_t ldq, int64_t d, int64_t n, const double
   for (int64_t j0 = ((n - 1) / QB_NB) * QB_NB; j0 >= 0; j0 -= QB_NB) {
     const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
     const int64_t rows = d - j0, nc = n - j0;
-    int rc = qr_vtc(V + j0 * ldv + j0, ldv, Q + j0 * ldq + j0, ldq, jb, rows, nc, W, part,
-                    part_cap, st);
+    int rc = qr_wt(V + j0 * ldv + j0, ldv, Q + j0 * ldq + j0, ldq, jb, rows, nc,
+                   Tall + (j0 / QB_NB) * 32 * 32, 0, W2, part, part_cap, st);
     if (rc) return rc;
-    const int64_t tot = (int64_t)jb * nc;
-    qr_apply_tt_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256, 0, st>>>(
-        Tall + (j0 / QB_NB) * 32 * 32, W, W2, jb, nc, 0);
     SKL_CUDA_LAUNCH();
     dim3 g((unsigned)((rows + 63) / 64), (unsigned)((nc + 63) / 64));
     qr_update_kernel<<<g, 256, 0, st>>>(Q + j0 * ldq + j0, ldq, V + j0 * ldv + j0, ldv, W2, jb,
