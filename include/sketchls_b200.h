@@ -173,7 +173,8 @@ int skl_countsketch_buckets(const int32_t* rows, int64_t m, int64_t d, int32_t* 
 
 /* S*A for CSR A (device pointers; int64 indptr/indices as SparseMatrix
  * holds them, linalg.py:66-68).  bucket_rows/bucket_ptr from
- * skl_countsketch_buckets and the int8 signs, all on the device.  SA is
+ * skl_countsketch_buckets and the int8 signs in BUCKET order
+ * (bucket_signs[k] = signs[bucket_rows[k]]), all on the device.  SA is
  * d x n column-major, fully overwritten (bitwise-equal to scipy's
  * csr_matmat fold).  Replaces sketch.py:210-211. */
 int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices, const double* values,

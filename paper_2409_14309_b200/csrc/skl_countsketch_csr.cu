@@ -29,7 +29,7 @@ constexpr int CSR_B = 8;   // buckets (warps) per CTA
 __global__ void __launch_bounds__(CSR_B * 32)
     countsketch_csr_kernel(const int64_t* __restrict__ indptr, const int64_t* __restrict__ indices,
                            const double* __restrict__ values, const int32_t* __restrict__ brow,
-                           const int64_t* __restrict__ bptr, const int8_t* __restrict__ signs,
+                           const int64_t* __restrict__ bptr, const int8_t* __restrict__ bsign,
                            int64_t d, int64_t n, int64_t Cw, double* __restrict__ SA,
                            int64_t ldsa) {
   extern __shared__ double tile[];  // [CSR_B][cw + 1] (bucket-major, odd stride)
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(CSR_B * 32)
     const int64_t r_beg = bptr[i], r_end = bptr[i + 1];
     double* my = tile + warp * ldt;  // column c at my[c - c0]
     // Row metadata of round r+1 is fetched while round r is committed
-    // (two dependent loads: bucket row -> its CSR extent).
+    // (two dependent loads: bucket row -> its CSR extent; the signs come
+// pre-gathered in bucket order, so they stream).
     int64_t np0 = 0, ncnt = 0;
     double ns = 0.0;
     {
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
         const int32_t j = brow[r];
         np0 = indptr[j];
         ncnt = indptr[j + 1] - np0;
-        ns = (double)signs[j];
+        ns = (double)bsign[r];
       }
     }
     for (int64_t base = r_beg; base < r_end; base += 32) {
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
           const int32_t j = brow[r];
           np0 = indptr[j];
           ncnt = indptr[j + 1] - np0;
-          ns = (double)signs[j];
+          ns = (double)bsign[r];
         }
       }
       // exclusive scan of counts over the warp (lane order == ascending j)

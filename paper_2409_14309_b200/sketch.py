@@ -189,13 +189,14 @@ class SketchOperator:
         return c["plan"]
 
     def device_buckets(self):
-        """(bucket_rows int32, bucket_ptr int64, signs int8) on the current
-        device: the CSR of S consumed by the CSR-operand kernel."""
+        """(bucket_rows int32, bucket_ptr int64, bucket-ordered signs int8) on
+        the current device: the CSR of S consumed by the CSR-operand kernel."""
         require_cuda()
         c = self._cache()
         if "buckets" not in c:
             brow, bptr = _native.countsketch_buckets(self.rows, self.target_dim)
-            c["buckets"] = (to_device(brow), to_device(bptr), to_device(self.signs))
+            bsign = np.ascontiguousarray(self.signs[brow])
+            c["buckets"] = (to_device(brow), to_device(bptr), to_device(bsign))
         return c["buckets"]
 
     def device_srht(self):

@@ -407,3 +407,25 @@ def test_qr_solve_matches_lapack(d, n):
     assert rel_fro(Q @ R, M) <= 1e-13
     x_ref = np.linalg.lstsq(M, y, rcond=None)[0]
     assert rel_fro(x, x_ref) <= 1e-8
+
+
+@pytest.mark.parametrize("m,n,d,density,dense_rows", [
+    (1, 1, 1, 1.0, 0), (50, 7, 3, 0.5, 0), (5000, 40, 64, 0.02, 3), (20_000, 1024, 256, 1e-3, 0),
+    (30_000, 3000, 8, 2e-3, 1), (100_000, 64, 2048, 0.0, 0), (70_000, 300, 1024, 0.01, 2)])
+def test_countsketch_csr_kernel_bitwise(m, n, d, density, dense_rows):
+    """CSR operand: bitwise-equal to scipy's (S @ A).toarray() (csr_matmat
+    order) -- empty matrix/rows, fully dense rows (more nonzeros than one
+    staging pass), buckets with many rows, several column tiles."""
+    rng = np.random.default_rng(m + n + d)
+    A = scipy.sparse.random(m, n, density=density, format="csr", random_state=rng,
+                            data_rvs=rng.standard_normal)
+    if dense_rows:
+        A = A.tolil()
+        for r in rng.choice(m, size=dense_rows, replace=False):
+            A[r, :] = rng.standard_normal(n)
+        A = A.tocsr()
+    A.sort_indices()
+    op = E.build_sketch(E.SketchSpec("countsketch", d, seed=m ^ n), m)
+    got = E.apply_to_matrix(op, E.SparseMatrix.from_scipy(A)).data
+    want = O.countsketch_apply(op.rows.astype(np.int64), op.signs.astype(np.float64), d, A)
+    assert np.array_equal(np.asarray(got), want)
