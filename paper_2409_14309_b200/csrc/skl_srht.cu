@@ -239,6 +239,166 @@ __global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParam
   }
 }
 
+// Register-resident SRHT for full 4096-row blocks (m_pad >= 4096).
+//
+// A group of 64 threads transforms one 4096-row block of a column; a CTA
+// holds SR2_G groups (blocks q, q+1, ...).  Element e of a block (12 bits):
+// thread t of the group loads e = t + 64 i, i = 0..63, straight from global
+// memory (each warp load is one coalesced 256-byte segment), flips signs
+// from its own 64-bit word, and runs the 12 butterfly stages as
+//   bits 6..11 : in registers (over i),
+//   one shared-memory transpose (XOR-swizzled, conflict-free both ways):
+//                thread t then holds e = 64 t + i,
+//   bits 0..5  : in registers.
+// Each thread writes back only elements some output row samples, and the
+// output rows (KPT per thread) gather with the (-1)^popc(p_hi & j_hi) sign.
+// The next blocks' loads are issued before the gather, so HBM streams under
+// the sampling.  Shared-memory traffic: one transpose plus the sampled
+// values, ~0.24 wavefronts per element (a three-pass smem FWHT needs ~0.53).
+constexpr int SR2_G = 2;              // blocks (64-thread groups) per CTA
+constexpr int SR2_NT = 64 * SR2_G;
+
+__device__ __forceinline__ int sr2_swz(int e) { return e ^ ((e >> 6) & 31); }
+
+template <int KPT>
+__global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
+  extern __shared__ __align__(16) double work2[];  // [SR2_G][4096], then sps[KPT * SR2_NT]
+  __shared__ uint32_t sbm[SR_BMAX / 32];
+  uint32_t* sps = reinterpret_cast<uint32_t*>(work2 + SR2_G * SR_BMAX);  // sample positions
+  const int tid = threadIdx.x, g = tid >> 6, t = tid & 63;
+  double* wk = work2 + g * SR_BMAX;
+  const int64_t col = blockIdx.x;
+  const int64_t nblk = (p.m + SR_BMAX - 1) / SR_BMAX;
+  const int64_t q0 = nblk * blockIdx.y / p.P, q1 = nblk * (blockIdx.y + 1) / p.P;
+
+  // Output rows are processed in order of their in-block position p_lo
+  // (counting sort in shared memory), so a warp's 32 gathers fall in a few
+  // 128-byte rows instead of 32 random ones.  skk[] keeps the output index.
+  uint32_t* skk = sps + KPT * SR2_NT;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(work2);  // scratch before first use
+  for (int i = tid; i < SR_BMAX / 32; i += SR2_NT) sbm[i] = 0u;
+  for (int i = tid; i < SR_BMAX; i += SR2_NT) cnt[i] = 0u;
+  __syncthreads();
+  for (int64_t i = tid; i < p.d; i += SR2_NT) {
+    const uint32_t pl = (uint32_t)p.sample[i] & (SR_BMAX - 1);
+    atomicAdd(&cnt[pl], 1u);
+    atomicOr(&sbm[pl >> 5], 1u << (pl & 31));
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the 4096 counts by one warp
+    uint32_t run = 0;
+    for (int c = 0; c < SR_BMAX / 32; ++c) {
+      const uint32_t x = cnt[c * 32 + tid];
+      uint32_t y = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (tid >= o) y += z;
+      }
+      cnt[c * 32 + tid] = run + y - x;
+      run += __shfl_sync(0xffffffffu, y, 31);
+    }
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < p.d; i += SR2_NT) {
+    const uint32_t ps = (uint32_t)p.sample[i];
+    const uint32_t slot = atomicAdd(&cnt[ps & (SR_BMAX - 1)], 1u);
+    sps[slot] = ps;
+    skk[slot] = (uint32_t)i;
+  }
+  for (int64_t i = p.d + tid; i < (int64_t)KPT * SR2_NT; i += SR2_NT) {
+    sps[i] = 0u;
+    skk[i] = 0xffffffffu;
+  }
+  double acc[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) acc[k] = 0.0;
+  __syncthreads();
+  // after the transpose thread t holds e = 64 t + i: sampled bits i
+  const uint64_t smask = ((uint64_t)sbm[2 * t + 1] << 32) | sbm[2 * t];
+  const double* colp = p.A + col * p.lda;
+  const uint64_t* sw64 = reinterpret_cast<const uint64_t*>(p.sbits);
+
+  double v[64];
+  auto load = [&](int64_t q) {
+    const int64_t r0 = q * SR_BMAX;
+    const int64_t len = q < q1 ? min((int64_t)SR_BMAX, p.m - r0) : 0;
+    const double* src = colp + r0 + t;
+    if (len == SR_BMAX) {  // full block: unpredicated, immediate offsets
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = __ldcs(src + 64 * i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = t + 64 * i < len ? __ldcs(src + 64 * i) : 0.0;
+    }
+  };
+  load(q0 + g);
+  for (int64_t qb = q0; qb < q1; qb += SR2_G) {
+    const int64_t q = qb + g;  // my block (may be past q1: all zeros)
+    const uint64_t sw = q < q1 ? sw64[q * 64 + t] : 0ull;
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      v[i] = __hiloint2double(__double2hiint(v[i]) ^ (int)(((sw >> i) & 1ull) << 31),
+                              __double2loint(v[i]));
+    // bits 6..11
+#pragma unroll
+    for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (!(i & h)) {
+          const double a = v[i], c = v[i + h];
+          v[i] = a + c;
+          v[i + h] = a - c;
+        }
+    __syncthreads();  // the previous iteration's gathers are done with wk
+#pragma unroll
+    for (int i = 0; i < 64; ++i) wk[sr2_swz(t + 64 * i)] = v[i];
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");  // group barrier
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = wk[sr2_swz(64 * t + i)];
+    // bits 0..5
+#pragma unroll
+    for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (!(i & h)) {
+          const double a = v[i], c = v[i + h];
+          v[i] = a + c;
+          v[i + h] = a - c;
+        }
+    // owner-only rewrite of the sampled elements (no barrier needed)
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if ((smask >> i) & 1ull) wk[sr2_swz(64 * t + i)] = v[i];
+    load(qb + SR2_G + g);  // next blocks stream in under the gather
+    __syncthreads();
+#pragma unroll
+    for (int gg = 0; gg < SR2_G; ++gg) {
+      const int64_t qq = qb + gg;
+      if (qq >= q1) break;
+      const uint32_t jhi = (uint32_t)(p.jhi0 + qq);
+      const double* w = work2 + gg * SR_BMAX;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const uint32_t ps = sps[k * SR2_NT + tid];
+        const double y = w[sr2_swz((int)(ps & (SR_BMAX - 1)))];
+        const uint32_t flip = (uint32_t)(__popc((ps >> 12) & jhi) & 1) << 31;
+        acc[k] += __hiloint2double(__double2hiint(y) ^ (int)flip, __double2loint(y));
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const uint32_t kk = skk[k * SR2_NT + tid];
+    if (kk == 0xffffffffu) continue;
+    const int64_t i = kk;
+    if (p.P == 1)
+      p.out[col * p.ldo + i] = acc[k] / p.inv_scale_div;
+    else
+      p.part[((int64_t)blockIdx.y * p.n + col) * p.d + i] = acc[k];
+  }
+}
+
 __global__ void srht_reduce_kernel(const double* part, int P, int64_t n, int64_t d, double* out,
                                    int64_t ldo, double div) {
   const int64_t total = n * d;
@@ -273,7 +433,16 @@ static int block_log2(int64_t m_pad) {
 
 template <int KPT>
 static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kern = p.b == 12 ? srht_dense_kernel<KPT, true> : srht_dense_kernel<KPT, false>;
+  if (p.b == 12) {  // full blocks: register-resident kernel, KPT = d / 128 per thread
+    constexpr int K2 = KPT * SR_NT / SR2_NT;
+    auto kern = srht_reg_kernel<K2>;
+    const int sm2 = SR2_G * SR_BMAX * 8 + 2 * K2 * SR2_NT * 4;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, SR2_NT, sm2, st>>>(p);
+    return cudaGetLastError();
+  }
+  auto kern = srht_dense_kernel<KPT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SR_NT + 32, smem, st>>>(p);
@@ -419,9 +588,11 @@ extern "C" int skl_fwht_device(double* X, int64_t m_pad, int64_t n, int64_t lda,
   return SKL_OK;
 }
 
-// Packed signs for the SRHT kernel (host): per block of B = min(m_pad, 4096)
-// rows, one 16-bit word per first-pass task whose bit i is the sign of that
-// task's element i (1 = negative), padded to a multiple of 8 words.
+// Packed signs for the SRHT kernels (host): per block of B = min(m_pad, 4096)
+// rows, 16-bit words (1 = negative).  Full 4096-row blocks use the register
+// kernel's layout (64-bit word t, bit i = element t + 64 i, stored as four
+// u16); smaller blocks one word per first-pass task, bit i = that task's
+// element i.  Padded to a multiple of 8 words.
 extern "C" int64_t skl_srht_sign_words(int64_t B) {
   int b = 0;
   while ((1LL << (b + 1)) <= B) ++b;
@@ -440,6 +611,20 @@ extern "C" int skl_srht_pack_signs(const int8_t* signs, int64_t m_pad, uint16_t*
   int lo, nb;
   first_pass(b, &lo, &nb);
   const int64_t tasks = B >> nb, words = skl_srht_sign_words(B);
+  if (b == 12) {
+    // register kernel layout: per block 64 little-endian 64-bit words, word
+    // t bit i = element t + 64 i of the block (as 256 u16 words)
+    for (int64_t blk = 0; blk < m_pad / B; ++blk) {
+      uint16_t* w = packed + blk * words;
+      for (int64_t t = 0; t < 64; ++t) {
+        uint64_t mask = 0;
+        for (int i = 0; i < 64; ++i)
+          if (signs[blk * B + t + 64 * i] < 0) mask |= 1ull << i;
+        for (int h = 0; h < 4; ++h) w[t * 4 + h] = (uint16_t)(mask >> (16 * h));
+      }
+    }
+    return SKL_OK;
+  }
   for (int64_t blk = 0; blk < m_pad / B; ++blk) {
     uint16_t* w = packed + blk * words;
     for (int64_t t = 0; t < words; ++t) {
