@@ -18,7 +18,7 @@ from paper_2409_14309_b200.sketch import (  # noqa: E402
 which = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 if which == "srht":
-    m, n, d = 1 << 22, 256, 2048
+    m, n, d = 1 << 23, 256, 2048  # config 5
     A = torch.randn((n, m), dtype=torch.float64, device="cuda").t()
     op = E.build_sketch(E.SketchSpec("srht", d, seed=1), m)
     for _ in range(reps):
