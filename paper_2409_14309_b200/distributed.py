@@ -1,9 +1,10 @@
 """Row-sharded sketch-and-apply across GPUs.
 
 Row block k of A (and b) lives on rank k.  Every rank sketches its block
-with the hashes of its *global* row indices -- the operator is realised
-once for the global m, exactly as the reference would build it
-(sketch.py:93-103) -- producing a partial d x (n+1) [SA | Sb].  One
+with the operator realised once for the GLOBAL m, exactly as the reference
+would build it (sketch.py:84-127) -- CountSketch hashes of global rows,
+SRHT sign/sample with the shard's block offset, the Gaussian column block --
+producing a partial d x (n+1) [SA | Sb].  One
 NCCL reduce (sum, fp64) to rank 0 completes S[A | b]; rank 0 solves the
 reduced problem, broadcasts x, and the residual norm is an all-reduce of
 the per-block squared residuals.
@@ -40,22 +41,44 @@ def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class ShardPlan:
-    """The part of a global CountSketch operator that rank ``rank`` needs:
-    hashes of global rows [r0, r1) and their device plan."""
+    """The part of a global operator that the rank owning rows [r0, r1) needs.
+
+    * countsketch: the hashes/signs of the global rows [r0, r1) and their
+      device plan (the hash of row j is the reference's draw for GLOBAL j);
+    * srht: the packed sign words of the shard's 4096-row blocks (a slice of
+      the global packing, shards are block aligned) plus the global sample;
+      the kernel adds the (-1)^popc(p_hi & j_hi) factor for the shard's
+      block offset, i.e. H_m = H_G (x) H_{m/G} over (shard, local) bits;
+    * gaussian: the column block S[:, r0:r1] of the row-major d x m matrix
+      (the full G is generated on each rank -- the ziggurat stream is
+      sequential -- and the GEMM reads only the block)."""
 
     def __init__(self, op: SketchOperator, r0: int, r1: int):
-        if op.kind != "countsketch":
-            raise ValueError("row sharding is implemented for CountSketch operators")
+        if op.kind not in ("countsketch", "srht", "gaussian"):
+            raise ValueError(f"row sharding is not implemented for {op.kind!r} operators")
+        if op.kind == "srht":
+            B = min(op.padded_dim, 4096)
+            if r0 % B:
+                raise ValueError(f"SRHT shard start {r0} is not a multiple of the block {B}")
         self.op, self.r0, self.r1 = op, r0, r1
+        self.kind = op.kind
         self.d = op.target_dim
-        self.rows = np.ascontiguousarray(op.rows[r0:r1])
-        self.signs = np.ascontiguousarray(op.signs[r0:r1])
+        if op.kind == "countsketch":
+            self.rows = np.ascontiguousarray(op.rows[r0:r1])
+            self.signs = np.ascontiguousarray(op.signs[r0:r1])
         self._plan = None
 
     def device_plan(self) -> CountSketchPlan:
         if self._plan is None:
             self._plan = CountSketchPlan(self.rows, self.signs, self.d)
         return self._plan
+
+    def device_srht_words(self):
+        """Packed sign words of this shard's blocks (device view)."""
+        signs, _ = self.op.device_srht()
+        B = min(self.op.padded_dim, 4096)
+        per_block = int(_native.lib().skl_srht_sign_words(B))
+        return signs[(self.r0 // B) * per_block:]
 
 
 def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
@@ -67,7 +90,23 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
     d = plan.d
     ld = (d + 1) // 2 * 2  # keeps the Sb column 16-byte aligned
     out = device_f64((d, n + 1), fortran=True, ld=ld)
-    plan.device_plan().apply(A_local, m_loc, n, lda, b_local, out, ld, out[:, n], partitions=1)
+    st = current_stream()
+    if plan.kind == "countsketch":
+        plan.device_plan().apply(A_local, m_loc, n, lda, b_local, out, ld, out[:, n],
+                                 partitions=1)
+    elif plan.kind == "srht":
+        words = plan.device_srht_words()
+        _, sample = plan.op.device_srht()
+        for src, ncol, ldsrc, dst in ((A_local, n, lda, out), (b_local, 1, m_loc, out[:, n])):
+            _native.call("skl_srht_dense_shard", _native.ptr(src), m_loc, ncol, ldsrc,
+                         _native.ptr(words), _native.ptr(sample), plan.op.padded_dim, d, plan.r0,
+                         _native.ptr(dst), ld, st)
+    else:
+        G, ldg = plan.op.device_gaussian()
+        Gs = G[:, plan.r0:]
+        for src, ncol, ldsrc, dst in ((A_local, n, lda, out), (b_local, 1, m_loc, out[:, n])):
+            _native.call("skl_gemm_f64", _native.ptr(Gs), ldg, _native.ptr(src), ldsrc,
+                         _native.ptr(dst), ld, d, ncol, m_loc, 0, st)
     return out
 
 

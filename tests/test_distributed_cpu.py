@@ -43,6 +43,19 @@ def _oracle_partial(plan, A_local, b_local):
     return torch.from_numpy(np.asfortranarray(np.column_stack([SA, Sb])))
 
 
+def _oracle_partial_any(plan, A_local, b_local):
+    """S[:, r0:r1] [A_local | b_local] for any kind: the global operator
+    applied to the full-height matrix that is zero outside the shard."""
+    m = plan.op.source_dim
+    key = O.derive_seed(plan.op_seed, plan.kind, m)
+    a = np.zeros((m, A_local.shape[1]))
+    a[plan.r0:plan.r1] = A_local.numpy()
+    bb = np.zeros(m)
+    bb[plan.r0:plan.r1] = b_local.numpy()
+    SA, Sb = O.sketch_apply(plan.kind, key, plan.d, a, bb)
+    return torch.from_numpy(np.asfortranarray(np.column_stack([SA, Sb])))
+
+
 def _oracle_solve(partial):
     p = partial.numpy()
     q, r = O.economy_qr(p[:, :-1])
@@ -57,16 +70,23 @@ def _oracle_r2(A_local, b_local, x):
     return torch.tensor([float(r @ r)], dtype=torch.float64)
 
 
-def _worker(rank, world, port, m, n, d, seed, out):
+def _worker(rank, world, port, m, n, d, seed, out, kind="countsketch"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         A, b = _problem(m, n)
         r0, r1 = shard_rows(m, world, rank)
-        spec = SketchSpec("countsketch", d, seed=seed)
+        spec = SketchSpec(kind, d, seed=seed)
+
+        def local(plan, A_local, b_local):
+            if kind == "countsketch":
+                return _oracle_partial(plan, A_local, b_local)
+            plan.op_seed = seed
+            return _oracle_partial_any(plan, A_local, b_local)
+
         x, rnorm, dd = sharded_sketch_and_apply(
             torch.from_numpy(np.asfortranarray(A[r0:r1])), torch.from_numpy(b[r0:r1].copy()), m,
-            spec, dist, local_apply=_oracle_partial, solve_reduced=_oracle_solve,
+            spec, dist, local_apply=local, solve_reduced=_oracle_solve,
             residual_local=_oracle_r2)
         out[rank] = (x.numpy().copy(), rnorm, dd)
     finally:
@@ -125,3 +145,32 @@ def test_gloo_world2_matches_single_process():
         assert dd == d
         assert np.linalg.norm(x - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
         assert abs(rnorm - r_ref) <= 1e-12 * r_ref
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("kind", ["srht", "gaussian"])
+def test_gloo_world2_other_kinds(kind):
+    """SRHT (block-offset sign) and Gaussian (column block) shard plans over
+    gloo: the reduced partials solve to the single-process SAA answer."""
+    m, n, d, seed = 20_000, 5, 64, 8
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(2, port, m, n, d, seed, out, kind), nprocs=2, join=True)
+    A, b = _problem(m, n)
+    SA, Sb = O.sketch_apply(kind, O.derive_seed(seed, kind, m), d, A, b)
+    q, r = O.economy_qr(SA)
+    import scipy.linalg
+
+    want = scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False)
+    for rank in range(2):
+        x, rnorm, dd = out[rank]
+        assert dd == d
+        assert np.linalg.norm(x - want) <= 1e-10 * np.linalg.norm(want)
+        assert abs(rnorm - np.linalg.norm(A @ want - b)) <= 1e-10 * rnorm
+
+
+def test_srht_shard_must_be_block_aligned():
+    op = build_sketch(SketchSpec("srht", 64, seed=1), 20_000)
+    with pytest.raises(ValueError):
+        ShardPlan(op, 100, 20_000)

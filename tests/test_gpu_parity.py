@@ -429,3 +429,31 @@ def test_countsketch_csr_kernel_bitwise(m, n, d, density, dense_rows):
     got = E.apply_to_matrix(op, E.SparseMatrix.from_scipy(A)).data
     want = O.countsketch_apply(op.rows.astype(np.int64), op.signs.astype(np.float64), d, A)
     assert np.array_equal(np.asarray(got), want)
+
+
+@pytest.mark.parametrize("kind,m,n,d,world", [
+    ("countsketch", 50_000, 7, 512, 3), ("srht", 40_000, 5, 256, 2), ("srht", 1 << 16, 3, 512, 4),
+    ("gaussian", 30_000, 6, 128, 3)])
+def test_row_shards_sum_to_full_apply(kind, m, n, d, world):
+    """Multi-GPU partials computed one shard at a time on one GPU (no
+    collectives): the sum over shards equals the single-device S[A|b]
+    (CountSketch/SRHT/Gaussian shard plans: global hashes, SRHT block offsets,
+    Gaussian column blocks)."""
+    from paper_2409_14309_b200.distributed import ShardPlan, local_partial_device, shard_rows
+
+    rng = np.random.default_rng(m + d)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec(kind, d, seed=11), m)
+    total = None
+    for r in range(world):
+        r0, r1 = shard_rows(m, world, r)
+        if r1 <= r0:
+            continue
+        Ad = torch.from_numpy(np.asfortranarray(A[r0:r1])).cuda()
+        bd = torch.from_numpy(b[r0:r1].copy()).cuda()
+        part = local_partial_device(ShardPlan(op, r0, r1), Ad, r1 - r0, bd).cpu().numpy()
+        total = part if total is None else total + part
+    full = np.column_stack([E.apply_to_matrix(op, E.DenseMatrix(A)).data,
+                            E.apply_to_vector(op, E.Vector(b)).data])
+    assert rel_fro(total, full) <= 1e-13
