@@ -224,3 +224,126 @@ def saa_solve(A, b: np.ndarray, kind: str, seed: int, d_factor: float):
     q, r = economy_qr(SA)
     x = scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False, check_finite=False)
     return {"x": x, "residual": residual_norm(A, b, x), "SA": SA, "Sb": Sb, "d": d, "R": r}
+
+
+# ------------------------------------------------------------------ SAP / LSQR
+_EPS = float(np.finfo(np.float64).eps)  # solvers.py:37
+
+
+def sym_ortho(a: float, b: float):
+    """solvers.py:258-270: stable Givens rotation (c, s, r)."""
+    if b == 0.0:
+        return math.copysign(1.0, a) if a != 0 else 1.0, 0.0, abs(a)
+    if a == 0.0:
+        return 0.0, math.copysign(1.0, b), abs(b)
+    if abs(b) > abs(a):
+        tau = a / b
+        s = math.copysign(1.0, b) / math.sqrt(1.0 + tau * tau)
+        return s * tau, s, b / s
+    tau = b / a
+    c = math.copysign(1.0, a) / math.sqrt(1.0 + tau * tau)
+    return c, c * tau, a / c
+
+
+def lsqr(A, b: np.ndarray, atol: float = 1e-10, btol: float = 1e-10, max_iter=None,
+         precond_R=None):
+    """solvers.py:110-255 (Paige & Saunders LSQR, optionally right-
+    preconditioned by R: operator y -> A R^-1 y, returns x = R^-1 y).
+    Returns dict(x, iterations, termination, residual)."""
+    n = A.shape[1]
+    max_iter = 4 * n if max_iter is None else max_iter
+    r = precond_R
+
+    def inv_r(v, transposed=False):
+        return scipy.linalg.solve_triangular(r, v, lower=False, trans="T" if transposed else "N",
+                                             check_finite=False)
+
+    if r is None:
+        mv = lambda v: A @ v  # noqa: E731
+        rmv = lambda u: A.T @ u  # noqa: E731
+    else:
+        mv = lambda v: A @ inv_r(v)  # noqa: E731
+        rmv = lambda u: inv_r(A.T @ u, transposed=True)  # noqa: E731
+    x = np.zeros(n)
+    u = np.array(b, dtype=np.float64, copy=True)
+    beta = float(np.linalg.norm(u))
+    alfa = 0.0
+    v = np.zeros(n)
+    if beta > 0:
+        u /= beta
+        v = rmv(u)
+        alfa = float(np.linalg.norm(v))
+    if alfa > 0:
+        v /= alfa
+    w = v.copy()
+    itn = istop = 0
+    anorm = 0.0
+    rhobar, phibar, bnorm = alfa, beta, beta
+    if alfa * beta == 0.0:
+        xf = x if r is None else inv_r(x)
+        return {"x": xf, "iterations": 0, "termination": "atol_btol",
+                "residual": residual_norm(A, b, xf)}
+    while itn < max_iter:
+        itn += 1
+        u = mv(v) - alfa * u
+        beta = float(np.linalg.norm(u))
+        if beta > 0:
+            u /= beta
+            anorm = math.sqrt(anorm**2 + alfa**2 + beta**2)
+            v = rmv(u) - beta * v
+            alfa = float(np.linalg.norm(v))
+            if alfa > 0:
+                v /= alfa
+        cs, sn, rho = sym_ortho(rhobar, beta)
+        theta = sn * alfa
+        rhobar = -cs * alfa
+        phi = cs * phibar
+        phibar = sn * phibar
+        x += (phi / rho) * w
+        w = v + (-theta / rho) * w
+        rnorm = phibar
+        arnorm = alfa * abs(sn * phi)
+        xnorm = float(np.linalg.norm(x))
+        test1 = rnorm / bnorm
+        test2 = arnorm / (anorm * rnorm + _EPS)
+        t1 = test1 / (1.0 + anorm * xnorm / bnorm)
+        rtol = btol + atol * anorm * xnorm / bnorm
+        if itn >= max_iter:
+            istop = 7
+        if 1.0 + test2 <= 1.0:
+            istop = 5
+        if 1.0 + t1 <= 1.0:
+            istop = 4
+        if test2 <= atol:
+            istop = 2
+        if test1 <= rtol:
+            istop = 1
+        if istop != 0:
+            break
+    xf = x if r is None else inv_r(x)
+    return {"x": xf, "iterations": itn, "termination": "max_iter" if istop == 7 else "atol_btol",
+            "residual": residual_norm(A, b, xf)}
+
+
+def sap_solve(A, b: np.ndarray, kind: str, seed: int, d_factor: float, warm_start: bool = True,
+              atol: float = 1e-10, btol: float = 1e-10, max_iter=None):
+    """solvers.py:323-361 via solve(problem, "sap", SketchSpec(kind, 1, seed),
+    SolverOptions(...)): LSQR right-preconditioned by R of QR(S A), warm
+    started from the sketched solution."""
+    m, n = A.shape
+    if not scipy.sparse.issparse(A):
+        A = np.asfortranarray(A, dtype=np.float64)
+    d = default_embed_dim(m, n, d_factor)
+    key = operator_key(seed, kind, m, method="sap")
+    SA, Sb = sketch_apply(kind, key, d, A, b)
+    q, r = economy_qr(SA)
+    if warm_start:
+        x0 = scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False, check_finite=False)
+        r0 = b - A @ x0
+        inner = lsqr(A, r0, atol, btol, max_iter, precond_R=r)
+        x = x0 + inner["x"]
+    else:
+        inner = lsqr(A, b, atol, btol, max_iter, precond_R=r)
+        x = inner["x"]
+    return {"x": x, "iterations": inner["iterations"], "termination": inner["termination"],
+            "residual": residual_norm(A, b, x), "d": d, "R": r}

@@ -616,33 +616,48 @@ __global__ void __launch_bounds__(256) qr_reduce_tt_kernel(const double* __restr
                                                            int64_t nc, const double* __restrict__ T,
                                                            int jb, int transpose,
                                                            double* __restrict__ W2) {
+  // 2 columns per CTA; 4 groups of 32 threads split each column's S partials
   __shared__ double Tsm[32][33];
-  __shared__ double Wsm[8][33];
-  const int tid = threadIdx.x, k = tid & 31, cl = tid >> 5;
-  const int64_t c = (int64_t)blockIdx.x * 8 + cl;
-  #pragma unroll
+  __shared__ double Wg[2][4][32];
+  __shared__ double Wsm[2][33];
+  const int tid = threadIdx.x, k = tid & 31, g = (tid >> 5) & 3, cl = tid >> 7;
+  const int64_t c = (int64_t)blockIdx.x * 2 + cl;
+#pragma unroll
   for (int e = tid; e < 1024; e += 256) Tsm[e & 31][e >> 5] = T[e];  // Tsm[row][col]
   double w0 = 0.0, w1 = 0.0;
   if (c < nc) {
-    int q = 0;
-#pragma unroll 8
-    for (; q + 1 < S; q += 2) {
+    int q = g;
+#pragma unroll 4
+    for (; q + 4 < S; q += 8) {
       w0 += part[((int64_t)q * nc + c) * 32 + k];
-      w1 += part[((int64_t)(q + 1) * nc + c) * 32 + k];
+      w1 += part[((int64_t)(q + 4) * nc + c) * 32 + k];
     }
     if (q < S) w0 += part[((int64_t)q * nc + c) * 32 + k];
   }
-  Wsm[cl][k] = w0 + w1;
+  Wg[cl][g][k] = w0 + w1;
   __syncthreads();
-  if (c >= nc) return;
-  double u = 0.0;
+  if (g == 0) Wsm[cl][k] = (Wg[cl][0][k] + Wg[cl][1][k]) + (Wg[cl][2][k] + Wg[cl][3][k]);
+  __syncthreads();
+  if (c >= nc || g != 0) return;
+  double u0 = 0.0, u1 = 0.0;
   if (k < jb) {
-    if (transpose)
-      for (int l = 0; l <= k; ++l) u = fma(Tsm[l][k], Wsm[cl][l], u);
-    else
-      for (int l = k; l < jb; ++l) u = fma(Tsm[k][l], Wsm[cl][l], u);
+    if (transpose) {
+      int l = 0;
+      for (; l + 1 <= k; l += 2) {
+        u0 = fma(Tsm[l][k], Wsm[cl][l], u0);
+        u1 = fma(Tsm[l + 1][k], Wsm[cl][l + 1], u1);
+      }
+      if (l <= k) u0 = fma(Tsm[l][k], Wsm[cl][l], u0);
+    } else {
+      int l = k;
+      for (; l + 1 < jb; l += 2) {
+        u0 = fma(Tsm[k][l], Wsm[cl][l], u0);
+        u1 = fma(Tsm[k][l + 1], Wsm[cl][l + 1], u1);
+      }
+      if (l < jb) u0 = fma(Tsm[k][l], Wsm[cl][l], u0);
+    }
   }
-  W2[c * 32 + k] = u;
+  W2[c * 32 + k] = u0 + u1;
 }
 
 // W2 = T' V^T C for the block reflector (rows x jb, rows x nc)
@@ -654,7 +669,7 @@ static int qr_wt(const double* V, int64_t ldv, const double* C, int64_t ldc, int
   qr_vtc64_kernel<<<dim3((unsigned)((nc + 31) / 32), (unsigned)S), 256, 0, st>>>(V, ldv, C, ldc,
                                                                               jb, rows, nc, part);
   SKL_CUDA_LAUNCH();
-  qr_reduce_tt_kernel<<<(unsigned)((nc + 7) / 8), 256, 0, st>>>(part, (int)S, nc, T, jb, transpose,
+  qr_reduce_tt_kernel<<<(unsigned)((nc + 1) / 2), 256, 0, st>>>(part, (int)S, nc, T, jb, transpose,
                                                                 W2);
   SKL_CUDA_LAUNCH();
   return SKL_OK;

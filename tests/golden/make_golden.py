@@ -145,6 +145,36 @@ def main() -> None:
             g[f"{name}_SA_cols"] = SA[:, :4].copy()
         meta[f"{name}_shape"] = [c.m, c.n, c.d]
 
+    # --- SAP (sketch-and-precondition + LSQR, solvers.py:323-361, 110-255)
+    sap_cases = {
+        "sap_cfg1": (W.config(1), "countsketch", True),
+        "sap_cfg2r": (W.config(2, m=1 << 14), "countsketch", True),
+        "sap_cfg3r": (W.config(3, m=8192, n=64, d=256), "gaussian", True),
+        "sap_cfg4r": (W.config(4, m=1 << 16, n=256, d=2048), "countsketch", True),
+        "sap_cfg5r": (W.config(5, m=6000, n=32, d=256), "srht", False),
+    }
+    for name, (c, kind, warm) in sap_cases.items():
+        A, b, _ = W.make_problem(c)
+        Ac = ref.SparseMatrix.from_scipy(A) if scipy.sparse.issparse(A) else ref.DenseMatrix(A)
+        prob = ref.LeastSquaresProblem(A=Ac, b=ref.Vector(b))
+        spec = ref.SketchSpec(kind, 1, seed=W.SEED)
+        opts = ref.SolverOptions(d_factor=c.d / c.n, warm_start=warm)
+        res = ref.solve(prob, "sap", spec, opts)
+        assert res.d == c.d, (name, res.d, c.d)
+        g[f"{name}_x"] = res.x.data
+        meta[f"{name}_residual"] = res.residual_norm
+        meta[f"{name}_iterations"] = res.iterations
+        meta[f"{name}_termination"] = res.termination
+        meta[f"{name}_warm"] = warm
+    # plain LSQR (method "lsqr") on a small problem
+    c = W.config(1, m=3000, n=40)
+    A, b, _ = W.make_problem(c)
+    res = ref.solve(ref.LeastSquaresProblem(A=ref.DenseMatrix(A), b=ref.Vector(b)), "lsqr")
+    g["lsqr_small_x"] = res.x.data
+    meta["lsqr_small_residual"] = res.residual_norm
+    meta["lsqr_small_iterations"] = res.iterations
+    meta["lsqr_small_termination"] = res.termination
+
     # --- rank-deficient sketch message (test_solvers.py:121-127)
     rng = stream(15)
     a = rng.standard_normal((50, 4))

@@ -174,3 +174,35 @@ def test_csr_operand_matches_dense(golden):
     rows, signs = O.countsketch_draws(key, 64, 16)
     got = O.countsketch_apply(rows, signs, 16, scipy.sparse.csr_matrix(a))
     assert rel_fro(got, O.countsketch_apply(rows, signs, 16, a)) <= 1e-13
+
+
+SAP_CASES = {
+    "sap_cfg1": (W.config(1), "countsketch"),
+    "sap_cfg2r": (W.config(2, m=1 << 14), "countsketch"),
+    "sap_cfg3r": (W.config(3, m=8192, n=64, d=256), "gaussian"),
+    "sap_cfg4r": (W.config(4, m=1 << 16, n=256, d=2048), "countsketch"),
+    "sap_cfg5r": (W.config(5, m=6000, n=32, d=256), "srht"),
+}
+
+
+@pytest.mark.parametrize("name", list(SAP_CASES))
+def test_sap_oracle_matches_reference(golden, golden_meta, name):
+    """oracle.sap_solve (solvers.py:323-361 + lsqr :110-255) against the
+    reference's own solve(problem, "sap", ...) on the same inputs."""
+    c, kind = SAP_CASES[name]
+    A, b, _ = W.make_problem(c)
+    got = O.sap_solve(A, b, kind, W.SEED, c.d / c.n, warm_start=golden_meta[f"{name}_warm"])
+    assert got["d"] == c.d
+    assert got["iterations"] == golden_meta[f"{name}_iterations"]
+    assert got["termination"] == golden_meta[f"{name}_termination"]
+    assert rel_fro(got["x"], golden[f"{name}_x"]) <= 1e-12
+    assert abs(got["residual"] - golden_meta[f"{name}_residual"]) <= 1e-12 * got["residual"]
+
+
+def test_plain_lsqr_oracle_matches_reference(golden, golden_meta):
+    c = W.config(1, m=3000, n=40)
+    A, b, _ = W.make_problem(c)
+    got = O.lsqr(np.asfortranarray(A), b)
+    assert got["iterations"] == golden_meta["lsqr_small_iterations"]
+    assert got["termination"] == golden_meta["lsqr_small_termination"]
+    assert rel_fro(got["x"], golden["lsqr_small_x"]) <= 1e-12
