@@ -165,6 +165,34 @@ int skl_countsketch_dense_owned_host(const double* A_host, int64_t m, int64_t n,
                                      double* Sb_host, double* A_dev_keep, int64_t ld_keep,
                                      double* b_dev_keep, void* stream);
 
+/* ---- preconditioned LSQR (sketch-and-precondition, solvers.py:110-361) ----
+ * Device pieces of one LSQR iteration; the scalar recurrence stays on the
+ * host.  Column-major dense A (16-byte aligned, even lda); R is the explicit
+ * n x n upper factor of QR(S A) (column-major, ld ldr) or NULL (plain
+ * LSQR).  `work`/`counters` are scratch sized by skl_lsqr_work_size /
+ * skl_lsqr_counter_size (counters zero-initialised once).  Reductions are
+ * deterministic. */
+int64_t skl_lsqr_work_size(int64_t m, int64_t n);
+int64_t skl_lsqr_counter_size(int64_t n);
+/* u_out = s (A y) - alpha u_in  (u_in may be NULL; A NULL: no product),
+ * *norm2 = ||u_out||^2 (device scalar).  u_in and u_out must not alias. */
+int skl_lsqr_gemv_n(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                    double s, double alpha, const double* u_in, double* u_out, double* norm2,
+                    double* work, unsigned int* counters, void* stream);
+/* u_n = u_raw / beta (beta > 0), z = A^T u_n. */
+int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t lda, const double* u_raw,
+                    double beta, double* u_n, double* z, double* work, unsigned int* counters,
+                    void* stream);
+/* v_out = R^-T z - beta v_prev, *norm2 = ||v_out||^2 (R NULL: identity). */
+int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z, double beta,
+                    const double* v_prev, double* v_out, double* norm2, void* stream);
+/* v <- v / alfa (alfa > 0), y = R^-1 v (R NULL: y = v). */
+int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double alfa, double* v, double* y,
+                    void* stream);
+/* x += c1 w; w = v + c2 w; *norm2 = ||x||^2. */
+int skl_lsqr_xw(int64_t n, double c1, double c2, const double* v, double* w, double* x,
+                double* norm2, void* stream);
+
 /* Bucket-sorted source rows of a CountSketch (host): bucket_rows[bucket_ptr[i]
  * .. bucket_ptr[i+1]) are the rows j with rows[j] == i, ascending -- the CSR
  * of S (sketch.py:100-102) without its values.  bucket_ptr has d+1 entries. */

@@ -68,6 +68,22 @@ SIGNATURES: dict[str, tuple] = {
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     ),
+    "skl_lsqr_work_size": (c_i64, [c_i64, c_i64]),
+    "skl_lsqr_counter_size": (c_i64, [c_i64]),
+    "skl_lsqr_gemv_n": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, ctypes.c_double, ctypes.c_double, c_ptr, c_ptr, c_ptr,
+         c_ptr, c_ptr, c_ptr],
+    ),
+    "skl_lsqr_gemv_t": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    ),
+    "skl_lsqr_trsv_t": (
+        c_int, [c_ptr, c_i64, c_i64, c_ptr, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_lsqr_trsv_n": (c_int, [c_ptr, c_i64, c_i64, ctypes.c_double, c_ptr, c_ptr, c_ptr]),
+    "skl_lsqr_xw": (
+        c_int, [c_i64, ctypes.c_double, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_srht_dense": (
         c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_srht_dense_shard": (

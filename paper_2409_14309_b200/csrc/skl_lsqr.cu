@@ -1,0 +1,414 @@
+// Device kernels of the preconditioned LSQR iteration (reference:
+// /root/reference/pkg/src/sketchls/solvers.py:110-255 `lsqr`, driven by
+// `sketch_and_precondition` :323-361).  Per iteration the reference does
+//   u = A (R^-1 v) - alfa u;  beta = ||u||;  u /= beta
+//   v = R^-T (A^T u) - beta v;  alfa = ||v||;  v /= alfa
+//   x += (phi/rho) w;  w = v - (theta/rho) w;  ||x||
+// Two full passes over A (HBM-bound) and two n x n triangular solves.  The
+// kernels here fuse each step's vector work into the pass that produces it:
+//   skl_lsqr_gemv_n : u_out = s * (A y) - alpha * u_in, and ||u_out||^2
+//   skl_lsqr_gemv_t : u_n = u_raw / beta (written back), z = A^T u_n
+//   skl_lsqr_trsv_t : v_out = R^-T z - beta v, and ||v_out||^2
+//   skl_lsqr_trsv_n : v_n = v_raw / alfa (written back), y = R^-1 v_n
+//   skl_lsqr_xw     : x += c1 w;  w = v_n + c2 w;  ||x||^2
+// Every reduction is two-level with a fixed order (the last CTA to finish
+// folds the per-CTA partials in index order), so results are deterministic.
+// The scalar recurrence (Givens rotations, stopping tests) stays on the host
+// exactly as the reference writes it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "skl_common.h"
+
+namespace skl {
+
+constexpr int LQ_NT = 256;
+constexpr int LQ_YMAX = 8192;  // y staged in shared memory up to this n
+constexpr int LQ_TC = 16;      // columns per CTA in the transposed product
+
+__device__ __forceinline__ double lq_block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+// The last CTA to arrive folds part[0..nparts) in index order into *out and
+// resets the counter for the next launch.
+__device__ __forceinline__ void lq_finish(const double* part, int nparts, double* out,
+                                          unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == (unsigned)(nparts - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += ((volatile const double*)part)[i];
+    *out = s;
+    *counter = 0u;
+  }
+}
+
+// u_out = s * (A y) - alpha * u_in (u_in may be null), ||u_out||^2.
+// Column-major A; each thread owns two adjacent rows, the columns are folded
+// in ascending order with FMA (dgemv 'N' axpy order).  A null: u_out =
+// -alpha * u_in.
+__global__ void __launch_bounds__(LQ_NT) lsqr_gemv_n_kernel(
+    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ y,
+    double s, double alpha, const double* __restrict__ u_in, double* __restrict__ u_out,
+    double* part, double* norm2, unsigned int* counter) {
+  extern __shared__ double ys[];
+  __shared__ double red[32];
+  const bool stage = A && n <= LQ_YMAX;
+  if (stage)
+    for (int64_t c = threadIdx.x; c < n; c += LQ_NT) ys[c] = y[c];
+  __syncthreads();
+  const double* yv = stage ? ys : y;
+  double ss = 0.0;
+  const int64_t pairs = (m + 1) / 2;
+  for (int64_t pr = blockIdx.x * (int64_t)LQ_NT + threadIdx.x; pr < pairs;
+       pr += (int64_t)gridDim.x * LQ_NT) {
+    const int64_t i = 2 * pr;
+    double a0 = 0.0, a1 = 0.0;
+    if (A) {
+      if (i + 1 < m) {
+        const double* row = A + i;
+        int64_t c = 0;
+        for (; c + 8 <= n; c += 8) {
+          double2 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            v[q] = __ldcs(reinterpret_cast<const double2*>(row + (c + q) * lda));
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            a0 = fma(v[q].x, yv[c + q], a0);
+            a1 = fma(v[q].y, yv[c + q], a1);
+          }
+        }
+        for (; c < n; ++c) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(row + c * lda));
+          a0 = fma(v.x, yv[c], a0);
+          a1 = fma(v.y, yv[c], a1);
+        }
+      } else {
+        for (int64_t c = 0; c < n; ++c) a0 = fma(A[i + c * lda], yv[c], a0);
+      }
+    }
+    const double r0 = s * a0 - (u_in ? alpha * u_in[i] : 0.0);
+    u_out[i] = r0;
+    ss = fma(r0, r0, ss);
+    if (i + 1 < m) {
+      const double r1 = s * a1 - (u_in ? alpha * u_in[i + 1] : 0.0);
+      u_out[i + 1] = r1;
+      ss = fma(r1, r1, ss);
+    }
+  }
+  const double t = lq_block_sum(ss, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  lq_finish(part, gridDim.x, norm2, counter);
+}
+
+// u_n = u_raw / beta (written back), z[c] = sum_i A[i, c] u_n[i].
+// Grid (column groups of LQ_TC, row chunks); per CTA the chunk's u_n stays in
+// registers across the group's columns; partial dots are folded over the
+// chunks in fixed order by the last CTA of each column group.
+__global__ void __launch_bounds__(LQ_NT) lsqr_gemv_t_kernel(
+    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* u_raw,
+    double beta, double* u_n, int64_t rows_per, double* __restrict__ part, double* __restrict__ z,
+    unsigned int* counters) {
+  __shared__ double red[32];
+  __shared__ double sums[LQ_TC];
+  __shared__ bool last;
+  const int64_t g = blockIdx.x, rc = blockIdx.y, nrc = gridDim.y;
+  const int64_t c0 = g * LQ_TC;
+  const int tc = (int)min((int64_t)LQ_TC, n - c0);
+  const int64_t r0 = rc * rows_per, r1 = min(m, r0 + rows_per);
+  double acc[LQ_TC];
+#pragma unroll
+  for (int q = 0; q < LQ_TC; ++q) acc[q] = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += LQ_NT) {
+    const double un = u_raw[i] / beta;
+    if (g == 0) u_n[i] = un;
+    if (A) {
+#pragma unroll
+      for (int q = 0; q < LQ_TC; ++q)
+        if (q < tc) acc[q] = fma(__ldcs(A + (c0 + q) * lda + i), un, acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < LQ_TC; ++q) {
+    const double t = lq_block_sum(acc[q], red);
+    if (threadIdx.x == 0) sums[q] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < LQ_TC) part[(g * nrc + rc) * LQ_TC + threadIdx.x] = sums[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[g], 1u) == (unsigned)(nrc - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < tc) {
+    double s = 0.0;
+    for (int64_t q = 0; q < nrc; ++q)
+      s += ((volatile const double*)part)[(g * nrc + q) * LQ_TC + threadIdx.x];
+    z[c0 + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0) counters[g] = 0u;
+}
+
+// One-CTA triangular solves with the explicit n x n upper R (column-major,
+// ld ldr), 32-row blocks.  The off-diagonal part of a block is 32 dot
+// products (warp per row pair, lanes over the inner index, shuffle
+// reduction); the 32 x 32 diagonal block is solved by warp 0 with the block
+// in registers and x broadcast by shuffles, dividing by R_ii as dtrtrs does.
+constexpr int LT_NT = 512;
+
+// x <- R^-T x  (forward substitution with L = R^T)
+__device__ void lq_solve_t(const double* __restrict__ R, int64_t ldr, int n, double* xs) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int lo = 0; lo < n; lo += 32) {
+    const int w = min(32, n - lo);
+    // xs[lo + r] -= sum_{j < lo} R[j][lo + r] xs[j]
+    for (int r = warp; r < w; r += LT_NT / 32) {
+      const double* col = R + (int64_t)(lo + r) * ldr;
+      double t = 0.0;
+      for (int j = lane; j < lo; j += 32) t = fma(col[j], xs[j], t);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) xs[lo + r] -= t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane r holds column lo + r: Rc[j] = R[lo + j][lo + r] (j < r), diag
+      double Rc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        Rc[j] = (lane < w && j < lane) ? R[(int64_t)(lo + lane) * ldr + lo + j] : 0.0;
+      const double dg = lane < w ? R[(int64_t)(lo + lane) * ldr + lo + lane] : 1.0;
+      double br = lane < w ? xs[lo + lane] : 0.0;
+      double xr = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < w) {
+          if (lane == j) xr = br / dg;
+          const double xj = __shfl_sync(0xffffffffu, xr, j);
+          br = fma(-Rc[j], xj, br);  // Rc[j] = 0 unless j < lane
+        }
+      }
+      if (lane < w) xs[lo + lane] = xr;
+    }
+    __syncthreads();
+  }
+}
+
+// x <- R^-1 x  (backward substitution, dtrsv 'U','N' column order per block)
+__device__ void lq_solve_n(const double* __restrict__ R, int64_t ldr, int n, double* xs) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double xb[32];
+  for (int hi = n; hi > 0; hi -= 32) {
+    const int lo = max(0, hi - 32), w = hi - lo;
+    if (warp == 0) {
+      // lane r holds row lo + r: Rr[j] = R[lo + r][lo + j] (j > r)
+      double Rr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        Rr[j] = (lane < w && j > lane && j < w) ? R[(int64_t)(lo + j) * ldr + lo + lane] : 0.0;
+      const double dg = lane < w ? R[(int64_t)(lo + lane) * ldr + lo + lane] : 1.0;
+      double yr = lane < w ? xs[lo + lane] : 0.0;
+      double xr = 0.0;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < w) {
+          if (lane == j) xr = yr / dg;
+          const double xj = __shfl_sync(0xffffffffu, xr, j);
+          yr = fma(-Rr[j], xj, yr);
+        }
+      }
+      if (lane < w) {
+        xs[lo + lane] = xr;
+        xb[lane] = xr;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < lo; i += LT_NT) {
+      double t0 = 0.0, t1 = 0.0;
+      int j = 0;
+      for (; j + 1 < w; j += 2) {
+        t0 = fma(R[(int64_t)(lo + j) * ldr + i], xb[j], t0);
+        t1 = fma(R[(int64_t)(lo + j + 1) * ldr + i], xb[j + 1], t1);
+      }
+      if (j < w) t0 = fma(R[(int64_t)(lo + j) * ldr + i], xb[j], t0);
+      xs[i] -= t0 + t1;
+    }
+    __syncthreads();
+  }
+}
+
+// v_out = R^-T z - beta v_prev (R null: identity), ||v_out||^2.
+__global__ void __launch_bounds__(LT_NT) lsqr_trsv_t_kernel(const double* __restrict__ R,
+                                                            int64_t ldr, int n,
+                                                            const double* __restrict__ z,
+                                                            double beta, const double* v_prev,
+                                                            double* v_out, double* norm2) {
+  extern __shared__ double xs[];
+  __shared__ double red[32];
+  for (int i = threadIdx.x; i < n; i += LT_NT) xs[i] = z[i];
+  __syncthreads();
+  if (R) lq_solve_t(R, ldr, n, xs);
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < n; i += LT_NT) {
+    const double v = xs[i] - beta * v_prev[i];
+    v_out[i] = v;
+    ss = fma(v, v, ss);
+  }
+  const double t = lq_block_sum(ss, red);
+  if (threadIdx.x == 0) *norm2 = t;
+}
+
+// v_n = v_raw / alfa (alfa > 0; else unchanged), written back; y = R^-1 v_n.
+__global__ void __launch_bounds__(LT_NT) lsqr_trsv_n_kernel(const double* __restrict__ R,
+                                                            int64_t ldr, int n, double alfa,
+                                                            double* v, double* y) {
+  extern __shared__ double xs[];
+  for (int i = threadIdx.x; i < n; i += LT_NT) {
+    const double vn = alfa > 0.0 ? v[i] / alfa : v[i];
+    v[i] = vn;
+    xs[i] = vn;
+  }
+  __syncthreads();
+  if (R) lq_solve_n(R, ldr, n, xs);
+  for (int i = threadIdx.x; i < n; i += LT_NT) y[i] = xs[i];
+}
+
+// x += c1 w; w = v + c2 w; ||x||^2
+__global__ void __launch_bounds__(LT_NT) lsqr_xw_kernel(int n, double c1, double c2,
+                                                        const double* v, double* w, double* x,
+                                                        double* norm2) {
+  __shared__ double red[32];
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < n; i += LT_NT) {
+    const double wi = w[i];
+    const double xi = x[i] + c1 * wi;
+    x[i] = xi;
+    w[i] = v[i] + c2 * wi;
+    ss = fma(xi, xi, ss);
+  }
+  const double t = lq_block_sum(ss, red);
+  if (threadIdx.x == 0) *norm2 = t;
+}
+
+static int sm_count_lq() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : 148;
+  }
+  return cached;
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+// Scratch for the reductions: doubles of `work` and unsigned ints of
+// `counters` (zero-initialised once; the kernels reset what they use).
+extern "C" int64_t skl_lsqr_work_size(int64_t m, int64_t n) {
+  (void)m;
+  const int64_t groups = (n + LQ_TC - 1) / LQ_TC;
+  const int64_t sms = sm_count_lq();
+  return std::max<int64_t>(4 * sms, (4 * sms + groups) * LQ_TC) + 64;
+}
+
+extern "C" int64_t skl_lsqr_counter_size(int64_t n) { return (n + LQ_TC - 1) / LQ_TC + 8; }
+
+extern "C" int skl_lsqr_gemv_n(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                               double s, double alpha, const double* u_in, double* u_out,
+                               double* norm2, double* work, unsigned int* counters, void* stream) {
+  clear_error();
+  SKL_REQUIRE(m >= 1 && n >= 0 && u_out && norm2 && work && counters && (!A || (y && lda >= m)),
+              SKL_ERR_INVALID, "lsqr_gemv_n: bad arguments");
+  SKL_REQUIRE(!A || (((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || m == 1)), SKL_ERR_INVALID,
+              "lsqr_gemv_n: A must be 16-byte aligned with an even leading dimension");
+  const int64_t pairs = (m + 1) / 2;
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((pairs + LQ_NT - 1) / LQ_NT, 4LL * sm_count_lq()));
+  const size_t smem = (A && n <= LQ_YMAX) ? (size_t)n * sizeof(double) : 0;
+  lsqr_gemv_n_kernel<<<blocks, LQ_NT, smem, (cudaStream_t)stream>>>(
+      A, m, n, lda, y, s, alpha, u_in, u_out, work, norm2, counters);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t lda,
+                               const double* u_raw, double beta, double* u_n, double* z,
+                               double* work, unsigned int* counters, void* stream) {
+  clear_error();
+  SKL_REQUIRE(m >= 1 && n >= 1 && u_raw && u_n && z && work && counters && beta > 0.0 &&
+                  (!A || lda >= m),
+              SKL_ERR_INVALID, "lsqr_gemv_t: bad arguments");
+  const int64_t groups = (n + LQ_TC - 1) / LQ_TC;
+  // row chunks: ~2 waves of CTAs, each chunk a multiple of the CTA width
+  int64_t nrc = std::max<int64_t>(1, (4LL * sm_count_lq() + groups - 1) / groups);
+  nrc = std::min<int64_t>(nrc, 1024);
+  int64_t rows_per = (m + nrc - 1) / nrc;
+  rows_per = (rows_per + LQ_NT - 1) / LQ_NT * LQ_NT;
+  nrc = (m + rows_per - 1) / rows_per;
+  lsqr_gemv_t_kernel<<<dim3((unsigned)groups, (unsigned)nrc), LQ_NT, 0, (cudaStream_t)stream>>>(
+      A, m, n, lda, u_raw, beta, u_n, rows_per, work, z, counters);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z,
+                               double beta, const double* v_prev, double* v_out, double* norm2,
+                               void* stream) {
+  clear_error();
+  SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && z && v_prev && v_out && norm2 && (!R || ldr >= n),
+              SKL_ERR_INVALID, "lsqr_trsv_t: bad arguments");
+  const size_t smem = (size_t)n * sizeof(double);
+  if (smem > 48 * 1024)
+    SKL_CUDA(cudaFuncSetAttribute(lsqr_trsv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  lsqr_trsv_t_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, z, beta, v_prev,
+                                                               v_out, norm2);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double alfa, double* v,
+                               double* y, void* stream) {
+  clear_error();
+  SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && v && y && (!R || ldr >= n), SKL_ERR_INVALID,
+              "lsqr_trsv_n: bad arguments");
+  const size_t smem = (size_t)n * sizeof(double);
+  if (smem > 48 * 1024)
+    SKL_CUDA(cudaFuncSetAttribute(lsqr_trsv_n_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  lsqr_trsv_n_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, alfa, v, y);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_xw(int64_t n, double c1, double c2, const double* v, double* w, double* x,
+                           double* norm2, void* stream) {
+  clear_error();
+  SKL_REQUIRE(n >= 1 && v && w && x && norm2, SKL_ERR_INVALID, "lsqr_xw: bad arguments");
+  lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, c1, c2, v, w, x, norm2);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}

@@ -1,0 +1,159 @@
+"""Device LSQR (Paige & Saunders), plain or right-preconditioned by R.
+
+Mirrors /root/reference/pkg/src/sketchls/solvers.py:110-255 (`lsqr`) and
+:258-270 (`_sym_ortho`).  The vector work runs in the fused kernels of
+csrc/skl_lsqr.cu (two HBM passes over A per iteration, the n x n
+triangular solves with R in one CTA each); the scalar recurrence -- Givens
+rotations, the ||A|| estimate and the five stopping rules -- is the
+reference's code, line for line, on host floats read back once per step.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _native
+from ._device import current_stream, device_f64, require_cuda, torch
+from .errors import NumericalBreakdownError
+
+_EPS = float(np.finfo(np.float64).eps)  # solvers.py:37
+
+
+def sym_ortho(a: float, b: float) -> tuple[float, float, float]:
+    """Stable Givens rotation (c, s, r) with c*a + s*b = r (solvers.py:258-270)."""
+    if b == 0.0:
+        return math.copysign(1.0, a) if a != 0 else 1.0, 0.0, abs(a)
+    if a == 0.0:
+        return 0.0, math.copysign(1.0, b), abs(b)
+    if abs(b) > abs(a):
+        tau = a / b
+        s = math.copysign(1.0, b) / math.sqrt(1.0 + tau * tau)
+        return s * tau, s, b / s
+    tau = b / a
+    c = math.copysign(1.0, a) / math.sqrt(1.0 + tau * tau)
+    return c, c * tau, a / c
+
+
+class _Workspace:
+    def __init__(self, m: int, n: int):
+        self.u_raw = device_f64((m,))
+        self.u = device_f64((m,))
+        self.z = device_f64((n,))
+        self.v = device_f64((n,))
+        self.v_raw = device_f64((n,))
+        self.y = device_f64((n,))
+        self.w = device_f64((n,))
+        self.x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")  # beta2, alfa2, x2
+        nw = int(_native.lib().skl_lsqr_work_size(m, n))
+        nc = int(_native.lib().skl_lsqr_counter_size(n))
+        self.work = device_f64((nw,))
+        self.counters = torch.zeros(nc, dtype=torch.int32, device="cuda")
+
+
+def lsqr_device(A, lda: int, m: int, n: int, b, atol: float, btol: float, max_iter: int,
+                R=None, ldr: int = 0):
+    """LSQR on the device for column-major A (m x n, ld lda) and b (device
+    tensors).  With R (n x n upper, column-major) the iteration runs on
+    y -> A R^-1 y and returns x = R^-1 y (solvers.py:146-151, 241).
+    Returns (x tensor, iterations, istop)."""
+    require_cuda()
+    ws = _Workspace(m, n)
+    st = current_stream()
+    P = _native.ptr
+    Ap, Rp = P(A), (P(R) if R is not None else None)
+    sc = ws.scal
+
+    def read(i: int) -> float:
+        return float(sc[i].item())
+
+    # u = b; beta = ||u||  (u_out = -(-1) b: an exact copy plus its norm)
+    _native.call("skl_lsqr_gemv_n", None, m, 0, m, None, 0.0, -1.0, P(b), P(ws.u_raw),
+                 P(sc[0:1]), P(ws.work), P(ws.counters), st)
+    beta = math.sqrt(read(0))
+    alfa = 0.0
+    if beta > 0:
+        # u /= beta; v = rmv(u); alfa = ||v||
+        _native.call("skl_lsqr_gemv_t", Ap, m, n, lda, P(ws.u_raw), beta, P(ws.u), P(ws.z),
+                     P(ws.work), P(ws.counters), st)
+        ws.v.zero_()
+        _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), 0.0, P(ws.v), P(ws.v_raw),
+                     P(sc[1:2]), st)
+        alfa = math.sqrt(read(1))
+    else:
+        ws.u.copy_(ws.u_raw)
+        ws.v_raw.zero_()
+    # v /= alfa (if alfa > 0); y = R^-1 v; w = v
+    _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa, P(ws.v_raw), P(ws.y), st)
+    ws.v.copy_(ws.v_raw)
+    ws.w.copy_(ws.v)
+
+    itn = istop = 0
+    anorm = 0.0
+    rhobar, phibar, bnorm = alfa, beta, beta
+    if alfa * beta == 0.0:
+        return ws.x, 0, 0  # b or A^T b is zero: x = 0 exactly (solvers.py:176-189)
+
+    while itn < max_iter:
+        itn += 1
+        # u = mv(v) - alfa u ; beta = ||u||
+        _native.call("skl_lsqr_gemv_n", Ap, m, n, lda, P(ws.y), 1.0, alfa, P(ws.u), P(ws.u_raw),
+                     P(sc[0:1]), P(ws.work), P(ws.counters), st)
+        beta = math.sqrt(read(0))
+        if beta > 0:
+            anorm = math.sqrt(anorm**2 + alfa**2 + beta**2)
+            # u /= beta ; v = rmv(u) - beta v ; alfa = ||v|| ; v /= alfa
+            _native.call("skl_lsqr_gemv_t", Ap, m, n, lda, P(ws.u_raw), beta, P(ws.u), P(ws.z),
+                         P(ws.work), P(ws.counters), st)
+            _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), beta, P(ws.v), P(ws.v_raw),
+                         P(sc[1:2]), st)
+            alfa = math.sqrt(read(1))
+            _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa, P(ws.v_raw), P(ws.y), st)
+            ws.v, ws.v_raw = ws.v_raw, ws.v
+        else:
+            ws.u, ws.u_raw = ws.u_raw, ws.u  # u stays unnormalised (solvers.py:193)
+        if not (math.isfinite(alfa) and math.isfinite(beta)):
+            raise NumericalBreakdownError(
+                f"non-finite bidiagonalization coefficient at iteration {itn}")
+
+        cs, sn, rho = sym_ortho(rhobar, beta)
+        theta = sn * alfa
+        rhobar = -cs * alfa
+        phi = cs * phibar
+        phibar = sn * phibar
+
+        # x += (phi/rho) w ; w = v + (-theta/rho) w ; xnorm = ||x||
+        _native.call("skl_lsqr_xw", n, phi / rho, -theta / rho, P(ws.v), P(ws.w), P(ws.x),
+                     P(sc[2:3]), st)
+        rnorm = phibar
+        arnorm = alfa * abs(sn * phi)
+        xnorm = math.sqrt(read(2))
+        if not math.isfinite(rnorm):
+            raise NumericalBreakdownError(f"non-finite residual estimate at iteration {itn}")
+
+        test1 = rnorm / bnorm
+        test2 = arnorm / (anorm * rnorm + _EPS)
+        t1 = test1 / (1.0 + anorm * xnorm / bnorm)
+        rtol = btol + atol * anorm * xnorm / bnorm
+        if itn >= max_iter:
+            istop = 7
+        if 1.0 + test2 <= 1.0:
+            istop = 5
+        if 1.0 + t1 <= 1.0:
+            istop = 4
+        if test2 <= atol:
+            istop = 2
+        if test1 <= rtol:
+            istop = 1
+        if istop != 0:
+            break
+
+    x = ws.x
+    if R is not None:
+        xr = device_f64((n,))
+        tmp = ws.x.clone()
+        _native.call("skl_lsqr_trsv_n", Rp, ldr, n, 0.0, P(tmp), P(xr), st)
+        x = xr
+    return x, itn, istop

@@ -7,8 +7,10 @@ dispatcher `solve` :364-398.  The SAA path keeps everything on the device:
 operator build (host RNG, cached plan) -> one sketch pass over [A | b] ->
 Householder QR + back substitution -> a second pass for ||Ax - b||.
 
-Methods other than "saa" (LSQR, sketch-and-precondition, direct) are
-outside this engine's hot path and raise ``SpecError``.
+Sketch-and-precondition (:323-361) and plain LSQR (:110-255) run on the
+device too (lsqr.py, csrc/skl_lsqr.cu) for dense operands.  The "direct"
+normal-equations oracle (:364-398) is outside the engine and raises
+``SpecError``.
 """
 
 from __future__ import annotations
@@ -35,7 +37,7 @@ from .sketch import (
 )
 
 METHODS = ("lsqr", "saa", "sap", "direct")
-ENGINE_METHODS = ("saa",)
+ENGINE_METHODS = ("saa", "sap", "lsqr")
 
 
 @dataclass(frozen=True)
@@ -162,19 +164,107 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
                        residual_norm=rnorm, termination="direct", wall_time_s=wall)
 
 
+def _dense_device(A: Matrix, what: str):
+    if isinstance(A, SparseMatrix):
+        raise SpecError(f"{what} with a SparseMatrix operand is not implemented on the device "
+                        f"(dense operands only)")
+    A_dev = A.data if A.on_device else to_device(A.data)
+    lda = A.ld if A.on_device else A.rows
+    if A_dev.data_ptr() % 16 or (lda % 2 and A.cols > 1):
+        from .sketch import _aligned
+
+        A_dev, lda = _aligned(A_dev, lda, A.cols)
+    return A_dev, lda
+
+
+def _lsqr_result(A, b_dev, A_dev, lda, x_dev, itn, istop, method, sketch, d, t0):
+    wall = time.perf_counter() - t0
+    rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
+    x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
+    return SolveResult(x=Vector(x), method=method, sketch=sketch, d=d, iterations=itn,
+                       residual_norm=rnorm, termination="max_iter" if istop == 7 else "atol_btol",
+                       wall_time_s=wall)
+
+
+def lsqr(A: Matrix, b: Vector, opts: SolverOptions | None = None) -> SolveResult:
+    """Plain LSQR on the device (solvers.py:110-255, no preconditioner)."""
+    from .lsqr import lsqr_device
+
+    if b.len != A.rows:
+        raise ShapeError(f"A is {A.rows}x{A.cols} but b has length {b.len}")
+    require_cuda()
+    opts = opts or SolverOptions()
+    t0 = time.perf_counter()
+    A_dev, lda = _dense_device(A, "lsqr")
+    b_dev = b.data if b.on_device else to_device(b.data)
+    x, itn, istop = lsqr_device(A_dev, lda, A.rows, A.cols, b_dev, opts.atol, opts.btol,
+                                opts.resolve_max_iter(A.cols))
+    return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "lsqr", None, None, t0)
+
+
+def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | None = None,
+                            opts: SolverOptions | None = None) -> SolveResult:
+    """LSQR right-preconditioned by R from QR(S A), warm-started from the
+    sketched solution (solvers.py:323-361)."""
+    from .lsqr import lsqr_device
+
+    A, b = problem.A, problem.b
+    if A.rows < A.cols:
+        raise ShapeError(f"need rows >= cols, got {A.rows}x{A.cols}")
+    require_cuda()
+    opts = opts or SolverOptions()
+    op_spec = _operator_spec(spec, "sap", A.rows, A.cols, opts.d_factor)
+    t0 = time.perf_counter()
+    A_dev, lda = _dense_device(A, "sketch_and_precondition")
+    op = build_sketch(op_spec, A.rows)
+    SA, Sb, _, _, b_dev = sketch_operands_device(op, DenseMatrix(A_dev) if not A.on_device
+                                                 else A, b)
+    d, n = op.target_dim, A.cols
+    try:
+        x0, R, _ = qr_solve_device(SA, d, Sb, d, n, want_r=True)
+    except SingularFactorError as exc:
+        raise SingularFactorError(
+            f"sketched matrix ({op_spec.kind}, d={d}) is rank deficient: {exc}; "
+            f"a larger embedding dimension may help") from exc
+    max_iter = opts.resolve_max_iter(n)
+    if opts.warm_start:
+        # r0 = b - A x0 (solvers.py:345-349)
+        r0 = device_f64((A.rows,))
+        scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+        nw = int(_native.lib().skl_lsqr_work_size(A.rows, n))
+        work = device_f64((nw,))
+        cnt = torch.zeros(int(_native.lib().skl_lsqr_counter_size(n)), dtype=torch.int32,
+                          device="cuda")
+        _native.call("skl_lsqr_gemv_n", _native.ptr(A_dev), A.rows, n, lda, _native.ptr(x0),
+                     -1.0, -1.0, _native.ptr(b_dev), _native.ptr(r0), _native.ptr(scratch),
+                     _native.ptr(work), _native.ptr(cnt), current_stream())
+        xi, itn, istop = lsqr_device(A_dev, lda, A.rows, n, r0, opts.atol, opts.btol, max_iter,
+                                     R=R, ldr=n)
+        x = x0 + xi
+    else:
+        x, itn, istop = lsqr_device(A_dev, lda, A.rows, n, b_dev, opts.atol, opts.btol, max_iter,
+                                    R=R, ldr=n)
+    return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "sap", op_spec.kind, d, t0)
+
+
 def solve(problem: LeastSquaresProblem, method: str = "saa", spec: SketchSpec | None = None,
           opts: SolverOptions | None = None) -> SolveResult:
     """Dispatch (solvers.py:364-398); wall_time_s covers the full path.
 
-    Note: the reference defaults to ``method="lsqr"``; this engine implements
-    the sketch-and-apply path only, so ``"saa"`` is the default here and the
-    other reference methods raise ``SpecError``."""
+    Note: the reference defaults to ``method="lsqr"``; this engine's hot path
+    is sketch-and-apply, so ``"saa"`` is the default here.  "sap" and "lsqr"
+    run on the device for dense operands; "direct" raises ``SpecError``."""
     if method not in METHODS:
         raise SpecError(f"unknown method {method!r}, expected one of {METHODS}")
     if method not in ENGINE_METHODS:
         raise SpecError(f"method {method!r} is outside the B200 engine's scope "
                         f"(implemented: {ENGINE_METHODS})")
     t0 = time.perf_counter()
-    result = sketch_and_apply(problem, spec, opts)
+    if method == "saa":
+        result = sketch_and_apply(problem, spec, opts)
+    elif method == "sap":
+        result = sketch_and_precondition(problem, spec, opts)
+    else:
+        result = lsqr(problem.A, problem.b, opts)
     wall = time.perf_counter() - t0
     return replace(result, wall_time_s=wall)

@@ -457,3 +457,60 @@ def test_row_shards_sum_to_full_apply(kind, m, n, d, world):
     full = np.column_stack([E.apply_to_matrix(op, E.DenseMatrix(A)).data,
                             E.apply_to_vector(op, E.Vector(b)).data])
     assert rel_fro(total, full) <= 1e-13
+
+
+SAP_GPU_CASES = {
+    "sap_cfg1": (W.config(1), "countsketch", True),
+    "sap_cfg2r": (W.config(2, m=1 << 14), "countsketch", True),
+    "sap_cfg3r": (W.config(3, m=8192, n=64, d=256), "gaussian", True),
+    "sap_cfg5r": (W.config(5, m=6000, n=32, d=256), "srht", False),
+}
+
+
+@pytest.mark.parametrize("name", list(SAP_GPU_CASES))
+def test_sap_matches_oracle(golden_meta, name):
+    """solve(problem, "sap", ...): sketch -> device QR (R) -> warm start ->
+    device LSQR preconditioned by R (solvers.py:323-361, 110-255) against the
+    oracle on the same inputs: same iteration count and stopping rule, x and
+    ||Ax - b|| to 1e-9 / 1e-10."""
+    c, kind, warm = SAP_GPU_CASES[name]
+    A, b, _ = W.make_problem(c)
+    want = O.sap_solve(A, b, kind, W.SEED, c.d / c.n, warm_start=warm)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "sap",
+                  E.SketchSpec(kind, 1, seed=W.SEED),
+                  E.SolverOptions(d_factor=c.d / c.n, warm_start=warm))
+    assert res.method == "sap" and res.sketch == kind and res.d == c.d
+    assert res.termination == want["termination"]
+    assert abs(res.iterations - want["iterations"]) <= 1, (res.iterations, want["iterations"])
+    # cfg2 is kappa = 1e8: any backward-stable solve moves x by ~kappa*eps ~ 1e-8
+    # (SURVEY.md §7 H2); the residual still agrees to 1e-10
+    x_tol = 5e-8 if name == "sap_cfg2r" else 1e-9
+    assert rel_fro(res.x.data, want["x"]) <= x_tol
+    assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
+    assert golden_meta[f"{name}_iterations"] == want["iterations"]
+
+
+def test_plain_lsqr_matches_oracle():
+    c = W.config(1, m=3000, n=40)
+    A, b, _ = W.make_problem(c)
+    want = O.lsqr(np.asfortranarray(A), b)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "lsqr")
+    assert res.method == "lsqr" and res.termination == want["termination"]
+    assert abs(res.iterations - want["iterations"]) <= 1
+    assert rel_fro(res.x.data, want["x"]) <= 1e-9
+    assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
+
+
+def test_sap_device_resident_and_sparse_rejected():
+    c = W.config(1, m=4000, n=30)
+    A, b, _ = W.make_problem(c)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(Ad), E.Vector(torch.from_numpy(b).cuda())),
+                  "sap", E.SketchSpec("countsketch", 1, seed=3))
+    assert res.x.data.is_cuda
+    want = O.sap_solve(A, b, "countsketch", 3, 4.0)
+    assert rel_fro(res.x.data.cpu().numpy(), want["x"]) <= 1e-9
+    S = scipy.sparse.random(500, 20, density=0.2, format="csr", random_state=1)
+    with pytest.raises(E.SpecError):
+        E.solve(E.LeastSquaresProblem(E.SparseMatrix.from_scipy(S), E.Vector(np.ones(500))),
+                "sap")
