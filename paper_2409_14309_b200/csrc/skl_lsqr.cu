@@ -120,13 +120,22 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_gemv_n_kernel(
   lq_finish(part, gridDim.x, norm2, counter);
 }
 
-// u_n = u_raw / beta (written back), z[c] = sum_i A[i, c] u_n[i].
-// Grid (column groups of LQ_TC, row chunks); per CTA the chunk's u_n stays in
-// registers across the group's columns; partial dots are folded over the
-// chunks in fixed order by the last CTA of each column group.
+// u_n = u_raw / beta, once per element (the division is the reference's
+// `u /= beta`; doing it here keeps it out of the per-column-group loop).
+__global__ void lsqr_scale_kernel(const double* __restrict__ u_raw, double beta, int64_t m,
+                                  double* __restrict__ u_n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    u_n[i] = u_raw[i] / beta;
+}
+
+// z[c] = sum_i A[i, c] u_n[i].  Grid (column groups of LQ_TC, row chunks);
+// per CTA the chunk's u_n is loaded once per row for the group's columns;
+// partial dots are folded over the chunks in fixed order by the last CTA of
+// each column group.
 __global__ void __launch_bounds__(LQ_NT) lsqr_gemv_t_kernel(
-    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* u_raw,
-    double beta, double* u_n, int64_t rows_per, double* __restrict__ part, double* __restrict__ z,
+    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* u_n,
+    int64_t rows_per, double* __restrict__ part, double* __restrict__ z,
     unsigned int* counters) {
   __shared__ double red[32];
   __shared__ double sums[LQ_TC];
@@ -135,16 +144,31 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_gemv_t_kernel(
   const int64_t c0 = g * LQ_TC;
   const int tc = (int)min((int64_t)LQ_TC, n - c0);
   const int64_t r0 = rc * rows_per, r1 = min(m, r0 + rows_per);
+  // each thread takes row pairs (16-byte loads of A and u_n); rows_per is a
+  // multiple of 2 * LQ_NT, so only the last chunk can end mid-pair
   double acc[LQ_TC];
 #pragma unroll
   for (int q = 0; q < LQ_TC; ++q) acc[q] = 0.0;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += LQ_NT) {
-    const double un = u_raw[i] / beta;
-    if (g == 0) u_n[i] = un;
-    if (A) {
+#pragma unroll 2
+  for (int64_t i = r0 + 2 * threadIdx.x; i < r1; i += 2 * LQ_NT) {
+    if (i + 1 < r1) {
+      const double2 un = *reinterpret_cast<const double2*>(u_n + i);
+      if (A) {
+        double2 av[LQ_TC];
 #pragma unroll
-      for (int q = 0; q < LQ_TC; ++q)
-        if (q < tc) acc[q] = fma(__ldcs(A + (c0 + q) * lda + i), un, acc[q]);
+        for (int q = 0; q < LQ_TC; ++q)
+          av[q] = q < tc ? __ldcs(reinterpret_cast<const double2*>(A + (c0 + q) * lda + i))
+                         : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < LQ_TC; ++q) acc[q] = fma(av[q].y, un.y, fma(av[q].x, un.x, acc[q]));
+      }
+    } else {
+      const double un = u_n[i];
+      if (A) {
+#pragma unroll
+        for (int q = 0; q < LQ_TC; ++q)
+          if (q < tc) acc[q] = fma(A[(c0 + q) * lda + i], un, acc[q]);
+      }
     }
   }
 #pragma unroll
@@ -331,7 +355,7 @@ extern "C" int64_t skl_lsqr_work_size(int64_t m, int64_t n) {
   (void)m;
   const int64_t groups = (n + LQ_TC - 1) / LQ_TC;
   const int64_t sms = sm_count_lq();
-  return std::max<int64_t>(4 * sms, (4 * sms + groups) * LQ_TC) + 64;
+  return std::max<int64_t>(4 * sms, (8 * sms + groups) * LQ_TC) + 64;
 }
 
 extern "C" int64_t skl_lsqr_counter_size(int64_t n) { return (n + LQ_TC - 1) / LQ_TC + 8; }
@@ -361,15 +385,26 @@ extern "C" int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t ld
   SKL_REQUIRE(m >= 1 && n >= 1 && u_raw && u_n && z && work && counters && beta > 0.0 &&
                   (!A || lda >= m),
               SKL_ERR_INVALID, "lsqr_gemv_t: bad arguments");
+  SKL_REQUIRE(!A || (((uintptr_t)A & 15) == 0 && lda % 2 == 0) || m == 1, SKL_ERR_INVALID,
+              "lsqr_gemv_t: A must be 16-byte aligned with an even leading dimension");
+  SKL_REQUIRE(((uintptr_t)u_n & 15) == 0, SKL_ERR_INVALID, "lsqr_gemv_t: u_n must be 16-byte aligned");
   const int64_t groups = (n + LQ_TC - 1) / LQ_TC;
-  // row chunks: ~2 waves of CTAs, each chunk a multiple of the CTA width
-  int64_t nrc = std::max<int64_t>(1, (4LL * sm_count_lq() + groups - 1) / groups);
+  // one wave: row chunks so that groups x chunks fills the resident CTA slots
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_gemv_t_kernel, LQ_NT, 0);
+    occ = std::max(occ, 1);
+  }
+  int64_t nrc = std::max<int64_t>(1, (int64_t)occ * sm_count_lq() / groups);
   nrc = std::min<int64_t>(nrc, 1024);
   int64_t rows_per = (m + nrc - 1) / nrc;
-  rows_per = (rows_per + LQ_NT - 1) / LQ_NT * LQ_NT;
+  rows_per = (rows_per + 2 * LQ_NT - 1) / (2 * LQ_NT) * (2 * LQ_NT);
   nrc = (m + rows_per - 1) / rows_per;
+  const int sblocks = (int)std::min<int64_t>((m + 255) / 256, 8LL * sm_count_lq());
+  lsqr_scale_kernel<<<sblocks, 256, 0, (cudaStream_t)stream>>>(u_raw, beta, m, u_n);
+  SKL_CUDA_LAUNCH();
   lsqr_gemv_t_kernel<<<dim3((unsigned)groups, (unsigned)nrc), LQ_NT, 0, (cudaStream_t)stream>>>(
-      A, m, n, lda, u_raw, beta, u_n, rows_per, work, z, counters);
+      A, m, n, lda, u_n, rows_per, work, z, counters);
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }
