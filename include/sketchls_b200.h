@@ -189,6 +189,16 @@ int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z, do
 /* v <- v / alfa (alfa > 0), y = R^-1 v (R NULL: y = v). */
 int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double alfa, double* v, double* y,
                     void* stream);
+/* CSR operands: u_out = s (A y) - alpha u_in, *norm2 = ||u_out||^2 (rows
+ * folded in stored order); and u_n = u_raw / beta, z = A^T u_n from the
+ * CSC form of A (colptr int64 n+1, rowidx int32 ascending within a column,
+ * values), one warp per column. */
+int skl_lsqr_spmv(const int64_t* indptr, const int64_t* indices, const double* values, int64_t m,
+                  const double* y, double s, double alpha, const double* u_in, double* u_out,
+                  double* norm2, double* work, unsigned int* counters, void* stream);
+int skl_lsqr_csc_t(const int64_t* colptr, const int32_t* rowidx, const double* cval, int64_t m,
+                   int64_t n, const double* u_raw, double beta, double* u_n, double* z,
+                   void* stream);
 /* x += c1 w; w = v + c2 w; *norm2 = ||x||^2. */
 int skl_lsqr_xw(int64_t n, double c1, double c2, const double* v, double* w, double* x,
                 double* norm2, void* stream);

@@ -82,6 +82,15 @@ SIGNATURES: dict[str, tuple] = {
     "skl_lsqr_trsv_t": (
         c_int, [c_ptr, c_i64, c_i64, c_ptr, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_lsqr_trsv_n": (c_int, [c_ptr, c_i64, c_i64, ctypes.c_double, c_ptr, c_ptr, c_ptr]),
+    "skl_lsqr_spmv": (
+        c_int,
+        [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, ctypes.c_double, ctypes.c_double, c_ptr, c_ptr, c_ptr,
+         c_ptr, c_ptr, c_ptr],
+    ),
+    "skl_lsqr_csc_t": (
+        c_int,
+        [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, ctypes.c_double, c_ptr, c_ptr, c_ptr],
+    ),
     "skl_lsqr_xw": (
         c_int, [c_i64, ctypes.c_double, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_srht_dense": (

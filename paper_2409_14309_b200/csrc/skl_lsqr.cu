@@ -193,6 +193,49 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_gemv_t_kernel(
   if (threadIdx.x == 0) counters[g] = 0u;
 }
 
+// ---- CSR operands -------------------------------------------------------
+// u_out = s * (A y) - alpha * u_in, ||u_out||^2 for CSR A: one row per
+// thread, the row's nonzeros folded in stored order from 0 (csr_matvec).
+__global__ void __launch_bounds__(LQ_NT) lsqr_spmv_kernel(
+    const int64_t* __restrict__ indptr, const int64_t* __restrict__ indices,
+    const double* __restrict__ values, int64_t m, const double* __restrict__ y, double s,
+    double alpha, const double* __restrict__ u_in, double* __restrict__ u_out, double* part,
+    double* norm2, unsigned int* counter) {
+  __shared__ double red[32];
+  double ss = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)LQ_NT + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * LQ_NT) {
+    double a = 0.0;
+    const int64_t p1 = indptr[i + 1];
+    for (int64_t p = indptr[i]; p < p1; ++p) a = fma(values[p], y[indices[p]], a);
+    const double r = s * a - (u_in ? alpha * u_in[i] : 0.0);
+    u_out[i] = r;
+    ss = fma(r, r, ss);
+  }
+  const double t = lq_block_sum(ss, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  lq_finish(part, gridDim.x, norm2, counter);
+}
+
+// z[c] = sum over column c of A (CSC, rows ascending) of a_ic u_n[i]: one
+// warp per column, lanes stride the column, fixed shuffle-tree reduction.
+__global__ void __launch_bounds__(LQ_NT) lsqr_csc_t_kernel(const int64_t* __restrict__ colptr,
+                                                           const int32_t* __restrict__ rowidx,
+                                                           const double* __restrict__ cval,
+                                                           int64_t n, const double* __restrict__ u_n,
+                                                           double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = (blockIdx.x * (int64_t)LQ_NT + threadIdx.x) >> 5; c < n;
+       c += ((int64_t)gridDim.x * LQ_NT) >> 5) {
+    double t = 0.0;
+    const int64_t p1 = colptr[c + 1];
+    for (int64_t p = colptr[c] + lane; p < p1; p += 32) t = fma(cval[p], u_n[rowidx[p]], t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) z[c] = t;
+  }
+}
+
 // One-CTA triangular solves with the explicit n x n upper R (column-major,
 // ld ldr), 32-row blocks.  The off-diagonal part of a block is 32 dot
 // products (warp per row pair, lanes over the inner index, shuffle
@@ -444,6 +487,39 @@ extern "C" int skl_lsqr_xw(int64_t n, double c1, double c2, const double* v, dou
   clear_error();
   SKL_REQUIRE(n >= 1 && v && w && x && norm2, SKL_ERR_INVALID, "lsqr_xw: bad arguments");
   lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, c1, c2, v, w, x, norm2);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_spmv(const int64_t* indptr, const int64_t* indices, const double* values,
+                             int64_t m, const double* y, double s, double alpha,
+                             const double* u_in, double* u_out, double* norm2, double* work,
+                             unsigned int* counters, void* stream) {
+  clear_error();
+  SKL_REQUIRE(indptr && indices && values && y && u_out && norm2 && work && counters && m >= 1,
+              SKL_ERR_INVALID, "lsqr_spmv: bad arguments");
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((m + LQ_NT - 1) / LQ_NT, 4LL * sm_count_lq()));
+  lsqr_spmv_kernel<<<blocks, LQ_NT, 0, (cudaStream_t)stream>>>(indptr, indices, values, m, y, s,
+                                                               alpha, u_in, u_out, work, norm2,
+                                                               counters);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_csc_t(const int64_t* colptr, const int32_t* rowidx, const double* cval,
+                              int64_t m, int64_t n, const double* u_raw, double beta, double* u_n,
+                              double* z, void* stream) {
+  clear_error();
+  SKL_REQUIRE(colptr && rowidx && cval && u_raw && u_n && z && m >= 1 && n >= 1 && beta > 0.0,
+              SKL_ERR_INVALID, "lsqr_csc_t: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sblocks = (int)std::min<int64_t>((m + 255) / 256, 8LL * sm_count_lq());
+  lsqr_scale_kernel<<<sblocks, 256, 0, st>>>(u_raw, beta, m, u_n);
+  SKL_CUDA_LAUNCH();
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((n * 32 + LQ_NT - 1) / LQ_NT, 8LL * sm_count_lq()));
+  lsqr_csc_t_kernel<<<blocks, LQ_NT, 0, st>>>(colptr, rowidx, cval, n, u_n, z);
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }

@@ -36,6 +36,53 @@ def sym_ortho(a: float, b: float) -> tuple[float, float, float]:
     return c, c * tau, a / c
 
 
+class DenseOperator:
+    """x -> A x and u -> A^T u for column-major device A (m x n, ld lda)."""
+
+    def __init__(self, A, lda: int, m: int, n: int):
+        self.A, self.lda, self.m, self.n = A, lda, m, n
+
+    def mv(self, y, s, alpha, u_in, u_out, norm2, ws, st):
+        _native.call("skl_lsqr_gemv_n", _native.ptr(self.A), self.m, self.n, self.lda,
+                     _native.ptr(y), s, alpha, _native.ptr(u_in), _native.ptr(u_out),
+                     _native.ptr(norm2), _native.ptr(ws.work), _native.ptr(ws.counters), st)
+
+    def rmv(self, u_raw, beta, u_n, z, ws, st):
+        _native.call("skl_lsqr_gemv_t", _native.ptr(self.A), self.m, self.n, self.lda,
+                     _native.ptr(u_raw), beta, _native.ptr(u_n), _native.ptr(z),
+                     _native.ptr(ws.work), _native.ptr(ws.counters), st)
+
+
+class CsrOperator:
+    """The same two products for a CSR matrix (SparseMatrix device arrays).
+    A^T u runs on the CSC form, built once on the device: a stable sort of
+    the nonzeros by column keeps each column's rows ascending, so the
+    transposed product is deterministic."""
+
+    def __init__(self, indptr, indices, values, m: int, n: int):
+        self.indptr, self.indices, self.values, self.m, self.n = indptr, indices, values, m, n
+        counts = indptr[1:] - indptr[:-1]
+        rows = torch.repeat_interleave(torch.arange(m, dtype=torch.int32, device=indptr.device),
+                                       counts)
+        order = torch.sort(indices, stable=True).indices
+        self.rowidx = rows[order].contiguous()
+        self.cval = values[order].contiguous()
+        colptr = torch.zeros(n + 1, dtype=torch.int64, device=indptr.device)
+        colptr[1:] = torch.cumsum(torch.bincount(indices, minlength=n), 0)
+        self.colptr = colptr
+
+    def mv(self, y, s, alpha, u_in, u_out, norm2, ws, st):
+        _native.call("skl_lsqr_spmv", _native.ptr(self.indptr), _native.ptr(self.indices),
+                     _native.ptr(self.values), self.m, _native.ptr(y), s, alpha,
+                     _native.ptr(u_in), _native.ptr(u_out), _native.ptr(norm2),
+                     _native.ptr(ws.work), _native.ptr(ws.counters), st)
+
+    def rmv(self, u_raw, beta, u_n, z, ws, st):
+        _native.call("skl_lsqr_csc_t", _native.ptr(self.colptr), _native.ptr(self.rowidx),
+                     _native.ptr(self.cval), self.m, self.n, _native.ptr(u_raw), beta,
+                     _native.ptr(u_n), _native.ptr(z), st)
+
+
 class _Workspace:
     def __init__(self, m: int, n: int):
         self.u_raw = device_f64((m,))
@@ -53,17 +100,17 @@ class _Workspace:
         self.counters = torch.zeros(nc, dtype=torch.int32, device="cuda")
 
 
-def lsqr_device(A, lda: int, m: int, n: int, b, atol: float, btol: float, max_iter: int,
+def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
                 R=None, ldr: int = 0):
-    """LSQR on the device for column-major A (m x n, ld lda) and b (device
-    tensors).  With R (n x n upper, column-major) the iteration runs on
-    y -> A R^-1 y and returns x = R^-1 y (solvers.py:146-151, 241).
-    Returns (x tensor, iterations, istop)."""
+    """LSQR on the device for the operator ``op`` (DenseOperator or
+    CsrOperator, m x n) and b (device tensor).  With R (n x n upper,
+    column-major) the iteration runs on y -> A R^-1 y and returns x = R^-1 y
+    (solvers.py:146-151, 241).  Returns (x tensor, iterations, istop)."""
     require_cuda()
     ws = _Workspace(m, n)
     st = current_stream()
     P = _native.ptr
-    Ap, Rp = P(A), (P(R) if R is not None else None)
+    Rp = P(R) if R is not None else None
     sc = ws.scal
 
     def read(i: int) -> float:
@@ -76,8 +123,7 @@ def lsqr_device(A, lda: int, m: int, n: int, b, atol: float, btol: float, max_it
     alfa = 0.0
     if beta > 0:
         # u /= beta; v = rmv(u); alfa = ||v||
-        _native.call("skl_lsqr_gemv_t", Ap, m, n, lda, P(ws.u_raw), beta, P(ws.u), P(ws.z),
-                     P(ws.work), P(ws.counters), st)
+        op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
         ws.v.zero_()
         _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), 0.0, P(ws.v), P(ws.v_raw),
                      P(sc[1:2]), st)
@@ -99,14 +145,12 @@ def lsqr_device(A, lda: int, m: int, n: int, b, atol: float, btol: float, max_it
     while itn < max_iter:
         itn += 1
         # u = mv(v) - alfa u ; beta = ||u||
-        _native.call("skl_lsqr_gemv_n", Ap, m, n, lda, P(ws.y), 1.0, alfa, P(ws.u), P(ws.u_raw),
-                     P(sc[0:1]), P(ws.work), P(ws.counters), st)
+        op.mv(ws.y, 1.0, alfa, ws.u, ws.u_raw, sc[0:1], ws, st)
         beta = math.sqrt(read(0))
         if beta > 0:
             anorm = math.sqrt(anorm**2 + alfa**2 + beta**2)
             # u /= beta ; v = rmv(u) - beta v ; alfa = ||v|| ; v /= alfa
-            _native.call("skl_lsqr_gemv_t", Ap, m, n, lda, P(ws.u_raw), beta, P(ws.u), P(ws.z),
-                         P(ws.work), P(ws.counters), st)
+            op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
             _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), beta, P(ws.v), P(ws.v_raw),
                          P(sc[1:2]), st)
             alfa = math.sqrt(read(1))

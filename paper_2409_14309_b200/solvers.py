@@ -8,7 +8,7 @@ operator build (host RNG, cached plan) -> one sketch pass over [A | b] ->
 Householder QR + back substitution -> a second pass for ||Ax - b||.
 
 Sketch-and-precondition (:323-361) and plain LSQR (:110-255) run on the
-device too (lsqr.py, csrc/skl_lsqr.cu) for dense operands.  The "direct"
+device too (lsqr.py, csrc/skl_lsqr.cu) for dense and CSR operands.  The "direct"
 normal-equations oracle (:364-398) is outside the engine and raises
 ``SpecError``.
 """
@@ -164,17 +164,20 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
                        residual_norm=rnorm, termination="direct", wall_time_s=wall)
 
 
-def _dense_device(A: Matrix, what: str):
+def _operator_device(A: Matrix):
+    """(LSQR operator, dense device A or None, lda) for a carrier."""
+    from .lsqr import CsrOperator, DenseOperator
+
     if isinstance(A, SparseMatrix):
-        raise SpecError(f"{what} with a SparseMatrix operand is not implemented on the device "
-                        f"(dense operands only)")
+        indptr, indices, values = A.device_arrays()
+        return CsrOperator(indptr, indices, values, A.rows, A.cols), None, 0
     A_dev = A.data if A.on_device else to_device(A.data)
     lda = A.ld if A.on_device else A.rows
     if A_dev.data_ptr() % 16 or (lda % 2 and A.cols > 1):
         from .sketch import _aligned
 
         A_dev, lda = _aligned(A_dev, lda, A.cols)
-    return A_dev, lda
+    return DenseOperator(A_dev, lda, A.rows, A.cols), A_dev, lda
 
 
 def _lsqr_result(A, b_dev, A_dev, lda, x_dev, itn, istop, method, sketch, d, t0):
@@ -195,9 +198,9 @@ def lsqr(A: Matrix, b: Vector, opts: SolverOptions | None = None) -> SolveResult
     require_cuda()
     opts = opts or SolverOptions()
     t0 = time.perf_counter()
-    A_dev, lda = _dense_device(A, "lsqr")
+    lop, A_dev, lda = _operator_device(A)
     b_dev = b.data if b.on_device else to_device(b.data)
-    x, itn, istop = lsqr_device(A_dev, lda, A.rows, A.cols, b_dev, opts.atol, opts.btol,
+    x, itn, istop = lsqr_device(lop, A.rows, A.cols, b_dev, opts.atol, opts.btol,
                                 opts.resolve_max_iter(A.cols))
     return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "lsqr", None, None, t0)
 
@@ -215,10 +218,10 @@ def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | Non
     opts = opts or SolverOptions()
     op_spec = _operator_spec(spec, "sap", A.rows, A.cols, opts.d_factor)
     t0 = time.perf_counter()
-    A_dev, lda = _dense_device(A, "sketch_and_precondition")
+    lop, A_dev, lda = _operator_device(A)
     op = build_sketch(op_spec, A.rows)
-    SA, Sb, _, _, b_dev = sketch_operands_device(op, DenseMatrix(A_dev) if not A.on_device
-                                                 else A, b)
+    A_sk = A if (isinstance(A, SparseMatrix) or A.on_device) else DenseMatrix(A_dev)
+    SA, Sb, _, _, b_dev = sketch_operands_device(op, A_sk, b)
     d, n = op.target_dim, A.cols
     try:
         x0, R, _ = qr_solve_device(SA, d, Sb, d, n, want_r=True)
@@ -228,21 +231,17 @@ def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | Non
             f"a larger embedding dimension may help") from exc
     max_iter = opts.resolve_max_iter(n)
     if opts.warm_start:
-        # r0 = b - A x0 (solvers.py:345-349)
+        # r0 = b - A x0 (solvers.py:345-349): -(A x0) - (-1) b
         r0 = device_f64((A.rows,))
         scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
-        nw = int(_native.lib().skl_lsqr_work_size(A.rows, n))
-        work = device_f64((nw,))
-        cnt = torch.zeros(int(_native.lib().skl_lsqr_counter_size(n)), dtype=torch.int32,
-                          device="cuda")
-        _native.call("skl_lsqr_gemv_n", _native.ptr(A_dev), A.rows, n, lda, _native.ptr(x0),
-                     -1.0, -1.0, _native.ptr(b_dev), _native.ptr(r0), _native.ptr(scratch),
-                     _native.ptr(work), _native.ptr(cnt), current_stream())
-        xi, itn, istop = lsqr_device(A_dev, lda, A.rows, n, r0, opts.atol, opts.btol, max_iter,
+        from .lsqr import _Workspace
+
+        lop.mv(x0, -1.0, -1.0, b_dev, r0, scratch, _Workspace(A.rows, n), current_stream())
+        xi, itn, istop = lsqr_device(lop, A.rows, n, r0, opts.atol, opts.btol, max_iter,
                                      R=R, ldr=n)
         x = x0 + xi
     else:
-        x, itn, istop = lsqr_device(A_dev, lda, A.rows, n, b_dev, opts.atol, opts.btol, max_iter,
+        x, itn, istop = lsqr_device(lop, A.rows, n, b_dev, opts.atol, opts.btol, max_iter,
                                     R=R, ldr=n)
     return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "sap", op_spec.kind, d, t0)
 
@@ -253,7 +252,8 @@ def solve(problem: LeastSquaresProblem, method: str = "saa", spec: SketchSpec | 
 
     Note: the reference defaults to ``method="lsqr"``; this engine's hot path
     is sketch-and-apply, so ``"saa"`` is the default here.  "sap" and "lsqr"
-    run on the device for dense operands; "direct" raises ``SpecError``."""
+    run on the device for dense and CSR operands; "direct" raises
+    ``SpecError``."""
     if method not in METHODS:
         raise SpecError(f"unknown method {method!r}, expected one of {METHODS}")
     if method not in ENGINE_METHODS:

@@ -463,6 +463,7 @@ SAP_GPU_CASES = {
     "sap_cfg1": (W.config(1), "countsketch", True),
     "sap_cfg2r": (W.config(2, m=1 << 14), "countsketch", True),
     "sap_cfg3r": (W.config(3, m=8192, n=64, d=256), "gaussian", True),
+    "sap_cfg4r": (W.config(4, m=1 << 16, n=256, d=2048), "countsketch", True),
     "sap_cfg5r": (W.config(5, m=6000, n=32, d=256), "srht", False),
 }
 
@@ -476,7 +477,8 @@ def test_sap_matches_oracle(golden_meta, name):
     c, kind, warm = SAP_GPU_CASES[name]
     A, b, _ = W.make_problem(c)
     want = O.sap_solve(A, b, kind, W.SEED, c.d / c.n, warm_start=warm)
-    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "sap",
+    Ac = E.SparseMatrix.from_scipy(A) if scipy.sparse.issparse(A) else E.DenseMatrix(A)
+    res = E.solve(E.LeastSquaresProblem(Ac, E.Vector(b)), "sap",
                   E.SketchSpec(kind, 1, seed=W.SEED),
                   E.SolverOptions(d_factor=c.d / c.n, warm_start=warm))
     assert res.method == "sap" and res.sketch == kind and res.d == c.d
@@ -501,7 +503,7 @@ def test_plain_lsqr_matches_oracle():
     assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
 
 
-def test_sap_device_resident_and_sparse_rejected():
+def test_sap_device_resident_and_sparse_lsqr():
     c = W.config(1, m=4000, n=30)
     A, b, _ = W.make_problem(c)
     Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
@@ -510,7 +512,13 @@ def test_sap_device_resident_and_sparse_rejected():
     assert res.x.data.is_cuda
     want = O.sap_solve(A, b, "countsketch", 3, 4.0)
     assert rel_fro(res.x.data.cpu().numpy(), want["x"]) <= 1e-9
-    S = scipy.sparse.random(500, 20, density=0.2, format="csr", random_state=1)
-    with pytest.raises(E.SpecError):
-        E.solve(E.LeastSquaresProblem(E.SparseMatrix.from_scipy(S), E.Vector(np.ones(500))),
-                "sap")
+    # plain LSQR on a CSR operand (CSC transposed product on the device)
+    rng = np.random.default_rng(3)
+    S = scipy.sparse.random(5000, 40, density=0.05, format="csr", random_state=rng,
+                            data_rvs=rng.standard_normal)
+    bs = rng.standard_normal(5000)
+    want = O.lsqr(S, bs)
+    res = E.solve(E.LeastSquaresProblem(E.SparseMatrix.from_scipy(S), E.Vector(bs)), "lsqr")
+    assert res.termination == want["termination"]
+    assert abs(res.iterations - want["iterations"]) <= 1
+    assert rel_fro(res.x.data, want["x"]) <= 1e-9
