@@ -343,7 +343,18 @@ def main():
         qb.record(stream)
         torch.cuda.synchronize()
         qr_ms = qa.elapsed_time(qb) / reps
+        # sketch-and-precondition: LSQR preconditioned by R
+        sap_opts = E.SolverOptions(d_factor=d / n)
+        E.solve(prob, "sap", sspec, sap_opts)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            sap = E.solve(prob, "sap", sspec, sap_opts)
+        torch.cuda.synchronize()
+        sap_s = (time.perf_counter() - t0) / 3
         solve = {"solves_per_sec": round(1.0 / solve_s, 3), "ms_per_solve": round(solve_s * 1e3, 3),
+                 "sap_solves_per_sec": round(1.0 / sap_s, 3), "sap_ms_per_solve": round(sap_s * 1e3, 2),
+                 "sap_iterations": sap.iterations, "sap_residual": sap.residual_norm,
                  "solves_per_sec_cold": round(1.0 / cold_s, 3),
                  "ms_per_solve_cold": round(cold_s * 1e3, 3),
                  "qr_solve_ms": round(qr_ms, 3), "residual": res.residual_norm,
