@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "skl_common.h"
 #include "skl_ptx.cuh"
@@ -476,7 +477,25 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nblk = (m + B - 1) / B;
   int P = partitions;
-  if (P <= 0) P = n * 2 >= sms ? 1 : (int)((2 * sms + n - 1) / n);
+  if (P <= 0) {
+    if (b == 12) {
+      // the register kernel runs 2 CTAs per SM: split the blocks of each
+      // column so the grid fills whole waves (the few partial sums are
+      // reduced in fixed order afterwards)
+      const int64_t slots = (int64_t)sms * 2;
+      double best = -1.0;
+      for (int cand = 1; cand <= 8; ++cand) {
+        const int64_t ctas = n * cand;
+        const double eff = (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+        if (eff > best + 0.02) {
+          best = eff;
+          P = cand;
+        }
+      }
+    } else {
+      P = n * 2 >= sms ? 1 : (int)((2 * sms + n - 1) / n);
+    }
+  }
   P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nblk));
   SrParams p;
   p.A = A; p.lda = lda; p.m = m; p.n = n; p.sbits = sbits; p.sample = sample; p.d = d; p.b = b;
