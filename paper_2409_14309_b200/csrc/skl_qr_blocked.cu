@@ -713,7 +713,8 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
     const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
     const int64_t tail = d - j0 - jb;
     // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
-    int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + 127) / 128));
+    static const int tail_rows = getenv("SKL_QR_PANEL_ROWS") ? atoi(getenv("SKL_QR_PANEL_ROWS")) : 128;
+    int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + tail_rows - 1) / tail_rows));
     const int rows2 = (int)((tail + cl2 - 1) / cl2);
     const int rpw = (rows2 + QR_NW2 - 1) / QR_NW2;
     cudaLaunchConfig_t cfg = {};

@@ -522,3 +522,26 @@ def test_sap_device_resident_and_sparse_lsqr():
     assert res.termination == want["termination"]
     assert abs(res.iterations - want["iterations"]) <= 1
     assert rel_fro(res.x.data, want["x"]) <= 1e-9
+
+
+def test_lsqr_edge_cases():
+    """Zero right-hand side (x = 0, no iterations) and the max_iter stop,
+    against the oracle's LSQR (solvers.py:176-189, 232-233)."""
+    c = W.config(1, m=2000, n=25)
+    A, b, _ = W.make_problem(c)
+    prob0 = E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(np.zeros(2000)))
+    res = E.solve(prob0, "lsqr")
+    assert res.iterations == 0 and res.termination == "atol_btol"
+    assert np.array_equal(res.x.data, np.zeros(25))
+    want = O.lsqr(np.asfortranarray(A), b, max_iter=3)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "lsqr",
+                  opts=E.SolverOptions(max_iter=3))
+    assert res.iterations == 3 and res.termination == "max_iter" == want["termination"]
+    assert rel_fro(res.x.data, want["x"]) <= 1e-12
+    # sap without warm start on a device-resident problem, tight max_iter
+    want = O.sap_solve(A, b, "countsketch", 2, 4.0, warm_start=False, max_iter=2)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "sap",
+                  E.SketchSpec("countsketch", 1, seed=2),
+                  E.SolverOptions(warm_start=False, max_iter=2))
+    assert res.iterations == 2 and res.termination == "max_iter"
+    assert rel_fro(res.x.data, want["x"]) <= 1e-10
