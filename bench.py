@@ -247,14 +247,24 @@ def main():
     A, b, _ = W.make_problem(W.config(cfg.cfg, m=m_loc), seed=W.SEED + rank, backend="torch")
     lda = int(A.stride(1))
     spec = E.SketchSpec("countsketch", d, seed=derive_seed(W.SEED, "saa"))
-    t_build0 = time.perf_counter()
-    op = E.build_sketch(spec, m_total)
     r0, r1 = shard_rows(m_total, world, rank)
     assert r1 - r0 == m_loc
-    plan = ShardPlan(op, r0, r1)
-    plan.device_plan()
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t_build0
+
+    def build_operator():
+        E.clear_operator_cache()
+        o = E.build_sketch(spec, m_total)
+        pl = ShardPlan(o, r0, r1)
+        pl.device_plan()
+        torch.cuda.synchronize()
+        return o, pl
+
+    build_operator()  # first call loads kernels
+    builds = []
+    for _ in range(3):
+        t_build0 = time.perf_counter()
+        op, plan = build_operator()
+        builds.append(time.perf_counter() - t_build0)
+    build_s = statistics.median(builds)
 
     stream = torch.cuda.current_stream()
     ld = (d + 1) // 2 * 2
@@ -360,8 +370,8 @@ def main():
                  "qr_solve_ms": round(qr_ms, 3), "residual": res.residual_norm,
                  "operator_build_ms": round(build_s * 1e3, 2),
                  "includes": "sketch S[A|b], QR, back-solve, residual on device-resident A; "
-                             "the *_cold figures also rebuild the operator (host RNG + plan "
-                             "upload) every solve, as the reference does"}
+                             "the *_cold figures also rebuild the operator (device RNG + "
+                             "device plan) every solve, as the reference does"}
 
     # ---- e2e through the C-ABI host-buffer entry point
     e2e = None

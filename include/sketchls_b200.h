@@ -139,6 +139,19 @@ int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, co
 int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
                                int64_t chunk, int warps, uint16_t* lanes, int64_t* chunk_off,
                                int threads);
+/* Device builders (bit-identical to the host ones): hashes/signs into
+ * device arrays (falls back to the host walk in the rare case a Lemire draw
+ * is rejected), and the register-owned plan from device hashes.  The plan
+ * call is two-phase like the host one: lanes == NULL computes chunk_off
+ * (device, nch+1), the per-(chunk, warp) list lengths into maxlen (device,
+ * nch*warps int32) and writes {total words, max block} to total_and_max
+ * (host); the second call fills lanes (device). */
+int skl_rng_countsketch_device(uint64_t key, int64_t m, int64_t d, int32_t* rows, int8_t* signs,
+                               void* stream);
+int skl_countsketch_plan_owned_device(const int32_t* rows, const int8_t* signs, int64_t m,
+                                      int64_t d, int64_t chunk, int warps, uint16_t* lanes,
+                                      int64_t* chunk_off, int32_t* maxlen,
+                                      int64_t* total_and_max, void* stream);
 /* S*A, S*b with a register-owned plan (warps 8 or 16); otherwise as
  * skl_countsketch_dense (bitwise-equal to the reference for partitions 1). */
 int skl_countsketch_dense_owned(const double* A, int64_t m, int64_t n, int64_t lda,

@@ -63,6 +63,9 @@ SIGNATURES: dict[str, tuple] = {
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
          c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     ),
+    "skl_rng_countsketch_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
+    "skl_countsketch_plan_owned_device": (
+        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_countsketch_dense_owned_host": (
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,

@@ -63,14 +63,26 @@ class ShardPlan:
         self.op, self.r0, self.r1 = op, r0, r1
         self.kind = op.kind
         self.d = op.target_dim
-        if op.kind == "countsketch":
-            self.rows = np.ascontiguousarray(op.rows[r0:r1])
-            self.signs = np.ascontiguousarray(op.signs[r0:r1])
         self._plan = None
+
+    @property
+    def rows(self):
+        return np.ascontiguousarray(self.op.rows[self.r0:self.r1])
+
+    @property
+    def signs(self):
+        return np.ascontiguousarray(self.op.signs[self.r0:self.r1])
 
     def device_plan(self) -> CountSketchPlan:
         if self._plan is None:
-            self._plan = CountSketchPlan(self.rows, self.signs, self.d)
+            h = self.op._cache().get("hash") if torch.cuda.is_available() else None
+            if h is not None and _native.plan_geometry(self.d)[0] == "owned":
+                # slices of the device draws: the plan is built on the device
+                self._plan = CountSketchPlan.from_device(h[0][self.r0:self.r1],
+                                                         h[1][self.r0:self.r1], self.d,
+                                                         self.r1 - self.r0)
+            else:
+                self._plan = CountSketchPlan(self.rows, self.signs, self.d)
         return self._plan
 
     def device_srht_words(self):

@@ -79,6 +79,35 @@ class CountSketchPlan:
         self.max_block = mx
         self.plan_bytes = int(lanes.nbytes + off.nbytes)
 
+    @classmethod
+    def from_device(cls, rows_d, signs_d, d: int, m: int) -> "CountSketchPlan":
+        """Register-owned plan built on the device from device hashes
+        (skl_countsketch_plan_owned_device: the same words as the host)."""
+        self = cls.__new__(cls)
+        self.d = int(d)
+        self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, "owned")
+        st = current_stream()
+        tm = np.zeros(2, dtype=np.int64)
+        while True:
+            nch = (m + self.chunk - 1) // self.chunk
+            off = torch.empty(nch + 1, dtype=torch.int64, device="cuda")
+            maxlen = torch.empty(nch * self.warps, dtype=torch.int32, device="cuda")
+            _native.call("skl_countsketch_plan_owned_device", _native.ptr(rows_d),
+                         _native.ptr(signs_d), m, self.d, self.chunk, self.warps, None,
+                         _native.ptr(off), _native.ptr(maxlen), _native.ptr(tm), st)
+            mx = int(tm[1])
+            need = 2 * ((self.chunk + 2) * 8 + 2 * mx + 127)
+            if need <= _SMEM_BUDGET or self.chunk <= 8:
+                break
+            self.chunk = max(8, int(self.chunk * 0.9 * _SMEM_BUDGET / need) // 8 * 8)
+        lanes = torch.empty(max(int(tm[0]), 8), dtype=torch.int16, device="cuda")
+        _native.call("skl_countsketch_plan_owned_device", _native.ptr(rows_d),
+                     _native.ptr(signs_d), m, self.d, self.chunk, self.warps, _native.ptr(lanes),
+                     _native.ptr(off), _native.ptr(maxlen), None, st)
+        self.lanes, self.off, self.max_block = lanes, off, mx
+        self.plan_bytes = int(tm[0]) * 2 + (nch + 1) * 8
+        return self
+
     def apply(self, A, m: int, n: int, lda: int, b, out, ldo: int, outb,
               partitions: int = 0, accumulate: int = 0, stream=None) -> None:
         """out[:, :n] (+)= S A, outb (+)= S b on the device (raw pointers or tensors)."""
@@ -131,18 +160,43 @@ class SketchOperator:
     kernels consume.  ``sparse_map`` / ``gaussian_entries`` are built on
     demand for compatibility with code that inspects them."""
 
-    __slots__ = ("kind", "source_dim", "target_dim", "rows", "signs", "sign_diag",
+    __slots__ = ("kind", "source_dim", "target_dim", "_rows", "_signs", "sign_diag",
                  "row_sample", "padded_dim", "key", "_dev", "_host")
 
     def __init__(self, kind, source_dim, target_dim, rows=None, signs=None, sign_diag=None,
-                 row_sample=None, padded_dim=None, key=None):
+                 row_sample=None, padded_dim=None, key=None, device_hashes=None):
         for name, val in (("kind", kind), ("source_dim", source_dim),
-                          ("target_dim", target_dim), ("rows", rows), ("signs", signs),
+                          ("target_dim", target_dim), ("_rows", rows), ("_signs", signs),
                           ("sign_diag", sign_diag), ("row_sample", row_sample),
                           ("padded_dim", padded_dim), ("key", key)):
             object.__setattr__(self, name, val)
         object.__setattr__(self, "_dev", {})
         object.__setattr__(self, "_host", {})
+        if device_hashes is not None:
+            self._dev.setdefault(device_hashes[0].device.index, {})["hash"] = device_hashes
+
+    # CountSketch hashes: built on the device when a GPU is present (see
+    # _build_sketch); the host copies are fetched on first use.
+    def _host_hashes(self):
+        if "hash" not in self._host:
+            for c in self._dev.values():
+                if "hash" in c:
+                    r, g = c["hash"]
+                    self._host["hash"] = (_freeze(r.cpu().numpy()), _freeze(g.cpu().numpy()))
+                    break
+        return self._host.get("hash")
+
+    @property
+    def rows(self):
+        if self._rows is None and self.kind == "countsketch":
+            return self._host_hashes()[0]
+        return self._rows
+
+    @property
+    def signs(self):
+        if self._signs is None and self.kind == "countsketch":
+            return self._host_hashes()[1]
+        return self._signs
 
     def __setattr__(self, name, value):
         raise AttributeError("SketchOperator is immutable")
@@ -181,11 +235,17 @@ class SketchOperator:
         return self._dev.setdefault(dev, {})
 
     def device_plan(self) -> CountSketchPlan:
-        """The CountSketch apply plan on the current device (built once)."""
+        """The CountSketch apply plan on the current device (built once; on
+        the device from device hashes when they are there)."""
         require_cuda()
         c = self._cache()
         if "plan" not in c:
-            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim)
+            d = self.target_dim
+            if "hash" in c and _native.plan_geometry(d)[0] == "owned":
+                c["plan"] = CountSketchPlan.from_device(c["hash"][0], c["hash"][1], d,
+                                                        self.source_dim)
+            else:
+                c["plan"] = CountSketchPlan(self.rows, self.signs, d)
         return c["plan"]
 
     def device_buckets(self):
@@ -266,6 +326,13 @@ def _build_sketch(spec: SketchSpec, m: int) -> SketchOperator:
     if spec.kind == "gaussian":
         return SketchOperator("gaussian", m, d, key=key)
     if spec.kind == "countsketch":
+        if torch.cuda.is_available():
+            # draws on the device (bit-identical to the host walk)
+            rows_d = torch.empty(m, dtype=torch.int32, device="cuda")
+            signs_d = torch.empty(m, dtype=torch.int8, device="cuda")
+            _native.call("skl_rng_countsketch_device", key, m, d, _native.ptr(rows_d),
+                         _native.ptr(signs_d), current_stream())
+            return SketchOperator("countsketch", m, d, key=key, device_hashes=(rows_d, signs_d))
         rows, signs = _native.rng_countsketch(key, m, d)
         return SketchOperator("countsketch", m, d, rows=_freeze(rows), signs=_freeze(signs),
                               key=key)

@@ -545,3 +545,41 @@ def test_lsqr_edge_cases():
                   E.SolverOptions(warm_start=False, max_iter=2))
     assert res.iterations == 2 and res.termination == "max_iter"
     assert rel_fro(res.x.data, want["x"]) <= 1e-10
+
+
+@pytest.mark.parametrize("m,d", [(1, 1), (7, 2), (20_000, 800), (1 << 20, 2048), (123_457, 3),
+                                 (4000, 3 << 29)])
+def test_device_countsketch_draws_match_host(m, d):
+    """skl_rng_countsketch_device == the host walk (== numpy), including the
+    forced-rejection stream (d = 3*2^29: a quarter of the draws rejected)
+    that takes the host path."""
+    key = O.derive_seed(77, "countsketch", m)
+    rows_d = torch.empty(m, dtype=torch.int32, device="cuda")
+    signs_d = torch.empty(m, dtype=torch.int8, device="cuda")
+    _native.call("skl_rng_countsketch_device", key, m, d, rows_d.data_ptr(), signs_d.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+    rows, signs = _native.rng_countsketch(key, m, d)
+    assert np.array_equal(rows_d.cpu().numpy(), rows)
+    assert np.array_equal(signs_d.cpu().numpy(), signs)
+
+
+@pytest.mark.parametrize("m,d", [(1, 1), (100, 4), (8185, 5), (20_000, 800), (65_537, 2048),
+                                 (1 << 20, 2048), (30_001, 1025)])
+def test_device_owned_plan_matches_host(m, d):
+    """The device plan builder emits the host planner's words exactly
+    (bitonic bucket sort + the same greedy bank-balancing merge), including
+    the chunk shrink for tiny d."""
+    from paper_2409_14309_b200.sketch import CountSketchPlan
+
+    E.clear_operator_cache()
+    op = E.build_sketch(E.SketchSpec("countsketch", d, seed=m + d), m)
+    rows, signs = op.rows, op.signs  # host copies of the device draws
+    key = O.derive_seed(m + d, "countsketch", m)
+    want_rows, want_signs = O.countsketch_draws(key, m, d)
+    assert np.array_equal(rows, want_rows) and np.array_equal(signs, want_signs)
+    dev = op.device_plan()
+    host = CountSketchPlan(rows, signs, d)
+    assert (dev.chunk, dev.warps, dev.max_block) == (host.chunk, host.warps, host.max_block)
+    assert np.array_equal(dev.off.cpu().numpy(), host.off.cpu().numpy())
+    n = host.lanes.numel()
+    assert np.array_equal(dev.lanes[:n].cpu().numpy(), host.lanes.cpu().numpy())
