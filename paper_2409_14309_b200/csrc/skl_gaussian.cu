@@ -34,12 +34,26 @@ namespace skl {
 
 constexpr double ZIG_R = 3.6541528853610087963519472518;
 constexpr double ZIG_INV_R = 0.27366123732975827203338247596;
-constexpr int ZIG_S = 4096;  // words per segment
+constexpr int ZIG_S = 1024;  // words per segment
 constexpr int ZIG_MASKW = ZIG_S / 32;
 
 __constant__ uint64_t c_ki[256];
 __constant__ double c_wi[256];
 __constant__ double c_fi[256];
+// Per-CTA shared copies: the ziggurat strip index is random per thread, and
+// divergent __constant__ reads serialise across the warp (up to 32 ways).
+__shared__ uint64_t s_ki[256];
+__shared__ double s_wi[256];
+__shared__ double s_fi[256];
+
+__device__ __forceinline__ void zig_load_tables() {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    s_ki[i] = c_ki[i];
+    s_wi[i] = c_wi[i];
+    s_fi[i] = c_fi[i];
+  }
+  __syncthreads();
+}
 
 static std::mutex g_tab_mu;
 static bool g_tab_set = false;
@@ -70,9 +84,9 @@ __host__ __device__ __forceinline__ double next_double_of(uint64_t w) {
 #define ZMUL(a, b) __dmul_rn((a), (b))
 #define ZADD(a, b) __dadd_rn((a), (b))
 #define ZSUB(a, b) __dsub_rn((a), (b))
-#define ZKI c_ki
-#define ZWI c_wi
-#define ZFI c_fi
+#define ZKI s_ki
+#define ZWI s_wi
+#define ZFI s_fi
 #else
 #define ZMUL(a, b) ((a) * (b))
 #define ZADD(a, b) ((a) + (b))
@@ -122,6 +136,7 @@ __host__ __device__ __forceinline__ uint64_t zig_parse(WordStream& ws, uint64_t 
 
 // A: speculative parse of each segment.
 __global__ void zig_spec_kernel(uint64_t key, int64_t nseg, uint32_t* mask, uint64_t* exitpos) {
+  zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
   WordStream ws(key);
@@ -158,6 +173,7 @@ __device__ __forceinline__ int zig_count_from(const uint32_t* mk, int off) {
 // B: true per-segment counts from the true entries; flags a broken chain.
 __global__ void zig_count_kernel(uint64_t key, int64_t nseg, const uint32_t* mask,
                                  const uint64_t* exitpos, int64_t* count, int* bad) {
+  zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
   const uint64_t s0 = (uint64_t)k * ZIG_S;
@@ -216,6 +232,7 @@ __global__ void zig_write_kernel(uint64_t key, int64_t nseg, const uint64_t* exi
                                  const int64_t* count, const int64_t* offset, int64_t N,
                                  int64_t m, double* G, int64_t ldg, double sqrt_d,
                                  int64_t* tail_t, uint64_t* tail_pos, int* tail_n, int tail_cap) {
+  zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
   int64_t t = offset[k];
