@@ -45,35 +45,39 @@ __global__ void __launch_bounds__(CSR_B * 32)
   if (i < d) {
     const int64_t r_beg = bptr[i], r_end = bptr[i + 1];
     double* my = tile + warp * ldt;  // column c at my[c - c0]
-    // Row metadata of round r+1 is fetched while round r is committed
-    // (two dependent loads: bucket row -> its CSR extent; the signs come
-// pre-gathered in bucket order, so they stream).
-    int64_t np0 = 0, ncnt = 0;
-    double ns = 0.0;
+    // Software pipeline over rounds of 32 rows: the bucket-row index of
+    // round r+2 (coalesced) and the CSR extent of round r+1 (dependent on
+    // it) are in flight while round r commits; the signs come pre-gathered
+    // in bucket order, so they stream.
+    // raw loads of the next round; converted only when the round starts, so
+    // nothing waits on them early
+    int64_t np0 = 0, np1 = 0;
+    int8_t nsg = 0;
+    int32_t nj = -1;  // bucket row of round r+2 for this lane
     {
       const int64_t r = r_beg + lane;
       if (r < r_end) {
         const int32_t j = brow[r];
         np0 = indptr[j];
-        ncnt = indptr[j + 1] - np0;
-        ns = (double)bsign[r];
+        np1 = indptr[j + 1];
+        nsg = bsign[r];
       }
+      const int64_t r2 = r_beg + 32 + lane;
+      if (r2 < r_end) nj = brow[r2];
     }
     for (int64_t base = r_beg; base < r_end; base += 32) {
-      const int64_t p0 = np0, cnt = ncnt;
-      const double s = ns;
+      const int64_t p0 = np0, cnt = np1 - np0;
+      const double s = (double)nsg;
       np0 = 0;
-      ncnt = 0;
-      ns = 0.0;
-      if (base + 32 < r_end) {
-        const int64_t r = base + 32 + lane;
-        if (r < r_end) {
-          const int32_t j = brow[r];
-          np0 = indptr[j];
-          ncnt = indptr[j + 1] - np0;
-          ns = (double)bsign[r];
-        }
+      np1 = 0;
+      nsg = 0;
+      if (nj >= 0) {
+        np0 = indptr[nj];
+        np1 = indptr[nj + 1];
+        nsg = bsign[base + 32 + lane];
       }
+      nj = -1;
+      if (base + 64 + lane < r_end) nj = brow[base + 64 + lane];
       // exclusive scan of counts over the warp (lane order == ascending j)
       int64_t incl = cnt;
 #pragma unroll
