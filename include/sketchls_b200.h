@@ -160,6 +160,25 @@ int skl_countsketch_dense_owned(const double* A, int64_t m, int64_t n, int64_t l
                                 int64_t ldsa, double* Sb, int partitions, int accumulate,
                                 void* stream);
 
+/* Sparse sign embedding (sketch.py:104-115: s distinct buckets per source
+ * row, values +-1/sqrt(s)): the same register-owned plan with s entries per
+ * row (rows/signs are m x s, row-major) and the apply with every entry scaled
+ * by `scale` = fl(1/sqrt(s)) (one rounded product, as csr_matvecs).  The CSR
+ * operand variant takes the bucket lists of S (bucket_rows = source rows,
+ * ascending per bucket; signs in bucket order). */
+int skl_sparsesign_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m, int64_t s,
+                              int64_t d, int64_t chunk, int warps, uint16_t* lanes,
+                              int64_t* chunk_off, int threads);
+int skl_sparsesign_dense_owned(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                               const uint16_t* lanes, const int64_t* chunk_off, int64_t max_block,
+                               int64_t d, int64_t chunk, int warps, double scale, double* SA,
+                               int64_t ldsa, double* Sb, int partitions, int accumulate,
+                               void* stream);
+int skl_sparsesign_csr(const int64_t* indptr, const int64_t* indices, const double* values,
+                       int64_t m, int64_t n, const int32_t* bucket_rows, const int64_t* bucket_ptr,
+                       const int8_t* signs, double scale, int64_t d, double* SA, int64_t ldsa,
+                       void* stream);
+
 /* Same apply with HOST A/b/SA/Sb: streams row blocks of A through the
  * device with host-to-device copies overlapped with the kernel; if
  * A_dev_keep != NULL the device copy of A (ld = m rounded up to 32) is

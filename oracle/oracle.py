@@ -94,6 +94,38 @@ def gaussian_draws(key: int, d: int, m: int) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ applies
+def sparsesign_draws(key: int, m: int, d: int, s: int):
+    """sketch.py:104-110, 130-149: (rows (m, s) int64, signs (m, s) +-1.0)."""
+    rng = stream(key)
+    if s == d:
+        rows = np.tile(np.arange(d, dtype=np.int64), (m, 1))
+    elif d <= 4 * s * s:
+        rows = np.empty((m, s), dtype=np.int64)
+        chunk = max(1, 5 * 10**7 // d)
+        for lo in range(0, m, chunk):
+            hi = min(m, lo + chunk)
+            keys = rng.random((hi - lo, d))
+            rows[lo:hi] = np.argpartition(keys, s - 1, axis=1)[:, :s]
+    else:
+        rows = rng.integers(0, d, size=(m, s))
+        while True:
+            srt = np.sort(rows, axis=1)
+            bad = np.flatnonzero(np.any(np.diff(srt, axis=1) == 0, axis=1))
+            if bad.size == 0:
+                break
+            rows[bad] = rng.integers(0, d, size=(bad.size, s))
+    signs = 2.0 * rng.integers(0, 2, size=(m, s)) - 1.0
+    return rows, signs
+
+
+def sparsesign_map(rows, signs, d: int, m: int) -> scipy.sparse.csr_matrix:
+    """sketch.py:111-114."""
+    s = rows.shape[1]
+    vals = signs.ravel() / math.sqrt(s)
+    cols = np.repeat(np.arange(m), s)
+    return scipy.sparse.csr_matrix((vals, (rows.ravel(), cols)), shape=(d, m), dtype=np.float64)
+
+
 def countsketch_map(rows, signs, d: int, m: int) -> scipy.sparse.csr_matrix:
     """sketch.py:100-102."""
     return scipy.sparse.csr_matrix((signs, (rows, np.arange(m))), shape=(d, m), dtype=np.float64)
@@ -207,6 +239,11 @@ def sketch_apply(kind: str, key: int, d: int, A, b=None):
         G = gaussian_draws(key, d, m)
         SA = gaussian_apply(G, A)
         Sb = gaussian_apply(G, b) if b is not None else None
+    elif kind == "sparsesign":  # default sparsity s = 8 (sketch.py:52)
+        rows, signs = sparsesign_draws(key, m, d, 8)
+        smap = sparsesign_map(rows, signs, d, m)
+        SA = (smap @ scipy.sparse.csr_matrix(A)).toarray() if scipy.sparse.issparse(A) else smap @ A
+        Sb = smap @ b if b is not None else None
     else:
         raise ValueError(kind)
     return SA, Sb

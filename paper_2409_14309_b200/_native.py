@@ -66,6 +66,18 @@ SIGNATURES: dict[str, tuple] = {
     "skl_rng_countsketch_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
     "skl_countsketch_plan_owned_device": (
         c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_sparsesign_plan_owned": (
+        c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_int]),
+    "skl_sparsesign_dense_owned": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int,
+         ctypes.c_double, c_ptr, c_i64, c_ptr, c_int, c_int, c_ptr],
+    ),
+    "skl_sparsesign_csr": (
+        c_int,
+        [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, ctypes.c_double, c_i64, c_ptr,
+         c_i64, c_ptr],
+    ),
     "skl_countsketch_dense_owned_host": (
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
@@ -263,16 +275,22 @@ def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, wa
 
 
 def countsketch_plan_owned(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
-                           threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
-    """(lanes u16, chunk_off i64 [nch+1], max block words) of the register-owned plan."""
-    m = rows.shape[0]
+                           threads: int = 0, spr: int = 1) -> tuple[np.ndarray, np.ndarray, int]:
+    """(lanes u16, chunk_off i64 [nch+1], max block words) of the register-owned
+    plan; ``spr`` entries per source row (rows/signs flattened m x spr)."""
+    m = rows.shape[0] // spr
     nch = (m + chunk - 1) // chunk
     off = np.zeros(nch + 1, dtype=np.int64)
-    call("skl_countsketch_plan_owned", ptr(rows), ptr(signs), m, d, chunk, warps, None, ptr(off),
-         threads)
+    if spr == 1:
+        args = lambda lanes: (ptr(rows), ptr(signs), m, d, chunk, warps, lanes, ptr(off), threads)  # noqa: E731
+        fn = "skl_countsketch_plan_owned"
+    else:
+        args = lambda lanes: (ptr(rows), ptr(signs), m, spr, d, chunk, warps, lanes, ptr(off),  # noqa: E731
+                              threads)
+        fn = "skl_sparsesign_plan_owned"
+    call(fn, *args(None))
     lanes = np.empty(int(off[-1]), dtype=np.uint16)
-    call("skl_countsketch_plan_owned", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(lanes),
-         ptr(off), threads)
+    call(fn, *args(ptr(lanes)))
     return lanes, off, int(np.diff(off).max())
 
 

@@ -237,9 +237,13 @@ struct OwParams {
   double* outb;
   double* part;
   int accumulate;
+  double scale;  // entry value magnitude (sparse sign embedding: fl(1/sqrt(s)))
 };
 
-template <int NT>
+// SCALED: every entry is (+-scale) * A[j] rounded once, as scipy's
+// csr_matvecs computes val * x for val = +-scale (sparse sign embeddings);
+// CountSketch entries are +-1 (exact sign flips, no multiply).
+template <int NT, bool SCALED>
 __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -319,7 +323,8 @@ __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwP
     for (int r = r0; r < r1; ++r) {
       const uint32_t e = Lr[r * 32];
       const uint2 w = *reinterpret_cast<const uint2*>(st + (e & 0x1fffu) * 8);
-      const double x = __hiloint2double((int)(w.y ^ ((e & 0x8000u) << 16)), (int)w.x);
+      double x = __hiloint2double((int)(w.y ^ ((e & 0x8000u) << 16)), (int)w.x);
+      if (SCALED) x = __dmul_rn(x, p.scale);
       // Exactly one slot accumulates.  Written as branches around each add
       // so ptxas emits four predicated DADDs (a C if-chain or predicated PTX
       // adds come out as DADD + FSEL select chains, 3x the issue slots).
@@ -485,7 +490,7 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
                                     const int64_t* chunk_off, int64_t max_block, int64_t d,
                                     int64_t chunk, int warps, double* SA, int64_t ldsa, double* Sb,
                                     int partitions, int accumulate, int64_t row_begin,
-                                    int64_t row_end, cudaStream_t st) {
+                                    int64_t row_end, cudaStream_t st, double scale = 1.0) {
   SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld", (long long)m, (long long)n,
               (long long)d);
@@ -523,7 +528,7 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   p.A = A; p.lda = lda; p.b = b; p.n = n; p.ncols = ncols; p.row_begin = row_begin;
   p.row_end = row_end; p.lanes = lanes; p.chunk_off = chunk_off; p.max_block = (int)max_block;
   p.d = (int)d; p.T = T; p.head = (warps + 1 + 7) / 8 * 8; p.P = P; p.stages = stages; p.out = SA; p.ldo = ldsa;
-  p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
+  p.outb = Sb; p.part = nullptr; p.accumulate = accumulate; p.scale = scale;
   double* part = nullptr;
   if (P > 1) {
     SKL_CUDA(malloc_async(&part, (size_t)P * ncols * d * sizeof(double), st));
@@ -531,8 +536,9 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   }
   dim3 grid((unsigned)ncols, (unsigned)P);
   cudaError_t e;
+  const bool scaled = scale != 1.0;
   if (warps == 16) {
-    auto k = countsketch_owned_kernel<512>;
+    auto k = scaled ? countsketch_owned_kernel<512, true> : countsketch_owned_kernel<512, false>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -542,7 +548,7 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
       e = cudaGetLastError();
     }
   } else {
-    auto k = countsketch_owned_kernel<256>;
+    auto k = scaled ? countsketch_owned_kernel<256, true> : countsketch_owned_kernel<256, false>;
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -580,6 +586,18 @@ extern "C" int skl_countsketch_dense_owned(const double* A, int64_t m, int64_t n
   clear_error();
   return countsketch_owned_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps,
                                   SA, ldsa, Sb, partitions, accumulate, 0, m, (cudaStream_t)stream);
+}
+
+extern "C" int skl_sparsesign_dense_owned(const double* A, int64_t m, int64_t n, int64_t lda,
+                                          const double* b, const uint16_t* lanes,
+                                          const int64_t* chunk_off, int64_t max_block, int64_t d,
+                                          int64_t chunk, int warps, double scale, double* SA,
+                                          int64_t ldsa, double* Sb, int partitions,
+                                          int accumulate, void* stream) {
+  clear_error();
+  return countsketch_owned_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps,
+                                  SA, ldsa, Sb, partitions, accumulate, 0, m, (cudaStream_t)stream,
+                                  scale);
 }
 
 extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
                            const double* __restrict__ values, const int32_t* __restrict__ brow,
                            const int64_t* __restrict__ bptr, const int8_t* __restrict__ bsign,
                            int64_t d, int64_t n, int64_t Cw, double* __restrict__ SA,
-                           int64_t ldsa) {
+                           int64_t ldsa, double scale) {
   extern __shared__ double tile[];  // [CSR_B][cw + 1] (bucket-major, odd stride)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)blockIdx.x * CSR_B;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
     }
     for (int64_t base = r_beg; base < r_end; base += 32) {
       const int64_t p0 = np0, cnt = np1 - np0;
-      const double s = (double)nsg;
+      const double s = (double)nsg * scale;  // +-1 (CountSketch) or +-fl(1/sqrt(s))
       np0 = 0;
       np1 = 0;
       nsg = 0;
@@ -152,13 +152,10 @@ extern "C" int skl_countsketch_buckets(const int32_t* rows, int64_t m, int64_t d
   return SKL_OK;
 }
 
-extern "C" int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices,
-                                   const double* values, int64_t m, int64_t n,
-                                   const int32_t* bucket_rows, const int64_t* bucket_ptr,
-                                   const int8_t* signs, int64_t d, double* SA, int64_t ldsa,
-                                   void* stream) {
-  clear_error();
-  cudaStream_t st = (cudaStream_t)stream;
+static int csr_launch(const int64_t* indptr, const int64_t* indices, const double* values,
+                      int64_t m, int64_t n, const int32_t* bucket_rows, const int64_t* bucket_ptr,
+                      const int8_t* signs, double scale, int64_t d, double* SA, int64_t ldsa,
+                      cudaStream_t st) {
   SKL_REQUIRE(indptr && bucket_rows && bucket_ptr && signs && SA && m >= 1 && n >= 1 && d >= 1 &&
                   ldsa >= d,
               SKL_ERR_SHAPE, "countsketch_csr: bad arguments");
@@ -170,8 +167,29 @@ extern "C" int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices
                                 (int)smem));
   dim3 grid((unsigned)((d + CSR_B - 1) / CSR_B), (unsigned)((n + Cw - 1) / Cw));
   countsketch_csr_kernel<<<grid, CSR_B * 32, smem, st>>>(indptr, indices, values, bucket_rows,
-                                                         bucket_ptr, signs, d, n, Cw, SA, ldsa);
+                                                         bucket_ptr, signs, d, n, Cw, SA, ldsa,
+                                                         scale);
   SKL_CUDA_LAUNCH();
   (void)m;
   return SKL_OK;
+}
+
+extern "C" int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices,
+                                   const double* values, int64_t m, int64_t n,
+                                   const int32_t* bucket_rows, const int64_t* bucket_ptr,
+                                   const int8_t* signs, int64_t d, double* SA, int64_t ldsa,
+                                   void* stream) {
+  clear_error();
+  return csr_launch(indptr, indices, values, m, n, bucket_rows, bucket_ptr, signs, 1.0, d, SA,
+                    ldsa, (cudaStream_t)stream);
+}
+
+extern "C" int skl_sparsesign_csr(const int64_t* indptr, const int64_t* indices,
+                                  const double* values, int64_t m, int64_t n,
+                                  const int32_t* bucket_rows, const int64_t* bucket_ptr,
+                                  const int8_t* signs, double scale, int64_t d, double* SA,
+                                  int64_t ldsa, void* stream) {
+  clear_error();
+  return csr_launch(indptr, indices, values, m, n, bucket_rows, bucket_ptr, signs, scale, d, SA,
+                    ldsa, (cudaStream_t)stream);
 }

@@ -46,19 +46,21 @@ int64_t head_words(int warps) { return (warps + 1 + 7) / 8 * 8; }
 struct OwnedScratch {
   std::vector<uint32_t> cnt, start, pos, rows_of;
   std::vector<uint16_t> sorted;
-  OwnedScratch(int64_t d, int64_t chunk)
-      : cnt((size_t)d), start((size_t)d), pos((size_t)d), sorted((size_t)chunk) {}
+  OwnedScratch(int64_t d, int64_t entries)
+      : cnt((size_t)d), start((size_t)d), pos((size_t)d), sorted((size_t)entries) {}
 };
 
 // Returns the block length (u16 words) of chunk k; fills blk when non-null.
-// -1 on a bucket out of range.
-int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d, int64_t chunk,
-                    int warps, int64_t k, OwnedScratch& S, uint16_t* blk) {
+// -1 on a bucket out of range.  Source row j contributes `spr` entries
+// (rows/signs[j * spr + q], distinct buckets -- 1 for CountSketch, s for a
+// sparse sign embedding).  sorted[] holds row | negative << 15.
+int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                    int64_t chunk, int warps, int64_t k, OwnedScratch& S, uint16_t* blk) {
   const int64_t r0 = k * chunk;
   const int len = (int)std::min<int64_t>(chunk, m - r0);
   std::fill(S.cnt.begin(), S.cnt.end(), 0u);
-  for (int j = 0; j < len; ++j) {
-    const int32_t r = rows[r0 + j];
+  for (int64_t e = 0; e < (int64_t)len * spr; ++e) {
+    const int32_t r = rows[r0 * spr + e];
     if (r < 0 || r >= d) return -1;
     ++S.cnt[(size_t)r];
   }
@@ -68,7 +70,11 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int64_t
     S.pos[(size_t)b] = run;
     run += S.cnt[(size_t)b];
   }
-  for (int j = 0; j < len; ++j) S.sorted[S.pos[(size_t)rows[r0 + j]]++] = (uint16_t)j;
+  for (int j = 0; j < len; ++j)
+    for (int q = 0; q < spr; ++q) {
+      const int64_t e = (r0 + j) * spr + q;
+      S.sorted[S.pos[(size_t)rows[e]]++] = (uint16_t)(j | ((signs[e] < 0 ? 1u : 0u) << 15));
+    }
   const int64_t head = head_words(warps);
   const uint16_t pad = (uint16_t)chunk;  // zero slot, slot 0, positive
   int64_t total_rows = 0;
@@ -96,7 +102,7 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int64_t
           for (int s = 0; s < kSlots; ++s) {
             const int64_t b = (int64_t)w * 32 + l + (int64_t)s * 32 * warps;
             if (b >= d || nxt[l][s] >= S.cnt[(size_t)b]) continue;
-            const uint32_t j = S.sorted[S.start[(size_t)b] + nxt[l][s]];
+            const uint32_t j = S.sorted[S.start[(size_t)b] + nxt[l][s]] & 0x1fffu;
             const int ld = kNoBank ? 0 : load[j & 15];
             const uint32_t left = S.cnt[(size_t)b] - nxt[l][s];
             if (ld < bload || (ld == bload && left > bleft)) {
@@ -108,9 +114,10 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int64_t
           uint16_t word = pad;
           if (best >= 0) {
             const int64_t b = (int64_t)w * 32 + l + (int64_t)best * 32 * warps;
-            const uint32_t j = S.sorted[S.start[(size_t)b] + nxt[l][best]++];
+            const uint32_t e = S.sorted[S.start[(size_t)b] + nxt[l][best]++];
+            const uint32_t j = e & 0x1fffu;
             load[j & 15]++;
-            word = (uint16_t)(j | ((uint32_t)best << 13) | ((signs[r0 + j] < 0 ? 1u : 0u) << 15));
+            word = (uint16_t)(j | ((uint32_t)best << 13) | (e & 0x8000u));
           }
           R[(size_t)step * 32 + l] = word;
         }
@@ -123,14 +130,11 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int64_t
   return head + total_rows * 32;
 }
 
-}  // namespace
-
-extern "C" int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m,
-                                          int64_t d, int64_t chunk, int warps, uint16_t* lanes,
-                                          int64_t* chunk_off, int threads) {
-  skl::clear_error();
-  SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1, SKL_ERR_INVALID,
-              "skl_countsketch_plan_owned: bad arguments");
+int plan_owned(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                      int64_t chunk, int warps, uint16_t* lanes, int64_t* chunk_off,
+                      int threads) {
+  SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1 && spr >= 1, SKL_ERR_INVALID,
+              "owned plan: bad arguments");
   SKL_REQUIRE(warps >= 1 && warps <= 31 && d <= (int64_t)warps * 32 * kSlots, SKL_ERR_SPEC,
               "owned plan: embed_dim %lld needs more than %d warps x 32 lanes x %d slots",
               (long long)d, warps, kSlots);
@@ -141,9 +145,9 @@ extern "C" int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* sig
   std::vector<int64_t> sz((size_t)nch);
   std::atomic<int> bad{0};
   par_for(nch, threads, [&](int64_t lo, int64_t hi) {
-    OwnedScratch S(d, chunk);
+    OwnedScratch S(d, chunk * spr);
     for (int64_t k = lo; k < hi; ++k) {
-      const int64_t n = owned_chunk(rows, signs, m, d, chunk, warps, k, S, nullptr);
+      const int64_t n = owned_chunk(rows, signs, m, spr, d, chunk, warps, k, S, nullptr);
       if (n < 0 || n > 65535 * 32) {
         bad = n < 0 ? 1 : 2;
         return;
@@ -162,9 +166,27 @@ extern "C" int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* sig
     SKL_REQUIRE(chunk_off[k + 1] - chunk_off[k] == sz[(size_t)k], SKL_ERR_INVALID,
                 "owned plan: chunk offsets do not match");
   par_for(nch, threads, [&](int64_t lo, int64_t hi) {
-    OwnedScratch S(d, chunk);
+    OwnedScratch S(d, chunk * spr);
     for (int64_t k = lo; k < hi; ++k)
-      owned_chunk(rows, signs, m, d, chunk, warps, k, S, lanes + chunk_off[k]);
+      owned_chunk(rows, signs, m, spr, d, chunk, warps, k, S, lanes + chunk_off[k]);
   });
   return SKL_OK;
+}
+
+}  // namespace
+
+extern "C" int skl_countsketch_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m,
+                                          int64_t d, int64_t chunk, int warps, uint16_t* lanes,
+                                          int64_t* chunk_off, int threads) {
+  skl::clear_error();
+  return plan_owned(rows, signs, m, 1, d, chunk, warps, lanes, chunk_off, threads);
+}
+
+extern "C" int skl_sparsesign_plan_owned(const int32_t* rows, const int8_t* signs, int64_t m,
+                                         int64_t s, int64_t d, int64_t chunk, int warps,
+                                         uint16_t* lanes, int64_t* chunk_off, int threads) {
+  skl::clear_error();
+  SKL_REQUIRE(s >= 1 && s <= d, SKL_ERR_SPEC, "sparse sign plan: sparsity %lld out of [1, d]",
+              (long long)s);
+  return plan_owned(rows, signs, m, (int)s, d, chunk, warps, lanes, chunk_off, threads);
 }

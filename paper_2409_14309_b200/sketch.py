@@ -33,12 +33,16 @@ from . import _native
 from ._device import current_stream, device_f64, require_cuda, to_device, torch
 from .errors import CapacityError, ShapeError, SpecError
 from .linalg import DenseMatrix, Matrix, SparseMatrix, Vector, _freeze
-from .rng import derive_seed
+from .rng import derive_seed, stream
 
 KINDS = ("gaussian", "srht", "countsketch", "sparsesign", "identity")
 DEFAULT_KIND = "countsketch"
-# Kinds with a native implementation in this engine (sparsesign is "next").
-ENGINE_KINDS = ("gaussian", "srht", "countsketch", "identity")
+# Kinds with a native implementation in this engine.
+ENGINE_KINDS = ("gaussian", "srht", "countsketch", "sparsesign", "identity")
+
+# Chunk bound (entries) of the dense key matrix when sampling distinct rows in
+# the collision-prone regime (sketch.py:35).
+_SAMPLE_CHUNK_ENTRIES = 5 * 10**7
 
 _MATERIALIZE_GUARD = 10**7
 
@@ -57,15 +61,25 @@ class CountSketchPlan:
     lists (skl_countsketch_dense).  Either way the per-bucket fold order is
     ascending source row, so the ordered apply is bitwise-equal to scipy."""
 
-    def __init__(self, rows: np.ndarray, signs: np.ndarray, d: int, kind: str | None = None):
+    def __init__(self, rows: np.ndarray, signs: np.ndarray, d: int, kind: str | None = None,
+                 spr: int = 1):
         self.d = int(d)
+        self.spr = int(spr)
+        self.scale = 1.0 / math.sqrt(spr) if spr > 1 else 1.0
         self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, kind)
+        if spr > 1:
+            if self.kind != "owned":
+                raise SpecError(f"sparse sign embeddings with embed_dim {d} > "
+                                f"{_native.OWNED_MAX_D} are implemented for CSR operands only")
+            self.chunk = max(8, self.chunk // spr // 8 * 8)
+            rows = np.ascontiguousarray(rows, dtype=np.int32).reshape(-1)
+            signs = np.ascontiguousarray(signs, dtype=np.int8).reshape(-1)
         # The kernels' ring stages (A chunk + plan block) must fit shared
         # memory: shrink the chunk when few buckets make per-lane lists long.
         while True:
             if self.kind == "owned":
                 lanes, off, mx = _native.countsketch_plan_owned(rows, signs, self.d, self.chunk,
-                                                                self.warps)
+                                                                self.warps, spr=self.spr)
                 need = 2 * ((self.chunk + 2) * 8 + 2 * mx + 127)
             else:
                 lanes, off, mx = _native.countsketch_plan(rows, signs, self.d, self.chunk,
@@ -85,6 +99,7 @@ class CountSketchPlan:
         (skl_countsketch_plan_owned_device: the same words as the host)."""
         self = cls.__new__(cls)
         self.d = int(d)
+        self.spr, self.scale = 1, 1.0
         self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, "owned")
         st = current_stream()
         tm = np.zeros(2, dtype=np.int64)
@@ -111,6 +126,13 @@ class CountSketchPlan:
     def apply(self, A, m: int, n: int, lda: int, b, out, ldo: int, outb,
               partitions: int = 0, accumulate: int = 0, stream=None) -> None:
         """out[:, :n] (+)= S A, outb (+)= S b on the device (raw pointers or tensors)."""
+        if getattr(self, "spr", 1) > 1:
+            _native.call("skl_sparsesign_dense_owned", _native.ptr(A), m, n, lda, _native.ptr(b),
+                         _native.ptr(self.lanes), _native.ptr(self.off), self.max_block, self.d,
+                         self.chunk, self.warps, self.scale, _native.ptr(out), ldo,
+                         _native.ptr(outb), partitions, accumulate,
+                         current_stream() if stream is None else stream)
+            return
         fn = "skl_countsketch_dense_owned" if self.kind == "owned" else "skl_countsketch_dense"
         _native.call(fn, _native.ptr(A), m, n, lda, _native.ptr(b), _native.ptr(self.lanes),
                      _native.ptr(self.off), self.max_block, self.d, self.chunk, self.warps,
@@ -161,14 +183,14 @@ class SketchOperator:
     demand for compatibility with code that inspects them."""
 
     __slots__ = ("kind", "source_dim", "target_dim", "_rows", "_signs", "sign_diag",
-                 "row_sample", "padded_dim", "key", "_dev", "_host")
+                 "row_sample", "padded_dim", "key", "sparsity", "_dev", "_host")
 
     def __init__(self, kind, source_dim, target_dim, rows=None, signs=None, sign_diag=None,
-                 row_sample=None, padded_dim=None, key=None, device_hashes=None):
+                 row_sample=None, padded_dim=None, key=None, device_hashes=None, sparsity=None):
         for name, val in (("kind", kind), ("source_dim", source_dim),
                           ("target_dim", target_dim), ("_rows", rows), ("_signs", signs),
                           ("sign_diag", sign_diag), ("row_sample", row_sample),
-                          ("padded_dim", padded_dim), ("key", key)):
+                          ("padded_dim", padded_dim), ("key", key), ("sparsity", sparsity)):
             object.__setattr__(self, name, val)
         object.__setattr__(self, "_dev", {})
         object.__setattr__(self, "_host", {})
@@ -208,14 +230,21 @@ class SketchOperator:
     # ------------------------------------------------ reference-compatible views
     @property
     def sparse_map(self):
-        """d x m scipy CSR of a CountSketch (sketch.py:100-102), built lazily."""
-        if self.kind != "countsketch":
+        """d x m scipy CSR of a CountSketch (sketch.py:100-102) or a sparse
+        sign embedding (:110-114), built lazily."""
+        if self.kind not in ("countsketch", "sparsesign"):
             return None
         if "csr" not in self._host:
             m, d = self.source_dim, self.target_dim
-            self._host["csr"] = scipy.sparse.csr_matrix(
-                (self.signs.astype(np.float64), (self.rows.astype(np.int64), np.arange(m))),
-                shape=(d, m), dtype=np.float64)
+            if self.kind == "countsketch":
+                vals = self.signs.astype(np.float64)
+                rows, cols = self.rows.astype(np.int64), np.arange(m)
+            else:
+                s = self.sparsity
+                vals = self.signs.astype(np.float64).ravel() / math.sqrt(s)
+                rows, cols = self.rows.astype(np.int64).ravel(), np.repeat(np.arange(m), s)
+            self._host["csr"] = scipy.sparse.csr_matrix((vals, (rows, cols)), shape=(d, m),
+                                                        dtype=np.float64)
         return self._host["csr"]
 
     @property
@@ -239,6 +268,12 @@ class SketchOperator:
         the device from device hashes when they are there)."""
         require_cuda()
         c = self._cache()
+        if "plan" not in c and self.kind == "sparsesign":
+            if self.target_dim > _native.OWNED_MAX_D:
+                raise SpecError(f"sparse sign embeddings with embed_dim {self.target_dim} > "
+                                f"{_native.OWNED_MAX_D} are implemented for CSR operands only")
+            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim, kind="owned",
+                                        spr=self.sparsity)
         if "plan" not in c:
             d = self.target_dim
             if "hash" in c and _native.plan_geometry(d)[0] == "owned":
@@ -250,12 +285,16 @@ class SketchOperator:
 
     def device_buckets(self):
         """(bucket_rows int32, bucket_ptr int64, bucket-ordered signs int8) on
-        the current device: the CSR of S consumed by the CSR-operand kernel."""
+        the current device: the CSR of S consumed by the CSR-operand kernel
+        (for a sparse sign embedding each source row appears in s buckets)."""
         require_cuda()
         c = self._cache()
         if "buckets" not in c:
-            brow, bptr = _native.countsketch_buckets(self.rows, self.target_dim)
-            bsign = np.ascontiguousarray(self.signs[brow])
+            spr = self.sparsity if self.kind == "sparsesign" else 1
+            flat_rows = np.ascontiguousarray(self.rows.reshape(-1), dtype=np.int32)
+            ent, bptr = _native.countsketch_buckets(flat_rows, self.target_dim)
+            bsign = np.ascontiguousarray(self.signs.reshape(-1)[ent])
+            brow = (ent // spr).astype(np.int32) if spr > 1 else ent
             c["buckets"] = (to_device(brow), to_device(bptr), to_device(bsign))
         return c["buckets"]
 
@@ -337,12 +376,43 @@ def _build_sketch(spec: SketchSpec, m: int) -> SketchOperator:
         return SketchOperator("countsketch", m, d, rows=_freeze(rows), signs=_freeze(signs),
                               key=key)
     if spec.kind == "sparsesign":
-        raise SpecError("sparsesign is not implemented by the B200 engine yet "
-                        f"(engine kinds: {ENGINE_KINDS})")
+        # sketch.py:104-115: the draws come from numpy's own Generator on the
+        # operator stream (bit-identical by construction, including the
+        # argpartition and redraw paths); the apply runs on the device
+        s = spec.sparsity
+        if s > d:
+            raise SpecError(f"sparsesign needs sparsity <= embed_dim, got s={s}, d={d}")
+        rng = stream(key)
+        rows = _sample_distinct_rows(rng, m, d, s)
+        signs = 2.0 * rng.integers(0, 2, size=(m, s)) - 1.0
+        return SketchOperator("sparsesign", m, d, rows=_freeze(rows.astype(np.int32)),
+                              signs=_freeze(signs.astype(np.int8)), key=key, sparsity=s)
     m_pad = 1 << (m - 1).bit_length()
     signs8, sample = _native.rng_srht(key, m_pad, d)
     return SketchOperator("srht", m, d, sign_diag=_freeze(signs8.astype(np.float64)),
                           row_sample=_freeze(sample), padded_dim=m_pad, key=key)
+
+
+def _sample_distinct_rows(rng, m: int, d: int, s: int) -> np.ndarray:
+    """m independent uniform samples of s distinct rows out of d -- the
+    reference's draw sequence (sketch.py:130-149) on the same Generator."""
+    if s == d:
+        return np.tile(np.arange(d, dtype=np.int64), (m, 1))
+    if d <= 4 * s * s:
+        out = np.empty((m, s), dtype=np.int64)
+        chunk = max(1, _SAMPLE_CHUNK_ENTRIES // d)
+        for lo in range(0, m, chunk):
+            hi = min(m, lo + chunk)
+            keys = rng.random((hi - lo, d))
+            out[lo:hi] = np.argpartition(keys, s - 1, axis=1)[:, :s]
+        return out
+    rows = rng.integers(0, d, size=(m, s))
+    while True:
+        srt = np.sort(rows, axis=1)
+        bad = np.flatnonzero(np.any(np.diff(srt, axis=1) == 0, axis=1))
+        if bad.size == 0:
+            return rows
+        rows[bad] = rng.integers(0, d, size=(bad.size, s))
 
 
 # ------------------------------------------------------------------ applies
@@ -389,6 +459,12 @@ def _countsketch_csr_device(op: SketchOperator, A: SparseMatrix):
     brow, bptr, signs = op.device_buckets()
     d, n = op.target_dim, A.cols
     SA = device_f64((d, n), fortran=True)
+    if op.kind == "sparsesign":
+        _native.call("skl_sparsesign_csr", _native.ptr(indptr), _native.ptr(indices),
+                     _native.ptr(values), A.rows, n, _native.ptr(brow), _native.ptr(bptr),
+                     _native.ptr(signs), 1.0 / math.sqrt(op.sparsity), d, _native.ptr(SA), d,
+                     current_stream())
+        return SA
     _native.call("skl_countsketch_csr", _native.ptr(indptr), _native.ptr(indices),
                  _native.ptr(values), A.rows, n, _native.ptr(brow), _native.ptr(bptr),
                  _native.ptr(signs), d, _native.ptr(SA), d, current_stream())
@@ -422,7 +498,7 @@ def _apply_device(op: SketchOperator, operand):
     Returns a column-major tensor (d x n) or a vector tensor (d)."""
     require_cuda()
     if isinstance(operand, SparseMatrix):
-        if op.kind == "countsketch":
+        if op.kind in ("countsketch", "sparsesign"):
             return _countsketch_csr_device(op, operand)
         if op.kind == "identity":
             return to_device(operand.to_scipy().toarray(order="F"))
@@ -442,7 +518,7 @@ def _apply_dense_tensor(op: SketchOperator, t, m: int, n: int, lda: int | None =
     lda = lda if lda is not None else (int(t.stride(1)) if n > 1 else m)
     if op.kind == "identity":
         return t.clone()
-    if op.kind == "countsketch":
+    if op.kind in ("countsketch", "sparsesign"):
         SA, _ = _countsketch_dense_device(op, t, lda, n)
         return SA
     if op.kind == "srht":
@@ -508,6 +584,8 @@ def materialize(op: SketchOperator) -> DenseMatrix:
         out = np.zeros((d, m))
         out[op.rows, np.arange(m)] = op.signs
         return DenseMatrix(out)
+    if op.kind == "sparsesign":
+        return DenseMatrix(op.sparse_map.toarray())
     cols = np.arange(m, dtype=np.int64)
     parity = np.bitwise_count(op.row_sample[:, None] & cols[None, :]) & 1
     h_rows = 1.0 - 2.0 * parity.astype(np.float64)

@@ -120,7 +120,7 @@ def sketch_operands_device(op, A: Matrix, b: Vector):
     are uploaded once when host-resident and reused for the residual."""
     b_dev = b.data if b.on_device else to_device(b.data)
     if isinstance(A, SparseMatrix):
-        if op.kind == "countsketch":
+        if op.kind in ("countsketch", "sparsesign"):
             SA = _countsketch_csr_device(op, A)
             Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
             return SA, Sb, None, 0, b_dev
@@ -130,7 +130,7 @@ def sketch_operands_device(op, A: Matrix, b: Vector):
         return SA, Sb, None, 0, b_dev
     A_dev = A.data if A.on_device else to_device(A.data)
     lda = A.ld if A.on_device else A.rows
-    if op.kind == "countsketch":
+    if op.kind in ("countsketch", "sparsesign"):
         SA, Sb = _countsketch_dense_device(op, A_dev, lda, A.cols, b=b_dev)
     else:
         SA = _apply_dense_tensor(op, A_dev, A.rows, A.cols, lda=lda)

@@ -145,6 +145,25 @@ def main() -> None:
             g[f"{name}_SA_cols"] = SA[:, :4].copy()
         meta[f"{name}_shape"] = [c.m, c.n, c.d]
 
+    # --- sparse sign embeddings (sketch.py:104-115, 130-149): both row-sampling
+    # regimes (argpartition when d <= 4 s^2, integers + redraw otherwise)
+    for m, d, s_, seed in [(60, 32, 5, 5), (40, 9, 8, 1), (3000, 64, 8, 2), (5000, 2048, 8, 3),
+                           (20_000, 800, 8, 4), (100, 8, 8, 6)]:
+        op = ref.build_sketch(ref.SketchSpec("sparsesign", d, seed=seed, sparsity=s_), m)
+        coo = op.sparse_map.tocoo()
+        g[f"ss_row_{m}_{d}_{s_}_{seed}"] = coo.row.astype(np.int32)
+        g[f"ss_col_{m}_{d}_{s_}_{seed}"] = coo.col.astype(np.int32)
+        g[f"ss_val_{m}_{d}_{s_}_{seed}"] = coo.data
+    c = W.config(1)
+    A, b, _ = W.make_problem(c)
+    prob = ref.LeastSquaresProblem(A=ref.DenseMatrix(A), b=ref.Vector(b))
+    res = ref.solve(prob, "saa", ref.SketchSpec("sparsesign", 1, seed=W.SEED),
+                    ref.SolverOptions(d_factor=c.d / c.n))
+    g["ss_cfg1_x"] = res.x.data
+    meta["ss_cfg1_residual"] = res.residual_norm
+    op = ref.build_sketch(ref.SketchSpec("sparsesign", c.d, seed=derive_seed(W.SEED, "saa")), c.m)
+    meta["ss_cfg1_SA_sha"] = sha(np.asfortranarray(ref.apply_to_matrix(op, ref.DenseMatrix(A)).data))
+
     # --- SAP (sketch-and-precondition + LSQR, solvers.py:323-361, 110-255)
     sap_cases = {
         "sap_cfg1": (W.config(1), "countsketch", True),

@@ -583,3 +583,46 @@ def test_device_owned_plan_matches_host(m, d):
     assert np.array_equal(dev.off.cpu().numpy(), host.off.cpu().numpy())
     n = host.lanes.numel()
     assert np.array_equal(dev.lanes[:n].cpu().numpy(), host.lanes.cpu().numpy())
+
+
+@pytest.mark.parametrize("m,n,d,s", [(1, 1, 1, 1), (60, 3, 32, 5), (40, 2, 9, 8), (3000, 7, 64, 8),
+                                     (20_000, 200, 800, 8), (65_537, 5, 2048, 8),
+                                     (10_000, 4, 512, 1), (5000, 3, 100, 100)])
+def test_sparsesign_dense_apply_bitwise(m, n, d, s):
+    """Sparse sign embedding S A, S b on the device (register-owned plan with
+    s entries per row, one rounded product per entry) against scipy's
+    csr_matvecs fold: bitwise."""
+    rng = np.random.default_rng(m + s)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec("sparsesign", d, seed=m + d, sparsity=s), m)
+    smap = op.sparse_map
+    assert np.array_equal(E.apply_to_matrix(op, E.DenseMatrix(A)).data, smap @ A)
+    assert np.array_equal(E.apply_to_vector(op, E.Vector(b)).data, smap @ b)
+
+
+@pytest.mark.parametrize("m,n,d,s", [(3000, 40, 64, 8), (20_000, 300, 4096, 8), (500, 9, 9, 8)])
+def test_sparsesign_csr_apply_bitwise(m, n, d, s):
+    rng = np.random.default_rng(m)
+    A = scipy.sparse.random(m, n, density=0.05, format="csr", random_state=rng,
+                            data_rvs=rng.standard_normal)
+    A.sort_indices()
+    op = E.build_sketch(E.SketchSpec("sparsesign", d, seed=3, sparsity=s), m)
+    got = E.apply_to_matrix(op, E.SparseMatrix.from_scipy(A)).data
+    assert np.array_equal(np.asarray(got), (op.sparse_map @ A).toarray())
+
+
+def test_sparsesign_saa_and_limits(golden, golden_meta):
+    c = W.config(1)
+    A, b, _ = W.make_problem(c)
+    want = O.saa_solve(A, b, "sparsesign", W.SEED, c.d / c.n)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "saa",
+                  E.SketchSpec("sparsesign", 1, seed=W.SEED), E.SolverOptions(d_factor=c.d / c.n))
+    assert res.sketch == "sparsesign" and res.d == c.d
+    assert rel_fro(res.x.data, want["x"]) <= 1e-9
+    assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
+    assert rel_fro(want["x"], golden["ss_cfg1_x"]) <= 1e-12
+    # dense operands with d > 2048 are not implemented for sparse sign embeddings
+    op = E.build_sketch(E.SketchSpec("sparsesign", 4096, seed=1), 10_000)
+    with pytest.raises(E.SpecError):
+        E.apply_to_matrix(op, E.DenseMatrix(np.ones((10_000, 2))))

@@ -206,3 +206,40 @@ def test_plain_lsqr_oracle_matches_reference(golden, golden_meta):
     assert got["iterations"] == golden_meta["lsqr_small_iterations"]
     assert got["termination"] == golden_meta["lsqr_small_termination"]
     assert rel_fro(got["x"], golden["lsqr_small_x"]) <= 1e-12
+
+
+SS_CASES = [(60, 32, 5, 5), (40, 9, 8, 1), (3000, 64, 8, 2), (5000, 2048, 8, 3), (20_000, 800, 8, 4),
+            (100, 8, 8, 6)]
+
+
+@pytest.mark.parametrize("m,d,s,seed", SS_CASES)
+def test_sparsesign_oracle_structure(golden, m, d, s, seed):
+    """oracle.sparsesign_draws/map == the reference's sparse_map (COO triples),
+    in both row-sampling regimes (argpartition, integers + redraw) and s == d."""
+    rows, signs = O.sparsesign_draws(O.derive_seed(seed, "sparsesign", m), m, d, s)
+    coo = O.sparsesign_map(rows, signs, d, m).tocoo()
+    assert np.array_equal(coo.row.astype(np.int32), golden[f"ss_row_{m}_{d}_{s}_{seed}"])
+    assert np.array_equal(coo.col.astype(np.int32), golden[f"ss_col_{m}_{d}_{s}_{seed}"])
+    assert np.array_equal(coo.data, golden[f"ss_val_{m}_{d}_{s}_{seed}"])
+
+
+@pytest.mark.parametrize("m,d,s,seed", SS_CASES)
+def test_sparsesign_engine_draws_match_reference(golden, m, d, s, seed):
+    """The engine's operator (numpy draws on the operator stream) builds the
+    same S as the reference (CPU: no device needed for the draws)."""
+    import paper_2409_14309_b200 as E
+
+    op = E.build_sketch(E.SketchSpec("sparsesign", d, seed=seed, sparsity=s), m)
+    coo = op.sparse_map.tocoo()
+    assert np.array_equal(coo.row.astype(np.int32), golden[f"ss_row_{m}_{d}_{s}_{seed}"])
+    assert np.array_equal(coo.col.astype(np.int32), golden[f"ss_col_{m}_{d}_{s}_{seed}"])
+    assert np.array_equal(coo.data, golden[f"ss_val_{m}_{d}_{s}_{seed}"])
+
+
+def test_sparsesign_saa_oracle(golden, golden_meta):
+    c = W.config(1)
+    A, b, _ = W.make_problem(c)
+    got = O.saa_solve(A, b, "sparsesign", W.SEED, c.d / c.n)
+    assert rel_fro(got["x"], golden["ss_cfg1_x"]) <= 1e-12
+    assert hashlib.sha256(np.asfortranarray(got["SA"]).tobytes()).hexdigest() == \
+        golden_meta["ss_cfg1_SA_sha"]
