@@ -23,8 +23,6 @@
 namespace {
 
 constexpr int kSlots = 4;
-// experiment switch: ignore the shared-memory bank balance when merging
-static const bool kNoBank = getenv("SKL_PLAN_NOBANK") != nullptr;
 
 template <class F>
 void par_for(int64_t n, int threads, F&& f) {
@@ -103,7 +101,7 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr
             const int64_t b = (int64_t)w * 32 + l + (int64_t)s * 32 * warps;
             if (b >= d || nxt[l][s] >= S.cnt[(size_t)b]) continue;
             const uint32_t j = S.sorted[S.start[(size_t)b] + nxt[l][s]] & 0x1fffu;
-            const int ld = kNoBank ? 0 : load[j & 15];
+            const int ld = load[j & 15];
             const uint32_t left = S.cnt[(size_t)b] - nxt[l][s];
             if (ld < bload || (ld == bload && left > bleft)) {
               best = s;

@@ -626,3 +626,40 @@ def test_sparsesign_saa_and_limits(golden, golden_meta):
     op = E.build_sketch(E.SketchSpec("sparsesign", 4096, seed=1), 10_000)
     with pytest.raises(E.SpecError):
         E.apply_to_matrix(op, E.DenseMatrix(np.ones((10_000, 2))))
+
+
+def test_concurrent_solves_from_threads():
+    """The C-ABI is reentrant (SURVEY.md §8b threading): four host threads
+    solving different problems at once, each on its own CUDA stream, get the
+    same answers as serial solves."""
+    import threading
+
+    cases = []
+    for t in range(4):
+        c = W.config(1, m=6000 + 1000 * t, n=20 + t)
+        A, b, _ = W.make_problem(c, seed=100 + t)
+        cases.append((A, b, "countsketch" if t % 2 == 0 else "srht"))
+    serial = [E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "saa",
+                      E.SketchSpec(kind, 1, seed=5)).x.data for A, b, kind in cases]
+    out = [None] * 4
+    errs = []
+
+    def work(t):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                A, b, kind = cases[t]
+                r = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "saa",
+                            E.SketchSpec(kind, 1, seed=5))
+                torch.cuda.current_stream().synchronize()
+                out[t] = r.x.data
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errs, errs
+    for t in range(4):
+        assert np.array_equal(out[t], serial[t])
