@@ -268,7 +268,10 @@ def main():
 
     stream = torch.cuda.current_stream()
     ld = (d + 1) // 2 * 2
-    out = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda").t()[:d]
+    # column-major d x (n+1) view of a contiguous buffer: the collective
+    # reduces the buffer itself (NCCL needs contiguous tensors)
+    outbuf = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda")
+    out = outbuf.t()[:d]
     cs_plan = plan.device_plan()
 
     def apply():
@@ -278,7 +281,7 @@ def main():
     def step():
         apply()
         if world > 1:
-            dist.reduce(out, dst=0)
+            dist.reduce(outbuf, dst=0)
 
     for _ in range(args.warmup):
         step()
@@ -298,7 +301,7 @@ def main():
             apply()
             k_ev[i][1].record(stream)
             if world > 1:
-                dist.reduce(out, dst=0)
+                dist.reduce(outbuf, dst=0)
         stop.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -396,7 +399,11 @@ def main():
             e2e_call()
             ts.append(time.perf_counter() - t0)
         te = statistics.median(ts)
-        e2e = {"value": round(bytes_local / te / 1e9, 3), "unit": "GB/s",
+        if world > 1:  # whole job: all ranks' bytes over the slowest rank's time
+            t = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": round(bytes_local * world / te / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": bytes_local, "d2h_bytes_per_step": 8 * d * (n + 1),
                "ms_per_step": round(te * 1e3, 3),
                "path": f"{'skl_countsketch_dense_owned_host' if cs_plan.kind == 'owned' else 'skl_countsketch_dense_host'}"

@@ -123,8 +123,16 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local):
 
 
 def reduce_partials(partial, dist, group=None, dst: int = 0):
-    """Sum the per-rank partials onto rank ``dst`` (one NCCL reduce)."""
-    dist.reduce(partial, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    """Sum the per-rank partials onto rank ``dst`` (one NCCL reduce).  The
+    d x (n+1) column-major partial is reduced through its contiguous
+    transpose (collectives need contiguous buffers)."""
+    flat = partial.t()
+    if flat.is_contiguous():
+        dist.reduce(flat, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    else:
+        tmp = flat.contiguous()
+        dist.reduce(tmp, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        flat.copy_(tmp)
     return partial
 
 
