@@ -82,6 +82,14 @@ int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t*
 int skl_gaussian_set_tables(const uint64_t* ki, const double* wi, const double* fi);
 int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G_dev, int64_t ldg,
                             void* stream);
+/* Standard normals of Generator(Philox(key)) starting at 64-bit stream word
+ * `start_word` (numpy's random_standard_normal, one ziggurat draw after
+ * another), written C-order as rows x cols into a device buffer with row
+ * stride ld >= cols; *end_word (may be NULL) receives the word after the last
+ * normal, i.e. where the next standard_normal call continues.  Replaces the
+ * generator calls of probgen.generate_problem (probgen.py:52-68). */
+int skl_rng_normal_device(uint64_t key, uint64_t start_word, int64_t rows, int64_t cols,
+                          double* out, int64_t ld, uint64_t* end_word, void* stream);
 /* Host (sequential, glibc libm) reference generator of the same stream;
  * used to patch the rare ziggurat tail draws and by tests. */
 int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);

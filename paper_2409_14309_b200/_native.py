@@ -118,6 +118,7 @@ SIGNATURES: dict[str, tuple] = {
     "skl_srht_pack_signs": (c_int, [c_ptr, c_i64, c_ptr]),
     "skl_gaussian_set_tables": (c_int, [c_ptr, c_ptr, c_ptr]),
     "skl_rng_gaussian_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_rng_normal_device": (c_int, [c_u64, c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
     "skl_rng_gaussian_host": (c_int, [c_u64, c_i64, c_ptr]),
     "skl_gemm_f64": (
         c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_i64, c_int, c_ptr]),

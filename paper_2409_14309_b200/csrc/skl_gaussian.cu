@@ -135,12 +135,13 @@ __host__ __device__ __forceinline__ uint64_t zig_parse(WordStream& ws, uint64_t 
 }
 
 // A: speculative parse of each segment.
-__global__ void zig_spec_kernel(uint64_t key, int64_t nseg, uint32_t* mask, uint64_t* exitpos) {
+__global__ void zig_spec_kernel(uint64_t key, uint64_t base, int64_t nseg, uint32_t* mask,
+                                uint64_t* exitpos) {
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
   WordStream ws(key);
-  const uint64_t s0 = (uint64_t)k * ZIG_S;
+  const uint64_t s0 = base + (uint64_t)k * ZIG_S;
   uint64_t pos = s0;
   uint32_t* mk = mask + k * ZIG_MASKW;
   int cur = 0;
@@ -171,13 +172,13 @@ __device__ __forceinline__ int zig_count_from(const uint32_t* mk, int off) {
 }
 
 // B: true per-segment counts from the true entries; flags a broken chain.
-__global__ void zig_count_kernel(uint64_t key, int64_t nseg, const uint32_t* mask,
+__global__ void zig_count_kernel(uint64_t key, uint64_t base, int64_t nseg, const uint32_t* mask,
                                  const uint64_t* exitpos, int64_t* count, int* bad) {
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
-  const uint64_t s0 = (uint64_t)k * ZIG_S;
-  const uint64_t entry = k == 0 ? 0 : exitpos[k - 1];
+  const uint64_t s0 = base + (uint64_t)k * ZIG_S;
+  const uint64_t entry = k == 0 ? base : exitpos[k - 1];
   const uint32_t* mk = mask + k * ZIG_MASKW;
   int64_t cnt = 0;
   uint64_t pos = entry;
@@ -227,18 +228,21 @@ __global__ void zig_scan_kernel(const int64_t* count, int64_t nseg, int64_t* off
   }
 }
 
-// C: write the normals of each segment; record strip-0 tail positions.
-__global__ void zig_write_kernel(uint64_t key, int64_t nseg, const uint64_t* exitpos,
-                                 const int64_t* count, const int64_t* offset, int64_t N,
-                                 int64_t m, double* G, int64_t ldg, double sqrt_d,
-                                 int64_t* tail_t, uint64_t* tail_pos, int* tail_n, int tail_cap) {
+// C: write the normals of each segment (normal t at G[(t / m) * ldg + t % m],
+// divided by `div`); record strip-0 tail positions and the word after the
+// last normal.
+__global__ void zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
+                                 const uint64_t* exitpos, const int64_t* count,
+                                 const int64_t* offset, int64_t N, int64_t m, double* G,
+                                 int64_t ldg, double div, int64_t* tail_t, uint64_t* tail_pos,
+                                 int* tail_n, int tail_cap, uint64_t* end_word) {
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
   int64_t t = offset[k];
   const int64_t cnt = count[k];
   if (t >= N || cnt == 0) return;
-  uint64_t pos = k == 0 ? 0 : exitpos[k - 1];
+  uint64_t pos = k == 0 ? base : exitpos[k - 1];
   WordStream ws(key);
   int64_t i = t / m, j = t % m;
   for (int64_t q = 0; q < cnt && t < N; ++q, ++t) {
@@ -246,7 +250,8 @@ __global__ void zig_write_kernel(uint64_t key, int64_t nseg, const uint64_t* exi
     bool tail;
     const uint64_t start = pos;
     pos = zig_parse(ws, pos, &v, &tail);
-    G[i * ldg + j] = v / sqrt_d;
+    G[i * ldg + j] = v / div;
+    if (t == N - 1) *end_word = pos;
     if (tail) {
       const int slot = atomicAdd(tail_n, 1);
       if (slot < tail_cap) {
@@ -310,17 +315,17 @@ extern "C" int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out) {
   return SKL_OK;
 }
 
-extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G, int64_t ldg,
-                                       void* stream) {
-  clear_error();
-  cudaStream_t st = (cudaStream_t)stream;
-  SKL_REQUIRE(d >= 1 && m >= 1 && ldg >= m && G, SKL_ERR_SHAPE, "gaussian: bad arguments");
+// Normals [first normal at word `start`] of Generator(Philox(key)) laid out
+// as `rows` x `cols` C-order (normal t at out[(t / cols) * ld + t % cols]),
+// divided by `div`; *end_word receives the stream word after the last one.
+static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t cols, double* G,
+                          int64_t ldg, double div, uint64_t* end_word, cudaStream_t st) {
   int rc = upload_tables(st);
   if (rc) return rc;
-  const int64_t N = d * m;
+  const int64_t N = rows * cols;
+  const int64_t m = cols;
   // expected words per normal ~1.025; start with 3% slack
   int64_t nseg = (int64_t)((double)N * 1.03 / ZIG_S) + 8;
-  const double sqrt_d = std::sqrt((double)d);
   for (int attempt = 0; attempt < 4; ++attempt) {
     uint32_t* mask = nullptr;
     uint64_t* exitpos = nullptr;
@@ -329,6 +334,7 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
     const int tail_cap = (int)std::min<int64_t>(N / 256 + 4096, 1 << 26);
     int64_t* tail_t = nullptr;
     uint64_t* tail_pos = nullptr;
+    uint64_t* endw = nullptr;
     SKL_CUDA(malloc_async(&mask, (size_t)nseg * ZIG_MASKW * 4, st));
     SKL_CUDA(malloc_async(&exitpos, (size_t)nseg * 8, st));
     SKL_CUDA(malloc_async(&count, (size_t)nseg * 8, st));
@@ -337,11 +343,12 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
     SKL_CUDA(malloc_async(&flags, 8, st));
     SKL_CUDA(malloc_async(&tail_t, (size_t)tail_cap * 8, st));
     SKL_CUDA(malloc_async(&tail_pos, (size_t)tail_cap * 8, st));
+    SKL_CUDA(malloc_async(&endw, 8, st));
     SKL_CUDA(cudaMemsetAsync(flags, 0, 8, st));
     const int tb = 128;
     const int blocks = (int)((nseg + tb - 1) / tb);
-    zig_spec_kernel<<<blocks, tb, 0, st>>>(key, nseg, mask, exitpos);
-    zig_count_kernel<<<blocks, tb, 0, st>>>(key, nseg, mask, exitpos, count, flags);
+    zig_spec_kernel<<<blocks, tb, 0, st>>>(key, start, nseg, mask, exitpos);
+    zig_count_kernel<<<blocks, tb, 0, st>>>(key, start, nseg, mask, exitpos, count, flags);
     zig_scan_kernel<<<1, 1024, 0, st>>>(count, nseg, offset, total);
     int64_t h_total = 0;
     int h_flags[2] = {0, 0};
@@ -351,7 +358,7 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
     auto release = [&]() {
       cudaFreeAsync(mask, st); cudaFreeAsync(exitpos, st); cudaFreeAsync(count, st);
       cudaFreeAsync(offset, st); cudaFreeAsync(total, st); cudaFreeAsync(flags, st);
-      cudaFreeAsync(tail_t, st); cudaFreeAsync(tail_pos, st);
+      cudaFreeAsync(tail_t, st); cudaFreeAsync(tail_pos, st); cudaFreeAsync(endw, st);
     };
     if (h_flags[0]) {
       release();
@@ -362,10 +369,12 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
       nseg = nseg + nseg / 8 + 16;
       continue;
     }
-    zig_write_kernel<<<blocks, tb, 0, st>>>(key, nseg, exitpos, count, offset, N, m, G, ldg,
-                                             sqrt_d, tail_t, tail_pos, flags + 1, tail_cap);
+    zig_write_kernel<<<blocks, tb, 0, st>>>(key, start, nseg, exitpos, count, offset, N, m, G, ldg,
+                                             div, tail_t, tail_pos, flags + 1, tail_cap, endw);
     SKL_CUDA_LAUNCH();
+    uint64_t h_end = 0;
     SKL_CUDA(cudaMemcpyAsync(h_flags, flags, 8, cudaMemcpyDeviceToHost, st));
+    SKL_CUDA(cudaMemcpyAsync(&h_end, endw, 8, cudaMemcpyDeviceToHost, st));
     SKL_CUDA(cudaStreamSynchronize(st));
     const int ntail = h_flags[1];
     if (ntail > tail_cap) {
@@ -385,7 +394,7 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
         bool tl;
         double v;
         zig_parse(ws, hp[(size_t)q], &v, &tl);
-        hv[(size_t)q] = v / sqrt_d;
+        hv[(size_t)q] = v / div;
       }
       double* dv = nullptr;
       SKL_CUDA(malloc_async(&dv, (size_t)ntail * 8, st));
@@ -396,7 +405,23 @@ extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, doubl
       SKL_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
     }
     release();
+    if (end_word) *end_word = h_end;
     return SKL_OK;
   }
   SKL_FAIL(SKL_ERR_CUDA, "gaussian: stream segmentation did not converge");
+}
+
+extern "C" int skl_rng_gaussian_device(uint64_t key, int64_t d, int64_t m, double* G, int64_t ldg,
+                                       void* stream) {
+  clear_error();
+  SKL_REQUIRE(d >= 1 && m >= 1 && ldg >= m && G, SKL_ERR_SHAPE, "gaussian: bad arguments");
+  return normals_device(key, 0, d, m, G, ldg, std::sqrt((double)d), nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int skl_rng_normal_device(uint64_t key, uint64_t start_word, int64_t rows, int64_t cols,
+                                     double* out, int64_t ld, uint64_t* end_word, void* stream) {
+  clear_error();
+  SKL_REQUIRE(rows >= 1 && cols >= 1 && ld >= cols && out, SKL_ERR_SHAPE,
+              "normal_device: bad arguments");
+  return normals_device(key, start_word, rows, cols, out, ld, 1.0, end_word, (cudaStream_t)stream);
 }

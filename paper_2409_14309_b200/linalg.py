@@ -257,3 +257,105 @@ def _check_diagonal(r: np.ndarray) -> None:
     zero = np.flatnonzero(np.diagonal(r) == 0.0)
     if zero.size:
         raise SingularFactorError(f"zero diagonal entry at index {int(zero[0])}")
+
+
+# ---------------------------------------------------------------------------
+# Products, triangular solves and the direct solve (linalg.py:148-246), on
+# the device through the LSQR kernels (csrc/skl_lsqr.cu) and skl_qr_solve.
+# Results live where the operand lives: device tensors for device carriers,
+# host arrays otherwise.
+
+
+def _vec_dev(v: Vector):
+    return v.data if v.on_device else to_device(v.data)
+
+
+def _result(t, on_device: bool) -> Vector:
+    return Vector(t if on_device else t.cpu().numpy())
+
+
+def _operator(A):
+    from .solvers import _operator_device
+
+    return _operator_device(A)[0]
+
+
+def matvec(A, x: Vector) -> Vector:
+    """A @ x (linalg.py:148-154); O(nnz) for sparse A."""
+    from .lsqr import _Workspace
+
+    if x.len != A.cols:
+        raise ShapeError(f"matvec: A is {A.rows}x{A.cols} but x has length {x.len}")
+    require_cuda()
+    op = _operator(A)
+    out = device_f64((A.rows,))
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    op.mv(_vec_dev(x).contiguous(), 1.0, 0.0, None, out, nrm, _Workspace(A.rows, A.cols),
+          current_stream())
+    return _result(out, isinstance(A, DenseMatrix) and A.on_device)
+
+
+def matvec_transpose(A, y: Vector) -> Vector:
+    """A.T @ y (linalg.py:157-163); O(nnz) for sparse A."""
+    from .lsqr import _Workspace
+
+    if y.len != A.rows:
+        raise ShapeError(f"matvec_transpose: A is {A.rows}x{A.cols} but y has length {y.len}")
+    require_cuda()
+    op = _operator(A)
+    z = device_f64((A.cols,))
+    scratch = device_f64((A.rows,))
+    op.rmv(_vec_dev(y).contiguous(), 1.0, scratch, z, _Workspace(A.rows, A.cols),
+           current_stream())
+    return _result(z, isinstance(A, DenseMatrix) and A.on_device)
+
+
+def solve_triangular(R: DenseMatrix, y: Vector, transposed: bool = False) -> Vector:
+    """Solve R z = y (or R^T z = y) for upper-triangular R (linalg.py:195-204)."""
+    if R.rows != R.cols:
+        raise ShapeError(f"triangular factor must be square, got {R.rows}x{R.cols}")
+    if y.len != R.rows:
+        raise ShapeError(f"solve_triangular: R is {R.rows}x{R.cols} but y has length {y.len}")
+    require_cuda()
+    n = R.rows
+    Rt, ldr = _as_device_matrix(R)
+    diag = torch.diagonal(Rt[:n, :n])
+    zero = torch.nonzero(diag == 0.0)
+    if zero.numel():
+        raise SingularFactorError(f"zero diagonal entry at index {int(zero[0, 0])}")
+    yd = _vec_dev(y).contiguous()
+    z = device_f64((n,))
+    if transposed:
+        zeros = torch.zeros(n, dtype=torch.float64, device="cuda")
+        nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _native.call("skl_lsqr_trsv_t", _native.ptr(Rt), ldr, n, _native.ptr(yd), 0.0,
+                     _native.ptr(zeros), _native.ptr(z), _native.ptr(nrm), current_stream())
+    else:
+        _native.call("skl_lsqr_trsv_n", _native.ptr(Rt), ldr, n, 0.0, _native.ptr(yd),
+                     _native.ptr(z), current_stream())
+    return _result(z, R.on_device)
+
+
+def normal_equations_oracle(A: DenseMatrix, b: Vector) -> Vector:
+    """argmin ||A x - b|| by Householder QR of A itself, x = R^-1 Q^T b
+    (linalg.py:221-232), on the device."""
+    if b.len != A.rows:
+        raise ShapeError(f"A is {A.rows}x{A.cols} but b has length {b.len}")
+    if A.rows < A.cols:
+        raise ShapeError(f"need rows >= cols, got {A.rows}x{A.cols}")
+    require_cuda()
+    t, ld = _as_device_matrix(A)
+    x, _, _ = qr_solve_device(t, ld, _vec_dev(b).contiguous(), A.rows, A.cols)
+    return _result(x, A.on_device)
+
+
+def spectral_condition_number(M: DenseMatrix) -> float:
+    """sigma_max / sigma_min from all singular values (linalg.py:235-247;
+    cuSOLVER through torch); inf when sigma_min is zero."""
+    if M.rows < M.cols:
+        raise ShapeError(f"need rows >= cols, got {M.rows}x{M.cols}")
+    require_cuda()
+    t, _ = _as_device_matrix(M)
+    s = torch.linalg.svdvals(t[:M.rows, :M.cols])
+    smin = float(s[-1])
+    return float("inf") if smin == 0.0 else float(s[0]) / smin

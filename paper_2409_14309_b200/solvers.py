@@ -37,7 +37,7 @@ from .sketch import (
 )
 
 METHODS = ("lsqr", "saa", "sap", "direct")
-ENGINE_METHODS = ("saa", "sap", "lsqr")
+ENGINE_METHODS = ("saa", "sap", "lsqr", "direct")
 
 
 @dataclass(frozen=True)
@@ -246,25 +246,55 @@ def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | Non
     return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "sap", op_spec.kind, d, t0)
 
 
-def solve(problem: LeastSquaresProblem, method: str = "saa", spec: SketchSpec | None = None,
+def direct(problem: LeastSquaresProblem) -> SolveResult:
+    """The ``direct`` method: Householder QR of A itself on the device and
+    x = R^-1 Q^T b (solvers.py:381-396 via linalg.py:221-232
+    ``normal_equations_oracle``); sparse A is densified on the device first."""
+    A, b = problem.A, problem.b
+    if b.len != A.rows:
+        raise ShapeError(f"A is {A.rows}x{A.cols} but b has length {b.len}")
+    if A.rows < A.cols:
+        raise ShapeError(f"need rows >= cols, got {A.rows}x{A.cols}")
+    require_cuda()
+    t0 = time.perf_counter()
+    b_dev = b.data if b.on_device else to_device(b.data)
+    if isinstance(A, SparseMatrix):
+        indptr, indices, values = A.device_arrays()
+        rows = torch.repeat_interleave(
+            torch.arange(A.rows, device="cuda"), indptr[1:] - indptr[:-1])
+        dense = torch.zeros((A.cols, A.rows), dtype=torch.float64, device="cuda")
+        dense[indices, rows] = values  # column-major m x n: row j of dense is column j
+        A_dev, lda = dense.t(), A.rows
+    else:
+        A_dev = A.data if A.on_device else to_device(A.data)
+        lda = A.ld if A.on_device else A.rows
+    x_dev, _, _ = qr_solve_device(A_dev, lda, b_dev, A.rows, A.cols)
+    wall = time.perf_counter() - t0
+    if isinstance(A, SparseMatrix):
+        rnorm = _residual_device(A, None, 0, b_dev, x_dev)
+    else:
+        rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
+    x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
+    return SolveResult(x=Vector(x), method="direct", sketch=None, d=None, iterations=0,
+                       residual_norm=rnorm, termination="direct", wall_time_s=wall)
+
+
+def solve(problem: LeastSquaresProblem, method: str = "lsqr", spec: SketchSpec | None = None,
           opts: SolverOptions | None = None) -> SolveResult:
     """Dispatch (solvers.py:364-398); wall_time_s covers the full path.
 
-    Note: the reference defaults to ``method="lsqr"``; this engine's hot path
-    is sketch-and-apply, so ``"saa"`` is the default here.  "sap" and "lsqr"
-    run on the device for dense and CSR operands; "direct" raises
-    ``SpecError``."""
+    Same default as the reference (``method="lsqr"``).  Every method runs on
+    the device, for dense and CSR operands."""
     if method not in METHODS:
         raise SpecError(f"unknown method {method!r}, expected one of {METHODS}")
-    if method not in ENGINE_METHODS:
-        raise SpecError(f"method {method!r} is outside the B200 engine's scope "
-                        f"(implemented: {ENGINE_METHODS})")
     t0 = time.perf_counter()
     if method == "saa":
         result = sketch_and_apply(problem, spec, opts)
     elif method == "sap":
         result = sketch_and_precondition(problem, spec, opts)
-    else:
+    elif method == "lsqr":
         result = lsqr(problem.A, problem.b, opts)
+    else:
+        result = direct(problem)
     wall = time.perf_counter() - t0
     return replace(result, wall_time_s=wall)

@@ -208,6 +208,48 @@ def main() -> None:
     except ref.SingularFactorError as exc:
         meta["rankdef_msg"] = str(exc)
 
+    # --- device problem generator (probgen.py:43-80), SURVEY.md §8f f3
+    pg_cases = {"pg_tall": (300, 12, 1e6, 1e-4, 3), "pg_square": (40, 40, 1e3, 0.0, 1),
+                "pg_col": (50, 1, 1e10, 1e-10, 7), "pg_default": (513, 33, 1e10, 1e-10, 0)}
+    for name, (m, n, kappa, beta, seed) in pg_cases.items():
+        prob = ref.generate_problem(ref.ProblemSpec(m=m, n=n, kappa=kappa, beta=beta, seed=seed))
+        g[f"{name}_A"] = prob.A.data
+        g[f"{name}_b"] = prob.b.data
+        g[f"{name}_xstar"] = prob.x_star.data
+        meta[f"{name}_spec"] = [m, n, kappa, beta, seed]
+    # the "direct" method (solvers.py:381-396) on the plain-LSQR problem
+    c = W.config(1, m=3000, n=40)
+    A, b, _ = W.make_problem(c)
+    res = ref.solve(ref.LeastSquaresProblem(A=ref.DenseMatrix(A), b=ref.Vector(b)), "direct")
+    g["direct_small_x"] = res.x.data
+    meta["direct_small_residual"] = res.residual_norm
+
+    # --- Matrix Market / CLI files written by the reference (mmio.py, probgen.py:83-98,
+    # bench.py:186-245), compared byte for byte by tests/test_io_cpu.py
+    io = OUT.parent / "io"
+    io.mkdir(exist_ok=True)
+    dense = np.array([[0.1, -2.5e-7], [1e16, 5e-324], [-0.0, 123456789.0], [1.0 / 3.0, -7.0]])
+    ref.write_matrix(str(io / "dense.mtx"), ref.DenseMatrix(dense))
+    sp = scipy.sparse.csr_matrix(np.array([[0.0, 1.5, 0.0], [0.0, 0.0, 0.0], [-2.0, 0.0, 1e-300],
+                                           [0.0, 3.25, 0.0]]))
+    ref.write_matrix(str(io / "sparse.mtx"), ref.SparseMatrix.from_scipy(sp))
+    ref.write_vector(str(io / "vector.mtx"), ref.Vector(np.array([2.0, -0.5, 1e-9])))
+    (io / "dups.mtx").write_text("%%MatrixMarket matrix coordinate integer general\n"
+                                 "% comment line\n3 2 5\n3 1 4\n1 2 1\n3 1 -1\n2 2 7\n1 2 2\n")
+    dup = ref.read_matrix(str(io / "dups.mtx"))
+    g["io_dups_indptr"], g["io_dups_indices"], g["io_dups_values"] = (
+        dup.indptr, dup.indices, dup.values)
+    spec = ref.ProblemSpec(m=30, n=4, kappa=1e4, beta=1e-6, seed=11)
+    ref.write_problem_dir(spec, ref.generate_problem(spec), str(io / "problem"))
+    recs = [ref.BenchRecord("saa", "countsketch", 1000, 20, 80, 1e10, 1e-10, 0, 0.125,
+                            3.0e-7, 0.0, 0, "direct"),
+            ref.BenchRecord("lsqr", None, 1000, 20, None, 1e10, 1e-10, 1, 2.5, -1.0, -1.0, 0,
+                            "failed")]
+    ref.write_csv(recs, str(io / "results.csv"))
+    ref.write_meta(ref.BenchConfig(m_list=(1000, 2000), n=20, methods=("lsqr", "saa"),
+                                   sketches=("countsketch", "srht"), repeats=2, seed=4),
+                   str(io / "bench_meta.txt"))
+
     g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB)")
