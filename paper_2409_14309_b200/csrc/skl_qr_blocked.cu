@@ -266,14 +266,44 @@ __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelPara
 // argument at the buffers).
 constexpr int QR_NT2 = 512;
 constexpr int QR_NW2 = QR_NT2 / 32;
+#ifndef QR_PUSHW
+#define QR_PUSHW 2  // warps that push the column sums to the cluster
+#endif
 // extra shared memory of the register panel (doubles): inbox[2][16][32],
-// inrow[2][32], red[16][32], G[32][32], Ts[32][32], colscale[32],
+// inrow[2][32], red[16][33], G[32][32], Ts[32][32], colscale[32],
 // sc[2][128], mbarriers
-constexpr int QR2_SMEM_EXTRA = 2 * QB_MAXCL * 32 + 64 + 512 + 1024 + 1024 + 32 + 256 + 8;
+constexpr int QR2_SMEM_EXTRA = 2 * QB_MAXCL * 32 + 64 + 16 * 33 + 1024 + 1024 + 32 + 256 + 8;
 
 // staging doubles, even so the buffers after it stay 16-byte aligned
 __host__ __device__ inline size_t qr2_staging(int rows_per) {
   return ((size_t)(rows_per > 32 ? rows_per : 32) * QB_PLD + 1) & ~(size_t)1;
+}
+
+// The block-reflector factor T of a panel (dlarft, forward columnwise):
+// T[k][k] = tau_k (already in Ts), T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k]
+// with G[l][k] = V_l^T v_k stored at G[k * 32 + l].  One warp, lane = row
+// i of T.  Instead of one dot product per column (a dependent chain of
+// loads and FMAs), each finished T[i][k] is immediately folded into the
+// running sums of every later column, acc[k'] += T[i][k] G[k][k'], so a
+// column step is one multiply on the critical path plus independent FMAs.
+// Runs after the panel's rows are written back, when their registers are
+// free.
+__device__ __forceinline__ void panel_t_build(double* Ts, const double* G, int jb, int lane) {
+  double acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k < jb) {
+      const double tk = Ts[k * 32 + k];
+      const double t = lane < k ? -tk * acc[k] : (lane == k ? tk : 0.0);
+#pragma unroll
+      for (int kk = k + 1; kk < 32; ++kk) acc[kk] = fma(t, G[kk * 32 + k], acc[kk]);
+      __syncwarp();
+      Ts[k * 32 + lane] = t;
+    }
+  }
+  __syncwarp();
 }
 
 template <int RPW>
@@ -292,8 +322,8 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   double* S = qsm;                                         // staging [max(rows_per, 32)][QB_PLD]
   double* inbox = S + qr2_staging(p.rows_per);             // [2][16][32]
   double* inrow = inbox + 2 * QB_MAXCL * 32;               // [2][32]
-  double* red = inrow + 64;                                // [16][32]
-  double* G = red + 512;                                   // [32][32]: column k = V^T v_k
+  double* red = inrow + 64;                                // [16][33]
+  double* G = red + 16 * 33;                               // [32][32]: column k = V^T v_k
   double* Ts = G + 1024;                                   // [32][32]
   double* colscale = Ts + 1024;                            // [32]
   double* sc = colscale + 32;                              // [2][128]: w_j scale, w_j, beta
@@ -360,42 +390,43 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
       if (warp + 16 > k) s1 = fma(xh1, H1, s1);
     }
     QR_PROBE(1);
-    red[warp * 32 + lane] = s0 + s1;
+    red[warp * 33 + lane] = s0 + s1;
     __syncthreads();
     QR_PROBE(2);
-    if (warp == 0) {
-      // Buffers of parity b are rewritten only at column k + 2: by then this
-      // CTA has received every CTA's column-(k+1) push, each sent after that
-      // CTA finished column k, i.e. after our column-k copies into it landed
-      // and after it read its column-k inbox.
+    // Buffers of parity b are rewritten only at column k + 2: by then this
+    // CTA has received every CTA's column-(k+1) push, each sent after that
+    // CTA's column-(k+1) __syncthreads, i.e. after it read its column-k
+    // inbox, and after our column-k copies into it landed.
+    // Warps 0 .. QR_PUSHW-1 each fold the 16 warp partials (fixed order, so
+    // bitwise the same sums everywhere) and push them, one coalesced
+    // 256-byte store per destination, into the inboxes of CTAs
+    // w, w + QR_PUSHW, ...
+    if (warp < QR_PUSHW) {
       double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
 #pragma unroll
       for (int w = 0; w < QR_NW2; w += 4) {
-        t0 += red[w * 32 + lane];
-        t1 += red[(w + 1) * 32 + lane];
-        t2 += red[(w + 2) * 32 + lane];
-        t3 += red[(w + 3) * 32 + lane];
+        t0 += red[w * 33 + lane];
+        t1 += red[(w + 1) * 33 + lane];
+        t2 += red[(w + 2) * 33 + lane];
+        t3 += red[(w + 3) * 33 + lane];
       }
       const double tot = (t0 + t1) + (t2 + t3);
-      if (lane == 0) mbar_arrive_expect_tx(&mb[b], (ncta + 1) * 256);
-      // push the column sums: lane j stores s_j into every CTA's inbox
+      if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&mb[b], (ncta + 1) * 256);
       const uint32_t dst = smem_u32(inbox + (b * QB_MAXCL + rank) * 32 + lane);
       const uint32_t mbl = smem_u32(&mb[b]);
-      for (uint32_t q = 0; q < ncta; ++q) st_async_f64(mapa_u32(dst, q), tot, mapa_u32(mbl, q));
+      for (uint32_t q = warp; q < ncta; q += QR_PUSHW)
+        st_async_f64(mapa_u32(dst, q), tot, mapa_u32(mbl, q));
+    }
+    if (warp == 0) {
       QR_PROBE(3);
       mbar_wait_cluster(&mb[b], (uint32_t)((k >> 1) & 1));
       QR_PROBE(4);
-      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+      double u[4] = {0.0, 0.0, 0.0, 0.0};
       const double* ib = inbox + b * QB_MAXCL * 32 + lane;
-      uint32_t q = 0;
-      for (; q + 3 < ncta; q += 4) {
-        u0 += ib[q * 32];
-        u1 += ib[(q + 1) * 32];
-        u2 += ib[(q + 2) * 32];
-        u3 += ib[(q + 3) * 32];
-      }
-      for (; q < ncta; ++q) u0 += ib[q * 32];
-      const double Sj = (u0 + u1) + (u2 + u3);
+#pragma unroll
+      for (int q = 0; q < QB_MAXCL; ++q)  // all loads in flight at once
+        if (q < (int)ncta) u[q & 3] += ib[q * 32];
+      const double Sj = (u[0] + u[1]) + (u[2] + u[3]);
       const double pj = inrow[b * 32 + lane];
       const double Sk = __shfl_sync(0xffffffffu, Sj, k);
       const double alpha = __shfl_sync(0xffffffffu, pj, k);
@@ -487,31 +518,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
       p.M[gj * p.ldm + gi] = val;
       p.V[gj * p.ldm + gi] = i < j ? 0.0 : (i == j ? 1.0 : val);
     }
-    // T (dlarft, forward columnwise): T[k][k] = tau_k,
-    // T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k].  One warp; lane j keeps row
-    // j of T in registers, G[., k] is read by broadcast.
-    if (warp == 0) {
-      double Trow[32];
-#pragma unroll
-      for (int l = 0; l < 32; ++l) Trow[l] = 0.0;
-      for (int k = 0; k < jb; ++k) {
-        const double tk = Ts[k * 32 + k];
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-        for (int l = 0; l < 32; l += 4) {
-          a0 = fma(Trow[l], G[k * 32 + l], a0);      // G[l][k] = 0 for l >= k
-          a1 = fma(Trow[l + 1], G[k * 32 + l + 1], a1);
-          a2 = fma(Trow[l + 2], G[k * 32 + l + 2], a2);
-          a3 = fma(Trow[l + 3], G[k * 32 + l + 3], a3);
-        }
-        const double t = lane < k ? -tk * ((a0 + a1) + (a2 + a3)) : (lane == k ? tk : 0.0);
-#pragma unroll
-        for (int l = 0; l < 32; ++l)
-          if (l == k) Trow[l] = t;
-      }
-#pragma unroll
-      for (int l = 0; l < 32; ++l) Ts[l * 32 + lane] = Trow[l];
-    }
+    if (warp == 0) panel_t_build(Ts, G, jb, lane);
     QR_PROBE(11);
     __syncthreads();
     #pragma unroll 8
