@@ -360,7 +360,7 @@ __global__ void q_signfix_copy_kernel(const double* Qw, int64_t ldw, const doubl
 bool qr_blocked_supported(int64_t d);
 int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau, double* beta,
                       double* V, double* Tall, double* W, double* W2, double* part,
-                      int64_t part_cap, cudaStream_t st);
+                      int64_t part_cap, double* W2b, double* partb, cudaStream_t st);
 int qr_blocked_form_q(double* Q, int64_t ldq, int64_t d, int64_t n, const double* V, int64_t ldv,
                       const double* Tall, double* W, double* W2, double* part, int64_t part_cap,
                       cudaStream_t st);
@@ -402,9 +402,11 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
                oT = blocked ? take((size_t)npan * 32 * 32 * 8) : 0,
                oW = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oW2 = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
+               oW2b = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oQ = (blocked && Q) ? take((size_t)ldm * n * 8) : 0;
   const int64_t part_cap = blocked ? 32 * (n + 1) * ((d + 63) / 64) : 0;  // 64-row splits
   const size_t oP = blocked ? take((size_t)part_cap * 8) : 0;
+  const size_t oPb = blocked ? take((size_t)part_cap * 8) : 0;  // second stream's scratch
   unsigned char* ws = nullptr;
   SKL_CUDA(malloc_async(&ws, off, st));
   double* M = (double*)(ws + oM);
@@ -432,7 +434,8 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
       double* W = (double*)(ws + oW);
       double* W2 = (double*)(ws + oW2);
       double* Pw = (double*)(ws + oP);
-      rc = qr_blocked_factor(M, ldm, d, n, tau, beta, V, T, W, W2, Pw, part_cap, st);
+      rc = qr_blocked_factor(M, ldm, d, n, tau, beta, V, T, W, W2, Pw, part_cap,
+                             (double*)(ws + oW2b), (double*)(ws + oPb), st);
       if (rc) break;
       qr_finish_kernel<<<1, 256, 0, st>>>(M, ldm, n, beta, fro2, R, ldr, y, badc, badv);
       qr_backsolve_blocked_kernel<<<1, 512, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);

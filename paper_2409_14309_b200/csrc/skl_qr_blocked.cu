@@ -21,6 +21,8 @@
 // work becomes GEMM-shaped.
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -696,12 +698,38 @@ bool qr_blocked_supported(int64_t d) {
   return panel_cluster(d, &rp) > 0;
 }
 
-// Blocked factorisation of M (d x (n+1), ld ldm); fills tau, beta, V
-// (explicit reflectors, ld ldm), T (per panel 32 x 32 blocks, n/32+1 of
-// them).  The last column of M (Sb) is transformed into Q^T Sb.
-int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau, double* beta,
-                      double* V, double* Tall, double* W, double* W2, double* part,
-                      int64_t part_cap, cudaStream_t st) {
+// Per-thread, per-device helper streams of the look-ahead factorisation: a
+// high-priority stream for the critical path (panels) and a low-priority one
+// for the bulk trailing updates, plus a pool of events.  Thread-local, so
+// concurrent callers never share them (the C-ABI is reentrant).
+struct QrStreams {
+  cudaStream_t hi = nullptr, lo = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+
+static int qr_streams(QrStreams** out, size_t nev) {
+  static thread_local QrStreams per_dev[16];
+  int dev = 0;
+  SKL_CUDA(cudaGetDevice(&dev));
+  SKL_REQUIRE(dev >= 0 && dev < 16, SKL_ERR_CUDA, "qr: device index %d out of range", dev);
+  QrStreams& q = per_dev[dev];
+  if (!q.hi) {
+    int least = 0, greatest = 0;
+    SKL_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SKL_CUDA(cudaStreamCreateWithPriority(&q.hi, cudaStreamNonBlocking, greatest));
+    SKL_CUDA(cudaStreamCreateWithPriority(&q.lo, cudaStreamNonBlocking, least));
+  }
+  while (q.ev.size() < nev) {
+    cudaEvent_t e;
+    SKL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    q.ev.push_back(e);
+  }
+  *out = &q;
+  return SKL_OK;
+}
+
+static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb, double* V,
+                           double* Tblk, double* tau, double* beta, cudaStream_t st) {
   static bool attr_set = false;
   const int smem_max = (int)(QB_SMEM_EXTRA + QB_MAXROWS * QB_PLD) * (int)sizeof(double);
   if (!attr_set) {
@@ -716,58 +744,117 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
     attr_set = true;
   }
   static const bool smem_panel = getenv("SKL_QR_SMEM_PANEL") != nullptr;
-  for (int64_t j0 = 0; j0 < n; j0 += QB_NB) {
-    const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
-    const int64_t tail = d - j0 - jb;
-    // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
-    static const int tail_rows = getenv("SKL_QR_PANEL_ROWS") ? atoi(getenv("SKL_QR_PANEL_ROWS")) : 128;
-    int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + tail_rows - 1) / tail_rows));
-    const int rows2 = (int)((tail + cl2 - 1) / cl2);
-    const int rpw = (rows2 + QR_NW2 - 1) / QR_NW2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (!smem_panel && rpw <= 32) {
-      PanelParams pp{M, ldm, d, j0, jb, rows2, V, Tall + (j0 / QB_NB) * 32 * 32, tau, beta};
-      cfg.gridDim = dim3(cl2);
-      cfg.blockDim = dim3(QR_NT2);
-      cfg.dynamicSmemBytes = (qr2_staging(rows2) + QR2_SMEM_EXTRA) * sizeof(double);
-      attr[0].val.clusterDim.x = cl2;
-      if (rpw <= 8)
-        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<8>, pp));
-      else if (rpw <= 16)
-        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<16>, pp));
-      else
-        SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<32>, pp));
-    } else {
-      int rows_per = 0;
-      const int cl = panel_cluster(d - j0, &rows_per);
-      SKL_REQUIRE(cl > 0, SKL_ERR_INVALID, "qr panel does not fit the cluster");
-      PanelParams pp{M, ldm, d, j0, jb, rows_per, V, Tall + (j0 / QB_NB) * 32 * 32, tau, beta};
-      cfg.gridDim = dim3(cl);
-      cfg.blockDim = dim3(QB_NT);
-      cfg.dynamicSmemBytes = (size_t)(rows_per * QB_PLD + QB_SMEM_EXTRA) * sizeof(double);
-      attr[0].val.clusterDim.x = cl;
-      SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, pp));
-    }
-    const int64_t c0 = j0 + jb;
-    const int64_t nc = (n + 1) - c0;  // trailing columns incl. Sb
-    if (nc <= 0) continue;
-    const int64_t rows = d - j0;
-    int rc = qr_wt(V + j0 * ldm + j0, ldm, M + c0 * ldm + j0, ldm, jb, rows, nc,
-                   Tall + (j0 / QB_NB) * 32 * 32, 1, W2, part, part_cap, st);
-    if (rc) return rc;
-    SKL_CUDA_LAUNCH();
-    dim3 g((unsigned)((rows + 63) / 64), (unsigned)((nc + 63) / 64));
-    qr_update_kernel<<<g, 256, 0, st>>>(M + c0 * ldm + j0, ldm, V + j0 * ldm + j0, ldm, W2, jb,
-                                        rows, nc);
-    SKL_CUDA_LAUNCH();
+  // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
+  static const int tail_rows = getenv("SKL_QR_PANEL_ROWS") ? atoi(getenv("SKL_QR_PANEL_ROWS")) : 128;
+  const int64_t tail = d - j0 - jb;
+  int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + tail_rows - 1) / tail_rows));
+  const int rows2 = (int)((tail + cl2 - 1) / cl2);
+  const int rpw = (rows2 + QR_NW2 - 1) / QR_NW2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!smem_panel && rpw <= 32) {
+    PanelParams pp{M, ldm, d, j0, jb, rows2, V, Tblk, tau, beta};
+    cfg.gridDim = dim3(cl2);
+    cfg.blockDim = dim3(QR_NT2);
+    cfg.dynamicSmemBytes = (qr2_staging(rows2) + QR2_SMEM_EXTRA) * sizeof(double);
+    attr[0].val.clusterDim.x = cl2;
+    if (rpw <= 8)
+      SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<8>, pp));
+    else if (rpw <= 16)
+      SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<16>, pp));
+    else
+      SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<32>, pp));
+  } else {
+    int rows_per = 0;
+    const int cl = panel_cluster(d - j0, &rows_per);
+    SKL_REQUIRE(cl > 0, SKL_ERR_INVALID, "qr panel does not fit the cluster");
+    PanelParams pp{M, ldm, d, j0, jb, rows_per, V, Tblk, tau, beta};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(QB_NT);
+    cfg.dynamicSmemBytes = (size_t)(rows_per * QB_PLD + QB_SMEM_EXTRA) * sizeof(double);
+    attr[0].val.clusterDim.x = cl;
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, pp));
   }
+  return SKL_OK;
+}
+
+// C (rows x nc, ld ldm) <- (I - V T V^T)^T C for the block reflector of the
+// panel at column j0 (rows j0 .. d-1).
+static int qr_apply_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb, int64_t c0,
+                          int64_t nc, const double* V, const double* Tblk, double* W2,
+                          double* part, int64_t part_cap, cudaStream_t st) {
+  if (nc <= 0) return SKL_OK;
+  const int64_t rows = d - j0;
+  int rc = qr_wt(V + j0 * ldm + j0, ldm, M + c0 * ldm + j0, ldm, jb, rows, nc, Tblk, 1, W2, part,
+                 part_cap, st);
+  if (rc) return rc;
+  dim3 g((unsigned)((rows + 63) / 64), (unsigned)((nc + 63) / 64));
+  qr_update_kernel<<<g, 256, 0, st>>>(M + c0 * ldm + j0, ldm, V + j0 * ldm + j0, ldm, W2, jb, rows,
+                                      nc);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+// Blocked factorisation of M (d x (n+1), ld ldm); fills tau, beta, V
+// (explicit reflectors, ld ldm), T (per panel 32 x 32 blocks, n/32+1 of
+// them).  The last column of M (Sb) is transformed into Q^T Sb.
+//
+// Look-ahead: panel k + 1 only needs its own 32 columns updated by panel k's
+// reflectors, so the critical path is panel, small update of the next
+// panel's columns, panel, ... on a high-priority stream, while the bulk
+// trailing update of panel k (every column after panel k + 1, including Sb)
+// runs concurrently on a low-priority stream.  Event k orders: panel k done
+// -> bulk update k; bulk update k - 2 done -> small update before panel k.
+// Each stream has its own W2 / partial scratch.
+int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau, double* beta,
+                      double* V, double* Tall, double* W, double* W2, double* part,
+                      int64_t part_cap, double* W2b, double* partb, cudaStream_t st) {
+  (void)W;
+  const int64_t npan = (n + QB_NB - 1) / QB_NB;
+  QrStreams* qs = nullptr;
+  int rc = qr_streams(&qs, (size_t)(2 * npan + 3));
+  if (rc) return rc;
+  cudaEvent_t* E = qs->ev.data();            // [0, npan): panel k done
+  cudaEvent_t* F = qs->ev.data() + npan;     // [npan, 2 npan): bulk update k done
+  cudaEvent_t* X = qs->ev.data() + 2 * npan; // fork / join
+  SKL_CUDA(cudaEventRecord(X[0], st));
+  SKL_CUDA(cudaStreamWaitEvent(qs->hi, X[0], 0));
+  SKL_CUDA(cudaStreamWaitEvent(qs->lo, X[0], 0));
+  for (int64_t k = 0; k < npan; ++k) {
+    const int64_t j0 = k * QB_NB;
+    const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
+    if (k > 0) {
+      // panel k's columns: reflectors 0 .. k-2 came with bulk update k-2,
+      // reflector k-1 is applied here
+      if (k >= 2) SKL_CUDA(cudaStreamWaitEvent(qs->hi, F[k - 2], 0));
+      const int64_t p0 = j0 - QB_NB;
+      rc = qr_apply_panel(M, ldm, d, p0, QB_NB, j0, jb, V, Tall + (k - 1) * 32 * 32, W2, part,
+                          part_cap, qs->hi);
+      if (rc) return rc;
+    }
+    rc = qr_launch_panel(M, ldm, d, j0, jb, V, Tall + k * 32 * 32, tau, beta, qs->hi);
+    if (rc) return rc;
+    SKL_CUDA(cudaEventRecord(E[k], qs->hi));
+    // bulk update: every column after panel k + 1 (and Sb)
+    const int64_t c0 = j0 + jb;
+    const int64_t jb_next = std::min<int64_t>(QB_NB, std::max<int64_t>(0, n - c0));
+    const int64_t cs = c0 + jb_next;
+    SKL_CUDA(cudaStreamWaitEvent(qs->lo, E[k], 0));
+    rc = qr_apply_panel(M, ldm, d, j0, jb, cs, (n + 1) - cs, V, Tall + k * 32 * 32, W2b, partb,
+                        part_cap, qs->lo);
+    if (rc) return rc;
+    SKL_CUDA(cudaEventRecord(F[k], qs->lo));
+  }
+  SKL_CUDA(cudaEventRecord(X[1], qs->hi));
+  SKL_CUDA(cudaEventRecord(X[2], qs->lo));
+  SKL_CUDA(cudaStreamWaitEvent(st, X[1], 0));
+  SKL_CUDA(cudaStreamWaitEvent(st, X[2], 0));
 #ifdef SKL_QR_PROBE
   {
     unsigned long long h[12] = {}, z[12] = {};
