@@ -8,10 +8,11 @@
 // Design (B200): a CTA owns 8 buckets x Cw output columns held as a dense
 // tile in shared memory (bucket-major, odd row stride); one warp per bucket
 // walks the bucket's source rows (the operator's bucket-sorted row list, i.e.
-// the CSR of S) 32 rows at a time, fetching the next 32 rows' CSR extents
-// while committing the current ones.  The warp flattens those rows'
-// nonzeros in (row, position) order, lanes gather one nonzero each, and
-// commit into the tile in flattened order: lanes hitting the same column are
+// the CSR of S) 32 rows at a time.  The warp flattens those rows'
+// nonzeros in (row, position) order and lanes gather them, one round ahead
+// of the commit (software pipeline: bucket rows 3 rounds, CSR extents 2
+// rounds and nonzeros 1 round ahead), then commit into the tile in
+// flattened order: lanes hitting the same column are
 // serialised by lane rank (__match_any_sync), distinct columns commit
 // together.  The tile is then written once; the output needs no memset and
 // no atomics.
@@ -25,6 +26,82 @@
 namespace skl {
 
 constexpr int CSR_B = 8;   // buckets (warps) per CTA
+
+// One round = 32 consecutive source rows of a bucket (lane l: row base + l).
+struct CsrRound {
+  int64_t p0;     // first nonzero of my row
+  int64_t start;  // exclusive scan of the rows' nonzero counts (flattened index)
+  int64_t total;  // nonzeros of the round
+  double s;       // my row's sign (x scale)
+};
+
+// A prefetched nonzero of a round's flattened order: column, value, row sign.
+struct CsrSlot {
+  int64_t c;
+  double v, s;
+  bool ok;
+};
+
+__device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t sg, double scale) {
+  CsrRound r;
+  const int lane = threadIdx.x & 31;
+  const int64_t cnt = np1 - np0;
+  int64_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  r.p0 = np0;
+  r.start = incl - cnt;
+  r.total = __shfl_sync(0xffffffffu, incl, 31);
+  r.s = (double)sg * scale;  // +-1 (CountSketch) or +-fl(1/sqrt(s)) (sparse sign)
+  return r;
+}
+
+// Issue the loads of flattened nonzero f of round r (owner lane = the
+// largest l with start_l <= f; among equal starts, i.e. empty rows, the
+// largest index).  The values are consumed a round later.
+__device__ __forceinline__ CsrSlot csr_fetch(const CsrRound& r, int64_t f,
+                                             const int64_t* __restrict__ indices,
+                                             const double* __restrict__ values) {
+  int lo = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int64_t st = __shfl_sync(0xffffffffu, r.start, min(lo + step, 31));
+    if (lo + step <= 31 && st <= f) lo += step;
+  }
+  const int64_t st_o = __shfl_sync(0xffffffffu, r.start, lo);
+  const int64_t p0_o = __shfl_sync(0xffffffffu, r.p0, lo);
+  CsrSlot sl;
+  sl.s = __shfl_sync(0xffffffffu, r.s, lo);
+  sl.ok = f < r.total;
+  sl.c = -1;
+  sl.v = 0.0;
+  if (sl.ok) {
+    const int64_t p = p0_o + (f - st_o);
+    sl.c = indices[p];
+    sl.v = values[p];
+  }
+  return sl;
+}
+
+// Add the slot into the bucket's tile row: lanes hitting the same column
+// commit in lane (= flattened, = ascending source row) order.
+__device__ __forceinline__ void csr_commit(const CsrSlot& sl, double* my, int64_t c0, int64_t cw) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = sl.ok && sl.c >= c0 && sl.c < c0 + cw;
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!act) return;
+  const unsigned peers = __match_any_sync(0xffffffffu, valid ? sl.c : -1);
+  const unsigned grp = peers & act;
+  const int rank = __popc(grp & ((1u << lane) - 1));
+  const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
+  for (int q = 0; q < rounds; ++q) {
+    if (valid && rank == q) my[sl.c - c0] += sl.s * sl.v;
+    __syncwarp();
+  }
+}
 
 __global__ void __launch_bounds__(CSR_B * 32)
     countsketch_csr_kernel(const int64_t* __restrict__ indptr, const int64_t* __restrict__ indices,
@@ -45,88 +122,58 @@ __global__ void __launch_bounds__(CSR_B * 32)
   if (i < d) {
     const int64_t r_beg = bptr[i], r_end = bptr[i + 1];
     double* my = tile + warp * ldt;  // column c at my[c - c0]
-    // Software pipeline over rounds of 32 rows: the bucket-row index of
-    // round r+2 (coalesced) and the CSR extent of round r+1 (dependent on
-    // it) are in flight while round r commits; the signs come pre-gathered
-    // in bucket order, so they stream.
-    // raw loads of the next round; converted only when the round starts, so
-    // nothing waits on them early
+    // Software pipeline over rounds of 32 rows, one round of latency for
+    // every dependent load: while round r commits, the nonzeros of round
+    // r+1 (two flattened passes, 64 entries), the CSR extents of round r+2
+    // and the bucket-row indices of round r+3 are in flight.
+    auto brow_at = [&](int64_t base) -> int32_t {
+      const int64_t r = base + lane;
+      return r < r_end ? brow[r] : -1;
+    };
     int64_t np0 = 0, np1 = 0;
     int8_t nsg = 0;
-    int32_t nj = -1;  // bucket row of round r+2 for this lane
-    {
-      const int64_t r = r_beg + lane;
-      if (r < r_end) {
-        const int32_t j = brow[r];
-        np0 = indptr[j];
-        np1 = indptr[j + 1];
-        nsg = bsign[r];
-      }
-      const int64_t r2 = r_beg + 32 + lane;
-      if (r2 < r_end) nj = brow[r2];
-    }
-    for (int64_t base = r_beg; base < r_end; base += 32) {
-      const int64_t p0 = np0, cnt = np1 - np0;
-      const double s = (double)nsg * scale;  // +-1 (CountSketch) or +-fl(1/sqrt(s))
+    auto extent = [&](int32_t j, int64_t base) {
       np0 = 0;
       np1 = 0;
       nsg = 0;
-      if (nj >= 0) {
-        np0 = indptr[nj];
-        np1 = indptr[nj + 1];
-        nsg = bsign[base + 32 + lane];
+      if (j >= 0) {
+        np0 = indptr[j];
+        np1 = indptr[j + 1];
+        nsg = bsign[base + lane];
       }
-      nj = -1;
-      if (base + 64 + lane < r_end) nj = brow[base + 64 + lane];
-      // exclusive scan of counts over the warp (lane order == ascending j)
-      int64_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int64_t start = incl - cnt;
-      const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
-      for (int64_t f0 = 0; f0 < total; f0 += 32) {
-        const int64_t f = f0 + lane;
-        // owner lane: largest l with start_l <= f (starts are nondecreasing)
-        int lo = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int64_t st = __shfl_sync(0xffffffffu, start, min(lo + step, 31));
-          if (lo + step <= 31 && st <= f) lo += step;
-        }
-        // among equal starts (empty rows) the largest index is the owner
-        const int64_t st_o = __shfl_sync(0xffffffffu, start, lo);
-        const int64_t p0_o = __shfl_sync(0xffffffffu, p0, lo);
-        const double s_o = __shfl_sync(0xffffffffu, s, lo);
-        bool valid = f < total;
-        int64_t c = -1;
-        double v = 0.0;
-        if (valid) {
-          const int64_t p = p0_o + (f - st_o);
-          c = indices[p];
-          v = values[p];
-          valid = (c >= c0) && (c < c0 + cw);
-        }
-        const unsigned act = __ballot_sync(0xffffffffu, valid);
-        const unsigned peers = __match_any_sync(0xffffffffu, valid ? c : -1);
-        const unsigned grp = peers & act;
-        const int rank = __popc(grp & ((1u << lane) - 1));
-        const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
-        for (int q = 0; q < rounds; ++q) {
-          if (valid && rank == q) my[c - c0] += s_o * v;
-          __syncwarp();
-        }
-      }
+    };
+    // prologue: round 0 extents (dependent), round 0 nonzeros, round 1
+    // extents, round 2 rows
+    extent(brow_at(r_beg), r_beg);
+    CsrRound cur = csr_round(np0, np1, nsg, scale);
+    CsrSlot a = csr_fetch(cur, lane, indices, values);
+    CsrSlot b = csr_fetch(cur, 32 + lane, indices, values);
+    extent(brow_at(r_beg + 32), r_beg + 32);
+    int32_t nj = brow_at(r_beg + 64);
+    for (int64_t base = r_beg; base < r_end; base += 32) {
+      // round r+1: extents arrived last iteration -> scan, issue its nonzeros
+      const CsrRound nxt = csr_round(np0, np1, nsg, scale);
+      const CsrSlot na = csr_fetch(nxt, lane, indices, values);
+      const CsrSlot nb = csr_fetch(nxt, 32 + lane, indices, values);
+      // round r+2 extents, round r+3 rows
+      extent(nj, base + 64);
+      nj = brow_at(base + 96);
+      // commit round r
+      csr_commit(a, my, c0, cw);
+      csr_commit(b, my, c0, cw);
+      for (int64_t f0 = 64; f0 < cur.total; f0 += 32)  // rare: > 64 nonzeros in 32 rows
+        csr_commit(csr_fetch(cur, f0 + lane, indices, values), my, c0, cw);
+      cur = nxt;
+      a = na;
+      b = nb;
     }
   }
   __syncthreads();
   // write the tile: column c of the output gets CSR_B consecutive buckets
-  const int64_t nb = min((int64_t)CSR_B, d - i0);
+  const int64_t nbk = min((int64_t)CSR_B, d - i0);
   for (int64_t k = threadIdx.x; k < cw * CSR_B; k += blockDim.x) {
-    const int64_t cc = k / CSR_B, b = k % CSR_B;
-    if (b < nb) SA[(c0 + cc) * ldsa + i0 + b] = tile[b * ldt + cc];
+    const int64_t cc = k / CSR_B, bb = k % CSR_B;
+    if (bb < nbk) SA[(c0 + cc) * ldsa + i0 + bb] = tile[bb * ldt + cc];
   }
 }
 
