@@ -270,6 +270,130 @@ __global__ void __launch_bounds__(512) qr_backsolve_blocked_kernel(const double*
 #endif
 }
 
+// Inverses of the 32 x 32 diagonal blocks of R, all blocks at once (one
+// warp per block), so the back substitution's serial chain becomes one
+// 32 x 32 product per block.  Block bi covers rows/columns [lo, hi) with
+// hi = n - 32 bi, lo = max(0, hi - 32), counted from the bottom; a partial
+// block is padded with the identity.  Lane j builds column j of the inverse
+// (X[j][j] = 1 / R_jj, X[i][j] = -(sum_{k>i} R_ik X_kj) / R_ii upward) with
+// the block's rows broadcast from shared memory; Rinv[bi] is stored
+// row-major (32 x 32).
+constexpr int TRI_WPB = 4;  // blocks (warps) per CTA
+__global__ void __launch_bounds__(TRI_WPB * 32) qr_trinv_kernel(const double* M, int64_t ldm,
+                                                                 int64_t n, const double* beta,
+                                                                 double* Rinv) {
+  __shared__ double Rs[TRI_WPB][32][33];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t bi = (int64_t)blockIdx.x * TRI_WPB + wl;
+  const int64_t nb = (n + 31) / 32;
+  if (bi >= nb) return;
+  const int64_t hi = n - 32 * bi, lo = hi > 32 ? hi - 32 : 0;
+  const int w = (int)(hi - lo);
+  double (*R)[33] = Rs[wl];
+  // lane = row i (coalesced along the column): R[i][j] for i < j (sign of
+  // row i), diagonal |beta_i|, identity padding past w
+  {
+    const bool live = lane < w;
+    const double bt = live ? beta[lo + lane] : 1.0;
+    const double sg = bt < 0.0 ? -1.0 : 1.0;
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (live && j > lane && j < w) ? M[(lo + j) * ldm + lo + lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) R[lane][j] = j == lane ? (live ? fabs(bt) : 1.0) : sg * v[j];
+  }
+  __syncwarp();
+  // Upward over k; acc[i] collects sum_{k' > i, done} R[i][k'] X[k'] as soon
+  // as each X[k'] is known, so a step's critical path is one multiply.
+  const double rd = 1.0 / R[lane][lane];
+  double acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+  double* out = Rinv + bi * 1024;
+#pragma unroll
+  for (int k = 31; k >= 0; --k) {
+    const double rk = __shfl_sync(0xffffffffu, rd, k);
+    const double xk = k == lane ? rk : (k < lane ? -acc[k] * rk : 0.0);
+    out[k * 32 + lane] = xk;
+#pragma unroll
+    for (int i = 0; i < k; ++i) acc[i] = fma(R[i][k], xk, acc[i]);
+  }
+}
+
+// Back substitution with the inverted diagonal blocks: per block (from the
+// bottom) warp 0 forms x_b = Rinv_b y_b (lane i: row i of Rinv_b from shared
+// memory, y_b broadcast), then every thread subtracts R[i, lo:hi] x_b from
+// its rows above the block.  Nothing of R depends on x: the loads of the
+// column block are issued before the product and the next Rinv block is
+// staged by the other warps meanwhile, so per block the critical path is
+// one 32-term product, two barriers and one 32-term dot product per row.
+constexpr int BS_NT = 512;
+__global__ void __launch_bounds__(BS_NT) qr_backsolve_inv_kernel(const double* M, int64_t ldm,
+                                                                 int64_t n, const double* beta,
+                                                                 const double* Rinv,
+                                                                 const double* y_in, double* x) {
+  extern __shared__ double ys[];
+  __shared__ double rv[2][32][33];
+  __shared__ double xb[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int64_t i = tid; i < n; i += BS_NT) ys[i] = y_in[i];
+  const int64_t nb = (n + 31) / 32;
+  for (int e = tid; e < 1024; e += BS_NT) rv[0][e >> 5][e & 31] = Rinv[e];
+  __syncthreads();
+  for (int64_t bi = 0; bi < nb; ++bi) {
+    const int64_t hi = n - 32 * bi, lo = hi > 32 ? hi - 32 : 0;
+    const int w = (int)(hi - lo);
+    const int buf = (int)(bi & 1);
+    // row tid's part of the column block (independent of x): in flight now
+    double c[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) c[j] = (tid < lo && j < w) ? M[(lo + j) * ldm + tid] : 0.0;
+    if (tid < 32) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const double y0 = j < w ? ys[lo + j] : 0.0, y1 = j + 1 < w ? ys[lo + j + 1] : 0.0;
+        a0 = fma(rv[buf][lane][j], y0, a0);
+        a1 = fma(rv[buf][lane][j + 1], y1, a1);
+      }
+      const double xr = a0 + a1;
+      xb[lane] = xr;
+      if (lane < w) x[lo + lane] = xr;
+    } else if (bi + 1 < nb) {  // next block's inverse: async copies, waited at the block end
+      for (int e = tid - 32; e < 1024; e += BS_NT - 32) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&rv[buf ^ 1][e >> 5][e & 31]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                     "l"(Rinv + (bi + 1) * 1024 + e)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < lo) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        t0 = fma(c[j], xb[j], t0);
+        t1 = fma(c[j + 1], xb[j + 1], t1);
+      }
+      ys[tid] -= (beta[tid] < 0.0 ? -1.0 : 1.0) * (t0 + t1);
+    }
+    for (int64_t i = tid + BS_NT; i < lo; i += BS_NT) {  // n > BS_NT + 32: more rows
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const double m0 = j < w ? M[(lo + j) * ldm + i] : 0.0;
+        const double m1 = j + 1 < w ? M[(lo + j + 1) * ldm + i] : 0.0;
+        t0 = fma(m0, xb[j], t0);
+        t1 = fma(m1, xb[j + 1], t1);
+      }
+      ys[i] -= (beta[i] < 0.0 ? -1.0 : 1.0) * (t0 + t1);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+}
+
 // Q = H_0 H_1 ... H_{n-1} [I; 0] by backward accumulation (dorg2r), one
 // cooperative kernel, then column sign normalisation.
 __global__ void __launch_bounds__(QR_NT) qr_form_q_kernel(const double* V, int64_t d, int64_t n,
@@ -403,6 +527,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
                oW = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oW2 = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
                oW2b = blocked ? take((size_t)32 * (n + 1) * 8) : 0,
+               oRinv = blocked ? take((size_t)((n + 31) / 32) * 1024 * 8) : 0,
                oQ = (blocked && Q) ? take((size_t)ldm * n * 8) : 0;
   const int64_t part_cap = blocked ? 32 * (n + 1) * ((d + 63) / 64) : 0;  // 64-row splits
   const size_t oP = blocked ? take((size_t)part_cap * 8) : 0;
@@ -438,7 +563,17 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
                              (double*)(ws + oW2b), (double*)(ws + oPb), st);
       if (rc) break;
       qr_finish_kernel<<<1, 256, 0, st>>>(M, ldm, n, beta, fro2, R, ldr, y, badc, badv);
-      qr_backsolve_blocked_kernel<<<1, 512, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
+      static const bool subst = getenv("SKL_QR_SUBST_BACKSOLVE") != nullptr;  // A/B knob
+      if (!subst) {
+        double* Rinv = (double*)(ws + oRinv);
+        const int64_t nb = (n + 31) / 32;
+        qr_trinv_kernel<<<(unsigned)((nb + TRI_WPB - 1) / TRI_WPB), TRI_WPB * 32, 0, st>>>(
+            M, ldm, n, beta, Rinv);
+        qr_backsolve_inv_kernel<<<1, BS_NT, n * sizeof(double), st>>>(M, ldm, n, beta, Rinv, y,
+                                                                      xd);
+      } else {
+        qr_backsolve_blocked_kernel<<<1, 512, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
+      }
       if (Q) {
         double* Qw = (double*)(ws + oQ);
         const int64_t tot = d * n;
