@@ -283,12 +283,29 @@ class SketchOperator:
                 c["plan"] = CountSketchPlan(self.rows, self.signs, d)
         return c["plan"]
 
+    def device_hashes(self):
+        """CountSketch hashes in row order on the current device: (rows int32,
+        signs int8) -- drawn there by _build_sketch, else uploaded once."""
+        require_cuda()
+        c = self._cache()
+        if "hash" not in c:
+            c["hash"] = (to_device(np.ascontiguousarray(self.rows, dtype=np.int32)),
+                         to_device(np.ascontiguousarray(self.signs, dtype=np.int8)))
+        return c["hash"]
+
     def device_buckets(self):
         """(bucket_rows int32, bucket_ptr int64, bucket-ordered signs int8) on
         the current device: the CSR of S consumed by the CSR-operand kernel
         (for a sparse sign embedding each source row appears in s buckets)."""
         require_cuda()
         c = self._cache()
+        if "buckets" not in c and self.kind == "countsketch":
+            # stable sort of the row-order hashes by bucket, on the device
+            rows_d, signs_d = self.device_hashes()
+            order = torch.sort(rows_d, stable=True).indices
+            bptr = torch.zeros(self.target_dim + 1, dtype=torch.int64, device=rows_d.device)
+            bptr[1:] = torch.cumsum(torch.bincount(rows_d, minlength=self.target_dim), 0)
+            c["buckets"] = (order.to(torch.int32), bptr, signs_d[order].contiguous())
         if "buckets" not in c:
             spr = self.sparsity if self.kind == "sparsesign" else 1
             flat_rows = np.ascontiguousarray(self.rows.reshape(-1), dtype=np.int32)
