@@ -176,3 +176,13 @@ def test_sweep_runs_on_device(tmp_path):
     assert cli.main(["bench", "--m-list", "300", "--n", "8", "--repeats", "1",
                      "--out", str(tmp_path / "b")]) == 0
     assert len(E.parse_csv(str(tmp_path / "b" / "results.csv"))) == 3
+
+
+def test_readme_example_runs():
+    """The README's Python snippet, executed as written."""
+    text = (Path(__file__).resolve().parents[1] / "README.md").read_text()
+    code = text.split("```python\n", 1)[1].split("```", 1)[0]
+    ns: dict = {}
+    exec(compile(code, "README.md", "exec"), ns)
+    assert ns["res"].d == 2048 and ns["res"].method == "saa"
+    assert ns["SA"].rows == 800 and ns["SA"].cols == 200
