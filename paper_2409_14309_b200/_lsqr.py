@@ -101,11 +101,14 @@ class _Workspace:
 
 
 def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
-                R=None, ldr: int = 0):
+                R=None, ldr: int = 0, callback=None):
     """LSQR on the device for the operator ``op`` (DenseOperator or
     CsrOperator, m x n) and b (device tensor).  With R (n x n upper,
     column-major) the iteration runs on y -> A R^-1 y and returns x = R^-1 y
-    (solvers.py:146-151, 241).  Returns (x tensor, iterations, istop)."""
+    (solvers.py:146-151, 241).  ``callback(itn, iterate, rnorm)`` is called
+    once per iteration with a host copy of the iterate (y when
+    preconditioned) and the recurrence residual estimate (solvers.py:220-221).
+    Returns (x tensor, iterations, istop)."""
     require_cuda()
     ws = _Workspace(m, n)
     st = current_stream()
@@ -176,6 +179,8 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
         xnorm = math.sqrt(read(2))
         if not math.isfinite(rnorm):
             raise NumericalBreakdownError(f"non-finite residual estimate at iteration {itn}")
+        if callback is not None:
+            callback(itn, ws.x.cpu().numpy(), rnorm)
 
         test1 = rnorm / bnorm
         test2 = arnorm / (anorm * rnorm + _EPS)

@@ -282,7 +282,7 @@ def _operator(A):
 
 def matvec(A, x: Vector) -> Vector:
     """A @ x (linalg.py:148-154); O(nnz) for sparse A."""
-    from .lsqr import _Workspace
+    from ._lsqr import _Workspace
 
     if x.len != A.cols:
         raise ShapeError(f"matvec: A is {A.rows}x{A.cols} but x has length {x.len}")
@@ -297,7 +297,7 @@ def matvec(A, x: Vector) -> Vector:
 
 def matvec_transpose(A, y: Vector) -> Vector:
     """A.T @ y (linalg.py:157-163); O(nnz) for sparse A."""
-    from .lsqr import _Workspace
+    from ._lsqr import _Workspace
 
     if y.len != A.rows:
         raise ShapeError(f"matvec_transpose: A is {A.rows}x{A.cols} but y has length {y.len}")

@@ -4,13 +4,13 @@ Mirrors /root/reference/pkg/src/sketchls/solvers.py: `LeastSquaresProblem`
 :43-60, `SolverOptions` :63-87, `SolveResult` :90-99, `_operator_spec`
 :273-279, `_sketch_qr` :282-293, `sketch_and_apply` :296-320 and the
 dispatcher `solve` :364-398.  The SAA path keeps everything on the device:
-operator build (host RNG, cached plan) -> one sketch pass over [A | b] ->
+operator build (device RNG, cached plan) -> one sketch pass over [A | b] ->
 Householder QR + back substitution -> a second pass for ||Ax - b||.
 
-Sketch-and-precondition (:323-361) and plain LSQR (:110-255) run on the
-device too (lsqr.py, csrc/skl_lsqr.cu) for dense and CSR operands.  The "direct"
-normal-equations oracle (:364-398) is outside the engine and raises
-``SpecError``.
+Sketch-and-precondition (:323-361), LSQR (:110-255, optionally with a
+user preconditioner and a per-iteration callback) and the "direct" QR of A
+itself (:381-396) run on the device too (_lsqr.py, csrc/skl_lsqr.cu,
+skl_qr_solve) for dense and CSR operands.
 """
 
 from __future__ import annotations
@@ -166,7 +166,7 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
 
 def _operator_device(A: Matrix):
     """(LSQR operator, dense device A or None, lda) for a carrier."""
-    from .lsqr import CsrOperator, DenseOperator
+    from ._lsqr import CsrOperator, DenseOperator
 
     if isinstance(A, SparseMatrix):
         indptr, indices, values = A.device_arrays()
@@ -189,19 +189,40 @@ def _lsqr_result(A, b_dev, A_dev, lda, x_dev, itn, istop, method, sketch, d, t0)
                        wall_time_s=wall)
 
 
-def lsqr(A: Matrix, b: Vector, opts: SolverOptions | None = None) -> SolveResult:
-    """Plain LSQR on the device (solvers.py:110-255, no preconditioner)."""
-    from .lsqr import lsqr_device
+def _precond_device(R: DenseMatrix, n: int):
+    """Validate a user preconditioner as the reference does (solvers.py:137-145)
+    and return it column-major on the device."""
+    if R.rows != R.cols or R.cols != n:
+        raise ShapeError(f"preconditioner must be {n}x{n}, got {R.rows}x{R.cols}")
+    r = R.to_numpy()
+    if np.any(np.tril(r, -1) != 0.0):
+        raise ShapeError("preconditioner must be upper triangular")
+    zero = np.flatnonzero(np.diagonal(r) == 0.0)
+    if zero.size:
+        raise SingularFactorError(f"zero diagonal entry at index {int(zero[0])}")
+    require_cuda()
+    return to_device(np.asfortranarray(r))
+
+
+def lsqr(A: Matrix, b: Vector, opts: SolverOptions | None = None,
+         precond_R: DenseMatrix | None = None, callback=None) -> SolveResult:
+    """LSQR on the device (solvers.py:110-255): plain, or right-preconditioned
+    by an upper-triangular ``precond_R`` (the iteration runs on A R^-1 and the
+    result is x = R^-1 y); ``callback(itn, iterate, rnorm)`` once per
+    iteration, as in the reference."""
+    from ._lsqr import lsqr_device
 
     if b.len != A.rows:
         raise ShapeError(f"A is {A.rows}x{A.cols} but b has length {b.len}")
-    require_cuda()
     opts = opts or SolverOptions()
+    R_dev = _precond_device(precond_R, A.cols) if precond_R is not None else None
+    require_cuda()
     t0 = time.perf_counter()
     lop, A_dev, lda = _operator_device(A)
     b_dev = b.data if b.on_device else to_device(b.data)
     x, itn, istop = lsqr_device(lop, A.rows, A.cols, b_dev, opts.atol, opts.btol,
-                                opts.resolve_max_iter(A.cols))
+                                opts.resolve_max_iter(A.cols), R=R_dev,
+                                ldr=A.cols if R_dev is not None else 0, callback=callback)
     return _lsqr_result(A, b_dev, A_dev, lda, x, itn, istop, "lsqr", None, None, t0)
 
 
@@ -209,7 +230,7 @@ def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | Non
                             opts: SolverOptions | None = None) -> SolveResult:
     """LSQR right-preconditioned by R from QR(S A), warm-started from the
     sketched solution (solvers.py:323-361)."""
-    from .lsqr import lsqr_device
+    from ._lsqr import lsqr_device
 
     A, b = problem.A, problem.b
     if A.rows < A.cols:
@@ -234,7 +255,7 @@ def sketch_and_precondition(problem: LeastSquaresProblem, spec: SketchSpec | Non
         # r0 = b - A x0 (solvers.py:345-349): -(A x0) - (-1) b
         r0 = device_f64((A.rows,))
         scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
-        from .lsqr import _Workspace
+        from ._lsqr import _Workspace
 
         lop.mv(x0, -1.0, -1.0, b_dev, r0, scratch, _Workspace(A.rows, n), current_stream())
         xi, itn, istop = lsqr_device(lop, A.rows, n, r0, opts.atol, opts.btol, max_iter,

@@ -663,3 +663,24 @@ def test_concurrent_solves_from_threads():
     assert not errs, errs
     for t in range(4):
         assert np.array_equal(out[t], serial[t])
+
+
+def test_lsqr_with_preconditioner_and_callback():
+    """lsqr(A, b, opts, precond_R, callback) as solvers.py:110-255: the
+    preconditioned iteration matches the oracle, the callback sees every
+    iteration with a nonincreasing residual estimate."""
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((3000, 24)) @ np.diag(np.logspace(0, -4, 24))
+    b = rng.standard_normal(3000)
+    R = np.linalg.qr(A[rng.choice(3000, 200, replace=False)], mode="r")
+    R = np.triu(R)
+    want = O.lsqr(A, b, precond_R=R)
+    seen = []
+    res = E.lsqr(E.DenseMatrix(A), E.Vector(b), precond_R=E.DenseMatrix(R),
+                 callback=lambda itn, x, rn: seen.append((itn, x.shape, rn)))
+    assert res.method == "lsqr" and res.iterations == want["iterations"]
+    assert rel_fro(res.x.data, want["x"]) < 1e-9
+    assert [s[0] for s in seen] == list(range(1, res.iterations + 1))
+    assert all(s[1] == (24,) for s in seen)
+    rn = [s[2] for s in seen]
+    assert all(rn[i + 1] <= rn[i] * (1 + 1e-12) for i in range(len(rn) - 1))
