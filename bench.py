@@ -269,7 +269,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # SKL_BENCH_PEER=1 runs the fused peer-slot reduce even at N = 1 (a
+    # one-rank group), so the N > 1 code path can be exercised on one GPU
+    force_peer = bool(os.environ.get("SKL_BENCH_PEER"))
+    grouped = world > 1 or force_peer
+    if grouped:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     # ---- data: every rank owns a full config-sized row block (weak scaling)
@@ -304,15 +308,34 @@ def main():
     outbuf = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda")
     out = outbuf.t()[:d]
     cs_plan = plan.device_plan()
+    # N > 1: the reduce is fused with the sketch -- each rank's kernel writes
+    # its partial into its slot of rank 0's symmetric buffer over NVLink and
+    # rank 0 sums the slots in rank order after a device barrier
+    # (distributed.PeerSlots); one NCCL reduce where that is unavailable.
+    from paper_2409_14309_b200.distributed import peer_slots_or_none
+
+    slots = peer_slots_or_none(d, n + 1) if grouped else None
+    collective = ("peer-slots" if slots is not None else
+                  ("nccl-reduce" if world > 1 else "none"))
 
     def apply():
-        cs_plan.apply(A, m_loc, n, lda, b, out, ld, out[:, n], partitions=1,
-                      stream=stream.cuda_stream)
+        if slots is not None:
+            base = slots.slot_ptr()
+            cs_plan.apply(A, m_loc, n, lda, b, base, slots.ld, base + 8 * slots.ld * n,
+                          partitions=1, stream=stream.cuda_stream)
+        else:
+            cs_plan.apply(A, m_loc, n, lda, b, out, ld, out[:, n], partitions=1,
+                          stream=stream.cuda_stream)
+
+    def collect():
+        if slots is not None:
+            slots.finish(out, ld)
+        elif world > 1:
+            dist.reduce(outbuf, dst=0)
 
     def step():
         apply()
-        if world > 1:
-            dist.reduce(outbuf, dst=0)
+        collect()
 
     for _ in range(args.warmup):
         step()
@@ -331,8 +354,7 @@ def main():
             k_ev[i][0].record(stream)
             apply()
             k_ev[i][1].record(stream)
-            if world > 1:
-                dist.reduce(outbuf, dst=0)
+            collect()
         stop.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -463,7 +485,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"config {cfg.cfg}: dense {m_loc}x{n} fp64 (kappa=1e8) per GPU, "
                                    f"CountSketch d={d}, one pass S[A|b]"
-                                   + (" + NCCL reduce of d x (n+1) partials" if world > 1 else ""),
+                                   + (" + reduce of the d x (n+1) partials" if world > 1 else ""),
+                       "collective": collective,
                        "m_per_gpu": m_loc, "n": n, "d": d, "m_total": m_total,
                        "parallelism": f"rows sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (2 GiB of A per GPU per step); no flush"},
@@ -483,7 +506,7 @@ def main():
         if solve:
             line["solve"] = solve
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if grouped:
         dist.destroy_process_group()
 
 

@@ -312,6 +312,15 @@ int skl_residual_csr(const int64_t* indptr, const int64_t* indices, const double
                      int64_t m, int64_t n, const double* x, const double* b, double* out,
                      void* stream);
 
+/* ---- row-sharded apply: the reduce step ----
+ * out[:, c] = sum over q = 0 .. nslots-1, in that order, of
+ * slots[q * slot_stride + c * ld + i] (rows x cols, column-major slots).
+ * The slots are the per-rank partial sketches the ranks' kernels wrote into
+ * the destination's symmetric buffer over NVLink; replaces the NCCL reduce
+ * of the reference-style sharding with a deterministic fixed-order sum. */
+int skl_sum_slots(const double* slots, int64_t nslots, int64_t slot_stride, int64_t rows,
+                  int64_t cols, int64_t ld, double* out, int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -133,6 +133,7 @@ SIGNATURES: dict[str, tuple] = {
          c_ptr],
     ),
     "skl_residual_dense": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_sum_slots": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_residual_csr": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
 }
 
@@ -208,6 +209,8 @@ def ptr(a) -> int | None:
     """Raw address of a numpy array or torch tensor (None passes NULL)."""
     if a is None:
         return None
+    if isinstance(a, int):  # already a device address (e.g. a peer buffer)
+        return a
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()

@@ -174,3 +174,22 @@ def test_srht_shard_must_be_block_aligned():
     op = build_sketch(SketchSpec("srht", 64, seed=1), 20_000)
     with pytest.raises(ValueError):
         ShardPlan(op, 100, 20_000)
+
+
+def test_peer_slots_pointer_parity():
+    """PeerSlots' slot addressing (host logic, no device): rank r writes slot r
+    of the destination's buffer, alternating halves by step parity."""
+    from paper_2409_14309_b200.distributed import PeerSlots, partial_ld
+
+    s = PeerSlots.__new__(PeerSlots)
+    s.rank, s.world, s.rows, s.cols = 2, 4, 100, 7
+    s.ld = partial_ld(100)
+    s.slot = s.cols * s.ld
+    s.dst_base, s.step = 1 << 40, 0
+    half = 4 * s.slot * 8
+    assert s.slot_ptr() == (1 << 40) + 8 * 2 * s.slot
+    s.step = 1
+    assert s.slot_ptr() == (1 << 40) + half + 8 * 2 * s.slot
+    s.step = 2
+    assert s.slot_ptr() == (1 << 40) + 8 * 2 * s.slot
+    assert s.ld == 100 and partial_ld(101) == 102
