@@ -31,7 +31,7 @@ from typing import Callable
 import numpy as np
 
 from . import _native
-from ._device import current_stream, device_f64, require_cuda, to_device, torch
+from ._device import current_stream, device_f64, require_cuda, torch
 from .sketch import SHARD_ALIGN, CountSketchPlan, SketchOperator, build_sketch
 
 

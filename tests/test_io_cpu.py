@@ -10,9 +10,10 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-import paper_2409_14309_b200 as E
-from paper_2409_14309_b200 import cli, mmio, sweep
 import torch
+
+import paper_2409_14309_b200 as E
+from paper_2409_14309_b200 import cli, sweep
 
 IO = Path(__file__).resolve().parent / "golden" / "io"
 

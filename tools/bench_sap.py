@@ -10,7 +10,6 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2409_14309_b200 as E  # noqa: E402
