@@ -79,3 +79,39 @@ def test_random_saa_solves_match_oracle(i):
     assert res.d == want["d"]
     assert rel_fro(res.x.data, want["x"]) <= 1e-9, (kind, m, n, res.d)
     assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_sap_lsqr_direct_match_oracle(i):
+    """sap (all kinds, warm start on/off, dense and CSR), plain lsqr and
+    direct on random shapes: x within 1e-9 of the oracle / LAPACK."""
+    rng = np.random.default_rng(7000 + i)
+    n = int(rng.integers(2, 30))
+    m = int(rng.integers(6 * n, 15000))
+    A = rng.standard_normal((m, n)) * np.logspace(0, -3, n)
+    if i % 3 == 2:
+        S = scipy.sparse.random(m, n, density=0.2, random_state=i, format="csr")
+        S.data = rng.standard_normal(S.nnz)
+        A = S.toarray() + np.eye(m, n)  # full column rank
+        carrier = E.SparseMatrix.from_scipy(scipy.sparse.csr_matrix(A))
+    else:
+        carrier = E.DenseMatrix(A)
+    b = A @ rng.standard_normal(n) + 1e-2 * rng.standard_normal(m)
+    prob = E.LeastSquaresProblem(A=carrier, b=E.Vector(b))
+    kind = KINDS[i % 4]
+    seed = int(rng.integers(0, 2**31))
+    warm = bool(i % 2)
+    want = O.sap_solve(A, b, kind, seed, 4.0, warm_start=warm)
+    res = E.solve(prob, "sap", E.SketchSpec(kind, 1, seed=seed),
+                  E.SolverOptions(d_factor=4.0, warm_start=warm))
+    assert res.iterations == want["iterations"], (kind, m, n)
+    assert rel_fro(res.x.data, want["x"]) <= 1e-9, (kind, m, n)
+    # unpreconditioned LSQR on kappa ~1e3..1e4: the iterates amplify the
+    # different rounding of the device reductions; compare to that bound
+    plain = E.solve(prob, "lsqr")
+    ref = O.lsqr(A, b)
+    assert rel_fro(plain.x.data, ref["x"]) <= 1e-7
+    assert abs(plain.residual_norm - ref["residual"]) <= 1e-10 * ref["residual"]
+    assert abs(plain.iterations - ref["iterations"]) <= max(2, ref["iterations"] // 10)
+    direct = E.solve(prob, "direct")
+    assert rel_fro(direct.x.data, np.linalg.lstsq(A, b, rcond=None)[0]) <= 1e-10
