@@ -25,7 +25,16 @@
 
 namespace skl {
 
-constexpr int GM_BM = 128, GM_BN = 128, GM_BK = 32, GM_PAD = 2, GM_STAGES = 3;
+#ifndef SKL_GM_BK
+#define SKL_GM_BK 32
+#endif
+#ifndef SKL_GM_STAGES
+#define SKL_GM_STAGES 3
+#endif
+#ifndef SKL_GM_MINB
+#define SKL_GM_MINB 1
+#endif
+constexpr int GM_BM = 128, GM_BN = 128, GM_BK = SKL_GM_BK, GM_PAD = 2, GM_STAGES = SKL_GM_STAGES;
 constexpr int GM_LD = GM_BK + GM_PAD;  // smem row stride (doubles)
 constexpr int GM_THREADS = 256;
 
@@ -88,7 +97,7 @@ __device__ __forceinline__ void gm_load(const GemmParams& p, double* Gs, double*
   }
 }
 
-__global__ void __launch_bounds__(GM_THREADS, 1) gemm_f64_dmma_kernel(const GemmParams p) {
+__global__ void __launch_bounds__(GM_THREADS, SKL_GM_MINB) gemm_f64_dmma_kernel(const GemmParams p) {
   extern __shared__ __align__(128) double gsm[];
   double* Gs = gsm;                                   // [STAGES][BM][LD]
   double* As = gsm + GM_STAGES * GM_BM * GM_LD;       // [STAGES][BN][LD]
