@@ -131,15 +131,16 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
     const int32_t* __restrict__ rows, const int8_t* __restrict__ signs, int64_t m, int d,
     int chunk, int warps, const int32_t* __restrict__ maxlen, const int64_t* __restrict__ off,
     uint16_t* __restrict__ lanes) {
-  extern __shared__ uint32_t keys[];  // [PB_KEYS], then start[d], cnt[d], per-warp scratch
+  extern __shared__ uint32_t keys[];  // [PB_KEYS], then start[d], cnt[d], the chunk's signs
   int32_t* start = reinterpret_cast<int32_t*>(keys + PB_KEYS);
   int32_t* cnt = start + d;
-  uint16_t* stepbuf = reinterpret_cast<uint16_t*>(cnt + d);  // [warps][32]
+  int8_t* sg = reinterpret_cast<int8_t*>(cnt + d);  // [chunk] signs of the chunk's rows
   const int64_t k = blockIdx.x, r0 = k * chunk;
   const int len = (int)min((int64_t)chunk, m - r0);
   const int tid = threadIdx.x;
   for (int i = tid; i < PB_KEYS; i += PB_NT)
     keys[i] = i < len ? ((uint32_t)rows[r0 + i] << 13) | (uint32_t)i : 0xffffffffu;
+  for (int i = tid; i < len; i += PB_NT) sg[i] = signs[r0 + i];
   for (int b = tid; b < d; b += PB_NT) cnt[b] = 0;
   __syncthreads();
   // bitonic sort of the keys (ascending: bucket, then row)
@@ -186,31 +187,34 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
     for (int q = 0; q < w; ++q) rowbase += maxlen[k * warps + q];
     const int ml = maxlen[k * warps + w];
     uint16_t* R = blk + head + (int64_t)rowbase * 32;
-    uint16_t* sb = stepbuf + w * 32;
-    // lane l keeps its next-entry counters for the four slots
-    int nxt[PB_SLOTS] = {0, 0, 0, 0};
-    int cb[PB_SLOTS], st[PB_SLOTS];
+    // lane l's four slot lists: next row (register), entries left
+    int nxt[PB_SLOTS], cb[PB_SLOTS], st[PB_SLOTS];
+    uint32_t cand[PB_SLOTS];
 #pragma unroll
     for (int s = 0; s < PB_SLOTS; ++s) {
       const int b = w * 32 + lane + s * 32 * warps;
       cb[s] = b < d ? cnt[b] : 0;
       st[s] = b < d ? start[b] : 0;
+      nxt[s] = 0;
+      cand[s] = cb[s] > 0 ? (keys[st[s]] & 0x1fffu) : 0u;
     }
     for (int step = 0; step < ml; ++step) {
-      // the lanes choose in lane order; each choice sees the bank loads of
-      // the lanes before it (exactly the host planner's greedy)
+      // The lanes choose in lane order, each seeing the bank loads of the
+      // lanes before it -- exactly the host planner's greedy.  Only register
+      // compares sit on this serial chain: the candidates are preloaded, the
+      // chosen list advances and the word (with its sign) is formed after.
       uint32_t ld4[4] = {0u, 0u, 0u, 0u};  // 16 bank counters, 8 bits each
+      int mine = -1;
+#pragma unroll 4
       for (int l = 0; l < 32; ++l) {
         int choice = -1;
-        uint32_t jrow = 0;
         if (lane == l) {
           int bload = 1 << 30;
           int bleft = 0;
 #pragma unroll
           for (int s = 0; s < PB_SLOTS; ++s) {
             if (nxt[s] >= cb[s]) continue;
-            const uint32_t j = keys[st[s] + nxt[s]] & 0x1fffu;
-            const int bank = (int)(j & 15);
+            const int bank = (int)(cand[s] & 15);
             const uint32_t word4 = bank < 8 ? (bank < 4 ? ld4[0] : ld4[1])
                                             : (bank < 12 ? ld4[2] : ld4[3]);
             const int ld = (int)((word4 >> (8 * (bank & 3))) & 255u);
@@ -219,35 +223,36 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
               choice = s;
               bload = ld;
               bleft = left;
-              jrow = j;
             }
           }
-          uint16_t word = pad;
-          if (choice >= 0) {
-            ++nxt[choice];
-            word = (uint16_t)(jrow | ((uint32_t)choice << 13) |
-                              ((signs[r0 + jrow] < 0 ? 1u : 0u) << 15));
-          }
-          sb[l] = word;
+          mine = choice;
         }
-        choice = __shfl_sync(0xffffffffu, choice, l);
-        jrow = __shfl_sync(0xffffffffu, jrow, l);
-        if (choice >= 0) {
-          const int bank = (int)(jrow & 15);
-          const uint32_t inc = 1u << (8 * (bank & 3));
-          if (bank < 4)
+        const int bank_l = __shfl_sync(0xffffffffu,
+                                       choice >= 0 ? (int)(cand[choice & 3] & 15) : -1, l);
+        if (bank_l >= 0) {
+          const uint32_t inc = 1u << (8 * (bank_l & 3));
+          if (bank_l < 4)
             ld4[0] += inc;
-          else if (bank < 8)
+          else if (bank_l < 8)
             ld4[1] += inc;
-          else if (bank < 12)
+          else if (bank_l < 12)
             ld4[2] += inc;
           else
             ld4[3] += inc;
         }
       }
-      __syncwarp();
-      R[(int64_t)step * 32 + lane] = sb[lane];
-      __syncwarp();
+      uint16_t word = pad;
+      if (mine >= 0) {
+        const uint32_t jrow = cand[mine & 3];
+        word = (uint16_t)(jrow | ((uint32_t)mine << 13) | ((sg[jrow] < 0 ? 1u : 0u) << 15));
+#pragma unroll
+        for (int s = 0; s < PB_SLOTS; ++s)
+          if (s == mine) {
+            ++nxt[s];
+            cand[s] = nxt[s] < cb[s] ? (keys[st[s] + nxt[s]] & 0x1fffu) : 0u;
+          }
+      }
+      R[(int64_t)step * 32 + lane] = word;
     }
   }
 }
@@ -352,7 +357,7 @@ extern "C" int skl_countsketch_plan_owned_device(const int32_t* rows, const int8
     SKL_REQUIRE(total_and_max[1] <= 65535LL * 32, SKL_ERR_SPEC, "owned plan: chunk block too large");
     return SKL_OK;
   }
-  const size_t smem = (size_t)PB_KEYS * 4 + (size_t)d * 8 + (size_t)warps * 32 * 2;
+  const size_t smem = (size_t)PB_KEYS * 4 + (size_t)d * 8 + (size_t)chunk;
   SKL_CUDA(cudaFuncSetAttribute(owned_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   owned_fill_kernel<<<(unsigned)nch, PB_NT, smem, st>>>(rows, signs, m, (int)d, (int)chunk, warps,
