@@ -514,9 +514,12 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   const size_t budget = 227 * 1024 - 128;
   int stages = (int)std::min<size_t>(OW_MAX_STAGES, budget / stage);
   SKL_REQUIRE(stages >= 2, SKL_ERR_INVALID, "countsketch: plan blocks too large");
+  const int64_t nch = (row_end - row_begin + T - 1) / T;
+  // a short column stream gains nothing from a deep ring; two stages let
+  // several column CTAs share an SM so the grid fits one wave
+  if (nch <= 5) stages = std::min(stages, 2);
   if (const char* env = getenv("SKL_OWNED_STAGES")) stages = std::max(2, std::min(stages, atoi(env)));
   const size_t smem = 128 + stages * stage;
-  const int64_t nch = (row_end - row_begin + T - 1) / T;
   int P = partitions;
   if (P <= 0) {
     const int sms = sm_count();

@@ -66,7 +66,8 @@ class CountSketchPlan:
         self.d = int(d)
         self.spr = int(spr)
         self.scale = 1.0 / math.sqrt(spr) if spr > 1 else 1.0
-        self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, kind)
+        self.kind, self.chunk, self.warps = _native.plan_geometry(
+            self.d, kind, m=None if spr > 1 else int(np.asarray(signs).shape[0]))
         if spr > 1:
             if self.kind != "owned":
                 raise SpecError(f"sparse sign embeddings with embed_dim {d} > "
@@ -100,7 +101,7 @@ class CountSketchPlan:
         self = cls.__new__(cls)
         self.d = int(d)
         self.spr, self.scale = 1, 1.0
-        self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, "owned")
+        self.kind, self.chunk, self.warps = _native.plan_geometry(self.d, "owned", m=m)
         st = current_stream()
         tm = np.zeros(2, dtype=np.int64)
         while True:
