@@ -465,7 +465,7 @@ def main():
             assert np.array_equal(SAh, out[:, :n].cpu().numpy())
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU leg: rank 0 at N = 1 only
         ms = 1 << 17
         Ah_s = np.asfortranarray(A[:ms].cpu().numpy())
         bh_s = b[:ms].cpu().numpy()
@@ -500,7 +500,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
-            "gpu_launches": args.steps,
+            # our kernels per timed step: the sketch, plus the slot sum on rank 0
+            "gpu_launches": args.steps * (2 if slots is not None else 1),
         }
         if solve:
             line["solve"] = solve
