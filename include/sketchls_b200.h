@@ -121,6 +121,13 @@ int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out);
 int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
                          int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
                          int threads);
+/* The same plan for a sparse sign embedding with d > 2048 (the register-owned
+ * plan covers d <= 2048): source row j contributes `spr` entries, rows and
+ * signs hold m * spr values (entry j * spr + q, distinct buckets per row);
+ * chunk * spr <= 65536.  Consumed by skl_sparsesign_dense. */
+int skl_sparsesign_plan(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                        int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                        int threads);
 
 /* S*A and S*b for dense column-major A (device pointers, plan on device;
  * max_block = largest chunk block in words).
@@ -133,6 +140,14 @@ int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda, co
                           const uint32_t* lanes, const int64_t* chunk_off, int64_t max_block,
                           int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                           double* Sb, int partitions, int accumulate, void* stream);
+/* skl_countsketch_dense for a sparse sign plan (skl_sparsesign_plan): every
+ * entry adds fl(+-scale * A[j, c]) (scale = fl(1/sqrt(s)), csr_matvecs'
+ * product), so the result is bitwise-equal to sparse_map @ A
+ * (sketch.py:104-115, 209-212). */
+int skl_sparsesign_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                         const uint32_t* lanes, const int64_t* chunk_off, int64_t max_block,
+                         int64_t d, int64_t chunk, int warps, double scale, double* SA,
+                         int64_t ldsa, double* Sb, int partitions, int accumulate, void* stream);
 
 /* Register-owned plan for d <= 128 * warps (the common case): bucket b is
  * held for the whole apply in a register of consumer thread b % (32*warps),

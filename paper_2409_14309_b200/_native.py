@@ -46,6 +46,12 @@ SIGNATURES: dict[str, tuple] = {
     "skl_rng_srht": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_int]),
     "skl_countsketch_plan": (
         c_int, [c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_int]),
+    "skl_sparsesign_plan": (
+        c_int, [c_ptr, c_ptr, c_i64, c_int, c_i64, c_i64, c_int, c_ptr, c_ptr, c_int]),
+    "skl_sparsesign_dense": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, ctypes.c_double,
+         c_ptr, c_i64, c_ptr, c_int, c_int, c_ptr]),
     "skl_countsketch_dense": (
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_int, c_ptr,
@@ -270,16 +276,19 @@ def plan_geometry(d: int, kind: str | None = None, m: int | None = None) -> tupl
 
 
 def countsketch_plan(rows: np.ndarray, signs: np.ndarray, d: int, chunk: int, warps: int,
-                     threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
-    """(lanes u32, chunk_off i64 [nch+1], max block words) -- see the header."""
-    m = rows.shape[0]
+                     threads: int = 0, spr: int = 1) -> tuple[np.ndarray, np.ndarray, int]:
+    """(lanes u32, chunk_off i64 [nch+1], max block words) -- see the header;
+    ``spr`` entries per source row (a sparse sign plan, rows/signs flattened)."""
+    m = rows.shape[0] // spr
     nch = (m + chunk - 1) // chunk
     off = np.zeros(nch + 1, dtype=np.int64)
-    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, None, ptr(off),
-         threads)
+    if spr == 1:
+        fn, pre = "skl_countsketch_plan", (ptr(rows), ptr(signs), m, d, chunk, warps)
+    else:
+        fn, pre = "skl_sparsesign_plan", (ptr(rows), ptr(signs), m, spr, d, chunk, warps)
+    call(fn, *pre, None, ptr(off), threads)
     lanes = np.empty(int(off[-1]), dtype=np.uint32)
-    call("skl_countsketch_plan", ptr(rows), ptr(signs), m, d, chunk, warps, ptr(lanes), ptr(off),
-         threads)
+    call(fn, *pre, ptr(lanes), ptr(off), threads)
     return lanes, off, int(np.diff(off).max())
 
 

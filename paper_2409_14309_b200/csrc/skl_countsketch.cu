@@ -59,6 +59,7 @@ struct CsParams {
   double* outb;     // Sb (P == 1)
   double* part;     // [P][ncols][d] (P > 1)
   int accumulate;
+  double scale;     // entry magnitude (sparse sign: fl(1/sqrt(s))), SCALED kernels only
 };
 
 __device__ __forceinline__ const double* cs_col(const CsParams& p, int64_t c) {
@@ -70,7 +71,7 @@ __device__ __forceinline__ void cs_consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-template <int NT, int C>
+template <int NT, int C, bool SCALED>
 __global__ void __launch_bounds__(NT + 32, 2)
     countsketch_dense_kernel(const CsParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -176,6 +177,8 @@ __global__ void __launch_bounds__(NT + 32, 2)
       for (int c = 0; c < C; ++c) {
         const uint2 w = *reinterpret_cast<const uint2*>(src + (size_t)c * (T + 2) * 8);
         x[c] = __hiloint2double((int)(w.y ^ (e & 0x80000000u)), (int)w.x);
+        // fl(+-1/sqrt(s) * a) rounded on its own, as csr_matvecs forms it (no FMA)
+        if (SCALED) x[c] = __dmul_rn(p.scale, x[c]);
       }
       const int b = (int)((e >> 16) & 0x7fffu);
       if (b != cur) {
@@ -390,7 +393,8 @@ static int sm_count() {
 
 template <int NT, int C>
 static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kern = countsketch_dense_kernel<NT, C>;
+  auto kern = p.scale != 1.0 ? countsketch_dense_kernel<NT, C, true>
+                             : countsketch_dense_kernel<NT, C, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -414,7 +418,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
                               const uint32_t* lanes, const int64_t* chunk_off, int64_t max_block,
                               int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                               double* Sb, int partitions, int accumulate, int64_t row_begin,
-                              int64_t row_end, cudaStream_t st) {
+                              int64_t row_end, cudaStream_t st, double scale = 1.0) {
   SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld lda=%lld ldsa=%lld", (long long)m,
               (long long)n, (long long)d, (long long)lda, (long long)ldsa);
@@ -462,6 +466,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
   p.d = (int)d; p.T = T; p.P = P;
   p.head = (warps + 1 + 3) / 4 * 4;
   p.out = SA; p.ldo = ldsa; p.outb = Sb; p.part = nullptr; p.accumulate = accumulate;
+  p.scale = scale;
 
   double* part = nullptr;
   if (P > 1) {
@@ -601,6 +606,17 @@ extern "C" int skl_sparsesign_dense_owned(const double* A, int64_t m, int64_t n,
   return countsketch_owned_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps,
                                   SA, ldsa, Sb, partitions, accumulate, 0, m, (cudaStream_t)stream,
                                   scale);
+}
+
+extern "C" int skl_sparsesign_dense(const double* A, int64_t m, int64_t n, int64_t lda,
+                                    const double* b, const uint32_t* lanes,
+                                    const int64_t* chunk_off, int64_t max_block, int64_t d,
+                                    int64_t chunk, int warps, double scale, double* SA,
+                                    int64_t ldsa, double* Sb, int partitions, int accumulate,
+                                    void* stream) {
+  clear_error();
+  return countsketch_launch(A, m, n, lda, b, lanes, chunk_off, max_block, d, chunk, warps, SA, ldsa,
+                            Sb, partitions, accumulate, 0, m, (cudaStream_t)stream, scale);
 }
 
 extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int64_t lda,

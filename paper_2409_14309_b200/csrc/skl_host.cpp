@@ -112,18 +112,23 @@ namespace {
 // parallel; the segmentation never depends on the thread count.
 constexpr int64_t kPlanSegment = 32;
 
+// Entries of a chunk: source row j contributes `spr` entries (e = j * spr + q:
+// bucket rows[(r0 + j) * spr + q], sign signs[same]) -- one for a
+// CountSketch, s for a sparse sign embedding (distinct buckets per row).
 struct ChunkSort {
   std::vector<uint32_t> cnt, start, pos;
-  std::vector<uint16_t> sorted;
-  ChunkSort(int64_t d, int64_t chunk)
-      : cnt((size_t)d), start((size_t)d), pos((size_t)d), sorted((size_t)chunk) {}
-  // stable counting sort of chunk k's rows by bucket; false on a bad bucket
+  std::vector<uint16_t> sorted;  // entry index e, bucket-major, rows ascending
+  int spr;
+  ChunkSort(int64_t d, int64_t chunk, int spr_)
+      : cnt((size_t)d), start((size_t)d), pos((size_t)d), sorted((size_t)(chunk * spr_)),
+        spr(spr_) {}
+  // stable counting sort of chunk k's entries by bucket; false on a bad bucket
   bool run(const int32_t* rows, int64_t m, int64_t d, int64_t chunk, int64_t k) {
     const int64_t r0 = k * chunk;
-    const int len = (int)std::min<int64_t>(chunk, m - r0);
+    const int len = (int)std::min<int64_t>(chunk, m - r0) * spr;
     std::fill(cnt.begin(), cnt.end(), 0u);
-    for (int j = 0; j < len; ++j) {
-      const int32_t r = rows[r0 + j];
+    for (int e = 0; e < len; ++e) {
+      const int32_t r = rows[r0 * spr + e];
       if (r < 0 || r >= d) return false;
       ++cnt[(size_t)r];
     }
@@ -133,9 +138,11 @@ struct ChunkSort {
       pos[(size_t)b] = run;
       run += cnt[(size_t)b];
     }
-    for (int j = 0; j < len; ++j) sorted[pos[(size_t)rows[r0 + j]]++] = (uint16_t)j;
+    for (int e = 0; e < len; ++e) sorted[pos[(size_t)rows[r0 * spr + e]]++] = (uint16_t)e;
     return true;
   }
+  // source row (within the chunk) of the t-th sorted entry
+  uint32_t row(size_t t) const { return (uint32_t)sorted[t] / (uint32_t)spr; }
 };
 
 struct WarpSched {
@@ -177,7 +184,7 @@ void schedule_chunk(const int8_t* signs, int64_t d, int64_t chunk, int64_t r0, i
     W.bank[g].clear();
     W.bhead[g] = 0;
   }
-  for (uint32_t b : W.pool) W.bank[S.sorted[S.start[b]] & 15].push_back(b);
+  for (uint32_t b : W.pool) W.bank[S.row(S.start[b]) & 15].push_back(b);
   size_t left = W.pool.size();
   for (int l = 0; l < 32; ++l) run[l] = -1;
   for (int l = 0; l < 32; ++l) {  // continuations keep their register sum
@@ -196,7 +203,7 @@ void schedule_chunk(const int8_t* signs, int64_t d, int64_t chunk, int64_t r0, i
     if (!first && !busy && !left) break;
     int gl[16] = {0}, al[16] = {0};
     for (int l = 0; l < 32; ++l)
-      if (run[l] >= 0) gl[S.sorted[S.start[(uint32_t)run[l]] + pos[l]] & 15]++;
+      if (run[l] >= 0) gl[S.row(S.start[(uint32_t)run[l]] + pos[l]) & 15]++;
     for (int l = 0; l < 32 && left; ++l) {
       if (run[l] >= 0) continue;
       // least-loaded gather bank with work left, then the least-loaded
@@ -230,8 +237,9 @@ void schedule_chunk(const int8_t* signs, int64_t d, int64_t chunk, int64_t r0, i
       uint32_t word;
       if (run[l] >= 0) {
         const uint32_t b = (uint32_t)run[l];
-        const uint32_t j = S.sorted[S.start[b] + pos[l]];
-        word = (8u * j) | (b << 16) | ((signs[r0 + j] < 0 ? 1u : 0u) << 31);
+        const uint32_t e = S.sorted[S.start[b] + pos[l]];
+        const uint32_t j = e / (uint32_t)S.spr;
+        word = (8u * j) | (b << 16) | ((signs[r0 * S.spr + e] < 0 ? 1u : 0u) << 31);
         cur[l] = b;
         if (++pos[l] == S.cnt[b]) run[l] = -1;
         any = true;
@@ -255,10 +263,10 @@ void schedule_chunk(const int8_t* signs, int64_t d, int64_t chunk, int64_t r0, i
 // Runs the schedule of chunks [k0, k1) for all warps; per chunk calls
 // sink(k, warp_rows[warps], words_of_warp[warps]).
 template <class Sink>
-bool plan_segment(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d, int64_t chunk,
-                  int warps, int64_t k0, int64_t k1, Sink&& sink) {
+bool plan_segment(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                  int64_t chunk, int warps, int64_t k0, int64_t k1, Sink&& sink) {
   const int64_t gsize = (d + warps - 1) / warps;
-  ChunkSort S(d, chunk);
+  ChunkSort S(d, chunk, spr);
   std::vector<WarpSched> W((size_t)warps);
   for (auto& ws : W)
     for (int l = 0; l < 32; ++l) ws.cur[l] = (uint32_t)d;
@@ -482,12 +490,14 @@ int skl_rng_srht(uint64_t key, int64_t m_pad, int64_t d, int8_t* signs, int64_t*
   return SKL_OK;
 }
 
-int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
-                         int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
-                         int threads) {
-  clear_error();
-  SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1, SKL_ERR_INVALID,
+static int lanes_plan(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                      int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                      int threads) {
+  SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1 && spr >= 1, SKL_ERR_INVALID,
               "skl_countsketch_plan: bad arguments");
+  SKL_REQUIRE(chunk * spr <= 65536, SKL_ERR_INVALID,
+              "plan chunk %lld x %d entries per row exceeds the 16-bit entry index",
+              (long long)chunk, spr);
   SKL_REQUIRE(d <= 32767, SKL_ERR_SPEC, "countsketch plan: embed_dim %lld > 32767",
               (long long)d);
   SKL_REQUIRE(chunk >= 8 && chunk <= 4088 && chunk % 8 == 0, SKL_ERR_INVALID,
@@ -504,7 +514,7 @@ int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, in
   parallel_for(nseg, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t g = lo; g < hi; ++g) {
       const int64_t k0 = g * kPlanSegment, k1 = std::min(nch, k0 + kPlanSegment);
-      if (!plan_segment(rows, signs, m, d, chunk, warps, k0, k1,
+      if (!plan_segment(rows, signs, m, spr, d, chunk, warps, k0, k1,
                         [&](int64_t k, const std::vector<std::vector<uint32_t>>& wd) {
                           for (int w = 0; w < warps; ++w)
                             R[(size_t)(k * warps + w)] = (uint32_t)(wd[(size_t)w].size() / 32);
@@ -530,7 +540,7 @@ int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, in
   parallel_for(nseg, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t g = lo; g < hi; ++g) {
       const int64_t k0 = g * kPlanSegment, k1 = std::min(nch, k0 + kPlanSegment);
-      plan_segment(rows, signs, m, d, chunk, warps, k0, k1,
+      plan_segment(rows, signs, m, spr, d, chunk, warps, k0, k1,
                    [&](int64_t k, const std::vector<std::vector<uint32_t>>& wd) {
                      uint32_t* blk = lanes + off[(size_t)k];
                      uint32_t base = 0;
@@ -545,6 +555,20 @@ int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, in
     }
   }, 1);
   return SKL_OK;
+}
+
+int skl_countsketch_plan(const int32_t* rows, const int8_t* signs, int64_t m, int64_t d,
+                         int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                         int threads) {
+  clear_error();
+  return lanes_plan(rows, signs, m, 1, d, chunk, warps, lanes, chunk_off, threads);
+}
+
+int skl_sparsesign_plan(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int64_t d,
+                        int64_t chunk, int warps, uint32_t* lanes, int64_t* chunk_off,
+                        int threads) {
+  clear_error();
+  return lanes_plan(rows, signs, m, spr, d, chunk, warps, lanes, chunk_off, threads);
 }
 
 }  // extern "C"

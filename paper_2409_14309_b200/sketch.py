@@ -69,10 +69,8 @@ class CountSketchPlan:
         self.kind, self.chunk, self.warps = _native.plan_geometry(
             self.d, kind, m=None if spr > 1 else int(np.asarray(signs).shape[0]))
         if spr > 1:
-            if self.kind != "owned":
-                raise SpecError(f"sparse sign embeddings with embed_dim {d} > "
-                                f"{_native.OWNED_MAX_D} are implemented for CSR operands only")
-            self.chunk = max(8, self.chunk // spr // 8 * 8)
+            if self.kind == "owned":  # the owned plan's 13-bit row field counts entries
+                self.chunk = max(8, self.chunk // spr // 8 * 8)
             rows = np.ascontiguousarray(rows, dtype=np.int32).reshape(-1)
             signs = np.ascontiguousarray(signs, dtype=np.int8).reshape(-1)
         # The kernels' ring stages (A chunk + plan block) must fit shared
@@ -84,7 +82,7 @@ class CountSketchPlan:
                 need = 2 * ((self.chunk + 2) * 8 + 2 * mx + 127)
             else:
                 lanes, off, mx = _native.countsketch_plan(rows, signs, self.d, self.chunk,
-                                                          self.warps)
+                                                          self.warps, spr=self.spr)
                 need = 3 * ((self.chunk + 2) * 8 + 4 * mx + 127) + (self.d + 1) * 8 + 256
             if need <= _SMEM_BUDGET or self.chunk <= 8:
                 break
@@ -128,7 +126,8 @@ class CountSketchPlan:
               partitions: int = 0, accumulate: int = 0, stream=None) -> None:
         """out[:, :n] (+)= S A, outb (+)= S b on the device (raw pointers or tensors)."""
         if getattr(self, "spr", 1) > 1:
-            _native.call("skl_sparsesign_dense_owned", _native.ptr(A), m, n, lda, _native.ptr(b),
+            fn = "skl_sparsesign_dense_owned" if self.kind == "owned" else "skl_sparsesign_dense"
+            _native.call(fn, _native.ptr(A), m, n, lda, _native.ptr(b),
                          _native.ptr(self.lanes), _native.ptr(self.off), self.max_block, self.d,
                          self.chunk, self.warps, self.scale, _native.ptr(out), ldo,
                          _native.ptr(outb), partitions, accumulate,
@@ -270,10 +269,8 @@ class SketchOperator:
         require_cuda()
         c = self._cache()
         if "plan" not in c and self.kind == "sparsesign":
-            if self.target_dim > _native.OWNED_MAX_D:
-                raise SpecError(f"sparse sign embeddings with embed_dim {self.target_dim} > "
-                                f"{_native.OWNED_MAX_D} are implemented for CSR operands only")
-            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim, kind="owned",
+            # register-owned plan up to d = 2048, shared-memory lane lists beyond
+            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim,
                                         spr=self.sparsity)
         if "plan" not in c:
             d = self.target_dim

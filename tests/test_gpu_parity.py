@@ -622,10 +622,36 @@ def test_sparsesign_saa_and_limits(golden, golden_meta):
     assert rel_fro(res.x.data, want["x"]) <= 1e-9
     assert abs(res.residual_norm - want["residual"]) <= 1e-10 * want["residual"]
     assert rel_fro(want["x"], golden["ss_cfg1_x"]) <= 1e-12
-    # dense operands with d > 2048 are not implemented for sparse sign embeddings
+    # dense operands with d > 2048: shared-memory lane-list plan, s entries per row
+    rng = np.random.default_rng(4)
+    A2 = rng.standard_normal((10_000, 3))
     op = E.build_sketch(E.SketchSpec("sparsesign", 4096, seed=1), 10_000)
-    with pytest.raises(E.SpecError):
-        E.apply_to_matrix(op, E.DenseMatrix(np.ones((10_000, 2))))
+    assert np.array_equal(E.apply_to_matrix(op, E.DenseMatrix(A2)).data, op.sparse_map @ A2)
+
+
+@pytest.mark.parametrize("m,n,d,s", [(30_000, 6, 3000, 8), (20_001, 3, 8192, 4), (5000, 2, 2049, 1),
+                                     (9000, 5, 4500, 16)])
+def test_sparsesign_dense_large_d_bitwise(m, n, d, s):
+    """Sparse sign embeddings with d > 2048 on dense operands (lane-list plan
+    with s entries per source row, SCALED kernel): bitwise to scipy."""
+    rng = np.random.default_rng(m + d)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec("sparsesign", d, seed=d, sparsity=s), m)
+    assert np.array_equal(E.apply_to_matrix(op, E.DenseMatrix(A)).data, op.sparse_map @ A)
+    assert np.array_equal(E.apply_to_vector(op, E.Vector(b)).data, op.sparse_map @ b)
+
+
+def test_sparsesign_saa_large_n():
+    """method "saa" with a sparse sign embedding at n = 600 (d = 2400 > 2048)."""
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((20_000, 600))
+    b = A @ rng.standard_normal(600) + 1e-3 * rng.standard_normal(20_000)
+    want = O.saa_solve(A, b, "sparsesign", 5, 4.0)
+    res = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "saa",
+                  E.SketchSpec("sparsesign", 1, seed=5), E.SolverOptions(d_factor=4.0))
+    assert res.d == 2400 == want["d"]
+    assert rel_fro(res.x.data, want["x"]) <= 1e-9
 
 
 def test_concurrent_solves_from_threads():
