@@ -452,14 +452,26 @@ static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaSt
 
 int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16_t* sbits,
                 const int64_t* sample, int64_t m_pad, int64_t d, double* SA, int64_t ldsa,
-                int64_t row_offset, int partitions, cudaStream_t st) {
+                int64_t row_offset, int partitions, cudaStream_t st, int64_t d_scale = 0) {
+  // d_scale: the embedding dimension the 1/sqrt(d) normalisation uses (the
+  // whole d when this launch covers a slice of the sampled rows)
+  if (d_scale <= 0) d_scale = d;
   const int64_t* sample_ = sample;
   SKL_REQUIRE(A && sbits && sample && SA && m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d,
               SKL_ERR_SHAPE, "srht: bad arguments");
   SKL_REQUIRE(m_pad >= 1 && (m_pad & (m_pad - 1)) == 0, SKL_ERR_SHAPE,
               "srht: padded dimension %lld is not a power of two", (long long)m_pad);
-  SKL_REQUIRE(d <= 32 * SR_NT, SKL_ERR_SPEC, "srht: embed_dim %lld > %d not supported",
-              (long long)d, 32 * SR_NT);
+  if (d > 32 * SR_NT) {
+    // more sampled rows than one launch holds in registers: one pass over A
+    // per 8192 output rows (each pass samples a slice of row_sample)
+    for (int64_t k0 = 0; k0 < d; k0 += 32 * SR_NT) {
+      const int64_t dk = std::min<int64_t>(32 * SR_NT, d - k0);
+      const int rc = srht_launch(A, m, n, lda, sbits, sample + k0, m_pad, dk, SA + k0, ldsa,
+                                 row_offset, partitions, st, d_scale);
+      if (rc) return rc;
+    }
+    return SKL_OK;
+  }
   SKL_REQUIRE(((uintptr_t)A & 15) == 0 && (lda % 2 == 0 || n == 1) && ((uintptr_t)sbits & 15) == 0,
               SKL_ERR_INVALID, "srht: A/signs must be 16-byte aligned with an even leading dimension");
   SKL_REQUIRE(m_pad <= 0x100000000LL, SKL_ERR_SPEC, "srht: padded dimension > 2^32");
@@ -501,7 +513,7 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   p.A = A; p.lda = lda; p.m = m; p.n = n; p.sbits = sbits; p.sample = sample; p.d = d; p.b = b;
   p.sw_block = sw_block;
   p.jhi0 = row_offset >> b; p.P = P; p.out = SA; p.ldo = ldsa; p.part = nullptr;
-  p.inv_scale_div = std::sqrt((double)d);
+  p.inv_scale_div = std::sqrt((double)d_scale);
   double* part = nullptr;
   if (P > 1) {
     SKL_CUDA(malloc_async(&part, (size_t)P * n * d * sizeof(double), st));
@@ -524,7 +536,7 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   if (P > 1) {
     const int64_t total = n * d;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4LL * sms);
-    srht_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, n, d, SA, ldsa, std::sqrt((double)d));
+    srht_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, n, d, SA, ldsa, std::sqrt((double)d_scale));
     SKL_CUDA_LAUNCH();
     SKL_CUDA(cudaFreeAsync(part, st));
   }

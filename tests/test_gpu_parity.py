@@ -710,3 +710,15 @@ def test_lsqr_with_preconditioner_and_callback():
     assert all(s[1] == (24,) for s in seen)
     rn = [s[2] for s in seen]
     assert all(rn[i + 1] <= rn[i] * (1 + 1e-12) for i in range(len(rn) - 1))
+
+
+@pytest.mark.parametrize("m,n,d", [(40_000, 3, 10_000), (20_000, 2, 16_385)])
+def test_srht_more_rows_than_one_launch(m, n, d):
+    """SRHT with d > 8192 sampled rows: one pass over A per 8192-row slice of
+    row_sample, all normalised by the whole 1/sqrt(d)."""
+    rng = np.random.default_rng(d)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    op = E.build_sketch(E.SketchSpec("srht", d, seed=2), m)
+    got = E.apply_to_matrix(op, E.DenseMatrix(A)).data
+    want, _ = O.sketch_apply("srht", O.operator_key(2, "srht", m), d, A)
+    assert rel_fro(got, want) <= 1e-13
