@@ -503,7 +503,17 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   SKL_REQUIRE(SA && ldsa >= d && bad_col && bad_val, SKL_ERR_INVALID, "qr_solve: bad arguments");
   SKL_REQUIRE(!R || ldr >= n, SKL_ERR_INVALID, "qr_solve: ldr < n");
   SKL_REQUIRE(!Q || ldq >= d, SKL_ERR_INVALID, "qr_solve: ldq < d");
-  SKL_REQUIRE(n <= (48 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
+  // the back-solves keep y (n doubles) in shared memory
+  SKL_REQUIRE(n <= (200 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
+  if (n * 8 > 48 * 1024) {
+    const int bytes = (int)(n * 8);
+    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_inv_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_blocked_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  }
 
   const int fro_blocks = 256;
   // the blocked factorisation (register cluster panels + GEMM-shaped

@@ -722,3 +722,18 @@ def test_srht_more_rows_than_one_launch(m, n, d):
     got = E.apply_to_matrix(op, E.DenseMatrix(A)).data
     want, _ = O.sketch_apply("srht", O.operator_key(2, "srht", m), d, A)
     assert rel_fro(got, want) <= 1e-13
+
+
+def test_qr_solve_wide_system():
+    """n above the 48 KB default shared-memory window of the back-solve
+    (n = 6400: y takes 51 KB)."""
+    from paper_2409_14309_b200.linalg import qr_solve_device
+
+    rng = np.random.default_rng(64)
+    d, n = 6600, 6400
+    M = rng.standard_normal((d, n)) + 4 * np.eye(d, n)
+    y = rng.standard_normal(d)
+    Md = torch.from_numpy(np.asfortranarray(M)).cuda()
+    x, _, _ = qr_solve_device(Md, d, torch.from_numpy(y).cuda(), d, n)
+    want = np.linalg.lstsq(M, y, rcond=None)[0]
+    assert rel_fro(x.cpu().numpy(), want) <= 1e-10
