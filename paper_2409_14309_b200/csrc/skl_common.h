@@ -47,7 +47,36 @@ int resolve_threads(int threads);
                cudaGetErrorString(e__), __FILE__, __LINE__);                    \
   } while (0)
 
+#include <atomic>
+#include <mutex>
+
 namespace skl {
+// SM count of the current device, cached per device (thread-safe).
+inline int sm_count_cached() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// Runs `f` once per device (thread-safe: concurrent first callers wait for
+// it to finish), for one-time setup such as kernel attributes.  Returns the
+// status of the run (later calls return SKL_OK).
+template <class F>
+inline int once_per_device(std::once_flag* flags /* [64] */, F&& f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return f();
+  int rc = 0;
+  std::call_once(flags[dev], [&] { rc = f(); });
+  return rc;
+}
+
 // Stream-ordered workspace allocation.  The first call on a device raises
 // the default memory pool's release threshold so freed workspaces stay
 // mapped across stream synchronisations (the default threshold of 0 unmaps
@@ -55,16 +84,16 @@ namespace skl {
 // QR's workspaces).
 template <class T>
 inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
-  static bool retained[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !retained[dev]) {
+  static std::once_flag retained[64];
+  once_per_device(retained, [] {
+    int dev = 0;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    retained[dev] = true;
-  }
+    return 0;
+  });
   return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
 }
 }  // namespace skl

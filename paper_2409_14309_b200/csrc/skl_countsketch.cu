@@ -379,17 +379,7 @@ __global__ void countsketch_reduce_kernel(const double* part, int P, int64_t nco
   }
 }
 
-static int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+static int sm_count() { return sm_count_cached(); }
 
 template <int NT, int C>
 static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStream_t st) {

@@ -257,16 +257,7 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
   }
 }
 
-static int sm_count_pb() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+static int sm_count_pb() { return sm_count_cached(); }
 
 }  // namespace skl
 

@@ -377,16 +377,7 @@ __global__ void __launch_bounds__(LT_NT) lsqr_xw_kernel(int n, double c1, double
   if (threadIdx.x == 0) *norm2 = t;
 }
 
-static int sm_count_lq() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+static int sm_count_lq() { return sm_count_cached(); }
 
 }  // namespace skl
 

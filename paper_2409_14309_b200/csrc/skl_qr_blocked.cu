@@ -730,9 +730,9 @@ static int qr_streams(QrStreams** out, size_t nev) {
 
 static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb, double* V,
                            double* Tblk, double* tau, double* beta, cudaStream_t st) {
-  static bool attr_set = false;
+  static std::once_flag attr_set[64];
   const int smem_max = (int)(QB_SMEM_EXTRA + QB_MAXROWS * QB_PLD) * (int)sizeof(double);
-  if (!attr_set) {
+  const int arc = once_per_device(attr_set, [&]() -> int {
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -741,8 +741,9 @@ static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     SKL_CUDA(cudaFuncSetAttribute(qr_panel_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    attr_set = true;
-  }
+    return SKL_OK;
+  });
+  if (arc) return arc;
   static const bool smem_panel = getenv("SKL_QR_SMEM_PANEL") != nullptr;
   // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
   static const int tail_rows = getenv("SKL_QR_PANEL_ROWS") ? atoi(getenv("SKL_QR_PANEL_ROWS")) : 128;
