@@ -249,8 +249,9 @@ def rng_srht(key: int, m_pad: int, d: int, threads: int = 0) -> tuple[np.ndarray
     return signs, sample
 
 
-# Register-owned plans cover d <= 128 * 16; larger embeddings use lane lists.
-OWNED_MAX_D = 2048
+# Register-owned plans cover d <= 16 warps x 32 lanes x 8 slots; larger
+# embeddings use lane lists (shared-memory bucket sums).
+OWNED_MAX_D = 4096
 OWNED_CHUNK = 8184   # rows per chunk (<= 8184: 13-bit row field incl. the zero slot)
 OWNED_SMALL_CHUNK = 4096  # short sources (<= 4 full chunks)
 LANES_CHUNK = 2048
@@ -258,7 +259,8 @@ LANES_CHUNK = 2048
 
 def plan_geometry(d: int, kind: str | None = None, m: int | None = None) -> tuple[str, int, int]:
     """(plan kind, chunk rows, consumer warps) of the CountSketch plan for
-    embed_dim d: "owned" (register-owned buckets) when d <= 2048, else
+    embed_dim d: "owned" (register-owned buckets, 4 or 8 per thread) when
+    d <= 4096, else
     "lanes" (shared-memory accumulators, lane lists).  ``kind`` forces one
     (tests exercise both kernels on the same operator).  Short sources (m
     rows, at most four full chunks) get half-size chunks: the kernel's ring
@@ -268,8 +270,12 @@ def plan_geometry(d: int, kind: str | None = None, m: int | None = None) -> tupl
     if kind == "owned":
         if d > OWNED_MAX_D:
             raise ValueError(f"owned plan needs d <= {OWNED_MAX_D}, got {d}")
-        chunk = OWNED_CHUNK if m is None or m > 4 * OWNED_CHUNK else OWNED_SMALL_CHUNK
-        return "owned", chunk, (8 if d <= 1024 else 16)
+        warps = 8 if d <= 1024 else 16
+        if d <= 2048:  # 4 slots per thread: 13-bit row field
+            chunk = OWNED_CHUNK if m is None or m > 4 * OWNED_CHUNK else OWNED_SMALL_CHUNK
+        else:  # 8 slots: 12-bit row field
+            chunk = 4088
+        return "owned", chunk, warps
     if kind != "lanes":
         raise ValueError(f"unknown plan kind {kind!r}")
     return "lanes", LANES_CHUNK, (16 if d >= 1024 else 8)

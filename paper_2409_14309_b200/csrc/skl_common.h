@@ -17,6 +17,21 @@ void clear_error();
 // Number of host worker threads for `threads` <= 0 requests.
 int resolve_threads(int threads);
 
+// Register-owned CountSketch plan geometry (skl_countsketch_plan_owned):
+// every consumer thread owns `slots` buckets (4 or 8: d <= 32 x warps x
+// slots), and the u16 entry word is row | slot << row_bits | negative << 15,
+// so the chunk (row field incl. the zero slot at index `chunk`) shrinks as
+// the slot field grows: 8184 or 4088 rows.  0: d too large.  (16 slots fit
+// the format too -- 2040-row chunks -- but were measured slower than the
+// lane-list kernel: short lane lists pad heavily and 16 predicated adds per
+// entry cost more issue slots than the shared-memory sums.)
+inline int owned_slots(int64_t d, int warps) {
+  const int64_t per = (d + 32 * (int64_t)warps - 1) / (32 * (int64_t)warps);
+  return per <= 4 ? 4 : per <= 8 ? 8 : 0;
+}
+inline int owned_row_bits(int slots) { return slots == 4 ? 13 : slots == 8 ? 12 : 11; }
+inline int64_t owned_max_chunk(int slots) { return (1LL << owned_row_bits(slots)) - 8; }
+
 }  // namespace skl
 
 #define SKL_FAIL(code, ...)          \

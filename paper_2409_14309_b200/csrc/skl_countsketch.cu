@@ -246,8 +246,29 @@ struct OwParams {
 // SCALED: every entry is (+-scale) * A[j] rounded once, as scipy's
 // csr_matvecs computes val * x for val = +-scale (sparse sign embeddings);
 // CountSketch entries are +-1 (exact sign flips, no multiply).
-template <int NT, bool SCALED>
+// Predicated add into slot K of the thread's accumulators: a branch around
+// the add, so ptxas emits a predicated DADD (an if-chain or predicated PTX
+// add comes out as DADD + FSEL select chains, 3x the issue slots).
+template <int K>
+__device__ __forceinline__ void ow_add(double& a, uint32_t slot, double x) {
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.ne.u32 q, %1, %3;\n\t@q bra SK%=;\n\tadd.rn.f64 %0, %0, %2;\n\tSK%=:\n\t}"
+      : "+d"(a)
+      : "r"(slot), "d"(x), "n"(K));
+}
+
+template <int SL, int K = 0>
+__device__ __forceinline__ void ow_add_all(double (&a)[SL], uint32_t slot, double x) {
+  if constexpr (K < SL) {
+    ow_add<K>(a[K], slot, x);
+    ow_add_all<SL, K + 1>(a, slot, x);
+  }
+}
+
+template <int NT, bool SCALED, int SL>
 __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwParams p) {
+  constexpr int RB = SL == 4 ? 13 : SL == 8 ? 12 : 11;  // owned_row_bits
+  constexpr uint32_t RMASK = (1u << RB) - 1u;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + OW_MAX_STAGES;
@@ -306,13 +327,14 @@ __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwP
 
   const int wid = tid >> 5, lane = tid & 31;
   // slot q of this thread owns bucket tid + q * NT
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double a[SL];
+#pragma unroll
+  for (int q = 0; q < SL; ++q) a[q] = 0.0;
   if (p.P == 1 && p.accumulate) {
     const double* src = col < p.n ? p.out + col * p.ldo : p.outb;
-    if (tid + 0 * NT < p.d) a0 = src[tid + 0 * NT];
-    if (tid + 1 * NT < p.d) a1 = src[tid + 1 * NT];
-    if (tid + 2 * NT < p.d) a2 = src[tid + 2 * NT];
-    if (tid + 3 * NT < p.d) a3 = src[tid + 3 * NT];
+#pragma unroll
+    for (int q = 0; q < SL; ++q)
+      if (tid + q * NT < p.d) a[q] = src[tid + q * NT];
   }
   int s = 0;
   uint32_t ph = 0;
@@ -325,20 +347,11 @@ __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwP
 #pragma unroll 4
     for (int r = r0; r < r1; ++r) {
       const uint32_t e = Lr[r * 32];
-      const uint2 w = *reinterpret_cast<const uint2*>(st + (e & 0x1fffu) * 8);
+      const uint2 w = *reinterpret_cast<const uint2*>(st + (e & RMASK) * 8);
       double x = __hiloint2double((int)(w.y ^ ((e & 0x8000u) << 16)), (int)w.x);
       if (SCALED) x = __dmul_rn(x, p.scale);
-      // Exactly one slot accumulates.  Written as branches around each add
-      // so ptxas emits four predicated DADDs (a C if-chain or predicated PTX
-      // adds come out as DADD + FSEL select chains, 3x the issue slots).
-      const uint32_t slot = e & 0x6000u;
-      asm("{\n\t.reg .pred q;\n\t"
-          "setp.ne.u32 q, %4, 0x0000;\n\t@q bra SK0%=;\n\tadd.rn.f64 %0, %0, %5;\n\tSK0%=:\n\t"
-          "setp.ne.u32 q, %4, 0x2000;\n\t@q bra SK1%=;\n\tadd.rn.f64 %1, %1, %5;\n\tSK1%=:\n\t"
-          "setp.ne.u32 q, %4, 0x4000;\n\t@q bra SK2%=;\n\tadd.rn.f64 %2, %2, %5;\n\tSK2%=:\n\t"
-          "setp.ne.u32 q, %4, 0x6000;\n\t@q bra SK3%=;\n\tadd.rn.f64 %3, %3, %5;\n\tSK3%=:\n\t}"
-          : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3)
-          : "r"(slot), "d"(x));
+      // exactly one slot accumulates (predicated DADDs, see ow_add)
+      ow_add_all<SL>(a, (e >> RB) & (SL - 1), x);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -347,18 +360,17 @@ __global__ void __launch_bounds__(NT + 32, 2) countsketch_owned_kernel(const OwP
       ph ^= 1u;
     }
   }
-  const double av[4] = {a0, a1, a2, a3};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < SL; ++q) {
     const int bkt = tid + q * NT;
     if (bkt >= p.d) continue;
     if (p.P == 1) {
       if (col < p.n)
-        p.out[col * p.ldo + bkt] = av[q];
+        p.out[col * p.ldo + bkt] = a[q];
       else
-        p.outb[bkt] = av[q];
+        p.outb[bkt] = a[q];
     } else {
-      p.part[((int64_t)blockIdx.y * p.ncols + col) * p.d + bkt] = av[q];
+      p.part[((int64_t)blockIdx.y * p.ncols + col) * p.d + bkt] = a[q];
     }
   }
 }
@@ -480,6 +492,37 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
   return SKL_OK;
 }
 
+template <int NT, bool SC, int SL>
+static cudaError_t launch_owned(const OwParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  auto k = countsketch_owned_kernel<NT, SC, SL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  k<<<grid, NT + 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int NT, bool SC>
+static cudaError_t dispatch_owned_sl(int nsl, const OwParams& p, dim3 grid, size_t smem,
+                                     cudaStream_t st) {
+  switch (nsl) {
+    case 4: return launch_owned<NT, SC, 4>(p, grid, smem, st);
+    case 8: return launch_owned<NT, SC, 8>(p, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+static cudaError_t dispatch_owned(int nt, int nsl, bool scaled, const OwParams& p, dim3 grid,
+                                  size_t smem, cudaStream_t st) {
+  if (nt == 512)
+    return scaled ? dispatch_owned_sl<512, true>(nsl, p, grid, smem, st)
+                  : dispatch_owned_sl<512, false>(nsl, p, grid, smem, st);
+  return scaled ? dispatch_owned_sl<256, true>(nsl, p, grid, smem, st)
+                : dispatch_owned_sl<256, false>(nsl, p, grid, smem, st);
+}
+
 static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64_t lda,
                                     const double* b, const uint16_t* lanes,
                                     const int64_t* chunk_off, int64_t max_block, int64_t d,
@@ -489,9 +532,10 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld", (long long)m, (long long)n,
               (long long)d);
-  SKL_REQUIRE((warps == 8 || warps == 16) && d <= (int64_t)warps * 128, SKL_ERR_SPEC,
+  const int nsl = owned_slots(d, warps);
+  SKL_REQUIRE((warps == 8 || warps == 16) && nsl > 0, SKL_ERR_SPEC,
               "countsketch (owned): d=%lld does not fit %d warps", (long long)d, warps);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 8184 && chunk % 8 == 0, SKL_ERR_INVALID,
+  SKL_REQUIRE(chunk >= 8 && chunk <= owned_max_chunk(nsl) && chunk % 8 == 0, SKL_ERR_INVALID,
               "countsketch: bad plan chunk %lld", (long long)chunk);
   SKL_REQUIRE(A && lanes && chunk_off && SA && (!b || Sb) && max_block > 0, SKL_ERR_INVALID,
               "countsketch: null pointer");
@@ -533,29 +577,8 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
     p.part = part;
   }
   dim3 grid((unsigned)ncols, (unsigned)P);
-  cudaError_t e;
   const bool scaled = scale != 1.0;
-  if (warps == 16) {
-    auto k = scaled ? countsketch_owned_kernel<512, true> : countsketch_owned_kernel<512, false>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) {
-      k<<<grid, 512 + 32, smem, st>>>(p);
-      e = cudaGetLastError();
-    }
-  } else {
-    auto k = scaled ? countsketch_owned_kernel<256, true> : countsketch_owned_kernel<256, false>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) {
-      k<<<grid, 256 + 32, smem, st>>>(p);
-      e = cudaGetLastError();
-    }
-  }
+  const cudaError_t e = dispatch_owned(warps == 16 ? 512 : 256, nsl, scaled, p, grid, smem, st);
   if (e != cudaSuccess) {
     if (part) cudaFreeAsync(part, st);
     SKL_FAIL(SKL_ERR_CUDA, "countsketch (owned) launch failed: %s", cudaGetErrorString(e));

@@ -71,7 +71,6 @@ __global__ void cs_signs_kernel(uint64_t key, int64_t m, uint64_t pos0, int8_t* 
 }
 
 constexpr int PB_NT = 512;
-constexpr int PB_SLOTS = 4;
 constexpr int PB_KEYS = 8192;  // chunk <= 8184 rows (+ pads), power of two
 
 __device__ __forceinline__ int pb_head(int warps) { return (warps + 1 + 7) / 8 * 8; }
@@ -79,7 +78,7 @@ __device__ __forceinline__ int pb_head(int warps) { return (warps + 1 + 7) / 8 *
 // Pass 1: per-warp list lengths and block size of every chunk.
 __global__ void __launch_bounds__(PB_NT) owned_sizes_kernel(const int32_t* __restrict__ rows,
                                                             int64_t m, int d, int chunk, int warps,
-                                                            int32_t* __restrict__ maxlen,
+                                                            int nsl, int32_t* __restrict__ maxlen,
                                                             int64_t* __restrict__ sizes) {
   extern __shared__ int32_t cnt[];  // [d]
   __shared__ int32_t wmax[32];
@@ -92,8 +91,7 @@ __global__ void __launch_bounds__(PB_NT) owned_sizes_kernel(const int32_t* __res
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int w = wid; w < warps; w += PB_NT / 32) {
     int tot = 0;
-#pragma unroll
-    for (int s = 0; s < PB_SLOTS; ++s) {
+    for (int s = 0; s < nsl; ++s) {
       const int b = w * 32 + lane + s * 32 * warps;
       if (b < d) tot += cnt[b];
     }
@@ -127,6 +125,7 @@ __global__ void owned_scan_kernel(const int64_t* __restrict__ sizes, int64_t nch
 }
 
 // Pass 2: the plan words of every chunk (same format and greedy as the host).
+template <int SL>
 __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
     const int32_t* __restrict__ rows, const int8_t* __restrict__ signs, int64_t m, int d,
     int chunk, int warps, const int32_t* __restrict__ maxlen, const int64_t* __restrict__ off,
@@ -188,10 +187,10 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
     const int ml = maxlen[k * warps + w];
     uint16_t* R = blk + head + (int64_t)rowbase * 32;
     // lane l's four slot lists: next row (register), entries left
-    int nxt[PB_SLOTS], cb[PB_SLOTS], st[PB_SLOTS];
-    uint32_t cand[PB_SLOTS];
+    int nxt[SL], cb[SL], st[SL];
+    uint32_t cand[SL];
 #pragma unroll
-    for (int s = 0; s < PB_SLOTS; ++s) {
+    for (int s = 0; s < SL; ++s) {
       const int b = w * 32 + lane + s * 32 * warps;
       cb[s] = b < d ? cnt[b] : 0;
       st[s] = b < d ? start[b] : 0;
@@ -212,7 +211,7 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
           int bload = 1 << 30;
           int bleft = 0;
 #pragma unroll
-          for (int s = 0; s < PB_SLOTS; ++s) {
+          for (int s = 0; s < SL; ++s) {
             if (nxt[s] >= cb[s]) continue;
             const int bank = (int)(cand[s] & 15);
             const uint32_t word4 = bank < 8 ? (bank < 4 ? ld4[0] : ld4[1])
@@ -227,8 +226,11 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
           }
           mine = choice;
         }
-        const int bank_l = __shfl_sync(0xffffffffu,
-                                       choice >= 0 ? (int)(cand[choice & 3] & 15) : -1, l);
+        int cbank = -1;
+#pragma unroll
+        for (int s = 0; s < SL; ++s)
+          if (s == choice) cbank = (int)(cand[s] & 15);
+        const int bank_l = __shfl_sync(0xffffffffu, cbank, l);
         if (bank_l >= 0) {
           const uint32_t inc = 1u << (8 * (bank_l & 3));
           if (bank_l < 4)
@@ -243,10 +245,14 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
       }
       uint16_t word = pad;
       if (mine >= 0) {
-        const uint32_t jrow = cand[mine & 3];
-        word = (uint16_t)(jrow | ((uint32_t)mine << 13) | ((sg[jrow] < 0 ? 1u : 0u) << 15));
+        constexpr int RB = SL == 4 ? 13 : SL == 8 ? 12 : 11;  // owned_row_bits
+        uint32_t jrow = 0;
 #pragma unroll
-        for (int s = 0; s < PB_SLOTS; ++s)
+        for (int s = 0; s < SL; ++s)
+          if (s == mine) jrow = cand[s];
+        word = (uint16_t)(jrow | ((uint32_t)mine << RB) | ((sg[jrow] < 0 ? 1u : 0u) << 15));
+#pragma unroll
+        for (int s = 0; s < SL; ++s)
           if (s == mine) {
             ++nxt[s];
             cand[s] = nxt[s] < cb[s] ? (keys[st[s] + nxt[s]] & 0x1fffu) : 0u;
@@ -319,18 +325,21 @@ extern "C" int skl_countsketch_plan_owned_device(const int32_t* rows, const int8
   cudaStream_t st = (cudaStream_t)stream;
   SKL_REQUIRE(rows && signs && chunk_off && maxlen && m >= 1 && d >= 1, SKL_ERR_INVALID,
               "plan_owned_device: bad arguments");
-  SKL_REQUIRE(warps >= 1 && warps <= 16 && d <= (int64_t)warps * 32 * PB_SLOTS, SKL_ERR_SPEC,
-              "owned plan: embed_dim %lld needs more than %d warps x 32 lanes x %d slots",
-              (long long)d, warps, PB_SLOTS);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 8184 && chunk % 8 == 0, SKL_ERR_INVALID,
-              "owned plan chunk must be a multiple of 8 in [8, 8184], got %lld", (long long)chunk);
+  const int nsl = owned_slots(d, warps);
+  SKL_REQUIRE(warps >= 1 && warps <= 16 && nsl > 0, SKL_ERR_SPEC,
+              "owned plan: embed_dim %lld needs more than %d warps x 32 lanes x 16 slots",
+              (long long)d, warps);
+  const int64_t cmax = owned_max_chunk(nsl);
+  SKL_REQUIRE(chunk >= 8 && chunk <= cmax && chunk % 8 == 0, SKL_ERR_INVALID,
+              "owned plan chunk must be a multiple of 8 in [8, %lld], got %lld", (long long)cmax,
+              (long long)chunk);
   const int64_t nch = (m + chunk - 1) / chunk;
   if (!lanes) {
     SKL_REQUIRE(total_and_max, SKL_ERR_INVALID, "plan_owned_device: total_and_max missing");
     int64_t* sizes = nullptr;
     SKL_CUDA(malloc_async(&sizes, (size_t)(nch + 1) * sizeof(int64_t), st));
     owned_sizes_kernel<<<(unsigned)nch, PB_NT, (size_t)d * sizeof(int32_t), st>>>(
-        rows, m, (int)d, (int)chunk, warps, maxlen, sizes);
+        rows, m, (int)d, (int)chunk, warps, nsl, maxlen, sizes);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) {
       owned_scan_kernel<<<1, 32, 0, st>>>(sizes, nch, chunk_off, sizes + nch);
@@ -349,10 +358,10 @@ extern "C" int skl_countsketch_plan_owned_device(const int32_t* rows, const int8
     return SKL_OK;
   }
   const size_t smem = (size_t)PB_KEYS * 4 + (size_t)d * 8 + (size_t)chunk;
-  SKL_CUDA(cudaFuncSetAttribute(owned_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  owned_fill_kernel<<<(unsigned)nch, PB_NT, smem, st>>>(rows, signs, m, (int)d, (int)chunk, warps,
-                                                        maxlen, chunk_off, lanes);
+  auto fill = nsl == 4 ? owned_fill_kernel<4> : owned_fill_kernel<8>;
+  SKL_CUDA(cudaFuncSetAttribute(fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill<<<(unsigned)nch, PB_NT, smem, st>>>(rows, signs, m, (int)d, (int)chunk, warps, maxlen,
+                                           chunk_off, lanes);
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }

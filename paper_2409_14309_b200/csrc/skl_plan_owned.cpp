@@ -6,7 +6,8 @@
 // bucket's running sum in a register, so the device kernel never stages
 // accumulators in shared memory.  The strided map spreads any d evenly over
 // the warps.
-// Per chunk, a lane's list is the union of its four buckets' rows; rows of
+// Per chunk, a lane's list is the union of its 4, 8 or 16 buckets' rows
+// (slots = ceil(d / 32 W) rounded up to a power of two); rows of
 // one bucket stay in ascending order (scipy csr_matvecs' fold order, so the
 // result is bitwise-equal to the reference), while the four streams are
 // interleaved step by step to spread the warp's 32 shared-memory gathers
@@ -22,7 +23,7 @@
 
 namespace {
 
-constexpr int kSlots = 4;
+constexpr int kMaxSlots = 8;
 
 template <class F>
 void par_for(int64_t n, int threads, F&& f) {
@@ -74,6 +75,8 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr
       S.sorted[S.pos[(size_t)rows[e]]++] = (uint16_t)(j | ((signs[e] < 0 ? 1u : 0u) << 15));
     }
   const int64_t head = head_words(warps);
+  const int nsl = skl::owned_slots(d, warps), rb = skl::owned_row_bits(nsl);
+  const uint32_t rmask = (1u << rb) - 1u;
   const uint16_t pad = (uint16_t)chunk;  // zero slot, slot 0, positive
   int64_t total_rows = 0;
   for (int w = 0; w < warps; ++w) {
@@ -81,7 +84,7 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr
     int maxlen = 0;
     for (int l = 0; l < 32; ++l) {
       int n = 0;
-      for (int s = 0; s < kSlots; ++s) {
+      for (int s = 0; s < nsl; ++s) {
         const int64_t b = (int64_t)w * 32 + l + (int64_t)s * 32 * warps;
         if (b < d) n += (int)S.cnt[(size_t)b];
       }
@@ -89,15 +92,15 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr
     }
     if (blk) {
       uint16_t* R = blk + head + total_rows * 32;
-      uint32_t nxt[32][kSlots];  // next entry index per lane and slot
+      uint32_t nxt[32][kMaxSlots];  // next entry index per lane and slot
       for (int l = 0; l < 32; ++l)
-        for (int s = 0; s < kSlots; ++s) nxt[l][s] = 0;
+        for (int s = 0; s < kMaxSlots; ++s) nxt[l][s] = 0;
       for (int step = 0; step < maxlen; ++step) {
         int load[16] = {0};
         for (int l = 0; l < 32; ++l) {
           int best = -1, bload = 1 << 30;
           uint32_t bleft = 0;
-          for (int s = 0; s < kSlots; ++s) {
+          for (int s = 0; s < nsl; ++s) {
             const int64_t b = (int64_t)w * 32 + l + (int64_t)s * 32 * warps;
             if (b >= d || nxt[l][s] >= S.cnt[(size_t)b]) continue;
             const uint32_t j = S.sorted[S.start[(size_t)b] + nxt[l][s]] & 0x1fffu;
@@ -113,9 +116,9 @@ int64_t owned_chunk(const int32_t* rows, const int8_t* signs, int64_t m, int spr
           if (best >= 0) {
             const int64_t b = (int64_t)w * 32 + l + (int64_t)best * 32 * warps;
             const uint32_t e = S.sorted[S.start[(size_t)b] + nxt[l][best]++];
-            const uint32_t j = e & 0x1fffu;
+            const uint32_t j = e & rmask;
             load[j & 15]++;
-            word = (uint16_t)(j | ((uint32_t)best << 13) | (e & 0x8000u));
+            word = (uint16_t)(j | ((uint32_t)best << rb) | (e & 0x8000u));
           }
           R[(size_t)step * 32 + l] = word;
         }
@@ -133,11 +136,13 @@ int plan_owned(const int32_t* rows, const int8_t* signs, int64_t m, int spr, int
                       int threads) {
   SKL_REQUIRE(rows && signs && chunk_off && m >= 1 && d >= 1 && spr >= 1, SKL_ERR_INVALID,
               "owned plan: bad arguments");
-  SKL_REQUIRE(warps >= 1 && warps <= 31 && d <= (int64_t)warps * 32 * kSlots, SKL_ERR_SPEC,
+  SKL_REQUIRE(warps >= 1 && warps <= 31 && skl::owned_slots(d, warps) > 0, SKL_ERR_SPEC,
               "owned plan: embed_dim %lld needs more than %d warps x 32 lanes x %d slots",
-              (long long)d, warps, kSlots);
-  SKL_REQUIRE(chunk >= 8 && chunk <= 8184 && chunk % 8 == 0, SKL_ERR_INVALID,
-              "owned plan chunk must be a multiple of 8 in [8, 8184], got %lld", (long long)chunk);
+              (long long)d, warps, kMaxSlots);
+  const int64_t cmax = skl::owned_max_chunk(skl::owned_slots(d, warps));
+  SKL_REQUIRE(chunk >= 8 && chunk <= cmax && chunk % 8 == 0, SKL_ERR_INVALID,
+              "owned plan chunk must be a multiple of 8 in [8, %lld], got %lld", (long long)cmax,
+              (long long)chunk);
   const int64_t nch = (m + chunk - 1) / chunk;
   threads = skl::resolve_threads(threads);
   std::vector<int64_t> sz((size_t)nch);

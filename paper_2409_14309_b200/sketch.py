@@ -55,7 +55,7 @@ _SMEM_BUDGET = 226 * 1024
 class CountSketchPlan:
     """Device form of a CountSketch's hashes for the dense apply kernels.
 
-    kind "owned" (d <= 2048): each bucket's running sum lives in a register
+    kind "owned" (d <= 4096): each bucket's running sum lives in a register
     of one lane for the whole apply (skl_countsketch_dense_owned);
     kind "lanes" (larger d): shared-memory accumulators fed by per-lane
     lists (skl_countsketch_dense).  Either way the per-bucket fold order is
@@ -269,7 +269,7 @@ class SketchOperator:
         require_cuda()
         c = self._cache()
         if "plan" not in c and self.kind == "sparsesign":
-            # register-owned plan up to d = 2048, shared-memory lane lists beyond
+            # register-owned plan up to d = 4096, shared-memory lane lists beyond
             c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim,
                                         spr=self.sparsity)
         if "plan" not in c:
