@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParam
 // memory (each warp load is one coalesced 256-byte segment), flips signs
 // from its own 64-bit word, and runs the 12 butterfly stages as
 //   bits 6..11 : in registers (over i),
-//   one shared-memory transpose (XOR-swizzled, conflict-free both ways):
+//   one shared-memory transpose (rows padded to 65 doubles: conflict-free
+//                both ways, immediate offsets):
 //                thread t then holds e = 64 t + i,
 //   bits 0..5  : in registers.
 // Each thread writes back only elements some output row samples, and the
@@ -259,15 +260,22 @@ __global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParam
 constexpr int SR2_G = 2;              // blocks (64-thread groups) per CTA
 constexpr int SR2_NT = 64 * SR2_G;
 
-__device__ __forceinline__ int sr2_swz(int e) { return e ^ ((e >> 6) & 31); }
+// Work buffer: a 64 x 64 tile with rows padded to 65 doubles.  Element
+// e = 64 r + c lives at 65 r + c, so both the row-order writes (fixed r,
+// consecutive c) and the column-order reads (fixed c, consecutive r) of a warp
+// hit every bank pair once, and every access is a thread base plus an
+// immediate offset (no per-element address arithmetic).
+constexpr int SR2_LD = 65;
+constexpr int SR2_BUF = 64 * SR2_LD;
+__device__ __forceinline__ int sr2_pad(int e) { return e + (e >> 6); }
 
 template <int KPT>
 __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
-  extern __shared__ __align__(16) double work2[];  // [SR2_G][4096], then sps[KPT * SR2_NT]
+  extern __shared__ __align__(16) double work2[];  // [SR2_G][SR2_BUF], then sps[KPT * SR2_NT]
   __shared__ uint32_t sbm[SR_BMAX / 32];
-  uint32_t* sps = reinterpret_cast<uint32_t*>(work2 + SR2_G * SR_BMAX);  // sample positions
+  uint32_t* sps = reinterpret_cast<uint32_t*>(work2 + SR2_G * SR2_BUF);  // sample positions
   const int tid = threadIdx.x, g = tid >> 6, t = tid & 63;
-  double* wk = work2 + g * SR_BMAX;
+  double* wk = work2 + g * SR2_BUF;
   const int64_t col = blockIdx.x;
   const int64_t nblk = (p.m + SR_BMAX - 1) / SR_BMAX;
   const int64_t q0 = nblk * blockIdx.y / p.P, q1 = nblk * (blockIdx.y + 1) / p.P;
@@ -353,10 +361,10 @@ __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
         }
     __syncthreads();  // the previous iteration's gathers are done with wk
 #pragma unroll
-    for (int i = 0; i < 64; ++i) wk[sr2_swz(t + 64 * i)] = v[i];
+    for (int i = 0; i < 64; ++i) wk[SR2_LD * i + t] = v[i];
     asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");  // group barrier
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = wk[sr2_swz(64 * t + i)];
+    for (int i = 0; i < 64; ++i) v[i] = wk[SR2_LD * t + i];
     // bits 0..5
 #pragma unroll
     for (int h = 1; h < 64; h <<= 1)
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
     // owner-only rewrite of the sampled elements (no barrier needed)
 #pragma unroll
     for (int i = 0; i < 64; ++i)
-      if ((smask >> i) & 1ull) wk[sr2_swz(64 * t + i)] = v[i];
+      if ((smask >> i) & 1ull) wk[SR2_LD * t + i] = v[i];
     load(qb + SR2_G + g);  // next blocks stream in under the gather
     __syncthreads();
 #pragma unroll
@@ -378,11 +386,11 @@ __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
       const int64_t qq = qb + gg;
       if (qq >= q1) break;
       const uint32_t jhi = (uint32_t)(p.jhi0 + qq);
-      const double* w = work2 + gg * SR_BMAX;
+      const double* w = work2 + gg * SR2_BUF;
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         const uint32_t ps = sps[k * SR2_NT + tid];
-        const double y = w[sr2_swz((int)(ps & (SR_BMAX - 1)))];
+        const double y = w[sr2_pad((int)(ps & (SR_BMAX - 1)))];
         const uint32_t flip = (uint32_t)(__popc((ps >> 12) & jhi) & 1) << 31;
         acc[k] += __hiloint2double(__double2hiint(y) ^ (int)flip, __double2loint(y));
       }
@@ -437,7 +445,7 @@ static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaSt
   if (p.b == 12) {  // full blocks: register-resident kernel, KPT = d / 128 per thread
     constexpr int K2 = KPT * SR_NT / SR2_NT;
     auto kern = srht_reg_kernel<K2>;
-    const int sm2 = SR2_G * SR_BMAX * 8 + 2 * K2 * SR2_NT * 4;
+    const int sm2 = SR2_G * SR2_BUF * 8 + 2 * K2 * SR2_NT * 4;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     if (e != cudaSuccess) return e;
     kern<<<grid, SR2_NT, sm2, st>>>(p);
