@@ -238,6 +238,15 @@ int skl_lsqr_gemv_n(const double* A, int64_t m, int64_t n, int64_t lda, const do
 int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t lda, const double* u_raw,
                     double beta, double* u_n, double* z, double* work, unsigned int* counters,
                     void* stream);
+/* Both products of one step in one pass over A (n <= 256):
+ * u = r_prev / beta_prev (r_prev NULL: no alpha term), r_out = s (A y) -
+ * alpha u, *norm2 = ||r_out||^2 and z = A^T r_out / ||r_out|| (z = 0 when
+ * r_out = 0).  `work` holds skl_lsqr_fused_work_size(n) doubles; `counters`
+ * as for the other LSQR kernels. */
+int64_t skl_lsqr_fused_work_size(int64_t n);
+int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda, const double* y, double s,
+                   double alpha, const double* r_prev, double beta_prev, double* r_out, double* z,
+                   double* norm2, double* work, unsigned int* counters, void* stream);
 /* v_out = R^-T z - beta v_prev, *norm2 = ||v_out||^2 (R NULL: identity). */
 int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z, double beta,
                     const double* v_prev, double* v_out, double* norm2, void* stream);

@@ -11,6 +11,7 @@ reference's code, line for line, on host floats read back once per step.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -51,6 +52,18 @@ class DenseOperator:
         _native.call("skl_lsqr_gemv_t", _native.ptr(self.A), self.m, self.n, self.lda,
                      _native.ptr(u_raw), beta, _native.ptr(u_n), _native.ptr(z),
                      _native.ptr(ws.work), _native.ptr(ws.counters), st)
+
+    def fusable(self) -> bool:
+        """Both products in one pass (skl_lsqr_fused): n <= 256, A 16-byte
+        aligned with an even leading dimension."""
+        return (self.n <= 256 and self.lda % 2 == 0 and self.A.data_ptr() % 16 == 0
+                and not os.environ.get("SKL_LSQR_TWO_PASS"))
+
+    def fused(self, y, alpha, r_prev, beta_prev, r_out, z, norm2, work, ws, st):
+        _native.call("skl_lsqr_fused", _native.ptr(self.A), self.m, self.n, self.lda,
+                     _native.ptr(y), 1.0, alpha, _native.ptr(r_prev), beta_prev,
+                     _native.ptr(r_out), _native.ptr(z), _native.ptr(norm2), _native.ptr(work),
+                     _native.ptr(ws.counters), st)
 
 
 class CsrOperator:
@@ -145,21 +158,36 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
     if alfa * beta == 0.0:
         return ws.x, 0, 0  # b or A^T b is zero: x = 0 exactly (solvers.py:176-189)
 
+    # one pass over A per step where the operator allows it: u = r_prev /
+    # beta_prev is formed inside the pass, A^T u comes out of the same pass
+    fused = isinstance(op, DenseOperator) and op.fusable()
+    if fused:
+        fwork = device_f64((int(_native.lib().skl_lsqr_fused_work_size(n)),))
+        r_prev, r_out, beta_prev = ws.u_raw, ws.u, beta
+
     while itn < max_iter:
         itn += 1
-        # u = mv(v) - alfa u ; beta = ||u||
-        op.mv(ws.y, 1.0, alfa, ws.u, ws.u_raw, sc[0:1], ws, st)
-        beta = math.sqrt(read(0))
+        if fused:
+            # u = r_prev / beta_prev ; r = mv(v) - alfa u ; beta = ||r|| ; z = rmv(r / beta)
+            op.fused(ws.y, alfa, r_prev, beta_prev, r_out, ws.z, sc[0:1], fwork, ws, st)
+            beta = math.sqrt(read(0))
+            r_prev, r_out = r_out, r_prev
+            beta_prev = beta if beta > 0 else 1.0  # u stays unnormalised (solvers.py:193)
+        else:
+            # u = mv(v) - alfa u ; beta = ||u||
+            op.mv(ws.y, 1.0, alfa, ws.u, ws.u_raw, sc[0:1], ws, st)
+            beta = math.sqrt(read(0))
         if beta > 0:
             anorm = math.sqrt(anorm**2 + alfa**2 + beta**2)
             # u /= beta ; v = rmv(u) - beta v ; alfa = ||v|| ; v /= alfa
-            op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
+            if not fused:
+                op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
             _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), beta, P(ws.v), P(ws.v_raw),
                          P(sc[1:2]), st)
             alfa = math.sqrt(read(1))
             _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa, P(ws.v_raw), P(ws.y), st)
             ws.v, ws.v_raw = ws.v_raw, ws.v
-        else:
+        elif not fused:
             ws.u, ws.u_raw = ws.u_raw, ws.u  # u stays unnormalised (solvers.py:193)
         if not (math.isfinite(alfa) and math.isfinite(beta)):
             raise NumericalBreakdownError(

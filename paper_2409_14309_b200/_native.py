@@ -133,6 +133,13 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr],
     ),
+    "skl_lsqr_fused_work_size": (c_i64, [c_i64]),
+    "skl_lsqr_fused": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, ctypes.c_double, ctypes.c_double, c_ptr, ctypes.c_double,
+         c_ptr, c_ptr,
+         c_ptr, c_ptr, c_ptr, c_ptr],
+    ),
     "skl_qr_solve": (
         c_int,
         [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr,

@@ -193,6 +193,141 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_gemv_t_kernel(
   if (threadIdx.x == 0) counters[g] = 0u;
 }
 
+// ---- one pass over A per iteration (n <= 256) ----------------------------
+// The reference's two products of one LSQR step share a pass over A:
+//   u     = u_raw_prev / beta_prev                 (the previous `u /= beta`)
+//   r     = s * (A y) - alpha * u ; ||r||^2         (the next u_raw)
+//   z     = (A^T r) / sqrt(||r||^2)                 (= A^T (r / beta))
+// A CTA takes 64-row blocks; warp g owns columns g, g+8, ... (NC of them)
+// and lane l rows 2l, 2l+1 of the block.  Phase 1 folds each row's dot
+// product over the warp's columns, the eight warp partials are added in
+// warp order; phase 2 multiplies the same values, still in registers, by
+// the block's r, and every lane keeps per-column partial sums of A^T r in
+// registers across all of its CTA's blocks.  The per-CTA partials are folded
+// in CTA order by the last CTA, so the result is deterministic; the
+// rounding differs from the two-pass kernels only in the summation order of
+// the products and in dividing A^T r (instead of r) by beta.
+constexpr int LF_RB = 64;  // rows per block
+template <int NC>
+__global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
+    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ y,
+    double s, double alpha, const double* __restrict__ r_prev, double beta_prev,
+    double* __restrict__ r_out, double* __restrict__ zpart, double* __restrict__ npart,
+    double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter) {
+  __shared__ double ys[8 * NC];
+  __shared__ double pdot[8][LF_RB];
+  __shared__ double rs[LF_RB];
+  __shared__ double red[32];
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+  for (int c = tid; c < 8 * NC; c += LQ_NT) ys[c] = c < n ? y[c] : 0.0;
+  double zacc[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) zacc[q] = 0.0;
+  double ss = 0.0;
+  __syncthreads();
+  const int64_t nblk = (m + LF_RB - 1) / LF_RB;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t i0 = blk * LF_RB + 2 * lane;
+    const bool full = i0 + 1 < m;
+    // the block's A values stay in registers for both phases: all NC loads
+    // are in flight at once and nothing is read twice
+    double2 v[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int c = g + 8 * q;
+      v[q] = make_double2(0.0, 0.0);
+      if (c < n) {
+        if (full) {
+          v[q] = __ldcs(reinterpret_cast<const double2*>(A + c * lda + i0));
+        } else if (i0 < m) {
+          v[q].x = A[c * lda + i0];
+        }
+      }
+    }
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int c = g + 8 * q;
+      if (c < n) {
+        a0 = fma(v[q].x, ys[c], a0);
+        a1 = fma(v[q].y, ys[c], a1);
+      }
+    }
+    pdot[g][2 * lane] = a0;
+    pdot[g][2 * lane + 1] = a1;
+    __syncthreads();
+    if (tid < LF_RB) {
+      const int64_t i = blk * LF_RB + tid;
+      double r = 0.0;
+      if (i < m) {
+        double dot = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) dot += pdot[w][tid];
+        r = s * dot - (r_prev ? alpha * (r_prev[i] / beta_prev) : 0.0);
+        r_out[i] = r;
+        ss = fma(r, r, ss);
+      }
+      rs[tid] = r;
+    }
+    __syncthreads();
+    const double r0 = rs[2 * lane], r1 = rs[2 * lane + 1];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) zacc[q] = fma(v[q].y, r1, fma(v[q].x, r0, zacc[q]));
+    __syncthreads();  // pdot / rs reused by the next block
+  }
+  // per-CTA partials: column sums over the lanes, the norm over the CTA
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double t = zacc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    const int c = g + 8 * q;
+    if (lane == 0 && c < n) zpart[(int64_t)blockIdx.x * n + c] = t;
+  }
+  const double tn = lq_block_sum(ss, red);
+  if (tid == 0) npart[blockIdx.x] = tn;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double nb;
+  // fixed-order folds; loads are batched (L2, bypassing L1) so that their
+  // latency is paid once per batch, not once per partial
+  constexpr int FB = 16;
+  if (tid == 0) {
+    double sn = 0.0;
+    for (unsigned b0 = 0; b0 < gridDim.x; b0 += FB) {
+      double t[FB];
+#pragma unroll
+      for (int q = 0; q < FB; ++q) t[q] = b0 + q < gridDim.x ? __ldcg(npart + b0 + q) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        if (b0 + q < gridDim.x) sn += t[q];
+    }
+    *norm2 = sn;
+    nb = sqrt(sn);
+    *counter = 0u;
+  }
+  __syncthreads();
+  const double beta = nb;
+  for (int c = tid; c < n; c += LQ_NT) {
+    double sz = 0.0;
+    for (unsigned b0 = 0; b0 < gridDim.x; b0 += FB) {
+      double t[FB];
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        t[q] = b0 + q < gridDim.x ? __ldcg(zpart + (int64_t)(b0 + q) * n + c) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        if (b0 + q < gridDim.x) sz += t[q];
+    }
+    z[c] = beta > 0.0 ? sz / beta : 0.0;
+  }
+}
+
 // ---- CSR operands -------------------------------------------------------
 // u_out = s * (A y) - alpha * u_in, ||u_out||^2 for CSR A: one row per
 // thread, the row's nonzeros folded in stored order from 0 (csr_matvec).
@@ -439,6 +574,50 @@ extern "C" int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t ld
   SKL_CUDA_LAUNCH();
   lsqr_gemv_t_kernel<<<dim3((unsigned)groups, (unsigned)nrc), LQ_NT, 0, (cudaStream_t)stream>>>(
       A, m, n, lda, u_n, rows_per, work, z, counters);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+// One pass: r_out = s A y - alpha (r_prev / beta_prev), ||r_out||^2 and
+// z = A^T r_out / ||r_out|| (see lsqr_fused_kernel).  n <= 256; r_prev may
+// be null (no alpha term).  `work` needs skl_lsqr_fused_work_size doubles.
+extern "C" int64_t skl_lsqr_fused_work_size(int64_t n) {
+  return (int64_t)sm_count_lq() * 2 * (n + 1) + 64;
+}
+
+extern "C" int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                              double s, double alpha, const double* r_prev, double beta_prev,
+                              double* r_out, double* z, double* norm2, double* work,
+                              unsigned int* counters, void* stream) {
+  clear_error();
+  SKL_REQUIRE(A && y && r_out && z && norm2 && work && counters && m >= 1 && n >= 1 &&
+                  n <= 256 && lda >= m && (!r_prev || beta_prev > 0.0),
+              SKL_ERR_INVALID, "lsqr_fused: bad arguments");
+  SKL_REQUIRE(((uintptr_t)A & 15) == 0 && lda % 2 == 0, SKL_ERR_INVALID,
+              "lsqr_fused: A must be 16-byte aligned with an even leading dimension");
+  const int64_t nblk = (m + LF_RB - 1) / LF_RB;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, 2LL * sm_count_lq()));
+  double* zpart = work;
+  double* npart = work + (int64_t)grid * n;
+  unsigned int* counter = counters + (skl_lsqr_counter_size(n) - 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nc = (int)((n + 7) / 8);
+#define SKL_LF_LAUNCH(NCV)                                                                    \
+  do {                                                                                        \
+    int occ = 1;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_fused_kernel<NCV>, LQ_NT, 0);    \
+    const int gr = (int)std::max<int64_t>(                                                    \
+        1, std::min<int64_t>({nblk, (int64_t)std::max(occ, 1) * sm_count_lq(), (int64_t)grid})); \
+    lsqr_fused_kernel<NCV><<<gr, LQ_NT, 0, st>>>(A, m, n, lda, y, s, alpha, r_prev, beta_prev, \
+                                                 r_out, zpart, npart, z, norm2, counter);     \
+  } while (0)
+  if (nc <= 8)
+    SKL_LF_LAUNCH(8);
+  else if (nc <= 16)
+    SKL_LF_LAUNCH(16);
+  else
+    SKL_LF_LAUNCH(32);
+#undef SKL_LF_LAUNCH
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }
