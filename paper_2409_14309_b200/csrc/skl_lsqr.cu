@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
     double* __restrict__ r_out, double* __restrict__ zpart, double* __restrict__ npart,
     double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter) {
   __shared__ double ys[8 * NC];
-  __shared__ double pdot[8][LF_RB];
-  __shared__ double rs[LF_RB];
+  __shared__ double pdot[2][8][LF_RB];  // by block parity: one barrier less per block
+  __shared__ double rs[2][LF_RB];
   __shared__ double red[32];
   __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
@@ -227,7 +227,8 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
   double ss = 0.0;
   __syncthreads();
   const int64_t nblk = (m + LF_RB - 1) / LF_RB;
-  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  int par = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, par ^= 1) {
     const int64_t i0 = blk * LF_RB + 2 * lane;
     const bool full = i0 + 1 < m;
     // the block's A values stay in registers for both phases: all NC loads
@@ -254,8 +255,8 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
         a1 = fma(v[q].y, ys[c], a1);
       }
     }
-    pdot[g][2 * lane] = a0;
-    pdot[g][2 * lane + 1] = a1;
+    pdot[par][g][2 * lane] = a0;
+    pdot[par][g][2 * lane + 1] = a1;
     __syncthreads();
     if (tid < LF_RB) {
       const int64_t i = blk * LF_RB + tid;
@@ -263,18 +264,17 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
       if (i < m) {
         double dot = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) dot += pdot[w][tid];
+        for (int w = 0; w < 8; ++w) dot += pdot[par][w][tid];
         r = s * dot - (r_prev ? alpha * (r_prev[i] / beta_prev) : 0.0);
         r_out[i] = r;
         ss = fma(r, r, ss);
       }
-      rs[tid] = r;
+      rs[par][tid] = r;
     }
     __syncthreads();
-    const double r0 = rs[2 * lane], r1 = rs[2 * lane + 1];
+    const double r0 = rs[par][2 * lane], r1 = rs[par][2 * lane + 1];
 #pragma unroll
     for (int q = 0; q < NC; ++q) zacc[q] = fma(v[q].y, r1, fma(v[q].x, r0, zacc[q]));
-    __syncthreads();  // pdot / rs reused by the next block
   }
   // per-CTA partials: column sums over the lanes, the norm over the CTA
 #pragma unroll
