@@ -2,8 +2,8 @@
 
 Mirrors /root/reference/pkg/src/sketchls/solvers.py:110-255 (`lsqr`) and
 :258-270 (`_sym_ortho`).  The vector work runs in the fused kernels of
-csrc/skl_lsqr.cu (two HBM passes over A per iteration, the n x n
-triangular solves with R in one CTA each); the scalar recurrence -- Givens
+csrc/skl_lsqr.cu (one HBM pass over dense A per iteration for n <= 256,
+two otherwise; the n x n triangular solves with R in one CTA each); the scalar recurrence -- Givens
 rotations, the ||A|| estimate and the five stopping rules -- is the
 reference's code, line for line, on host floats read back once per step.
 """

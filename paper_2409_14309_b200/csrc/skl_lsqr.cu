@@ -4,8 +4,10 @@
 //   u = A (R^-1 v) - alfa u;  beta = ||u||;  u /= beta
 //   v = R^-T (A^T u) - beta v;  alfa = ||v||;  v /= alfa
 //   x += (phi/rho) w;  w = v - (theta/rho) w;  ||x||
-// Two full passes over A (HBM-bound) and two n x n triangular solves.  The
-// kernels here fuse each step's vector work into the pass that produces it:
+// Two products with A (HBM-bound) and two n x n triangular solves.  For
+// dense A with n <= 256 both products share one pass (skl_lsqr_fused, below);
+// otherwise the kernels fuse each step's vector work into the pass that
+// produces it:
 //   skl_lsqr_gemv_n : u_out = s * (A y) - alpha * u_in, and ||u_out||^2
 //   skl_lsqr_gemv_t : u_n = u_raw / beta (written back), z = A^T u_n
 //   skl_lsqr_trsv_t : v_out = R^-T z - beta v, and ||v_out||^2
