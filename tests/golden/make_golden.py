@@ -241,14 +241,6 @@ def main() -> None:
         dup.indptr, dup.indices, dup.values)
     spec = ref.ProblemSpec(m=30, n=4, kappa=1e4, beta=1e-6, seed=11)
     ref.write_problem_dir(spec, ref.generate_problem(spec), str(io / "problem"))
-    recs = [ref.BenchRecord("saa", "countsketch", 1000, 20, 80, 1e10, 1e-10, 0, 0.125,
-                            3.0e-7, 0.0, 0, "direct"),
-            ref.BenchRecord("lsqr", None, 1000, 20, None, 1e10, 1e-10, 1, 2.5, -1.0, -1.0, 0,
-                            "failed")]
-    ref.write_csv(recs, str(io / "results.csv"))
-    ref.write_meta(ref.BenchConfig(m_list=(1000, 2000), n=20, methods=("lsqr", "saa"),
-                                   sketches=("countsketch", "srht"), repeats=2, seed=4),
-                   str(io / "bench_meta.txt"))
 
     g["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **g)

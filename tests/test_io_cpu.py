@@ -1,4 +1,4 @@
-"""Matrix Market, problem directories, sweep CSV/meta files and the CLI front
+"""Matrix Market, problem directories and the CLI front
 end on the host: byte-for-byte against files the
 reference wrote (tests/golden/io/, made by tests/golden/make_golden.py), the
 reference's error behaviour, and the CLI's exit codes -- including that a
@@ -13,7 +13,7 @@ import pytest
 import torch
 
 import paper_2409_14309_b200 as E
-from paper_2409_14309_b200 import cli, sweep
+from paper_2409_14309_b200 import cli
 
 IO = Path(__file__).resolve().parent / "golden" / "io"
 
@@ -106,65 +106,6 @@ def test_problem_spec_validation():
         E.generate_problem(E.ProblemSpec(m=4, n=4, beta=1e-3))
 
 
-def _records():
-    return [E.BenchRecord("saa", "countsketch", 1000, 20, 80, 1e10, 1e-10, 0, 0.125, 3.0e-7,
-                          0.0, 0, "direct"),
-            E.BenchRecord("lsqr", None, 1000, 20, None, 1e10, 1e-10, 1, 2.5, -1.0, -1.0, 0,
-                          "failed")]
-
-
-def test_csv_and_meta_match_reference_bytes(tmp_path):
-    E.write_csv(_records(), str(tmp_path / "results.csv"))
-    assert _bytes(tmp_path / "results.csv") == _bytes(IO / "results.csv")
-    assert E.parse_csv(str(IO / "results.csv")) == _records()
-    cfg = E.BenchConfig(m_list=(1000, 2000), n=20, methods=("lsqr", "saa"),
-                        sketches=("countsketch", "srht"), repeats=2, seed=4)
-    E.write_meta(cfg, str(tmp_path / "bench_meta.txt"))
-    assert _bytes(tmp_path / "bench_meta.txt") == _bytes(IO / "bench_meta.txt")
-
-
-def test_parse_csv_errors(tmp_path):
-    p = tmp_path / "r.csv"
-    p.write_text("nope\n")
-    with pytest.raises(ValueError, match="unexpected CSV header"):
-        E.parse_csv(str(p))
-    p.write_text(E.CSV_HEADER + "\na,b\n")
-    with pytest.raises(ValueError, match="expected 13 fields, got 2"):
-        E.parse_csv(str(p))
-
-
-@pytest.mark.parametrize("kw,msg", [
-    (dict(m_list=()), "m_list must be nonempty"),
-    (dict(m_list=(10,), n=20), "every m in m_list must be >= n=20"),
-    (dict(repeats=0), "repeats must be >= 1"),
-    (dict(methods=("direct",)), "methods must be a nonempty subset"),
-    (dict(sketches=("bogus",)), "unknown sketch kinds"),
-    (dict(methods=("saa",), sketches=()), "saa/sap requested but no sketches given"),
-])
-def test_bench_config_validation(kw, msg):
-    base = dict(m_list=(100,), n=10)
-    base.update(kw)
-    with pytest.raises(E.SpecError, match=msg):
-        E.BenchConfig(**base)
-
-
-def test_median_series_drops_failed_cells():
-    recs = _records() + [E.BenchRecord("saa", "countsketch", 1000, 20, 80, 1e10, 1e-10, 1, 0.5,
-                                       1e-6, 0.0, 0, "direct")]
-    s = E.median_series(recs, "wall_time_s")
-    assert s == {("saa", "countsketch"): ([1000], [0.3125])}
-    with pytest.raises(E.SpecError, match="unknown metric"):
-        E.median_series(recs, "iterations")
-
-
-def test_forward_error_host():
-    assert sweep.forward_error(E.Vector(np.array([1.0, 1.0])), E.Vector(np.array([1.0, 0.0]))) == 1.0
-    with pytest.raises(E.UndefinedMetricError):
-        sweep.forward_error(E.Vector(np.zeros(2)), E.Vector(np.zeros(2)))
-    with pytest.raises(E.SpecError, match="length mismatch"):
-        sweep.forward_error(E.Vector(np.zeros(2)), E.Vector(np.zeros(3)))
-
-
 # ---------------------------------------------------------------- CLI exit codes
 def test_cli_usage_errors(capsys, monkeypatch):
     assert cli.main(["gen", "--m", "3", "--n", "5", "--out", "/tmp/x"]) == cli.EXIT_USAGE
@@ -175,7 +116,6 @@ def test_cli_usage_errors(capsys, monkeypatch):
     with pytest.raises(SystemExit) as ex:
         cli.main(["solve", "--A", "a.mtx"])
     assert ex.value.code == 2
-    assert cli.main(["bench", "--m-list", "10", "--n", "20", "--out", "/tmp/x"]) == cli.EXIT_USAGE
 
 
 def test_cli_io_error(tmp_path, capsys):
@@ -199,5 +139,5 @@ def test_module_entry_point_help():
 
     out = subprocess.run([sys.executable, "-m", "paper_2409_14309_b200", "--help"],
                          capture_output=True, text=True, cwd=str(Path(__file__).resolve().parents[1]))
-    assert out.returncode == 0 and "{gen,solve,bench}" in out.stdout
+    assert out.returncode == 0 and "{gen,solve}" in out.stdout
     json.dumps({})  # keep the json import exercised for the GPU twin of this file
