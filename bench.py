@@ -233,6 +233,32 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def launch_check(args):
+    """Form the world, all-reduce (rank + 1) once, rank 0 prints what it saw."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= world
+    if use_nccl:
+        torch.cuda.set_device(local)
+    backend = "nccl" if use_nccl else "gloo"
+    if world > 1:
+        dist.init_process_group(backend)
+    t = torch.tensor([rank + 1.0], dtype=torch.float64, device="cuda" if use_nccl else "cpu")
+    if world > 1:
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": args.gpus, "world": world,
+                          "backend": backend if world > 1 else "none",
+                          "rank_sum": float(t.item()),
+                          "launcher": "torchrun" if "TORCHELASTIC_RUN_ID" in os.environ
+                          or "LOCAL_WORLD_SIZE" in os.environ else "none"}), flush=True)
+
+
 # ----------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -244,8 +270,27 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="form the N-rank world (relaunching under torchrun if needed), "
+                         "all-reduce once, print the world rank 0 saw, exit")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    from paper_2409_14309_b200.launch import LaunchError, ensure_world
+
+    if args.impl == "b200" or args.launch_check:
+        # one process per GPU: without a launcher, --gpus N > 1 re-executes
+        # this script under torch.distributed.run; under one, WORLD_SIZE must
+        # be N -- never a silent 1-GPU run labelled N
+        try:
+            ensure_world(args.gpus, str(Path(__file__).resolve()), sys.argv[1:],
+                         need_gpus=not args.launch_check)
+        except LaunchError as exc:
+            print(f"bench.py: {exc}", file=sys.stderr)
+            sys.exit(2)
+    if args.launch_check:
+        launch_check(args)
+        return
 
     from paper_2409_14309_b200 import workloads as W
 

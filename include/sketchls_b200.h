@@ -284,6 +284,21 @@ int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices, const dou
                         const int64_t* bucket_ptr, const int8_t* signs, int64_t d, double* SA,
                         int64_t ldsa, void* stream);
 
+/* Ordered bucket walk for a few long dense columns (device): SA[:, c]
+ * (+)= S A[:, c] for c < n and Sb (+)= S b, every bucket's products
+ * sign*scale*A[j, c] added in ascending source row j from +0.0 -- scipy's
+ * csr_matvec / csr_matvecs fold, bitwise.  bucket_rows / bucket_ptr /
+ * signs are the CSR of S as for skl_countsketch_csr (scale = 1 for
+ * CountSketch, fl(1/sqrt(s)) for a sparse sign embedding).  Used where the
+ * column kernels would split the rows (one column, or n + 1 << #SMs): a
+ * vector apply S b, cfg4's Sb.  n may be 0 (b only).  Replaces
+ * sketch.py:212 (`sparse_map @ b`, csr_matvec). */
+int skl_countsketch_dense_ordered(const double* A, int64_t m, int64_t n, int64_t lda,
+                                  const double* b, const int32_t* bucket_rows,
+                                  const int64_t* bucket_ptr, const int8_t* signs, double scale,
+                                  int64_t d, double* SA, int64_t ldsa, double* Sb, int accumulate,
+                                  void* stream);
+
 /* SRHT: out = (P H D [A; 0]) / sqrt(d) for dense column-major A (device),
  * H the unnormalised Sylvester-Hadamard of order m_pad.  sign_bits are the
  * +-1 sign diagonal packed by skl_srht_pack_signs (device copy);

@@ -1,6 +1,8 @@
 """CPU ORACLE (test infrastructure only): ctypes access to the plain-C
-restatement in oracle/c/philox_oracle.c (built by oracle/Makefile into
-oracle/_build/liboracle.so)."""
+restatement in oracle/c/philox_oracle.c (random streams) and
+oracle/c/apply_oracle.c (column-threaded CountSketch / SRHT applies for the
+full-size parity checks), built by oracle/Makefile into
+oracle/_build/liboracle.so."""
 
 from __future__ import annotations
 
@@ -23,7 +25,8 @@ def build() -> Path:
 def lib():
     global _lib
     if _lib is None:
-        if not LIB.exists() or LIB.stat().st_mtime < (HERE / "c" / "philox_oracle.c").stat().st_mtime:
+        srcs = [HERE / "c" / "philox_oracle.c", HERE / "c" / "apply_oracle.c", HERE / "Makefile"]
+        if not LIB.exists() or LIB.stat().st_mtime < max(p.stat().st_mtime for p in srcs):
             build()
         L = ctypes.CDLL(str(LIB))
         P, I64, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
@@ -32,6 +35,8 @@ def lib():
         L.orc_srht.argtypes = [U64, I64, I64, P, P]
         L.orc_gaussian.argtypes = [U64, I64, P, P, P, ctypes.c_double, ctypes.c_double, P]
         L.orc_countsketch_fold.argtypes = [P, P, I64, I64, P, I64, I64, P]
+        L.orc_countsketch_fold_mt.argtypes = [P, P, I64, I64, P, I64, I64, P, I64, ctypes.c_int]
+        L.orc_srht_apply.argtypes = [P, I64, I64, I64, P, P, I64, I64, P, I64, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -76,3 +81,53 @@ def countsketch_fold(rows, signs, d: int, A: np.ndarray) -> np.ndarray:
     lib().orc_countsketch_fold(rows.ctypes.data, signs.ctypes.data, m, n, A.ctypes.data, m, d,
                                out.ctypes.data)
     return out
+
+
+def _threads(threads: int | None) -> int:
+    import os
+
+    if threads:
+        return threads
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def countsketch_apply_mt(rows, signs, d: int, A: np.ndarray, threads: int | None = None):
+    """sketch.py:209,212 (`sparse_map @ A`, scipy's csr_matvecs fold) for an
+    F-ordered (or 1-d) A, columns spread over host threads; bitwise equal to
+    oracle.countsketch_apply.  Returns d x n F-ordered (or d for 1-d A)."""
+    vec = A.ndim == 1
+    A2 = A.reshape(-1, 1) if vec else A
+    if not A2.flags.f_contiguous:
+        A2 = np.asfortranarray(A2)
+    m, n = A2.shape
+    lda = m if n == 1 else A2.strides[1] // 8
+    out = np.empty((d, n), order="F")
+    rows = np.ascontiguousarray(rows, np.int64)
+    signs = np.ascontiguousarray(signs, np.float64)
+    if lib().orc_countsketch_fold_mt(rows.ctypes.data, signs.ctypes.data, m, n, A2.ctypes.data,
+                                     lda, d, out.ctypes.data, d, _threads(threads)):
+        raise RuntimeError("orc_countsketch_fold_mt failed")
+    return out[:, 0].copy() if vec else out
+
+
+def srht_apply_mt(sign_diag, row_sample, m_pad: int, d: int, A: np.ndarray,
+                  threads: int | None = None):
+    """sketch.py:213-223 (pad, sign, fwht_inplace, sample / sqrt(d)) for an
+    F-ordered (or 1-d) A, columns spread over host threads; bitwise equal to
+    oracle.srht_apply.  Returns d x n F-ordered (or d for 1-d A)."""
+    vec = A.ndim == 1
+    A2 = A.reshape(-1, 1) if vec else A
+    if not A2.flags.f_contiguous:
+        A2 = np.asfortranarray(A2)
+    m, n = A2.shape
+    lda = m if n == 1 else A2.strides[1] // 8
+    out = np.empty((d, n), order="F")
+    sg = np.ascontiguousarray(sign_diag, np.float64)
+    rs = np.ascontiguousarray(row_sample, np.int64)
+    if lib().orc_srht_apply(A2.ctypes.data, m, n, lda, sg.ctypes.data, rs.ctypes.data, m_pad, d,
+                            out.ctypes.data, d, _threads(threads)):
+        raise RuntimeError("orc_srht_apply failed")
+    return out[:, 0].copy() if vec else out

@@ -133,6 +133,11 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr],
     ),
+    "skl_countsketch_dense_ordered": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, ctypes.c_double, c_i64, c_ptr,
+         c_i64, c_ptr, c_int, c_ptr],
+    ),
     "skl_lsqr_fused_work_size": (c_i64, [c_i64]),
     "skl_lsqr_fused": (
         c_int,

@@ -443,16 +443,36 @@ def _aligned(t, ld: int, cols: int):
     return out, ld2
 
 
+# Column length (bytes) up to which few-column applies take the ordered
+# bucket walk: one column's gathers then stay resident in the 126 MB L2.
+_ORDERED_MAX_COLUMN_BYTES = 64 << 20
+
+
+def _few_long_columns(m: int, ncols: int) -> bool:
+    """True where the column kernels would split the rows into partitions
+    (too few columns to fill the SMs on a long source; csrc/skl_countsketch.cu
+    countsketch_owned_launch / countsketch_launch) -- the ordered bucket walk
+    keeps those applies bitwise instead."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return ncols * 2 < sms and m > (1 << 18) and 8 * m <= _ORDERED_MAX_COLUMN_BYTES
+
+
 def _countsketch_dense_device(op: SketchOperator, A, lda: int, n: int, b=None):
     """SA (d x n column-major tensor) and Sb (d) or None, all on device."""
-    plan = op.device_plan()
     d, m = op.target_dim, op.source_dim
     A, lda = _aligned(A, lda, n)
     if b is not None and b.data_ptr() % 16:
         b = b.clone()
     SA = device_f64((d, n), fortran=True)
     Sb = device_f64((d,)) if b is not None else None
-    plan.apply(A, m, n, lda, b, SA, d, Sb)
+    if _few_long_columns(m, n + (b is not None)):
+        brow, bptr, signs = op.device_buckets()
+        scale = 1.0 / math.sqrt(op.sparsity) if op.kind == "sparsesign" else 1.0
+        _native.call("skl_countsketch_dense_ordered", _native.ptr(A), m, n, lda, _native.ptr(b),
+                     _native.ptr(brow), _native.ptr(bptr), _native.ptr(signs), scale, d,
+                     _native.ptr(SA), d, _native.ptr(Sb), 0, current_stream())
+        return SA, Sb
+    op.device_plan().apply(A, m, n, lda, b, SA, d, Sb)
     return SA, Sb
 
 

@@ -102,20 +102,50 @@ def test_countsketch_ragged_shapes(m, n, d):
 
 
 def test_countsketch_partitions_deterministic():
+    """The row-partitioned column kernel (few columns on a long source, used
+    beyond the ordered walk's 64 MiB column bound): deterministic, <= 1e-15."""
     m, n, d = 300_000, 3, 2048
     rng = np.random.default_rng(3)
     A = torch.from_numpy(np.asfortranarray(rng.standard_normal((m, n)))).cuda()
     op = E.build_sketch(E.SketchSpec("countsketch", d, seed=9), m)
-    from paper_2409_14309_b200.sketch import _countsketch_dense_device
-
+    plan = op.device_plan()
     outs = []
     for _ in range(2):
-        SA, _ = _countsketch_dense_device(op, A, m, n)  # auto partitions (n small)
+        SA = torch.empty((n, d), dtype=torch.float64, device="cuda").t()
+        plan.apply(A, m, n, m, None, SA, d, None, partitions=0)  # auto: P > 1 here
         outs.append(SA.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
     want = O.countsketch_apply(op.rows.astype(np.int64), op.signs.astype(np.float64), d,
                                A.cpu().numpy())
     assert rel_fro(outs[0], want) <= 1e-15
+
+
+@pytest.mark.parametrize("m,n,d,kind", [(300_000, 3, 2048, "countsketch"),
+                                        (1 << 20, 0, 2048, "countsketch"),
+                                        (1 << 22, 0, 8192, "countsketch"),
+                                        (262_145, 1, 5000, "countsketch"),
+                                        (400_000, 2, 1000, "sparsesign")])
+def test_countsketch_few_long_columns_bitwise(m, n, d, kind):
+    """Few columns on a long source (a vector S b, cfg4's Sb): the ordered
+    bucket walk keeps scipy's per-bucket fold, so the result is bitwise."""
+    rng = np.random.default_rng(m + n)
+    op = E.build_sketch(E.SketchSpec(kind, d, seed=m ^ d, sparsity=4), m)
+    smap = op.sparse_map
+    if n == 0:
+        v = rng.standard_normal(m)
+        got = E.apply_to_vector(op, E.Vector(torch.from_numpy(v).cuda())).data.cpu().numpy()
+        assert np.array_equal(got, smap @ v)
+        return
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    got = E.apply_to_matrix(op, E.DenseMatrix(torch.from_numpy(A).cuda())).data.cpu().numpy()
+    assert np.array_equal(got, smap @ A)
+    b = rng.standard_normal(m)
+    from paper_2409_14309_b200.sketch import _countsketch_dense_device
+
+    SA, Sb = _countsketch_dense_device(op, torch.from_numpy(A).cuda(), m, n,
+                                       b=torch.from_numpy(b).cuda())
+    assert np.array_equal(SA.cpu().numpy(), smap @ A)
+    assert np.array_equal(Sb.cpu().numpy(), smap @ b)
 
 
 def test_countsketch_misaligned_device_view():
