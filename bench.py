@@ -352,28 +352,28 @@ def main():
     outbuf = torch.empty((n + 1, ld), dtype=torch.float64, device="cuda")
     out = outbuf.t()[:d]
     cs_plan = plan.device_plan()
-    # N > 1: the reduce is fused with the sketch -- each rank's kernel writes
-    # its partial into its slot of rank 0's symmetric buffer over NVLink and
-    # rank 0 sums the slots in rank order after a device barrier
-    # (distributed.PeerSlots); one NCCL reduce where that is unavailable.
-    from paper_2409_14309_b200.distributed import peer_slots_or_none
+    # N > 1: every rank's kernel writes its partial into its own symmetric
+    # buffer; the ranks then reduce-scatter the partials over NVLink in rank
+    # order straight into rank 0's result (distributed.PeerReduce); one NCCL
+    # reduce where symmetric memory is unavailable.
+    from paper_2409_14309_b200.distributed import peer_reduce_or_none
 
-    slots = peer_slots_or_none(d, n + 1) if grouped else None
-    collective = ("peer-slots" if slots is not None else
-                  ("nccl-reduce" if world > 1 else "none"))
+    peer = peer_reduce_or_none(d, n + 1) if grouped else None
+    collective = ("peer-reduce-scatter (symmetric memory, skl_reduce_peers)" if peer is not None
+                  else ("nccl-reduce" if world > 1 else "none"))
 
     def apply():
-        if slots is not None:
-            base = slots.slot_ptr()
-            cs_plan.apply(A, m_loc, n, lda, b, base, slots.ld, base + 8 * slots.ld * n,
+        if peer is not None:
+            base = peer.partial_ptr()
+            cs_plan.apply(A, m_loc, n, lda, b, base, peer.ld, base + 8 * peer.ld * n,
                           partitions=1, stream=stream.cuda_stream)
         else:
             cs_plan.apply(A, m_loc, n, lda, b, out, ld, out[:, n], partitions=1,
                           stream=stream.cuda_stream)
 
     def collect():
-        if slots is not None:
-            slots.finish(out, ld)
+        if peer is not None:
+            peer.finish(out, ld)
         elif world > 1:
             dist.reduce(outbuf, dst=0)
 
@@ -545,8 +545,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
-            # our kernels per timed step: the sketch, plus the slot sum on rank 0
-            "gpu_launches": args.steps * (2 if slots is not None else 1),
+            # our kernels per timed step: the sketch, plus this rank's block of
+            # the peer reduce
+            "gpu_launches": args.steps * (2 if peer is not None else 1),
         }
         if solve:
             line["solve"] = solve

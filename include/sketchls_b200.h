@@ -202,22 +202,25 @@ int skl_sparsesign_csr(const int64_t* indptr, const int64_t* indices, const doub
                        const int8_t* signs, double scale, int64_t d, double* SA, int64_t ldsa,
                        void* stream);
 
-/* Same apply with HOST A/b/SA/Sb: streams row blocks of A through the
- * device with host-to-device copies overlapped with the kernel; if
- * A_dev_keep != NULL the device copy of A (ld = m rounded up to 32) is
- * left there for a later residual pass.  plan pointers are device. */
+/* Same apply with HOST A/b (preferably pinned): streams ~64 MiB row blocks
+ * of A through a two-slot device ring with host-to-device copies overlapped
+ * with the kernel (bitwise the same result); if A_dev_keep != NULL the blocks
+ * land there instead (column-major, ld_keep even, 16-byte aligned) and the
+ * full device copy of A (and of b in b_dev_keep) is left for a later residual
+ * pass.  SA_out / Sb_out may be host or device memory.  Synchronises the
+ * stream before returning.  plan pointers are device. */
 int skl_countsketch_dense_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
                                const double* b_host, const uint32_t* lanes,
                                const int64_t* chunk_off, int64_t max_block, int64_t d,
-                               int64_t chunk, int warps, double* SA_host, int64_t ldsa, double* Sb_host,
-                               double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
-                               void* stream);
+                               int64_t chunk, int warps, double* SA_out, int64_t ldsa,
+                               double* Sb_out, double* A_dev_keep, int64_t ld_keep,
+                               double* b_dev_keep, void* stream);
 /* skl_countsketch_dense_host with a register-owned plan. */
 int skl_countsketch_dense_owned_host(const double* A_host, int64_t m, int64_t n, int64_t lda,
                                      const double* b_host, const uint16_t* lanes,
                                      const int64_t* chunk_off, int64_t max_block, int64_t d,
-                                     int64_t chunk, int warps, double* SA_host, int64_t ldsa,
-                                     double* Sb_host, double* A_dev_keep, int64_t ld_keep,
+                                     int64_t chunk, int warps, double* SA_out, int64_t ldsa,
+                                     double* Sb_out, double* A_dev_keep, int64_t ld_keep,
                                      double* b_dev_keep, void* stream);
 
 /* ---- preconditioned LSQR (sketch-and-precondition, solvers.py:110-361) ----
@@ -359,6 +362,17 @@ int skl_residual_csr(const int64_t* indptr, const int64_t* indices, const double
  * of the reference-style sharding with a deterministic fixed-order sum. */
 int skl_sum_slots(const double* slots, int64_t nslots, int64_t slot_stride, int64_t rows,
                   int64_t cols, int64_t ld, double* out, int64_t ldo, void* stream);
+
+/* Reduce-scatter step of the multi-GPU apply: out[i] = peers[0][i] +
+ * peers[1][i] + ... + peers[npeers-1][i] (rank order, the same bits as
+ * skl_sum_slots) for i in [begin, end).  peers is a HOST array of npeers
+ * (<= 16) device addresses -- the ranks' partials in their symmetric
+ * buffers, read over NVLink -- and out may be a peer address (the
+ * destination rank's result buffer).  Each rank calls it for its own element
+ * block, so the destination receives every block once.  Replaces the NCCL
+ * reduce of the d x (n+1) partials. */
+int skl_reduce_peers(const double* const* peers, int npeers, int64_t begin, int64_t end,
+                     double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -152,6 +152,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "skl_residual_dense": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_sum_slots": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_reduce_peers": (c_int, [c_ptr, c_int, c_i64, c_i64, c_ptr, c_ptr]),
     "skl_residual_csr": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
 }
 
@@ -221,6 +222,11 @@ def check(status: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args))
+
+
+def ptr_array(addrs) -> ctypes.Array:
+    """Host array of device addresses (e.g. the ranks' symmetric buffers)."""
+    return (ctypes.c_void_p * len(addrs))(*[int(a) for a in addrs])
 
 
 def ptr(a) -> int | None:

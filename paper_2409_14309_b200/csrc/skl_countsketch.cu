@@ -648,71 +648,122 @@ extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int6
 // Host-buffer apply: row blocks of A are copied host->device on a side
 // stream while the kernel sketches the previous block (ordered pass,
 // accumulate across blocks, so the result stays bitwise-equal).
+//
+// Without A_dev_keep the blocks land in a two-slot ring (2 x ~64 MiB, not a
+// device copy of all of A): block k is sketched out of slot k % 2 through
+// the pointer A_slot - r0 (the kernels address rows absolutely), and the copy
+// of block k + 2 waits for the kernel of block k.  With A_dev_keep the blocks
+// land in place and the full device copy is left for the residual pass.
+// The copy stream and events are per thread and device (created once), and
+// SA_out / Sb_out may be host or device memory (cudaMemcpyDefault).
+struct HostStreamCtx {
+  cudaStream_t cp = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+
+static int host_stream_ctx(HostStreamCtx** out, size_t nev) {
+  static thread_local HostStreamCtx per_dev[64];
+  int dev = 0;
+  SKL_CUDA(cudaGetDevice(&dev));
+  SKL_REQUIRE(dev >= 0 && dev < 64, SKL_ERR_CUDA, "countsketch_host: device %d out of range", dev);
+  HostStreamCtx& c = per_dev[dev];
+  if (!c.cp) SKL_CUDA(cudaStreamCreateWithFlags(&c.cp, cudaStreamNonBlocking));
+  while (c.ev.size() < nev) {
+    cudaEvent_t e;
+    SKL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.ev.push_back(e);
+  }
+  *out = &c;
+  return SKL_OK;
+}
+
 template <class Launch>
 static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, int64_t lda,
                                    const double* b_host, int64_t d, int64_t chunk,
-                                   double* SA_host, int64_t ldsa, double* Sb_host,
+                                   double* SA_out, int64_t ldsa, double* Sb_out,
                                    double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                    cudaStream_t st, Launch&& launch) {
-  SKL_REQUIRE(A_host && SA_host && m >= 1 && n >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+  SKL_REQUIRE(A_host && SA_out && m >= 1 && n >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch_host: bad arguments");
-  SKL_REQUIRE(!b_host || Sb_host, SKL_ERR_INVALID, "countsketch_host: Sb_host missing");
-  const int64_t ld_dev = A_dev_keep ? ld_keep : (m + 31) / 32 * 32;
-  SKL_REQUIRE(ld_dev >= m && ld_dev % 2 == 0, SKL_ERR_INVALID, "countsketch_host: bad ld_keep");
-  double* A_dev = A_dev_keep;
+  SKL_REQUIRE(!b_host || Sb_out, SKL_ERR_INVALID, "countsketch_host: Sb_out missing");
+  SKL_REQUIRE(!A_dev_keep || (ld_keep >= m && ld_keep % 2 == 0 &&
+                              ((uintptr_t)A_dev_keep & 15) == 0),
+              SKL_ERR_INVALID, "countsketch_host: bad A_dev_keep / ld_keep");
+  // blocks of whole plan chunks, ~64 MiB of A each (chunk is even, so every
+  // block start keeps the slot pointer A_slot - r0 16-byte aligned)
+  const int64_t rows_per_block =
+      std::min<int64_t>((m + chunk - 1) / chunk * chunk,
+                        std::max<int64_t>(chunk, ((64LL << 20) / (8 * n)) / chunk * chunk));
+  const int64_t nblk = (m + rows_per_block - 1) / rows_per_block;
+  HostStreamCtx* cx = nullptr;
+  int rc = host_stream_ctx(&cx, (size_t)(2 * nblk + 1));
+  if (rc) return rc;
+  cudaEvent_t* copied = cx->ev.data();         // [nblk]: block k on the device
+  cudaEvent_t* used = cx->ev.data() + nblk;    // [nblk]: kernel of block k done
+  cudaEvent_t ready = cx->ev.data()[2 * nblk];
+  const int64_t ld_ring = (rows_per_block + 1) / 2 * 2;
+  double* ring = nullptr;
   double* b_dev = b_dev_keep;
   double *SA_dev = nullptr, *Sb_dev = nullptr;
-  if (!A_dev) SKL_CUDA(malloc_async(&A_dev, (size_t)ld_dev * n * sizeof(double), st));
+  if (!A_dev_keep)
+    SKL_CUDA(malloc_async(&ring, (size_t)2 * ld_ring * n * sizeof(double), st));
   if (b_host && !b_dev) SKL_CUDA(malloc_async(&b_dev, (size_t)m * sizeof(double), st));
   SKL_CUDA(malloc_async(&SA_dev, (size_t)d * n * sizeof(double), st));
   if (b_host) SKL_CUDA(malloc_async(&Sb_dev, (size_t)d * sizeof(double), st));
-
-  cudaStream_t cp;
-  SKL_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-  cudaEvent_t ready;
-  SKL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   SKL_CUDA(cudaEventRecord(ready, st));  // allocations visible to the copy stream
-  SKL_CUDA(cudaStreamWaitEvent(cp, ready, 0));
+  SKL_CUDA(cudaStreamWaitEvent(cx->cp, ready, 0));
 
-  // Blocks of whole plan chunks, ~256 MiB of A each.
-  int64_t rows_per_block = std::max<int64_t>(chunk, ((256LL << 20) / (8 * n)) / chunk * chunk);
-  const int64_t nblk = (m + rows_per_block - 1) / rows_per_block;
-  int rc = SKL_OK;
-  std::vector<cudaEvent_t> evs((size_t)nblk);
   for (int64_t k = 0; k < nblk && rc == SKL_OK; ++k) {
     const int64_t r0 = k * rows_per_block, r1 = std::min(m, r0 + rows_per_block);
-    cudaEventCreateWithFlags(&evs[(size_t)k], cudaEventDisableTiming);
-    cudaError_t e = cudaMemcpy2DAsync(A_dev + r0, ld_dev * sizeof(double), A_host + r0,
-                                      lda * sizeof(double), (r1 - r0) * sizeof(double), n,
-                                      cudaMemcpyHostToDevice, cp);
+    double* dst;
+    int64_t ld_dst;
+    const double* A_base;  // pointer the kernel indexes with absolute rows
+    if (A_dev_keep) {
+      dst = A_dev_keep + r0;
+      ld_dst = ld_keep;
+      A_base = A_dev_keep;
+    } else {
+      double* slot = ring + (size_t)(k & 1) * ld_ring * n;
+      dst = slot;
+      ld_dst = ld_ring;
+      A_base = slot - r0;
+    }
+    cudaError_t e = cudaSuccess;
+    if (!A_dev_keep && k >= 2) e = cudaStreamWaitEvent(cx->cp, used[k - 2], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(dst, ld_dst * sizeof(double), A_host + r0, lda * sizeof(double),
+                            (r1 - r0) * sizeof(double), n, cudaMemcpyHostToDevice, cx->cp);
     if (e == cudaSuccess && b_host)
       e = cudaMemcpyAsync(b_dev + r0, b_host + r0, (r1 - r0) * sizeof(double),
-                          cudaMemcpyHostToDevice, cp);
-    if (e == cudaSuccess) e = cudaEventRecord(evs[(size_t)k], cp);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, evs[(size_t)k], 0);
+                          cudaMemcpyHostToDevice, cx->cp);
+    if (e == cudaSuccess) e = cudaEventRecord(copied[k], cx->cp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, copied[k], 0);
     if (e != cudaSuccess) {
       set_error("countsketch_host: copy failed: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
       break;
     }
-    rc = launch(A_dev, ld_dev, b_host ? b_dev : nullptr, SA_dev, Sb_dev, k > 0 ? 1 : 0, r0, r1);
+    rc = launch(A_base, A_dev_keep ? ld_keep : ld_ring, b_host ? b_dev : nullptr, SA_dev, Sb_dev,
+                k > 0 ? 1 : 0, r0, r1);
+    if (rc == SKL_OK && cudaEventRecord(used[k], st) != cudaSuccess) {
+      set_error("countsketch_host: event record failed");
+      rc = SKL_ERR_CUDA;
+    }
   }
+  // the copy stream never runs ahead of this call: join it before returning
+  if (cudaEventRecord(ready, cx->cp) == cudaSuccess) cudaStreamWaitEvent(st, ready, 0);
   if (rc == SKL_OK) {
-    cudaError_t e = cudaMemcpy2DAsync(SA_host, ldsa * sizeof(double), SA_dev, d * sizeof(double),
-                                      d * sizeof(double), n, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaMemcpy2DAsync(SA_out, ldsa * sizeof(double), SA_dev, d * sizeof(double),
+                                      d * sizeof(double), n, cudaMemcpyDefault, st);
     if (e == cudaSuccess && b_host)
-      e = cudaMemcpyAsync(Sb_host, Sb_dev, d * sizeof(double), cudaMemcpyDeviceToHost, st);
+      e = cudaMemcpyAsync(Sb_out, Sb_dev, d * sizeof(double), cudaMemcpyDefault, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       set_error("countsketch_host: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
     }
   }
-  for (auto& ev : evs)
-    if (ev) cudaEventDestroy(ev);
-  cudaEventDestroy(ready);
-  cudaStreamDestroy(cp);
-  if (!A_dev_keep) cudaFreeAsync(A_dev, st);
+  if (ring) cudaFreeAsync(ring, st);
   if (b_host && !b_dev_keep) cudaFreeAsync(b_dev, st);
   cudaFreeAsync(SA_dev, st);
   if (Sb_dev) cudaFreeAsync(Sb_dev, st);
@@ -723,13 +774,13 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
                                           const double* b_host, const uint32_t* lanes,
                                           const int64_t* chunk_off, int64_t max_block,
                                           int64_t d, int64_t chunk, int warps,
-                                          double* SA_host, int64_t ldsa, double* Sb_host,
+                                          double* SA_out, int64_t ldsa, double* Sb_out,
                                           double* A_dev_keep, int64_t ld_keep, double* b_dev_keep,
                                           void* stream) {
   clear_error();
   cudaStream_t st = (cudaStream_t)stream;
   return countsketch_host_stream(
-      A_host, m, n, lda, b_host, d, chunk, SA_host, ldsa, Sb_host, A_dev_keep, ld_keep,
+      A_host, m, n, lda, b_host, d, chunk, SA_out, ldsa, Sb_out, A_dev_keep, ld_keep,
       b_dev_keep, st,
       [&](const double* A_dev, int64_t ld_dev, const double* b_dev, double* SA_dev, double* Sb_dev,
           int acc, int64_t r0, int64_t r1) {
@@ -741,12 +792,12 @@ extern "C" int skl_countsketch_dense_host(const double* A_host, int64_t m, int64
 extern "C" int skl_countsketch_dense_owned_host(
     const double* A_host, int64_t m, int64_t n, int64_t lda, const double* b_host,
     const uint16_t* lanes, const int64_t* chunk_off, int64_t max_block, int64_t d, int64_t chunk,
-    int warps, double* SA_host, int64_t ldsa, double* Sb_host, double* A_dev_keep,
+    int warps, double* SA_out, int64_t ldsa, double* Sb_out, double* A_dev_keep,
     int64_t ld_keep, double* b_dev_keep, void* stream) {
   clear_error();
   cudaStream_t st = (cudaStream_t)stream;
   return countsketch_host_stream(
-      A_host, m, n, lda, b_host, d, chunk, SA_host, ldsa, Sb_host, A_dev_keep, ld_keep,
+      A_host, m, n, lda, b_host, d, chunk, SA_out, ldsa, Sb_out, A_dev_keep, ld_keep,
       b_dev_keep, st,
       [&](const double* A_dev, int64_t ld_dev, const double* b_dev, double* SA_dev, double* Sb_dev,
           int acc, int64_t r0, int64_t r1) {

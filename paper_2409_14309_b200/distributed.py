@@ -4,34 +4,45 @@ Row block k of A (and b) lives on rank k.  Every rank sketches its block
 with the operator realised once for the GLOBAL m, exactly as the reference
 would build it (sketch.py:84-127) -- CountSketch hashes of global rows,
 SRHT sign/sample with the shard's block offset, the Gaussian column block --
-producing a partial d x (n+1) [SA | Sb].
+producing a partial d x (n+1) [SA | Sb].  Dense and CSR row blocks are both
+supported (a CSR block is the rows [r0, r1) of the global CSR with its
+indptr rebased; CountSketch uses the CSR kernel with the bucket lists of the
+shard's rows, SRHT / Gaussian densify the block on the device as the
+reference densifies CSR input, sketch.py:205-206, 214).
 
-The reduce is fused with the sketch (``PeerSlots``): every rank's kernel
-writes its partial straight into its own slot of rank 0's symmetric buffer
-(NVLink peer stores from the kernel's epilogue, overlapping the CTAs still
-streaming A), a device-side barrier orders the slots, and rank 0 sums them
-in rank order (``skl_sum_slots``) -- deterministic for a given world size.
-Where symmetric memory is unavailable (or on CPU with gloo, in the tests)
-the partials are combined by one collective reduce instead.  Rank 0 solves
-the reduced problem, broadcasts x, and the residual norm is an all-reduce
-of the per-block squared residuals.
+The reduce runs over NVLink peer memory (``PeerReduce``): every rank's
+kernels write the partial into the rank's own symmetric buffer; after a
+device-side barrier rank r sums element block r of all N partials in rank
+order (loads from the peers' buffers) and stores it straight into the
+destination's result buffer; a second barrier publishes the result.  That
+is a reduce-scatter whose gather is the destination's inbox: each rank
+moves ~(N-1)/N of one partial in and 1/N out (config 4's 64 MiB partial:
+~56 MiB per rank, instead of the destination pulling N x 64 MiB), and the
+sum is deterministic for a given world size.  Where symmetric memory is
+unavailable (or on CPU with gloo, in the tests) the partials are combined by
+one collective reduce instead.  The destination solves the reduced problem,
+broadcasts x, and the residual norm is an all-reduce of the per-block
+squared residuals.
 
 The sum over ranks changes the floating-point order relative to the
 single-pass fold, so the result is within ~1e-15 relative of the 1-GPU
 (bitwise-reference) sketch, not bitwise.  Process layout: one process per
-GPU, launched by torchrun; ``torch.distributed`` is the plumbing (process
-group, symmetric-memory rendezvous, broadcast).
+GPU, launched by torchrun (``launch.py``); ``torch.distributed`` is the
+plumbing (process group, symmetric-memory rendezvous, broadcast).  The same
+shard plans drive the single-process multi-device ``solve()``
+(``multidevice.py``).
 """
 
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 from typing import Callable
 
 import numpy as np
 
 from . import _native
-from ._device import current_stream, device_f64, require_cuda, torch
+from ._device import current_stream, device_f64, require_cuda, to_device, torch
 from .sketch import SHARD_ALIGN, CountSketchPlan, SketchOperator, build_sketch
 
 
@@ -47,18 +58,81 @@ def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
     return min(m, c0 * SHARD_ALIGN), min(m, c1 * SHARD_ALIGN)
 
 
+def element_block(total: int, world: int, rank: int, align: int = 2) -> tuple[int, int]:
+    """Rank ``rank``'s share [e0, e1) of ``total`` flat elements in the
+    reduce-scatter (block starts on multiples of ``align`` so 16-byte loads
+    stay aligned; the blocks tile [0, total))."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank {rank} of {world}")
+    units = math.ceil(total / align)
+    u0, u1 = units * rank // world, units * (rank + 1) // world
+    return min(total, u0 * align), min(total, u1 * align)
+
+
+@dataclass(frozen=True)
+class CsrBlock:
+    """Rows [r0, r1) of a CSR matrix on one device: indptr rebased to 0
+    (int64), the block's int64 column indices and float64 values."""
+
+    indptr: object
+    indices: object
+    values: object
+    rows: int
+    cols: int
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+    def dense(self):
+        """Column-major m_loc x n dense copy on the device (the reference
+        densifies CSR input for SRHT / Gaussian, sketch.py:205-206, 214)."""
+        rows = torch.repeat_interleave(torch.arange(self.rows, device=self.indptr.device),
+                                       self.indptr[1:] - self.indptr[:-1])
+        out = torch.zeros((self.cols, self.rows), dtype=torch.float64, device=self.indptr.device)
+        out[self.indices, rows] = self.values
+        return out.t()
+
+
+def csr_row_block(A, r0: int, r1: int, device=None) -> CsrBlock:
+    """Rows [r0, r1) of a SparseMatrix (or scipy CSR) as a CsrBlock on
+    ``device`` (a CUDA index, default the current device, or a torch device)."""
+    if hasattr(A, "values"):  # SparseMatrix carrier (linalg.py:56-114)
+        vals, ncols = A.values, A.cols
+    else:  # scipy.sparse CSR
+        vals, ncols = A.data, A.shape[1]
+    indptr = np.asarray(A.indptr, dtype=np.int64)
+    p0, p1 = int(indptr[r0]), int(indptr[r1])
+    if isinstance(device, (str, torch.device)):
+        dev = torch.device(device)  # e.g. "cpu" for the gloo tests' oracle ranks
+    else:
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+
+    def up(a, dtype):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(dev)
+
+    return CsrBlock(up(indptr[r0:r1 + 1] - p0, np.int64), up(np.asarray(A.indices)[p0:p1], np.int64),
+                    up(np.asarray(vals)[p0:p1], np.float64), r1 - r0, int(ncols))
+
+
 class ShardPlan:
     """The part of a global operator that the rank owning rows [r0, r1) needs.
 
-    * countsketch: the hashes/signs of the global rows [r0, r1) and their
-      device plan (the hash of row j is the reference's draw for GLOBAL j);
+    * countsketch: the hashes/signs of the global rows [r0, r1), their dense
+      plan and (for CSR blocks and vector applies) their bucket lists -- the
+      hash of row j is the reference's draw for GLOBAL j; the device hashes
+      are drawn on the shard's device from the operator's key;
     * srht: the packed sign words of the shard's 4096-row blocks (a slice of
       the global packing, shards are block aligned) plus the global sample;
       the kernel adds the (-1)^popc(p_hi & j_hi) factor for the shard's
       block offset, i.e. H_m = H_G (x) H_{m/G} over (shard, local) bits;
     * gaussian: the column block S[:, r0:r1] of the row-major d x m matrix
-      (the full G is generated on each rank -- the ziggurat stream is
-      sequential -- and the GEMM reads only the block)."""
+      (``op.device_gaussian_block``: on a multi-device run each device
+      generates only its band of the stream and the blocks are exchanged)."""
 
     def __init__(self, op: SketchOperator, r0: int, r1: int):
         if op.kind not in ("countsketch", "srht", "gaussian"):
@@ -70,7 +144,7 @@ class ShardPlan:
         self.op, self.r0, self.r1 = op, r0, r1
         self.kind = op.kind
         self.d = op.target_dim
-        self._plan = None
+        self._dev: dict = {}
 
     @property
     def rows(self):
@@ -80,17 +154,40 @@ class ShardPlan:
     def signs(self):
         return np.ascontiguousarray(self.op.signs[self.r0:self.r1])
 
+    def _cache(self) -> dict:
+        return self._dev.setdefault(torch.cuda.current_device(), {})
+
+    def device_hashes(self):
+        """(rows int32, signs int8) of the shard's rows on the current device."""
+        c = self._cache()
+        if "hash" not in c:
+            r, s = self.op.device_hashes()
+            c["hash"] = (r[self.r0:self.r1], s[self.r0:self.r1])
+        return c["hash"]
+
     def device_plan(self) -> CountSketchPlan:
-        if self._plan is None:
-            h = self.op._cache().get("hash") if torch.cuda.is_available() else None
-            if h is not None and _native.plan_geometry(self.d)[0] == "owned":
-                # slices of the device draws: the plan is built on the device
-                self._plan = CountSketchPlan.from_device(h[0][self.r0:self.r1],
-                                                         h[1][self.r0:self.r1], self.d,
-                                                         self.r1 - self.r0)
+        c = self._cache()
+        if "plan" not in c:
+            m_loc = self.r1 - self.r0
+            if torch.cuda.is_available() and _native.plan_geometry(self.d)[0] == "owned":
+                h = self.device_hashes()
+                c["plan"] = CountSketchPlan.from_device(h[0], h[1], self.d, m_loc)
             else:
-                self._plan = CountSketchPlan(self.rows, self.signs, self.d)
-        return self._plan
+                c["plan"] = CountSketchPlan(self.rows, self.signs, self.d)
+        return c["plan"]
+
+    def device_buckets(self):
+        """(bucket_rows int32 local, bucket_ptr int64, bucket-ordered signs)
+        of the shard's rows: the CSR of S[:, r0:r1] (within a bucket the rows
+        stay ascending -- the stable sort of the shard's hashes)."""
+        c = self._cache()
+        if "buckets" not in c:
+            rows_d, signs_d = self.device_hashes()
+            order = torch.sort(rows_d, stable=True).indices
+            bptr = torch.zeros(self.d + 1, dtype=torch.int64, device=rows_d.device)
+            bptr[1:] = torch.cumsum(torch.bincount(rows_d, minlength=self.d), 0)
+            c["buckets"] = (order.to(torch.int32), bptr, signs_d[order].contiguous())
+        return c["buckets"]
 
     def device_srht_words(self):
         """Packed sign words of this shard's blocks (device view)."""
@@ -98,6 +195,11 @@ class ShardPlan:
         B = min(self.op.padded_dim, 4096)
         per_block = int(_native.lib().skl_srht_sign_words(B))
         return signs[(self.r0 // B) * per_block:]
+
+    def device_gaussian(self):
+        """(G block view d x (r1 - r0), ld) on the current device."""
+        G, ldg = self.op.device_gaussian_block(self.r0, self.r1)
+        return G, ldg
 
 
 def partial_ld(d: int) -> int:
@@ -109,9 +211,9 @@ def partial_ld(d: int) -> int:
 def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local, dest: int | None = None):
     """Partial [SA | Sb] of one row block on this rank's GPU: a d x (n+1)
     column-major tensor (ld ``partial_ld(d)``) whose last column is the
-    partial Sb.  With ``dest`` (a device address, e.g. this rank's slot in
-    a peer's symmetric buffer) the kernels write there instead and None is
-    returned."""
+    partial Sb.  ``A_local`` is a dense column-major tensor (ld ``lda``) or a
+    CsrBlock.  With ``dest`` (a device address, e.g. this rank's symmetric
+    buffer) the kernels write there instead and None is returned."""
     require_cuda()
     m_loc = plan.r1 - plan.r0
     n = A_local.shape[1]
@@ -123,6 +225,19 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local, dest: int 
     else:
         out, base, col_n = None, int(dest), int(dest) + 8 * ld * n
     st = current_stream()
+    if isinstance(A_local, CsrBlock):
+        if plan.kind == "countsketch":
+            brow, bptr, bsign = plan.device_buckets()
+            _native.call("skl_countsketch_csr", _native.ptr(A_local.indptr),
+                         _native.ptr(A_local.indices), _native.ptr(A_local.values), m_loc, n,
+                         _native.ptr(brow), _native.ptr(bptr), _native.ptr(bsign), d,
+                         _native.ptr(base), ld, st)
+            _native.call("skl_countsketch_dense_ordered", None, m_loc, 0, m_loc,
+                         _native.ptr(b_local), _native.ptr(brow), _native.ptr(bptr),
+                         _native.ptr(bsign), 1.0, d, None, ld, _native.ptr(col_n), 0, st)
+            return out
+        A_local = A_local.dense()
+        lda = m_loc
     if plan.kind == "countsketch":
         plan.device_plan().apply(A_local, m_loc, n, lda, b_local, base, ld, col_n, partitions=1)
     elif plan.kind == "srht":
@@ -133,26 +248,25 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local, dest: int 
                          _native.ptr(words), _native.ptr(sample), plan.op.padded_dim, d, plan.r0,
                          _native.ptr(dst), ld, st)
     else:
-        G, ldg = plan.op.device_gaussian()
-        Gs = G[:, plan.r0:]
+        Gs, ldg = plan.device_gaussian()
         for src, ncol, ldsrc, dst in ((A_local, n, lda, base), (b_local, 1, m_loc, col_n)):
             _native.call("skl_gemm_f64", _native.ptr(Gs), ldg, _native.ptr(src), ldsrc,
                          _native.ptr(dst), ld, d, ncol, m_loc, 0, st)
     return out
 
 
-class PeerSlots:
-    """Fused reduce of the per-rank partials through NVLink peer memory.
+class PeerReduce:
+    """Reduce of the per-rank partials over NVLink peer memory.
 
-    Every rank owns a symmetric buffer of 2 x world slots of ``rows x cols``
-    (column-major, ld ``partial_ld(rows)``); rank r's sketch kernels write
-    their partial into slot r of the destination rank's buffer
-    (``slot_ptr()``, double-buffered by step parity), ``finish()`` runs the
-    device-side barrier and, on the destination, the fixed-order slot sum.
-    The parity buffers make one barrier per step enough: a rank rewrites a
-    slot two steps later, after the barrier that follows the destination's
-    previous sum.  ``timeout_ms`` turns a missing peer into an error instead
-    of a hang."""
+    Every rank owns a symmetric buffer [partial | result] of ``rows x cols``
+    each (column-major, ld ``partial_ld(rows)``).  A rank's sketch kernels
+    write into ``partial_ptr()`` (its own buffer); ``finish()`` runs a
+    device-side barrier, reduces this rank's element block of all partials
+    in rank order into the destination's result buffer (skl_reduce_peers:
+    peer loads, peer stores), and a second barrier publishes the result.
+    Two barriers per step also make one partial buffer enough: no rank
+    rewrites its partial before every rank has finished reading it.
+    ``timeout_ms`` turns a missing peer into an error instead of a hang."""
 
     def __init__(self, rows: int, cols: int, group=None, dst: int = 0, timeout_ms: int = 60000):
         import torch.distributed as dist
@@ -161,36 +275,48 @@ class PeerSlots:
         require_cuda()
         self.group = group if group is not None else dist.group.WORLD
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        if self.world > 16:
+            raise ValueError("PeerReduce supports up to 16 ranks")
         self.rows, self.cols, self.ld = rows, cols, partial_ld(rows)
-        self.slot = cols * self.ld  # elements per slot
-        self.dst, self.timeout_ms, self.step = dst, timeout_ms, 0
-        self.buf = symm_mem.empty(2 * self.world * self.slot, dtype=torch.float64, device="cuda")
+        self.slot = cols * self.ld  # elements per partial
+        self.dst, self.timeout_ms = dst, timeout_ms
+        self.buf = symm_mem.empty(2 * self.slot, dtype=torch.float64, device="cuda")
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
-        self.dst_base = int(self.hdl.buffer_ptrs[dst])
+        self.peers = [int(p) for p in self.hdl.buffer_ptrs]
+        self.e0, self.e1 = element_block(self.slot, self.world, self.rank)
+        self._peer_arr = _native.ptr_array(self.peers)
 
-    def slot_ptr(self) -> int:
-        """Device address of this rank's slot (current step) on the destination."""
-        half = (self.step & 1) * self.world * self.slot
-        return self.dst_base + 8 * (half + self.rank * self.slot)
+    def partial_ptr(self) -> int:
+        """Device address of this rank's partial (its own buffer)."""
+        return self.peers[self.rank]
+
+    def result_view(self):
+        """The reduced rows x cols result (column-major view) on the destination."""
+        r = self.buf[self.slot:].view(self.cols, self.ld).t()
+        return r[: self.rows]
 
     def finish(self, out=None, ldo: int = 0):
-        """Barrier over the ranks' slot writes; on the destination the slots are
-        summed in rank order into ``out`` (rows x cols, ld ``ldo``; None: the
-        barrier only)."""
+        """Barrier, this rank's block of the fixed-order sum into the
+        destination's result, barrier.  On the destination the result is
+        copied into ``out`` (rows x cols, ld ``ldo``) when given; returns the
+        result view there (None elsewhere)."""
         self.hdl.barrier(channel=0, timeout_ms=self.timeout_ms)
-        if self.rank == self.dst and out is not None:
-            half = (self.step & 1) * self.world * self.slot
-            _native.call("skl_sum_slots", self.buf.data_ptr() + 8 * half, self.world, self.slot,
-                         self.rows, self.cols, self.ld, _native.ptr(out), ldo, current_stream())
-        self.step += 1
-        return out
+        _native.call("skl_reduce_peers", self._peer_arr, self.world, self.e0, self.e1,
+                     self.peers[self.dst] + 8 * self.slot, current_stream())
+        self.hdl.barrier(channel=0, timeout_ms=self.timeout_ms)
+        if self.rank != self.dst:
+            return None
+        res = self.result_view()
+        if out is not None:
+            out.copy_(res)
+        return res
 
 
-def peer_slots_or_none(rows: int, cols: int, group=None, dst: int = 0):
-    """PeerSlots when symmetric memory can be set up on this job, else None
+def peer_reduce_or_none(rows: int, cols: int, group=None, dst: int = 0):
+    """PeerReduce when symmetric memory can be set up on this job, else None
     (the caller then falls back to a collective reduce)."""
     try:
-        return PeerSlots(rows, cols, group, dst)
+        return PeerReduce(rows, cols, group, dst)
     except Exception:  # noqa: BLE001 - no symmetric memory: collective fallback
         return None
 
@@ -209,18 +335,35 @@ def reduce_partials(partial, dist, group=None, dst: int = 0):
     return partial
 
 
+def residual_sq_local(A_local, lda: int, b_local, x) -> float:
+    """||A_local x - b_local||^2 of one row block (dense or CsrBlock) on its
+    device (the reference's _residual_norm, solvers.py:102-107, per block)."""
+    out = np.zeros(1)
+    st = current_stream()
+    if isinstance(A_local, CsrBlock):
+        _native.call("skl_residual_csr", _native.ptr(A_local.indptr), _native.ptr(A_local.indices),
+                     _native.ptr(A_local.values), A_local.rows, A_local.cols, _native.ptr(x),
+                     _native.ptr(b_local), _native.ptr(out), st)
+    else:
+        _native.call("skl_residual_dense", _native.ptr(A_local), A_local.shape[0],
+                     A_local.shape[1], lda, _native.ptr(x), _native.ptr(b_local),
+                     _native.ptr(out), st)
+    return float(out[0]) ** 2
+
+
 def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=None,
                              local_apply: Callable | None = None, solve_reduced=None,
                              residual_local=None, collective: str = "auto"):
     """SAA over row-sharded data.  Returns (x, residual_norm, d) on every rank.
 
-    ``local_apply(plan, A_local, b_local) -> partial`` defaults to the CUDA
-    kernel; ``solve_reduced(partial) -> x`` and ``residual_local(A, b, x)``
-    default to the device QR / residual kernels.  The hooks exist so the
-    host-side sharding and collective logic can be exercised on CPU (gloo).
-    ``collective``: "peer" (kernels write into rank 0's symmetric slots,
-    fixed-order sum), "reduce" (one collective reduce), or "auto" (peer when
-    the device path and symmetric memory are available).
+    ``A_local`` is this rank's row block: a dense column-major tensor or a
+    CsrBlock.  ``local_apply(plan, A_local, b_local) -> partial`` defaults to
+    the CUDA kernels; ``solve_reduced(partial) -> x`` and
+    ``residual_local(A, b, x)`` default to the device QR / residual kernels.
+    The hooks exist so the host-side sharding and collective logic can be
+    exercised on CPU (gloo).  ``collective``: "peer" (PeerReduce over
+    symmetric memory), "reduce" (one collective reduce), or "auto" (peer
+    when the device path and symmetric memory are available).
     """
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     r0, r1 = shard_rows(m_total, world, rank)
@@ -230,18 +373,17 @@ def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=N
     plan = ShardPlan(op, r0, r1)
     n = A_local.shape[1]
     d = plan.d
-    slots = None
+    dense = not isinstance(A_local, CsrBlock)
+    lda = (int(A_local.stride(1)) if n > 1 else A_local.shape[0]) if dense else 0
+    peer = None
     if local_apply is None and collective in ("auto", "peer"):
-        slots = PeerSlots(d, n + 1, group) if collective == "peer" else peer_slots_or_none(
+        peer = PeerReduce(d, n + 1, group) if collective == "peer" else peer_reduce_or_none(
             d, n + 1, group)
-    if slots is not None:
-        lda = int(A_local.stride(1)) if n > 1 else A_local.shape[0]
-        local_partial_device(plan, A_local, lda, b_local, dest=slots.slot_ptr())
-        partial = device_f64((d, n + 1), fortran=True, ld=partial_ld(d))
-        slots.finish(partial, partial_ld(d))
+    if peer is not None:
+        local_partial_device(plan, A_local, lda, b_local, dest=peer.partial_ptr())
+        partial = peer.finish()
     else:
         if local_apply is None:
-            lda = int(A_local.stride(1)) if n > 1 else A_local.shape[0]
             partial = local_partial_device(plan, A_local, lda, b_local)
         else:
             partial = local_apply(plan, A_local, b_local)
@@ -254,14 +396,12 @@ def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=N
         else:
             x = solve_reduced(partial)
     else:
-        x = torch.empty(n, dtype=torch.float64, device=partial.device)
+        x = torch.empty(n, dtype=torch.float64,
+                        device=b_local.device if hasattr(b_local, "device") else "cpu")
     dist.broadcast(x, src=0, group=group)
     if residual_local is None:
-        out = np.zeros(1)
-        lda = int(A_local.stride(1)) if n > 1 else A_local.shape[0]
-        _native.call("skl_residual_dense", _native.ptr(A_local), A_local.shape[0], n, lda,
-                     _native.ptr(x), _native.ptr(b_local), _native.ptr(out), current_stream())
-        r2 = torch.tensor([out[0] ** 2], dtype=torch.float64, device=partial.device)
+        r2 = torch.tensor([residual_sq_local(A_local, lda, b_local, x)], dtype=torch.float64,
+                          device=x.device)
     else:
         r2 = residual_local(A_local, b_local, x)
     dist.all_reduce(r2, op=dist.ReduceOp.SUM, group=group)

@@ -183,7 +183,7 @@ class SketchOperator:
     demand for compatibility with code that inspects them."""
 
     __slots__ = ("kind", "source_dim", "target_dim", "_rows", "_signs", "sign_diag",
-                 "row_sample", "padded_dim", "key", "sparsity", "_dev", "_host")
+                 "row_sample", "padded_dim", "key", "sparsity", "_dev", "_host", "_lock")
 
     def __init__(self, kind, source_dim, target_dim, rows=None, signs=None, sign_diag=None,
                  row_sample=None, padded_dim=None, key=None, device_hashes=None, sparsity=None):
@@ -194,19 +194,24 @@ class SketchOperator:
             object.__setattr__(self, name, val)
         object.__setattr__(self, "_dev", {})
         object.__setattr__(self, "_host", {})
+        object.__setattr__(self, "_lock", threading.RLock())
         if device_hashes is not None:
-            self._dev.setdefault(device_hashes[0].device.index, {})["hash"] = device_hashes
+            with torch.cuda.device(device_hashes[0].device):
+                self._cached("hash", lambda: device_hashes)
 
     # CountSketch hashes: built on the device when a GPU is present (see
     # _build_sketch); the host copies are fetched on first use.
     def _host_hashes(self):
-        if "hash" not in self._host:
-            for c in self._dev.values():
-                if "hash" in c:
-                    r, g = c["hash"]
-                    self._host["hash"] = (_freeze(r.cpu().numpy()), _freeze(g.cpu().numpy()))
-                    break
-        return self._host.get("hash")
+        with self._lock:
+            if "hash" not in self._host:
+                for dev, c in list(self._dev.items()):
+                    if "hash" in c:
+                        with torch.cuda.device(dev):
+                            r, g = self._cached("hash", None)
+                            self._host["hash"] = (_freeze(r.cpu().numpy()),
+                                                  _freeze(g.cpu().numpy()))
+                        break
+            return self._host.get("hash")
 
     @property
     def rows(self):
@@ -259,81 +264,135 @@ class SketchOperator:
         return self._host["g"]
 
     # ------------------------------------------------------------ device caches
+    # Per-device artifacts (hashes, plans, bucket lists, SRHT words, G) are
+    # built once on the stream of the first caller and shared with callers
+    # on any stream: each entry keeps the event recorded after its build,
+    # every consumer's stream waits on it, and the tensors are recorded on
+    # the consumer's stream so an evicted operator's memory is not reused
+    # while a kernel on another stream still reads it.
     def _cache(self):
         dev = torch.cuda.current_device()
-        return self._dev.setdefault(dev, {})
+        with self._lock:
+            return self._dev.setdefault(dev, {})
+
+    def _cached(self, name: str, build):
+        c = self._cache()
+        with self._lock:
+            entry = c.get(name)
+            if entry is None:
+                if build is None:
+                    return None
+                value = build()
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())
+                entry = c[name] = (value, ev)
+        value, ev = entry
+        st = torch.cuda.current_stream()
+        st.wait_event(ev)
+        for t in _tensors_of(value):
+            t.record_stream(st)
+        return value
 
     def device_plan(self) -> CountSketchPlan:
         """The CountSketch apply plan on the current device (built once; on
         the device from device hashes when they are there)."""
         require_cuda()
-        c = self._cache()
-        if "plan" not in c and self.kind == "sparsesign":
-            # register-owned plan up to d = 4096, shared-memory lane lists beyond
-            c["plan"] = CountSketchPlan(self.rows, self.signs, self.target_dim,
-                                        spr=self.sparsity)
-        if "plan" not in c:
+
+        def build():
+            if self.kind == "sparsesign":
+                # register-owned plan up to d = 4096, shared-memory lane lists beyond
+                return CountSketchPlan(self.rows, self.signs, self.target_dim, spr=self.sparsity)
             d = self.target_dim
-            if "hash" in c and _native.plan_geometry(d)[0] == "owned":
-                c["plan"] = CountSketchPlan.from_device(c["hash"][0], c["hash"][1], d,
-                                                        self.source_dim)
-            else:
-                c["plan"] = CountSketchPlan(self.rows, self.signs, d)
-        return c["plan"]
+            if _native.plan_geometry(d)[0] == "owned":
+                rows_d, signs_d = self.device_hashes()
+                return CountSketchPlan.from_device(rows_d, signs_d, d, self.source_dim)
+            return CountSketchPlan(self.rows, self.signs, d)
+
+        return self._cached("plan", build)
 
     def device_hashes(self):
         """CountSketch hashes in row order on the current device: (rows int32,
-        signs int8) -- drawn there by _build_sketch, else uploaded once."""
+        signs int8) -- drawn there from the operator's key (the device draw
+        is bit-identical to the host walk), else uploaded once."""
         require_cuda()
-        c = self._cache()
-        if "hash" not in c:
-            c["hash"] = (to_device(np.ascontiguousarray(self.rows, dtype=np.int32)),
-                         to_device(np.ascontiguousarray(self.signs, dtype=np.int8)))
-        return c["hash"]
+
+        def build():
+            if self.kind == "countsketch" and self.key is not None:
+                m, d = self.source_dim, self.target_dim
+                rows_d = torch.empty(m, dtype=torch.int32, device="cuda")
+                signs_d = torch.empty(m, dtype=torch.int8, device="cuda")
+                _native.call("skl_rng_countsketch_device", self.key, m, d, _native.ptr(rows_d),
+                             _native.ptr(signs_d), current_stream())
+                return rows_d, signs_d
+            return (to_device(np.ascontiguousarray(self.rows, dtype=np.int32)),
+                    to_device(np.ascontiguousarray(self.signs, dtype=np.int8)))
+
+        return self._cached("hash", build)
 
     def device_buckets(self):
         """(bucket_rows int32, bucket_ptr int64, bucket-ordered signs int8) on
         the current device: the CSR of S consumed by the CSR-operand kernel
-        (for a sparse sign embedding each source row appears in s buckets)."""
+        and the ordered few-column walk (for a sparse sign embedding each
+        source row appears in s buckets)."""
         require_cuda()
-        c = self._cache()
-        if "buckets" not in c and self.kind == "countsketch":
-            # stable sort of the row-order hashes by bucket, on the device
-            rows_d, signs_d = self.device_hashes()
-            order = torch.sort(rows_d, stable=True).indices
-            bptr = torch.zeros(self.target_dim + 1, dtype=torch.int64, device=rows_d.device)
-            bptr[1:] = torch.cumsum(torch.bincount(rows_d, minlength=self.target_dim), 0)
-            c["buckets"] = (order.to(torch.int32), bptr, signs_d[order].contiguous())
-        if "buckets" not in c:
+
+        def build():
+            if self.kind == "countsketch":
+                # stable sort of the row-order hashes by bucket, on the device
+                rows_d, signs_d = self.device_hashes()
+                order = torch.sort(rows_d, stable=True).indices
+                bptr = torch.zeros(self.target_dim + 1, dtype=torch.int64, device=rows_d.device)
+                bptr[1:] = torch.cumsum(torch.bincount(rows_d, minlength=self.target_dim), 0)
+                return order.to(torch.int32), bptr, signs_d[order].contiguous()
             spr = self.sparsity if self.kind == "sparsesign" else 1
             flat_rows = np.ascontiguousarray(self.rows.reshape(-1), dtype=np.int32)
             ent, bptr = _native.countsketch_buckets(flat_rows, self.target_dim)
             bsign = np.ascontiguousarray(self.signs.reshape(-1)[ent])
             brow = (ent // spr).astype(np.int32) if spr > 1 else ent
-            c["buckets"] = (to_device(brow), to_device(bptr), to_device(bsign))
-        return c["buckets"]
+            return to_device(brow), to_device(bptr), to_device(bsign)
+
+        return self._cached("buckets", build)
 
     def device_srht(self):
         require_cuda()
-        c = self._cache()
-        if "srht" not in c:
+
+        def build():
             signs8 = np.where(self.sign_diag > 0, 1, -1).astype(np.int8)
-            c["srht"] = (to_device(_native.srht_pack_signs(signs8)), to_device(self.row_sample))
-        return c["srht"]
+            return to_device(_native.srht_pack_signs(signs8)), to_device(self.row_sample)
+
+        return self._cached("srht", build)
+
+    def device_gaussian_block(self, r0: int, r1: int):
+        """(G[:, r0:r1] view, ld) on the current device: the column block a
+        row shard [r0, r1) of A multiplies."""
+        G, ldg = self.device_gaussian()
+        return G[:, r0:r1], ldg
 
     def device_gaussian(self):
         """G (d x m, row-major like numpy's C order, ld = ldg) on the device."""
         require_cuda()
-        c = self._cache()
-        if "gauss" not in c:
+
+        def build():
             d, m = self.target_dim, self.source_dim
             ldg = (m + 31) // 32 * 32
             G = torch.empty((d, ldg), dtype=torch.float64, device="cuda")
             _native.install_gaussian_tables()
             _native.call("skl_rng_gaussian_device", self.key, d, m, _native.ptr(G), ldg,
                          current_stream())
-            c["gauss"] = (G, ldg)
-        return c["gauss"]
+            return G, ldg
+
+        return self._cached("gauss", build)
+
+
+def _tensors_of(value):
+    """The CUDA tensors inside a cached artifact (tensor, tuple, or plan)."""
+    if torch is not None and isinstance(value, torch.Tensor):
+        return (value,) if value.is_cuda else ()
+    if isinstance(value, (tuple, list)):
+        return tuple(t for v in value for t in _tensors_of(v))
+    if isinstance(value, CountSketchPlan):
+        return tuple(t for t in (value.lanes, value.off) if isinstance(t, torch.Tensor))
+    return ()
 
 
 _OP_CACHE: "OrderedDict[tuple, SketchOperator]" = OrderedDict()

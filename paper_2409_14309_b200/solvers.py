@@ -60,14 +60,17 @@ class LeastSquaresProblem:
 
 @dataclass(frozen=True)
 class SolverOptions:
-    """Tolerances and sizing knobs (solvers.py:63-87).  Only d_factor matters
-    to sketch-and-apply."""
+    """Tolerances and sizing knobs (solvers.py:63-87).  Sketch-and-apply uses
+    d_factor and the engine's ``devices`` list."""
 
     atol: float = 1e-10
     btol: float = 1e-10
     max_iter: int | None = None
     d_factor: float = 4.0
     warm_start: bool = True
+    # Engine option (not in the reference): CUDA devices the sketch-and-apply
+    # shards A's rows over (multidevice.py); None = the current device.
+    devices: tuple[int, ...] | None = None
 
     def __post_init__(self) -> None:
         if not (self.atol > 0 and self.btol > 0):
@@ -76,6 +79,10 @@ class SolverOptions:
             raise SpecError("max_iter must be >= 1")
         if self.d_factor < 1:
             raise SpecError("d_factor must be >= 1")
+        if self.devices is not None:
+            from .multidevice import check_devices
+
+            object.__setattr__(self, "devices", check_devices(self.devices))
 
     def resolve_max_iter(self, n: int) -> int:
         return 4 * n if self.max_iter is None else self.max_iter
@@ -148,6 +155,11 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
     opts = opts or SolverOptions()
     op_spec = _operator_spec(spec, "saa", A.rows, A.cols, opts.d_factor)
     t0 = time.perf_counter()
+    if opts.devices is not None and len(opts.devices) > 1:
+        return _sketch_and_apply_devices(A, b, op_spec, opts.devices, t0)
+    if opts.devices is not None:
+        with torch.cuda.device(opts.devices[0]):
+            return sketch_and_apply(problem, spec, replace(opts, devices=None))
     op = build_sketch(op_spec, A.rows)
     SA, Sb, A_dev, lda, b_dev = sketch_operands_device(op, A, b)
     d = op.target_dim
@@ -160,6 +172,26 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
     wall = time.perf_counter() - t0
     rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
     x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
+    return SolveResult(x=Vector(x), method="saa", sketch=op_spec.kind, d=d, iterations=0,
+                       residual_norm=rnorm, termination="direct", wall_time_s=wall)
+
+
+def _sketch_and_apply_devices(A: Matrix, b: Vector, op_spec: SketchSpec, devices, t0: float):
+    """SAA with A's rows sharded over several devices (multidevice.py); the
+    operator is the global one (same hashes/signs/samples as one device)."""
+    from .multidevice import sketch_and_apply_devices
+
+    with torch.cuda.device(devices[0]):
+        op = build_sketch(op_spec, A.rows)
+        d = op.target_dim
+        try:
+            x_dev, rnorm = sketch_and_apply_devices(op, A, b, devices)
+        except SingularFactorError as exc:
+            raise SingularFactorError(
+                f"sketched matrix ({op_spec.kind}, d={d}) is rank deficient: {exc}; "
+                f"a larger embedding dimension may help") from exc
+        wall = time.perf_counter() - t0
+        x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
     return SolveResult(x=Vector(x), method="saa", sketch=op_spec.kind, d=d, iterations=0,
                        residual_norm=rnorm, termination="direct", wall_time_s=wall)
 

@@ -176,20 +176,91 @@ def test_srht_shard_must_be_block_aligned():
         ShardPlan(op, 100, 20_000)
 
 
-def test_peer_slots_pointer_parity():
-    """PeerSlots' slot addressing (host logic, no device): rank r writes slot r
-    of the destination's buffer, alternating halves by step parity."""
-    from paper_2409_14309_b200.distributed import PeerSlots, partial_ld
+def test_element_blocks_tile_and_align():
+    """PeerReduce's reduce-scatter split (host logic): the ranks' element
+    blocks tile the partial exactly, start 16-byte aligned and are near-equal."""
+    from paper_2409_14309_b200.distributed import element_block, partial_ld
 
-    s = PeerSlots.__new__(PeerSlots)
-    s.rank, s.world, s.rows, s.cols = 2, 4, 100, 7
-    s.ld = partial_ld(100)
-    s.slot = s.cols * s.ld
-    s.dst_base, s.step = 1 << 40, 0
-    half = 4 * s.slot * 8
-    assert s.slot_ptr() == (1 << 40) + 8 * 2 * s.slot
-    s.step = 1
-    assert s.slot_ptr() == (1 << 40) + half + 8 * 2 * s.slot
-    s.step = 2
-    assert s.slot_ptr() == (1 << 40) + 8 * 2 * s.slot
-    assert s.ld == 100 and partial_ld(101) == 102
+    for total in (1, 2, 7, 96 * 13, 8192 * 1025, 2048 * 257):
+        for world in (1, 2, 3, 8, 16):
+            spans = [element_block(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0
+            assert all(e0 % 2 == 0 for e0, _ in spans)
+            sizes = [e1 - e0 for e0, e1 in spans]
+            assert max(sizes) - min(sizes) <= 2 or total < 2 * world
+    assert partial_ld(100) == 100 and partial_ld(101) == 102
+
+
+def _csr_problem(m, n, seed=3):
+    import scipy.sparse
+
+    rng = np.random.default_rng(seed)
+    A = scipy.sparse.random(m, n, density=0.02, format="csr", random_state=seed,
+                            data_rvs=rng.standard_normal)
+    A.sort_indices()
+    b = A @ rng.standard_normal(n) + 1e-3 * rng.standard_normal(m)
+    return A, b
+
+
+def _csr_worker(rank, world, port, m, n, d, seed, out):
+    import scipy.sparse
+
+    from paper_2409_14309_b200.distributed import csr_row_block
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, b = _csr_problem(m, n)
+        r0, r1 = shard_rows(m, world, rank)
+        blk = csr_row_block(A, r0, r1, device="cpu")
+        assert blk.shape == (r1 - r0, n) and int(blk.indptr[0]) == 0
+        assert blk.nnz == int(A.indptr[r1] - A.indptr[r0])
+
+        def to_sp(block):
+            return scipy.sparse.csr_matrix((block.values.numpy(), block.indices.numpy(),
+                                            block.indptr.numpy()), shape=block.shape)
+
+        def local(plan, A_local, b_local):
+            rows, signs = plan.rows.astype(np.int64), plan.signs.astype(np.float64)
+            SA = O.countsketch_apply(rows, signs, plan.d, to_sp(A_local))
+            Sb = O.countsketch_apply(rows, signs, plan.d, b_local.numpy())
+            return torch.from_numpy(np.asfortranarray(np.column_stack([SA, Sb])))
+
+        def r2(A_local, b_local, x):
+            r = to_sp(A_local) @ x.numpy() - b_local.numpy()
+            return torch.tensor([float(r @ r)], dtype=torch.float64)
+
+        x, rnorm, dd = sharded_sketch_and_apply(
+            blk, torch.from_numpy(b[r0:r1].copy()), m, SketchSpec("countsketch", d, seed=seed),
+            dist, local_apply=local, solve_reduced=_oracle_solve, residual_local=r2)
+        out[rank] = (x.numpy().copy(), rnorm, dd)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_csr_row_blocks():
+    """CSR row sharding (config 4's layout): each rank holds rows [r0, r1) of
+    the CSR with a rebased indptr and sketches them with the global hashes of
+    those rows; the reduced partials solve to the single-process answer."""
+    m, n, d, seed = 30_000, 40, 256, 9
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_csr_worker, args=(2, port, m, n, d, seed, out), nprocs=2, join=True)
+    A, b = _csr_problem(m, n)
+    rows, signs = O.countsketch_draws(O.derive_seed(seed, "countsketch", m), m, d)
+    SA = O.countsketch_apply(rows, signs, d, A)
+    Sb = O.countsketch_apply(rows, signs, d, b)
+    q, r = O.economy_qr(SA)
+    import scipy.linalg
+
+    x_ref = scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False)
+    r_ref = np.linalg.norm(A @ x_ref - b)
+    for rank in range(2):
+        x, rnorm, dd = out[rank]
+        assert dd == d
+        assert np.linalg.norm(x - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
+        assert abs(rnorm - r_ref) <= 1e-12 * r_ref
