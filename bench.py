@@ -57,15 +57,22 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic():
-    """dram bytes per launch of the CountSketch kernel from the committed
-    ncu --set full capture summary (profiles/*countsketch*_full.json)."""
+def profiled_traffic(kernel_regex: str):
+    """DRAM bytes per launch of the timed kernel from the committed ncu
+    --set full capture summaries (profiles/*countsketch*_full.json): only a
+    capture whose kernel name matches the kernel this run timed counts (the
+    newest such file); None otherwise."""
+    import re
+
     best = None
     for f in sorted((ROOT / "profiles").glob("*countsketch*full*.json")):
         try:
-            best = json.loads(f.read_text()).get("dram_bytes_per_launch")
+            summ = json.loads(f.read_text())
         except Exception:
-            pass
+            continue
+        name = str(summ.get("metrics", {}).get("Kernel Name", ""))
+        if re.search(kernel_regex, name):
+            best = (summ.get("dram_bytes_per_launch"), f.name, name)
     return best
 
 
@@ -186,6 +193,42 @@ def cpu_reference_sample(cfg, A_host: np.ndarray, b_host: np.ndarray, rows, sign
     return bytes_ / t / 1e9, t, times, threads
 
 
+def cpu_stock_apply(A_host: np.ndarray, b_host: np.ndarray, rows, signs, d: int):
+    """The reference's own apply as it stands (sketch.py:209-212 on the
+    column-major DenseMatrix, linalg.py:38): `sparse_map @ A.data` -- scipy's
+    single-threaded csr_matvecs after its internal F->C copy of A -- plus
+    `sparse_map @ b`, once, on the full block."""
+    from oracle import oracle as O
+
+    smap = O.countsketch_map(np.asarray(rows, np.int64), np.asarray(signs, np.float64), d,
+                             A_host.shape[0])
+    t0 = time.perf_counter()
+    smap @ A_host
+    smap @ b_host
+    t = time.perf_counter() - t0
+    return {"value": round((8 * A_host.size + 8 * b_host.size) / t / 1e9, 4), "unit": "GB/s",
+            "cores": 1, "seconds": round(t, 3),
+            "what": "sparse_map @ A (F-ordered, incl. scipy's F->C copy) + sparse_map @ b, once"}
+
+
+def cpu_reference_solve(A_host: np.ndarray, b_host: np.ndarray, d_factor: float):
+    """One solve(problem, "saa", SketchSpec("countsketch", 1, SEED),
+    SolverOptions(d_factor)) of the reference's algorithm on the host (the
+    oracle restatement of solvers.py:296-320: operator draws, sparse_map @ A,
+    numpy QR, triangular solve, ||Ax - b||), timed like the reference's
+    wall_time_s (solvers.py:374/397)."""
+    from oracle import oracle as O
+    from paper_2409_14309_b200 import workloads as W
+
+    t0 = time.perf_counter()
+    res = O.saa_solve(A_host, b_host, "countsketch", W.SEED, d_factor)
+    t = time.perf_counter() - t0
+    return {"solves_per_sec": round(1.0 / t, 4), "seconds": round(t, 3),
+            "residual": res["residual"], "cores": host_threads(),
+            "what": "oracle saa_solve on the full block: draws + scipy csr @ A (1 thread) + "
+                    "numpy QR / solve_triangular / residual (OpenBLAS, all cores)"}
+
+
 def run_reference_arm(args, cfg):
     import torch
 
@@ -195,8 +238,8 @@ def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # bounded sample of the same workload: the first ms rows of config 2
-    ms = 1 << 17
+    # the full config-2 block: one step = S[A|b] over all 2^20 rows
+    ms = cfg.m
     c = W.config(cfg.cfg, m=ms)
     if torch.cuda.is_available():
         A, b, _ = W.make_problem(c, backend="torch")
@@ -211,7 +254,7 @@ def run_reference_arm(args, cfg):
     _, _, _, threads = cpu_reference_sample(cfg, A_host, b_host, rows, signs, args.warmup)
     _, t, times, _ = cpu_reference_sample(cfg, A_host, b_host, rows, signs, args.steps, threads)
     gbs = (8 * A_host.size + 8 * b_host.size) / t / 1e9
-    sample = (f"first {ms} of {cfg.m} rows of config {cfg.cfg} (A {ms}x{cfg.n} column-major + b), "
+    sample = (f"all {ms} rows of config {cfg.cfg} (A {ms}x{cfg.n} column-major + b), "
               f"scipy CSR @ A as sketch.py:209-212, {threads} row blocks on {threads} threads; "
               f"median of {args.steps}")
     line = {
@@ -221,7 +264,7 @@ def run_reference_arm(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config {cfg.cfg}: dense {cfg.m}x{cfg.n} fp64 (kappa=1e8) per GPU, "
-                               f"CountSketch d={cfg.d}, one pass S[A|b]; bounded host sample",
+                               f"CountSketch d={cfg.d}, one pass S[A|b]",
                    "m_per_gpu": cfg.m, "n": cfg.n, "d": cfg.d, "m_sample": ms,
                    "parallelism": f"{threads} host threads"},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
@@ -270,6 +313,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the check of the timed output against the oracle")
     ap.add_argument("--launch-check", action="store_true",
                     help="form the N-rank world (relaunching under torchrun if needed), "
                          "all-reduce once, print the world rank 0 saw, exit")
@@ -453,6 +498,24 @@ def main():
         qb.record(stream)
         torch.cuda.synchronize()
         qr_ms = qa.elapsed_time(qb) / reps
+        # host-input solves: pinned host carriers through solve(); the sketch
+        # streams row blocks of A to the device under the kernel and keeps the
+        # device copy for the residual pass (skl_countsketch_dense_owned_host
+        # with A_dev_keep), x comes back to the host
+        from paper_2409_14309_b200._device import pinned_empty_f64
+
+        Ah_solve = pinned_empty_f64((m_loc, n), fortran=True)
+        Ah_solve[...] = A.cpu().numpy()
+        bh_solve = pinned_empty_f64((m_loc,))
+        bh_solve[...] = b.cpu().numpy()
+        prob_h = E.LeastSquaresProblem(A=E.DenseMatrix(Ah_solve), b=E.Vector(bh_solve))
+        res_h = E.solve(prob_h, "saa", sspec, opts)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            res_h = E.solve(prob_h, "saa", sspec, opts)
+        host_s = (time.perf_counter() - t0) / 3
+        host_x_err = float(np.linalg.norm(res_h.x.data - res.x.data.cpu().numpy())
+                           / np.linalg.norm(res_h.x.data))
         # sketch-and-precondition: LSQR preconditioned by R
         sap_opts = E.SolverOptions(d_factor=d / n)
         E.solve(prob, "sap", sspec, sap_opts)
@@ -468,10 +531,15 @@ def main():
                  "solves_per_sec_cold": round(1.0 / cold_s, 3),
                  "ms_per_solve_cold": round(cold_s * 1e3, 3),
                  "qr_solve_ms": round(qr_ms, 3), "residual": res.residual_norm,
+                 "host_solves_per_sec": round(1.0 / host_s, 3),
+                 "host_ms_per_solve": round(host_s * 1e3, 3),
+                 "host_vs_device_x_rel_diff": host_x_err,
                  "operator_build_ms": round(build_s * 1e3, 2),
                  "includes": "sketch S[A|b], QR, back-solve, residual on device-resident A; "
                              "the *_cold figures also rebuild the operator (device RNG + "
-                             "device plan) every solve, as the reference does"}
+                             "device plan) every solve, as the reference does; host_* solves "
+                             "take pinned host A,b (H2D streamed under the sketch, device copy "
+                             "kept for the residual, x to the host)"}
 
     # ---- e2e through the C-ABI host-buffer entry point
     e2e = None
@@ -509,17 +577,48 @@ def main():
             # parity of the timed output against the device run (bitwise)
             assert np.array_equal(SAh, out[:, :n].cpu().numpy())
 
+    # parity of the timed output: the device S[A|b] of the timed loop against
+    # the oracle's csr_matvecs fold (threaded C restatement), bitwise
+    parity = None
+    if world == 1 and not args.no_parity:
+        from oracle import clib
+
+        A_host = np.asfortranarray(A.cpu().numpy())
+        b_host = b.cpu().numpy()
+        rows_h, signs_h = op.rows, op.signs
+        want = clib.countsketch_apply_mt(rows_h, signs_h, d, A_host)
+        want_b = clib.countsketch_apply_mt(rows_h, signs_h, d, b_host)
+        got = out.cpu().numpy()
+        bitwise = bool(np.array_equal(got[:, :n], want) and np.array_equal(got[:, n], want_b))
+        parity = {"timed_output_vs_oracle": "bitwise" if bitwise else "MISMATCH",
+                  "oracle": "oracle/c/apply_oracle.c (scipy csr_matvecs fold, sketch.py:209-212)"}
+        if not bitwise:
+            print("bench.py: timed S[A|b] differs from the oracle", file=sys.stderr)
+            sys.exit(3)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU leg: rank 0 at N = 1 only
-        ms = 1 << 17
-        Ah_s = np.asfortranarray(A[:ms].cpu().numpy())
-        bh_s = b[:ms].cpu().numpy()
-        gbs, t, _, threads = cpu_reference_sample(cfg, Ah_s, bh_s, op.rows, op.signs, 5)
+        A_host = np.asfortranarray(A.cpu().numpy()) if parity is None else A_host
+        b_host = b.cpu().numpy() if parity is None else b_host
+        gbs, t, _, threads = cpu_reference_sample(cfg, A_host, b_host, op.rows, op.signs, 3)
+        stock = cpu_stock_apply(A_host, b_host, op.rows, op.signs, d)
+        ref_solve = cpu_reference_solve(A_host, b_host, d / n)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"first {ms} rows x {n} (+b) of the config-{cfg.cfg} block, column-major, "
-                         f"scipy CSR @ A (the reference's csr_matvecs path) in {threads} row blocks "
-                         f"on {threads} threads, median of 5 = {t * 1e3:.1f} ms"}
-
+               "sample": f"the full config-{cfg.cfg} block ({m_loc} x {n} column-major + b), "
+                         f"scipy CSR @ A (the reference's csr_matvecs path, sketch.py:209-212) in "
+                         f"{threads} row blocks on {threads} threads, median of 3 = "
+                         f"{t * 1e3:.1f} ms",
+               "stock_single_thread": stock,
+               "reference_saa_solve": ref_solve}
+    if cs_plan.kind == "owned":
+        threads = 32 * cs_plan.warps
+        nsl = 4 if d <= threads * 4 else 8
+        kernel_name = f"skl::countsketch_owned_kernel<{threads}, 0, {nsl}>"
+        kernel_rx = rf"countsketch_owned_kernel<{threads},\s*(0|false),\s*{nsl}>"
+    else:
+        kernel_name = f"skl::countsketch_dense_kernel<{32 * cs_plan.warps}, ...>"
+        kernel_rx = rf"countsketch_dense_kernel<{32 * cs_plan.warps}\b"
+    traffic = profiled_traffic(kernel_rx)
     if rank == 0:
         line = {
             "metric": metric_name(cfg),
@@ -531,19 +630,25 @@ def main():
                                    f"CountSketch d={d}, one pass S[A|b]"
                                    + (" + reduce of the d x (n+1) partials" if world > 1 else ""),
                        "collective": collective,
+                       "ranks": world,
+                       "launcher": ("torchrun" if "LOCAL_WORLD_SIZE" in os.environ
+                                    else "none (single process)"),
                        "m_per_gpu": m_loc, "n": n, "d": d, "m_total": m_total,
                        "parallelism": f"rows sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (2 GiB of A per GPU per step); no flush"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": profiled_traffic(), "peak_source": peak_src,
-                         "kernel": (f"countsketch_owned_kernel<{32 * cs_plan.warps}>" if cs_plan.kind == "owned"
-                           else f"countsketch_dense_kernel<{32 * cs_plan.warps},1>"),
+                         "traffic": traffic[0] if traffic else None,
+                         "traffic_source": (f"profiles/{traffic[1]}: {traffic[2]}" if traffic
+                                            else "no ncu capture of this kernel"),
+                         "peak_source": peak_src,
+                         "kernel": kernel_name,
                          "kernel_ms": round(kern_avg, 4),
                          "algorithmic_bytes_per_launch": bytes_local,
                          "frac_of_8TBps": round(achieved / 8000.0, 4)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "parity": parity,
             "clocks": clocks.summary(),
             # our kernels per timed step: the sketch, plus this rank's block of
             # the peer reduce

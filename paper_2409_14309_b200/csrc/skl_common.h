@@ -63,7 +63,9 @@ inline int64_t owned_max_chunk(int slots) { return (1LL << owned_row_bits(slots)
   } while (0)
 
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <utility>
 
 namespace skl {
 // SM count of the current device, cached per device (thread-safe).
@@ -92,24 +94,65 @@ inline int once_per_device(std::once_flag* flags /* [64] */, F&& f) {
   return rc;
 }
 
-// Stream-ordered workspace allocation.  The first call on a device raises
-// the default memory pool's release threshold so freed workspaces stay
-// mapped across stream synchronisations (the default threshold of 0 unmaps
-// them at every sync and the next call pays the remap, milliseconds for the
-// QR's workspaces).
-template <class T>
-inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
-  static std::once_flag retained[64];
-  once_per_device(retained, [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
+// Raise (never lower) a kernel's dynamic shared-memory limit on the current
+// device.  The attribute is process-global: setting it to each call's own
+// size would let a concurrent caller with a smaller size lower it between
+// another thread's set and launch, failing that launch.  Only ever raising
+// it keeps every request that was granted valid.
+inline cudaError_t raise_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = granted[{dev, func}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+template <class K>
+inline cudaError_t raise_smem_limit(K* kernel, size_t bytes) {
+  return raise_smem_limit(reinterpret_cast<const void*>(kernel), bytes);
+}
+
+// Stream-ordered workspace allocation from a memory pool the library owns
+// (one per device, created on first use), not the device's default pool:
+// memory it keeps cached is the library's alone.  Up to kPoolKeepBytes stay
+// mapped across stream synchronisations, so the per-call workspaces of the
+// QR, split-K partials and host-streaming rings are reused without a remap;
+// anything above that (a one-off multi-GiB workspace) goes back to the
+// driver at the next synchronisation instead of staying mapped for the life
+// of the process, out of reach of torch's allocator.
+constexpr uint64_t kPoolKeepBytes = 1ULL << 30;
+
+inline cudaMemPool_t library_pool() {
+  static std::once_flag made[64];
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  once_per_device(made, [dev] {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      uint64_t keep = kPoolKeepBytes;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = pool;
     }
     return 0;
   });
-  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+  return pools[dev];
+}
+
+template <class T>
+inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = library_pool();
+  if (!pool) return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
 }
 }  // namespace skl
 #endif

@@ -397,7 +397,7 @@ template <int NT, int C>
 static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   auto kern = p.scale != 1.0 ? countsketch_dense_kernel<NT, C, true>
                              : countsketch_dense_kernel<NT, C, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
@@ -421,7 +421,10 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
                               int64_t d, int64_t chunk, int warps, double* SA, int64_t ldsa,
                               double* Sb, int partitions, int accumulate, int64_t row_begin,
                               int64_t row_end, cudaStream_t st, double scale = 1.0) {
-  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+  // rows are addressed absolutely in [row_begin, row_end): the columns of
+  // that window must not overlap (the host-streaming ring passes a base
+  // pointer offset by -row_begin with lda = the slot height)
+  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= row_end - row_begin && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld lda=%lld ldsa=%lld", (long long)m,
               (long long)n, (long long)d, (long long)lda, (long long)ldsa);
   SKL_REQUIRE(d <= 32767, SKL_ERR_SPEC, "countsketch: embed_dim %lld > 32767 not supported",
@@ -495,7 +498,7 @@ static int countsketch_launch(const double* A, int64_t m, int64_t n, int64_t lda
 template <int NT, bool SC, int SL>
 static cudaError_t launch_owned(const OwParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   auto k = countsketch_owned_kernel<NT, SC, SL>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = raise_smem_limit(k, smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
@@ -529,7 +532,10 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
                                     int64_t chunk, int warps, double* SA, int64_t ldsa, double* Sb,
                                     int partitions, int accumulate, int64_t row_begin,
                                     int64_t row_end, cudaStream_t st, double scale = 1.0) {
-  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d, SKL_ERR_SHAPE,
+  // rows are addressed absolutely in [row_begin, row_end): the columns of
+  // that window must not overlap (the host-streaming ring passes a base
+  // pointer offset by -row_begin with lda = the slot height)
+  SKL_REQUIRE(m >= 1 && n >= 1 && d >= 1 && lda >= row_end - row_begin && ldsa >= d, SKL_ERR_SHAPE,
               "countsketch: bad shape m=%lld n=%lld d=%lld", (long long)m, (long long)n,
               (long long)d);
   const int nsl = owned_slots(d, warps);
@@ -691,9 +697,10 @@ static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, i
               SKL_ERR_INVALID, "countsketch_host: bad A_dev_keep / ld_keep");
   // blocks of whole plan chunks, ~64 MiB of A each (chunk is even, so every
   // block start keeps the slot pointer A_slot - r0 16-byte aligned)
+  static const int64_t block_mb = getenv("SKL_HOST_BLOCK_MB") ? atoll(getenv("SKL_HOST_BLOCK_MB")) : 64;
   const int64_t rows_per_block =
       std::min<int64_t>((m + chunk - 1) / chunk * chunk,
-                        std::max<int64_t>(chunk, ((64LL << 20) / (8 * n)) / chunk * chunk));
+                        std::max<int64_t>(chunk, ((block_mb << 20) / (8 * n)) / chunk * chunk));
   const int64_t nblk = (m + rows_per_block - 1) / rows_per_block;
   HostStreamCtx* cx = nullptr;
   int rc = host_stream_ctx(&cx, (size_t)(2 * nblk + 1));

@@ -359,7 +359,7 @@ extern "C" int skl_countsketch_plan_owned_device(const int32_t* rows, const int8
   }
   const size_t smem = (size_t)PB_KEYS * 4 + (size_t)d * 8 + (size_t)chunk;
   auto fill = nsl == 4 ? owned_fill_kernel<4> : owned_fill_kernel<8>;
-  SKL_CUDA(cudaFuncSetAttribute(fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SKL_CUDA(raise_smem_limit(fill, smem));
   fill<<<(unsigned)nch, PB_NT, smem, st>>>(rows, signs, m, (int)d, (int)chunk, warps, maxlen,
                                            chunk_off, lanes);
   SKL_CUDA_LAUNCH();

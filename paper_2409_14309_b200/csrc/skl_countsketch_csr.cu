@@ -210,8 +210,7 @@ static int csr_launch(const int64_t* indptr, const int64_t* indices, const doubl
   const int64_t max_cw = (192 * 1024) / (CSR_B * 8) - 1;
   const int64_t Cw = std::min<int64_t>(n, max_cw);
   const size_t smem = (size_t)(Cw + 1) * CSR_B * sizeof(double);
-  SKL_CUDA(cudaFuncSetAttribute(countsketch_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  SKL_CUDA(raise_smem_limit(countsketch_csr_kernel, smem));
   dim3 grid((unsigned)((d + CSR_B - 1) / CSR_B), (unsigned)((n + Cw - 1) / Cw));
   countsketch_csr_kernel<<<grid, CSR_B * 32, smem, st>>>(indptr, indices, values, bucket_rows,
                                                          bucket_ptr, signs, d, n, Cw, SA, ldsa,

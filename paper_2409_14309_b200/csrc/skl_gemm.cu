@@ -251,8 +251,7 @@ extern "C" int skl_gemm_f64(const double* G, int64_t ldg, const double* A, int64
     p.C = C;
   }
   const size_t smem = (size_t)GM_STAGES * (GM_BM + GM_BN) * GM_LD * sizeof(double);
-  SKL_CUDA(cudaFuncSetAttribute(gemm_f64_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  SKL_CUDA(raise_smem_limit(gemm_f64_dmma_kernel, smem));
   dim3 grid((unsigned)((n + GM_BN - 1) / GM_BN), (unsigned)((d + GM_BM - 1) / GM_BM), (unsigned)S);
   gemm_f64_dmma_kernel<<<grid, GM_THREADS, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();

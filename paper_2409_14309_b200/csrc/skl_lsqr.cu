@@ -561,10 +561,15 @@ extern "C" int skl_lsqr_gemv_t(const double* A, int64_t m, int64_t n, int64_t ld
   SKL_REQUIRE(((uintptr_t)u_n & 15) == 0, SKL_ERR_INVALID, "lsqr_gemv_t: u_n must be 16-byte aligned");
   const int64_t groups = (n + LQ_TC - 1) / LQ_TC;
   // one wave: row chunks so that groups x chunks fills the resident CTA slots
-  static int occ = 0;
+  // resident CTAs per SM, cached per device (atomic: concurrent callers)
+  static std::atomic<int> occ_cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int occ = (dev >= 0 && dev < 64) ? occ_cache[dev].load(std::memory_order_relaxed) : 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_gemv_t_kernel, LQ_NT, 0);
     occ = std::max(occ, 1);
+    if (dev >= 0 && dev < 64) occ_cache[dev].store(occ, std::memory_order_relaxed);
   }
   int64_t nrc = std::max<int64_t>(1, (int64_t)occ * sm_count_lq() / groups);
   nrc = std::min<int64_t>(nrc, 1024);
@@ -631,9 +636,7 @@ extern "C" int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const do
   SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && z && v_prev && v_out && norm2 && (!R || ldr >= n),
               SKL_ERR_INVALID, "lsqr_trsv_t: bad arguments");
   const size_t smem = (size_t)n * sizeof(double);
-  if (smem > 48 * 1024)
-    SKL_CUDA(cudaFuncSetAttribute(lsqr_trsv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_trsv_t_kernel, smem));
   lsqr_trsv_t_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, z, beta, v_prev,
                                                                v_out, norm2);
   SKL_CUDA_LAUNCH();
@@ -646,9 +649,7 @@ extern "C" int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double a
   SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && v && y && (!R || ldr >= n), SKL_ERR_INVALID,
               "lsqr_trsv_n: bad arguments");
   const size_t smem = (size_t)n * sizeof(double);
-  if (smem > 48 * 1024)
-    SKL_CUDA(cudaFuncSetAttribute(lsqr_trsv_n_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_trsv_n_kernel, smem));
   lsqr_trsv_n_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, alfa, v, y);
   SKL_CUDA_LAUNCH();
   return SKL_OK;

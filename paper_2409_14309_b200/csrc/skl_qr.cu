@@ -507,12 +507,9 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   SKL_REQUIRE(n <= (200 * 1024) / 8, SKL_ERR_SPEC, "qr_solve: n=%lld too large", (long long)n);
   if (n * 8 > 48 * 1024) {
     const int bytes = (int)(n * 8);
-    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_inv_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_blocked_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    SKL_CUDA(cudaFuncSetAttribute(qr_backsolve_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    SKL_CUDA(raise_smem_limit(qr_backsolve_inv_kernel, (size_t)bytes));
+    SKL_CUDA(raise_smem_limit(qr_backsolve_blocked_kernel, (size_t)bytes));
+    SKL_CUDA(raise_smem_limit(qr_backsolve_kernel, (size_t)bytes));
   }
 
   const int fro_blocks = 256;

@@ -827,6 +827,21 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
   SKL_CUDA(cudaEventRecord(X[0], st));
   SKL_CUDA(cudaStreamWaitEvent(qs->hi, X[0], 0));
   SKL_CUDA(cudaStreamWaitEvent(qs->lo, X[0], 0));
+  // From here on work is forked onto hi / lo: every exit path -- success or
+  // an error return from a launch below -- joins both back into the
+  // caller's stream, so the caller's cudaFreeAsync of the workspace is
+  // ordered after everything that still uses it.
+  struct Join {
+    QrStreams* q;
+    cudaStream_t st;
+    cudaEvent_t a, b;
+    ~Join() {
+      cudaEventRecord(a, q->hi);
+      cudaEventRecord(b, q->lo);
+      cudaStreamWaitEvent(st, a, 0);
+      cudaStreamWaitEvent(st, b, 0);
+    }
+  } join{qs, st, X[1], X[2]};
   for (int64_t k = 0; k < npan; ++k) {
     const int64_t j0 = k * QB_NB;
     const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
@@ -852,14 +867,11 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
     if (rc) return rc;
     SKL_CUDA(cudaEventRecord(F[k], qs->lo));
   }
-  SKL_CUDA(cudaEventRecord(X[1], qs->hi));
-  SKL_CUDA(cudaEventRecord(X[2], qs->lo));
-  SKL_CUDA(cudaStreamWaitEvent(st, X[1], 0));
-  SKL_CUDA(cudaStreamWaitEvent(st, X[2], 0));
 #ifdef SKL_QR_PROBE
   {
     unsigned long long h[12] = {}, z[12] = {};
-    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(qs->hi);
+    cudaStreamSynchronize(qs->lo);
     cudaMemcpyFromSymbol(h, g_qr_probe, sizeof(h));
     cudaMemcpyToSymbol(g_qr_probe, z, sizeof(z));
     fprintf(stderr, "qr panel probe d=%lld n=%lld (cycles, CTA 0 thread 0, all panels):",

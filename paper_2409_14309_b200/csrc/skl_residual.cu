@@ -157,9 +157,7 @@ extern "C" int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t
   SKL_CUDA(malloc_async(&part, (blocks + 1) * sizeof(double), st));
   if (vec) {
     const size_t smem = n <= RS_XMAX ? n * sizeof(double) : 0;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(residual_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+    if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(residual_dense_kernel, smem));
     residual_dense_kernel<<<blocks, RS_NT, smem, st>>>(A, m, n, lda, x, b, part);
   } else {
     residual_dense_scalar_kernel<<<blocks, RS_NT, 0, st>>>(A, m, n, lda, x, b, part);

@@ -446,13 +446,13 @@ static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaSt
     constexpr int K2 = KPT * SR_NT / SR2_NT;
     auto kern = srht_reg_kernel<K2>;
     const int sm2 = SR2_G * SR2_BUF * 8 + 2 * K2 * SR2_NT * 4;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaError_t e = raise_smem_limit(kern, (size_t)sm2);
     if (e != cudaSuccess) return e;
     kern<<<grid, SR2_NT, sm2, st>>>(p);
     return cudaGetLastError();
   }
   auto kern = srht_dense_kernel<KPT, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SR_NT + 32, smem, st>>>(p);
   return cudaGetLastError();

@@ -32,6 +32,7 @@ from .sketch import (
     _apply_dense_tensor,
     _countsketch_csr_device,
     _countsketch_dense_device,
+    _few_long_columns,
     build_sketch,
     default_embed_dim,
 )
@@ -125,8 +126,8 @@ def _residual_device(A: Matrix, A_dev, lda: int, b_dev, x_dev) -> float:
 def sketch_operands_device(op, A: Matrix, b: Vector):
     """(SA, Sb, A_dev, lda, b_dev) on the device for one SAA solve; A and b
     are uploaded once when host-resident and reused for the residual."""
-    b_dev = b.data if b.on_device else to_device(b.data)
     if isinstance(A, SparseMatrix):
+        b_dev = b.data if b.on_device else to_device(b.data)
         if op.kind in ("countsketch", "sparsesign"):
             SA = _countsketch_csr_device(op, A)
             Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
@@ -135,6 +136,20 @@ def sketch_operands_device(op, A: Matrix, b: Vector):
         SA = _apply_dense_tensor(op, dense, A.rows, A.cols, lda=A.rows)
         Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)
         return SA, Sb, None, 0, b_dev
+    if (not A.on_device and not b.on_device and op.kind == "countsketch"
+            and not _few_long_columns(A.rows, A.cols + 1)):
+        # host A: row blocks stream to the device under the sketch kernel and
+        # land in a device copy kept for the residual pass (one H2D of A)
+        m, n, d = A.rows, A.cols, op.target_dim
+        ld = (m + 1) // 2 * 2
+        A_dev = device_f64((m, n), fortran=True, ld=ld)
+        b_dev = device_f64((m,))
+        SA = device_f64((d, n), fortran=True)
+        Sb = device_f64((d,))
+        op.device_plan().apply_host(A.data, m, n, m, np.ascontiguousarray(b.data), SA, d, Sb,
+                                    A_keep=A_dev, ld_keep=ld, b_keep=b_dev)
+        return SA, Sb, A_dev, ld, b_dev
+    b_dev = b.data if b.on_device else to_device(b.data)
     A_dev = A.data if A.on_device else to_device(A.data)
     lda = A.ld if A.on_device else A.rows
     if op.kind in ("countsketch", "sparsesign"):

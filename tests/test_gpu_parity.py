@@ -266,6 +266,53 @@ def test_host_streaming_abi_bitwise(golden, golden_meta, kind):
 
 
 @pytest.mark.parametrize("kind", ["owned", "lanes"])
+@pytest.mark.parametrize("keep", [False, True])
+def test_host_streaming_ring_many_blocks_bitwise(kind, keep):
+    """More row blocks than ring slots (64 MiB blocks of a 160 MiB A): every
+    block through the two-slot ring (or in place into A_dev_keep), device
+    outputs, bitwise the oracle's fold; the kept device copy equals A."""
+    from oracle import clib
+    from paper_2409_14309_b200._device import pinned_empty_f64
+    from paper_2409_14309_b200.sketch import CountSketchPlan
+
+    m, n, d = (1 << 20) + 4099, 20, 2048 if kind == "owned" else 5000
+    rng = np.random.default_rng(7)
+    A = pinned_empty_f64((m, n), fortran=True)
+    A[...] = rng.standard_normal((m, n))
+    b = pinned_empty_f64((m,))
+    b[...] = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec("countsketch", d, seed=8), m)
+    plan = CountSketchPlan(op.rows, op.signs, d, kind=kind)
+    SA = torch.full((n, d), float("nan"), dtype=torch.float64, device="cuda").t()
+    Sb = torch.full((d,), float("nan"), dtype=torch.float64, device="cuda")
+    ld = m + 1
+    A_keep = torch.zeros((n, ld), dtype=torch.float64, device="cuda").t() if keep else None
+    b_keep = torch.zeros(m, dtype=torch.float64, device="cuda") if keep else None
+    plan.apply_host(A, m, n, m, b, SA, d, Sb, A_keep=A_keep, ld_keep=ld if keep else 0,
+                    b_keep=b_keep)
+    assert np.array_equal(SA.cpu().numpy(), clib.countsketch_apply_mt(op.rows, op.signs, d, A))
+    assert np.array_equal(Sb.cpu().numpy(), clib.countsketch_apply_mt(op.rows, op.signs, d, b))
+    if keep:
+        assert np.array_equal(A_keep[:m].cpu().numpy(), A)
+        assert np.array_equal(b_keep.cpu().numpy(), b)
+
+
+def test_host_input_solve_equals_device_input_solve():
+    """solve() with host carriers streams A to the device under the sketch and
+    reuses the device copy for the residual: the same bits as the solve on
+    device carriers."""
+    c = W.config(1)
+    A, b, _ = W.make_problem(c)
+    spec, opts = E.SketchSpec("countsketch", 1, seed=3), E.SolverOptions(d_factor=4)
+    rh = E.solve(E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b)), "saa", spec, opts)
+    rd = E.solve(E.LeastSquaresProblem(E.DenseMatrix(torch.from_numpy(A).cuda()),
+                                       E.Vector(torch.from_numpy(b).cuda())), "saa", spec, opts)
+    assert isinstance(rh.x.data, np.ndarray)
+    assert np.array_equal(rh.x.data, rd.x.data.cpu().numpy())
+    assert rh.residual_norm == rd.residual_norm
+
+
+@pytest.mark.parametrize("kind", ["owned", "lanes"])
 @pytest.mark.parametrize("m,n,d", [(1, 1, 1), (9, 2, 3), (8184, 3, 5), (8185, 2, 2048),
                                    (50_000, 5, 1024), (50_001, 3, 1025), (100_000, 2, 17)])
 def test_countsketch_both_plans_bitwise(m, n, d, kind):
