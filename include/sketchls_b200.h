@@ -202,7 +202,7 @@ int skl_sparsesign_csr(const int64_t* indptr, const int64_t* indices, const doub
                        const int8_t* signs, double scale, int64_t d, double* SA, int64_t ldsa,
                        void* stream);
 
-/* Same apply with HOST A/b (preferably pinned): streams ~64 MiB row blocks
+/* Same apply with HOST A/b (preferably pinned): streams ~128 MiB row blocks
  * of A through a two-slot device ring with host-to-device copies overlapped
  * with the kernel (bitwise the same result); if A_dev_keep != NULL the blocks
  * land there instead (column-major, ld_keep even, 16-byte aligned) and the
@@ -353,6 +353,27 @@ int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda, const
 int skl_residual_csr(const int64_t* indptr, const int64_t* indices, const double* values,
                      int64_t m, int64_t n, const double* x, const double* b, double* out,
                      void* stream);
+
+/* ---- Gaussian operator generated in bands across devices ----
+ * The d x m Gaussian operator (sketch.py:94-96) is one ziggurat stream cut
+ * into segments of skl_gaussian_segment_words() words.  Device k parses
+ * only its band of segments [seg0, seg1): band_begin enqueues the parse
+ * on the stream and returns it in *handle (count may be NULL: it is
+ * reported by band_count, which synchronises the stream, so every device's
+ * parse runs before the host waits on any); after the host's prefix sum over
+ * the bands, band_write stores normal t (global,
+ * first <= t < first + count, t < N = d * m) at G[(t / m - row0) * ldg +
+ * t % m] divided by `div` (sqrt(d)) and frees the handle (band_free frees
+ * it without writing).  Bit-identical to skl_rng_gaussian_device.  The
+ * bands are then exchanged so every device holds the column block S[:, r0:r1]
+ * its row shard multiplies (multidevice.py). */
+int64_t skl_gaussian_segment_words(void);
+int skl_gaussian_band_begin(uint64_t key, int64_t seg0, int64_t seg1, void** handle,
+                            int64_t* count, void* stream);
+int skl_gaussian_band_count(void* handle, int64_t* count, void* stream);
+int skl_gaussian_band_write(void* handle, int64_t first, int64_t N, int64_t m, int64_t row0,
+                            double* G, int64_t ldg, double div, void* stream);
+void skl_gaussian_band_free(void* handle, void* stream);
 
 /* ---- row-sharded apply: the reduce step ----
  * out[:, c] = sum over q = 0 .. nslots-1, in that order, of

@@ -126,6 +126,12 @@ SIGNATURES: dict[str, tuple] = {
     "skl_rng_gaussian_device": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_rng_normal_device": (c_int, [c_u64, c_u64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
     "skl_rng_gaussian_host": (c_int, [c_u64, c_i64, c_ptr]),
+    "skl_gaussian_segment_words": (c_i64, []),
+    "skl_gaussian_band_begin": (c_int, [c_u64, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
+    "skl_gaussian_band_count": (c_int, [c_ptr, c_ptr, c_ptr]),
+    "skl_gaussian_band_write": (
+        c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, ctypes.c_double, c_ptr]),
+    "skl_gaussian_band_free": (None, [c_ptr, c_ptr]),
     "skl_gemm_f64": (
         c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_i64, c_int, c_ptr]),
     "skl_countsketch_buckets": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),

@@ -655,7 +655,7 @@ extern "C" int skl_countsketch_dense(const double* A, int64_t m, int64_t n, int6
 // stream while the kernel sketches the previous block (ordered pass,
 // accumulate across blocks, so the result stays bitwise-equal).
 //
-// Without A_dev_keep the blocks land in a two-slot ring (2 x ~64 MiB, not a
+// Without A_dev_keep the blocks land in a two-slot ring (2 x ~128 MiB, not a
 // device copy of all of A): block k is sketched out of slot k % 2 through
 // the pointer A_slot - r0 (the kernels address rows absolutely), and the copy
 // of block k + 2 waits for the kernel of block k.  With A_dev_keep the blocks
@@ -695,9 +695,9 @@ static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, i
   SKL_REQUIRE(!A_dev_keep || (ld_keep >= m && ld_keep % 2 == 0 &&
                               ((uintptr_t)A_dev_keep & 15) == 0),
               SKL_ERR_INVALID, "countsketch_host: bad A_dev_keep / ld_keep");
-  // blocks of whole plan chunks, ~64 MiB of A each (chunk is even, so every
+  // blocks of whole plan chunks, ~128 MiB of A each (chunk is even, so every
   // block start keeps the slot pointer A_slot - r0 16-byte aligned)
-  static const int64_t block_mb = getenv("SKL_HOST_BLOCK_MB") ? atoll(getenv("SKL_HOST_BLOCK_MB")) : 64;
+  static const int64_t block_mb = getenv("SKL_HOST_BLOCK_MB") ? atoll(getenv("SKL_HOST_BLOCK_MB")) : 128;
   const int64_t rows_per_block =
       std::min<int64_t>((m + chunk - 1) / chunk * chunk,
                         std::max<int64_t>(chunk, ((block_mb << 20) / (8 * n)) / chunk * chunk));

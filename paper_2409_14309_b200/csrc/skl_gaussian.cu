@@ -231,20 +231,23 @@ __global__ void zig_scan_kernel(const int64_t* count, int64_t nseg, int64_t* off
 // C: write the normals of each segment (normal t at G[(t / m) * ldg + t % m],
 // divided by `div`); record strip-0 tail positions and the word after the
 // last normal.
+// (t_base, row0: the band variant -- normal t of the band is global normal
+// t_base + t and lands at row (t_base + t) / m - row0 of G.)
 __global__ void zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
                                  const uint64_t* exitpos, const int64_t* count,
                                  const int64_t* offset, int64_t N, int64_t m, double* G,
                                  int64_t ldg, double div, int64_t* tail_t, uint64_t* tail_pos,
-                                 int* tail_n, int tail_cap, uint64_t* end_word) {
+                                 int* tail_n, int tail_cap, uint64_t* end_word,
+                                 int64_t t_base = 0, int64_t row0 = 0) {
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
-  int64_t t = offset[k];
+  int64_t t = t_base + offset[k];
   const int64_t cnt = count[k];
   if (t >= N || cnt == 0) return;
   uint64_t pos = k == 0 ? base : exitpos[k - 1];
   WordStream ws(key);
-  int64_t i = t / m, j = t % m;
+  int64_t i = t / m - row0, j = t % m;
   for (int64_t q = 0; q < cnt && t < N; ++q, ++t) {
     double v;
     bool tail;
@@ -267,11 +270,11 @@ __global__ void zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
 }
 
 __global__ void zig_patch_kernel(const int64_t* tail_t, const double* vals, int n, int64_t m,
-                                 double* G, int64_t ldg) {
+                                 double* G, int64_t ldg, int64_t row0 = 0) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const int64_t t = tail_t[q];
-  G[(t / m) * ldg + t % m] = vals[q];
+  G[(t / m - row0) * ldg + t % m] = vals[q];
 }
 
 static int upload_tables(cudaStream_t st) {
@@ -424,4 +427,177 @@ extern "C" int skl_rng_normal_device(uint64_t key, uint64_t start_word, int64_t 
   SKL_REQUIRE(rows >= 1 && cols >= 1 && ld >= cols && out, SKL_ERR_SHAPE,
               "normal_device: bad arguments");
   return normals_device(key, start_word, rows, cols, out, ld, 1.0, end_word, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// Banded generation for a multi-device operator (multidevice.py): device k
+// parses only segments [seg0, seg1) of the stream.  begin(): speculative
+// parse of [seg0 - 1, seg1) -- the extra segment gives the true entry of
+// seg0, which is the speculative exit of seg0 - 1 because the true chain
+// merges with it inside that segment (checked by the count of the device
+// owning seg0 - 1, which reports a broken chain otherwise) -- and the true
+// counts; *count = normals starting in the band.  After the host's prefix
+// sum over the bands, write() stores band normal q (global t = first + q,
+// t < N) at G[(t / m - row0) * ldg + t % m], recomputes the strip-0 tails on
+// the host, and frees the band.
+namespace skl {
+struct GaussBand {
+  uint64_t key = 0;
+  uint64_t base = 0;  // first word parsed (segment seg0 - 1, or 0)
+  int64_t nseg = 0;   // segments parsed (incl. the entry segment)
+  uint32_t* mask = nullptr;
+  uint64_t* exitpos = nullptr;
+  int64_t *count = nullptr, *offset = nullptr, *total = nullptr;
+  int* flags = nullptr;
+  void release(cudaStream_t st) {
+    cudaFreeAsync(mask, st); cudaFreeAsync(exitpos, st); cudaFreeAsync(count, st);
+    cudaFreeAsync(offset, st); cudaFreeAsync(total, st); cudaFreeAsync(flags, st);
+  }
+};
+}  // namespace skl
+
+extern "C" int64_t skl_gaussian_segment_words(void) { return ZIG_S; }
+
+extern "C" int skl_gaussian_band_begin(uint64_t key, int64_t seg0, int64_t seg1, void** handle,
+                                       int64_t* count, void* stream) {
+  clear_error();
+  SKL_REQUIRE(handle && seg0 >= 0 && seg1 > seg0, SKL_ERR_INVALID,
+              "gaussian_band_begin: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = upload_tables(st);
+  if (rc) return rc;
+  GaussBand* b = new GaussBand();
+  b->key = key;
+  const int64_t pre = seg0 > 0 ? 1 : 0;
+  b->base = (uint64_t)(seg0 - pre) * ZIG_S;
+  b->nseg = seg1 - seg0 + pre;
+  const int64_t nseg = b->nseg;
+  auto fail = [&](const char* what, cudaError_t e) {
+    b->release(st);
+    delete b;
+    SKL_FAIL(SKL_ERR_CUDA, "gaussian_band_begin: %s: %s", what, cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = malloc_async(&b->mask, (size_t)nseg * ZIG_MASKW * 4, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->exitpos, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->count, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->offset, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->total, 8, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->flags, 8, st)) != cudaSuccess) return fail("alloc", e);
+  cudaMemsetAsync(b->flags, 0, 8, st);
+  const int tb = 128;
+  const int blocks = (int)((nseg + tb - 1) / tb);
+  zig_spec_kernel<<<blocks, tb, 0, st>>>(key, b->base, nseg, b->mask, b->exitpos);
+  zig_count_kernel<<<blocks, tb, 0, st>>>(key, b->base, nseg, b->mask, b->exitpos, b->count,
+                                          b->flags);
+  if (pre) cudaMemsetAsync(b->count, 0, 8, st);  // the entry segment is the previous band's
+  zig_scan_kernel<<<1, 1024, 0, st>>>(b->count, nseg, b->offset, b->total);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail("launch", e);
+  *handle = b;
+  (void)count;
+  return SKL_OK;
+}
+
+// The band's normal count (synchronises the stream; fails if the chain of
+// this band did not resynchronise).
+extern "C" int skl_gaussian_band_count(void* handle, int64_t* count, void* stream) {
+  clear_error();
+  SKL_REQUIRE(handle && count, SKL_ERR_INVALID, "gaussian_band_count: bad arguments");
+  GaussBand* b = static_cast<GaussBand*>(handle);
+  cudaStream_t st = (cudaStream_t)stream;
+  int h_flags[2] = {0, 0};
+  SKL_CUDA(cudaMemcpyAsync(count, b->total, 8, cudaMemcpyDeviceToHost, st));
+  SKL_CUDA(cudaMemcpyAsync(h_flags, b->flags, 8, cudaMemcpyDeviceToHost, st));
+  SKL_CUDA(cudaStreamSynchronize(st));
+  SKL_REQUIRE(!h_flags[0], SKL_ERR_CUDA,
+              "gaussian: ziggurat segment chain failed to resynchronise");
+  return SKL_OK;
+}
+
+extern "C" int skl_gaussian_band_write(void* handle, int64_t first, int64_t N, int64_t m,
+                                       int64_t row0, double* G, int64_t ldg, double div,
+                                       void* stream) {
+  clear_error();
+  SKL_REQUIRE(handle && G && m >= 1 && ldg >= m && first >= 0 && N >= 1 && div > 0.0,
+              SKL_ERR_INVALID, "gaussian_band_write: bad arguments");
+  GaussBand* b = static_cast<GaussBand*>(handle);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nseg = b->nseg;
+  const int tail_cap = (int)std::min<int64_t>(nseg * ZIG_S / 256 + 4096, 1 << 26);
+  int64_t* tail_t = nullptr;
+  uint64_t* tail_pos = nullptr;
+  uint64_t* endw = nullptr;
+  int rc = SKL_OK;
+  do {
+    cudaError_t e;
+    if ((e = malloc_async(&tail_t, (size_t)tail_cap * 8, st)) != cudaSuccess ||
+        (e = malloc_async(&tail_pos, (size_t)tail_cap * 8, st)) != cudaSuccess ||
+        (e = malloc_async(&endw, 8, st)) != cudaSuccess) {
+      set_error("gaussian_band_write: alloc: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    cudaMemsetAsync(b->flags, 0, 8, st);
+    const int tb = 128;
+    const int blocks = (int)((nseg + tb - 1) / tb);
+    zig_write_kernel<<<blocks, tb, 0, st>>>(b->key, b->base, nseg, b->exitpos, b->count,
+                                            b->offset, N, m, G, ldg, div, tail_t, tail_pos,
+                                            b->flags + 1, tail_cap, endw, first, row0);
+    int h_flags[2] = {0, 0};
+    if ((e = cudaGetLastError()) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h_flags, b->flags, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      set_error("gaussian_band_write: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    const int ntail = h_flags[1];
+    if (ntail > tail_cap) {
+      set_error("gaussian: tail record overflow (%d > %d)", ntail, tail_cap);
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    if (ntail > 0) {
+      std::vector<int64_t> ht((size_t)ntail);
+      std::vector<uint64_t> hp((size_t)ntail);
+      std::vector<double> hv((size_t)ntail);
+      cudaMemcpyAsync(ht.data(), tail_t, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hp.data(), tail_pos, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+        set_error("gaussian_band_write: %s", cudaGetErrorString(e));
+        rc = SKL_ERR_CUDA;
+        break;
+      }
+      for (int q = 0; q < ntail; ++q) {
+        WordStream ws(b->key);
+        bool tl;
+        double v;
+        zig_parse(ws, hp[(size_t)q], &v, &tl);
+        hv[(size_t)q] = v / div;
+      }
+      double* dv = nullptr;
+      if ((e = malloc_async(&dv, (size_t)ntail * 8, st)) != cudaSuccess) {
+        set_error("gaussian_band_write: alloc: %s", cudaGetErrorString(e));
+        rc = SKL_ERR_CUDA;
+        break;
+      }
+      cudaMemcpyAsync(dv, hv.data(), (size_t)ntail * 8, cudaMemcpyHostToDevice, st);
+      zig_patch_kernel<<<(ntail + 255) / 256, 256, 0, st>>>(tail_t, dv, ntail, m, G, ldg, row0);
+      cudaFreeAsync(dv, st);
+      cudaStreamSynchronize(st);  // host vectors go out of scope
+    }
+  } while (0);
+  if (tail_t) cudaFreeAsync(tail_t, st);
+  if (tail_pos) cudaFreeAsync(tail_pos, st);
+  if (endw) cudaFreeAsync(endw, st);
+  b->release(st);
+  delete b;
+  return rc;
+}
+
+extern "C" void skl_gaussian_band_free(void* handle, void* stream) {
+  if (!handle) return;
+  GaussBand* b = static_cast<GaussBand*>(handle);
+  b->release((cudaStream_t)stream);
+  delete b;
 }

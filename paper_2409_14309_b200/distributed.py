@@ -145,6 +145,9 @@ class ShardPlan:
         self.kind = op.kind
         self.d = op.target_dim
         self._dev: dict = {}
+        # (G block, ld) supplied by a banded multi-device generation
+        # (multidevice.gaussian_column_blocks); None: slice the full G
+        self.gaussian_block = None
 
     @property
     def rows(self):
@@ -198,6 +201,8 @@ class ShardPlan:
 
     def device_gaussian(self):
         """(G block view d x (r1 - r0), ld) on the current device."""
+        if self.gaussian_block is not None:
+            return self.gaussian_block
         G, ldg = self.op.device_gaussian_block(self.r0, self.r1)
         return G, ldg
 

@@ -8,7 +8,9 @@ through its own stream: row block k of A and b goes to ``devices[k]``
 (host carriers are uploaded block by block; device carriers are copied peer
 to peer), every device sketches its block with the global operator's shard
 plan (distributed.ShardPlan: the hashes of the global rows, the SRHT block
-offset, the Gaussian column block), the partial d x (n+1) sketches are
+offset, the Gaussian column block -- generated in bands, each device parsing
+~1/N of the operator's ziggurat stream, then exchanged; see
+gaussian_column_blocks), the partial d x (n+1) sketches are
 copied to ``devices[0]`` and summed there in device order
 (skl_reduce_peers: the same fixed-order fold as the multi-process path),
 the reduced QR solve runs on ``devices[0]``, and every device computes its
@@ -24,6 +26,9 @@ change the fp64 association), not bitwise.
 """
 
 from __future__ import annotations
+
+import ctypes
+import math
 
 import numpy as np
 
@@ -79,6 +84,96 @@ def _vec_block(b, r0: int, r1: int, dev: int):
     return b[r0:r1].to(torch.device("cuda", dev)).contiguous()
 
 
+def _band_begin(op, seg0: int, seg1: int):
+    h = ctypes.c_void_p()
+    _native.call("skl_gaussian_band_begin", op.key, seg0, seg1, ctypes.byref(h), None,
+                 current_stream())
+    return h
+
+
+def gaussian_column_blocks(op, devs, spans):
+    """The Gaussian operator's column blocks S[:, r0:r1] for row shards
+    ``spans`` on devices ``devs``, generated in bands: device k parses only
+    segment band k of the stream (skl_gaussian_band_*), the host prefix-sums
+    the bands' normal counts, every device writes its band's normals (rows
+    of S), and the bands are exchanged so device k holds the columns its
+    shard multiplies.  Each device generates ~1/N of the d x m operator
+    instead of all of it.  Returns [(block d x w_k, ld)], bit-identical to
+    the single-device G[:, r0:r1]."""
+    _native.install_gaussian_tables()
+    lib = _native.lib()
+    d, m = op.target_dim, op.source_dim
+    N = d * m
+    seg_words = int(lib.skl_gaussian_segment_words())
+    world = len(devs)
+    # ~1.025 stream words per normal: 3 % slack, as the one-device generator
+    seg_total = int(N * 1.03 / seg_words) + 8
+    bounds = [seg_total * k // world for k in range(world + 1)]
+    handles, counts = [None] * world, [0] * world
+    for k, dev in enumerate(devs):  # enqueue every band before waiting on any
+        with torch.cuda.device(dev):
+            handles[k] = _band_begin(op, bounds[k], bounds[k + 1])
+    for k, dev in enumerate(devs):
+        with torch.cuda.device(dev):
+            c = ctypes.c_int64()
+            _native.call("skl_gaussian_band_count", handles[k], ctypes.byref(c), current_stream())
+            counts[k] = int(c.value)
+    while sum(counts) < N:  # too few words: extend the last band
+        dev = devs[-1]
+        with torch.cuda.device(dev):
+            lib.skl_gaussian_band_free(handles[-1], ctypes.c_void_p(current_stream()))
+            bounds[-1] += (bounds[-1] - bounds[-2]) // 8 + 16
+            handles[-1] = _band_begin(op, bounds[-2], bounds[-1])
+            c = ctypes.c_int64()
+            _native.call("skl_gaussian_band_count", handles[-1], ctypes.byref(c),
+                         current_stream())
+            counts[-1] = int(c.value)
+    firsts = [sum(counts[:k]) for k in range(world)]
+    ldg = (m + 31) // 32 * 32
+    div = math.sqrt(d)
+    bands = []  # (tensor rows x ldg, row0, t0, t1)
+    for k, dev in enumerate(devs):
+        t0, t1 = min(N, firsts[k]), min(N, firsts[k] + counts[k])
+        with torch.cuda.device(dev):
+            if t1 <= t0:
+                lib.skl_gaussian_band_free(handles[k], ctypes.c_void_p(current_stream()))
+                bands.append(None)
+                continue
+            row0, row1 = t0 // m, (t1 - 1) // m + 1
+            band = torch.empty((row1 - row0, ldg), dtype=torch.float64,
+                               device=torch.device("cuda", dev))
+            _native.call("skl_gaussian_band_write", handles[k], firsts[k], N, m, row0,
+                         _native.ptr(band), ldg, div, current_stream())
+            bands.append((band, row0, t0, t1))
+    blocks = []
+    for (r0, r1), dev in zip(spans, devs):
+        w = r1 - r0
+        ldb = (w + 31) // 32 * 32
+        with torch.cuda.device(dev):
+            blk = torch.empty((d, ldb), dtype=torch.float64, device=torch.device("cuda", dev))
+            for bd in bands:
+                if bd is None:
+                    continue
+                band, row0, t0, t1 = bd
+                i_first, i_last = t0 // m, (t1 - 1) // m
+                # partial first / last rows, full rows between
+                pieces = []
+                for i in sorted({i_first, i_last}):
+                    lo, hi = max(0, t0 - i * m), min(m, t1 - i * m)
+                    pieces.append((i, i + 1, lo, hi))
+                if i_last - i_first >= 2:
+                    pieces.append((i_first + 1, i_last, 0, m))
+                for ia, ib, lo, hi in pieces:
+                    a, c = max(lo, r0), min(hi, r1)
+                    if a >= c or ib <= ia:
+                        continue
+                    blk[ia:ib, a - r0:c - r0].copy_(band[ia - row0:ib - row0, a:c])
+            blocks.append((blk, ldb))
+    for dev in set(devs):
+        torch.cuda.synchronize(dev)
+    return blocks
+
+
 def sketch_and_apply_devices(op, A, b, devices):
     """Row-sharded S[A | b] over ``devices`` followed by the reduced solve on
     devices[0].  Returns (x tensor on devices[0], residual norm)."""
@@ -92,13 +187,20 @@ def sketch_and_apply_devices(op, A, b, devices):
     ld = partial_ld(d)
     slot = (n + 1) * ld
     dev0 = devs[0]
+    spans = [shard_rows(m, world, k) for k in range(world)]
+    gblocks = None
+    if op.kind == "gaussian":
+        key = ("gauss_blocks", devs)
+        gblocks = op._host.get(key)
+        if gblocks is None:  # per-device bands of the stream, exchanged (cached)
+            gblocks = op._host[key] = gaussian_column_blocks(op, devs, spans)
     caller = torch.cuda.current_stream(dev0)
     start = torch.cuda.Event()
     start.record(caller)
     shards = []
     # 1. per-device row blocks and partials, each device on its own stream
     for k, dev in enumerate(devs):
-        r0, r1 = shard_rows(m, world, k)
+        r0, r1 = spans[k]
         with torch.cuda.device(dev):
             st = torch.cuda.Stream(dev)
             st.wait_event(start)
@@ -109,6 +211,8 @@ def sketch_and_apply_devices(op, A, b, devices):
                     A_loc, lda = _dense_block(A, r0, r1, dev)
                 b_loc = _vec_block(b.data, r0, r1, dev)
                 plan = ShardPlan(op, r0, r1)
+                if gblocks is not None:
+                    plan.gaussian_block = gblocks[k]
                 part = torch.empty(slot, dtype=torch.float64, device=torch.device("cuda", dev))
                 local_partial_device(plan, A_loc, lda, b_loc, dest=part.data_ptr())
                 done = torch.cuda.Event()
@@ -148,4 +252,4 @@ def sketch_and_apply_devices(op, A, b, devices):
     return x, float(np.sqrt(r2))
 
 
-__all__ = ["check_devices", "sketch_and_apply_devices", "CsrBlock"]
+__all__ = ["check_devices", "gaussian_column_blocks", "sketch_and_apply_devices", "CsrBlock"]

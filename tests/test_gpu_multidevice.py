@@ -144,3 +144,22 @@ def test_concurrent_first_use_from_threads():
     assert not errs, errs
     for i in range(4):
         assert np.array_equal(out[i], want)
+
+
+@pytest.mark.parametrize("d,m,world", [(64, 50_000, 8), (16, 3 * 8192, 3), (300, 70_001, 5),
+                                       (2048, 262_144, 8)])
+def test_gaussian_bands_equal_one_device_operator(d, m, world):
+    """Banded generation over a device list (each 'device' parses ~1/N of the
+    ziggurat stream, then the bands are exchanged into column blocks): every
+    block is bitwise the one-device G[:, r0:r1] -- including config 3's
+    2048 x 262144 operator."""
+    from paper_2409_14309_b200.distributed import shard_rows
+    from paper_2409_14309_b200.multidevice import gaussian_column_blocks
+
+    op = E.build_sketch(E.SketchSpec("gaussian", d, seed=d + m), m)
+    spans = [shard_rows(m, world, k) for k in range(world)]
+    blocks = gaussian_column_blocks(op, (0,) * world, spans)
+    G, _ = op.device_gaussian()
+    for (r0, r1), (blk, ldb) in zip(spans, blocks):
+        assert ldb >= r1 - r0
+        assert torch.equal(blk[:, : r1 - r0], G[:, r0:r1])
