@@ -33,7 +33,7 @@ import math
 import numpy as np
 
 from . import _native
-from ._device import current_stream, require_cuda, torch
+from ._device import current_stream, require_cuda, to_device, torch
 from .distributed import CsrBlock, ShardPlan, csr_row_block, local_partial_device, partial_ld
 from .distributed import residual_sq_local, shard_rows
 from .errors import SpecError
@@ -65,9 +65,8 @@ def _dense_block(A: DenseMatrix, r0: int, r1: int, dev: int):
     n = A.cols
     m_loc = r1 - r0
     if not A.on_device:
-        blk = np.asfortranarray(A.data[r0:r1])
-        t = torch.from_numpy(blk).to(torch.device("cuda", dev))
-        return t, m_loc
+        with torch.cuda.device(dev):
+            return to_device(np.asfortranarray(A.data[r0:r1])), m_loc
     src = A.data[r0:r1]
     if src.device.index == dev:
         return src, A.ld  # a view: same leading dimension
@@ -80,7 +79,8 @@ def _dense_block(A: DenseMatrix, r0: int, r1: int, dev: int):
 
 def _vec_block(b, r0: int, r1: int, dev: int):
     if isinstance(b, np.ndarray):
-        return torch.from_numpy(np.ascontiguousarray(b[r0:r1])).to(torch.device("cuda", dev))
+        with torch.cuda.device(dev):
+            return to_device(np.ascontiguousarray(b[r0:r1]))
     return b[r0:r1].to(torch.device("cuda", dev)).contiguous()
 
 
@@ -188,6 +188,11 @@ def sketch_and_apply_devices(op, A, b, devices):
     slot = (n + 1) * ld
     dev0 = devs[0]
     spans = [shard_rows(m, world, k) for k in range(world)]
+    # shard plans (per-shard hashes, plans, bucket lists) are cached with the
+    # operator, like its one-device plan
+    plans = op._host.get(("shard_plans", devs))
+    if plans is None:
+        plans = op._host[("shard_plans", devs)] = [ShardPlan(op, r0, r1) for r0, r1 in spans]
     gblocks = None
     if op.kind == "gaussian":
         key = ("gauss_blocks", devs)
@@ -210,7 +215,7 @@ def sketch_and_apply_devices(op, A, b, devices):
                 else:
                     A_loc, lda = _dense_block(A, r0, r1, dev)
                 b_loc = _vec_block(b.data, r0, r1, dev)
-                plan = ShardPlan(op, r0, r1)
+                plan = plans[k]
                 if gblocks is not None:
                     plan.gaussian_block = gblocks[k]
                 part = torch.empty(slot, dtype=torch.float64, device=torch.device("cuda", dev))
