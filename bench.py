@@ -406,6 +406,9 @@ def main():
     peer = peer_reduce_or_none(d, n + 1) if grouped else None
     collective = ("peer-reduce-scatter (symmetric memory, skl_reduce_peers)" if peer is not None
                   else ("nccl-reduce" if world > 1 else "none"))
+    # one line per rank on stderr: the world this run actually formed
+    print(f"[bench] rank {rank}/{world} local {local} device {torch.cuda.current_device()} "
+          f"({torch.cuda.get_device_name()}) collective={collective}", file=sys.stderr, flush=True)
 
     def apply():
         if peer is not None:

@@ -69,6 +69,34 @@ def element_block(total: int, world: int, rank: int, align: int = 2) -> tuple[in
     return min(total, u0 * align), min(total, u1 * align)
 
 
+def band_pieces(t0: int, t1: int, m: int, r0: int, r1: int):
+    """The rectangles of S (row-major d x m, normal t at [t // m, t % m])
+    that a band holding normals [t0, t1) contributes to the column block
+    [r0, r1): [(row_begin, row_end, col_begin, col_end)] -- the band's
+    partial first row, its full rows, its partial last row."""
+    if t1 <= t0:
+        return []
+    i_first, i_last = t0 // m, (t1 - 1) // m
+    rects = []
+    for i in sorted({i_first, i_last}):
+        rects.append((i, i + 1, max(0, t0 - i * m), min(m, t1 - i * m)))
+    if i_last - i_first >= 2:
+        rects.append((i_first + 1, i_last, 0, m))
+    out = []
+    for ia, ib, lo, hi in rects:
+        a, c = max(lo, r0), min(hi, r1)
+        if a < c and ia < ib:
+            out.append((ia, ib, a, c))
+    return out
+
+
+def band_bounds(N: int, world: int, seg_words: int) -> list[int]:
+    """Segment boundaries of the N-normal stream's bands (~1.025 words per
+    normal: 3 % slack, as the one-device generator)."""
+    seg_total = int(N * 1.03 / seg_words) + 8
+    return [seg_total * k // world for k in range(world + 1)]
+
+
 @dataclass(frozen=True)
 class CsrBlock:
     """Rows [r0, r1) of a CSR matrix on one device: indptr rebased to 0
@@ -356,6 +384,92 @@ def residual_sq_local(A_local, lda: int, b_local, x) -> float:
     return float(out[0]) ** 2
 
 
+def exchange_gaussian_bands(band, t0: int, t1: int, all_t, m: int, d: int, spans, rank: int,
+                            dist, group=None, device=None):
+    """All-to-all of the Gaussian operator's bands (multi-process form of
+    multidevice.gaussian_column_blocks): this rank holds normals [t0, t1)
+    (``band``: rows t0 // m .. of S, row-major, any ld; None when empty),
+    ``all_t`` every rank's range, ``spans`` every rank's row shard.  Each
+    rank sends every other rank the rectangles of its band inside that
+    rank's column block (band_pieces), packed in order; the receiver
+    unpacks them with the same rectangles computed from the sender's range.
+    Returns this rank's block S[:, r0:r1] (d x w tensor, ld rounded to 32)."""
+    world = len(spans)
+    r0, r1 = spans[rank]
+    w = r1 - r0
+    ldb = (w + 31) // 32 * 32
+    dev = device if device is not None else (band.device if band is not None else "cpu")
+    blk = torch.zeros((d, ldb), dtype=torch.float64, device=dev)
+    row0 = t0 // m
+    send = []
+    for s in range(world):
+        ps = band_pieces(t0, t1, m, *spans[s]) if band is not None else []
+        send.append([band[ia - row0:ib - row0, a:c].reshape(-1) for ia, ib, a, c in ps])
+    in_sizes = [sum(p.numel() for p in parts) for parts in send]
+    recv_pieces = [band_pieces(tk0, tk1, m, r0, r1) for tk0, tk1 in all_t]
+    out_sizes = [sum((ib - ia) * (c - a) for ia, ib, a, c in ps) for ps in recv_pieces]
+    flat = [p for parts in send for p in parts]
+    sendbuf = (torch.cat(flat) if flat else torch.zeros(0, dtype=torch.float64, device=dev))
+    recvbuf = torch.empty(sum(out_sizes), dtype=torch.float64, device=dev)
+    dist.all_to_all_single(recvbuf, sendbuf, out_sizes, in_sizes, group=group)
+    off = 0
+    for ps in recv_pieces:
+        for ia, ib, a, c in ps:
+            nel = (ib - ia) * (c - a)
+            blk[ia:ib, a - r0:c - r0] = recvbuf[off:off + nel].view(ib - ia, c - a)
+            off += nel
+    return blk, ldb
+
+
+def gaussian_block_distributed(op, spans, dist, group=None):
+    """This rank's Gaussian column block, generated in bands across the ranks
+    (skl_gaussian_band_*: each rank parses ~1/N of the stream; the bands'
+    normal counts are all-gathered, then exchange_gaussian_bands)."""
+    import ctypes
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    _native.install_gaussian_tables()
+    lib = _native.lib()
+    d, m = op.target_dim, op.source_dim
+    N = d * m
+    bounds = band_bounds(N, world, int(lib.skl_gaussian_segment_words()))
+    st = current_stream()
+
+    def begin(seg0, seg1):
+        h = ctypes.c_void_p()
+        _native.call("skl_gaussian_band_begin", op.key, seg0, seg1, ctypes.byref(h), None, st)
+        c = ctypes.c_int64()
+        _native.call("skl_gaussian_band_count", h, ctypes.byref(c), st)
+        return h, int(c.value)
+
+    h, cnt = begin(bounds[rank], bounds[rank + 1])
+    while True:
+        counts = torch.zeros(world, dtype=torch.int64, device="cuda")
+        counts[rank] = cnt
+        dist.all_reduce(counts, group=group)
+        counts = [int(v) for v in counts.cpu()]
+        if sum(counts) >= N:
+            break
+        if rank == world - 1:  # too few words: the last band grows
+            lib.skl_gaussian_band_free(h, ctypes.c_void_p(st))
+        bounds[-1] += (bounds[-1] - bounds[-2]) // 8 + 16
+        if rank == world - 1:
+            h, cnt = begin(bounds[-2], bounds[-1])
+    firsts = [sum(counts[:k]) for k in range(world)]
+    all_t = [(min(N, firsts[k]), min(N, firsts[k] + counts[k])) for k in range(world)]
+    t0, t1 = all_t[rank]
+    band = None
+    if t1 > t0:
+        ldg = (m + 31) // 32 * 32
+        band = torch.empty(((t1 - 1) // m + 1 - t0 // m, ldg), dtype=torch.float64, device="cuda")
+        _native.call("skl_gaussian_band_write", h, firsts[rank], N, m, t0 // m,
+                     _native.ptr(band), ldg, math.sqrt(d), st)
+    else:
+        lib.skl_gaussian_band_free(h, ctypes.c_void_p(st))
+    return exchange_gaussian_bands(band, t0, t1, all_t, m, d, spans, rank, dist, group,
+                                   device=torch.device("cuda", torch.cuda.current_device()))
+
+
 def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=None,
                              local_apply: Callable | None = None, solve_reduced=None,
                              residual_local=None, collective: str = "auto"):
@@ -376,6 +490,13 @@ def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=N
         raise ValueError(f"rank {rank} holds {A_local.shape[0]} rows, expected {r1 - r0}")
     op = build_sketch(spec, m_total)
     plan = ShardPlan(op, r0, r1)
+    if op.kind == "gaussian" and local_apply is None and world > 1:
+        # the operator in bands across the ranks, not all of G on every rank
+        key = ("gauss_dist", world, rank)
+        if key not in op._host:
+            spans = [shard_rows(m_total, world, k) for k in range(world)]
+            op._host[key] = gaussian_block_distributed(op, spans, dist, group)
+        plan.gaussian_block = op._host[key]
     n = A_local.shape[1]
     d = plan.d
     dense = not isinstance(A_local, CsrBlock)

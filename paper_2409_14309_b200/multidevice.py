@@ -35,7 +35,7 @@ import numpy as np
 from . import _native
 from ._device import current_stream, require_cuda, to_device, torch
 from .distributed import CsrBlock, ShardPlan, csr_row_block, local_partial_device, partial_ld
-from .distributed import residual_sq_local, shard_rows
+from .distributed import band_bounds, band_pieces, residual_sq_local, shard_rows
 from .errors import SpecError
 from .linalg import DenseMatrix, SparseMatrix
 from .sketch import SHARD_ALIGN
@@ -106,9 +106,7 @@ def gaussian_column_blocks(op, devs, spans):
     N = d * m
     seg_words = int(lib.skl_gaussian_segment_words())
     world = len(devs)
-    # ~1.025 stream words per normal: 3 % slack, as the one-device generator
-    seg_total = int(N * 1.03 / seg_words) + 8
-    bounds = [seg_total * k // world for k in range(world + 1)]
+    bounds = band_bounds(N, world, seg_words)
     handles, counts = [None] * world, [0] * world
     for k, dev in enumerate(devs):  # enqueue every band before waiting on any
         with torch.cuda.device(dev):
@@ -155,18 +153,7 @@ def gaussian_column_blocks(op, devs, spans):
                 if bd is None:
                     continue
                 band, row0, t0, t1 = bd
-                i_first, i_last = t0 // m, (t1 - 1) // m
-                # partial first / last rows, full rows between
-                pieces = []
-                for i in sorted({i_first, i_last}):
-                    lo, hi = max(0, t0 - i * m), min(m, t1 - i * m)
-                    pieces.append((i, i + 1, lo, hi))
-                if i_last - i_first >= 2:
-                    pieces.append((i_first + 1, i_last, 0, m))
-                for ia, ib, lo, hi in pieces:
-                    a, c = max(lo, r0), min(hi, r1)
-                    if a >= c or ib <= ia:
-                        continue
+                for ia, ib, a, c in band_pieces(t0, t1, m, r0, r1):
                     blk[ia:ib, a - r0:c - r0].copy_(band[ia - row0:ib - row0, a:c])
             blocks.append((blk, ldb))
     for dev in set(devs):
@@ -257,4 +244,5 @@ def sketch_and_apply_devices(op, A, b, devices):
     return x, float(np.sqrt(r2))
 
 
-__all__ = ["check_devices", "gaussian_column_blocks", "sketch_and_apply_devices", "CsrBlock"]
+__all__ = ["band_pieces", "check_devices", "gaussian_column_blocks", "sketch_and_apply_devices",
+           "CsrBlock"]

@@ -264,3 +264,69 @@ def test_gloo_world2_csr_row_blocks():
         assert dd == d
         assert np.linalg.norm(x - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
         assert abs(rnorm - r_ref) <= 1e-12 * r_ref
+
+
+def test_band_pieces_tile_every_block():
+    """The rectangles a band of normals contributes to a column block: over
+    all bands they tile every block exactly once (host logic of the banded
+    Gaussian generation, multidevice.py / distributed.py)."""
+    from paper_2409_14309_b200.distributed import band_pieces
+
+    rng = np.random.default_rng(0)
+    for d, m in [(3, 10), (16, 8192 * 3), (7, 1001)]:
+        N = d * m
+        for nb in (1, 2, 5):
+            cuts = np.sort(rng.integers(0, N + 1, nb - 1))
+            ts = list(zip([0, *cuts], [*cuts, N]))
+            for r0, r1 in [(0, m), (0, m // 3), (m // 3, m), (m // 2, m // 2 + 1)]:
+                cover = np.zeros((d, m), dtype=np.int64)
+                for t0, t1 in ts:
+                    for ia, ib, a, c in band_pieces(t0, t1, m, r0, r1):
+                        assert r0 <= a < c <= r1 and 0 <= ia < ib <= d
+                        cover[ia:ib, a:c] += 1
+                        # every covered cell's normal index lies in the band
+                        tt = np.arange(ia, ib)[:, None] * m + np.arange(a, c)[None, :]
+                        assert tt.min() >= t0 and tt.max() < t1
+                assert np.all(cover[:, r0:r1] == 1) and cover.sum() == d * (r1 - r0)
+
+
+def _band_worker(rank, world, port, d, m, cuts, out):
+    from paper_2409_14309_b200.distributed import exchange_gaussian_bands
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        G = np.random.default_rng(5).standard_normal((d, m))
+        ts = list(zip([0, *cuts], [*cuts, d * m]))
+        t0, t1 = ts[rank]
+        band = None
+        if t1 > t0:
+            r_lo, r_hi = t0 // m, (t1 - 1) // m + 1
+            ldg = m + 3  # any leading dimension
+            band = torch.full((r_hi - r_lo, ldg), float("nan"), dtype=torch.float64)
+            flat = G.reshape(-1)
+            for t in range(t0, t1):  # only the band's own normals are valid
+                band[t // m - r_lo, t % m] = flat[t]
+        spans = [shard_rows(m, world, k) for k in range(world)]
+        blk, ldb = exchange_gaussian_bands(band, t0, t1, ts, m, d, spans, rank, dist)
+        r0, r1 = spans[rank]
+        out[rank] = (blk[:, : r1 - r0].numpy().copy(), G[:, r0:r1].copy(), ldb)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world3_gaussian_band_exchange():
+    """The all-to-all of the banded Gaussian generation (distributed.py):
+    ranks holding arbitrary bands of the d x m operator's normals end with
+    exactly their column blocks (bands cut mid-row, one empty band)."""
+    d, m, world = 6, 3 * 8192, 3
+    N = d * m
+    cuts = [N // 3 + 17, N // 3 + 17]  # rank 1's band is empty
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_band_worker, args=(world, port, d, m, cuts, out), nprocs=world, join=True)
+    for rank in range(world):
+        got, want, ldb = out[rank]
+        assert np.array_equal(got, want) and ldb % 32 == 0
