@@ -313,6 +313,9 @@ class PeerReduce:
         self.rows, self.cols, self.ld = rows, cols, partial_ld(rows)
         self.slot = cols * self.ld  # elements per partial
         self.dst, self.timeout_ms = dst, timeout_ms
+        enable = getattr(symm_mem, "enable_symm_mem_for_group", None)
+        if enable is not None:  # idempotent; required before rendezvous on some versions
+            enable(self.group.group_name)
         self.buf = symm_mem.empty(2 * self.slot, dtype=torch.float64, device="cuda")
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
         self.peers = [int(p) for p in self.hdl.buffer_ptrs]
