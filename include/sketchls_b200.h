@@ -287,6 +287,17 @@ int skl_countsketch_csr(const int64_t* indptr, const int64_t* indices, const dou
                         const int64_t* bucket_ptr, const int8_t* signs, int64_t d, double* SA,
                         int64_t ldsa, void* stream);
 
+/* SRHT of [A | b] in one pass: b rides along as the (n+1)-th column (SA
+ * d x n, ld ldsa; Sb d).  row_offset: first global row of this row block
+ * (0 unsharded; a multiple of the 4096-row block for a shard, whose partial
+ * the caller sums across ranks).  partitions: row partitions per column, 0 =
+ * automatic.  Replaces sketch.py:213-223 for the SAA solve's S A and S b
+ * (solvers.py:308, 287). */
+int skl_srht_dense_ab(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                      const uint16_t* sign_bits, const int64_t* row_sample, int64_t m_pad,
+                      int64_t d, int64_t row_offset, double* SA, int64_t ldsa, double* Sb,
+                      int partitions, void* stream);
+
 /* Ordered bucket walk for a few long dense columns (device): SA[:, c]
  * (+)= S A[:, c] for c < n and Sb (+)= S b, every bucket's products
  * sign*scale*A[j, c] added in ascending source row j from +0.0 -- scipy's

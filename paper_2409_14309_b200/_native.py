@@ -116,6 +116,10 @@ SIGNATURES: dict[str, tuple] = {
         c_int, [c_i64, ctypes.c_double, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_srht_dense": (
         c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "skl_srht_dense_ab": (
+        c_int,
+        [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr,
+         c_int, c_ptr]),
     "skl_srht_dense_shard": (
         c_int,
         [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),

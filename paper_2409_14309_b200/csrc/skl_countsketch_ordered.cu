@@ -12,8 +12,9 @@
 // warp owns one (bucket, column), walks the bucket's source rows (the CSR of
 // S built with the operator, rows ascending within a bucket) 128 entries at
 // a time -- each lane gathers four entries, the next block's gathers are in
-// flight while the current one is folded -- and folds them in order through
-// warp broadcasts.  Bitwise-equal to csr_matvec / csr_matvecs.
+// flight while the current one is folded -- and lane 0 folds them in order
+// out of a per-warp shared-memory stage (16-byte loads; a warp shuffle per
+// term made the fold MIO-bound).  Bitwise-equal to csr_matvec / csr_matvecs.
 //
 // Bound: latency of the dependent fold (~512 entries per bucket at the
 // BASELINE configs) and the gathers; the column itself is read once from HBM
@@ -57,25 +58,34 @@ countsketch_ordered_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
                            const int64_t* __restrict__ bptr, const int8_t* __restrict__ bsign,
                            double scale, int d, double* __restrict__ out, int64_t ldo,
                            double* __restrict__ outb, int accumulate) {
-  const int lane = threadIdx.x & 31;
-  const int64_t bucket = (int64_t)blockIdx.x * ORD_WARPS + (threadIdx.x >> 5);
+  __shared__ __align__(16) double stage[ORD_WARPS][ORD_BLOCK];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bucket = (int64_t)blockIdx.x * ORD_WARPS + warp;
   const int64_t c = blockIdx.y;  // column (n == the b column when b != null)
   if (bucket >= d) return;
   const double* col = c < n ? A + c * lda : b;
   double* dst = c < n ? out + c * ldo + bucket : outb + bucket;
   const int64_t p0 = __ldg(bptr + bucket), p1 = __ldg(bptr + bucket + 1);
+  double* buf = stage[warp];
   double s = 0.0;  // csr_matvec starts every output from +0.0
   OrdBlock cur = ord_fetch(p0, p1, lane, brow, bsign, col, scale);
   for (int64_t base = p0; base < p1; base += ORD_BLOCK) {
     const OrdBlock nxt = ord_fetch(base + ORD_BLOCK, p1, lane, brow, bsign, col, scale);
-    const int64_t cnt = p1 - base;
+    const int cnt = p1 - base < ORD_BLOCK ? (int)(p1 - base) : ORD_BLOCK;
+    // the block's products go through shared memory and lane 0 folds them
+    // in order: 16-byte loads by one lane instead of a warp shuffle per term
+    __syncwarp();
 #pragma unroll
-    for (int q = 0; q < ORD_PER_LANE; ++q) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const double v = __shfl_sync(0xffffffffu, cur.v[q], i);
-        if (32 * q + i < cnt) s = __dadd_rn(s, v);
+    for (int q = 0; q < ORD_PER_LANE; ++q) buf[lane + 32 * q] = cur.v[q];
+    __syncwarp();
+    if (lane == 0) {
+      const double2* b2 = reinterpret_cast<const double2*>(buf);
+      int i = 0;
+      for (; i + 1 < cnt; i += 2) {
+        const double2 v = b2[i >> 1];
+        s = __dadd_rn(__dadd_rn(s, v.x), v.y);
       }
+      if (i < cnt) s = __dadd_rn(s, buf[i]);
     }
     cur = nxt;
   }

@@ -60,7 +60,18 @@ struct SrParams {
   double* part;       // [P][n][d]
   double inv_scale_div;  // sqrt(d) (division at the end)
   int sw_block;         // packed sign words per block (multiple of 8)
+  // column nA (when bcol != null) is b: the [A | b] pass of the SAA solve
+  int64_t nA;
+  const double* bcol;
+  double* outb;
 };
+
+__device__ __forceinline__ const double* sr_src(const SrParams& p, int64_t col) {
+  return col < p.nA ? p.A + col * p.lda : p.bcol;
+}
+__device__ __forceinline__ double* sr_dst(const SrParams& p, int64_t col) {
+  return col < p.nA ? p.out + col * p.ldo : p.outb;
+}
 
 // One pass of NB butterfly stages at bits [lo, lo+NB).  FIRST reads the
 // natural-layout stage buffer, applies the signs (bit i of the task's packed
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParam
     if (tid == SR_NT) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      const double* colp = p.A + col * p.lda;
+      const double* colp = sr_src(p, col);
       for (int64_t it = 0; it < niter; ++it) {
         const int s = (int)(it % SR_STAGES);
         if (it >= SR_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / SR_STAGES) + 1) & 1));
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(SR_NT + 32, 1) srht_dense_kernel(const SrParam
     const int64_t i = (int64_t)k * SR_NT + tid;
     if (i >= p.d) continue;
     if (p.P == 1)
-      p.out[col * p.ldo + i] = acc[k] / p.inv_scale_div;
+      sr_dst(p, col)[i] = acc[k] / p.inv_scale_div;
     else
       p.part[((int64_t)blockIdx.y * p.n + col) * p.d + i] = acc[k];
   }
@@ -325,7 +336,7 @@ __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
   __syncthreads();
   // after the transpose thread t holds e = 64 t + i: sampled bits i
   const uint64_t smask = ((uint64_t)sbm[2 * t + 1] << 32) | sbm[2 * t];
-  const double* colp = p.A + col * p.lda;
+  const double* colp = sr_src(p, col);
   const uint64_t* sw64 = reinterpret_cast<const uint64_t*>(p.sbits);
 
   double v[64];
@@ -402,21 +413,21 @@ __global__ void __launch_bounds__(SR2_NT, 2) srht_reg_kernel(const SrParams p) {
     if (kk == 0xffffffffu) continue;
     const int64_t i = kk;
     if (p.P == 1)
-      p.out[col * p.ldo + i] = acc[k] / p.inv_scale_div;
+      sr_dst(p, col)[i] = acc[k] / p.inv_scale_div;
     else
       p.part[((int64_t)blockIdx.y * p.n + col) * p.d + i] = acc[k];
   }
 }
 
 __global__ void srht_reduce_kernel(const double* part, int P, int64_t n, int64_t d, double* out,
-                                   int64_t ldo, double div) {
+                                   int64_t ldo, double div, int64_t nA, double* outb) {
   const int64_t total = n * d;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t col = idx / d, i = idx % d;
     double s = 0.0;
     for (int q = 0; q < P; ++q) s += part[((int64_t)q * n + col) * d + i];
-    out[col * ldo + i] = s / div;
+    (col < nA ? out + col * ldo : outb)[i] = s / div;
   }
 }
 
@@ -460,13 +471,17 @@ static cudaError_t launch_srht(const SrParams& p, dim3 grid, size_t smem, cudaSt
 
 int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16_t* sbits,
                 const int64_t* sample, int64_t m_pad, int64_t d, double* SA, int64_t ldsa,
-                int64_t row_offset, int partitions, cudaStream_t st, int64_t d_scale = 0) {
+                int64_t row_offset, int partitions, cudaStream_t st, int64_t d_scale = 0,
+                const double* bvec = nullptr, double* Sb = nullptr) {
   // d_scale: the embedding dimension the 1/sqrt(d) normalisation uses (the
   // whole d when this launch covers a slice of the sampled rows)
   if (d_scale <= 0) d_scale = d;
   const int64_t* sample_ = sample;
   SKL_REQUIRE(A && sbits && sample && SA && m >= 1 && n >= 1 && d >= 1 && lda >= m && ldsa >= d,
               SKL_ERR_SHAPE, "srht: bad arguments");
+  SKL_REQUIRE(!bvec == !Sb, SKL_ERR_INVALID, "srht: b and Sb go together");
+  const int64_t nA = n;
+  if (bvec) n = nA + 1;  // b rides along as the last column
   SKL_REQUIRE(m_pad >= 1 && (m_pad & (m_pad - 1)) == 0, SKL_ERR_SHAPE,
               "srht: padded dimension %lld is not a power of two", (long long)m_pad);
   if (d > 32 * SR_NT) {
@@ -475,7 +490,8 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
     for (int64_t k0 = 0; k0 < d; k0 += 32 * SR_NT) {
       const int64_t dk = std::min<int64_t>(32 * SR_NT, d - k0);
       const int rc = srht_launch(A, m, n, lda, sbits, sample + k0, m_pad, dk, SA + k0, ldsa,
-                                 row_offset, partitions, st, d_scale);
+                                 row_offset, partitions, st, d_scale, bvec,
+                                 Sb ? Sb + k0 : nullptr);
       if (rc) return rc;
     }
     return SKL_OK;
@@ -498,7 +514,11 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   const int64_t nblk = (m + B - 1) / B;
   int P = partitions;
   if (P <= 0) {
-    if (b == 12) {
+    if (b == 12 && 2 * n < 2 * (int64_t)sms) {
+      // few long columns (a vector S b): split each column's blocks over
+      // enough CTAs to fill the GPU
+      P = (int)((2 * (int64_t)sms + n - 1) / n);
+    } else if (b == 12) {
       // the register kernel runs 2 CTAs per SM: split the blocks of each
       // column so the grid fills whole waves (the few partial sums are
       // reduced in fixed order afterwards)
@@ -522,6 +542,7 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   p.sw_block = sw_block;
   p.jhi0 = row_offset >> b; p.P = P; p.out = SA; p.ldo = ldsa; p.part = nullptr;
   p.inv_scale_div = std::sqrt((double)d_scale);
+  p.nA = nA; p.bcol = bvec; p.outb = Sb;
   double* part = nullptr;
   if (P > 1) {
     SKL_CUDA(malloc_async(&part, (size_t)P * n * d * sizeof(double), st));
@@ -544,7 +565,8 @@ int srht_launch(const double* A, int64_t m, int64_t n, int64_t lda, const uint16
   if (P > 1) {
     const int64_t total = n * d;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4LL * sms);
-    srht_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, n, d, SA, ldsa, std::sqrt((double)d_scale));
+    srht_reduce_kernel<<<blocks, 256, 0, st>>>(part, P, n, d, SA, ldsa, std::sqrt((double)d_scale),
+                                               nA, Sb);
     SKL_CUDA_LAUNCH();
     SKL_CUDA(cudaFreeAsync(part, st));
   }
@@ -592,6 +614,17 @@ extern "C" int skl_srht_dense(const double* A, int64_t m, int64_t n, int64_t lda
   clear_error();
   return srht_launch(A, m, n, lda, sign_bits, row_sample, m_pad, d, SA, ldsa, 0, 0,
                      (cudaStream_t)stream);
+}
+
+extern "C" int skl_srht_dense_ab(const double* A, int64_t m, int64_t n, int64_t lda,
+                                 const double* b, const uint16_t* sign_bits,
+                                 const int64_t* row_sample, int64_t m_pad, int64_t d,
+                                 int64_t row_offset, double* SA, int64_t ldsa, double* Sb,
+                                 int partitions, void* stream) {
+  clear_error();
+  SKL_REQUIRE(b && Sb, SKL_ERR_INVALID, "srht_dense_ab: b and Sb are required");
+  return srht_launch(A, m, n, lda, sign_bits, row_sample, m_pad, d, SA, ldsa, row_offset,
+                     partitions, (cudaStream_t)stream, 0, b, Sb);
 }
 
 extern "C" int skl_srht_dense_shard(const double* A, int64_t m_local, int64_t n, int64_t lda,

@@ -274,12 +274,12 @@ def local_partial_device(plan: ShardPlan, A_local, lda: int, b_local, dest: int 
     if plan.kind == "countsketch":
         plan.device_plan().apply(A_local, m_loc, n, lda, b_local, base, ld, col_n, partitions=1)
     elif plan.kind == "srht":
+        # [A | b] of the shard in one pass, b as the last column
         words = plan.device_srht_words()
         _, sample = plan.op.device_srht()
-        for src, ncol, ldsrc, dst in ((A_local, n, lda, base), (b_local, 1, m_loc, col_n)):
-            _native.call("skl_srht_dense_shard", _native.ptr(src), m_loc, ncol, ldsrc,
-                         _native.ptr(words), _native.ptr(sample), plan.op.padded_dim, d, plan.r0,
-                         _native.ptr(dst), ld, st)
+        _native.call("skl_srht_dense_ab", _native.ptr(A_local), m_loc, n, lda, _native.ptr(b_local),
+                     _native.ptr(words), _native.ptr(sample), plan.op.padded_dim, d, plan.r0,
+                     _native.ptr(base), ld, _native.ptr(col_n), 1, st)
     else:
         Gs, ldg = plan.device_gaussian()
         for src, ncol, ldsrc, dst in ((A_local, n, lda, base), (b_local, 1, m_loc, col_n)):

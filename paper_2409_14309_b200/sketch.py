@@ -287,6 +287,11 @@ class SketchOperator:
                 ev.record(torch.cuda.current_stream())
                 entry = c[name] = (value, ev)
         value, ev = entry
+        if torch.cuda.is_current_stream_capturing():
+            # inside a CUDA-graph capture the artifact was built before the
+            # capture began (the warm-up call); an event from outside the
+            # capture cannot be waited on there
+            return value
         st = torch.cuda.current_stream()
         st.wait_event(ev)
         for t in _tensors_of(value):
@@ -575,6 +580,21 @@ def _srht_device(op: SketchOperator, A, lda: int, n: int):
     _native.call("skl_srht_dense", _native.ptr(A), op.source_dim, n, lda, _native.ptr(signs),
                  _native.ptr(sample), op.padded_dim, d, _native.ptr(SA), d, current_stream())
     return SA
+
+
+def _srht_device_ab(op: SketchOperator, A, lda: int, n: int, b):
+    """(S A, S b) of a dense [A | b] in one SRHT pass (b as the last column)."""
+    signs, sample = op.device_srht()
+    A, lda = _aligned(A, lda, n)
+    if lda % 2 and n > 1:
+        A, lda = _aligned(A.clone(), lda, n)
+    d = op.target_dim
+    SA = device_f64((d, n), fortran=True)
+    Sb = device_f64((d,))
+    _native.call("skl_srht_dense_ab", _native.ptr(A), op.source_dim, n, lda, _native.ptr(b),
+                 _native.ptr(signs), _native.ptr(sample), op.padded_dim, d, 0, _native.ptr(SA), d,
+                 _native.ptr(Sb), 0, current_stream())
+    return SA, Sb
 
 
 def _gaussian_device(op: SketchOperator, A, lda: int, n: int):

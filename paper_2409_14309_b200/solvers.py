@@ -33,6 +33,7 @@ from .sketch import (
     _countsketch_csr_device,
     _countsketch_dense_device,
     _few_long_columns,
+    _srht_device_ab,
     build_sketch,
     default_embed_dim,
 )
@@ -154,6 +155,8 @@ def sketch_operands_device(op, A: Matrix, b: Vector):
     lda = A.ld if A.on_device else A.rows
     if op.kind in ("countsketch", "sparsesign"):
         SA, Sb = _countsketch_dense_device(op, A_dev, lda, A.cols, b=b_dev)
+    elif op.kind == "srht":
+        SA, Sb = _srht_device_ab(op, A_dev, lda, A.cols, b_dev.contiguous())
     else:
         SA = _apply_dense_tensor(op, A_dev, A.rows, A.cols, lda=lda)
         Sb = _apply_dense_tensor(op, b_dev.reshape(-1, 1), A.rows, 1, lda=A.rows).reshape(-1)

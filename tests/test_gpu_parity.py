@@ -814,3 +814,41 @@ def test_qr_solve_wide_system():
     x, _, _ = qr_solve_device(Md, d, torch.from_numpy(y).cuda(), d, n)
     want = np.linalg.lstsq(M, y, rcond=None)[0]
     assert rel_fro(x.cpu().numpy(), want) <= 1e-10
+
+
+@pytest.mark.parametrize("m,n,d", [(1 << 16, 5, 256), (100_000, 3, 64), (1 << 20, 1, 2048)])
+def test_srht_ab_single_pass(m, n, d):
+    """S [A | b] in one SRHT pass (b as the last column, the SAA solve's
+    path) against the oracle's separate applies; a single long column (the
+    vector apply, split over enough CTAs to fill the GPU) too."""
+    from paper_2409_14309_b200.sketch import _srht_device_ab
+
+    rng = np.random.default_rng(m + n)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    op = E.build_sketch(E.SketchSpec("srht", d, seed=m ^ d), m)
+    SA, Sb = _srht_device_ab(op, torch.from_numpy(A).cuda(), m, n, torch.from_numpy(b).cuda())
+    ref_A, ref_b = O.sketch_apply("srht", O.derive_seed(m ^ d, "srht", m), d, A, b)
+    assert rel_fro(SA.cpu().numpy(), ref_A) <= 1e-13
+    assert rel_fro(Sb.cpu().numpy(), ref_b) <= 1e-13
+    v = E.apply_to_vector(op, E.Vector(torch.from_numpy(b).cuda())).data.cpu().numpy()
+    assert rel_fro(v, ref_b) <= 1e-13
+
+
+@pytest.mark.parametrize("kind", ["countsketch", "srht", "gaussian"])
+def test_apply_captures_in_cuda_graph(kind):
+    """A warmed-up apply captures in a CUDA graph (the cached operator's
+    artifacts are not waited on inside the capture) and replays exactly."""
+    m, n, d = 50_000, 6, 256
+    A = torch.randn((n, m), dtype=torch.float64, device="cuda").t()
+    op = E.build_sketch(E.SketchSpec(kind, d, seed=3), m)
+    from paper_2409_14309_b200.sketch import _apply_dense_tensor
+
+    want = _apply_dense_tensor(op, A, m, n, lda=m).clone()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = _apply_dense_tensor(op, A, m, n, lda=m)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)

@@ -109,6 +109,10 @@ def run(cfg_id: int, reps: int):
                    gbs=round(byts / ms / 1e6, 1), frac_hbm=round(byts / ms / 1e6 / PEAK_HBM, 4))
         SA = _countsketch_csr_device(op, Ac)
         Sb, _ = _countsketch_dense_device(op, b.reshape(-1, 1), c.m, 1)
+        # S b: one long column -> the ordered bucket walk (bitwise csr_matvec)
+        vms, _ = timed_graph(lambda: _countsketch_dense_device(op, b.reshape(-1, 1), c.m, 1), reps)
+        out.update(sb_ordered_walk_ms=round(vms, 4),
+                   sb_gbs=round(8 * c.m / vms / 1e6, 1))
         out["qr_ms"] = round(timed(lambda: qr_solve_device(SA, c.d, Sb[:, 0], c.d, c.n), 3), 3)
         out["solve"] = solve_rate(Ac, b, "countsketch", c.d, c.n)
         return out
@@ -128,7 +132,7 @@ def run(cfg_id: int, reps: int):
             ms, graph = timed_graph(lambda: _srht_device(op, A, lda, c.n), reps)
             byts = 8 * c.m * c.n
             rec.update(kernel_ms=round(ms, 4), graph_timed=graph, gbs=round(byts / ms / 1e6, 1),
-                       frac_hbm=round(byts / ms / 1e6 / PEAK_HBM, 4), note="A only (b is a second launch)")
+                       frac_hbm=round(byts / ms / 1e6 / PEAK_HBM, 4), note="A only (the SAA solve sketches [A | b] in one pass, skl_srht_dense_ab)")
         elif kind == "gaussian":
             t0 = time.perf_counter()
             G, ldg = op.device_gaussian()
