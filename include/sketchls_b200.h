@@ -256,6 +256,36 @@ int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z, do
 /* v <- v / alfa (alfa > 0), y = R^-1 v (R NULL: y = v). */
 int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double alfa, double* v, double* y,
                     void* stream);
+
+/* The same two triangular solves with the inverted 32 x 32 diagonal blocks
+ * of R (skl_lsqr_rinv_blocks, computed once per preconditioned solve: R
+ * does not change across iterations): each block step is one 32-term
+ * product instead of 32 dependent divide-and-update steps.  Rinv holds
+ * ceil(n / 32) * 1024 doubles (device). */
+int skl_lsqr_rinv_blocks(const double* R, int64_t ldr, int64_t n, double* Rinv, void* stream);
+int skl_lsqr_trsv_t_inv(const double* R, int64_t ldr, int64_t n, const double* Rinv,
+                        const double* z, double beta, const double* v_prev, double* v_out,
+                        double* norm2, void* stream);
+int skl_lsqr_trsv_n_inv(const double* R, int64_t ldr, int64_t n, const double* Rinv, double alfa,
+                        double* v, double* y, void* stream);
+
+/* Device-driven LSQR iteration (dense, n <= 256): the scalar recurrence of
+ * solvers.py:193-222 runs on the device in `state` (skl_lsqr_state_size()
+ * doubles: ||r||^2, ||v||^2, ||x||^2, alfa, beta, rhobar, phibar, anorm,
+ * phi/rho, -theta/rho, rnorm, arnorm, the next pass's beta_prev, ...), with
+ * the host loop's IEEE operations in the same order, so the host reads the
+ * state once per iteration -- while the next pass already runs.
+ * skl_lsqr_fused_dev is skl_lsqr_fused taking alfa and beta_prev from
+ * state; skl_lsqr_step_dev runs the rest of one iteration: R^-T z - beta v
+ * (beta from state), v_n and y = R^-1 v_n (alfa from state), the recurrence,
+ * and x += c1 w, w = v_n + c2 w.  v holds v on entry and v_n on exit. */
+int64_t skl_lsqr_state_size(void);
+int skl_lsqr_fused_dev(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                       const double* r_prev, double* r_out, double* z, double* norm2,
+                       double* work, unsigned int* counters, const double* state, void* stream);
+int skl_lsqr_step_dev(const double* R, int64_t ldr, int64_t n, const double* Rinv,
+                      const double* z, double* v, double* v_raw, double* y, double* w, double* x,
+                      double* state, void* stream);
 /* CSR operands: u_out = s (A y) - alpha u_in, *norm2 = ||u_out||^2 (rows
  * folded in stored order); and u_n = u_raw / beta, z = A^T u_n from the
  * CSC form of A (colptr int64 n+1, rowidx int32 ascending within a column,

@@ -113,6 +113,83 @@ class _Workspace:
         self.counters = torch.zeros(nc, dtype=torch.int32, device="cuda")
 
 
+# indices of the device-side recurrence state (csrc/skl_lsqr.cu, LS_*)
+_LS_BETA2, _LS_ALFA2, _LS_XNORM2, _LS_ALFA, _LS_BETA = 0, 1, 2, 3, 4
+_LS_RHOBAR, _LS_PHIBAR, _LS_ANORM, _LS_RNORM, _LS_ARNORM, _LS_BPREV = 5, 6, 7, 10, 11, 12
+
+
+def _lsqr_device_driven(op, ws, fwork, n, Rp, ldr, Rinv, alfa, beta, atol, btol, max_iter, R,
+                        trsv_n, callback, st):
+    """The fused-pass LSQR loop with the scalar recurrence on the device
+    (skl_lsqr_step_dev): per iteration one D2H read of the state, taken
+    while the next iteration's pass over A already runs (it does not depend
+    on the stopping decision, and if the loop stops its result is unused).
+    The recurrence performs the host loop's IEEE operations in the same
+    order, so iterates, iteration counts and stopping rule are the same."""
+    P = _native.ptr
+    nst = int(_native.lib().skl_lsqr_state_size())
+    state = torch.zeros(nst, dtype=torch.float64, device="cuda")
+    init = torch.zeros(nst, dtype=torch.float64)
+    init[_LS_ALFA], init[_LS_RHOBAR], init[_LS_PHIBAR], init[_LS_BPREV] = alfa, alfa, beta, beta
+    state.copy_(init)
+    rep = torch.empty(nst, dtype=torch.float64, pin_memory=True)
+    done = torch.cuda.Event()
+    bnorm = beta
+    r_prev, r_out = ws.u_raw, ws.u
+
+    def enqueue_pass(rp, ro):
+        _native.call("skl_lsqr_fused_dev", P(op.A), op.m, op.n, op.lda, P(ws.y), P(rp), P(ro),
+                     P(ws.z), state.data_ptr() + 8 * _LS_BETA2, P(fwork), P(ws.counters),
+                     P(state), st)
+
+    enqueue_pass(r_prev, r_out)
+    itn = istop = 0
+    while itn < max_iter:
+        itn += 1
+        _native.call("skl_lsqr_step_dev", Rp, ldr, n, P(Rinv), P(ws.z), P(ws.v), P(ws.v_raw),
+                     P(ws.y), P(ws.w), P(ws.x), P(state), st)
+        rep.copy_(state, non_blocking=True)
+        done.record()
+        r_prev, r_out = r_out, r_prev
+        if itn < max_iter:
+            enqueue_pass(r_prev, r_out)  # the next pass overlaps the host's read
+        done.synchronize()
+        s_ = rep.tolist()
+        alfa, beta = s_[_LS_ALFA], s_[_LS_BETA]
+        anorm, rnorm, arnorm = s_[_LS_ANORM], s_[_LS_RNORM], s_[_LS_ARNORM]
+        if not (math.isfinite(alfa) and math.isfinite(beta)):
+            raise NumericalBreakdownError(
+                f"non-finite bidiagonalization coefficient at iteration {itn}")
+        xnorm = math.sqrt(s_[_LS_XNORM2])
+        if not math.isfinite(rnorm):
+            raise NumericalBreakdownError(f"non-finite residual estimate at iteration {itn}")
+        if callback is not None:
+            callback(itn, ws.x.cpu().numpy(), rnorm)
+        test1 = rnorm / bnorm
+        test2 = arnorm / (anorm * rnorm + _EPS)
+        t1 = test1 / (1.0 + anorm * xnorm / bnorm)
+        rtol = btol + atol * anorm * xnorm / bnorm
+        if itn >= max_iter:
+            istop = 7
+        if 1.0 + test2 <= 1.0:
+            istop = 5
+        if 1.0 + t1 <= 1.0:
+            istop = 4
+        if test2 <= atol:
+            istop = 2
+        if test1 <= rtol:
+            istop = 1
+        if istop != 0:
+            break
+    x = ws.x
+    if R is not None:
+        xr = device_f64((n,))
+        tmp = ws.x.clone()
+        trsv_n(0.0, tmp, xr)
+        x = xr
+    return x, itn, istop
+
+
 def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
                 R=None, ldr: int = 0, callback=None):
     """LSQR on the device for the operator ``op`` (DenseOperator or
@@ -128,6 +205,27 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
     P = _native.ptr
     Rp = P(R) if R is not None else None
     sc = ws.scal
+    # R is fixed for the whole solve: invert its 32 x 32 diagonal blocks once
+    # and let every triangular solve use them (SKL_LSQR_DTRTRS=1 keeps the
+    # per-element dtrsv substitution order instead)
+    Rinv = None
+    if R is not None and not os.environ.get("SKL_LSQR_DTRTRS"):
+        Rinv = device_f64((((n + 31) // 32) * 1024,))
+        _native.call("skl_lsqr_rinv_blocks", Rp, ldr, n, P(Rinv), st)
+
+    def trsv_t(z, beta_, v_prev, v_out, norm2):
+        if Rinv is not None:
+            _native.call("skl_lsqr_trsv_t_inv", Rp, ldr, n, P(Rinv), P(z), beta_, P(v_prev),
+                         P(v_out), P(norm2), st)
+        else:
+            _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(z), beta_, P(v_prev), P(v_out),
+                         P(norm2), st)
+
+    def trsv_n(alfa_, v, y):
+        if Rinv is not None:
+            _native.call("skl_lsqr_trsv_n_inv", Rp, ldr, n, P(Rinv), alfa_, P(v), P(y), st)
+        else:
+            _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa_, P(v), P(y), st)
 
     def read(i: int) -> float:
         return float(sc[i].item())
@@ -141,14 +239,13 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
         # u /= beta; v = rmv(u); alfa = ||v||
         op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
         ws.v.zero_()
-        _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), 0.0, P(ws.v), P(ws.v_raw),
-                     P(sc[1:2]), st)
+        trsv_t(ws.z, 0.0, ws.v, ws.v_raw, sc[1:2])
         alfa = math.sqrt(read(1))
     else:
         ws.u.copy_(ws.u_raw)
         ws.v_raw.zero_()
     # v /= alfa (if alfa > 0); y = R^-1 v; w = v
-    _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa, P(ws.v_raw), P(ws.y), st)
+    trsv_n(alfa, ws.v_raw, ws.y)
     ws.v.copy_(ws.v_raw)
     ws.w.copy_(ws.v)
 
@@ -164,6 +261,9 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
     if fused:
         fwork = device_f64((int(_native.lib().skl_lsqr_fused_work_size(n)),))
         r_prev, r_out, beta_prev = ws.u_raw, ws.u, beta
+        if not os.environ.get("SKL_LSQR_HOST_LOOP"):
+            return _lsqr_device_driven(op, ws, fwork, n, Rp, ldr, Rinv, alfa, beta, atol, btol,
+                                       max_iter, R, trsv_n, callback, st)
 
     while itn < max_iter:
         itn += 1
@@ -182,10 +282,9 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
             # u /= beta ; v = rmv(u) - beta v ; alfa = ||v|| ; v /= alfa
             if not fused:
                 op.rmv(ws.u_raw, beta, ws.u, ws.z, ws, st)
-            _native.call("skl_lsqr_trsv_t", Rp, ldr, n, P(ws.z), beta, P(ws.v), P(ws.v_raw),
-                         P(sc[1:2]), st)
+            trsv_t(ws.z, beta, ws.v, ws.v_raw, sc[1:2])
             alfa = math.sqrt(read(1))
-            _native.call("skl_lsqr_trsv_n", Rp, ldr, n, alfa, P(ws.v_raw), P(ws.y), st)
+            trsv_n(alfa, ws.v_raw, ws.y)
             ws.v, ws.v_raw = ws.v_raw, ws.v
         elif not fused:
             ws.u, ws.u_raw = ws.u_raw, ws.u  # u stays unnormalised (solvers.py:193)
@@ -231,6 +330,6 @@ def lsqr_device(op, m: int, n: int, b, atol: float, btol: float, max_iter: int,
     if R is not None:
         xr = device_f64((n,))
         tmp = ws.x.clone()
-        _native.call("skl_lsqr_trsv_n", Rp, ldr, n, 0.0, P(tmp), P(xr), st)
+        trsv_n(0.0, tmp, xr)
         x = xr
     return x, itn, istop

@@ -26,6 +26,25 @@
 namespace skl {
 
 constexpr int LQ_NT = 256;
+
+// Device-driven LSQR iteration (skl_lsqr_*_dev): the scalar state the host
+// loop would otherwise read back three times per iteration, as doubles.
+enum {
+  LS_BETA2 = 0,   // ||r||^2 of the step's pass (written by the fused pass)
+  LS_ALFA2 = 1,   // ||v||^2 (written by the transposed solve)
+  LS_XNORM2 = 2,  // ||x||^2 (written by the x/w update)
+  LS_ALFA = 3,    // alfa of the current step (the recurrence's input / output)
+  LS_BETA = 4,
+  LS_RHOBAR = 5,
+  LS_PHIBAR = 6,
+  LS_ANORM = 7,
+  LS_C1 = 8,      // phi / rho
+  LS_C2 = 9,      // -theta / rho
+  LS_RNORM = 10,
+  LS_ARNORM = 11,
+  LS_BPREV = 12,  // beta the next pass divides r by (1 when beta == 0)
+  LS_STATE = 16
+};
 constexpr int LQ_YMAX = 8192;  // y staged in shared memory up to this n
 constexpr int LQ_TC = 16;      // columns per CTA in the transposed product
 
@@ -215,7 +234,12 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
     const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ y,
     double s, double alpha, const double* __restrict__ r_prev, double beta_prev,
     double* __restrict__ r_out, double* __restrict__ zpart, double* __restrict__ npart,
-    double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter) {
+    double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter,
+    const double* __restrict__ dscal) {
+  if (dscal) {  // device-driven iteration: alfa and beta_prev from the recurrence state
+    alpha = dscal[LS_ALFA];
+    beta_prev = dscal[LS_BPREV];
+  }
   __shared__ double ys[8 * NC];
   __shared__ double pdot[2][8][LF_RB];  // by block parity: one barrier less per block
   __shared__ double rs[2][LF_RB];
@@ -233,6 +257,10 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, par ^= 1) {
     const int64_t i0 = blk * LF_RB + 2 * lane;
     const bool full = i0 + 1 < m;
+    // the block's r_prev entries are loaded with A (not after the barrier:
+    // that would put a second memory latency on every block)
+    double rp = 0.0;
+    if (tid < LF_RB && r_prev && blk * LF_RB + tid < m) rp = __ldcs(r_prev + blk * LF_RB + tid);
     // the block's A values stay in registers for both phases: all NC loads
     // are in flight at once and nothing is read twice
     double2 v[NC];
@@ -267,7 +295,7 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
         double dot = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) dot += pdot[par][w][tid];
-        r = s * dot - (r_prev ? alpha * (r_prev[i] / beta_prev) : 0.0);
+        r = s * dot - (r_prev ? alpha * (rp / beta_prev) : 0.0);
         r_out[i] = r;
         ss = fma(r, r, ss);
       }
@@ -381,10 +409,19 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_csc_t_kernel(const int64_t* __rest
 constexpr int LT_NT = 512;
 
 // x <- R^-T x  (forward substitution with L = R^T)
-__device__ void lq_solve_t(const double* __restrict__ R, int64_t ldr, int n, double* xs) {
+// Rinv (optional): the inverted 32 x 32 diagonal blocks of R
+// (lsqr_trinv_kernel; block b covers rows [n - 32(b+1), n - 32b), clipped at
+// 0, row-major): the block step becomes one 32-term product instead of 32
+// dependent divide-and-update steps.  Without it the substitution keeps
+// dtrsv's division order.
+__device__ void lq_solve_t(const double* __restrict__ R, int64_t ldr, int n, double* xs,
+                           const double* __restrict__ Rinv = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int lo = 0; lo < n; lo += 32) {
-    const int w = min(32, n - lo);
+  // with Rinv the blocks align with the inverses (from the bottom, the top
+  // one partial); without, from the top as dtrsv's column sweep
+  const int first = (Rinv && n % 32) ? n % 32 : 32;
+  for (int lo = 0; lo < n; lo += (lo == 0 ? first : 32)) {
+    const int w = min(lo == 0 ? first : 32, n - lo);
     // xs[lo + r] -= sum_{j < lo} R[j][lo + r] xs[j]
     for (int r = warp; r < w; r += LT_NT / 32) {
       const double* col = R + (int64_t)(lo + r) * ldr;
@@ -395,7 +432,21 @@ __device__ void lq_solve_t(const double* __restrict__ R, int64_t ldr, int n, dou
       if (lane == 0) xs[lo + r] -= t;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (Rinv && warp == 0) {
+      // x_b = Rinv_b^T y_b (lane r: column r of Rinv_b)
+      // (a partial top block occupies the w x w top-left corner of its slot)
+      const double* Ri = Rinv + (int64_t)((n - lo - w) / 32) * 1024;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const double y0 = (j < w) ? xs[lo + j] : 0.0;
+        const double y1 = (j + 1 < w) ? xs[lo + j + 1] : 0.0;
+        a0 = fma((j < w && lane < w) ? Ri[j * 32 + lane] : 0.0, y0, a0);
+        a1 = fma((j + 1 < w && lane < w) ? Ri[(j + 1) * 32 + lane] : 0.0, y1, a1);
+      }
+      __syncwarp();
+      if (lane < w) xs[lo + lane] = a0 + a1;
+    } else if (warp == 0) {
       // lane r holds column lo + r: Rc[j] = R[lo + j][lo + r] (j < r), diag
       double Rc[32];
 #pragma unroll
@@ -419,12 +470,29 @@ __device__ void lq_solve_t(const double* __restrict__ R, int64_t ldr, int n, dou
 }
 
 // x <- R^-1 x  (backward substitution, dtrsv 'U','N' column order per block)
-__device__ void lq_solve_n(const double* __restrict__ R, int64_t ldr, int n, double* xs) {
+__device__ void lq_solve_n(const double* __restrict__ R, int64_t ldr, int n, double* xs,
+                           const double* __restrict__ Rinv = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double xb[32];
   for (int hi = n; hi > 0; hi -= 32) {
     const int lo = max(0, hi - 32), w = hi - lo;
-    if (warp == 0) {
+    if (Rinv && warp == 0) {
+      // x_b = Rinv_b y_b (lane r: row r of Rinv_b)
+      const double* Ri = Rinv + (int64_t)((n - hi) / 32) * 1024;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const double y0 = (j < w) ? xs[lo + j] : 0.0;
+        const double y1 = (j + 1 < w) ? xs[lo + j + 1] : 0.0;
+        a0 = fma((j < w && lane < w) ? Ri[lane * 32 + j] : 0.0, y0, a0);
+        a1 = fma((j + 1 < w && lane < w) ? Ri[lane * 32 + j + 1] : 0.0, y1, a1);
+      }
+      __syncwarp();
+      if (lane < w) {
+        xs[lo + lane] = a0 + a1;
+        xb[lane] = a0 + a1;
+      }
+    } else if (warp == 0) {
       // lane r holds row lo + r: Rr[j] = R[lo + r][lo + j] (j > r)
       double Rr[32];
 #pragma unroll
@@ -462,16 +530,58 @@ __device__ void lq_solve_n(const double* __restrict__ R, int64_t ldr, int n, dou
 }
 
 // v_out = R^-T z - beta v_prev (R null: identity), ||v_out||^2.
+// The inverted 32 x 32 diagonal blocks of an explicit upper-triangular R
+// (column-major, ld ldr): block b = rows [max(0, n - 32(b+1)), n - 32b), a
+// partial top block in the top-left w x w corner of its slot with identity
+// padding; Rinv_b[i][k] at Rinv[b * 1024 + i * 32 + k].  One warp per block:
+// lane l solves R_bb X = e_l upward (column l of the inverse), each finished
+// X[k] folded into the running sums of the rows above at once.
+__global__ void __launch_bounds__(128) lsqr_trinv_kernel(const double* __restrict__ R,
+                                                         int64_t ldr, int n,
+                                                         double* __restrict__ Rinv) {
+  __shared__ double Rs[4][32][33];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int bi = blockIdx.x * 4 + wl;
+  const int nb = (n + 31) / 32;
+  if (bi >= nb) return;
+  const int hi = n - 32 * bi, lo = hi > 32 ? hi - 32 : 0, w = hi - lo;
+  double (*Rb)[33] = Rs[wl];
+#pragma unroll
+  for (int j = 0; j < 32; ++j)  // lane = row
+    Rb[lane][j] = (lane < w && j < w) ? (j >= lane ? R[(int64_t)(lo + j) * ldr + lo + lane] : 0.0)
+                                      : (j == lane ? 1.0 : 0.0);
+  __syncwarp();
+  const double rd = 1.0 / Rb[lane][lane];
+  double acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+  double* out = Rinv + (int64_t)bi * 1024;
+#pragma unroll
+  for (int k = 31; k >= 0; --k) {
+    const double rk = __shfl_sync(0xffffffffu, rd, k);
+    const double xk = k == lane ? rk : (k < lane ? -acc[k] * rk : 0.0);
+    out[k * 32 + lane] = xk;  // Rinv_b[k][lane]
+#pragma unroll
+    for (int i = 0; i < k; ++i) acc[i] = fma(Rb[i][k], xk, acc[i]);
+  }
+}
+
 __global__ void __launch_bounds__(LT_NT) lsqr_trsv_t_kernel(const double* __restrict__ R,
                                                             int64_t ldr, int n,
                                                             const double* __restrict__ z,
                                                             double beta, const double* v_prev,
-                                                            double* v_out, double* norm2) {
+                                                            double* v_out, double* norm2,
+                                                            const double* __restrict__ Rinv,
+                                                            const double* __restrict__ dscal) {
   extern __shared__ double xs[];
   __shared__ double red[32];
+  if (dscal) {  // beta = ||r|| of the step's pass; nothing to do when it is 0
+    beta = sqrt(dscal[LS_BETA2]);
+    if (beta == 0.0) return;
+  }
   for (int i = threadIdx.x; i < n; i += LT_NT) xs[i] = z[i];
   __syncthreads();
-  if (R) lq_solve_t(R, ldr, n, xs);
+  if (R) lq_solve_t(R, ldr, n, xs, Rinv);
   double ss = 0.0;
   for (int i = threadIdx.x; i < n; i += LT_NT) {
     const double v = xs[i] - beta * v_prev[i];
@@ -485,23 +595,36 @@ __global__ void __launch_bounds__(LT_NT) lsqr_trsv_t_kernel(const double* __rest
 // v_n = v_raw / alfa (alfa > 0; else unchanged), written back; y = R^-1 v_n.
 __global__ void __launch_bounds__(LT_NT) lsqr_trsv_n_kernel(const double* __restrict__ R,
                                                             int64_t ldr, int n, double alfa,
-                                                            double* v, double* y) {
+                                                            double* v, double* y,
+                                                            const double* __restrict__ Rinv,
+                                                            const double* __restrict__ dscal,
+                                                            double* __restrict__ vcopy) {
   extern __shared__ double xs[];
+  if (dscal) {  // alfa = ||v|| from the transposed solve; skipped when beta == 0
+    if (sqrt(dscal[LS_BETA2]) == 0.0) return;
+    alfa = sqrt(dscal[LS_ALFA2]);
+  }
   for (int i = threadIdx.x; i < n; i += LT_NT) {
     const double vn = alfa > 0.0 ? v[i] / alfa : v[i];
     v[i] = vn;
+    if (vcopy) vcopy[i] = vn;
     xs[i] = vn;
   }
   __syncthreads();
-  if (R) lq_solve_n(R, ldr, n, xs);
+  if (R) lq_solve_n(R, ldr, n, xs, Rinv);
   for (int i = threadIdx.x; i < n; i += LT_NT) y[i] = xs[i];
 }
 
 // x += c1 w; w = v + c2 w; ||x||^2
 __global__ void __launch_bounds__(LT_NT) lsqr_xw_kernel(int n, double c1, double c2,
                                                         const double* v, double* w, double* x,
-                                                        double* norm2) {
+                                                        double* norm2,
+                                                        const double* __restrict__ dscal) {
   __shared__ double red[32];
+  if (dscal) {
+    c1 = dscal[LS_C1];
+    c2 = dscal[LS_C2];
+  }
   double ss = 0.0;
   for (int i = threadIdx.x; i < n; i += LT_NT) {
     const double wi = w[i];
@@ -592,13 +715,12 @@ extern "C" int64_t skl_lsqr_fused_work_size(int64_t n) {
   return (int64_t)sm_count_lq() * 2 * (n + 1) + 64;
 }
 
-extern "C" int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
-                              double s, double alpha, const double* r_prev, double beta_prev,
-                              double* r_out, double* z, double* norm2, double* work,
-                              unsigned int* counters, void* stream) {
-  clear_error();
+static int fused_launch(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                        double s, double alpha, const double* r_prev, double beta_prev,
+                        double* r_out, double* z, double* norm2, double* work,
+                        unsigned int* counters, const double* dscal, void* stream) {
   SKL_REQUIRE(A && y && r_out && z && norm2 && work && counters && m >= 1 && n >= 1 &&
-                  n <= 256 && lda >= m && (!r_prev || beta_prev > 0.0),
+                  n <= 256 && lda >= m && (dscal || !r_prev || beta_prev > 0.0),
               SKL_ERR_INVALID, "lsqr_fused: bad arguments");
   SKL_REQUIRE(((uintptr_t)A & 15) == 0 && lda % 2 == 0, SKL_ERR_INVALID,
               "lsqr_fused: A must be 16-byte aligned with an even leading dimension");
@@ -616,7 +738,8 @@ extern "C" int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda
     const int gr = (int)std::max<int64_t>(                                                    \
         1, std::min<int64_t>({nblk, (int64_t)std::max(occ, 1) * sm_count_lq(), (int64_t)grid})); \
     lsqr_fused_kernel<NCV><<<gr, LQ_NT, 0, st>>>(A, m, n, lda, y, s, alpha, r_prev, beta_prev, \
-                                                 r_out, zpart, npart, z, norm2, counter);     \
+                                                 r_out, zpart, npart, z, norm2, counter,      \
+                                                 dscal);                                      \
   } while (0)
   if (nc <= 8)
     SKL_LF_LAUNCH(8);
@@ -629,16 +752,75 @@ extern "C" int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda
   return SKL_OK;
 }
 
-extern "C" int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z,
-                               double beta, const double* v_prev, double* v_out, double* norm2,
-                               void* stream) {
+extern "C" int skl_lsqr_fused(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                              double s, double alpha, const double* r_prev, double beta_prev,
+                              double* r_out, double* z, double* norm2, double* work,
+                              unsigned int* counters, void* stream) {
+  clear_error();
+  return fused_launch(A, m, n, lda, y, s, alpha, r_prev, beta_prev, r_out, z, norm2, work,
+                      counters, nullptr, stream);
+}
+
+extern "C" int skl_lsqr_fused_dev(const double* A, int64_t m, int64_t n, int64_t lda,
+                                  const double* y, const double* r_prev, double* r_out, double* z,
+                                  double* norm2, double* work, unsigned int* counters,
+                                  const double* state, void* stream) {
+  clear_error();
+  SKL_REQUIRE(state, SKL_ERR_INVALID, "lsqr_fused_dev: state is required");
+  return fused_launch(A, m, n, lda, y, 1.0, 0.0, r_prev, 1.0, r_out, z, norm2, work, counters,
+                      state, stream);
+}
+
+extern "C" int skl_lsqr_rinv_blocks(const double* R, int64_t ldr, int64_t n, double* Rinv,
+                                    void* stream) {
+  clear_error();
+  SKL_REQUIRE(R && Rinv && n >= 1 && ldr >= n && n <= 24 * 1024, SKL_ERR_INVALID,
+              "lsqr_rinv_blocks: bad arguments");
+  const int nb = (int)((n + 31) / 32);
+  lsqr_trinv_kernel<<<(nb + 3) / 4, 128, 0, (cudaStream_t)stream>>>(R, ldr, (int)n, Rinv);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+static int trsv_t_launch(const double* R, int64_t ldr, int64_t n, const double* z, double beta,
+                         const double* v_prev, double* v_out, double* norm2, const double* Rinv,
+                         void* stream, const double* dscal = nullptr) {
   clear_error();
   SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && z && v_prev && v_out && norm2 && (!R || ldr >= n),
               SKL_ERR_INVALID, "lsqr_trsv_t: bad arguments");
   const size_t smem = (size_t)n * sizeof(double);
   if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_trsv_t_kernel, smem));
   lsqr_trsv_t_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, z, beta, v_prev,
-                                                               v_out, norm2);
+                                                               v_out, norm2, Rinv, dscal);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const double* z,
+                               double beta, const double* v_prev, double* v_out, double* norm2,
+                               void* stream) {
+  clear_error();
+  return trsv_t_launch(R, ldr, n, z, beta, v_prev, v_out, norm2, nullptr, stream);
+}
+
+extern "C" int skl_lsqr_trsv_t_inv(const double* R, int64_t ldr, int64_t n, const double* Rinv,
+                                   const double* z, double beta, const double* v_prev,
+                                   double* v_out, double* norm2, void* stream) {
+  clear_error();
+  SKL_REQUIRE(R && Rinv, SKL_ERR_INVALID, "lsqr_trsv_t_inv: R and Rinv are required");
+  return trsv_t_launch(R, ldr, n, z, beta, v_prev, v_out, norm2, Rinv, stream);
+}
+
+static int trsv_n_launch(const double* R, int64_t ldr, int64_t n, double alfa, double* v,
+                         double* y, const double* Rinv, void* stream,
+                         const double* dscal = nullptr, double* vcopy = nullptr) {
+  clear_error();
+  SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && v && y && (!R || ldr >= n), SKL_ERR_INVALID,
+              "lsqr_trsv_n: bad arguments");
+  const size_t smem = (size_t)n * sizeof(double);
+  if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_trsv_n_kernel, smem));
+  lsqr_trsv_n_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, alfa, v, y, Rinv,
+                                                               dscal, vcopy);
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }
@@ -646,23 +828,110 @@ extern "C" int skl_lsqr_trsv_t(const double* R, int64_t ldr, int64_t n, const do
 extern "C" int skl_lsqr_trsv_n(const double* R, int64_t ldr, int64_t n, double alfa, double* v,
                                double* y, void* stream) {
   clear_error();
-  SKL_REQUIRE(n >= 1 && n <= 24 * 1024 && v && y && (!R || ldr >= n), SKL_ERR_INVALID,
-              "lsqr_trsv_n: bad arguments");
-  const size_t smem = (size_t)n * sizeof(double);
-  if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_trsv_n_kernel, smem));
-  lsqr_trsv_n_kernel<<<1, LT_NT, smem, (cudaStream_t)stream>>>(R, ldr, (int)n, alfa, v, y);
-  SKL_CUDA_LAUNCH();
-  return SKL_OK;
+  return trsv_n_launch(R, ldr, n, alfa, v, y, nullptr, stream);
+}
+
+extern "C" int skl_lsqr_trsv_n_inv(const double* R, int64_t ldr, int64_t n, const double* Rinv,
+                                   double alfa, double* v, double* y, void* stream) {
+  clear_error();
+  SKL_REQUIRE(R && Rinv, SKL_ERR_INVALID, "lsqr_trsv_n_inv: R and Rinv are required");
+  return trsv_n_launch(R, ldr, n, alfa, v, y, Rinv, stream);
 }
 
 extern "C" int skl_lsqr_xw(int64_t n, double c1, double c2, const double* v, double* w, double* x,
                            double* norm2, void* stream) {
   clear_error();
   SKL_REQUIRE(n >= 1 && v && w && x && norm2, SKL_ERR_INVALID, "lsqr_xw: bad arguments");
-  lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, c1, c2, v, w, x, norm2);
+  lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, c1, c2, v, w, x, norm2, nullptr);
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }
+
+// One step of LSQR's scalar recurrence on the device (solvers.py:193-222 as
+// the host loop writes it, the same IEEE operations in the same order: no
+// contraction, correctly rounded sqrt and division), so the host reads the
+// state once per iteration instead of three times.
+__device__ __forceinline__ void ls_sym_ortho(double a, double b, double* c, double* s,
+                                             double* r) {
+  if (b == 0.0) {
+    *c = a != 0.0 ? copysign(1.0, a) : 1.0;
+    *s = 0.0;
+    *r = fabs(a);
+    return;
+  }
+  if (a == 0.0) {
+    *c = 0.0;
+    *s = copysign(1.0, b);
+    *r = fabs(b);
+    return;
+  }
+  if (fabs(b) > fabs(a)) {
+    const double tau = __ddiv_rn(a, b);
+    const double sn = __ddiv_rn(copysign(1.0, b), __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(tau, tau))));
+    *c = __dmul_rn(sn, tau);
+    *s = sn;
+    *r = __ddiv_rn(b, sn);
+    return;
+  }
+  const double tau = __ddiv_rn(b, a);
+  const double cs = __ddiv_rn(copysign(1.0, a), __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(tau, tau))));
+  *c = cs;
+  *s = __dmul_rn(cs, tau);
+  *r = __ddiv_rn(a, cs);
+}
+
+__global__ void lsqr_recur_kernel(double* st) {
+  const double beta = __dsqrt_rn(st[LS_BETA2]);
+  double alfa = st[LS_ALFA];
+  double anorm = st[LS_ANORM];
+  if (beta > 0.0) {
+    anorm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(anorm, anorm), __dmul_rn(alfa, alfa)),
+                                 __dmul_rn(beta, beta)));
+    alfa = __dsqrt_rn(st[LS_ALFA2]);
+  }
+  double cs, sn, rho;
+  ls_sym_ortho(st[LS_RHOBAR], beta, &cs, &sn, &rho);
+  const double theta = __dmul_rn(sn, alfa);
+  const double rhobar = __dmul_rn(-cs, alfa);
+  const double phibar0 = st[LS_PHIBAR];
+  const double phi = __dmul_rn(cs, phibar0);
+  const double phibar = __dmul_rn(sn, phibar0);
+  st[LS_C1] = __ddiv_rn(phi, rho);
+  st[LS_C2] = __ddiv_rn(-theta, rho);
+  st[LS_RNORM] = phibar;
+  st[LS_ARNORM] = __dmul_rn(alfa, fabs(__dmul_rn(sn, phi)));
+  st[LS_ALFA] = alfa;
+  st[LS_BETA] = beta;
+  st[LS_RHOBAR] = rhobar;
+  st[LS_PHIBAR] = phibar;
+  st[LS_ANORM] = anorm;
+  st[LS_BPREV] = beta > 0.0 ? beta : 1.0;
+}
+
+// One device-driven LSQR step after the fused pass (n <= 256 dense): the
+// transposed solve (beta from the pass), the solve for y (alfa from it), the
+// scalar recurrence and the x/w update, with no host scalar on the way;
+// state (LS_STATE doubles, device) carries the recurrence.  v_prev holds v
+// on entry and v_n on exit (v_raw is scratch).
+extern "C" int skl_lsqr_step_dev(const double* R, int64_t ldr, int64_t n, const double* Rinv,
+                                 const double* z, double* v, double* v_raw, double* y, double* w,
+                                 double* x, double* state, void* stream) {
+  clear_error();
+  SKL_REQUIRE(z && v && v_raw && y && w && x && state && n >= 1, SKL_ERR_INVALID,
+              "lsqr_step_dev: bad arguments");
+  int rc = trsv_t_launch(R, ldr, n, z, 0.0, v, v_raw, state + LS_ALFA2, Rinv, stream, state);
+  if (rc) return rc;
+  rc = trsv_n_launch(R, ldr, n, 0.0, v_raw, y, Rinv, stream, state, v);
+  if (rc) return rc;
+  lsqr_recur_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(state);
+  SKL_CUDA_LAUNCH();
+  lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, 0.0, 0.0, v, w, x,
+                                                        state + LS_XNORM2, state);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+extern "C" int64_t skl_lsqr_state_size(void) { return LS_STATE; }
 
 extern "C" int skl_lsqr_spmv(const int64_t* indptr, const int64_t* indices, const double* values,
                              int64_t m, const double* y, double s, double alpha,

@@ -65,3 +65,19 @@ for _ in range(20):
 out["sketch_enqueue_us"] = (time.perf_counter() - t0) / 20 * 1e6
 torch.cuda.synchronize()
 print({k: round(v, 4) for k, v in out.items()})
+
+# cold solves: the operator (device draws + device plan) rebuilt every solve,
+# as the reference rebuilds it (solvers.py:279 -> sketch.py:84)
+def cold_solve():
+    E.clear_operator_cache()
+    E.solve(prob, "saa", spec, opts)
+
+
+def cold_build():
+    E.clear_operator_cache()
+    o = E.build_sketch(E.solvers._operator_spec(spec, "saa", c.m, c.n, opts.d_factor), c.m)
+    o.device_plan()
+
+
+print({"cold_solve_wall_ms": round(wall(cold_solve), 4),
+       "cold_build_wall_ms": round(wall(cold_build), 4)})
