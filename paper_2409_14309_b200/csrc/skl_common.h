@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/sketchls_b200.h"
@@ -13,6 +14,20 @@ namespace skl {
 
 void set_error(const char* fmt, ...);
 void clear_error();
+
+// Tuning / A-B knobs from the environment: a flag is set only by a non-empty
+// value other than "0"; an integer knob falls back to `dflt` when unset,
+// empty or not positive.
+inline bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && !(v[0] == '0' && v[1] == 0);
+}
+inline long long env_int(const char* name, long long dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  const long long x = atoll(v);
+  return x > 0 ? x : dflt;
+}
 
 // Number of host worker threads for `threads` <= 0 requests.
 int resolve_threads(int threads);

@@ -563,7 +563,7 @@ static int countsketch_owned_launch(const double* A, int64_t m, int64_t n, int64
   // a short column stream gains nothing from a deep ring; two stages let
   // several column CTAs share an SM so the grid fits one wave
   if (nch <= 5) stages = std::min(stages, 2);
-  if (const char* env = getenv("SKL_OWNED_STAGES")) stages = std::max(2, std::min(stages, atoi(env)));
+  if (env_int("SKL_OWNED_STAGES", 0) > 0) stages = std::max(2, std::min(stages, (int)env_int("SKL_OWNED_STAGES", 0)));
   const size_t smem = 128 + stages * stage;
   int P = partitions;
   if (P <= 0) {
@@ -697,7 +697,7 @@ static int countsketch_host_stream(const double* A_host, int64_t m, int64_t n, i
               SKL_ERR_INVALID, "countsketch_host: bad A_dev_keep / ld_keep");
   // blocks of whole plan chunks, ~128 MiB of A each (chunk is even, so every
   // block start keeps the slot pointer A_slot - r0 16-byte aligned)
-  static const int64_t block_mb = getenv("SKL_HOST_BLOCK_MB") ? atoll(getenv("SKL_HOST_BLOCK_MB")) : 128;
+  static const int64_t block_mb = env_int("SKL_HOST_BLOCK_MB", 128);
   const int64_t rows_per_block =
       std::min<int64_t>((m + chunk - 1) / chunk * chunk,
                         std::max<int64_t>(chunk, ((block_mb << 20) / (8 * n)) / chunk * chunk));

@@ -516,7 +516,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   // the blocked factorisation (register cluster panels + GEMM-shaped
   // trailing updates) wins from a few panels on; very narrow systems use the
   // unblocked kernel (SKL_QR_BLOCKED_MIN_N overrides the cut-over)
-  static const int64_t min_n = getenv("SKL_QR_BLOCKED_MIN_N") ? atoll(getenv("SKL_QR_BLOCKED_MIN_N")) : 64;
+  static const int64_t min_n = env_int("SKL_QR_BLOCKED_MIN_N", 64);
   const bool blocked = n >= min_n && qr_blocked_supported(d);
   const int64_t ldm = blocked ? (d + 1) / 2 * 2 : d;
   const int64_t npan = (n + 31) / 32;
@@ -570,7 +570,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
                              (double*)(ws + oW2b), (double*)(ws + oPb), st);
       if (rc) break;
       qr_finish_kernel<<<1, 256, 0, st>>>(M, ldm, n, beta, fro2, R, ldr, y, badc, badv);
-      static const bool subst = getenv("SKL_QR_SUBST_BACKSOLVE") != nullptr;  // A/B knob
+      static const bool subst = env_flag("SKL_QR_SUBST_BACKSOLVE");  // A/B knob
       if (!subst) {
         double* Rinv = (double*)(ws + oRinv);
         const int64_t nb = (n + 31) / 32;

@@ -744,9 +744,9 @@ static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb
     return SKL_OK;
   });
   if (arc) return arc;
-  static const bool smem_panel = getenv("SKL_QR_SMEM_PANEL") != nullptr;
+  static const bool smem_panel = env_flag("SKL_QR_SMEM_PANEL");
   // register panel: tail rows over up to 16 CTAs, <= 32 rows per warp
-  static const int tail_rows = getenv("SKL_QR_PANEL_ROWS") ? atoi(getenv("SKL_QR_PANEL_ROWS")) : 128;
+  static const int tail_rows = (int)env_int("SKL_QR_PANEL_ROWS", 128);
   const int64_t tail = d - j0 - jb;
   int cl2 = (int)std::min<int64_t>(QB_MAXCL, std::max<int64_t>(1, (tail + tail_rows - 1) / tail_rows));
   const int rows2 = (int)((tail + cl2 - 1) / cl2);
