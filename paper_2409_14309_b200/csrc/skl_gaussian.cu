@@ -200,32 +200,86 @@ __global__ void zig_count_kernel(uint64_t key, uint64_t base, int64_t nseg, cons
   count[k] = cnt;
 }
 
-// Single-block exclusive scan of the counts (nseg is O(1e5)).
-__global__ void zig_scan_kernel(const int64_t* count, int64_t nseg, int64_t* offset,
-                                int64_t* total) {
-  __shared__ int64_t part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (nseg + 1023) / 1024;
-  const int64_t lo = t * per, hi = min(nseg, lo + per);
-  int64_t s = 0;
-  for (int64_t k = lo; k < hi; ++k) s += count[k];
-  part[t] = s;
+// Exclusive scan of the per-segment counts in two passes: (1) every CTA
+// scans its tile of SC_TILE counts (8 consecutive per thread, warp shuffles,
+// then the warps' totals) into local prefixes and writes the tile total;
+// (2) every CTA adds the sum of the tiles before it (at most a few hundred
+// totals) and the last CTA writes the grand total.  (A single-CTA walk over
+// the ~5e5 segments of config 3's operator took 1.15 ms.)
+constexpr int SC_NT = 1024;
+constexpr int SC_PER = 8;
+constexpr int SC_TILE = SC_NT * SC_PER;
+
+__global__ void __launch_bounds__(SC_NT) zig_scan_tiles_kernel(const int64_t* __restrict__ count,
+                                                               int64_t nseg,
+                                                               int64_t* __restrict__ offset,
+                                                               int64_t* __restrict__ tile_sum) {
+  __shared__ int64_t wsum[SC_NT / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)t * SC_PER;
+  int64_t v[SC_PER];
+  int64_t mine = 0;
+#pragma unroll
+  for (int q = 0; q < SC_PER; ++q) {
+    v[q] = base + q < nseg ? count[base + q] : 0;
+    mine += v[q];
+  }
+  int64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  if (t == 0) {
-    int64_t run = 0;
-    for (int i = 0; i < 1024; ++i) {
-      const int64_t v = part[i];
-      part[i] = run;
-      run += v;
+  if (w == 0) {
+    int64_t x = wsum[lane];
+    int64_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
     }
-    *total = run;
+    wsum[lane] = xi - x;  // exclusive prefix of the warps
+    if (lane == 31) tile_sum[blockIdx.x] = xi;
   }
   __syncthreads();
-  int64_t run = part[t];
-  for (int64_t k = lo; k < hi; ++k) {
-    offset[k] = run;
-    run += count[k];
+  int64_t run = wsum[w] + incl - mine;
+#pragma unroll
+  for (int q = 0; q < SC_PER; ++q) {
+    if (base + q < nseg) offset[base + q] = run;
+    run += v[q];
   }
+}
+
+__global__ void __launch_bounds__(SC_NT) zig_scan_add_kernel(int64_t* __restrict__ offset,
+                                                             int64_t nseg,
+                                                             const int64_t* __restrict__ tile_sum,
+                                                             int ntiles, int64_t* total) {
+  __shared__ int64_t pre;
+  if (threadIdx.x < 32) {
+    int64_t s = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) s += tile_sum[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      pre = s;
+      if ((int)blockIdx.x == ntiles - 1) *total = s + tile_sum[blockIdx.x];
+    }
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * SC_TILE;
+  for (int i = threadIdx.x; i < SC_TILE; i += SC_NT)
+    if (base + i < nseg) offset[base + i] += pre;
+}
+
+// offset = exclusive scan of count[0 .. nseg), *total = the sum; tile_sum
+// holds ceil(nseg / SC_TILE) scratch entries.
+static void zig_scan(const int64_t* count, int64_t nseg, int64_t* offset, int64_t* total,
+                     int64_t* tile_sum, cudaStream_t st) {
+  const int ntiles = (int)((nseg + SC_TILE - 1) / SC_TILE);
+  zig_scan_tiles_kernel<<<ntiles, SC_NT, 0, st>>>(count, nseg, offset, tile_sum);
+  zig_scan_add_kernel<<<ntiles, SC_NT, 0, st>>>(offset, nseg, tile_sum, ntiles, total);
 }
 
 // C: write the normals of each segment (normal t at G[(t / m) * ldg + t % m],
@@ -342,7 +396,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
     SKL_CUDA(malloc_async(&exitpos, (size_t)nseg * 8, st));
     SKL_CUDA(malloc_async(&count, (size_t)nseg * 8, st));
     SKL_CUDA(malloc_async(&offset, (size_t)nseg * 8, st));
-    SKL_CUDA(malloc_async(&total, 8, st));
+    SKL_CUDA(malloc_async(&total, 8 * (1 + (nseg + SC_TILE - 1) / SC_TILE), st));
     SKL_CUDA(malloc_async(&flags, 8, st));
     SKL_CUDA(malloc_async(&tail_t, (size_t)tail_cap * 8, st));
     SKL_CUDA(malloc_async(&tail_pos, (size_t)tail_cap * 8, st));
@@ -352,7 +406,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
     const int blocks = (int)((nseg + tb - 1) / tb);
     zig_spec_kernel<<<blocks, tb, 0, st>>>(key, start, nseg, mask, exitpos);
     zig_count_kernel<<<blocks, tb, 0, st>>>(key, start, nseg, mask, exitpos, count, flags);
-    zig_scan_kernel<<<1, 1024, 0, st>>>(count, nseg, offset, total);
+    zig_scan(count, nseg, offset, total, total + 1, st);
     int64_t h_total = 0;
     int h_flags[2] = {0, 0};
     SKL_CUDA(cudaMemcpyAsync(&h_total, total, 8, cudaMemcpyDeviceToHost, st));
@@ -482,7 +536,8 @@ extern "C" int skl_gaussian_band_begin(uint64_t key, int64_t seg0, int64_t seg1,
   if ((e = malloc_async(&b->exitpos, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
   if ((e = malloc_async(&b->count, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
   if ((e = malloc_async(&b->offset, (size_t)nseg * 8, st)) != cudaSuccess) return fail("alloc", e);
-  if ((e = malloc_async(&b->total, 8, st)) != cudaSuccess) return fail("alloc", e);
+  if ((e = malloc_async(&b->total, 8 * (1 + (nseg + SC_TILE - 1) / SC_TILE), st)) != cudaSuccess)
+    return fail("alloc", e);
   if ((e = malloc_async(&b->flags, 8, st)) != cudaSuccess) return fail("alloc", e);
   cudaMemsetAsync(b->flags, 0, 8, st);
   const int tb = 128;
@@ -491,7 +546,7 @@ extern "C" int skl_gaussian_band_begin(uint64_t key, int64_t seg0, int64_t seg1,
   zig_count_kernel<<<blocks, tb, 0, st>>>(key, b->base, nseg, b->mask, b->exitpos, b->count,
                                           b->flags);
   if (pre) cudaMemsetAsync(b->count, 0, 8, st);  // the entry segment is the previous band's
-  zig_scan_kernel<<<1, 1024, 0, st>>>(b->count, nseg, b->offset, b->total);
+  zig_scan(b->count, nseg, b->offset, b->total, b->total + 1, st);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail("launch", e);
   *handle = b;
   (void)count;
