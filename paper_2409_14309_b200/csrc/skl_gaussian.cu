@@ -23,8 +23,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "skl_common.h"
@@ -99,7 +101,8 @@ __host__ __device__ __forceinline__ double next_double_of(uint64_t w) {
 // One standard normal starting at word `pos` (numpy random_standard_normal).
 // Returns the position after it; *tail is set when the strip-0 tail (log1p)
 // produced the value.
-__host__ __device__ __forceinline__ uint64_t zig_parse(WordStream& ws, uint64_t pos, double* val,
+template <class Stream>
+__host__ __device__ __forceinline__ uint64_t zig_parse(Stream& ws, uint64_t pos, double* val,
                                                        bool* tail) {
   *tail = false;
   for (;;) {
@@ -134,29 +137,71 @@ __host__ __device__ __forceinline__ uint64_t zig_parse(WordStream& ws, uint64_t 
   }
 }
 
+// Per-thread window of the word stream in shared memory, refilled 16 words
+// (four Philox blocks) at a time by all threads of the warp together.  A
+// segment parse that pulled each word through WordStream computed a Philox
+// block whenever ANY lane of the warp crossed a 4-word boundary (the lanes'
+// positions drift apart as normals take 1 or more words), i.e. nearly every
+// normal; here the parse runs in rounds: a converged refill, then every lane
+// parses while 4 words are left in its window.  Words outside the window
+// (a strip-0 tail running past it, rare) are computed directly.
+constexpr int ZR_SLOTS = 32;   // window words per thread
+constexpr int ZR_FILL = 16;    // words added per round
+constexpr int ZR_NT = 128;     // threads per CTA of the parse kernels
+
+struct RingStream {
+  uint64_t key, hi;  // window: words [hi - ZR_SLOTS, hi) that were written
+  uint64_t* ring;    // [ZR_SLOTS][ZR_NT]: word w of this thread at ring[(w % 32) * ZR_NT + tid]
+  int tid;
+  __device__ RingStream(uint64_t k, uint64_t start, uint64_t* r)
+      : key(k), hi(start & ~3ULL), ring(r), tid(threadIdx.x) {}
+  __device__ __forceinline__ void refill() {
+#pragma unroll
+    for (int b = 0; b < ZR_FILL / 4; ++b) {
+      uint64_t w[4];
+      philox_block(key, (hi >> 2) + b, w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ring[((hi + 4 * b + q) & (ZR_SLOTS - 1)) * ZR_NT + tid] = w[q];
+    }
+    hi += ZR_FILL;
+  }
+  __device__ __forceinline__ uint64_t at(uint64_t pos) {
+    if (pos < hi && pos + ZR_SLOTS >= hi)
+      return ring[(pos & (ZR_SLOTS - 1)) * ZR_NT + tid];
+    uint64_t w[4];
+    philox_block(key, pos >> 2, w);
+    return w[pos & 3];
+  }
+};
+
 // A: speculative parse of each segment.
-__global__ void zig_spec_kernel(uint64_t key, uint64_t base, int64_t nseg, uint32_t* mask,
-                                uint64_t* exitpos) {
+__global__ void __launch_bounds__(ZR_NT) zig_spec_kernel(uint64_t key, uint64_t base,
+                                                         int64_t nseg, uint32_t* mask,
+                                                         uint64_t* exitpos) {
+  __shared__ uint64_t ring[ZR_SLOTS * ZR_NT];
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
-  WordStream ws(key);
   const uint64_t s0 = base + (uint64_t)k * ZIG_S;
+  RingStream ws(key, s0, ring);
   uint64_t pos = s0;
   uint32_t* mk = mask + k * ZIG_MASKW;
   int cur = 0;
   uint32_t bits = 0;
   while (pos < s0 + ZIG_S) {
-    const int off = (int)(pos - s0);
-    const int w = off >> 5;
-    while (cur < w) {
-      mk[cur++] = bits;
-      bits = 0;
+    ws.refill();
+    while (pos < s0 + ZIG_S && pos + 4 <= ws.hi) {
+      const int off = (int)(pos - s0);
+      const int w = off >> 5;
+      while (cur < w) {
+        mk[cur++] = bits;
+        bits = 0;
+      }
+      bits |= 1u << (off & 31);
+      double v;
+      bool t;
+      pos = zig_parse(ws, pos, &v, &t);
     }
-    bits |= 1u << (off & 31);
-    double v;
-    bool t;
-    pos = zig_parse(ws, pos, &v, &t);
   }
   while (cur < ZIG_MASKW) {
     mk[cur++] = bits;
@@ -287,12 +332,13 @@ static void zig_scan(const int64_t* count, int64_t nseg, int64_t* offset, int64_
 // last normal.
 // (t_base, row0: the band variant -- normal t of the band is global normal
 // t_base + t and lands at row (t_base + t) / m - row0 of G.)
-__global__ void zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
+__global__ void __launch_bounds__(ZR_NT) zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
                                  const uint64_t* exitpos, const int64_t* count,
                                  const int64_t* offset, int64_t N, int64_t m, double* G,
                                  int64_t ldg, double div, int64_t* tail_t, uint64_t* tail_pos,
                                  int* tail_n, int tail_cap, uint64_t* end_word,
                                  int64_t t_base = 0, int64_t row0 = 0) {
+  __shared__ uint64_t ring[1];
   zig_load_tables();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nseg) return;
@@ -300,27 +346,36 @@ __global__ void zig_write_kernel(uint64_t key, uint64_t base, int64_t nseg,
   const int64_t cnt = count[k];
   if (t >= N || cnt == 0) return;
   uint64_t pos = k == 0 ? base : exitpos[k - 1];
-  WordStream ws(key);
+  const int64_t nq = min(cnt, N - t);  // normals this segment writes
   int64_t i = t / m - row0, j = t % m;
-  for (int64_t q = 0; q < cnt && t < N; ++q, ++t) {
-    double v;
-    bool tail;
-    const uint64_t start = pos;
-    pos = zig_parse(ws, pos, &v, &tail);
-    G[i * ldg + j] = v / div;
-    if (t == N - 1) *end_word = pos;
-    if (tail) {
-      const int slot = atomicAdd(tail_n, 1);
-      if (slot < tail_cap) {
-        tail_t[slot] = t;
-        tail_pos[slot] = start;
+  // (the shared-memory window of zig_spec_kernel measured 2.2x slower here:
+  // 11.9 G instructions, the refill executed ~11x more often than the
+  // parse needs -- not understood; the per-word Philox path is kept)
+  WordStream ws(key);
+  (void)ring;
+  int64_t q = 0;
+  {
+    while (q < nq) {
+      double v;
+      bool tail;
+      const uint64_t start = pos;
+      pos = zig_parse(ws, pos, &v, &tail);
+      G[i * ldg + j] = v / div;
+      if (tail) {
+        const int slot = atomicAdd(tail_n, 1);
+        if (slot < tail_cap) {
+          tail_t[slot] = t + q;
+          tail_pos[slot] = start;
+        }
       }
-    }
-    if (++j == m) {
-      j = 0;
-      ++i;
+      if (++j == m) {
+        j = 0;
+        ++i;
+      }
+      ++q;
     }
   }
+  if (t + nq == N) *end_word = pos;
 }
 
 __global__ void zig_patch_kernel(const int64_t* tail_t, const double* vals, int n, int64_t m,
@@ -372,11 +427,43 @@ extern "C" int skl_rng_gaussian_host(uint64_t key, int64_t count, double* out) {
   return SKL_OK;
 }
 
+// Recompute strip-0 tail values on the host (the host libm's log1p, as
+// numpy's): out[q] = the normal starting at word pos[q], divided by div.
+// The ~2.6e-4 of draws that take the tail are independent: spread over the
+// host cores (one thread took 9 ms for config 3's ~1.4e5 tails).
+static void recompute_tails_host(uint64_t key, const uint64_t* pos, double* out, int ntail,
+                                 double div) {
+  auto work = [&](int lo, int hi) {
+    for (int q = lo; q < hi; ++q) {
+      WordStream ws(key);
+      bool tl;
+      double v;
+      zig_parse(ws, pos[q], &v, &tl);
+      out[q] = v / div;
+    }
+  };
+  const int nth = std::max(1, std::min(resolve_threads(0), ntail / 2048));
+  if (nth == 1) {
+    work(0, ntail);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back(work, (int)((int64_t)ntail * t / nth), (int)((int64_t)ntail * (t + 1) / nth));
+  for (auto& x : th) x.join();
+}
+
 // Normals [first normal at word `start`] of Generator(Philox(key)) laid out
 // as `rows` x `cols` C-order (normal t at out[(t / cols) * ld + t % cols]),
 // divided by `div`; *end_word receives the stream word after the last one.
 static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t cols, double* G,
                           int64_t ldg, double div, uint64_t* end_word, cudaStream_t st) {
+  static const bool probe = env_flag("SKL_ZIG_PROBE");
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_since = [&]() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start)
+        .count();
+  };
   int rc = upload_tables(st);
   if (rc) return rc;
   const int64_t N = rows * cols;
@@ -412,6 +499,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
     SKL_CUDA(cudaMemcpyAsync(&h_total, total, 8, cudaMemcpyDeviceToHost, st));
     SKL_CUDA(cudaMemcpyAsync(h_flags, flags, 8, cudaMemcpyDeviceToHost, st));
     SKL_CUDA(cudaStreamSynchronize(st));
+    if (probe) fprintf(stderr, "zig: counts ready %.3f ms\n", ms_since());
     auto release = [&]() {
       cudaFreeAsync(mask, st); cudaFreeAsync(exitpos, st); cudaFreeAsync(count, st);
       cudaFreeAsync(offset, st); cudaFreeAsync(total, st); cudaFreeAsync(flags, st);
@@ -434,6 +522,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
     SKL_CUDA(cudaMemcpyAsync(&h_end, endw, 8, cudaMemcpyDeviceToHost, st));
     SKL_CUDA(cudaStreamSynchronize(st));
     const int ntail = h_flags[1];
+    if (probe) fprintf(stderr, "zig: written %.3f ms, %d tails\n", ms_since(), ntail);
     if (ntail > tail_cap) {
       release();
       SKL_FAIL(SKL_ERR_CUDA, "gaussian: tail record overflow (%d > %d)", ntail, tail_cap);
@@ -446,13 +535,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
       SKL_CUDA(cudaMemcpyAsync(ht.data(), tail_t, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st));
       SKL_CUDA(cudaMemcpyAsync(hp.data(), tail_pos, (size_t)ntail * 8, cudaMemcpyDeviceToHost, st));
       SKL_CUDA(cudaStreamSynchronize(st));
-      for (int q = 0; q < ntail; ++q) {
-        WordStream ws(key);
-        bool tl;
-        double v;
-        zig_parse(ws, hp[(size_t)q], &v, &tl);
-        hv[(size_t)q] = v / div;
-      }
+      recompute_tails_host(key, hp.data(), hv.data(), ntail, div);
       double* dv = nullptr;
       SKL_CUDA(malloc_async(&dv, (size_t)ntail * 8, st));
       SKL_CUDA(cudaMemcpyAsync(dv, hv.data(), (size_t)ntail * 8, cudaMemcpyHostToDevice, st));
@@ -463,6 +546,7 @@ static int normals_device(uint64_t key, uint64_t start, int64_t rows, int64_t co
     }
     release();
     if (end_word) *end_word = h_end;
+    if (probe) fprintf(stderr, "zig: done %.3f ms\n", ms_since());
     return SKL_OK;
   }
   SKL_FAIL(SKL_ERR_CUDA, "gaussian: stream segmentation did not converge");
@@ -623,13 +707,7 @@ extern "C" int skl_gaussian_band_write(void* handle, int64_t first, int64_t N, i
         rc = SKL_ERR_CUDA;
         break;
       }
-      for (int q = 0; q < ntail; ++q) {
-        WordStream ws(b->key);
-        bool tl;
-        double v;
-        zig_parse(ws, hp[(size_t)q], &v, &tl);
-        hv[(size_t)q] = v / div;
-      }
+      recompute_tails_host(b->key, hp.data(), hv.data(), ntail, div);
       double* dv = nullptr;
       if ((e = malloc_async(&dv, (size_t)ntail * 8, st)) != cudaSuccess) {
         set_error("gaussian_band_write: alloc: %s", cudaGetErrorString(e));
