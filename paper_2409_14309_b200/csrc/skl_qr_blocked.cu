@@ -308,6 +308,33 @@ __device__ __forceinline__ void panel_t_build(double* Ts, const double* G, int j
   __syncwarp();
 }
 
+// dlarfg's scalars for a column with sum of squares below the pivot Sk > 0
+// and pivot alpha: beta = -sign(alpha) N with N = sqrt(alpha^2 + Sk),
+// tau = (beta - alpha) / beta = 1 + |alpha| / N and scale = 1 / (alpha -
+// beta) = sign(alpha) / (|alpha| + N).  They sit on the panel's per-column
+// critical path: N comes from the IEEE square root (~80 cycles on the B200;
+// rsqrt.approx.f64 alone takes ~75), the two reciprocals from
+// rcp.approx.ftz.f64 (~18 cycles) refined by two independent Newton steps
+// each, side by side, instead of two IEEE divisions in sequence (~60 cycles
+// each plus their slow-path branches).  A few ulp, not correctly rounded; R
+// is compared with LAPACK within 1e-12.
+__device__ __forceinline__ double rcp_nr(double t) {
+  double q;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(q) : "d"(t));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) q = fma(q, fma(-t, q, 1.0), q);
+  return q;
+}
+__device__ __forceinline__ void house_scalars(double alpha, double Sk, double& beta, double& tau,
+                                              double& scale) {
+  const double N = sqrt(fma(alpha, alpha, Sk));
+  const double aa = fabs(alpha);
+  const double rN = rcp_nr(N), rs = rcp_nr(aa + N);
+  beta = alpha < 0.0 ? N : -N;
+  tau = fma(aa, rN, 1.0);
+  scale = alpha < 0.0 ? -rs : rs;
+}
+
 template <int RPW>
 __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams p) {
   constexpr bool KEEPX = RPW <= 16;
@@ -404,15 +431,27 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     // 256-byte store per destination, into the inboxes of CTAs
     // w, w + QR_PUSHW, ...
     if (warp < QR_PUSHW) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      double tot;
+      if (RPW == 32) {
+        double t[QR_NW2];
 #pragma unroll
-      for (int w = 0; w < QR_NW2; w += 4) {
-        t0 += red[w * 33 + lane];
-        t1 += red[(w + 1) * 33 + lane];
-        t2 += red[(w + 2) * 33 + lane];
-        t3 += red[(w + 3) * 33 + lane];
+        for (int w = 0; w < QR_NW2; ++w) t[w] = red[w * 33 + lane];
+#pragma unroll
+        for (int w = QR_NW2 / 2; w >= 1; w >>= 1)
+#pragma unroll
+          for (int q = 0; q < w; ++q) t[q] += t[q + w];
+        tot = t[0];
+      } else {
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+        for (int w = 0; w < QR_NW2; w += 4) {
+          t0 += red[w * 33 + lane];
+          t1 += red[(w + 1) * 33 + lane];
+          t2 += red[(w + 2) * 33 + lane];
+          t3 += red[(w + 3) * 33 + lane];
+        }
+        tot = (t0 + t1) + (t2 + t3);
       }
-      const double tot = (t0 + t1) + (t2 + t3);
       if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&mb[b], (ncta + 1) * 256);
       const uint32_t dst = smem_u32(inbox + (b * QB_MAXCL + rank) * 32 + lane);
       const uint32_t mbl = smem_u32(&mb[b]);
@@ -423,12 +462,25 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
       QR_PROBE(3);
       mbar_wait_cluster(&mb[b], (uint32_t)((k >> 1) & 1));
       QR_PROBE(4);
-      double u[4] = {0.0, 0.0, 0.0, 0.0};
+      double Sj;
       const double* ib = inbox + b * QB_MAXCL * 32 + lane;
+      if (RPW == 32) {
+        double u[QB_MAXCL];
 #pragma unroll
-      for (int q = 0; q < QB_MAXCL; ++q)  // all loads in flight at once
-        if (q < (int)ncta) u[q & 3] += ib[q * 32];
-      const double Sj = (u[0] + u[1]) + (u[2] + u[3]);
+        for (int q = 0; q < QB_MAXCL; ++q)  // all loads in flight at once
+          u[q] = q < (int)ncta ? ib[q * 32] : 0.0;
+#pragma unroll
+        for (int w = QB_MAXCL / 2; w >= 1; w >>= 1)  // fixed-order tree
+#pragma unroll
+          for (int q = 0; q < w; ++q) u[q] += u[q + w];
+        Sj = u[0];
+      } else {
+        double u[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < QB_MAXCL; ++q)  // all loads in flight at once
+          if (q < (int)ncta) u[q & 3] += ib[q * 32];
+        Sj = (u[0] + u[1]) + (u[2] + u[3]);
+      }
       const double pj = inrow[b * 32 + lane];
       const double Sk = __shfl_sync(0xffffffffu, Sj, k);
       const double alpha = __shfl_sync(0xffffffffu, pj, k);
@@ -438,9 +490,13 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
         beta = alpha;
         scale = 0.0;
       } else {
-        beta = -copysign(sqrt(fma(alpha, alpha, Sk)), alpha);
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+        if (RPW == 32) {
+          house_scalars(alpha, Sk, beta, tau, scale);
+        } else {  // measured faster here (timing, not accuracy)
+          beta = -copysign(sqrt(fma(alpha, alpha, Sk)), alpha);
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
       }
       if (lane == k) myscale = scale;
       // rows below the pivot: P_i[j] -= (w_j scale) x_i; the pivot row: -= w_j
@@ -842,10 +898,25 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
       cudaStreamWaitEvent(st, b, 0);
     }
   } join{qs, st, X[1], X[2]};
+#ifdef SKL_QR_TIMELINE
+  // instrumented build: timing events on both streams, printed per panel;
+  // SKL_QR_SKIP bit 1 drops the bulk updates, bit 2 the next-panel updates
+  // (wrong results: timing experiments only)
+  static const int skip = (int)env_int("SKL_QR_SKIP", 0);
+  std::vector<cudaEvent_t> tl(4 * npan + 1);
+  for (auto& e : tl) cudaEventCreate(&e);
+  cudaEventRecord(tl[4 * npan], qs->hi);
+#define QR_TL(i, s) cudaEventRecord(tl[i], s)
+#define QR_SKIP(b) (skip & (b))
+#else
+#define QR_TL(i, s) do {} while (0)
+#define QR_SKIP(b) 0
+#endif
   for (int64_t k = 0; k < npan; ++k) {
     const int64_t j0 = k * QB_NB;
     const int jb = (int)std::min<int64_t>(QB_NB, n - j0);
-    if (k > 0) {
+    QR_TL(4 * k, qs->hi);
+    if (k > 0 && !QR_SKIP(2)) {
       // panel k's columns: reflectors 0 .. k-2 came with bulk update k-2,
       // reflector k-1 is applied here
       if (k >= 2) SKL_CUDA(cudaStreamWaitEvent(qs->hi, F[k - 2], 0));
@@ -854,19 +925,48 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
                           part_cap, qs->hi);
       if (rc) return rc;
     }
+    QR_TL(4 * k + 1, qs->hi);
     rc = qr_launch_panel(M, ldm, d, j0, jb, V, Tall + k * 32 * 32, tau, beta, qs->hi);
     if (rc) return rc;
+    QR_TL(4 * k + 2, qs->hi);
     SKL_CUDA(cudaEventRecord(E[k], qs->hi));
     // bulk update: every column after panel k + 1 (and Sb)
     const int64_t c0 = j0 + jb;
     const int64_t jb_next = std::min<int64_t>(QB_NB, std::max<int64_t>(0, n - c0));
     const int64_t cs = c0 + jb_next;
     SKL_CUDA(cudaStreamWaitEvent(qs->lo, E[k], 0));
-    rc = qr_apply_panel(M, ldm, d, j0, jb, cs, (n + 1) - cs, V, Tall + k * 32 * 32, W2b, partb,
-                        part_cap, qs->lo);
-    if (rc) return rc;
+    if (!QR_SKIP(1)) {
+      rc = qr_apply_panel(M, ldm, d, j0, jb, cs, (n + 1) - cs, V, Tall + k * 32 * 32, W2b, partb,
+                          part_cap, qs->lo);
+      if (rc) return rc;
+    }
+    QR_TL(4 * k + 3, qs->lo);
     SKL_CUDA(cudaEventRecord(F[k], qs->lo));
   }
+#ifdef SKL_QR_TIMELINE
+  {
+    cudaStreamSynchronize(qs->hi);
+    cudaStreamSynchronize(qs->lo);
+    float t_small = 0, t_panel = 0, t_end = 0;
+    fprintf(stderr, "qr timeline d=%lld n=%lld skip=%d (us from start: small-update start, panel start, panel end, bulk end)\n",
+            (long long)d, (long long)n, skip);
+    for (int64_t k = 0; k < npan; ++k) {
+      float a, b, c, e;
+      cudaEventElapsedTime(&a, tl[4 * npan], tl[4 * k]);
+      cudaEventElapsedTime(&b, tl[4 * npan], tl[4 * k + 1]);
+      cudaEventElapsedTime(&c, tl[4 * npan], tl[4 * k + 2]);
+      cudaEventElapsedTime(&e, tl[4 * npan], tl[4 * k + 3]);
+      t_small += b - a;
+      t_panel += c - b;
+      t_end = std::max(t_end, std::max(c, e));
+      if (k < 4 || k + 2 >= npan)
+        fprintf(stderr, "  %3lld %8.1f %8.1f %8.1f %8.1f\n", (long long)k, a * 1e3, b * 1e3, c * 1e3, e * 1e3);
+    }
+    fprintf(stderr, "  sum small-update+wait %.1f us, sum panels %.1f us, end %.1f us\n", t_small * 1e3,
+            t_panel * 1e3, t_end * 1e3);
+    for (auto& e : tl) cudaEventDestroy(e);
+  }
+#endif
 #ifdef SKL_QR_PROBE
   {
     unsigned long long h[12] = {}, z[12] = {};

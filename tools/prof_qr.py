@@ -1,6 +1,12 @@
 """Profiling driver for the reduced solve: QR + back-solve of a d x n
-sketched system (default: config 4's 8192 x 1024, and config 2's 2048 x 256)."""
+sketched system (default: config 4's 8192 x 1024, and config 2's 2048 x 256).
+
+The GPU is kept busy for ~0.5 s before timing (clocks ramp up under load),
+then `reps` solves are timed one by one with CUDA events; the median and the
+SM clock read through NVML right after are printed."""
+import statistics
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -14,12 +20,26 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 M = torch.randn((n, d), dtype=torch.float64, device="cuda").t()
 y = torch.randn((d,), dtype=torch.float64, device="cuda")
-for _ in range(reps):
+t0 = time.perf_counter()
+while time.perf_counter() - t0 < 0.5:
     qr_solve_device(M, d, y, d, n)
-torch.cuda.synchronize()
-s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
-qr_solve_device(M, d, y, d, n)
-e.record()
-torch.cuda.synchronize()
-print(f"qr_solve {d}x{n}: {s.elapsed_time(e):.3f} ms")
+    torch.cuda.synchronize()
+ts = []
+for _ in range(reps):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    qr_solve_device(M, d, y, d, n)
+    e.record()
+    torch.cuda.synchronize()
+    ts.append(s.elapsed_time(e))
+clk = ""
+try:
+    import pynvml
+
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    clk = f" sm_clock {pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)} MHz"
+except Exception:  # noqa: BLE001 -- the clock is informational
+    pass
+print(f"qr_solve {d}x{n}: {statistics.median(ts):.3f} ms (median of {reps}, min "
+      f"{min(ts):.3f}){clk}")
