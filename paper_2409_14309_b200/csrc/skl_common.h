@@ -169,5 +169,30 @@ inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
   if (!pool) return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
   return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
 }
+// Launch with programmatic stream serialization (see pdl_enter in
+// skl_ptx.cuh) when `pdl`: only for a kernel whose sole dependency is the
+// kernel launched just before it in the same stream (never right after a
+// cudaStreamWaitEvent), and that calls pdl_enter() before touching global
+// memory.  SKL_NO_PDL=1 turns it off (A/B knob).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, bool pdl, Args... args) {
+  static const bool off = env_flag("SKL_NO_PDL");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && !off) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+inline bool pdl_enabled() {
+  static const bool off = env_flag("SKL_NO_PDL");
+  return !off;
+}
 }  // namespace skl
 #endif

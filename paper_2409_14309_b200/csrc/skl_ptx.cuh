@@ -103,4 +103,17 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor in the stream still runs; griddepcontrol.wait returns once the
+// predecessor has completed and its memory is visible (a no-op for a normal
+// launch).  Every kernel below waits before touching global memory and
+// signals its own dependent right away, so the dependent's launch latency is
+// spent while this kernel runs (everything a kernel reads after its wait was
+// produced by grids that have completed: the predecessor waited on its own
+// predecessor before it could complete).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");
+}
+
 }  // namespace skl

@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "skl_common.h"
+#include "skl_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -136,6 +137,7 @@ __global__ void qr_scale_reflectors(double* M, int64_t d, int64_t n, const doubl
 __global__ void qr_finish_kernel(const double* M, int64_t d, int64_t n, const double* beta,
                                  const double* fro2, double* R, int64_t ldr, double* y,
                                  int64_t* bad_col, double* bad_val) {
+  pdl_enter();
   __shared__ int64_t first_bad;
   if (threadIdx.x == 0) first_bad = -1;
   __syncthreads();
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(1024) qr_backsolve_kernel(const double* M, int
 __global__ void __launch_bounds__(512) qr_backsolve_blocked_kernel(const double* M, int64_t ldm,
                                                                     int64_t n, const double* beta,
                                                                     const double* y_in, double* x) {
+  pdl_enter();
   extern __shared__ double ys[];
   __shared__ double xb[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -282,6 +285,7 @@ constexpr int TRI_WPB = 4;  // blocks (warps) per CTA
 __global__ void __launch_bounds__(TRI_WPB * 32) qr_trinv_kernel(const double* M, int64_t ldm,
                                                                  int64_t n, const double* beta,
                                                                  double* Rinv) {
+  pdl_enter();
   __shared__ double Rs[TRI_WPB][32][33];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t bi = (int64_t)blockIdx.x * TRI_WPB + wl;
@@ -452,6 +456,7 @@ __global__ void copy_aug_kernel(const double* SA, int64_t ldsa, const double* Sb
 }
 
 __global__ void sum_parts_kernel(const double* part, int nparts, double* out) {
+  pdl_enter();
   __shared__ double red[33];
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
@@ -555,11 +560,19 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   int rc = SKL_OK;
   do {
     copy_aug_kernel<<<fro_blocks, 256, 0, st>>>(SA, ldsa, Sb, d, n, M, ldm, part);
-    sum_parts_kernel<<<1, 256, 0, st>>>(part, fro_blocks, fro2);
+    // a launch error leaves the loop with rc set, so the workspace is freed
+#define QR_LAUNCH(call)                                                     \
+  if ((e = (call)) != cudaSuccess) {                                        \
+    set_error("qr_solve: kernel launch failed: %s", cudaGetErrorString(e)); \
+    rc = SKL_ERR_CUDA;                                                      \
+    break;                                                                  \
+  }
+    cudaError_t e = cudaSuccess;
+    QR_LAUNCH(launch_k(sum_parts_kernel, dim3(1), dim3(256), 0, st, true, (const double*)part,
+                       fro_blocks, fro2));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaSuccess;
     if (blocked) {
       double* V = (double*)(ws + oV);
       double* T = (double*)(ws + oT);
@@ -574,10 +587,12 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
       if (!subst) {
         double* Rinv = (double*)(ws + oRinv);
         const int64_t nb = (n + 31) / 32;
-        qr_trinv_kernel<<<(unsigned)((nb + TRI_WPB - 1) / TRI_WPB), TRI_WPB * 32, 0, st>>>(
-            M, ldm, n, beta, Rinv);
-        qr_backsolve_inv_kernel<<<1, BS_NT, n * sizeof(double), st>>>(M, ldm, n, beta, Rinv, y,
-                                                                      xd);
+        QR_LAUNCH(launch_k(qr_trinv_kernel, dim3((unsigned)((nb + TRI_WPB - 1) / TRI_WPB)),
+                           dim3(TRI_WPB * 32), 0, st, true, (const double*)M, ldm, n,
+                           (const double*)beta, Rinv));
+        QR_LAUNCH(launch_k(qr_backsolve_inv_kernel, dim3(1), dim3(BS_NT), n * sizeof(double), st,
+                           true, (const double*)M, ldm, n, (const double*)beta,
+                           (const double*)Rinv, (const double*)y, xd));
       } else {
         qr_backsolve_blocked_kernel<<<1, 512, n * sizeof(double), st>>>(M, ldm, n, beta, y, xd);
       }
@@ -627,6 +642,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
       rc = SKL_ERR_CUDA;
     }
   } while (0);
+#undef QR_LAUNCH
   cudaFreeAsync(ws, st);
   if (rc == SKL_OK && *bad_col >= 0) {
     set_error("input is numerically rank deficient at column %lld (|R[%lld,%lld]| = %.3e)",

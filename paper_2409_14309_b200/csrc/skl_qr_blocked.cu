@@ -90,6 +90,7 @@ struct PanelParams {
 };
 
 __global__ void __launch_bounds__(QB_NT) qr_panel_cluster_kernel(const PanelParams p) {
+  pdl_enter();
   extern __shared__ __align__(16) double qsm[];
   const uint32_t rank = cta_rank_in_cluster();
   const uint32_t ncta = gridDim.x;  // one cluster spans the grid
@@ -337,6 +338,7 @@ __device__ __forceinline__ void house_scalars(double alpha, double Sk, double& b
 
 template <int RPW>
 __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams p) {
+  pdl_enter();
   constexpr bool KEEPX = RPW <= 16;
   extern __shared__ __align__(16) double qsm[];
   const uint32_t rank = cta_rank_in_cluster();
@@ -594,6 +596,7 @@ __global__ void __launch_bounds__(256) qr_update_kernel(double* __restrict__ C, 
                                                         const double* __restrict__ W2, int jb,
                                                         int64_t rows, int64_t nc) {
   __shared__ double Vs[32][64 + 1];
+  pdl_enter();
   __shared__ double Ws[32][64 + 1];
   const int64_t i0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
   const int tid = threadIdx.x;
@@ -645,6 +648,7 @@ __global__ void __launch_bounds__(256) qr_vtc64_kernel(const double* __restrict_
                                                        int jb, int64_t rows, int64_t nc,
                                                        double* __restrict__ part) {
   __shared__ double Vs[QV_ROWS][33];
+  pdl_enter();
   __shared__ double Cs[QV_ROWS][33];
   const int64_t c0 = (int64_t)blockIdx.x * 32;
   const int s = blockIdx.y;
@@ -681,6 +685,7 @@ __global__ void __launch_bounds__(256) qr_reduce_tt_kernel(const double* __restr
                                                            int64_t nc, const double* __restrict__ T,
                                                            int jb, int transpose,
                                                            double* __restrict__ W2) {
+  pdl_enter();
   // 2 columns per CTA; 4 groups of 32 threads split each column's S partials
   __shared__ double Tsm[32][33];
   __shared__ double Wg[2][4][32];
@@ -731,12 +736,10 @@ static int qr_wt(const double* V, int64_t ldv, const double* C, int64_t ldc, int
                  int64_t part_cap, cudaStream_t st) {
   const int64_t S = (rows + QV_ROWS - 1) / QV_ROWS;
   SKL_REQUIRE(S * nc * 32 <= part_cap, SKL_ERR_INVALID, "qr: partial buffer too small");
-  qr_vtc64_kernel<<<dim3((unsigned)((nc + 31) / 32), (unsigned)S), 256, 0, st>>>(V, ldv, C, ldc,
-                                                                              jb, rows, nc, part);
-  SKL_CUDA_LAUNCH();
-  qr_reduce_tt_kernel<<<(unsigned)((nc + 1) / 2), 256, 0, st>>>(part, (int)S, nc, T, jb, transpose,
-                                                                W2);
-  SKL_CUDA_LAUNCH();
+  SKL_CUDA(launch_k(qr_vtc64_kernel, dim3((unsigned)((nc + 31) / 32), (unsigned)S), dim3(256), 0,
+                    st, false, V, ldv, C, ldc, jb, rows, nc, part));
+  SKL_CUDA(launch_k(qr_reduce_tt_kernel, dim3((unsigned)((nc + 1) / 2)), dim3(256), 0, st, true,
+                    (const double*)part, (int)S, nc, T, jb, transpose, W2));
   return SKL_OK;
 }
 
@@ -785,7 +788,7 @@ static int qr_streams(QrStreams** out, size_t nev) {
 }
 
 static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb, double* V,
-                           double* Tblk, double* tau, double* beta, cudaStream_t st) {
+                           double* Tblk, double* tau, double* beta, bool pdl, cudaStream_t st) {
   static std::once_flag attr_set[64];
   const int smem_max = (int)(QB_SMEM_EXTRA + QB_MAXROWS * QB_PLD) * (int)sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
@@ -809,12 +812,14 @@ static int qr_launch_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb
   const int rpw = (rows2 + QR_NW2 - 1) / QR_NW2;
   cudaLaunchConfig_t cfg = {};
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
   if (!smem_panel && rpw <= 32) {
     PanelParams pp{M, ldm, d, j0, jb, rows2, V, Tblk, tau, beta};
     cfg.gridDim = dim3(cl2);
@@ -852,9 +857,8 @@ static int qr_apply_panel(double* M, int64_t ldm, int64_t d, int64_t j0, int jb,
                  part_cap, st);
   if (rc) return rc;
   dim3 g((unsigned)((rows + 63) / 64), (unsigned)((nc + 63) / 64));
-  qr_update_kernel<<<g, 256, 0, st>>>(M + c0 * ldm + j0, ldm, V + j0 * ldm + j0, ldm, W2, jb, rows,
-                                      nc);
-  SKL_CUDA_LAUNCH();
+  SKL_CUDA(launch_k(qr_update_kernel, g, dim3(256), 0, st, true, M + c0 * ldm + j0, ldm,
+                    (const double*)(V + j0 * ldm + j0), ldm, (const double*)W2, jb, rows, nc));
   return SKL_OK;
 }
 
@@ -926,7 +930,9 @@ int qr_blocked_factor(double* M, int64_t ldm, int64_t d, int64_t n, double* tau,
       if (rc) return rc;
     }
     QR_TL(4 * k + 1, qs->hi);
-    rc = qr_launch_panel(M, ldm, d, j0, jb, V, Tall + k * 32 * 32, tau, beta, qs->hi);
+    // PDL only right after the next-panel update kernels on this stream
+    rc = qr_launch_panel(M, ldm, d, j0, jb, V, Tall + k * 32 * 32, tau, beta,
+                         k > 0 && !QR_SKIP(2), qs->hi);
     if (rc) return rc;
     QR_TL(4 * k + 2, qs->hi);
     SKL_CUDA(cudaEventRecord(E[k], qs->hi));
