@@ -213,6 +213,26 @@ def rng_gaussian_host(key: int, count: int) -> np.ndarray:
     return out
 
 
+def _ensure_built() -> None:
+    """Build the library when it is missing or older than any of its sources
+    (a stale build would silently run old kernels).  A file lock keeps
+    concurrent processes (torchrun ranks) from building at the same time."""
+    import fcntl
+
+    from . import _build
+
+    if LIB_PATH.exists() and not _build._stale():
+        return
+    LIB_PATH.parent.mkdir(exist_ok=True)
+    with open(LIB_PATH.parent / ".build.lock", "w") as fh:
+        fcntl.flock(fh, fcntl.LOCK_EX)
+        try:
+            if not LIB_PATH.exists() or _build._stale():
+                _build.build()
+        finally:
+            fcntl.flock(fh, fcntl.LOCK_UN)
+
+
 def lib() -> ctypes.CDLL:
     """The loaded library (built on first use if absent)."""
     global _lib
@@ -220,10 +240,7 @@ def lib() -> ctypes.CDLL:
         return _lib
     with _lock:
         if _lib is None:
-            if not LIB_PATH.exists():
-                from . import _build
-
-                _build.build()
+            _ensure_built()
             if not LIB_PATH.exists():
                 raise DeviceError(f"native library missing: {LIB_PATH}")
             handle = ctypes.CDLL(str(LIB_PATH))

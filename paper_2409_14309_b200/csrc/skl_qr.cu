@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(BS_NT) qr_backsolve_inv_kernel(const double* M
                                                                  int64_t n, const double* beta,
                                                                  const double* Rinv,
                                                                  const double* y_in, double* x) {
+  pdl_enter();
   extern __shared__ double ys[];
   __shared__ double rv[2][32][33];
   __shared__ double xb[32];
