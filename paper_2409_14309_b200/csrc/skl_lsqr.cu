@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "skl_common.h"
+#include "skl_ptx.cuh"
 
 namespace skl {
 
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
     double* __restrict__ r_out, double* __restrict__ zpart, double* __restrict__ npart,
     double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter,
     const double* __restrict__ dscal) {
+  pdl_enter();  // lets the step kernel after it launch early (launch_k)
   if (dscal) {  // device-driven iteration: alfa and beta_prev from the recurrence state
     alpha = dscal[LS_ALFA];
     beta_prev = dscal[LS_BPREV];
@@ -326,6 +328,153 @@ __global__ void __launch_bounds__(LQ_NT) lsqr_fused_kernel(
   __shared__ double nb;
   // fixed-order folds; loads are batched (L2, bypassing L1) so that their
   // latency is paid once per batch, not once per partial
+  constexpr int FB = 16;
+  if (tid == 0) {
+    double sn = 0.0;
+    for (unsigned b0 = 0; b0 < gridDim.x; b0 += FB) {
+      double t[FB];
+#pragma unroll
+      for (int q = 0; q < FB; ++q) t[q] = b0 + q < gridDim.x ? __ldcg(npart + b0 + q) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        if (b0 + q < gridDim.x) sn += t[q];
+    }
+    *norm2 = sn;
+    nb = sqrt(sn);
+    *counter = 0u;
+  }
+  __syncthreads();
+  const double beta = nb;
+  for (int c = tid; c < n; c += LQ_NT) {
+    double sz = 0.0;
+    for (unsigned b0 = 0; b0 < gridDim.x; b0 += FB) {
+      double t[FB];
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        t[q] = b0 + q < gridDim.x ? __ldcg(zpart + (int64_t)(b0 + q) * n + c) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FB; ++q)
+        if (b0 + q < gridDim.x) sz += t[q];
+    }
+    z[c] = beta > 0.0 ? sz / beta : 0.0;
+  }
+}
+
+// The same pass with the blocks of A streamed into shared memory by
+// cp.async, two 32-row blocks in flight: the register version above keeps a
+// 64-row block in registers (236 registers, one CTA per SM), so no load is
+// in flight while a block is folded, and the pass ran at ~66 % of HBM.  Here
+// block b+1 streams in while block b is folded from shared memory (lane l =
+// row l, warp g = columns g, g+8, ...; the values stay in registers between
+// the two products, as above).  Same operations in the same order per row
+// and column as the register kernel with one row per lane.
+constexpr int LF2_RB = 32;  // rows per block
+__device__ __forceinline__ void lq_cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+template <int NC, int ST>
+__global__ void __launch_bounds__(LQ_NT) lsqr_fused_async_kernel(
+    const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ y,
+    double s, double alpha, const double* __restrict__ r_prev, double beta_prev,
+    double* __restrict__ r_out, double* __restrict__ zpart, double* __restrict__ npart,
+    double* __restrict__ z, double* __restrict__ norm2, unsigned int* counter,
+    const double* __restrict__ dscal) {
+  pdl_enter();
+  if (dscal) {
+    alpha = dscal[LS_ALFA];
+    beta_prev = dscal[LS_BPREV];
+  }
+  constexpr int NCOL = 8 * NC;              // columns held by the CTA (>= n)
+  constexpr int BUF = NCOL * LF2_RB;        // doubles per block buffer, [col][row]
+  constexpr int CH = BUF / 2;               // 16-byte chunks per block
+  extern __shared__ __align__(16) double abuf[];  // [ST][NCOL][LF2_RB] ring
+  __shared__ double ys[NCOL];
+  __shared__ double pdot[8][LF2_RB];
+  __shared__ double rs[LF2_RB];
+  __shared__ double red[32];
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+  for (int c = tid; c < NCOL; c += LQ_NT) ys[c] = c < n ? y[c] : 0.0;
+  const int64_t nblk = (m + LF2_RB - 1) / LF2_RB;
+  auto issue = [&](int64_t blk, int slot) {
+    if (blk < nblk) {
+      const int64_t r0 = blk * LF2_RB;
+      double* dst = abuf + slot * BUF;
+#pragma unroll 4
+      for (int ch = tid; ch < CH; ch += LQ_NT) {
+        const int c = ch / (LF2_RB / 2), r = (ch % (LF2_RB / 2)) * 2;
+        const int64_t i = r0 + r;
+        const int bytes = (c < n && i < m) ? (int)(min((int64_t)2, m - i) * 8) : 0;
+        lq_cp_async16(dst + c * LF2_RB + r, bytes ? A + c * lda + i : A, bytes);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double zacc[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) zacc[q] = 0.0;
+  double ss = 0.0;
+#pragma unroll
+  for (int k = 0; k < ST - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int slot = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    double rp = 0.0;
+    if (tid < LF2_RB && r_prev && blk * LF2_RB + tid < m) rp = __ldcs(r_prev + blk * LF2_RB + tid);
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
+    __syncthreads();  // block blk has landed for every thread; the previous slot is free
+    // ST - 1 blocks stay in flight while this one is folded
+    issue(blk + (int64_t)(ST - 1) * gridDim.x, slot == 0 ? ST - 1 : slot - 1);
+    const double* b = abuf + slot * BUF;
+    double v[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) v[q] = b[(g + 8 * q) * LF2_RB + lane];
+    double a = 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int c = g + 8 * q;
+      if (c < n) a = fma(v[q], ys[c], a);
+    }
+    pdot[g][lane] = a;
+    __syncthreads();
+    if (tid < LF2_RB) {
+      const int64_t i = blk * LF2_RB + tid;
+      double r = 0.0;
+      if (i < m) {
+        double dot = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) dot += pdot[w][tid];
+        r = s * dot - (r_prev ? alpha * (rp / beta_prev) : 0.0);
+        r_out[i] = r;
+        ss = fma(r, r, ss);
+      }
+      rs[tid] = r;
+    }
+    __syncthreads();  // rs ready
+    const double r0 = rs[lane];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) zacc[q] = fma(v[q], r0, zacc[q]);
+    slot = slot == ST - 1 ? 0 : slot + 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double t = zacc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    const int c = g + 8 * q;
+    if (lane == 0 && c < n) zpart[(int64_t)blockIdx.x * n + c] = t;
+  }
+  const double tn = lq_block_sum(ss, red);
+  if (tid == 0) npart[blockIdx.x] = tn;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double nb;
   constexpr int FB = 16;
   if (tid == 0) {
     double sn = 0.0;
@@ -474,18 +623,24 @@ __device__ void lq_solve_n(const double* __restrict__ R, int64_t ldr, int n, dou
                            const double* __restrict__ Rinv = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double xb[32];
+  __shared__ double Rsm[32][33];  // Rinv_b staged by coalesced rows (padded: conflict-free)
   for (int hi = n; hi > 0; hi -= 32) {
     const int lo = max(0, hi - 32), w = hi - lo;
     if (Rinv && warp == 0) {
-      // x_b = Rinv_b y_b (lane r: row r of Rinv_b)
+      // x_b = Rinv_b y_b (lane r: row r of Rinv_b).  Rinv_b is row-major, so
+      // lane r reading its row directly would touch 32 sectors per load; the
+      // block comes in by rows (32 coalesced loads in flight) instead.
       const double* Ri = Rinv + (int64_t)((n - hi) / 32) * 1024;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Rsm[j][lane] = Ri[j * 32 + lane];
+      __syncwarp();
       double a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
         const double y0 = (j < w) ? xs[lo + j] : 0.0;
         const double y1 = (j + 1 < w) ? xs[lo + j + 1] : 0.0;
-        a0 = fma((j < w && lane < w) ? Ri[lane * 32 + j] : 0.0, y0, a0);
-        a1 = fma((j + 1 < w && lane < w) ? Ri[lane * 32 + j + 1] : 0.0, y1, a1);
+        a0 = fma((j < w && lane < w) ? Rsm[lane][j] : 0.0, y0, a0);
+        a1 = fma((j + 1 < w && lane < w) ? Rsm[lane][j + 1] : 0.0, y1, a1);
       }
       __syncwarp();
       if (lane < w) {
@@ -741,13 +896,40 @@ static int fused_launch(const double* A, int64_t m, int64_t n, int64_t lda, cons
                                                  r_out, zpart, npart, z, norm2, counter,      \
                                                  dscal);                                      \
   } while (0)
-  if (nc <= 8)
-    SKL_LF_LAUNCH(8);
-  else if (nc <= 16)
-    SKL_LF_LAUNCH(16);
-  else
-    SKL_LF_LAUNCH(32);
+  static const bool reg_kernel = env_flag("SKL_LSQR_FUSED_REG");  // A/B knob
+#define SKL_LF2_LAUNCH(NCV, STV)                                                              \
+  do {                                                                                        \
+    const size_t smem = (size_t)(STV) * 8 * (NCV) * LF2_RB * sizeof(double);                  \
+    SKL_CUDA(raise_smem_limit(lsqr_fused_async_kernel<NCV, STV>, smem));                      \
+    int occ = 1;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_fused_async_kernel<NCV, STV>,    \
+                                                  LQ_NT, smem);                               \
+    const int64_t nb2 = (m + LF2_RB - 1) / LF2_RB;                                            \
+    const int gr = (int)std::max<int64_t>(                                                    \
+        1, std::min<int64_t>({nb2, (int64_t)std::max(occ, 1) * sm_count_lq(), (int64_t)grid})); \
+    lsqr_fused_async_kernel<NCV, STV><<<gr, LQ_NT, smem, st>>>(A, m, n, lda, y, s, alpha,     \
+                                                               r_prev,                         \
+                                                          beta_prev, r_out, zpart, npart, z,   \
+                                                          norm2, counter, dscal);              \
+  } while (0)
+  if (reg_kernel) {
+    if (nc <= 8)
+      SKL_LF_LAUNCH(8);
+    else if (nc <= 16)
+      SKL_LF_LAUNCH(16);
+    else
+      SKL_LF_LAUNCH(32);
+  } else {
+    // stages: ~192 KB of ring per CTA (64 KB blocks at n = 256)
+    if (nc <= 8)
+      SKL_LF2_LAUNCH(8, 8);
+    else if (nc <= 16)
+      SKL_LF2_LAUNCH(16, 6);
+    else
+      SKL_LF2_LAUNCH(32, 3);
+  }
 #undef SKL_LF_LAUNCH
+#undef SKL_LF2_LAUNCH
   SKL_CUDA_LAUNCH();
   return SKL_OK;
 }
@@ -880,7 +1062,7 @@ __device__ __forceinline__ void ls_sym_ortho(double a, double b, double* c, doub
   *r = __ddiv_rn(a, cs);
 }
 
-__global__ void lsqr_recur_kernel(double* st) {
+__device__ __forceinline__ void ls_recur(double* st) {
   const double beta = __dsqrt_rn(st[LS_BETA2]);
   double alfa = st[LS_ALFA];
   double anorm = st[LS_ANORM];
@@ -907,6 +1089,65 @@ __global__ void lsqr_recur_kernel(double* st) {
   st[LS_ANORM] = anorm;
   st[LS_BPREV] = beta > 0.0 ? beta : 1.0;
 }
+__global__ void lsqr_recur_kernel(double* st) { ls_recur(st); }
+
+// The whole device step after a pass in one CTA (what lsqr_trsv_t_kernel,
+// lsqr_trsv_n_kernel, lsqr_recur_kernel and lsqr_xw_kernel do in four
+// launches, with the same operations in the same order: bitwise the same
+// iterates), so an iteration is two kernels -- the pass and this -- and
+// the step's three launch gaps are gone.  Launched with programmatic
+// serialization right after the pass (pdl_enter).
+__global__ void __launch_bounds__(LT_NT) lsqr_step_kernel(
+    const double* __restrict__ R, int64_t ldr, int n, const double* __restrict__ Rinv,
+    const double* __restrict__ z, double* v, double* v_raw, double* y, double* w, double* x,
+    double* st) {
+  pdl_enter();
+  extern __shared__ double xs[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const double beta = sqrt(st[LS_BETA2]);  // ||r|| of the step's pass
+  if (beta != 0.0) {
+    // v_raw = R^-T z - beta v, ||v_raw||^2 -> LS_ALFA2
+    for (int i = tid; i < n; i += LT_NT) xs[i] = z[i];
+    __syncthreads();
+    if (R) lq_solve_t(R, ldr, n, xs, Rinv);
+    double ss = 0.0;
+    for (int i = tid; i < n; i += LT_NT) {
+      const double vv = xs[i] - beta * v[i];
+      v_raw[i] = vv;
+      ss = fma(vv, vv, ss);
+    }
+    const double t = lq_block_sum(ss, red);
+    if (tid == 0) st[LS_ALFA2] = t;
+    __syncthreads();
+    // v_n = v_raw / alfa into v_raw and v, y = R^-1 v_n
+    const double alfa = sqrt(st[LS_ALFA2]);
+    for (int i = tid; i < n; i += LT_NT) {
+      const double vn = alfa > 0.0 ? v_raw[i] / alfa : v_raw[i];
+      v_raw[i] = vn;
+      v[i] = vn;
+      xs[i] = vn;
+    }
+    __syncthreads();
+    if (R) lq_solve_n(R, ldr, n, xs, Rinv);
+    for (int i = tid; i < n; i += LT_NT) y[i] = xs[i];
+  }
+  __syncthreads();
+  if (tid == 0) ls_recur(st);
+  __syncthreads();
+  // x += c1 w; w = v + c2 w; ||x||^2 -> LS_XNORM2
+  const double c1 = st[LS_C1], c2 = st[LS_C2];
+  double ss = 0.0;
+  for (int i = tid; i < n; i += LT_NT) {
+    const double wi = w[i];
+    const double xi = x[i] + c1 * wi;
+    x[i] = xi;
+    w[i] = v[i] + c2 * wi;
+    ss = fma(xi, xi, ss);
+  }
+  const double t = lq_block_sum(ss, red);
+  if (tid == 0) st[LS_XNORM2] = t;
+}
 
 // One device-driven LSQR step after the fused pass (n <= 256 dense): the
 // transposed solve (beta from the pass), the solve for y (alfa from it), the
@@ -919,15 +1160,12 @@ extern "C" int skl_lsqr_step_dev(const double* R, int64_t ldr, int64_t n, const 
   clear_error();
   SKL_REQUIRE(z && v && v_raw && y && w && x && state && n >= 1, SKL_ERR_INVALID,
               "lsqr_step_dev: bad arguments");
-  int rc = trsv_t_launch(R, ldr, n, z, 0.0, v, v_raw, state + LS_ALFA2, Rinv, stream, state);
-  if (rc) return rc;
-  rc = trsv_n_launch(R, ldr, n, 0.0, v_raw, y, Rinv, stream, state, v);
-  if (rc) return rc;
-  lsqr_recur_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(state);
-  SKL_CUDA_LAUNCH();
-  lsqr_xw_kernel<<<1, LT_NT, 0, (cudaStream_t)stream>>>((int)n, 0.0, 0.0, v, w, x,
-                                                        state + LS_XNORM2, state);
-  SKL_CUDA_LAUNCH();
+  SKL_REQUIRE(n <= 24 * 1024 && (!R || ldr >= n), SKL_ERR_INVALID, "lsqr_step_dev: bad shape");
+  const size_t smem = (size_t)n * sizeof(double);
+  if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_step_kernel, smem));
+  // the pass is the kernel right before this one on the stream
+  SKL_CUDA(launch_k(lsqr_step_kernel, dim3(1), dim3(LT_NT), smem, (cudaStream_t)stream, true, R,
+                    ldr, (int)n, Rinv, z, v, v_raw, y, w, x, state));
   return SKL_OK;
 }
 
