@@ -373,12 +373,31 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     S[i * QB_PLD + j] = j < jb ? p.M[(p.j0 + j) * p.ldm + tbeg + i] : 0.0;
   }
   __syncthreads();
-  double P[RPW];
+  // Layout A (RPW <= 16): lane = column, RPW rows per thread.  Layout B
+  // (RPW == 32, d > 4096): lane = (column pair cp = lane & 15, row half
+  // hh = lane >> 4), 16 rows x 2 columns per thread -- a column step then
+  // needs 16 pivot values per thread (32 shuffles) instead of 32 (64), and
+  // they fit in registers for the update, which needs none (layout A at
+  // RPW = 32 spent two shuffle-bound phases of ~1.2 K cycles per column).
+  constexpr bool LB = RPW == 32;
+  constexpr int NP = LB ? RPW / 2 : RPW;  // row slots per thread
+  const int cp = lane & 15, hh = lane >> 4;
+  double P[NP];
+  double P1[LB ? NP : 1];  // layout B: the pair's second column
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int li = r * QR_NW2 + warp;
-    P[r] = li < nt ? S[li * QB_PLD + lane] : 0.0;
+  for (int r = 0; r < NP; ++r) {
+    if constexpr (LB) {
+      const int li = (2 * r + hh) * QR_NW2 + warp;
+      P[r] = li < nt ? S[li * QB_PLD + 2 * cp] : 0.0;
+      P1[r] = li < nt ? S[li * QB_PLD + 2 * cp + 1] : 0.0;
+    } else {
+      const int li = r * QR_NW2 + warp;
+      P[r] = li < nt ? S[li * QB_PLD + lane] : 0.0;
+    }
   }
+  (void)P1;
+  (void)cp;
+  (void)hh;
   __syncthreads();
   double H0 = 0.0, H1 = 0.0;  // head rows warp and warp + 16 (CTA 0)
   if (head) {
@@ -402,26 +421,52 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   for (int k = 0; k < jb; ++k) {
     const int b = k & 1;
     // ---- dot products s_j = sum_{i > pivot} x_i P_i[j]
-    double xs[KEEPX ? RPW : 1];
+    double xs[KEEPX ? NP : 1];
     double s0 = 0.0, s1 = 0.0;
+    if constexpr (LB) {
+      // pivot values of this thread's rows: column k lives in lane
+      // (k >> 1) of the same row half, in P (k even) or P1 (k odd)
+      const int src = (k >> 1) | (hh << 4);
+      const bool odd = k & 1;
+      double ev = 0.0, ov = 0.0;
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const double x = __shfl_sync(0xffffffffu, P[r], k);
-      if (KEEPX) xs[r & (KEEPX ? RPW - 1 : 0)] = x;
-      if (r & 1)
-        s1 = fma(x, P[r], s1);
-      else
-        s0 = fma(x, P[r], s0);
+      for (int r = 0; r < NP; ++r) {
+        const double x = __shfl_sync(0xffffffffu, odd ? P1[r] : P[r], src);
+        ev = fma(x, P[r], ev);
+        ov = fma(x, P1[r], ov);
+      }
+      // lane (cp, hh) keeps column 2 cp + hh: its half plus the other half's
+      const double other = __shfl_xor_sync(0xffffffffu, hh ? ev : ov, 16);
+      s0 = (hh ? ov : ev) + other;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const double x = __shfl_sync(0xffffffffu, P[r], k);
+        if (KEEPX) xs[r & (KEEPX ? RPW - 1 : 0)] = x;
+        if (r & 1)
+          s1 = fma(x, P[r], s1);
+        else
+          s0 = fma(x, P[r], s0);
+      }
     }
     double xh0 = 0.0, xh1 = 0.0;
     if (head) {
       xh0 = __shfl_sync(0xffffffffu, H0, k);
       xh1 = __shfl_sync(0xffffffffu, H1, k);
-      if (warp > k) s0 = fma(xh0, H0, s0);
-      if (warp + 16 > k) s1 = fma(xh1, H1, s1);
+      if constexpr (LB) {
+        // head rows stay in layout A (lane = column): move their column
+        // sums to the lane that holds the tail sum of the same column
+        double hs = 0.0;
+        if (warp > k) hs = fma(xh0, H0, hs);
+        if (warp + 16 > k) hs = fma(xh1, H1, hs);
+        s1 = __shfl_sync(0xffffffffu, hs, 2 * cp + hh);
+      } else {
+        if (warp > k) s0 = fma(xh0, H0, s0);
+        if (warp + 16 > k) s1 = fma(xh1, H1, s1);
+      }
     }
     QR_PROBE(1);
-    red[warp * 33 + lane] = s0 + s1;
+    red[warp * 33 + (LB ? 2 * cp + hh : lane)] = s0 + s1;
     __syncthreads();
     QR_PROBE(2);
     // Buffers of parity b are rewritten only at column k + 2: by then this
@@ -521,10 +566,24 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
     __syncthreads();
     QR_PROBE(6);
     const double ws = sc[b * 128 + lane];
+    if constexpr (LB) {
+      // the pivot values again (no registers left to keep them: 16 rows x 2
+      // columns of the panel, and the dlarfg path of warp 0)
+      const double w0 = sc[b * 128 + 2 * cp], w1 = sc[b * 128 + 2 * cp + 1];
+      const int src = (k >> 1) | (hh << 4);
+      const bool odd = k & 1;
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const double x = KEEPX ? xs[r & (KEEPX ? RPW - 1 : 0)] : __shfl_sync(0xffffffffu, P[r], k);
-      P[r] = fma(-ws, x, P[r]);
+      for (int r = 0; r < NP; ++r) {
+        const double x = __shfl_sync(0xffffffffu, odd ? P1[r] : P[r], src);
+        P[r] = fma(-w0, x, P[r]);
+        P1[r] = fma(-w1, x, P1[r]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const double x = KEEPX ? xs[r & (KEEPX ? RPW - 1 : 0)] : __shfl_sync(0xffffffffu, P[r], k);
+        P[r] = fma(-ws, x, P[r]);
+      }
     }
     if (head) {
       const double wj = sc[b * 128 + 32 + lane], beta = sc[b * 128 + 64];
@@ -548,9 +607,17 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   // ---- write back: column j rows below its pivot are scale_j * stored
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int li = r * QR_NW2 + warp;
-    if (li < nt) S[li * QB_PLD + lane] = P[r];
+  for (int r = 0; r < NP; ++r) {
+    if constexpr (LB) {
+      const int li = (2 * r + hh) * QR_NW2 + warp;
+      if (li < nt) {
+        S[li * QB_PLD + 2 * cp] = P[r];
+        S[li * QB_PLD + 2 * cp + 1] = P1[r];
+      }
+    } else {
+      const int li = r * QR_NW2 + warp;
+      if (li < nt) S[li * QB_PLD + lane] = P[r];
+    }
   }
   __syncthreads();
   #pragma unroll 8
