@@ -72,17 +72,10 @@ class CsrOperator:
     the nonzeros by column keeps each column's rows ascending, so the
     transposed product is deterministic."""
 
-    def __init__(self, indptr, indices, values, m: int, n: int):
-        self.indptr, self.indices, self.values, self.m, self.n = indptr, indices, values, m, n
-        counts = indptr[1:] - indptr[:-1]
-        rows = torch.repeat_interleave(torch.arange(m, dtype=torch.int32, device=indptr.device),
-                                       counts)
-        order = torch.sort(indices, stable=True).indices
-        self.rowidx = rows[order].contiguous()
-        self.cval = values[order].contiguous()
-        colptr = torch.zeros(n + 1, dtype=torch.int64, device=indptr.device)
-        colptr[1:] = torch.cumsum(torch.bincount(indices, minlength=n), 0)
-        self.colptr = colptr
+    def __init__(self, A):
+        self.indptr, self.indices, self.values = A.device_arrays()
+        self.m, self.n = A.rows, A.cols
+        self.colptr, self.rowidx, self.cval = A.device_csc()  # cached with the operand
 
     def mv(self, y, s, alpha, u_in, u_out, norm2, ws, st):
         _native.call("skl_lsqr_spmv", _native.ptr(self.indptr), _native.ptr(self.indices),

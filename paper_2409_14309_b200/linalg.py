@@ -165,6 +165,27 @@ class SparseMatrix:
                           to_device(self.values))
         return cache[dev]
 
+    def device_csc(self):
+        """(colptr int64 cols+1, rowidx int32, values) of the same matrix in
+        compressed-column form on the current device, built once from the
+        device CSR arrays (a stable sort of the nonzeros by column, so the
+        rows of every column stay ascending -- the order scipy's folds use)
+        and kept with the operand, like the device copy itself (LSQR's
+        A^T u; round 1 rebuilt it for every solve)."""
+        require_cuda()
+        key = ("csc", torch.cuda.current_device())
+        cache = self._dev
+        if key not in cache:
+            indptr, indices, values = self.device_arrays()
+            counts = indptr[1:] - indptr[:-1]
+            rows = torch.repeat_interleave(
+                torch.arange(self.rows, dtype=torch.int32, device=indptr.device), counts)
+            order = torch.sort(indices, stable=True).indices
+            colptr = torch.zeros(self.cols + 1, dtype=torch.int64, device=indptr.device)
+            colptr[1:] = torch.cumsum(torch.bincount(indices, minlength=self.cols), 0)
+            cache[key] = (colptr, rows[order].contiguous(), values[order].contiguous())
+        return cache[key]
+
 
 @dataclass(frozen=True)
 class Vector:

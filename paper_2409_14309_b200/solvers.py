@@ -219,8 +219,7 @@ def _operator_device(A: Matrix):
     from ._lsqr import CsrOperator, DenseOperator
 
     if isinstance(A, SparseMatrix):
-        indptr, indices, values = A.device_arrays()
-        return CsrOperator(indptr, indices, values, A.rows, A.cols), None, 0
+        return CsrOperator(A), None, 0
     A_dev = A.data if A.on_device else to_device(A.data)
     lda = A.ld if A.on_device else A.rows
     if A_dev.data_ptr() % 16 or (lda % 2 and A.cols > 1):
