@@ -385,6 +385,15 @@ int skl_gemm_f64(const double* G, int64_t ldg, const double* A, int64_t lda, dou
 int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
                  double* x, double* R, int64_t ldr, double* Q, int64_t ldq, int64_t* bad_col,
                  double* bad_val, void* stream);
+/* skl_qr_solve without the synchronisation: bad_col / bad_val (pinned host
+ * or device memory) are written in stream order and checked by the caller
+ * once the stream has passed them (*bad_col >= 0: rank deficient at that
+ * column, |R[c, c]| = *bad_val -- the SKL_ERR_SINGULAR case of
+ * skl_qr_solve), so the residual pass of a solve can be enqueued behind the
+ * factorisation with one synchronisation for both. */
+int skl_qr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
+                       double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
+                       int64_t* bad_col, double* bad_val, void* stream);
 
 /* ||A x - b||_2 for dense column-major A (device).  Replaces
  * solvers.py:102-107.  *out is host. */

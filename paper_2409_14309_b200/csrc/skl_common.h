@@ -131,6 +131,27 @@ template <class K>
 inline cudaError_t raise_smem_limit(K* kernel, size_t bytes) {
   return raise_smem_limit(reinterpret_cast<const void*>(kernel), bytes);
 }
+// Prefer the largest shared-memory carveout for a kernel, once per device
+// (cudaFuncSetAttribute costs microseconds of host time per call: it sat on
+// every launch of the sketch kernels).
+inline cudaError_t prefer_max_shared(const void* func) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  bool& d = done[{dev, func}];
+  if (d) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) d = true;
+  return e;
+}
+template <class K>
+inline cudaError_t prefer_max_shared(K* kernel) {
+  return prefer_max_shared(reinterpret_cast<const void*>(kernel));
+}
 
 // Stream-ordered workspace allocation from a memory pool the library owns
 // (one per device, created on first use), not the device's default pool:

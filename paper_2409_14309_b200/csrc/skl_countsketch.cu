@@ -399,8 +399,7 @@ static cudaError_t launch_cs(const CsParams& p, dim3 grid, size_t smem, cudaStre
                              : countsketch_dense_kernel<NT, C, false>;
   cudaError_t e = raise_smem_limit(kern, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
+  e = prefer_max_shared(kern);
   if (e != cudaSuccess) return e;
   kern<<<grid, NT + 32, smem, st>>>(p);
   return cudaGetLastError();
@@ -500,8 +499,7 @@ static cudaError_t launch_owned(const OwParams& p, dim3 grid, size_t smem, cudaS
   auto k = countsketch_owned_kernel<NT, SC, SL>;
   cudaError_t e = raise_smem_limit(k, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
+    e = prefer_max_shared(k);
   if (e != cudaSuccess) return e;
   k<<<grid, NT + 32, smem, st>>>(p);
   return cudaGetLastError();

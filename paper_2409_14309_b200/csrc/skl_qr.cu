@@ -499,10 +499,27 @@ int qr_blocked_form_q(double* Q, int64_t ldq, int64_t d, int64_t n, const double
 
 using namespace skl;
 
+static int qr_solve_impl(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
+                         double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
+                         int64_t* bad_col, double* bad_val, void* stream, bool sync);
+
 extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
                             int64_t n, double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
                             int64_t* bad_col, double* bad_val, void* stream) {
   clear_error();
+  return qr_solve_impl(SA, ldsa, Sb, d, n, x, R, ldr, Q, ldq, bad_col, bad_val, stream, true);
+}
+
+extern "C" int skl_qr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
+                                  int64_t n, double* x, double* R, int64_t ldr, double* Q,
+                                  int64_t ldq, int64_t* bad_col, double* bad_val, void* stream) {
+  clear_error();
+  return qr_solve_impl(SA, ldsa, Sb, d, n, x, R, ldr, Q, ldq, bad_col, bad_val, stream, false);
+}
+
+static int qr_solve_impl(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
+                         double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
+                         int64_t* bad_col, double* bad_val, void* stream, bool sync) {
   cudaStream_t st = (cudaStream_t)stream;
   SKL_REQUIRE(d >= n && n >= 1, SKL_ERR_SHAPE,
               "economy_qr requires rows >= cols, got %lldx%lld", (long long)d, (long long)n);
@@ -635,9 +652,9 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
       }
     }
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_col, badc, 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_val, badv, 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_col, badc, 8, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_val, badv, 8, cudaMemcpyDefault, st);
+    if (e == cudaSuccess && sync) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       set_error("qr_solve: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
@@ -645,7 +662,7 @@ extern "C" int skl_qr_solve(const double* SA, int64_t ldsa, const double* Sb, in
   } while (0);
 #undef QR_LAUNCH
   cudaFreeAsync(ws, st);
-  if (rc == SKL_OK && *bad_col >= 0) {
+  if (rc == SKL_OK && sync && *bad_col >= 0) {
     set_error("input is numerically rank deficient at column %lld (|R[%lld,%lld]| = %.3e)",
               (long long)*bad_col, (long long)*bad_col, (long long)*bad_col, *bad_val);
     return SKL_ERR_SINGULAR;

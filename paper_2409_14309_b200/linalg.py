@@ -14,6 +14,9 @@ kernels that consume it.
 
 from __future__ import annotations
 
+import math
+import threading
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -212,6 +215,23 @@ class Vector:
             raise ValueError("vector entries must be finite")
         object.__setattr__(self, "data", _freeze(a))
 
+    @classmethod
+    def _of_solution(cls, x, residual_norm: float) -> "Vector":
+        """Wrap a solver's x without the finiteness pass when ||A x - b|| is
+        finite (a non-finite entry of x makes the residual non-finite: every
+        column of A has a nonzero, or the sketched QR would have stopped),
+        sparing a device reduction and a synchronisation per solve; a
+        non-finite residual goes through the full check (and its error)."""
+        if not math.isfinite(residual_norm):
+            return cls(x)
+        if _is_tensor(x):
+            if x.dtype != torch.float64 or x.dim() != 1 or not x.is_cuda:
+                return cls(x)
+            v = object.__new__(cls)
+            object.__setattr__(v, "data", x.contiguous())
+            return v
+        return cls(x)
+
     @property
     def len(self) -> int:
         return int(self.data.shape[0])
@@ -259,6 +279,36 @@ def qr_solve_device(SA, ldsa: int, Sb, d: int, n: int, want_q: bool = False,
         _native.ptr(R), n, _native.ptr(Q), d, _native.ptr(bad_col), _native.ptr(bad_val),
         current_stream())
     return x, R, Q
+
+
+_RANK_FLAGS = threading.local()
+
+
+def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):
+    """qr_solve_device without its synchronisation: returns (x, check) where
+    check() -- to be called once the stream has been synchronised (e.g. by
+    the residual pass) -- raises the same SingularFactorError skl_qr_solve
+    would have.  The rank flag lands in a pinned per-thread buffer."""
+    flags = getattr(_RANK_FLAGS, "buf", None)
+    if flags is None:
+        flags = torch.empty(2, dtype=torch.float64, pin_memory=True)
+        _RANK_FLAGS.buf = flags
+    flags_i = flags.view(torch.int64)
+    x = device_f64((n,))
+    base = flags.data_ptr()
+    _native.call(
+        "skl_qr_solve_async", _native.ptr(SA), ldsa, _native.ptr(Sb), d, n, _native.ptr(x),
+        None, n, None, d, base, base + 8, current_stream())
+
+    def check() -> None:
+        bad = int(flags_i[0])
+        if bad >= 0:
+            val = float(flags[1])
+            raise SingularFactorError(
+                f"input is numerically rank deficient at column {bad} "
+                f"(|R[{bad},{bad}]| = {val:.3e})")
+
+    return x, check
 
 
 def economy_qr(M: DenseMatrix) -> QRFactors:

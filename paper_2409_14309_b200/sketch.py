@@ -283,16 +283,21 @@ class SketchOperator:
                 if build is None:
                     return None
                 value = build()
+                st0 = torch.cuda.current_stream()
                 ev = torch.cuda.Event()
-                ev.record(torch.cuda.current_stream())
-                entry = c[name] = (value, ev)
-        value, ev = entry
+                ev.record(st0)
+                entry = c[name] = (value, ev, st0.cuda_stream)
+        value, ev, made_on = entry
+        st = torch.cuda.current_stream()
+        if st.cuda_stream == made_on:
+            # the stream that built it: stream order already covers the build
+            # and the allocator's own bookkeeping the lifetime
+            return value
         if torch.cuda.is_current_stream_capturing():
             # inside a CUDA-graph capture the artifact was built before the
             # capture began (the warm-up call); an event from outside the
             # capture cannot be waited on there
             return value
-        st = torch.cuda.current_stream()
         st.wait_event(ev)
         for t in _tensors_of(value):
             t.record_stream(st)

@@ -1,0 +1,27 @@
+"""Host-side cost of one warm SAA solve (config 2, device-resident A): a
+cProfile of 200 solves, top entries by cumulative time."""
+import cProfile
+import pstats
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_2409_14309_b200 as E  # noqa: E402
+from paper_2409_14309_b200 import workloads as W  # noqa: E402
+
+c = W.config(2, kind="countsketch")
+A, b, _ = W.make_problem(c, backend="torch")
+prob = E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b))
+spec, opts = E.SketchSpec("countsketch", 1, seed=W.SEED), E.SolverOptions(d_factor=c.d / c.n)
+for _ in range(5):
+    E.solve(prob, "saa", spec, opts)
+torch.cuda.synchronize()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(200):
+    E.solve(prob, "saa", spec, opts)
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
