@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
   // needs 16 pivot values per thread (32 shuffles) instead of 32 (64), and
   // they fit in registers for the update, which needs none (layout A at
   // RPW = 32 spent two shuffle-bound phases of ~1.2 K cycles per column).
+  // (the 2-column layout for RPW <= 16 too measured 1-5 % slower)
   constexpr bool LB = RPW == 32;
   constexpr int NP = LB ? RPW / 2 : RPW;  // row slots per thread
   const int cp = lane & 15, hh = lane >> 4;
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
         const double x = __shfl_sync(0xffffffffu, odd ? P1[r] : P[r], src);
+        if constexpr (KEEPX) xs[r] = x;
         ev = fma(x, P[r], ev);
         ov = fma(x, P1[r], ov);
       }
@@ -574,7 +576,11 @@ __global__ void __launch_bounds__(QR_NT2) qr_panel_reg_kernel(const PanelParams 
       const bool odd = k & 1;
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
-        const double x = __shfl_sync(0xffffffffu, odd ? P1[r] : P[r], src);
+        double x;
+        if constexpr (KEEPX)
+          x = xs[r];
+        else
+          x = __shfl_sync(0xffffffffu, odd ? P1[r] : P[r], src);
         P[r] = fma(-w0, x, P[r]);
         P1[r] = fma(-w1, x, P1[r]);
       }
