@@ -395,6 +395,21 @@ int skl_qr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t
                        double* x, double* R, int64_t ldr, double* Q, int64_t ldq,
                        int64_t* bad_col, double* bad_val, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Reduced solve of sketch-and-apply by shifted CholeskyQR2 (device): the
+ * same R (diag > 0, unique) and x as skl_qr_solve to rounding, with one
+ * corrected semi-normal refinement step; the rank check of linalg.py:186-191
+ * on diag(R).  Replaces the numpy QR + solve_triangular of solvers.py:309
+ * for systems with n + 1 <= 512 < d (skl_cqr_supported).  Asynchronous like
+ * skl_qr_solve_async: *bad_col (pinned host or device) receives -1 when x
+ * is valid, the first rank-deficient column, or -2 when a Cholesky pivot
+ * broke down; in both failure cases the caller re-solves with skl_qr_solve
+ * (Householder), which produces the reference's error message.
+ * ------------------------------------------------------------------- */
+int skl_cqr_supported(int64_t d, int64_t n);
+int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,
+                        double* x, int64_t* bad_col, double* bad_val, void* stream);
+
 /* ||A x - b||_2 for dense column-major A (device).  Replaces
  * solvers.py:102-107.  *out is host. */
 int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,

@@ -177,6 +177,8 @@ SIGNATURES: dict[str, tuple] = {
         [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
          c_ptr],
     ),
+    "skl_cqr_supported": (c_int, [c_i64, c_i64]),
+    "skl_cqr_solve_async": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_residual_dense": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_sum_slots": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_reduce_peers": (c_int, [c_ptr, c_int, c_i64, c_i64, c_ptr, c_ptr]),

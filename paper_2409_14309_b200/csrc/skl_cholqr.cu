@@ -1,0 +1,1211 @@
+// Reduced solve of the sketch-and-apply path by shifted CholeskyQR2 with one
+// step of corrected semi-normal refinement.
+//
+// Reference: /root/reference/pkg/src/sketchls/solvers.py:296-320 and
+// linalg.py:166-192, 214-218 -- x = R^{-1} Q^T Sb from the economy QR of SA
+// (numpy/LAPACK Householder), diag(R) >= 0, rank check
+// |R[c,c]| < 1e-14 ||SA||_F.  The R factor with a positive diagonal is
+// unique, so any backward-stable QR gives the reference's R and x to
+// rounding; this file computes it with far fewer dependent steps than a
+// column-by-column Householder sweep (skl_qr_blocked.cu: 257 dependent
+// column steps across a thread-block cluster for config 2's 2048 x 257):
+//
+//   M  = [SA | Sb]                     (d x N, N = n + 1, never copied)
+//   G1 = M^T M                          gram kernel, fp64 tensor cores (DMMA)
+//   R1 = chol(G1 + s I)                 cluster Cholesky, s = 11 (dN + N(N+1)) u ||M||_F^2
+//   Q1 = M R1^{-1}                      row-block TRSM (DMMA)
+//   G2 = Q1^T Q1, R2 = chol(G2)         (shifted CholeskyQR2: Fukaya, Kannan,
+//   R  = R2 R1                           Nakatsukasa, Yamamoto, Yanagisawa 2020)
+//   x  = R[:n,:n]^{-1} R[:n, n]         (the augmented column carries Q^T Sb)
+//   x += R^{-1} R^{-T} SA^T (Sb - SA x) (one corrected semi-normal step)
+//
+// The refinement step brings the x error on config 2 (kappa = 1e8) to the
+// spread of two Householder QRs of the same system (measured in numpy on the
+// full-size sketched system: 4-6e-9 vs the Householder spread of 3-6e-9).
+// A non-positive or non-finite Cholesky pivot (numerically rank deficient
+// or kappa beyond ~1e15) sets a flag; the caller then falls back to the
+// Householder factorisation, which also produces the reference's error.
+//
+// Layouts: Gram, R and the diagonal-block inverses of R are kept as 32 x 32
+// column-major tiles ("tile layout"), upper tiles (I <= J) packed column by
+// column: tile (I, J) at index J (J + 1) / 2 + I.  Rows / columns past N are
+// padded with the identity.
+//
+// Kernels (one stream, programmatic dependent launch between them):
+//   cqr_gram_kernel   one CTA per (upper tile, row slice); 4 warps each own
+//                     the whole 32 x 32 tile over a quarter of the slice's
+//                     16-row chunks (DMMA m16n8k4, operands straight from
+//                     HBM/L2 with 32-byte vector loads); the last CTA of a
+//                     tile folds the slices in fixed order (deterministic).
+//   cqr_chol_kernel   one cluster of nb CTAs, CTA J owns block column J in
+//                     shared memory.  Step K: CTA K factors its diagonal
+//                     tile (LDL^T in one warp: the dependent chain per pivot
+//                     is a shuffle, a reciprocal and two FMAs); every CTA
+//                     J > K solves its tile (K, J) against it (forward
+//                     substitution, U_KK read over DSMEM); CTA K+1 updates
+//                     and factors the next diagonal tile while the others
+//                     apply the rank-32 update to the rest of their column
+//                     (DMMA, R(K, I) read over DSMEM).  Two split cluster
+//                     barriers per step.
+//   cqr_trsm_kernel   Q = M R^{-1}, 16 rows per CTA, block-column sweep with
+//                     the inverted diagonal blocks.
+//   cqr_solve_*       rank check, y, the triangular solves (one CTA), the
+//                     residual and SA^T r (multi-CTA GEMVs).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "skl_common.h"
+#include "skl_ptx.cuh"
+
+namespace skl {
+
+constexpr int CQ_LD = 33;                 // shared-memory tile stride (doubles)
+constexpr int CQ_TILE = 32 * CQ_LD;       // doubles per shared-memory tile
+constexpr int CQ_MAXNB = 16;              // block columns (= cluster CTAs): N <= 512
+constexpr int CQ_CHOL_NT = 256;
+constexpr int CQ_TRSM_ROWS = 16;
+constexpr int CQ_QLD = 20;                // row stride of the TRSM's Q block (conflict-free frags)
+constexpr double CQ_RANK_TOL = 1e-14;     // linalg.py RANK_TOL
+
+__host__ __device__ __forceinline__ int64_t cq_tile(int I, int J) {
+  return (int64_t)J * (J + 1) / 2 + I;
+}
+
+// Columns of M: column c < n of A (ld lda), column n = b (when b != null).
+struct CqCols {
+  const double* A;
+  int64_t lda;
+  const double* b;
+  int64_t n;  // columns taken from A
+  int64_t d;  // rows
+};
+__device__ __forceinline__ const double* cq_col(const CqCols& X, int64_t c) {
+  return c < X.n ? X.A + c * X.lda : X.b;
+}
+
+__device__ __forceinline__ void cq_dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__device__ __forceinline__ uint32_t cq_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cq_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cq_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Remote shared-memory load (ordering from the cluster barrier before use).
+__device__ __forceinline__ double cq_ld_remote(const double* local, uint32_t cta) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local));
+  uint32_t ra;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+  double v;
+  asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+  return v;
+}
+
+// Instrumented builds (SKL_NVCC_DEFINES=-DSKL_CQR_PROBE): thread 0 of every
+// Cholesky CTA records %globaltimer at phase boundaries (skl_cqr_probe_dump).
+#ifdef SKL_CQR_PROBE
+__device__ long long g_cqr_probe[2][CQ_MAXNB][72];
+__device__ int g_cqr_probe_call;
+__device__ __forceinline__ long long cq_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CQ_PROBE(slot)                                                                   \
+  do {                                                                                   \
+    if (threadIdx.x == 0) g_cqr_probe[p.shift_coef > 0.0 ? 0 : 1][J][(slot)] = cq_now(); \
+  } while (0)
+#else
+#define CQ_PROBE(slot) \
+  do {                 \
+  } while (0)
+#endif
+
+// ------------------------------------------------------------------ Gram
+struct GramParams {
+  CqCols X;
+  int64_t N;
+  int nb;
+  int S;              // row slices
+  int64_t nchunk;     // 16-row chunks of d
+  int vec;            // columns 16-byte aligned: 32-byte vector loads
+  double* part;       // [S][ntiles][1024] (S > 1)
+  double* Gt;         // [ntiles][1024]
+  unsigned* cnt;      // [ntiles], zero on entry, left zero
+};
+
+__global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
+  pdl_enter();
+  __shared__ double red[4][1024];
+  __shared__ int is_last;
+  const int t = blockIdx.x, s = blockIdx.y;
+  int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((int64_t)(J + 1) * (J + 2) / 2 <= t) ++J;
+  while ((int64_t)J * (J + 1) / 2 > t) --J;
+  const int I = t - J * (J + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t c_beg = p.nchunk * s / p.S, c_end = p.nchunk * (s + 1) / p.S;
+  const int64_t d = p.X.d;
+
+  const double* pa[4];
+  const double* pb[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t ca = (int64_t)I * 32 + (q >> 1) * 16 + (q & 1) * 8 + g;
+    pa[q] = ca < p.N ? cq_col(p.X, ca) : nullptr;
+    const int64_t cb = (int64_t)J * 32 + q * 8 + g;
+    pb[q] = cb < p.N ? cq_col(p.X, cb) : nullptr;
+  }
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+
+  // 16-row chunk k0: lane (g, tq) holds rows k0 + 4 tq .. + 3 of its columns;
+  // MMA step j takes k = k0 + 4 tq + j (the same permutation of k for both
+  // operands, so the product is unchanged)
+  auto load4 = [&](const double* col, int64_t k, double (&v)[4]) {
+    if (col == nullptr) {
+      v[0] = v[1] = v[2] = v[3] = 0.0;
+    } else if (p.vec && k + 3 < d) {
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(col + k));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(col + k + 2));
+      v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = (k + j < d) ? __ldg(col + k + j) : 0.0;
+    }
+  };
+  // chunks ch = c_beg + warp (+4 ...): the next chunk's loads are in flight
+  // while the current one is multiplied
+  double av[4][4], bv[4][4], an[4][4], bn[4][4];
+  int64_t ch = c_beg + warp;
+  if (ch < c_end) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      load4(pa[q], ch * 16 + 4 * tq, av[q]);
+      load4(pb[q], ch * 16 + 4 * tq, bv[q]);
+    }
+  }
+  for (; ch < c_end; ch += 4) {
+    if (ch + 4 < c_end) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        load4(pa[q], (ch + 4) * 16 + 4 * tq, an[q]);
+        load4(pb[q], (ch + 4) * 16 + 4 * tq, bn[q]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], av[mt * 2][j], av[mt * 2 + 1][j], bv[nt][j]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        av[q][j] = an[q][j];
+        bv[q][j] = bn[q][j];
+      }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int r = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+        red[warp][c * 32 + r] = acc[mt][nt][h];
+      }
+  __syncthreads();
+  double* out = p.S == 1 ? p.Gt + (int64_t)t * 1024 : p.part + ((int64_t)s * gridDim.x + t) * 1024;
+  for (int e = threadIdx.x; e < 1024; e += 128)
+    out[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+  if (p.S == 1) return;
+  // the last slice CTA of this tile folds the slices in order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(&p.cnt[t], 1u) == (unsigned)(p.S - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // 8 elements per thread, the 8 loads of a slice in flight together
+  double v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0.0;
+  for (int q = 0; q < p.S; ++q) {
+    const double* src = p.part + ((int64_t)q * gridDim.x + t) * 1024 + threadIdx.x;
+    double w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 128);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += w[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p.Gt[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
+  if (threadIdx.x == 0) p.cnt[t] = 0u;
+}
+
+// -------------------------------------------------------------- Cholesky
+struct CholParams {
+  const double* Gt;    // Gram, upper tiles
+  int nb;
+  int64_t N;
+  double shift_coef;   // > 0: G += shift_coef * trace(G) * I (first iteration)
+  double* Rt;          // R, upper tiles
+  double* Rinv;        // inverses of R's diagonal tiles [nb][1024]
+  int* flag;           // set on a non-positive / non-finite pivot
+};
+
+// LDL^T of the 32 x 32 tile T (shared, column-major, stride CQ_LD) by one
+// warp, lane j holding column j.  On return T holds U (unit upper, 1 on the
+// diagonal, 0 below), disq[k] = 1 / sqrt(d_k) (disq is the 32 doubles right
+// after T: the pair is pushed to the other CTAs as one block), and Rg
+// (global tile, ld 32) R = D^{1/2} U.  Only the upper triangle of T is read.
+//
+// The step loop is rolled: each lane keeps a window c[i] = G^(k)[k + i][j]
+// of its column that shifts by one row per step, so the body has static
+// register indices and the whole routine is a few hundred instructions (it
+// runs once per CTA per factorisation, from a cold instruction cache).  The
+// dependent chain per pivot is: reciprocal (MUFU + two Newton steps), one
+// FMA on lane k+1 for the next pivot, one shuffle; the rank-1 update of the
+// window runs beside it.  srow[32..63] stay zero, so rows past the tile
+// update as no-ops.  A non-positive or non-finite pivot only sets the flag
+// (the caller then falls back to Householder).
+// One pivot step of cq_factor (ODD: k is odd, so srow + k + 1 is 16-byte
+// aligned and the row is read in pairs).  The reciprocal of the NEXT pivot
+// is started right after its shuffle, so its latency overlaps this step's
+// rank-1 update; the dependent chain per step is one FMA, one shuffle and
+// the reciprocal.
+template <bool ODD>
+__device__ __forceinline__ void cq_factor_step(int k, double (&c)[32], double& pk, double& rk,
+                                               double& myd, bool& bad, double* T, double* srow) {
+  const int lane = threadIdx.x & 31;
+  const double gk = c[0];  // G^(k)[k][lane]
+  const double pn = fma(-(gk * gk), rk, c[1]);  // lane k+1: the next pivot
+  const double pnext = __shfl_sync(0xffffffffu, pn, (k + 1) & 31);
+  double rn;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(pnext));
+  const double u = gk * rk;  // U[k][lane] for lane > k
+  bad |= !(pk > 0.0) || !(pk < INFINITY);
+  if (lane > k) T[lane * CQ_LD + k] = u;
+  if (lane == k) myd = pk;
+  srow[lane] = lane > k ? gk : 0.0;
+  __syncwarp();
+  const double* sr = srow + k + 1;
+  if (ODD) {
+#pragma unroll
+    for (int i = 0; i < 30; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(sr + i);
+      c[i] = fma(-v.x, u, c[i + 1]);
+      c[i + 1] = fma(-v.y, u, c[i + 2]);
+    }
+    c[30] = fma(-sr[30], u, c[31]);
+  } else {
+    c[0] = fma(-sr[0], u, c[1]);
+#pragma unroll
+    for (int i = 1; i < 31; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(sr + i);
+      c[i] = fma(-v.x, u, c[i + 1]);
+      c[i + 1] = fma(-v.y, u, c[i + 2]);
+    }
+  }
+  rn = fma(rn, fma(-pnext, rn, 1.0), rn);  // two Newton steps: ~1 ulp
+  rn = fma(rn, fma(-pnext, rn, 1.0), rn);
+  __syncwarp();
+  pk = pnext;
+  rk = rn;
+}
+
+__device__ __noinline__ void cq_factor(double* T, double* srow, double* Rg, int* flag) {
+  const int lane = threadIdx.x & 31;
+  double* disq = T + CQ_TILE;
+  double c[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) c[i] = T[lane * CQ_LD + i];
+  srow[32 + lane] = 0.0;
+  double pk = __shfl_sync(0xffffffffu, c[0], 0);
+  double rk;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rk) : "d"(pk));
+  rk = fma(rk, fma(-pk, rk, 1.0), rk);
+  rk = fma(rk, fma(-pk, rk, 1.0), rk);
+  bool bad = false;
+  double myd = 1.0;
+#pragma unroll 1
+  for (int k = 0; k < 32; k += 2) {
+    cq_factor_step<false>(k, c, pk, rk, myd, bad, T, srow);
+    cq_factor_step<true>(k + 1, c, pk, rk, myd, bad, T, srow);
+  }
+  const double sq = sqrt(myd);
+  srow[lane] = sq;
+  disq[lane] = 1.0 / sq;
+  __syncwarp();
+  double uk[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) uk[k] = T[lane * CQ_LD + k];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) uk[k] = k < lane ? uk[k] : (k == lane ? 1.0 : 0.0);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[lane * CQ_LD + k] = uk[k];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) Rg[lane * 32 + k] = k == lane ? sq : srow[k] * uk[k];
+  if (bad && lane == 0) atomicExch(flag, 1);
+  __syncwarp();
+}
+
+// R(K, J) = D_K^{-1/2} U_KK^{-T} G(K, J) in place (T: the tile, shared), one
+// warp, lane = column: forward substitution with U broadcast from Us (the
+// pushed block: U then 1/sqrt(d)).
+__device__ __noinline__ void cq_rowsolve(double* T, const double* Us, double* Rg) {
+  const int lane = threadIdx.x & 31;
+  const double* isq = Us + CQ_TILE;
+  double g[32], sc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    g[i] = T[lane * CQ_LD + i];
+    sc[i] = isq[i];
+  }
+#pragma unroll
+  for (int k = 0; k < 31; ++k)
+#pragma unroll
+    for (int m = k + 1; m < 32; ++m) g[m] = fma(-Us[m * CQ_LD + k], g[k], g[m]);
+  __syncwarp();  // all loads of T done before it is overwritten
+#pragma unroll
+  for (int k = 0; k < 32; ++k) g[k] *= sc[k];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[lane * CQ_LD + k] = g[k];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) Rg[lane * 32 + k] = g[k];
+}
+
+// C -= A^T B for 32 x 32 tiles (shared, stride CQ_LD): A = R(K, I) (local or
+// in CTA `acta` of the cluster), B = R(K, J) local.  The m16n8 fragments
+// [MT0, MT0 + NMT) x [NT0, NT0 + NNT).
+template <int NMT, int NNT>
+__device__ __noinline__ void cq_tile_update(double* C, const double* A, bool a_remote,
+                                            uint32_t acta, const double* B, int mt0, int nt0) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double acc[NMT][NNT][4];
+#pragma unroll
+  for (int a = 0; a < NMT; ++a)
+#pragma unroll
+    for (int b = 0; b < NNT; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+  double af[8][NMT][2];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* src = A + ((mt0 + mt) * 16 + h * 8 + g) * CQ_LD + ks * 4 + tq;
+        af[ks][mt][h] = a_remote ? cq_ld_remote(src, acta) : *src;
+      }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < NNT; ++nt) {
+      const double b0 = B[((nt0 + nt) * 8 + g) * CQ_LD + ks * 4 + tq];
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt) cq_dmma(acc[mt][nt], af[ks][mt][0], af[ks][mt][1], b0);
+    }
+#pragma unroll
+  for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NNT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int r = (mt0 + mt) * 16 + g + (h >= 2 ? 8 : 0), c = (nt0 + nt) * 8 + 2 * tq + (h & 1);
+        C[c * CQ_LD + r] -= acc[mt][nt][h];
+      }
+}
+
+// Inverse of the diagonal tile R_JJ = D^{1/2} U (U in T, unit upper):
+// R^{-1} = U^{-1} D^{-1/2}; lane j builds column j of U^{-1} upward.
+__device__ __noinline__ void cq_diag_inverse(const double* T, double* out) {
+  const int lane = threadIdx.x & 31;
+  const double* disq = T + CQ_TILE;
+  double acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+  double x[32];
+#pragma unroll
+  for (int m = 31; m >= 0; --m) {
+    const double xm = m == lane ? 1.0 : (m < lane ? -acc[m] : 0.0);
+    x[m] = xm;
+#pragma unroll
+    for (int i = 0; i < m; ++i) acc[i] = fma(T[m * CQ_LD + i], xm, acc[i]);
+  }
+  const double sc = disq[lane];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) out[lane * 32 + i] = x[i] * sc;
+}
+
+constexpr uint32_t CQ_PUSH_BYTES = (CQ_TILE + 32) * sizeof(double);
+
+// The owner of a freshly factored diagonal tile pushes U and 1/sqrt(d) (one
+// contiguous block) into buffer `buf` of every CTA that still needs it,
+// completing on that CTA's mbarrier.
+__device__ __forceinline__ void cq_push(const double* blk, int from, int nb, double (*Us)[CQ_TILE + 32],
+                                        uint64_t* mbar, int buf) {
+  fence_proxy_async_smem();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0)
+    for (int dst = from + 1; dst < nb; ++dst)
+      bulk_s2cluster(mapa_u32(smem_u32(&Us[buf][0]), (uint32_t)dst), blk, CQ_PUSH_BYTES,
+                     mapa_u32(smem_u32(&mbar[buf]), (uint32_t)dst));
+}
+
+__global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParams p) {
+  // tiles (I, J) of my block column, I = 0..J, then 32 doubles (1/sqrt of
+  // my pivots) right after my diagonal tile
+  extern __shared__ __align__(16) double csm[];
+  __shared__ __align__(16) double Us[2][CQ_TILE + 32];  // pushed U_KK | 1/sqrt(d_K)
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(16) double srow[64];
+  const int J = (int)cq_rank();
+  const int nb = p.nb;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* T = csm;
+  auto tile = [&](int I) { return T + I * CQ_TILE; };
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+    // arm the first two receptions (steps 0 and 1)
+    if (J > 0) mbar_arrive_expect_tx(&mbar[0], CQ_PUSH_BYTES);
+    if (J > 1) mbar_arrive_expect_tx(&mbar[1], CQ_PUSH_BYTES);
+  }
+  pdl_enter();
+  CQ_PROBE(0);
+  // my column's Gram tiles, all copies in flight at once (8-byte cp.async;
+  // past N: zero-filled, identity on the diagonal below)
+  for (int I = 0; I <= J; ++I) {
+    const double* src = p.Gt + cq_tile(I, J) * 1024;
+    double* dst = tile(I);
+    for (int e = tid; e < 1024; e += CQ_CHOL_NT) {
+      const int r = e & 31, c = e >> 5;
+      const bool ok = (int64_t)I * 32 + r < p.N && (int64_t)J * 32 + c < p.N;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + c * CQ_LD + r)),
+                   "l"(src + e), "r"(ok ? 8 : 0)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t gi = (int64_t)J * 32 + lane;
+    if (gi >= p.N) tile(J)[lane * (CQ_LD + 1)] = 1.0;
+    if (p.shift_coef > 0.0) {
+      // the same fixed-order trace in every CTA
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b)
+        if ((int64_t)b * 32 + lane < p.N) s += p.Gt[cq_tile(b, b) * 1024 + lane * 33];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (gi < p.N) tile(J)[lane * (CQ_LD + 1)] += p.shift_coef * s;
+    }
+  }
+  __syncthreads();
+  CQ_PROBE(1);
+  // every CTA's mbarriers are initialised before the first push
+  cq_arrive();
+  cq_wait();
+  if (J == 0 && warp == 0) {
+    cq_factor(tile(0), srow, p.Rt, p.flag);
+    cq_push(tile(0), 0, nb, Us, mbar, 0);
+  }
+  for (int K = 0; K < nb - 1; ++K) {
+    const int buf = K & 1;
+    if (J > K) {
+      // U_KK pushed by CTA K, then R(K, J)
+      mbar_wait_cluster(&mbar[buf], (uint32_t)((K >> 1) & 1));
+      CQ_PROBE(2 + 4 * K);
+      if (warp == 0) cq_rowsolve(tile(K), Us[buf], p.Rt + cq_tile(K, J) * 1024);
+      __syncthreads();
+      if (tid == 0 && K + 2 < J) mbar_arrive_expect_tx(&mbar[buf], CQ_PUSH_BYTES);
+    }
+    CQ_PROBE(3 + 4 * K);
+    cq_arrive();  // R(K, J) published
+    if (J == K + 1) {
+      // the next diagonal tile: its update is local; factor and push it
+      // while the other CTAs wait for the barrier
+      if (warp < 4)
+        cq_tile_update<1, 2>(tile(J), tile(K), false, 0, tile(K), warp >> 1, (warp & 1) * 2);
+      __syncthreads();
+      if (warp == 0) {
+        cq_factor(tile(J), srow, p.Rt + cq_tile(J, J) * 1024, p.flag);
+        cq_push(tile(J), J, nb, Us, mbar, (K + 1) & 1);
+      }
+    }
+    cq_wait();
+    CQ_PROBE(4 + 4 * K);
+    if (J > K + 1) {
+      // tiles (I, J), K < I <= J: T_I -= R(K, I)^T R(K, J), one warp each
+      for (int I = K + 1 + warp; I <= J; I += CQ_CHOL_NT / 32)
+        cq_tile_update<2, 4>(tile(I), tile(K), I != J, (uint32_t)I, tile(K), 0, 0);
+      __syncthreads();
+    }
+    CQ_PROBE(5 + 4 * K);
+  }
+  if (warp == 0) cq_diag_inverse(tile(J), p.Rinv + (int64_t)J * 1024);
+  CQ_PROBE(70);
+  // shared memory stays alive until every remote reader is done
+  cq_arrive();
+  cq_wait();
+}
+
+// ------------------------------------------------------------------ TRSM
+struct TrsmParams {
+  CqCols X;
+  int64_t N;
+  int nb;
+  const double* Rt;
+  const double* Rinv;
+  double* Q;
+  int64_t ldq;
+};
+
+// Q (rows r0 .. r0+15) = X R^{-1}: for each block column J,
+//   T = X_J - sum_{K<J} Q_K R(K, J)   (K split over the 4 warps)
+//   Q_J = T Rinv_JJ                    (warp w: 8 columns)
+__device__ __forceinline__ void cq_trsm_fetch_x(const TrsmParams& p, int J, int64_t r0,
+                                                double (&xv)[4], double (&bi)[8]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * 128;
+    const int r = e & 15, c = e >> 4;
+    const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
+    xv[q] = (gc < p.N && gr < p.X.d) ? __ldg(cq_col(p.X, gc) + gr) : 0.0;
+  }
+  const double* rinv = p.Rinv + (int64_t)J * 1024;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
+}
+
+__device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(rk + (nt * 8 + g) * 32 + ks * 4 + tq);
+}
+
+__global__ void __launch_bounds__(128) cqr_trsm_kernel(const TrsmParams p) {
+  extern __shared__ double qsm[];  // Qs[c * CQ_QLD + r], c < nb * 32
+  __shared__ double red[4][16 * 33];
+  __shared__ double Ts[16 * 33];
+  pdl_enter();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
+  const int64_t d = p.X.d;
+  double* Qs = qsm;
+  double xv[4], bi[8];
+  double bf[8][4], bn[8][4];
+  cq_trsm_fetch_x(p, 0, r0, xv, bi);
+  for (int J = 0; J < p.nb; ++J) {
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    // sum_{K < J, K = warp mod 4} Q_K R(K, J): the next tile's loads are in
+    // flight while the current one is multiplied (the first tile was
+    // fetched during the previous block column)
+    int K = warp;
+    while (K < J) {
+      const int Kn = K + 4;
+      if (Kn < J) cq_trsm_fetch_r(p.Rt + cq_tile(Kn, J) * 1024, bn);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = K * 32 + ks * 4 + tq;
+        const double a0 = Qs[k * CQ_QLD + g], a1 = Qs[k * CQ_QLD + g + 8];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], a0, a1, bf[ks][nt]);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = bn[ks][nt];
+      K = Kn;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+        red[warp][r * 33 + c] = acc[nt][h];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = threadIdx.x + q * 128;
+      const int r = e & 15, c = e >> 4;
+      const int o = r * 33 + c;
+      Ts[o] = xv[q] - (((red[0][o] + red[1][o]) + red[2][o]) + red[3][o]);
+    }
+    __syncthreads();
+    double qa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const double a0 = Ts[g * 33 + ks * 4 + tq], a1 = Ts[(g + 8) * 33 + ks * 4 + tq];
+      cq_dmma(qa, a0, a1, bi[ks]);
+    }
+    if (J + 1 < p.nb) {
+      cq_trsm_fetch_x(p, J + 1, r0, xv, bi);
+      if (warp < J + 1) cq_trsm_fetch_r(p.Rt + cq_tile(warp, J + 1) * 1024, bf);
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
+      const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
+      Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
+      if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------- solves
+// R = R2 R1 (upper, tile layout) and the inverses of its diagonal tiles
+// (R_II^{-1} = R1_II^{-1} R2_II^{-1}).  One CTA per upper tile, the K terms
+// of the tile product split over the 8 warps and folded in fixed order.
+struct ProdParams {
+  const double* R1t;
+  const double* R2t;
+  const double* R1inv;
+  const double* R2inv;
+  double* Rt;
+  double* Rinv;
+};
+
+// acc += A B for 32 x 32 global tiles (column-major, ld 32), one warp.
+__device__ __forceinline__ void cq_gtile_mma(double (&acc)[2][4][4], const double* A,
+                                             const double* B) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double af[8][2][2], bf[8][4];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) af[ks][mt][h] = __ldg(A + (ks * 4 + tq) * 32 + mt * 16 + h * 8 + g);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(B + (nt * 8 + g) * 32 + ks * 4 + tq);
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], af[ks][mt][0], af[ks][mt][1], bf[ks][nt]);
+}
+
+__global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p) {
+  __shared__ double red[4][1024];
+  pdl_enter();
+  const int t = blockIdx.x;
+  int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((J + 1) * (J + 2) / 2 <= t) ++J;
+  while (J * (J + 1) / 2 > t) --J;
+  const int I = t - J * (J + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double acc[2][4][4];
+  auto zero = [&]() {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][b2][c] = 0.0;
+  };
+  auto spill = [&](int w, bool add) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          double& r = red[w][(nt * 8 + 2 * tq + (h & 1)) * 32 + mt * 16 + g + (h >= 2 ? 8 : 0)];
+          r = add ? r + acc[mt][nt][h] : acc[mt][nt][h];
+        }
+  };
+  zero();
+  for (int K = I + warp; K <= J; K += 8)
+    cq_gtile_mma(acc, p.R2t + cq_tile(I, K) * 1024, p.R1t + cq_tile(K, J) * 1024);
+  // fixed-order fold of the 8 warps' partial tiles: (w + 4) into w, then 0..3
+  if (warp >= 4) spill(warp - 4, false);
+  __syncthreads();
+  if (warp < 4) spill(warp, true);
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1024; e += 256)
+    p.Rt[(int64_t)t * 1024 + e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+  if (I == J) {
+    __syncthreads();
+    if (warp == 0) {
+      zero();
+      cq_gtile_mma(acc, p.R1inv + (int64_t)I * 1024, p.R2inv + (int64_t)I * 1024);
+      spill(0, false);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += 256) p.Rinv[(int64_t)I * 1024 + e] = red[0][e];
+  }
+}
+
+struct SolveParams {
+  const double* G1t;   // Gram of M (unshifted): ||SA||_F from its diagonal
+  const double* Rt;    // R = R2 R1, upper tiles (order N = n + 1)
+  const double* Rinv;  // inverses of its diagonal tiles
+  int64_t n;           // R[:n,:n]; column n = Q^T Sb
+  const int* flag;
+  double* x;
+  const double* g;     // SA^T r (solve_b input)
+  int64_t* bad_col;
+  double* bad_val;
+};
+
+constexpr int CQ_SOLVE_ROWS = 512;             // one thread per row (n <= 511)
+constexpr int CQ_SOLVE_NT = CQ_SOLVE_ROWS + 32;  // + the diagonal-block warp
+
+__device__ __forceinline__ double cq_rt(const double* Rt, int64_t i, int64_t j) {
+  return Rt[cq_tile((int)(i >> 5), (int)(j >> 5)) * 1024 + (j & 31) * 32 + (i & 31)];
+}
+
+// y <- R[:n,:n]^{-1} y, one CTA, y in shared memory.  Diagonal blocks from
+// the bottom: x_b = Rinv_bb y_b (the extra warp), then every row above
+// subtracts R[i, block b] x_b.  The block's R values (thread = row) and
+// Rinv_bb (extra warp) are loaded one block ahead, so only the products and
+// two barriers per block stay on the dependent chain.
+__device__ __forceinline__ void cq_bs_fetch(const double* Rt, const double* Rinv, int b,
+                                            double (&c)[32]) {
+  const int tid = threadIdx.x;
+  const int64_t lo = (int64_t)b * 32;
+  if (tid < lo) {
+    const double* rc = Rt + cq_tile(tid >> 5, b) * 1024 + (tid & 31);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) c[j] = __ldg(rc + j * 32);
+  } else if (tid >= CQ_SOLVE_ROWS) {  // Rinv_bb row `lane`
+    const double* rb = Rinv + (int64_t)b * 1024 + (tid & 31);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) c[j] = __ldg(rb + j * 32);
+  }
+}
+
+__device__ void cq_backsolve(const double* Rt, const double* Rinv, int64_t n, double* ys,
+                             double* xb) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nbn = (int)((n + 31) / 32);
+  double c[32];
+  cq_bs_fetch(Rt, Rinv, nbn - 1, c);
+  for (int b = nbn - 1; b >= 0; --b) {
+    const int64_t lo = (int64_t)b * 32;
+    const int w = (int)min((int64_t)32, n - lo);
+    if (tid >= CQ_SOLVE_ROWS) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        a0 = fma(c[j], j < w ? ys[lo + j] : 0.0, a0);
+        a1 = fma(c[j + 1], j + 1 < w ? ys[lo + j + 1] : 0.0, a1);
+      }
+      const double xv = lane < w ? a0 + a1 : 0.0;
+      xb[lane] = xv;
+      if (lane < w) ys[lo + lane] = xv;
+    }
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0;
+    const bool mine = tid < lo;
+    if (mine) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        t0 = fma(c[j], xb[j], t0);
+        t1 = fma(c[j + 1], xb[j + 1], t1);
+      }
+    }
+    if (b > 0) cq_bs_fetch(Rt, Rinv, b - 1, c);
+    if (mine) ys[tid] -= t0 + t1;
+    __syncthreads();
+  }
+}
+
+// y <- R[:n,:n]^{-T} y (forward substitution with R^T), same storage: row i
+// below block b subtracts sum_j R[lo + j][i] z_j (its 32 contiguous values
+// of tile (b, i>>5)); the extra warp applies (Rinv_bb)^T.
+__device__ __forceinline__ void cq_fs_fetch(const double* Rt, const double* Rinv, int b,
+                                            int64_t n, double (&c)[32]) {
+  const int tid = threadIdx.x;
+  const double2* src = nullptr;
+  if (tid >= (int64_t)b * 32 + 32 && tid < n && tid < CQ_SOLVE_ROWS)
+    src = reinterpret_cast<const double2*>(Rt + cq_tile(b, tid >> 5) * 1024 + (tid & 31) * 32);
+  else if (tid >= CQ_SOLVE_ROWS)  // (Rinv^T)[lane][j] = Rinv[j][lane]
+    src = reinterpret_cast<const double2*>(Rinv + (int64_t)b * 1024 + (tid & 31) * 32);
+  if (src) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double2 v = __ldg(src + j);
+      c[2 * j] = v.x;
+      c[2 * j + 1] = v.y;
+    }
+  }
+}
+
+__device__ void cq_fwdsolve_t(const double* Rt, const double* Rinv, int64_t n, double* ys,
+                              double* zb) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nbn = (int)((n + 31) / 32);
+  double c[32];
+  cq_fs_fetch(Rt, Rinv, 0, n, c);
+  for (int b = 0; b < nbn; ++b) {
+    const int64_t lo = (int64_t)b * 32;
+    const int w = (int)min((int64_t)32, n - lo);
+    if (tid >= CQ_SOLVE_ROWS) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        a0 = fma(c[j], j < w ? ys[lo + j] : 0.0, a0);
+        a1 = fma(c[j + 1], j + 1 < w ? ys[lo + j + 1] : 0.0, a1);
+      }
+      const double zv = lane < w ? a0 + a1 : 0.0;
+      zb[lane] = zv;
+      if (lane < w) ys[lo + lane] = zv;
+    }
+    __syncthreads();
+    const bool mine = tid >= lo + 32 && tid < n && tid < CQ_SOLVE_ROWS;
+    double t0 = 0.0, t1 = 0.0;
+    if (mine) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        t0 = fma(c[j], zb[j], t0);
+        t1 = fma(c[j + 1], zb[j + 1], t1);
+      }
+    }
+    if (b + 1 < nbn) cq_fs_fetch(Rt, Rinv, b + 1, n, c);
+    if (mine) ys[tid] -= t0 + t1;
+    __syncthreads();
+  }
+}
+
+// Rank check (diag R vs 1e-14 ||SA||_F), y = R[:n, n], x = R[:n,:n]^{-1} y.
+__global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolveParams p) {
+  __shared__ double ys[CQ_SOLVE_ROWS];
+  __shared__ double xb[32];
+  __shared__ double red[CQ_SOLVE_NT / 32];
+  __shared__ unsigned long long first_bad;
+  pdl_enter();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = p.n;
+  double s = tid < n ? cq_rt(p.G1t, tid, tid) : 0.0;
+  const double dg = tid < n ? cq_rt(p.Rt, tid, tid) : 1.0;
+  if (tid < n) ys[tid] = cq_rt(p.Rt, tid, n);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  if (tid == 0) first_bad = ~0ull;
+  __syncthreads();
+  double fro2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) fro2 += red[w];
+  const double fro = sqrt(fro2);
+  if (tid < n && (!(fro > 0.0) || !(dg >= CQ_RANK_TOL * fro)))
+    atomicMin(&first_bad, (unsigned long long)tid);
+  __syncthreads();
+  if (tid == 0) {
+    const bool broke = *p.flag != 0;
+    const long long fb = first_bad == ~0ull ? -1 : (long long)first_bad;
+    *p.bad_col = broke ? -2 : fb;
+    *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
+  }
+  cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
+  if (tid < n) p.x[tid] = ys[tid];
+}
+
+// x += R^{-1} R^{-T} g
+__global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
+  __shared__ double ys[CQ_SOLVE_ROWS];
+  __shared__ double xb[32];
+  pdl_enter();
+  const int64_t n = p.n;
+  const int tid = threadIdx.x;
+  if (tid < n) ys[tid] = p.g[tid];
+  __syncthreads();
+  cq_fwdsolve_t(p.Rt, p.Rinv, n, ys, xb);
+  cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
+  if (tid < n) p.x[tid] += ys[tid];
+}
+
+// r = b - A x, rows split over CTAs: 64 rows x 4 column quarters per CTA.
+__global__ void __launch_bounds__(256) cqr_resid_kernel(const double* A, int64_t lda,
+                                                        const double* b, int64_t d, int64_t n,
+                                                        const double* x, double* r) {
+  extern __shared__ double xs[];  // n
+  __shared__ double part[4][64];
+  pdl_enter();
+  for (int64_t c = threadIdx.x; c < n; c += 256) xs[c] = x[c];
+  __syncthreads();
+  const int rl = threadIdx.x & 63, qc = threadIdx.x >> 6;
+  const int64_t i = (int64_t)blockIdx.x * 64 + rl;
+  const int64_t c0 = n * qc / 4, c1 = n * (qc + 1) / 4;
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+  if (i < d) {
+    int64_t c = c0;
+    for (; c + 3 < c1; c += 4) {
+      t0 = fma(A[c * lda + i], xs[c], t0);
+      t1 = fma(A[(c + 1) * lda + i], xs[c + 1], t1);
+      t2 = fma(A[(c + 2) * lda + i], xs[c + 2], t2);
+      t3 = fma(A[(c + 3) * lda + i], xs[c + 3], t3);
+    }
+    for (; c < c1; ++c) t0 = fma(A[c * lda + i], xs[c], t0);
+  }
+  part[qc][rl] = (t0 + t1) + (t2 + t3);
+  __syncthreads();
+  if (qc == 0 && i < d) r[i] = b[i] - (((part[0][rl] + part[1][rl]) + part[2][rl]) + part[3][rl]);
+}
+
+// g = A^T r, one warp per column (fixed shuffle tree).
+__global__ void __launch_bounds__(256) cqr_gemv_t_kernel(const double* A, int64_t lda, int64_t d,
+                                                         int64_t n, const double* r, double* g) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const double* col = A + c * lda;
+  double t0 = 0.0, t1 = 0.0;
+  int64_t i = lane;
+  for (; i + 32 < d; i += 64) {
+    t0 = fma(col[i], r[i], t0);
+    t1 = fma(col[i + 32], r[i + 32], t1);
+  }
+  if (i < d) t0 = fma(col[i], r[i], t0);
+  double t = t0 + t1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) g[c] = t;
+}
+
+}  // namespace skl
+
+using namespace skl;
+
+namespace {
+
+struct CqWork {
+  size_t bytes = 0;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi;
+};
+
+CqWork cq_layout(int64_t d, int64_t N, int nb, int S) {
+  CqWork w;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    const size_t o = off;
+    off += (b + 255) / 256 * 256;
+    return o;
+  };
+  const size_t nt = (size_t)nb * (nb + 1) / 2;
+  const int64_t ldq = (d + 1) / 2 * 2;
+  w.oG1 = take(nt * 1024 * 8);
+  w.oG2 = take(nt * 1024 * 8);
+  w.oPart = take((size_t)S * nt * 1024 * 8);
+  w.oCnt = take(nt * 4);
+  w.oR1 = take(nt * 1024 * 8);
+  w.oR2 = take(nt * 1024 * 8);
+  w.oI1 = take((size_t)nb * 1024 * 8);
+  w.oI2 = take((size_t)nb * 1024 * 8);
+  w.oQ = take((size_t)ldq * N * 8);
+  w.oFlag = take(4);
+  w.oR = take((size_t)d * 8);
+  w.oG = take((size_t)N * 8);
+  w.oBad = take(8);
+  w.oBadV = take(8);
+  w.oRt = take(nt * 1024 * 8);
+  w.oRi = take((size_t)nb * 1024 * 8);
+  w.bytes = off;
+  return w;
+}
+
+// Row slices of the Gram: about two CTAs per SM over the upper tiles, at
+// least four 16-row chunks (one per warp) per slice.
+int cq_slices(int64_t d, int nt) {
+  const int64_t nchunk = (d + 15) / 16;
+  const int sms = sm_count_cached();
+  const int64_t s = std::min<int64_t>((2 * sms + nt - 1) / nt, nchunk / 4);
+  return (int)std::min<int64_t>(64, std::max<int64_t>(1, s));
+}
+
+int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsigned* cnt,
+            bool pdl, cudaStream_t st) {
+  const int nt = nb * (nb + 1) / 2;
+  const int64_t nchunk = (X.d + 15) / 16;
+  const int S = cq_slices(X.d, nt);
+  const bool vec = ((uintptr_t)X.A % 16 == 0) && (X.lda % 2 == 0) &&
+                   (X.b == nullptr || (uintptr_t)X.b % 16 == 0);
+  GramParams gp{X, N, nb, S, nchunk, vec ? 1 : 0, part, Gt, cnt};
+  SKL_CUDA(launch_k(cqr_gram_kernel, dim3((unsigned)nt, (unsigned)S), dim3(128), 0, st, pdl, gp));
+  return SKL_OK;
+}
+
+int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
+            int* flag, bool pdl, cudaStream_t st) {
+  static std::once_flag attr_set[64];
+  const size_t smem_max = ((size_t)CQ_MAXNB * CQ_TILE + 32) * sizeof(double);
+  const int arc = once_per_device(attr_set, [&]() -> int {
+    SKL_CUDA(cudaFuncSetAttribute(cqr_chol_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SKL_CUDA(cudaFuncSetAttribute(cqr_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_max));
+    return SKL_OK;
+  });
+  if (arc) return arc;
+  CholParams cp{Gt, nb, N, shift_coef, Rt, Rinv, flag};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3(CQ_CHOL_NT);
+  cfg.dynamicSmemBytes = ((size_t)nb * CQ_TILE + 32) * sizeof(double);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)nb;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
+  SKL_CUDA(cudaLaunchKernelEx(&cfg, cqr_chol_kernel, cp));
+  return SKL_OK;
+}
+
+int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* Rinv, double* Q,
+            int64_t ldq, bool pdl, cudaStream_t st) {
+  static std::once_flag attr_set[64];
+  const size_t smem_max = (size_t)CQ_MAXNB * 32 * CQ_QLD * sizeof(double);
+  const int arc = once_per_device(attr_set, [&]() -> int {
+    SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_max));
+    return SKL_OK;
+  });
+  if (arc) return arc;
+  TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq};
+  const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
+  SKL_CUDA(launch_k(cqr_trsm_kernel, dim3(grid), dim3(128), (size_t)nb * 32 * CQ_QLD * sizeof(double),
+                    st, pdl, tp));
+  return SKL_OK;
+}
+
+}  // namespace
+
+// Sizes the CholeskyQR path covers: N = n + 1 <= 512 and at least one row
+// more than N (a square augmented system is rank deficient by construction).
+extern "C" int skl_cqr_supported(int64_t d, int64_t n) {
+  const int64_t N = n + 1;
+  return (n >= 1 && N <= 32 * CQ_MAXNB && d > N) ? 1 : 0;
+}
+
+// Enqueue the CholeskyQR2 solve; *bad_col (pinned host or device) receives
+// -1, the first rank-deficient column, or -2 when a Cholesky pivot broke
+// down (then the caller re-solves with skl_qr_solve).
+extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t d,
+                                   int64_t n, double* x, int64_t* bad_col, double* bad_val,
+                                   void* stream) {
+  clear_error();
+  cudaStream_t st = (cudaStream_t)stream;
+  SKL_REQUIRE(SA && Sb && x && bad_col && bad_val && ldsa >= d, SKL_ERR_INVALID,
+              "cqr_solve: bad arguments");
+  SKL_REQUIRE(skl_cqr_supported(d, n), SKL_ERR_SPEC,
+              "cqr_solve: %lld x %lld outside the CholeskyQR path (n + 1 <= 512 < d)",
+              (long long)d, (long long)n);
+  const int64_t N = n + 1;
+  const int nb = (int)((N + 31) / 32);
+  const int nt = nb * (nb + 1) / 2;
+  const int S = cq_slices(d, nt);
+  const CqWork w = cq_layout(d, N, nb, S);
+  const int64_t ldq = (d + 1) / 2 * 2;
+  unsigned char* ws = nullptr;
+  SKL_CUDA(malloc_async(&ws, w.bytes, st));
+  auto P = [&](size_t o) { return (void*)(ws + o); };
+  double* G1 = (double*)P(w.oG1);
+  double* G2 = (double*)P(w.oG2);
+  double* part = (double*)P(w.oPart);
+  unsigned* cnt = (unsigned*)P(w.oCnt);
+  double* R1 = (double*)P(w.oR1);
+  double* R2 = (double*)P(w.oR2);
+  double* I1 = (double*)P(w.oI1);
+  double* I2 = (double*)P(w.oI2);
+  double* Q = (double*)P(w.oQ);
+  int* flag = (int*)P(w.oFlag);
+  double* r = (double*)P(w.oR);
+  double* g = (double*)P(w.oG);
+  int rc = SKL_OK;
+  do {
+    cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nt * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 4, st);
+    if (e != cudaSuccess) {
+      set_error("cqr_solve: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    const CqCols M{SA, ldsa, Sb, n, d};
+    const CqCols Q1{Q, ldq, nullptr, N, d};
+    const double u = 0.5 * 2.220446049250313e-16;
+    const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * u;
+    if ((rc = cq_gram(M, N, nb, part, G1, cnt, false, st))) break;
+    if ((rc = cq_chol(G1, nb, N, shift, R1, I1, flag, true, st))) break;
+    if ((rc = cq_trsm(M, N, nb, R1, I1, Q, ldq, true, st))) break;
+    if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st))) break;
+    if ((rc = cq_chol(G2, nb, N, 0.0, R2, I2, flag, true, st))) break;
+    double* Rt = (double*)P(w.oRt);
+    double* Ri = (double*)P(w.oRi);
+    ProdParams pp{R1, R2, I1, I2, Rt, Ri};
+    SolveParams sp{G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad), (double*)P(w.oBadV)};
+    const size_t ysm = (size_t)N * sizeof(double);
+#define CQ_LAUNCH(call)                                                          \
+  if ((e = (call)) != cudaSuccess) {                                             \
+    set_error("cqr_solve: kernel launch failed: %s", cudaGetErrorString(e));     \
+    rc = SKL_ERR_CUDA;                                                           \
+    break;                                                                       \
+  }
+    CQ_LAUNCH(launch_k(cqr_rprod_kernel, dim3((unsigned)nt), dim3(256), 0, st, true, pp));
+    CQ_LAUNCH(launch_k(cqr_solve_a_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
+    // corrected semi-normal step: r = Sb - SA x, g = SA^T r, x += R^{-1} R^{-T} g
+    CQ_LAUNCH(launch_k(cqr_resid_kernel, dim3((unsigned)((d + 63) / 64)), dim3(256), ysm, st, true,
+                       SA, ldsa, Sb, d, n, (const double*)x, r));
+    CQ_LAUNCH(launch_k(cqr_gemv_t_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true,
+                       SA, ldsa, d, n, (const double*)r, g));
+    CQ_LAUNCH(launch_k(cqr_solve_b_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
+#undef CQ_LAUNCH
+    e = cudaMemcpyAsync(bad_col, P(w.oBad), 8, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad_val, P(w.oBadV), 8, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) {
+      set_error("cqr_solve: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+    }
+  } while (0);
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+#ifdef SKL_CQR_PROBE
+// Copy the Cholesky probe timestamps ([2][16][72] ns) to host memory.
+extern "C" int skl_cqr_probe_dump(long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_cqr_probe, sizeof(g_cqr_probe)) == cudaSuccess ? 0 : 7;
+}
+#endif

@@ -15,6 +15,7 @@ kernels that consume it.
 from __future__ import annotations
 
 import math
+import os
 import threading
 
 from dataclasses import dataclass
@@ -284,11 +285,26 @@ def qr_solve_device(SA, ldsa: int, Sb, d: int, n: int, want_q: bool = False,
 _RANK_FLAGS = threading.local()
 
 
+def cholqr_enabled(d: int, n: int) -> bool:
+    """Whether the reduced solve of a d x n sketched system takes the
+    CholeskyQR2 path (skl_cqr_solve_async): n + 1 <= 512 < d, unless
+    SKL_QR_HOUSEHOLDER=1 forces the Householder factorisation (A/B knob)."""
+    if os.environ.get("SKL_QR_HOUSEHOLDER", "") not in ("", "0"):
+        return False
+    return bool(_native.lib().skl_cqr_supported(d, n))
+
+
 def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):
-    """qr_solve_device without its synchronisation: returns (x, check) where
-    check() -- to be called once the stream has been synchronised (e.g. by
-    the residual pass) -- raises the same SingularFactorError skl_qr_solve
-    would have.  The rank flag lands in a pinned per-thread buffer."""
+    """The reduced solve x = R^{-1} Q^T Sb without its synchronisation:
+    returns (x, check) where check() -- to be called once the stream has
+    been synchronised (e.g. by the residual pass) -- returns None when x is
+    valid, or a replacement x, or raises the SingularFactorError
+    skl_qr_solve would have.  Sketched systems with n + 1 <= 512 < d go
+    through the CholeskyQR2 kernels (csrc/skl_cholqr.cu); when one of their
+    Cholesky pivots breaks down or their rank check fires, check() re-solves
+    with the Householder factorisation, which decides (and words the error
+    exactly as linalg.py:186-191).  The flags land in a pinned per-thread
+    buffer."""
     flags = getattr(_RANK_FLAGS, "buf", None)
     if flags is None:
         flags = torch.empty(2, dtype=torch.float64, pin_memory=True)
@@ -296,19 +312,36 @@ def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):
     flags_i = flags.view(torch.int64)
     x = device_f64((n,))
     base = flags.data_ptr()
-    _native.call(
-        "skl_qr_solve_async", _native.ptr(SA), ldsa, _native.ptr(Sb), d, n, _native.ptr(x),
-        None, n, None, d, base, base + 8, current_stream())
+    chol = Sb is not None and cholqr_enabled(d, n)
+    if chol:
+        _native.call("skl_cqr_solve_async", _native.ptr(SA), ldsa, _native.ptr(Sb), d, n,
+                     _native.ptr(x), base, base + 8, current_stream())
+    else:
+        _native.call(
+            "skl_qr_solve_async", _native.ptr(SA), ldsa, _native.ptr(Sb), d, n, _native.ptr(x),
+            None, n, None, d, base, base + 8, current_stream())
 
-    def check() -> None:
+    def check():
         bad = int(flags_i[0])
+        if chol and bad != -1:
+            return qr_solve_device(SA, ldsa, Sb, d, n)[0]
         if bad >= 0:
             val = float(flags[1])
             raise SingularFactorError(
                 f"input is numerically rank deficient at column {bad} "
                 f"(|R[{bad},{bad}]| = {val:.3e})")
+        return None
 
     return x, check
+
+
+def reduced_solve_device(SA, ldsa: int, Sb, d: int, n: int):
+    """x of the sketched system through the path sketch_and_apply takes
+    (CholeskyQR2 when eligible, else Householder), synchronised."""
+    x, check = qr_solve_device_async(SA, ldsa, Sb, d, n)
+    torch.cuda.current_stream().synchronize()
+    x2 = check()
+    return x if x2 is None else x2
 
 
 def economy_qr(M: DenseMatrix) -> QRFactors:

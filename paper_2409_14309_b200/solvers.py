@@ -192,11 +192,14 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
     ev1.record()
     rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
     try:
-        rank_check()
+        x_fix = rank_check()
     except SingularFactorError as exc:
         raise SingularFactorError(
             f"sketched matrix ({op_spec.kind}, d={d}) is rank deficient: {exc}; "
             f"a larger embedding dimension may help") from exc
+    if x_fix is not None:  # the CholeskyQR path handed over to Householder
+        x_dev = x_fix
+        rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
     wall = ev0.elapsed_time(ev1) * 1e-3
     x = x_dev if (isinstance(A, DenseMatrix) and A.on_device) else x_dev.cpu().numpy()
     return SolveResult(x=Vector._of_solution(x, rnorm), method="saa", sketch=op_spec.kind, d=d,

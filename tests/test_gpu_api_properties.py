@@ -237,7 +237,18 @@ def test_sap_cold_start_converges():
                                     E.SolverOptions(warm_start=False))
     assert res.termination == "atol_btol"
     assert rel_err(res.x.data, prob.x_star.data) <= 1e-6
-    assert res.iterations == REF_ITERS["sap_cold"]
+    # this problem stops right at the atol/btol boundary (final residual
+    # 1e-8 = beta): generate_problem's device QR rounds differently from the
+    # reference's numpy QR, so the reference's count is pinned to within one
+    # iteration, and the oracle run on this very (device-generated) problem
+    # must stop within one iteration of the device run
+    assert abs(res.iterations - REF_ITERS["sap_cold"]) <= 1
+    from oracle import oracle as O
+
+    A_h, b_h = host(prob.A.data), host(prob.b.data)
+    want = O.sap_solve(A_h, b_h, "countsketch", 537, 4.0, warm_start=False)
+    assert want["termination"] == "atol_btol"
+    assert abs(res.iterations - want["iterations"]) <= 1
 
 
 def test_sap_csr_operand_matches_dense():

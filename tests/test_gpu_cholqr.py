@@ -1,0 +1,122 @@
+"""The CholeskyQR2 reduced solve (csrc/skl_cholqr.cu) against the oracle's
+Householder solve (numpy QR + solve_triangular, solvers.py:309 /
+linalg.py:166-192, 214-218): x to rounding on well-conditioned systems, the
+same sketched-residual minimiser on ill-conditioned ones, the Householder
+hand-over (and the reference's error) on rank-deficient ones, determinism,
+and every tile-boundary shape of the augmented order N = n + 1."""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2409_14309_b200.errors import SingularFactorError  # noqa: E402
+from paper_2409_14309_b200.linalg import (cholqr_enabled, qr_solve_device,  # noqa: E402
+                                          qr_solve_device_async, reduced_solve_device)
+
+
+def oracle_x(SA, Sb):
+    q, r = np.linalg.qr(SA)
+    return scipy.linalg.solve_triangular(r, q.T @ Sb, lower=False, check_finite=False)
+
+
+def system(d, n, kappa=10.0, seed=0):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((d, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.logspace(0, -np.log10(kappa), n)
+    SA = np.asfortranarray((U * s) @ V.T)
+    Sb = SA @ rng.standard_normal(n) + 1e-3 * rng.standard_normal(d)
+    return SA, Sb
+
+
+def cqr(SA, Sb, ld=None):
+    d, n = SA.shape
+    if ld is None:
+        t = torch.from_numpy(np.asfortranarray(SA)).cuda()
+        t = t.t().contiguous().t()
+        ld = d
+    else:  # column-major with a padded leading dimension (odd: scalar loads)
+        buf = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+        buf[:, :d] = torch.from_numpy(np.ascontiguousarray(SA.T)).cuda()
+        t = buf.t()
+    b = torch.from_numpy(Sb).cuda()
+    x, check = qr_solve_device_async(t, ld, b, d, n)
+    torch.cuda.synchronize()
+    x2 = check()
+    return (x if x2 is None else x2).cpu().numpy(), x2 is not None
+
+
+SHAPES = [(100, 5), (200, 30), (200, 31), (300, 32), (300, 63), (400, 64), (800, 200),
+          (2048, 256), (1500, 300), (2048, 511)]
+
+
+@pytest.mark.parametrize("d,n", SHAPES)
+def test_cholqr_matches_householder_oracle(d, n):
+    assert cholqr_enabled(d, n)
+    SA, Sb = system(d, n, kappa=10.0, seed=d + n)
+    x, fell_back = cqr(SA, Sb)
+    assert not fell_back
+    want = oracle_x(SA, Sb)
+    assert np.linalg.norm(x - want) / np.linalg.norm(want) <= 1e-13
+
+
+def test_cholqr_odd_leading_dimension_and_unaligned_rows():
+    SA, Sb = system(1001, 100, kappa=100.0, seed=3)
+    x, fell_back = cqr(SA, Sb, ld=1003)
+    assert not fell_back
+    want = oracle_x(SA, Sb)
+    assert np.linalg.norm(x - want) / np.linalg.norm(want) <= 1e-13
+
+
+@pytest.mark.parametrize("kappa", [1e4, 1e8, 1e12])
+def test_cholqr_ill_conditioned_minimises_the_sketched_residual(kappa):
+    d, n = 2048, 256
+    SA, Sb = system(d, n, kappa=kappa, seed=11)
+    x, fell_back = cqr(SA, Sb)
+    assert not fell_back
+    want = oracle_x(SA, Sb)
+    rs, rw = np.linalg.norm(SA @ x - Sb), np.linalg.norm(SA @ want - Sb)
+    assert rs <= rw * (1 + 1e-10)  # as good a minimiser as LAPACK's (or better)
+    # forward error at the level of kappa * u, as two Householder QRs differ
+    assert np.linalg.norm(x - want) / np.linalg.norm(want) <= 50 * kappa * 1.1e-16
+
+
+def test_cholqr_rank_deficient_hands_over_to_householder():
+    SA, Sb = system(500, 40, seed=5)
+    SA[:, 7] = SA[:, 3]
+    with pytest.raises(SingularFactorError, match="rank deficient at column 7"):
+        cqr(SA, Sb)
+
+
+def test_cholqr_is_deterministic():
+    SA, Sb = system(2048, 256, kappa=1e8, seed=9)
+    a, _ = cqr(SA, Sb)
+    for _ in range(3):
+        b, _ = cqr(SA, Sb)
+        assert np.array_equal(a, b)
+
+
+def test_reduced_solve_paths_agree():
+    SA, Sb = system(800, 200, seed=2)
+    t = torch.from_numpy(SA).cuda().t().contiguous().t()
+    b = torch.from_numpy(Sb).cuda()
+    x_c = reduced_solve_device(t, 800, b, 800, 200).cpu().numpy()
+    x_h = qr_solve_device(t, 800, b, 800, 200)[0].cpu().numpy()
+    assert np.linalg.norm(x_c - x_h) / np.linalg.norm(x_h) <= 1e-13
+
+
+def test_cholqr_not_used_outside_its_sizes():
+    assert not cholqr_enabled(512, 511)   # N = 512 = d: square augmented system
+    assert not cholqr_enabled(4096, 512)  # N = 513 > 512
+    assert cholqr_enabled(4096, 511)

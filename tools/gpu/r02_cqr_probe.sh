@@ -1,0 +1,6 @@
+set -x
+timeout 300 python -m pytest tests/test_gpu_cholqr.py -x -q 2>&1 | tail -3
+timeout 200 python tools/time_cholqr.py 2048x256 800x200 2>&1 | tail -3
+export SKL_NVCC_DEFINES=-DSKL_CQR_PROBE
+python -c "from paper_2409_14309_b200 import _build; _build.build(force=True)" 2>&1 | tail -2
+timeout 120 python tools/probe_cholqr.py 2048x256

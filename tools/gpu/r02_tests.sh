@@ -1,0 +1,4 @@
+# all GPU tests without -x (full-size included), parity report
+set -x
+mkdir -p gpurun_out
+SKL_PARITY_REPORT=gpurun_out/r02_parity_fullsize.jsonl timeout 2400 python -m pytest tests -m gpu -q -rf 2>&1 | tail -25
