@@ -68,6 +68,12 @@ constexpr int CQ_CHOL_NT = 256;
 constexpr int CQ_TRSM_ROWS = 16;
 constexpr int CQ_QLD = 20;                // row stride of the TRSM's Q block (conflict-free frags)
 constexpr double CQ_RANK_TOL = 1e-14;     // linalg.py RANK_TOL
+// Above this ratio of R's largest to smallest diagonal entry (a lower bound
+// of kappa(SA), 25-40x below it on log-spaced spectra) the corrected
+// semi-normal step is no longer reliable (it needs kappa^2 u well below 1):
+// the solve hands over to Householder.  Config 2 (kappa = 1e8) sits at
+// 4.3e6.
+constexpr double CQ_DIAG_RATIO_MAX = 2e7;
 
 __host__ __device__ __forceinline__ int64_t cq_tile(int I, int J) {
   return (int64_t)J * (J + 1) / 2 + I;
@@ -138,129 +144,153 @@ __device__ __forceinline__ long long cq_now() {
 struct GramParams {
   CqCols X;
   int64_t N;
-  int nb;
-  int S;              // row slices
-  int64_t nchunk;     // 16-row chunks of d
-  int vec;            // columns 16-byte aligned: 32-byte vector loads
-  double* part;       // [S][ntiles][1024] (S > 1)
+  uint32_t nchunk;    // 16-row chunks of d
+  uint32_t U;         // work units: upper tiles x chunks, tile-major (U * P < 2^32)
+  uint32_t P;         // CTAs (<= U): CTA c takes units [U c / P, U (c + 1) / P)
+  int SEG;            // partial slots per CTA (>= tiles any CTA touches)
+  double* part;       // [P][SEG][1024]
   double* Gt;         // [ntiles][1024]
   unsigned* cnt;      // [ntiles], zero on entry, left zero
 };
 
+__device__ __forceinline__ uint32_t cq_unit_lo(const GramParams& p, uint32_t c) { return p.U * c / p.P; }
+
+__device__ __forceinline__ void cq_tile_ij(int t, int& I, int& J) {
+  J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((J + 1) * (J + 2) / 2 <= t) ++J;
+  while (J * (J + 1) / 2 > t) --J;
+  I = t - J * (J + 1) / 2;
+}
+
+// Rows k .. k+3 of the lane's 8 columns (4 of block I, 4 of block J).
+template <bool VEC>
+__device__ __forceinline__ void cq_gram_load(const double* const (&pc)[8], int64_t k, int64_t d,
+                                             bool ragged, double (&v)[8][4]) {
+  if (VEC && !ragged) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(pc[q] + k));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(pc[q] + k + 2));
+      v[q][0] = x0.x; v[q][1] = x0.y; v[q][2] = x1.x; v[q][3] = x1.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[q][j] = (k + j < d) ? __ldg(pc[q] + k + j) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void cq_gram_mma(double (&acc)[2][4][4], const double (&v)[8][4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], v[mt * 2][j], v[mt * 2 + 1][j], v[4 + nt][j]);
+}
+
+// G = X^T X on the fp64 tensor cores, stream-K: one wave of CTAs, each
+// taking an equal contiguous range of (upper tile, 16-row chunk) units, so
+// the load is balanced to a chunk whatever the tile count.  Within a tile
+// segment the 4 warps split the chunks round-robin (each owns the whole
+// 32 x 32 tile: 2 x 4 m16n8k4 fragments; lane (g, tq) reads rows
+// k0 + 4 tq .. + 3 of its 8 columns with 32-byte vector loads, two chunks in
+// flight in ping-pong registers; MMA step j takes k = k0 + 4 tq + j, the
+// same permutation of k for both operands).  Columns past N read column
+// N - 1 instead (the Cholesky ignores those Gram entries).  Every segment
+// leaves a partial tile; the last CTA to finish a tile folds the partials
+// of the CTAs that cover it in CTA order (deterministic).
+template <bool VEC>
 __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
   pdl_enter();
   __shared__ double red[4][1024];
   __shared__ int is_last;
-  const int t = blockIdx.x, s = blockIdx.y;
-  int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-  while ((int64_t)(J + 1) * (J + 2) / 2 <= t) ++J;
-  while ((int64_t)J * (J + 1) / 2 > t) --J;
-  const int I = t - J * (J + 1) / 2;
+  const uint32_t c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t c_beg = p.nchunk * s / p.S, c_end = p.nchunk * (s + 1) / p.S;
   const int64_t d = p.X.d;
-
-  const double* pa[4];
-  const double* pb[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t ca = (int64_t)I * 32 + (q >> 1) * 16 + (q & 1) * 8 + g;
-    pa[q] = ca < p.N ? cq_col(p.X, ca) : nullptr;
-    const int64_t cb = (int64_t)J * 32 + q * 8 + g;
-    pb[q] = cb < p.N ? cq_col(p.X, cb) : nullptr;
-  }
-  double acc[2][4][4];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-
-  // 16-row chunk k0: lane (g, tq) holds rows k0 + 4 tq .. + 3 of its columns;
-  // MMA step j takes k = k0 + 4 tq + j (the same permutation of k for both
-  // operands, so the product is unchanged)
-  auto load4 = [&](const double* col, int64_t k, double (&v)[4]) {
-    if (col == nullptr) {
-      v[0] = v[1] = v[2] = v[3] = 0.0;
-    } else if (p.vec && k + 3 < d) {
-      const double2 x0 = __ldg(reinterpret_cast<const double2*>(col + k));
-      const double2 x1 = __ldg(reinterpret_cast<const double2*>(col + k + 2));
-      v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = (k + j < d) ? __ldg(col + k + j) : 0.0;
-    }
-  };
-  // chunks ch = c_beg + warp (+4 ...): the next chunk's loads are in flight
-  // while the current one is multiplied
-  double av[4][4], bv[4][4], an[4][4], bn[4][4];
-  int64_t ch = c_beg + warp;
-  if (ch < c_end) {
+  const uint32_t last_chunk = (d % 16) ? p.nchunk - 1 : 0xffffffffu;  // ragged: bounds checks
+  const uint32_t u0 = cq_unit_lo(p, c), u1 = cq_unit_lo(p, c + 1);
+  const int t_first = (int)(u0 / p.nchunk);
+  for (uint32_t ua = u0; ua < u1;) {
+    const int t = (int)(ua / p.nchunk);
+    const uint32_t tbase = (uint32_t)t * p.nchunk;
+    const uint32_t ub = min(u1, tbase + p.nchunk);
+    int I, J;
+    cq_tile_ij(t, I, J);
+    const double* pc[8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      load4(pa[q], ch * 16 + 4 * tq, av[q]);
-      load4(pb[q], ch * 16 + 4 * tq, bv[q]);
+      const int64_t ca = (int64_t)I * 32 + (q >> 1) * 16 + (q & 1) * 8 + g;
+      pc[q] = cq_col(p.X, min(ca, p.N - 1));
+      const int64_t cb = (int64_t)J * 32 + q * 8 + g;
+      pc[4 + q] = cq_col(p.X, min(cb, p.N - 1));
     }
-  }
-  for (; ch < c_end; ch += 4) {
-    if (ch + 4 < c_end) {
+    double acc[2][4][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        load4(pa[q], (ch + 4) * 16 + 4 * tq, an[q]);
-        load4(pb[q], (ch + 4) * 16 + 4 * tq, bn[q]);
-      }
+    for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) acc[a2][b2][c2] = 0.0;
+    const uint32_t ch1 = ub - tbase;
+    uint32_t ch = ua - tbase + warp;
+    double v0[8][4], v1[8][4];
+    if (ch < ch1) cq_gram_load<VEC>(pc, (int64_t)ch * 16 + 4 * tq, d, ch == last_chunk, v0);
+    while (ch < ch1) {
+      if (ch + 4 < ch1) cq_gram_load<VEC>(pc, (int64_t)(ch + 4) * 16 + 4 * tq, d, ch + 4 == last_chunk, v1);
+      cq_gram_mma(acc, v0);
+      ch += 4;
+      if (ch >= ch1) break;
+      if (ch + 4 < ch1) cq_gram_load<VEC>(pc, (int64_t)(ch + 4) * 16 + 4 * tq, d, ch + 4 == last_chunk, v0);
+      cq_gram_mma(acc, v1);
+      ch += 4;
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], av[mt * 2][j], av[mt * 2 + 1][j], bv[nt][j]);
+        for (int h = 0; h < 4; ++h) {
+          const int r = mt * 16 + g + (h >= 2 ? 8 : 0), cc = nt * 8 + 2 * tq + (h & 1);
+          red[warp][cc * 32 + r] = acc[mt][nt][h];
+        }
+    __syncthreads();
+    double* out = p.part + ((int64_t)c * p.SEG + (t - t_first)) * 1024;
+    for (int e = threadIdx.x; e < 1024; e += 128)
+      out[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+    // CTAs covering tile t: the last one to finish folds their partials
+    const uint32_t A = tbase, B = A + p.nchunk;
+    uint32_t cf = A * p.P / p.U, cl = (B - 1) * p.P / p.U;
+    while (cf > 0 && cq_unit_lo(p, cf) > A) --cf;
+    while (cq_unit_lo(p, cf + 1) <= A) ++cf;
+    while (cl + 1 < p.P && cq_unit_lo(p, cl + 1) < B) ++cl;
+    while (cq_unit_lo(p, cl) >= B) --cl;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(&p.cnt[t], 1u) == cl - cf;
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      double v[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+      for (int i = 0; i < 8; ++i) v[i] = 0.0;
+      for (uint32_t q = cf; q <= cl; ++q) {
+        const int jq = t - (int)(cq_unit_lo(p, q) / p.nchunk);
+        const double* src = p.part + ((int64_t)q * p.SEG + jq) * 1024 + threadIdx.x;
+        double w[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        av[q][j] = an[q][j];
-        bv[q][j] = bn[q][j];
+        for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += w[i];
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p.Gt[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
+      if (threadIdx.x == 0) p.cnt[t] = 0u;
+    }
+    __syncthreads();  // red reused by the next segment
+    ua = ub;
   }
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int r = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-        red[warp][c * 32 + r] = acc[mt][nt][h];
-      }
-  __syncthreads();
-  double* out = p.S == 1 ? p.Gt + (int64_t)t * 1024 : p.part + ((int64_t)s * gridDim.x + t) * 1024;
-  for (int e = threadIdx.x; e < 1024; e += 128)
-    out[e] = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
-  if (p.S == 1) return;
-  // the last slice CTA of this tile folds the slices in order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(&p.cnt[t], 1u) == (unsigned)(p.S - 1);
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // 8 elements per thread, the 8 loads of a slice in flight together
-  double v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = 0.0;
-  for (int q = 0; q < p.S; ++q) {
-    const double* src = p.part + ((int64_t)q * gridDim.x + t) * 1024 + threadIdx.x;
-    double w[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 128);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] += w[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) p.Gt[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
-  if (threadIdx.x == 0) p.cnt[t] = 0u;
 }
 
 // -------------------------------------------------------------- Cholesky
@@ -927,9 +957,26 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
   const double fro = sqrt(fro2);
   if (tid < n && (!(fro > 0.0) || !(dg >= CQ_RANK_TOL * fro)))
     atomicMin(&first_bad, (unsigned long long)tid);
+  // diagonal extremes (all entries positive by construction)
+  double dmax = tid < n ? dg : 0.0, dmin = tid < n ? dg : INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+  }
+  __shared__ double ext[2][CQ_SOLVE_NT / 32];
+  if (lane == 0) {
+    ext[0][warp] = dmax;
+    ext[1][warp] = dmin;
+  }
   __syncthreads();
   if (tid == 0) {
-    const bool broke = *p.flag != 0;
+    double mx = 0.0, mn = INFINITY;
+    for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) {
+      mx = fmax(mx, ext[0][w]);
+      mn = fmin(mn, ext[1][w]);
+    }
+    const bool broke = *p.flag != 0 || !(mx <= CQ_DIAG_RATIO_MAX * mn);
     const long long fb = first_bad == ~0ull ? -1 : (long long)first_bad;
     *p.bad_col = broke ? -2 : fb;
     *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
@@ -1012,7 +1059,7 @@ struct CqWork {
   size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi;
 };
 
-CqWork cq_layout(int64_t d, int64_t N, int nb, int S) {
+CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   CqWork w;
   size_t off = 0;
   auto take = [&](size_t b) {
@@ -1024,7 +1071,7 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int S) {
   const int64_t ldq = (d + 1) / 2 * 2;
   w.oG1 = take(nt * 1024 * 8);
   w.oG2 = take(nt * 1024 * 8);
-  w.oPart = take((size_t)S * nt * 1024 * 8);
+  w.oPart = take((size_t)nslots * 1024 * 8);
   w.oCnt = take(nt * 4);
   w.oR1 = take(nt * 1024 * 8);
   w.oR2 = take(nt * 1024 * 8);
@@ -1042,24 +1089,39 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int S) {
   return w;
 }
 
-// Row slices of the Gram: about two CTAs per SM over the upper tiles, at
-// least four 16-row chunks (one per warp) per slice.
-int cq_slices(int64_t d, int nt) {
-  const int64_t nchunk = (d + 15) / 16;
-  const int sms = sm_count_cached();
-  const int64_t s = std::min<int64_t>((2 * sms + nt - 1) / nt, nchunk / 4);
-  return (int)std::min<int64_t>(64, std::max<int64_t>(1, s));
+// Stream-K geometry of the Gram: P = min(2 x SMs, units) CTAs, partial
+// slots for the most tiles any CTA's unit range touches.
+struct CqGramGeom {
+  uint32_t nchunk, U, P;
+  int SEG;
+};
+CqGramGeom cq_gram_geom(int64_t d, int nt) {
+  CqGramGeom g;
+  g.nchunk = (uint32_t)((d + 15) / 16);
+  g.U = (uint32_t)nt * g.nchunk;
+  g.P = (uint32_t)std::min<int64_t>(2 * sm_count_cached(), g.U);
+  int seg = 1;
+  for (uint32_t c = 0; c < g.P; ++c) {
+    const uint32_t lo = (uint32_t)((uint64_t)g.U * c / g.P), hi = (uint32_t)((uint64_t)g.U * (c + 1) / g.P);
+    seg = std::max(seg, (int)((hi - 1) / g.nchunk - lo / g.nchunk + 1));
+  }
+  g.SEG = seg;
+  return g;
 }
 
 int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsigned* cnt,
             bool pdl, cudaStream_t st) {
   const int nt = nb * (nb + 1) / 2;
-  const int64_t nchunk = (X.d + 15) / 16;
-  const int S = cq_slices(X.d, nt);
+  const CqGramGeom gg = cq_gram_geom(X.d, nt);
+  SKL_REQUIRE((uint64_t)gg.U * (gg.P + 1) < (1ULL << 32), SKL_ERR_SPEC, "cqr_gram: %lld rows too many",
+              (long long)X.d);
   const bool vec = ((uintptr_t)X.A % 16 == 0) && (X.lda % 2 == 0) &&
                    (X.b == nullptr || (uintptr_t)X.b % 16 == 0);
-  GramParams gp{X, N, nb, S, nchunk, vec ? 1 : 0, part, Gt, cnt};
-  SKL_CUDA(launch_k(cqr_gram_kernel, dim3((unsigned)nt, (unsigned)S), dim3(128), 0, st, pdl, gp));
+  GramParams gp{X, N, gg.nchunk, gg.U, gg.P, gg.SEG, part, Gt, cnt};
+  if (vec)
+    SKL_CUDA(launch_k(cqr_gram_kernel<true>, dim3(gg.P), dim3(128), 0, st, pdl, gp));
+  else
+    SKL_CUDA(launch_k(cqr_gram_kernel<false>, dim3(gg.P), dim3(128), 0, st, pdl, gp));
   return SKL_OK;
 }
 
@@ -1135,8 +1197,8 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   const int64_t N = n + 1;
   const int nb = (int)((N + 31) / 32);
   const int nt = nb * (nb + 1) / 2;
-  const int S = cq_slices(d, nt);
-  const CqWork w = cq_layout(d, N, nb, S);
+  const CqGramGeom gg = cq_gram_geom(d, nt);
+  const CqWork w = cq_layout(d, N, nb, gg.P * gg.SEG);
   const int64_t ldq = (d + 1) / 2 * 2;
   unsigned char* ws = nullptr;
   SKL_CUDA(malloc_async(&ws, w.bytes, st));

@@ -84,7 +84,9 @@ def test_cholqr_ill_conditioned_minimises_the_sketched_residual(kappa):
     d, n = 2048, 256
     SA, Sb = system(d, n, kappa=kappa, seed=11)
     x, fell_back = cqr(SA, Sb)
-    assert not fell_back
+    # beyond kappa ~ 5e8 (R's diagonal ratio > 2e7) the refinement step is
+    # not reliable and the Householder factorisation takes over
+    assert fell_back == (kappa > 1e9)
     want = oracle_x(SA, Sb)
     rs, rw = np.linalg.norm(SA @ x - Sb), np.linalg.norm(SA @ want - Sb)
     assert rs <= rw * (1 + 1e-10)  # as good a minimiser as LAPACK's (or better)
