@@ -304,87 +304,102 @@ struct CholParams {
   int* flag;           // set on a non-positive / non-finite pivot
 };
 
+#ifdef CQ_FACTOR_CLOCKS
+__device__ long long cq_factor_clocks[17];
+#endif
+__device__ __forceinline__ double cq_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);  // two Newton steps: ~1 ulp
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
 // LDL^T of the 32 x 32 tile T (shared, column-major, stride CQ_LD) by one
 // warp, lane j holding column j.  On return T holds U (unit upper, 1 on the
 // diagonal, 0 below), disq[k] = 1 / sqrt(d_k) (disq is the 32 doubles right
 // after T: the pair is pushed to the other CTAs as one block), and Rg
-// (global tile, ld 32) R = D^{1/2} U.  Only the upper triangle of T is read.
+// (global tile, ld 32) R = D^{1/2} U.
 //
-// The step loop is rolled: each lane keeps a window c[i] = G^(k)[k + i][j]
-// of its column that shifts by one row per step, so the body has static
-// register indices and the whole routine is a few hundred instructions (it
-// runs once per CTA per factorisation, from a cold instruction cache).  The
-// dependent chain per pivot is: reciprocal (MUFU + two Newton steps), one
-// FMA on lane k+1 for the next pivot, one shuffle; the rank-1 update of the
-// window runs beside it.  srow[32..63] stay zero, so rows past the tile
-// update as no-ops.  A non-positive or non-finite pivot only sets the flag
-// (the caller then falls back to Householder).
-// One pivot step of cq_factor (ODD: k is odd, so srow + k + 1 is 16-byte
-// aligned and the row is read in pairs).  The reciprocal of the NEXT pivot
-// is started right after its shuffle, so its latency overlaps this step's
-// rank-1 update; the dependent chain per step is one FMA, one shuffle and
-// the reciprocal.
-template <bool ODD>
-__device__ __forceinline__ void cq_factor_step(int k, double (&c)[32], double& pk, double& rk,
-                                               double& myd, bool& bad, double* T, double* srow) {
-  const int lane = threadIdx.x & 31;
-  const double gk = c[0];  // G^(k)[k][lane]
-  const double pn = fma(-(gk * gk), rk, c[1]);  // lane k+1: the next pivot
-  const double pnext = __shfl_sync(0xffffffffu, pn, (k + 1) & 31);
-  double rn;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(pnext));
-  const double u = gk * rk;  // U[k][lane] for lane > k
-  bad |= !(pk > 0.0) || !(pk < INFINITY);
-  if (lane > k) T[lane * CQ_LD + k] = u;
-  if (lane == k) myd = pk;
-  srow[lane] = lane > k ? gk : 0.0;
-  __syncwarp();
-  const double* sr = srow + k + 1;
-  if (ODD) {
-#pragma unroll
-    for (int i = 0; i < 30; i += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(sr + i);
-      c[i] = fma(-v.x, u, c[i + 1]);
-      c[i + 1] = fma(-v.y, u, c[i + 2]);
-    }
-    c[30] = fma(-sr[30], u, c[31]);
-  } else {
-    c[0] = fma(-sr[0], u, c[1]);
-#pragma unroll
-    for (int i = 1; i < 31; i += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(sr + i);
-      c[i] = fma(-v.x, u, c[i + 1]);
-      c[i + 1] = fma(-v.y, u, c[i + 2]);
-    }
-  }
-  rn = fma(rn, fma(-pnext, rn, 1.0), rn);  // two Newton steps: ~1 ulp
-  rn = fma(rn, fma(-pnext, rn, 1.0), rn);
-  __syncwarp();
-  pk = pnext;
-  rk = rn;
-}
-
-__device__ __noinline__ void cq_factor(double* T, double* srow, double* Rg, int* flag) {
+// Two pivots per pass: with a = G[k][k], b = G[k][k+1], e = G[k+1][k+1],
+// l = b / a and d1 = e - b l, lane j forms U[k][j] = G[k][j] / a, the
+// eliminated row G'[k+1][j] = G[k+1][j] - l G[k][j] and U[k+1][j] =
+// G'[k+1][j] / d1, the two rows are exchanged once through shared memory
+// (one 16-byte store and 15 16-byte broadcast loads per lane) and the
+// window c[i] = G[k + i][j] of the lane's column takes the rank-2 update
+// while shifting by two rows, so the loop body has static register indices
+// (rolled loop: the routine runs once per CTA per factorisation, from a cold
+// instruction cache).  The next pivot block (lanes k+2, k+3) is formed from
+// the lanes' own registers plus one broadcast pair before the bulk update,
+// and its first reciprocal is in flight while the update issues.  The whole
+// tile is updated (lower entries too: the Gram tiles are symmetric), which
+// keeps the loop free of per-lane predicates.  s2[64..127] stay zero, so
+// rows past the tile update as no-ops.  A non-positive or non-finite pivot
+// only sets the flag (the caller then falls back to Householder).
+__device__ __noinline__ void cq_factor(double* T, double* s2, double* Rg, int* flag) {
   const int lane = threadIdx.x & 31;
   double* disq = T + CQ_TILE;
   double c[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) c[i] = T[lane * CQ_LD + i];
-  srow[32 + lane] = 0.0;
-  double pk = __shfl_sync(0xffffffffu, c[0], 0);
-  double rk;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rk) : "d"(pk));
-  rk = fma(rk, fma(-pk, rk, 1.0), rk);
-  rk = fma(rk, fma(-pk, rk, 1.0), rk);
+  reinterpret_cast<double2*>(s2)[32 + lane] = make_double2(0.0, 0.0);
+  double a = __shfl_sync(0xffffffffu, c[0], 0);
+  double b = __shfl_sync(0xffffffffu, c[0], 1);
+  double e = __shfl_sync(0xffffffffu, c[1], 1);
+  double ra = cq_rcp(a);
   bool bad = false;
   double myd = 1.0;
 #pragma unroll 1
   for (int k = 0; k < 32; k += 2) {
-    cq_factor_step<false>(k, c, pk, rk, myd, bad, T, srow);
-    cq_factor_step<true>(k + 1, c, pk, rk, myd, bad, T, srow);
+#ifdef CQ_FACTOR_CLOCKS
+    if (lane == 0) cq_factor_clocks[k >> 1] = clock64();
+#endif
+    const double l = b * ra;
+    const double d1 = fma(-b, l, e);
+    const double gk = c[0], gk1 = c[1];
+    const double u0 = gk * ra;             // U[k][lane]   (lane > k)
+    const double gk1p = fma(-l, gk, gk1);  // G'[k+1][lane]
+    const bool hi = lane > k + 1;
+    reinterpret_cast<double2*>(s2)[lane] = hi ? make_double2(gk, gk1p) : make_double2(0.0, 0.0);
+    const double r1 = cq_rcp(d1);
+    const double u1 = gk1p * r1;           // U[k+1][lane] (lane > k+1)
+    if (lane > k) T[lane * CQ_LD + k] = u0;
+    if (hi) T[lane * CQ_LD + k + 1] = u1;
+    if (lane == k) myd = a;
+    if (lane == k + 1) myd = d1;
+    bad |= !(a > 0.0) || !(a < INFINITY) || !(d1 > 0.0) || !(d1 < INFINITY);
+    __syncwarp();
+    const double2* sr = reinterpret_cast<const double2*>(s2) + k + 2;
+    // the next pivot block first: a' on lane k+2, b' and e' on lane k+3
+    const double2 v2 = sr[0];
+    const double pa = fma(-gk1p, u1, fma(-gk, u0, c[2]));
+    const double pe = fma(-gk1p, u1, fma(-gk, u0, c[3]));
+    const double pb = fma(-v2.y, u1, fma(-v2.x, u0, c[2]));
+    const double an = __shfl_sync(0xffffffffu, pa, (k + 2) & 31);
+    const double bn = __shfl_sync(0xffffffffu, pb, (k + 3) & 31);
+    const double en = __shfl_sync(0xffffffffu, pe, (k + 3) & 31);
+    double rn;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(an));
+    // rank-2 update of the window, shifted by two rows
+#pragma unroll
+    for (int i = 0; i < 30; ++i) {
+      const double2 v = sr[i];
+      c[i] = fma(-v.y, u1, fma(-v.x, u0, c[i + 2]));
+    }
+    c[30] = 0.0;
+    c[31] = 0.0;
+    rn = fma(rn, fma(-an, rn, 1.0), rn);
+    rn = fma(rn, fma(-an, rn, 1.0), rn);
+    __syncwarp();
+    a = an;
+    b = bn;
+    e = en;
+    ra = rn;
   }
+#ifdef CQ_FACTOR_CLOCKS
+  if (lane == 0) cq_factor_clocks[16] = clock64();
+#endif
   const double sq = sqrt(myd);
-  srow[lane] = sq;
+  s2[lane] = sq;
   disq[lane] = 1.0 / sq;
   __syncwarp();
   double uk[32];
@@ -395,8 +410,10 @@ __device__ __noinline__ void cq_factor(double* T, double* srow, double* Rg, int*
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 32; ++k) T[lane * CQ_LD + k] = uk[k];
+  __syncwarp();
+  // R = D^{1/2} U, written coalesced: lane = row, one column per store
 #pragma unroll
-  for (int k = 0; k < 32; ++k) Rg[lane * 32 + k] = k == lane ? sq : srow[k] * uk[k];
+  for (int cc = 0; cc < 32; ++cc) Rg[cc * 32 + lane] = sq * T[cc * CQ_LD + lane];
   if (bad && lane == 0) atomicExch(flag, 1);
   __syncwarp();
 }
@@ -422,8 +439,9 @@ __device__ __noinline__ void cq_rowsolve(double* T, const double* Us, double* Rg
   for (int k = 0; k < 32; ++k) g[k] *= sc[k];
 #pragma unroll
   for (int k = 0; k < 32; ++k) T[lane * CQ_LD + k] = g[k];
+  __syncwarp();
 #pragma unroll
-  for (int k = 0; k < 32; ++k) Rg[lane * 32 + k] = g[k];
+  for (int cc = 0; cc < 32; ++cc) Rg[cc * 32 + lane] = T[cc * CQ_LD + lane];  // coalesced
 }
 
 // C -= A^T B for 32 x 32 tiles (shared, stride CQ_LD): A = R(K, I) (local or
@@ -471,7 +489,7 @@ __device__ __noinline__ void cq_tile_update(double* C, const double* A, bool a_r
 
 // Inverse of the diagonal tile R_JJ = D^{1/2} U (U in T, unit upper):
 // R^{-1} = U^{-1} D^{-1/2}; lane j builds column j of U^{-1} upward.
-__device__ __noinline__ void cq_diag_inverse(const double* T, double* out) {
+__device__ __noinline__ void cq_diag_inverse(const double* T, double* out, double* scratch) {
   const int lane = threadIdx.x & 31;
   const double* disq = T + CQ_TILE;
   double acc[32];
@@ -485,9 +503,15 @@ __device__ __noinline__ void cq_diag_inverse(const double* T, double* out) {
 #pragma unroll
     for (int i = 0; i < m; ++i) acc[i] = fma(T[m * CQ_LD + i], xm, acc[i]);
   }
+  // out (column-major, ld 32) = X diag(disq): lane j holds column j; go
+  // through shared memory (the first 33 x 32 doubles of `scratch`) so the
+  // global stores are coalesced
   const double sc = disq[lane];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) out[lane * 32 + i] = x[i] * sc;
+  for (int i = 0; i < 32; ++i) scratch[i * CQ_LD + lane] = x[i] * sc;
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < 32; ++cc) out[cc * 32 + lane] = scratch[lane * CQ_LD + cc];
 }
 
 constexpr uint32_t CQ_PUSH_BYTES = (CQ_TILE + 32) * sizeof(double);
@@ -511,7 +535,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
   extern __shared__ __align__(16) double csm[];
   __shared__ __align__(16) double Us[2][CQ_TILE + 32];  // pushed U_KK | 1/sqrt(d_K)
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ __align__(16) double srow[64];
+  __shared__ __align__(16) double srow[128];
   const int J = (int)cq_rank();
   const int nb = p.nb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -597,7 +621,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
     }
     CQ_PROBE(5 + 4 * K);
   }
-  if (warp == 0) cq_diag_inverse(tile(J), p.Rinv + (int64_t)J * 1024);
+  if (warp == 0) cq_diag_inverse(tile(J), p.Rinv + (int64_t)J * 1024, Us[0]);
   CQ_PROBE(70);
   // shared memory stays alive until every remote reader is done
   cq_arrive();
@@ -616,21 +640,26 @@ struct TrsmParams {
 };
 
 // Q (rows r0 .. r0+15) = X R^{-1}: for each block column J,
-//   T = X_J - sum_{K<J} Q_K R(K, J)   (K split over the 4 warps)
-//   Q_J = T Rinv_JJ                    (warp w: 8 columns)
+//   T = X_J - sum_{K<J} Q_K R(K, J)   (K split over the 8 warps)
+//   Q_J = T Rinv_JJ                    (warps 0-3: 8 columns each)
+constexpr int CQ_TRSM_WARPS = 8;
+constexpr int CQ_TRSM_NT = CQ_TRSM_WARPS * 32;
+
 __device__ __forceinline__ void cq_trsm_fetch_x(const TrsmParams& p, int J, int64_t r0,
-                                                double (&xv)[4], double (&bi)[8]) {
+                                                double (&xv)[2], double (&bi)[8]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int e = threadIdx.x + q * 128;
+  for (int q = 0; q < 2; ++q) {
+    const int e = threadIdx.x + q * CQ_TRSM_NT;
     const int r = e & 15, c = e >> 4;
     const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
     xv[q] = (gc < p.N && gr < p.X.d) ? __ldg(cq_col(p.X, gc) + gr) : 0.0;
   }
-  const double* rinv = p.Rinv + (int64_t)J * 1024;
+  if (warp < 4) {
+    const double* rinv = p.Rinv + (int64_t)J * 1024;
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
+    for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
+  }
 }
 
 __device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8][4]) {
@@ -641,16 +670,16 @@ __device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8
     for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(rk + (nt * 8 + g) * 32 + ks * 4 + tq);
 }
 
-__global__ void __launch_bounds__(128) cqr_trsm_kernel(const TrsmParams p) {
+__global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p) {
   extern __shared__ double qsm[];  // Qs[c * CQ_QLD + r], c < nb * 32
-  __shared__ double red[4][16 * 33];
+  __shared__ double red[CQ_TRSM_WARPS][16 * 33];
   __shared__ double Ts[16 * 33];
   pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
   const int64_t d = p.X.d;
   double* Qs = qsm;
-  double xv[4], bi[8];
+  double xv[2], bi[8];
   double bf[8][4], bn[8][4];
   cq_trsm_fetch_x(p, 0, r0, xv, bi);
   for (int J = 0; J < p.nb; ++J) {
@@ -659,12 +688,12 @@ __global__ void __launch_bounds__(128) cqr_trsm_kernel(const TrsmParams p) {
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    // sum_{K < J, K = warp mod 4} Q_K R(K, J): the next tile's loads are in
+    // sum_{K < J, K = warp mod 8} Q_K R(K, J): the next tile's loads are in
     // flight while the current one is multiplied (the first tile was
     // fetched during the previous block column)
     int K = warp;
     while (K < J) {
-      const int Kn = K + 4;
+      const int Kn = K + CQ_TRSM_WARPS;
       if (Kn < J) cq_trsm_fetch_r(p.Rt + cq_tile(Kn, J) * 1024, bn);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
@@ -679,38 +708,47 @@ __global__ void __launch_bounds__(128) cqr_trsm_kernel(const TrsmParams p) {
         for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = bn[ks][nt];
       K = Kn;
     }
+    if (warp < J) {
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+      for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-        red[warp][r * 33 + c] = acc[nt][h];
-      }
+        for (int h = 0; h < 4; ++h) {
+          const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+          red[warp][r * 33 + c] = acc[nt][h];
+        }
+    }
     __syncthreads();
+    const int nw = min(J, CQ_TRSM_WARPS);  // warps holding partial sums
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = threadIdx.x + q * 128;
+    for (int q = 0; q < 2; ++q) {
+      const int e = threadIdx.x + q * CQ_TRSM_NT;
       const int r = e & 15, c = e >> 4;
       const int o = r * 33 + c;
-      Ts[o] = xv[q] - (((red[0][o] + red[1][o]) + red[2][o]) + red[3][o]);
+      double sacc = 0.0;
+      for (int w = 0; w < nw; ++w) sacc += red[w][o];
+      Ts[o] = xv[q] - sacc;
     }
     __syncthreads();
     double qa[4] = {0.0, 0.0, 0.0, 0.0};
+    if (warp < 4) {
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const double a0 = Ts[g * 33 + ks * 4 + tq], a1 = Ts[(g + 8) * 33 + ks * 4 + tq];
-      cq_dmma(qa, a0, a1, bi[ks]);
+      for (int ks = 0; ks < 8; ++ks) {
+        const double a0 = Ts[g * 33 + ks * 4 + tq], a1 = Ts[(g + 8) * 33 + ks * 4 + tq];
+        cq_dmma(qa, a0, a1, bi[ks]);
+      }
     }
     if (J + 1 < p.nb) {
       cq_trsm_fetch_x(p, J + 1, r0, xv, bi);
       if (warp < J + 1) cq_trsm_fetch_r(p.Rt + cq_tile(warp, J + 1) * 1024, bf);
     }
+    if (warp < 4) {
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
-      const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
-      Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
-      if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
+      for (int h = 0; h < 4; ++h) {
+        const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
+        const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
+        Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
+        if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
+      }
     }
     __syncthreads();
   }
@@ -1167,7 +1205,7 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* 
   if (arc) return arc;
   TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
-  SKL_CUDA(launch_k(cqr_trsm_kernel, dim3(grid), dim3(128), (size_t)nb * 32 * CQ_QLD * sizeof(double),
+  SKL_CUDA(launch_k(cqr_trsm_kernel, dim3(grid), dim3(CQ_TRSM_NT), (size_t)nb * 32 * CQ_QLD * sizeof(double),
                     st, pdl, tp));
   return SKL_OK;
 }

@@ -12,3 +12,6 @@ for r in rows:
 for k, v in per.items():
     v = sorted(v); print(f"{k:40s} n={len(v):4d} median={v[len(v)//2]:10.1f} min={v[0]:10.1f}")
 PY
+export SKL_NVCC_DEFINES=-DSKL_CQR_PROBE
+python -c "from paper_2409_14309_b200 import _build; _build.build(force=True)" 2>&1 | tail -2
+timeout 120 python tools/probe_cholqr.py 2048x256 2>&1 | head -11 | cut -c1-200

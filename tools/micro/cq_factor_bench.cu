@@ -3,13 +3,14 @@
 // (warm) calls of cq_factor / cq_rowsolve / cq_tile_update.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        tools/micro/cq_factor_bench.cu -o /tmp/cqfb && /tmp/cqfb
+#define CQ_FACTOR_CLOCKS
 #include "../../paper_2409_14309_b200/csrc/skl_cholqr.cu"
 #include <cstdio>
 
 __global__ void __launch_bounds__(256, 1) bench(const double* G, double* Rg, int* flag, long long* out) {
   __shared__ __align__(16) double T[skl::CQ_TILE + 32];
   __shared__ __align__(16) double U[skl::CQ_TILE + 32];
-  __shared__ __align__(16) double srow[64];
+  __shared__ __align__(16) double srow[128];
   const int tid = threadIdx.x;
   for (int rep = 0; rep < 4; ++rep) {
     for (int e = tid; e < 1024; e += 256) T[(e >> 5) * skl::CQ_LD + (e & 31)] = G[e];
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(256, 1) bench(const double* G, double* Rg, int
     if (tid < 32) skl::cq_tile_update<2, 4>(T, U, false, 0, U, 0, 0);
     __syncthreads();
     long long t4 = clock64();
-    if (tid < 32) skl::cq_diag_inverse(U, Rg);
+    if (tid < 32) skl::cq_diag_inverse(U, Rg, T);
     __syncthreads();
     long long t5 = clock64();
     if (tid == 0) {
@@ -51,6 +52,11 @@ int main() {
   long long ho[16];
   cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  long long fc[17];
+  cudaMemcpyFromSymbol(fc, skl::cq_factor_clocks, sizeof(fc));
+  printf("pair cycles:");
+  for (int i = 1; i < 17; ++i) printf(" %lld", fc[i] - fc[i - 1]);
+  printf("\n");
   for (int r = 0; r < 4; ++r)
     printf("rep %d: factor %lld  rowsolve %lld  tile_update %lld  diag_inverse %lld cycles\n", r,
            ho[r * 4], ho[r * 4 + 1], ho[r * 4 + 2], ho[r * 4 + 3]);
