@@ -519,9 +519,9 @@ def sharded_sketch_and_apply(A_local, b_local, m_total: int, spec, dist, group=N
         reduce_partials(partial, dist, group)
     if rank == 0:
         if solve_reduced is None:
-            from .linalg import qr_solve_device
+            from .linalg import reduced_solve_device
 
-            x, _, _ = qr_solve_device(partial[:, :n], int(partial.stride(1)), partial[:, n], d, n)
+            x = reduced_solve_device(partial[:, :n], int(partial.stride(1)), partial[:, n], d, n)
         else:
             x = solve_reduced(partial)
     else:

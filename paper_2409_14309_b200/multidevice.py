@@ -225,9 +225,9 @@ def sketch_and_apply_devices(op, A, b, devices):
             _native.call("skl_reduce_peers", _native.ptr_array([p.data_ptr() for p in parts]),
                          world, 0, slot, total.data_ptr(), current_stream())
             red = total.view(n + 1, ld).t()
-            from .linalg import qr_solve_device
+            from .linalg import reduced_solve_device
 
-            x, _, _ = qr_solve_device(red[:d, :n], ld, red[:d, n], d, n)
+            x = reduced_solve_device(red[:d, :n], ld, red[:d, n], d, n)
             x_done = torch.cuda.Event()
             x_done.record(caller)
     # 3. per-block squared residuals against x

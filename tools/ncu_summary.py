@@ -4,7 +4,7 @@
       per-kernel launch counts / total and mean gpu__time_duration from an
       `ncu --metrics gpu__time_duration.sum --csv` launch list, plus the
       share of the matching kernel among the launches after the first one.
-  python tools/ncu_summary.py full <report.ncu-rep> <out.json> [label]
+  python tools/ncu_summary.py full <report.ncu-rep> <out.json> [label] [kernel-regex]
       selected counters of a `ncu --set full` capture (one launch), read
       with `ncu -i ... --page raw --csv`; `dram_bytes_per_launch` is what
       bench.py reports as roofline.traffic.
@@ -101,11 +101,14 @@ def launches(path: str, out: str, pattern: str = "countsketch") -> None:
     print(json.dumps({k: summary[k] for k in list(summary)[:6]}))
 
 
-def full(rep: str, out: str, label: str = "") -> None:
+def full(rep: str, out: str, label: str = "", kernel: str = "") -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    # the first launch whose kernel name matches (all launches when no regex)
+    ki = hdr.index("Kernel Name")
+    vals = next(r for r in rows[2:] if not kernel or re.search(kernel, r[ki]))
     got = {}
     for h, u, v in zip(hdr, units, vals):
         if h in FULL_METRICS or h in ("Kernel Name", "Block Size", "Grid Size"):

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 import paper_2409_14309_b200 as E  # noqa: E402
 from paper_2409_14309_b200 import workloads as W  # noqa: E402
-from paper_2409_14309_b200.linalg import qr_solve_device  # noqa: E402
+from paper_2409_14309_b200.linalg import qr_solve_device, qr_solve_device_async  # noqa: E402
 from paper_2409_14309_b200.sketch import _countsketch_dense_device  # noqa: E402
 from paper_2409_14309_b200.solvers import _residual_device  # noqa: E402
 
@@ -56,13 +56,20 @@ x, _, _ = qr_solve_device(SA, c.d, Sb, c.d, c.n)
 out = {
     "solve_wall_ms": wall(lambda: E.solve(prob, "saa", spec, opts)),
     "sketch_ms": events(lambda: _countsketch_dense_device(op, A, int(A.stride(1)), c.n, b=b)),
-    "qr_ms": events(lambda: qr_solve_device(SA, c.d, Sb, c.d, c.n)),
+    "qr_ms": events(lambda: qr_solve_device_async(SA, c.d, Sb, c.d, c.n)),
+    "householder_qr_ms": events(lambda: qr_solve_device(SA, c.d, Sb, c.d, c.n)),
+    "solve_events_ms": events(lambda: E.solve(prob, "saa", spec, opts)),
     "residual_wall_ms": wall(lambda: _residual_device(prob.A, A, int(A.stride(1)), b, x)),
 }
 t0 = time.perf_counter()
 for _ in range(20):
     _countsketch_dense_device(op, A, int(A.stride(1)), c.n, b=b)
 out["sketch_enqueue_us"] = (time.perf_counter() - t0) / 20 * 1e6
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    qr_solve_device_async(SA, c.d, Sb, c.d, c.n)
+out["qr_enqueue_us"] = (time.perf_counter() - t0) / 20 * 1e6
 torch.cuda.synchronize()
 print({k: round(v, 4) for k, v in out.items()})
 
