@@ -16,13 +16,34 @@ except Exception:  # pragma: no cover - torch is present in this image
 from .errors import DeviceError
 
 
+_CUDA_OK = False
+
+
 def require_cuda() -> None:
+    # a device, once seen, stays (the check sat on every call of the solve
+    # path: torch.cuda.is_available() costs microseconds of host time)
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     if torch is None or not torch.cuda.is_available():
         raise DeviceError(
             "the sketch engine needs a CUDA device (sm_100a); there is no CPU fallback")
+    _CUDA_OK = True
+
+
+try:  # the raw cudaStream_t of the current stream without building a Stream object
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+    _cur_dev = torch._C._cuda_getDevice
+except Exception:  # pragma: no cover - older torch
+    _raw_stream = None
 
 
 def current_stream() -> int:
+    """cudaStream_t (as an int) of torch's current stream on the current
+    device.  Every native call takes it; torch.cuda.current_stream() builds a
+    Python Stream object (~10 us of host time), the raw accessor does not."""
+    if _raw_stream is not None:
+        return _raw_stream(_cur_dev())
     return torch.cuda.current_stream().cuda_stream
 
 

@@ -285,13 +285,15 @@ def qr_solve_device(SA, ldsa: int, Sb, d: int, n: int, want_q: bool = False,
 _RANK_FLAGS = threading.local()
 
 
+_CQR_OFF = os.environ.get("SKL_QR_HOUSEHOLDER", "") not in ("", "0")
+
+
 def cholqr_enabled(d: int, n: int) -> bool:
     """Whether the reduced solve of a d x n sketched system takes the
     CholeskyQR2 path (skl_cqr_solve_async): n + 1 <= 512 < d, unless
-    SKL_QR_HOUSEHOLDER=1 forces the Householder factorisation (A/B knob)."""
-    if os.environ.get("SKL_QR_HOUSEHOLDER", "") not in ("", "0"):
-        return False
-    return bool(_native.lib().skl_cqr_supported(d, n))
+    SKL_QR_HOUSEHOLDER=1 forces the Householder factorisation (A/B knob,
+    read at import)."""
+    return not _CQR_OFF and bool(_native.lib().skl_cqr_supported(d, n))
 
 
 def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):

@@ -288,11 +288,11 @@ class SketchOperator:
                 ev.record(st0)
                 entry = c[name] = (value, ev, st0.cuda_stream)
         value, ev, made_on = entry
-        st = torch.cuda.current_stream()
-        if st.cuda_stream == made_on:
+        if current_stream() == made_on:
             # the stream that built it: stream order already covers the build
             # and the allocator's own bookkeeping the lifetime
             return value
+        st = torch.cuda.current_stream()
         if torch.cuda.is_current_stream_capturing():
             # inside a CUDA-graph capture the artifact was built before the
             # capture began (the warm-up call); an event from outside the

@@ -16,6 +16,7 @@ skl_qr_solve) for dense and CSR operands.
 from __future__ import annotations
 
 import math
+import threading
 import time
 from dataclasses import dataclass, replace
 
@@ -164,6 +165,22 @@ def sketch_operands_device(op, A: Matrix, b: Vector):
     return SA, Sb, A_dev, lda, b_dev
 
 
+_EVENTS = threading.local()
+
+
+def _timing_events():
+    """A per-thread, per-device pair of timing events for wall_time_s (creating
+    two events on every solve cost host time ahead of the first launch)."""
+    dev = torch.cuda.current_device()
+    pairs = getattr(_EVENTS, "pairs", None)
+    if pairs is None:
+        pairs = _EVENTS.pairs = {}
+    ev = pairs.get(dev)
+    if ev is None:
+        ev = pairs[dev] = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    return ev
+
+
 def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = None,
                      opts: SolverOptions | None = None) -> SolveResult:
     """Solve min ||S A x - S b|| by QR, one shot (solvers.py:296-320)."""
@@ -183,7 +200,7 @@ def sketch_and_apply(problem: LeastSquaresProblem, spec: SketchSpec | None = Non
     # rank flag checked after the residual pass (one host round trip per
     # solve); wall_time_s still covers sketch + QR + back-solve, as the
     # reference's, through events on the stream.
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0, ev1 = _timing_events()
     ev0.record()
     op = build_sketch(op_spec, A.rows)
     SA, Sb, A_dev, lda, b_dev = sketch_operands_device(op, A, b)

@@ -1,12 +1,11 @@
-"""Host-side cost of one warm SAA solve (config 2, device-resident A): a
-cProfile of 200 solves, top entries by cumulative time."""
+"""Host-side cost of one sketch-and-apply solve() on device data (config 2):
+cProfile of 200 warm solves, top functions by own time."""
 import cProfile
 import pstats
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-
 import torch  # noqa: E402
 
 import paper_2409_14309_b200 as E  # noqa: E402
@@ -24,4 +23,4 @@ pr.enable()
 for _ in range(200):
     E.solve(prob, "saa", spec, opts)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
