@@ -418,6 +418,13 @@ int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda, const
 int skl_residual_csr(const int64_t* indptr, const int64_t* indices, const double* values,
                      int64_t m, int64_t n, const double* x, const double* b, double* out,
                      void* stream);
+/* The two residuals without their synchronisation: *out (pinned host or
+ * device) is written in stream order (batched solves, solve_many). */
+int skl_residual_dense_async(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
+                             const double* b, double* out, void* stream);
+int skl_residual_csr_async(const int64_t* indptr, const int64_t* indices, const double* values,
+                           int64_t m, int64_t n, const double* x, const double* b, double* out,
+                           void* stream);
 
 /* ---- Gaussian operator generated in bands across devices ----
  * The d x m Gaussian operator (sketch.py:94-96) is one ziggurat stream cut

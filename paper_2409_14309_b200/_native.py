@@ -10,6 +10,7 @@ the caller's current CUDA stream as ``void*``.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -180,6 +181,8 @@ SIGNATURES: dict[str, tuple] = {
     "skl_cqr_supported": (c_int, [c_i64, c_i64]),
     "skl_cqr_solve_async": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_residual_dense": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_residual_dense_async": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "skl_residual_csr_async": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_sum_slots": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "skl_reduce_peers": (c_int, [c_ptr, c_int, c_i64, c_i64, c_ptr, c_ptr]),
     "skl_residual_csr": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
@@ -337,6 +340,9 @@ def plan_geometry(d: int, kind: str | None = None, m: int | None = None) -> tupl
         warps = 8 if d <= 1024 else 16
         if d <= 2048:  # 4 slots per thread: 13-bit row field
             chunk = OWNED_CHUNK if m is None or m > 4 * OWNED_CHUNK else OWNED_SMALL_CHUNK
+            forced = int(os.environ.get("SKL_OWNED_CHUNK", "0") or 0)  # A/B knob
+            if forced >= 8:
+                chunk = min(OWNED_CHUNK, forced // 8 * 8)
         else:  # 8 slots: 12-bit row field
             chunk = 4088
         return "owned", chunk, warps

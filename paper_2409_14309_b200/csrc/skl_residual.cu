@@ -132,12 +132,14 @@ static int rs_grid(int64_t work) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work + RS_NT - 1) / RS_NT, (int64_t)sms * 8));
 }
 
-static int rs_finish(double* part, int blocks, double* out, cudaStream_t st) {
+// sync = false: *out (pinned host or device) is written in stream order and
+// read by the caller once the stream has passed it (batched solves).
+static int rs_finish(double* part, int blocks, double* out, cudaStream_t st, bool sync = true) {
   double* res = part + blocks;
   rs_finish_kernel<<<1, RS_NT, 0, st>>>(part, blocks, res);
   SKL_CUDA_LAUNCH();
-  SKL_CUDA(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, st));
-  SKL_CUDA(cudaStreamSynchronize(st));
+  SKL_CUDA(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDefault, st));
+  if (sync) SKL_CUDA(cudaStreamSynchronize(st));
   return SKL_OK;
 }
 
@@ -145,10 +147,9 @@ static int rs_finish(double* part, int blocks, double* out, cudaStream_t st) {
 
 using namespace skl;
 
-extern "C" int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda,
-                                  const double* x, const double* b, double* out, void* stream) {
-  clear_error();
-  cudaStream_t st = (cudaStream_t)stream;
+static int residual_dense_impl(const double* A, int64_t m, int64_t n, int64_t lda,
+                               const double* x, const double* b, double* out, cudaStream_t st,
+                               bool sync) {
   SKL_REQUIRE(A && x && b && out && m >= 1 && n >= 1 && lda >= m, SKL_ERR_SHAPE,
               "residual: bad arguments");
   const bool vec = ((uintptr_t)A & 15) == 0 && lda % 2 == 0;
@@ -167,16 +168,27 @@ extern "C" int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t
     cudaFreeAsync(part, st);
     SKL_FAIL(SKL_ERR_CUDA, "residual kernel: %s", cudaGetErrorString(e));
   }
-  int rc = rs_finish(part, blocks, out, st);
+  int rc = rs_finish(part, blocks, out, st, sync);
   cudaFreeAsync(part, st);
   return rc;
 }
 
-extern "C" int skl_residual_csr(const int64_t* indptr, const int64_t* indices,
-                                const double* values, int64_t m, int64_t n, const double* x,
-                                const double* b, double* out, void* stream) {
+extern "C" int skl_residual_dense(const double* A, int64_t m, int64_t n, int64_t lda,
+                                  const double* x, const double* b, double* out, void* stream) {
   clear_error();
-  cudaStream_t st = (cudaStream_t)stream;
+  return residual_dense_impl(A, m, n, lda, x, b, out, (cudaStream_t)stream, true);
+}
+
+extern "C" int skl_residual_dense_async(const double* A, int64_t m, int64_t n, int64_t lda,
+                                        const double* x, const double* b, double* out,
+                                        void* stream) {
+  clear_error();
+  return residual_dense_impl(A, m, n, lda, x, b, out, (cudaStream_t)stream, false);
+}
+
+static int residual_csr_impl(const int64_t* indptr, const int64_t* indices, const double* values,
+                             int64_t m, int64_t n, const double* x, const double* b, double* out,
+                             cudaStream_t st, bool sync) {
   SKL_REQUIRE(indptr && x && b && out && m >= 1 && n >= 1, SKL_ERR_SHAPE,
               "residual_csr: bad arguments");
   const int blocks = rs_grid(m);
@@ -188,7 +200,22 @@ extern "C" int skl_residual_csr(const int64_t* indptr, const int64_t* indices,
     cudaFreeAsync(part, st);
     SKL_FAIL(SKL_ERR_CUDA, "residual_csr kernel: %s", cudaGetErrorString(e));
   }
-  int rc = rs_finish(part, blocks, out, st);
+  int rc = rs_finish(part, blocks, out, st, sync);
   cudaFreeAsync(part, st);
   return rc;
+}
+
+extern "C" int skl_residual_csr(const int64_t* indptr, const int64_t* indices,
+                                const double* values, int64_t m, int64_t n, const double* x,
+                                const double* b, double* out, void* stream) {
+  clear_error();
+  return residual_csr_impl(indptr, indices, values, m, n, x, b, out, (cudaStream_t)stream, true);
+}
+
+extern "C" int skl_residual_csr_async(const int64_t* indptr, const int64_t* indices,
+                                      const double* values, int64_t m, int64_t n,
+                                      const double* x, const double* b, double* out,
+                                      void* stream) {
+  clear_error();
+  return residual_csr_impl(indptr, indices, values, m, n, x, b, out, (cudaStream_t)stream, false);
 }

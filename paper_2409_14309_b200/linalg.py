@@ -296,7 +296,7 @@ def cholqr_enabled(d: int, n: int) -> bool:
     return not _CQR_OFF and bool(_native.lib().skl_cqr_supported(d, n))
 
 
-def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):
+def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int, flags=None):
     """The reduced solve x = R^{-1} Q^T Sb without its synchronisation:
     returns (x, check) where check() -- to be called once the stream has
     been synchronised (e.g. by the residual pass) -- returns None when x is
@@ -307,10 +307,11 @@ def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int):
     with the Householder factorisation, which decides (and words the error
     exactly as linalg.py:186-191).  The flags land in a pinned per-thread
     buffer."""
-    flags = getattr(_RANK_FLAGS, "buf", None)
-    if flags is None:
-        flags = torch.empty(2, dtype=torch.float64, pin_memory=True)
-        _RANK_FLAGS.buf = flags
+    if flags is None:  # batched callers pass their own pinned pair per solve
+        flags = getattr(_RANK_FLAGS, "buf", None)
+        if flags is None:
+            flags = torch.empty(2, dtype=torch.float64, pin_memory=True)
+            _RANK_FLAGS.buf = flags
     flags_i = flags.view(torch.int64)
     x = device_f64((n,))
     base = flags.data_ptr()

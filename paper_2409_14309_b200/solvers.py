@@ -378,6 +378,101 @@ def direct(problem: LeastSquaresProblem) -> SolveResult:
                        residual_norm=rnorm, termination="direct", wall_time_s=wall)
 
 
+_SIDE = threading.local()
+
+
+def _side_streams():
+    """Two non-blocking streams per device (per thread) for solve_many."""
+    dev = torch.cuda.current_device()
+    per = getattr(_SIDE, "streams", None)
+    if per is None:
+        per = _SIDE.streams = {}
+    st = per.get(dev)
+    if st is None:
+        st = per[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return st
+
+
+def solve_many(problems, method: str = "saa", spec: SketchSpec | None = None,
+               opts: SolverOptions | None = None) -> list[SolveResult]:
+    """Independent solves, each the same as solve(problem, method, spec,
+    opts) (bitwise: the same kernels on the same data), enqueued back to
+    back on two streams with one host synchronisation for the batch.  On the
+    B200 the reduced solve of problem i (a latency-bound chain on a few SMs)
+    then runs beside the HBM-bound sketch and residual passes of its
+    neighbours instead of leaving the other SMs idle, and the host-side
+    turnaround between solves disappears.  Sketch-and-apply on one device is
+    batched; other methods and device lists run one solve at a time."""
+    problems = list(problems)
+    opts = opts or SolverOptions()
+    if method != "saa" or (opts.devices is not None and len(opts.devices) > 1):
+        return [solve(p, method, spec, opts) for p in problems]
+    if opts.devices is not None:
+        with torch.cuda.device(opts.devices[0]):
+            return solve_many(problems, method, spec, replace(opts, devices=None))
+    require_cuda()
+    if not problems:
+        return []
+    caller = torch.cuda.current_stream()
+    streams = _side_streams()
+    pinned = torch.zeros((len(problems), 3), dtype=torch.float64, pin_memory=True)
+    work = []
+    for i, prob in enumerate(problems):
+        A, b = prob.A, prob.b
+        if A.rows < A.cols:
+            raise ShapeError(f"need rows >= cols, got {A.rows}x{A.cols}")
+        op_spec = _operator_spec(spec, "saa", A.rows, A.cols, opts.d_factor)
+        st = streams[i & 1]
+        st.wait_stream(caller)
+        with torch.cuda.stream(st):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            op = build_sketch(op_spec, A.rows)
+            SA, Sb, A_dev, lda, b_dev = sketch_operands_device(op, A, b)
+            d = op.target_dim
+            x_dev, check = qr_solve_device_async(SA, d, Sb, d, A.cols, flags=pinned[i, :2])
+            ev1.record()
+            out = pinned[i, 2:]
+            if isinstance(A, SparseMatrix):
+                indptr, indices, values = A.device_arrays()
+                _native.call("skl_residual_csr_async", _native.ptr(indptr), _native.ptr(indices),
+                             _native.ptr(values), A.rows, A.cols, _native.ptr(x_dev),
+                             _native.ptr(b_dev), out.data_ptr(), current_stream())
+            else:
+                _native.call("skl_residual_dense_async", _native.ptr(A_dev), A.rows, A.cols, lda,
+                             _native.ptr(x_dev), _native.ptr(b_dev), out.data_ptr(),
+                             current_stream())
+            work.append((prob, op_spec, d, SA, Sb, A_dev, lda, b_dev, x_dev, check, ev0, ev1, st))
+    for st in streams:
+        caller.wait_stream(st)
+    for st in streams:
+        st.synchronize()
+    results = []
+    for i, (prob, op_spec, d, SA, Sb, A_dev, lda, b_dev, x_dev, check, ev0, ev1, st) in enumerate(work):
+        A = prob.A
+        with torch.cuda.stream(st):
+            try:
+                x_fix = check()
+            except SingularFactorError as exc:
+                raise SingularFactorError(
+                    f"sketched matrix ({op_spec.kind}, d={d}) is rank deficient: {exc}; "
+                    f"a larger embedding dimension may help") from exc
+            rnorm = float(pinned[i, 2])
+            if x_fix is not None:  # the CholeskyQR path handed over to Householder
+                x_dev = x_fix
+                rnorm = _residual_device(A, A_dev, lda, b_dev, x_dev)
+        wall = ev0.elapsed_time(ev1) * 1e-3
+        if isinstance(A, DenseMatrix) and A.on_device:
+            x_dev.record_stream(caller)  # handed to the caller's stream
+            x = x_dev
+        else:
+            x = x_dev.cpu().numpy()
+        results.append(SolveResult(x=Vector._of_solution(x, rnorm), method="saa",
+                                   sketch=op_spec.kind, d=d, iterations=0, residual_norm=rnorm,
+                                   termination="direct", wall_time_s=wall))
+    return results
+
+
 def solve(problem: LeastSquaresProblem, method: str = "lsqr", spec: SketchSpec | None = None,
           opts: SolverOptions | None = None) -> SolveResult:
     """Dispatch (solvers.py:364-398); wall_time_s covers the full path.

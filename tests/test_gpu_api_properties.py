@@ -301,3 +301,26 @@ def test_dispatcher_rejects_bad_requests():
     with pytest.raises(E.ShapeError):
         E.solve(wide, "saa")
     assert E.solve(dense_problem(545, 40, 4), "lsqr").wall_time_s > 0
+
+
+def test_solve_many_equals_solve_bitwise():
+    """solve_many (two streams, one host sync) returns, for every problem,
+    exactly what solve() returns for it alone -- dense device, dense host and
+    CSR operands, several sketch kinds, repeated problems."""
+    probs = [E.generate_problem(E.ProblemSpec(m=3000 + 100 * i, n=20 + i, kappa=10.0 ** (i % 4),
+                                              beta=1e-6, seed=700 + i)) for i in range(5)]
+    rng = np.random.default_rng(3)
+    csr = scipy.sparse.random(4000, 40, density=0.05, random_state=rng, format="csr")
+    probs.append(E.LeastSquaresProblem(E.SparseMatrix.from_scipy(csr), E.Vector(rng.standard_normal(4000))))
+    dense_h = rng.standard_normal((2500, 30))
+    probs.append(E.LeastSquaresProblem(E.DenseMatrix(np.asfortranarray(dense_h)),
+                                       E.Vector(dense_h @ rng.standard_normal(30))))
+    probs.append(probs[0])
+    for kind in ("countsketch", "srht", "gaussian"):
+        spec = E.SketchSpec(kind, 1, seed=11)
+        many = E.solve_many(probs, "saa", spec)
+        for p, r in zip(probs, many):
+            one = E.solve(p, "saa", spec)
+            assert np.array_equal(host(r.x.data), host(one.x.data))
+            assert r.residual_norm == one.residual_norm
+            assert r.d == one.d and r.method == "saa"
