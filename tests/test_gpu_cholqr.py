@@ -122,3 +122,44 @@ def test_cholqr_not_used_outside_its_sizes():
     assert not cholqr_enabled(512, 511)   # N = 512 = d: square augmented system
     assert not cholqr_enabled(4096, 512)  # N = 513 > 512
     assert cholqr_enabled(4096, 511)
+
+
+def test_cholqr_smallest_systems():
+    for d, n in [(3, 1), (4, 2), (40, 1), (33, 31), (34, 32)]:
+        if not cholqr_enabled(d, n):
+            continue
+        SA, Sb = system(d, n, seed=d * 7 + n)
+        x, _ = cqr(SA, Sb)
+        want = oracle_x(SA, Sb)
+        assert np.linalg.norm(x - want) / np.linalg.norm(want) <= 1e-12
+
+
+def test_cholqr_non_finite_input_hands_over():
+    SA, Sb = system(300, 20, seed=4)
+    SA[5, 3] = np.nan
+    t = torch.from_numpy(np.asfortranarray(SA)).cuda().t().contiguous().t()
+    b = torch.from_numpy(Sb).cuda()
+    x, check = qr_solve_device_async(t, 300, b, 300, 20)
+    torch.cuda.synchronize()
+    try:
+        x2 = check()
+    except SingularFactorError:
+        return  # Householder decided (NaN diagonal fails the rank check)
+    assert x2 is not None  # never silently accepted from the CholeskyQR path
+
+
+def test_solve_many_rank_deficient_member_raises_like_solve():
+    import paper_2409_14309_b200 as E
+
+    rng = np.random.default_rng(8)
+    A = np.asfortranarray(rng.standard_normal((400, 12)))
+    A[:, 5] = A[:, 2]
+    good = E.LeastSquaresProblem(E.DenseMatrix(np.asfortranarray(rng.standard_normal((400, 12)))),
+                                 E.Vector(rng.standard_normal(400)))
+    bad = E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(rng.standard_normal(400)))
+    spec = E.SketchSpec("countsketch", 1, seed=2)
+    with pytest.raises(SingularFactorError) as one:
+        E.solve(bad, "saa", spec)
+    with pytest.raises(SingularFactorError) as many:
+        E.solve_many([good, bad, good], "saa", spec)
+    assert str(one.value) == str(many.value)
