@@ -296,12 +296,13 @@ __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
 // -------------------------------------------------------------- Cholesky
 struct CholParams {
   const double* Gt;    // Gram, upper tiles
-  int nb;
+  int nb;              // block columns of this factorisation (= cluster CTAs)
   int64_t N;
-  double shift_coef;   // > 0: G += shift_coef * trace(G) * I (first iteration)
+  double shift_coef;   // > 0: G += shift_coef * trace(G) * I (first iteration; to == 0, all tiles)
   double* Rt;          // R, upper tiles
   double* Rinv;        // inverses of R's diagonal tiles [nb][1024]
   int* flag;           // set on a non-positive / non-finite pivot
+  int to;              // tile offset: this cluster factors diagonal block [to, to + nb)
 };
 
 #ifdef CQ_FACTOR_CLOCKS
@@ -554,11 +555,11 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
   // my column's Gram tiles, all copies in flight at once (8-byte cp.async;
   // past N: zero-filled, identity on the diagonal below)
   for (int I = 0; I <= J; ++I) {
-    const double* src = p.Gt + cq_tile(I, J) * 1024;
+    const double* src = p.Gt + cq_tile(I + p.to, J + p.to) * 1024;
     double* dst = tile(I);
     for (int e = tid; e < 1024; e += CQ_CHOL_NT) {
       const int r = e & 31, c = e >> 5;
-      const bool ok = (int64_t)I * 32 + r < p.N && (int64_t)J * 32 + c < p.N;
+      const bool ok = (int64_t)(I + p.to) * 32 + r < p.N && (int64_t)(J + p.to) * 32 + c < p.N;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + c * CQ_LD + r)),
                    "l"(src + e), "r"(ok ? 8 : 0)
                    : "memory");
@@ -567,7 +568,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
-    const int64_t gi = (int64_t)J * 32 + lane;
+    const int64_t gi = (int64_t)(J + p.to) * 32 + lane;
     if (gi >= p.N) tile(J)[lane * (CQ_LD + 1)] = 1.0;
     if (p.shift_coef > 0.0) {
       // the same fixed-order trace in every CTA
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
   cq_arrive();
   cq_wait();
   if (J == 0 && warp == 0) {
-    cq_factor(tile(0), srow, p.Rt, p.flag);
+    cq_factor(tile(0), srow, p.Rt + cq_tile(p.to, p.to) * 1024, p.flag);
     cq_push(tile(0), 0, nb, Us, mbar, 0);
   }
   for (int K = 0; K < nb - 1; ++K) {
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
       // U_KK pushed by CTA K, then R(K, J)
       mbar_wait_cluster(&mbar[buf], (uint32_t)((K >> 1) & 1));
       CQ_PROBE(2 + 4 * K);
-      if (warp == 0) cq_rowsolve(tile(K), Us[buf], p.Rt + cq_tile(K, J) * 1024);
+      if (warp == 0) cq_rowsolve(tile(K), Us[buf], p.Rt + cq_tile(K + p.to, J + p.to) * 1024);
       __syncthreads();
       if (tid == 0 && K + 2 < J) mbar_arrive_expect_tx(&mbar[buf], CQ_PUSH_BYTES);
     }
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
         cq_tile_update<1, 2>(tile(J), tile(K), false, 0, tile(K), warp >> 1, (warp & 1) * 2);
       __syncthreads();
       if (warp == 0) {
-        cq_factor(tile(J), srow, p.Rt + cq_tile(J, J) * 1024, p.flag);
+        cq_factor(tile(J), srow, p.Rt + cq_tile(J + p.to, J + p.to) * 1024, p.flag);
         cq_push(tile(J), J, nb, Us, mbar, (K + 1) & 1);
       }
     }
@@ -621,11 +622,176 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
     }
     CQ_PROBE(5 + 4 * K);
   }
-  if (warp == 0) cq_diag_inverse(tile(J), p.Rinv + (int64_t)J * 1024, Us[0]);
+  if (warp == 0) cq_diag_inverse(tile(J), p.Rinv + (int64_t)(J + p.to) * 1024, Us[0]);
   CQ_PROBE(70);
   // shared memory stays alive until every remote reader is done
   cq_arrive();
   cq_wait();
+}
+
+// ------------------------------------------- Cholesky beyond 16 block columns
+// N > 512: right-looking over super-blocks of up to 16 tiles.  For the
+// super-block [to, to + nbs): the cluster kernel factors its diagonal block,
+// cqr_trirow_kernel solves the block row R(I, J) = R_II^{-T} (G(I, J) -
+// sum_{to <= K < I} R(K, I)^T R(K, J)) for every later tile column J (one CTA
+// per column, the tile rows in order), cqr_syrk_kernel applies
+// G(I, J) -= sum_K R(K, I)^T R(K, J) to the trailing tiles.  The shift of
+// the first factorisation is applied once beforehand (cqr_shift_kernel),
+// because the trailing updates change the later diagonal tiles.
+constexpr int CQ_MAXNB_BIG = 33;  // N <= 1056
+
+// acc += A^T B for 32 x 32 global tiles (column-major, ld 32), one warp.
+__device__ __forceinline__ void cq_gtile_mma_tn(double (&acc)[2][4][4], const double* A,
+                                                const double* B) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double af[8][2][2], bf[8][4];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) af[ks][mt][h] = __ldcg(A + (mt * 16 + h * 8 + g) * 32 + ks * 4 + tq);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldcg(B + (nt * 8 + g) * 32 + ks * 4 + tq);
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], af[ks][mt][0], af[ks][mt][1], bf[ks][nt]);
+}
+
+// Fixed-order fold of 8 warps' accumulators into red[0..3] -> sum tile (column-major).
+__device__ __forceinline__ void cq_fold8(double (&acc)[2][4][4], double (*red)[1024]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  auto spill = [&](int w, bool add) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          double& r = red[w][(nt * 8 + 2 * tq + (h & 1)) * 32 + mt * 16 + g + (h >= 2 ? 8 : 0)];
+          r = add ? r + acc[mt][nt][h] : acc[mt][nt][h];
+        }
+  };
+  if (warp >= 4) spill(warp - 4, false);
+  __syncthreads();
+  if (warp < 4) spill(warp, true);
+  __syncthreads();
+}
+
+struct TriParams {
+  double* Gt;         // Gram (updated), tile layout
+  double* Rt;         // R tiles (diagonal block [to, to+nbs) factored)
+  const double* Rinv; // inverses of R's diagonal tiles
+  int to, nbs, nb;
+};
+
+__global__ void __launch_bounds__(256) cqr_trirow_kernel(const TriParams p) {
+  __shared__ double red[4][1024];
+  __shared__ double Ts[32 * 33];
+  pdl_enter();
+  const int J = p.to + p.nbs + blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  for (int I = p.to; I < p.to + p.nbs; ++I) {
+    double acc[2][4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+    for (int K = p.to + warp; K < I; K += 8)
+      cq_gtile_mma_tn(acc, p.Rt + cq_tile(K, I) * 1024, p.Rt + cq_tile(K, J) * 1024);
+    cq_fold8(acc, red);
+    const double* gij = p.Gt + cq_tile(I, J) * 1024;
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      const double sum = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
+      Ts[(e & 31) * 33 + (e >> 5)] = __ldcg(gij + e) - sum;  // Ts[k][n] row-major
+    }
+    __syncthreads();
+    // R(I, J) = Rinv_II^T T: warp w computes fragment (mt, nt) = (w / 4, w % 4)
+    {
+      const int mt = warp >> 2, nt = warp & 3;
+      const double* ri = p.Rinv + (int64_t)I * 1024;
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = ks * 4 + tq;
+        const double a0 = __ldcg(ri + (mt * 16 + g) * 32 + k);       // Rinv[k][m]
+        const double a1 = __ldcg(ri + (mt * 16 + 8 + g) * 32 + k);
+        const double b0 = Ts[k * 33 + nt * 8 + g];
+        cq_dmma(q, a0, a1, b0);
+      }
+      double* out = p.Rt + cq_tile(I, J) * 1024;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int r = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+        out[c * 32 + r] = q[h];
+      }
+    }
+    __syncthreads();  // R(I, J) visible to the next tile row of this column
+  }
+}
+
+__global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p) {
+  __shared__ double red[4][1024];
+  pdl_enter();
+  int jj = (int)((sqrtf(8.0f * blockIdx.x + 1.0f) - 1.0f) * 0.5f);
+  while ((jj + 1) * (jj + 2) / 2 <= (int)blockIdx.x) ++jj;
+  while (jj * (jj + 1) / 2 > (int)blockIdx.x) --jj;
+  const int ii = (int)blockIdx.x - jj * (jj + 1) / 2;
+  const int base = p.to + p.nbs, I = base + ii, J = base + jj;
+  const int warp = threadIdx.x >> 5;
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+  for (int K = p.to + warp; K < p.to + p.nbs; K += 8)
+    cq_gtile_mma_tn(acc, p.Rt + cq_tile(K, I) * 1024, p.Rt + cq_tile(K, J) * 1024);
+  cq_fold8(acc, red);
+  double* gij = p.Gt + cq_tile(I, J) * 1024;
+  for (int e = threadIdx.x; e < 1024; e += 256)
+    gij[e] = __ldcg(gij + e) - (((red[0][e] + red[1][e]) + red[2][e]) + red[3][e]);
+}
+
+// G += shift_coef * trace(G) * I over the first N diagonal entries, and
+// fro2 = ||SA||_F^2 (the first n diagonal entries of the unshifted G), both
+// in a fixed order.  One CTA.
+__global__ void __launch_bounds__(1024) cqr_shift_kernel(double* Gt, int64_t N, int64_t n,
+                                                         double shift_coef, double* fro2) {
+  __shared__ double red[2][32];
+  pdl_enter();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double t = 0.0, f = 0.0;
+  for (int64_t i = tid; i < N; i += 1024) {
+    const double v = Gt[cq_tile((int)(i >> 5), (int)(i >> 5)) * 1024 + (i & 31) * 33];
+    t += v;
+    if (i < n) f += v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = t;
+    red[1][warp] = f;
+  }
+  __syncthreads();
+  double tr = 0.0, fr = 0.0;
+  for (int w = 0; w < 32; ++w) {
+    tr += red[0][w];
+    fr += red[1][w];
+  }
+  if (tid == 0) *fro2 = fr;
+  for (int64_t i = tid; i < N; i += 1024)
+    Gt[cq_tile((int)(i >> 5), (int)(i >> 5)) * 1024 + (i & 31) * 33] += shift_coef * tr;
 }
 
 // ------------------------------------------------------------------ TRSM
@@ -670,8 +836,11 @@ __device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8
     for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(rk + (nt * 8 + g) * 32 + ks * 4 + tq);
 }
 
+// QS: earlier Q blocks kept in shared memory (nb <= 16); else read back
+// from the global Q (L2) -- small shared memory, several CTAs per SM.
+template <bool QS>
 __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p) {
-  extern __shared__ double qsm[];  // Qs[c * CQ_QLD + r], c < nb * 32
+  extern __shared__ double qsm[];  // Qs[c * CQ_QLD + r], c < nb * 32 (QS only)
   __shared__ double red[CQ_TRSM_WARPS][16 * 33];
   __shared__ double Ts[16 * 33];
   pdl_enter();
@@ -695,13 +864,22 @@ __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p
     while (K < J) {
       const int Kn = K + CQ_TRSM_WARPS;
       if (Kn < J) cq_trsm_fetch_r(p.Rt + cq_tile(Kn, J) * 1024, bn);
+      double qa0[8], qa1[8];
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int k = K * 32 + ks * 4 + tq;
-        const double a0 = Qs[k * CQ_QLD + g], a1 = Qs[k * CQ_QLD + g + 8];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], a0, a1, bf[ks][nt]);
+        if (QS) {
+          qa0[ks] = Qs[k * CQ_QLD + g];
+          qa1[ks] = Qs[k * CQ_QLD + g + 8];
+        } else {  // rows past d were never written: zero
+          qa0[ks] = r0 + g < d ? __ldcg(p.Q + (int64_t)k * p.ldq + r0 + g) : 0.0;
+          qa1[ks] = r0 + g + 8 < d ? __ldcg(p.Q + (int64_t)k * p.ldq + r0 + g + 8) : 0.0;
+        }
       }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qa0[ks], qa1[ks], bf[ks][nt]);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
@@ -746,7 +924,8 @@ __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p
       for (int h = 0; h < 4; ++h) {
         const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
         const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
-        Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
+        if (QS) Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
+        // (read-back path: only tiles K < J <= nb - 1 are read, all below N)
         if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
       }
     }
@@ -841,6 +1020,7 @@ __global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p) {
 }
 
 struct SolveParams {
+  const double* fro2;  // ||SA||_F^2 when the shift kernel ran (G1 shifted in place), else null
   const double* G1t;   // Gram of M (unshifted): ||SA||_F from its diagonal
   const double* Rt;    // R = R2 R1, upper tiles (order N = n + 1)
   const double* Rinv;  // inverses of its diagonal tiles
@@ -868,7 +1048,7 @@ __device__ __forceinline__ void cq_bs_fetch(const double* Rt, const double* Rinv
                                             double (&c)[32]) {
   const int tid = threadIdx.x;
   const int64_t lo = (int64_t)b * 32;
-  if (tid < lo) {
+  if (tid < lo && tid < CQ_SOLVE_ROWS) {
     const double* rc = Rt + cq_tile(tid >> 5, b) * 1024 + (tid & 31);
 #pragma unroll
     for (int j = 0; j < 32; ++j) c[j] = __ldg(rc + j * 32);
@@ -901,7 +1081,7 @@ __device__ void cq_backsolve(const double* Rt, const double* Rinv, int64_t n, do
     }
     __syncthreads();
     double t0 = 0.0, t1 = 0.0;
-    const bool mine = tid < lo;
+    const bool mine = tid < lo && tid < CQ_SOLVE_ROWS;
     if (mine) {
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
@@ -909,8 +1089,22 @@ __device__ void cq_backsolve(const double* Rt, const double* Rinv, int64_t n, do
         t1 = fma(c[j + 1], xb[j + 1], t1);
       }
     }
+    // rows 512 .. 1055 (n > 512): a second row per thread, loaded at use
+    const int64_t i2 = tid + CQ_SOLVE_ROWS;
+    double s2 = 0.0;
+    if (tid < CQ_SOLVE_ROWS && i2 < lo) {
+      const double* rc = Rt + cq_tile((int)(i2 >> 5), b) * 1024 + (i2 & 31);
+      double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        u0 = fma(__ldg(rc + j * 32), xb[j], u0);
+        u1 = fma(__ldg(rc + (j + 1) * 32), xb[j + 1], u1);
+      }
+      s2 = u0 + u1;
+    }
     if (b > 0) cq_bs_fetch(Rt, Rinv, b - 1, c);
     if (mine) ys[tid] -= t0 + t1;
+    if (tid < CQ_SOLVE_ROWS && i2 < lo) ys[i2] -= s2;
     __syncthreads();
   }
 }
@@ -966,37 +1160,63 @@ __device__ void cq_fwdsolve_t(const double* Rt, const double* Rinv, int64_t n, d
         t1 = fma(c[j + 1], zb[j + 1], t1);
       }
     }
+    const int64_t i2 = tid + CQ_SOLVE_ROWS;  // rows 512 .. 1055
+    const bool mine2 = tid < CQ_SOLVE_ROWS && i2 >= lo + 32 && i2 < n;
+    double s2 = 0.0;
+    if (mine2) {
+      const double2* rc = reinterpret_cast<const double2*>(Rt + cq_tile(b, (int)(i2 >> 5)) * 1024 + (i2 & 31) * 32);
+      double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double2 v = __ldg(rc + j);
+        u0 = fma(v.x, zb[2 * j], u0);
+        u1 = fma(v.y, zb[2 * j + 1], u1);
+      }
+      s2 = u0 + u1;
+    }
     if (b + 1 < nbn) cq_fs_fetch(Rt, Rinv, b + 1, n, c);
     if (mine) ys[tid] -= t0 + t1;
+    if (mine2) ys[i2] -= s2;
     __syncthreads();
   }
 }
 
 // Rank check (diag R vs 1e-14 ||SA||_F), y = R[:n, n], x = R[:n,:n]^{-1} y.
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolveParams p) {
-  __shared__ double ys[CQ_SOLVE_ROWS];
+  __shared__ double ys[CQ_MAXNB_BIG * 32];
   __shared__ double xb[32];
   __shared__ double red[CQ_SOLVE_NT / 32];
   __shared__ unsigned long long first_bad;
   pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = p.n;
-  double s = tid < n ? cq_rt(p.G1t, tid, tid) : 0.0;
-  const double dg = tid < n ? cq_rt(p.Rt, tid, tid) : 1.0;
-  if (tid < n) ys[tid] = cq_rt(p.Rt, tid, n);
+  double s = 0.0;
+  double dmax = 0.0, dmin = INFINITY;
+  if (tid == 0) first_bad = ~0ull;
+  __syncthreads();
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) {  // rows beyond 511 in a second pass
+    if (p.fro2 == nullptr) s += cq_rt(p.G1t, i, i);
+    const double dgi = cq_rt(p.Rt, i, i);
+    ys[i] = cq_rt(p.Rt, i, n);
+    dmax = fmax(dmax, dgi);
+    dmin = fmin(dmin, dgi);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) red[warp] = s;
-  if (tid == 0) first_bad = ~0ull;
   __syncthreads();
   double fro2 = 0.0;
+  if (p.fro2 != nullptr) {
+    fro2 = *p.fro2;
+  } else {
 #pragma unroll
-  for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) fro2 += red[w];
+    for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) fro2 += red[w];
+  }
   const double fro = sqrt(fro2);
-  if (tid < n && (!(fro > 0.0) || !(dg >= CQ_RANK_TOL * fro)))
-    atomicMin(&first_bad, (unsigned long long)tid);
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT)
+    if (!(fro > 0.0) || !(cq_rt(p.Rt, i, i) >= CQ_RANK_TOL * fro))
+      atomicMin(&first_bad, (unsigned long long)i);
   // diagonal extremes (all entries positive by construction)
-  double dmax = tid < n ? dg : 0.0, dmin = tid < n ? dg : INFINITY;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -1020,21 +1240,21 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
     *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
   }
   cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
-  if (tid < n) p.x[tid] = ys[tid];
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] = ys[i];
 }
 
 // x += R^{-1} R^{-T} g
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
-  __shared__ double ys[CQ_SOLVE_ROWS];
+  __shared__ double ys[CQ_MAXNB_BIG * 32];
   __shared__ double xb[32];
   pdl_enter();
   const int64_t n = p.n;
   const int tid = threadIdx.x;
-  if (tid < n) ys[tid] = p.g[tid];
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) ys[i] = p.g[i];
   __syncthreads();
   cq_fwdsolve_t(p.Rt, p.Rinv, n, ys, xb);
   cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
-  if (tid < n) p.x[tid] += ys[tid];
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] += ys[i];
 }
 
 // r = b - A x, rows split over CTAs: 64 rows x 4 column quarters per CTA.
@@ -1094,7 +1314,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1123,6 +1343,7 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oBadV = take(8);
   w.oRt = take(nt * 1024 * 8);
   w.oRi = take((size_t)nb * 1024 * 8);
+  w.oFro = take(8);
   w.bytes = off;
   return w;
 }
@@ -1164,7 +1385,7 @@ int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsign
 }
 
 int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
-            int* flag, bool pdl, cudaStream_t st) {
+            int* flag, bool pdl, cudaStream_t st, int to = 0) {
   static std::once_flag attr_set[64];
   const size_t smem_max = ((size_t)CQ_MAXNB * CQ_TILE + 32) * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
@@ -1174,7 +1395,7 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
     return SKL_OK;
   });
   if (arc) return arc;
-  CholParams cp{Gt, nb, N, shift_coef, Rt, Rinv, flag};
+  CholParams cp{Gt, nb, N, shift_coef, Rt, Rinv, flag, to};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nb);
   cfg.blockDim = dim3(CQ_CHOL_NT);
@@ -1193,20 +1414,44 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
   return SKL_OK;
 }
 
+// Cholesky of the tile-layout Gram: one cluster factorisation for nb <= 16,
+// else right-looking over 16-tile super-blocks (cluster kernel on the
+// diagonal block, block-row solve, trailing SYRK).  `shift_coef` only on the
+// single-cluster path (the blocked path shifts beforehand).
+int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
+                int* flag, bool pdl, cudaStream_t st) {
+  if (nb <= CQ_MAXNB) return cq_chol(Gt, nb, N, shift_coef, Rt, Rinv, flag, pdl, st);
+  for (int to = 0; to < nb; to += CQ_MAXNB) {
+    const int nbs = std::min(CQ_MAXNB, nb - to);
+    int rc = cq_chol(Gt, nbs, N, 0.0, Rt, Rinv, flag, pdl, st, to);
+    if (rc) return rc;
+    const int rest = nb - to - nbs;
+    if (rest == 0) break;
+    TriParams tp{Gt, Rt, Rinv, to, nbs, nb};
+    SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), 0, st, true, tp));
+    SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2)), dim3(256), 0, st,
+                      true, tp));
+  }
+  return SKL_OK;
+}
+
 int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* Rinv, double* Q,
             int64_t ldq, bool pdl, cudaStream_t st) {
   static std::once_flag attr_set[64];
-  const size_t smem_max = (size_t)CQ_MAXNB * 32 * CQ_QLD * sizeof(double);
+  const size_t smem_max = (size_t)CQ_MAXNB_BIG * 32 * CQ_QLD * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
-    SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem_max));
     return SKL_OK;
   });
   if (arc) return arc;
   TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
-  SKL_CUDA(launch_k(cqr_trsm_kernel, dim3(grid), dim3(CQ_TRSM_NT), (size_t)nb * 32 * CQ_QLD * sizeof(double),
-                    st, pdl, tp));
+  // (cqr_trsm_kernel<false>, reading earlier Q blocks back from L2 instead
+  // of shared memory, measured no faster at 8192 x 1025: the kernel holds
+  // one CTA per SM through its registers either way)
+  SKL_CUDA(launch_k(cqr_trsm_kernel<true>, dim3(grid), dim3(CQ_TRSM_NT),
+                    (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
   return SKL_OK;
 }
 
@@ -1216,7 +1461,7 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* 
 // more than N (a square augmented system is rank deficient by construction).
 extern "C" int skl_cqr_supported(int64_t d, int64_t n) {
   const int64_t N = n + 1;
-  return (n >= 1 && N <= 32 * CQ_MAXNB && d > N) ? 1 : 0;
+  return (n >= 1 && N <= 32 * CQ_MAXNB_BIG && d > N) ? 1 : 0;
 }
 
 // Enqueue the CholeskyQR2 solve; *bad_col (pinned host or device) receives
@@ -1266,15 +1511,26 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     const CqCols Q1{Q, ldq, nullptr, N, d};
     const double u = 0.5 * 2.220446049250313e-16;
     const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * u;
+    const bool big = nb > CQ_MAXNB;
+    double* fro2 = (double*)P(w.oFro);
     if ((rc = cq_gram(M, N, nb, part, G1, cnt, false, st))) break;
-    if ((rc = cq_chol(G1, nb, N, shift, R1, I1, flag, true, st))) break;
+    if (big) {  // shift once, before the super-block updates change the diagonal
+      if ((e = launch_k(cqr_shift_kernel, dim3(1), dim3(1024), 0, st, true, G1, N, n, shift,
+                        fro2)) != cudaSuccess) {
+        set_error("cqr_solve: %s", cudaGetErrorString(e));
+        rc = SKL_ERR_CUDA;
+        break;
+      }
+    }
+    if ((rc = cq_chol_any(G1, nb, N, big ? 0.0 : shift, R1, I1, flag, true, st))) break;
     if ((rc = cq_trsm(M, N, nb, R1, I1, Q, ldq, true, st))) break;
     if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st))) break;
-    if ((rc = cq_chol(G2, nb, N, 0.0, R2, I2, flag, true, st))) break;
+    if ((rc = cq_chol_any(G2, nb, N, 0.0, R2, I2, flag, true, st))) break;
     double* Rt = (double*)P(w.oRt);
     double* Ri = (double*)P(w.oRi);
     ProdParams pp{R1, R2, I1, I2, Rt, Ri};
-    SolveParams sp{G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad), (double*)P(w.oBadV)};
+    SolveParams sp{big ? fro2 : nullptr, G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad),
+                   (double*)P(w.oBadV)};
     const size_t ysm = (size_t)N * sizeof(double);
 #define CQ_LAUNCH(call)                                                          \
   if ((e = (call)) != cudaSuccess) {                                             \

@@ -58,7 +58,9 @@ def cqr(SA, Sb, ld=None):
 
 
 SHAPES = [(100, 5), (200, 30), (200, 31), (300, 32), (300, 63), (400, 64), (800, 200),
-          (2048, 256), (1500, 300), (2048, 511)]
+          (2048, 256), (1500, 300), (2048, 511),
+          # N = n + 1 > 512: blocked Cholesky over 16-tile super-blocks
+          (2048, 512), (3000, 700), (8192, 1024), (4096, 1055)]
 
 
 @pytest.mark.parametrize("d,n", SHAPES)
@@ -119,9 +121,9 @@ def test_reduced_solve_paths_agree():
 
 
 def test_cholqr_not_used_outside_its_sizes():
-    assert not cholqr_enabled(512, 511)   # N = 512 = d: square augmented system
-    assert not cholqr_enabled(4096, 512)  # N = 513 > 512
-    assert cholqr_enabled(4096, 511)
+    assert not cholqr_enabled(512, 511)    # N = 512 = d: square augmented system
+    assert not cholqr_enabled(8192, 1056)  # N = 1057 > 1056
+    assert cholqr_enabled(4096, 511) and cholqr_enabled(8192, 1055)
 
 
 def test_cholqr_smallest_systems():
