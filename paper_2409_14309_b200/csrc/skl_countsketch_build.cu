@@ -160,9 +160,26 @@ __global__ void __launch_bounds__(PB_NT) owned_fill_kernel(
   }
   for (int j = tid; j < len; j += PB_NT) atomicAdd(&cnt[keys[j] >> 13], 1);
   __syncthreads();
-  if (tid == 0) {
-    int32_t run = 0;
-    for (int b = 0; b < d; ++b) {
+  {
+    // exclusive scan of cnt[0..d) into start[]: each thread a run of
+    // consecutive buckets, then warp and block scans of the run totals
+    __shared__ int32_t wsum[PB_NT / 32];
+    const int per = (d + PB_NT - 1) / PB_NT;
+    const int b0 = tid * per, b1 = min(d, b0 + per);
+    int32_t own = 0;
+    for (int b = b0; b < b1; ++b) own += cnt[b];
+    const int lane = tid & 31, wid = tid >> 5;
+    int32_t incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int32_t run = incl - own;
+    for (int w = 0; w < wid; ++w) run += wsum[w];
+    for (int b = b0; b < b1; ++b) {
       start[b] = run;
       run += cnt[b];
     }
