@@ -26,7 +26,8 @@ import torch  # noqa: E402
 
 import paper_2409_14309_b200 as E  # noqa: E402
 from paper_2409_14309_b200 import workloads as W  # noqa: E402
-from paper_2409_14309_b200.linalg import qr_solve_device  # noqa: E402
+from paper_2409_14309_b200.linalg import (cholqr_enabled, qr_solve_device,  # noqa: E402
+                                          reduced_solve_device)
 from paper_2409_14309_b200.sketch import (  # noqa: E402
     _countsketch_csr_device,
     _countsketch_dense_device,
@@ -113,7 +114,9 @@ def run(cfg_id: int, reps: int):
         vms, _ = timed_graph(lambda: _countsketch_dense_device(op, b.reshape(-1, 1), c.m, 1), reps)
         out.update(sb_ordered_walk_ms=round(vms, 4),
                    sb_gbs=round(8 * c.m / vms / 1e6, 1))
-        out["qr_ms"] = round(timed(lambda: qr_solve_device(SA, c.d, Sb[:, 0], c.d, c.n), 3), 3)
+        out["qr_ms"] = round(timed(lambda: reduced_solve_device(SA, c.d, Sb[:, 0], c.d, c.n), 3), 3)
+        out["qr_path"] = "cholqr2+csne" if cholqr_enabled(c.d, c.n) else "householder"
+        out["householder_qr_ms"] = round(timed(lambda: qr_solve_device(SA, c.d, Sb[:, 0], c.d, c.n), 3), 3)
         out["solve"] = solve_rate(Ac, b, "countsketch", c.d, c.n)
         return out
     lda = int(A.stride(1))

@@ -1,0 +1,10 @@
+# end-of-round evidence: every GPU test (full-size parity report), both bench
+# arms, per-config timings, headline launch list
+set -x
+mkdir -p gpurun_out
+SKL_PARITY_REPORT=gpurun_out/r02_parity_fullsize.jsonl timeout 2400 python -m pytest tests -m gpu -q -rf 2>&1 | tail -4
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench.out 2> gpurun_out/r02_bench.err; echo bench rc=$?
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_bench_ref.out 2>&1; echo ref rc=$?
+timeout 1200 python tools/bench_configs.py > gpurun_out/r02_configs.jsonl 2> gpurun_out/r02_configs.err; echo cfg rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r02_bench_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-solve --no-e2e --no-parity > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
