@@ -74,6 +74,10 @@ constexpr double CQ_RANK_TOL = 1e-14;     // linalg.py RANK_TOL
 // the solve hands over to Householder.  Config 2 (kappa = 1e8) sits at
 // 4.3e6.
 constexpr double CQ_DIAG_RATIO_MAX = 2e7;
+// Below this diagonal ratio (kappa ~< 4e4) CholeskyQR2's own x is accurate
+// to ~kappa u and the corrected semi-normal step is skipped (its kernels
+// return at once).
+constexpr double CQ_REFINE_RATIO = 1e3;
 
 __host__ __device__ __forceinline__ int64_t cq_tile(int I, int J) {
   return (int64_t)J * (J + 1) / 2 + I;
@@ -1020,6 +1024,7 @@ __global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p) {
 }
 
 struct SolveParams {
+  int* refine;         // set by solve_a: run the refinement step
   const double* fro2;  // ||SA||_F^2 when the shift kernel ran (G1 shifted in place), else null
   const double* G1t;   // Gram of M (unshifted): ||SA||_F from its diagonal
   const double* Rt;    // R = R2 R1, upper tiles (order N = n + 1)
@@ -1235,6 +1240,7 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
       mn = fmin(mn, ext[1][w]);
     }
     const bool broke = *p.flag != 0 || !(mx <= CQ_DIAG_RATIO_MAX * mn);
+    *p.refine = (mx <= CQ_REFINE_RATIO * mn) ? 0 : 1;
     const long long fb = first_bad == ~0ull ? -1 : (long long)first_bad;
     *p.bad_col = broke ? -2 : fb;
     *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
@@ -1245,9 +1251,11 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
 
 // x += R^{-1} R^{-T} g
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
+  pdl_enter();
+  if (*p.refine == 0) return;
   __shared__ double ys[CQ_MAXNB_BIG * 32];
   __shared__ double xb[32];
-  pdl_enter();
+  
   const int64_t n = p.n;
   const int tid = threadIdx.x;
   for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) ys[i] = p.g[i];
@@ -1260,10 +1268,12 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolvePar
 // r = b - A x, rows split over CTAs: 64 rows x 4 column quarters per CTA.
 __global__ void __launch_bounds__(256) cqr_resid_kernel(const double* A, int64_t lda,
                                                         const double* b, int64_t d, int64_t n,
-                                                        const double* x, double* r) {
+                                                        const double* x, double* r,
+                                                        const int* refine) {
   extern __shared__ double xs[];  // n
   __shared__ double part[4][64];
   pdl_enter();
+  if (*refine == 0) return;
   for (int64_t c = threadIdx.x; c < n; c += 256) xs[c] = x[c];
   __syncthreads();
   const int rl = threadIdx.x & 63, qc = threadIdx.x >> 6;
@@ -1287,8 +1297,10 @@ __global__ void __launch_bounds__(256) cqr_resid_kernel(const double* A, int64_t
 
 // g = A^T r, one warp per column (fixed shuffle tree).
 __global__ void __launch_bounds__(256) cqr_gemv_t_kernel(const double* A, int64_t lda, int64_t d,
-                                                         int64_t n, const double* r, double* g) {
+                                                         int64_t n, const double* r, double* g,
+                                                         const int* refine) {
   pdl_enter();
+  if (*refine == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= n) return;
@@ -1314,7 +1326,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1344,6 +1356,7 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oRt = take(nt * 1024 * 8);
   w.oRi = take((size_t)nb * 1024 * 8);
   w.oFro = take(8);
+  w.oRef = take(4);
   w.bytes = off;
   return w;
 }
@@ -1529,7 +1542,8 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     double* Rt = (double*)P(w.oRt);
     double* Ri = (double*)P(w.oRi);
     ProdParams pp{R1, R2, I1, I2, Rt, Ri};
-    SolveParams sp{big ? fro2 : nullptr, G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad),
+    int* refine = (int*)P(w.oRef);
+    SolveParams sp{refine, big ? fro2 : nullptr, G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad),
                    (double*)P(w.oBadV)};
     const size_t ysm = (size_t)N * sizeof(double);
 #define CQ_LAUNCH(call)                                                          \
@@ -1542,9 +1556,9 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     CQ_LAUNCH(launch_k(cqr_solve_a_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
     // corrected semi-normal step: r = Sb - SA x, g = SA^T r, x += R^{-1} R^{-T} g
     CQ_LAUNCH(launch_k(cqr_resid_kernel, dim3((unsigned)((d + 63) / 64)), dim3(256), ysm, st, true,
-                       SA, ldsa, Sb, d, n, (const double*)x, r));
+                       SA, ldsa, Sb, d, n, (const double*)x, r, (const int*)refine));
     CQ_LAUNCH(launch_k(cqr_gemv_t_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true,
-                       SA, ldsa, d, n, (const double*)r, g));
+                       SA, ldsa, d, n, (const double*)r, g, (const int*)refine));
     CQ_LAUNCH(launch_k(cqr_solve_b_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
 #undef CQ_LAUNCH
     e = cudaMemcpyAsync(bad_col, P(w.oBad), 8, cudaMemcpyDefault, st);
