@@ -937,6 +937,92 @@ __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p
   }
 }
 
+// Right-looking TRSM: the CTA's 16 rows of X live in shared memory as T;
+// for each block column J, Q_J = T_J Rinv_JJ (warps 0-3, 8 columns each),
+// then every later block takes T_L -= Q_J R(J, L) (warp w: L = J+1+w,
+// J+9+w, ...; the tile loads of a warp's first L are issued before Q_J is
+// formed).  The dependent chain per block column is one 16 x 32 x 32
+// product; the bulk of the work (16 N^2 / 2 FMA per CTA) runs at the fp64
+// tensor rate.
+__global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_rl_kernel(const TrsmParams p) {
+  extern __shared__ double tsm[];  // T[c * CQ_QLD + r], c < nb * 32; becomes Q
+  pdl_enter();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
+  const int64_t d = p.X.d;
+  const int ncol = p.nb * 32;
+  // T = X (16 rows x nb*32 columns, zero past N and d)
+  for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
+    const int r = e & 15, c = e >> 4;
+    const int64_t gr = r0 + r;
+    tsm[c * CQ_QLD + r] = (c < p.N && gr < d) ? __ldg(cq_col(p.X, c) + gr) : 0.0;
+  }
+  __syncthreads();
+  double bf[8][4];
+  for (int J = 0; J < p.nb; ++J) {
+    // this warp's first update tile of the step: loads in flight now
+    const int L0 = J + 1 + warp;
+    if (L0 < p.nb) cq_trsm_fetch_r(p.Rt + cq_tile(J, L0) * 1024, bf);
+    double qa[4] = {0.0, 0.0, 0.0, 0.0};
+    if (warp < 4) {
+      const double* rinv = p.Rinv + (int64_t)J * 1024;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = J * 32 + ks * 4 + tq;
+        const double a0 = tsm[k * CQ_QLD + g], a1 = tsm[k * CQ_QLD + g + 8];
+        cq_dmma(qa, a0, a1, __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq));
+      }
+    }
+    __syncthreads();  // every read of T_J done
+    if (warp < 4) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
+        const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
+        tsm[(J * 32 + c) * CQ_QLD + r] = qa[h];
+        if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
+      }
+    }
+    __syncthreads();  // Q_J visible
+    // T_L -= Q_J R(J, L), L > J
+    double qf0[8], qf1[8];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int k = J * 32 + ks * 4 + tq;
+      qf0[ks] = tsm[k * CQ_QLD + g];
+      qf1[ks] = tsm[k * CQ_QLD + g + 8];
+    }
+    for (int L = L0; L < p.nb; L += CQ_TRSM_WARPS) {
+      double bn[8][4];
+      const int Ln = L + CQ_TRSM_WARPS;
+      if (Ln < p.nb) cq_trsm_fetch_r(p.Rt + cq_tile(J, Ln) * 1024, bn);
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qf0[ks], qf1[ks], bf[ks][nt]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+          tsm[(L * 32 + c) * CQ_QLD + r] -= acc[nt][h];
+        }
+      if (Ln < p.nb) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = bn[ks][nt];
+      }
+    }
+    __syncthreads();  // T_{J+1} final before the next step reads it
+  }
+}
+
 // ----------------------------------------------------------------- solves
 // R = R2 R1 (upper, tile layout) and the inverses of its diagonal tiles
 // (R_II^{-1} = R1_II^{-1} R2_II^{-1}).  One CTA per upper tile, the K terms
@@ -1463,8 +1549,21 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* 
   // (cqr_trsm_kernel<false>, reading earlier Q blocks back from L2 instead
   // of shared memory, measured no faster at 8192 x 1025: the kernel holds
   // one CTA per SM through its registers either way)
-  SKL_CUDA(launch_k(cqr_trsm_kernel<true>, dim3(grid), dim3(CQ_TRSM_NT),
-                    (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
+  static const bool left_looking = env_flag("SKL_CQR_TRSM_LL");  // A/B knob
+  if (left_looking) {
+    SKL_CUDA(launch_k(cqr_trsm_kernel<true>, dim3(grid), dim3(CQ_TRSM_NT),
+                      (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
+  } else {
+    static std::once_flag rl_set[64];
+    const int rc = once_per_device(rl_set, [&]() -> int {
+      SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_max));
+      return SKL_OK;
+    });
+    if (rc) return rc;
+    SKL_CUDA(launch_k(cqr_trsm_rl_kernel, dim3(grid), dim3(CQ_TRSM_NT),
+                      (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
+  }
   return SKL_OK;
 }
 
