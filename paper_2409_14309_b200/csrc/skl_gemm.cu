@@ -217,6 +217,50 @@ __global__ void gemm_split_reduce_kernel(const double* part, int S, int64_t d, i
   }
 }
 
+// y = G x for one column (n == 1): the tile GEMM would spend 127 of every
+// 128 tile columns on padding; this is one HBM pass over G instead.  A warp
+// owns a row of G (K-contiguous: coalesced 16-byte loads, eight in flight
+// per lane), x (m doubles) is re-read from L2, and the row sum folds in a
+// fixed order (per-lane accumulators, then a shuffle tree): deterministic.
+constexpr int GV_WARPS = 8;
+__global__ void __launch_bounds__(GV_WARPS * 32) gemv_f64_rows_kernel(
+    const double* __restrict__ G, int64_t ldg, const double* __restrict__ x, int64_t m,
+    int64_t d, double* __restrict__ y, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * GV_WARPS + (threadIdx.x >> 5);
+  if (row >= d) return;
+  const double2* g2 = reinterpret_cast<const double2*>(G + row * ldg);
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const int64_t m2 = m / 2;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = lane;
+  for (; i + 7 * 32 < m2; i += 8 * 32) {
+    double2 gv[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      gv[u] = __ldcs(g2 + i + u * 32);
+      xv[u] = __ldg(x2 + i + u * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      a0 = fma(gv[u].x, xv[u].x, a0);
+      a1 = fma(gv[u].y, xv[u].y, a1);
+      a2 = fma(gv[u + 1].x, xv[u + 1].x, a2);
+      a3 = fma(gv[u + 1].y, xv[u + 1].y, a3);
+    }
+  }
+  for (; i < m2; i += 32) {
+    const double2 gv = __ldcs(g2 + i), xv = __ldg(x2 + i);
+    a0 = fma(gv.x, xv.x, a0);
+    a1 = fma(gv.y, xv.y, a1);
+  }
+  if ((m & 1) && lane == 0) a2 = fma(G[row * ldg + m - 1], x[m - 1], a2);
+  double t = (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) y[row] = accumulate ? y[row] + t : t;
+}
+
 }  // namespace skl
 
 using namespace skl;
@@ -231,6 +275,12 @@ extern "C" int skl_gemm_f64(const double* G, int64_t ldg, const double* A, int64
   SKL_REQUIRE(((uintptr_t)G & 15) == 0 && ((uintptr_t)A & 15) == 0 && ldg % 2 == 0 &&
                   (lda % 2 == 0 || n == 1),
               SKL_ERR_INVALID, "gemm_f64: operands must be 16-byte aligned with even leading dims");
+  if (n == 1) {  // one column: an HBM pass over G (gemv_f64_rows_kernel)
+    gemv_f64_rows_kernel<<<(unsigned)((d + GV_WARPS - 1) / GV_WARPS), GV_WARPS * 32, 0, st>>>(
+        G, ldg, A, m, d, C, accumulate);
+    SKL_CUDA_LAUNCH();
+    return SKL_OK;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -1,0 +1,29 @@
+"""Kernel-level breakdown of one warm SAA solve() for a BASELINE config
+(torch.profiler CUDA activity: every kernel and copy of the solve)."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import paper_2409_14309_b200 as E  # noqa: E402
+from paper_2409_14309_b200 import workloads as W  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+c = W.config(cfg)
+A, b, _ = W.make_problem(c, backend="torch")
+if c.gen == "csr":
+    A = E.SparseMatrix.from_scipy(A)
+else:
+    A = E.DenseMatrix(A)
+prob = E.LeastSquaresProblem(A=A, b=E.Vector(b))
+spec = E.SketchSpec(c.kind, 1, seed=W.SEED)
+opts = E.SolverOptions(d_factor=c.d / c.n)
+for _ in range(2):
+    E.solve(prob, "saa", spec, opts)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    E.solve(prob, "saa", spec, opts)
+    torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
