@@ -693,50 +693,100 @@ struct TriParams {
   int to, nbs, nb;
 };
 
+// One CTA per later tile column J: the column's nbs blocks T(I, J) sit in
+// shared memory (stride 33); step I solves R(I, J) = Rinv_II^T T(I, J)
+// (warp w: fragment (w / 4, w % 4)), then the warps update every later block
+// T(I', J) -= R(I, I')^T R(I, J) (I' = I+1 first, split over 4 warps by
+// fragment quarters; the others one block per warp) -- the dependent chain
+// per step is one small product, the rest runs beside it.
+__device__ __forceinline__ void cq_frag_load_tn(const double* A, int mt, int nt0, int nnt,
+                                                double (&af)[8][2], const double* B,
+                                                double (&bfr)[8][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) af[ks][h] = __ldcg(A + (mt * 16 + h * 8 + g) * 32 + ks * 4 + tq);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      bfr[ks][q] = q < nnt ? B[((nt0 + q) * 8 + g) * 33 + ks * 4 + tq] : 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(256) cqr_trirow_kernel(const TriParams p) {
-  __shared__ double red[4][1024];
-  __shared__ double Ts[32 * 33];
+  extern __shared__ double Tc[];  // [nbs][32 * 33]: T(I, J) column-major, stride 33
   pdl_enter();
   const int J = p.to + p.nbs + blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  for (int I = p.to; I < p.to + p.nbs; ++I) {
-    double acc[2][4][4];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-    for (int K = p.to + warp; K < I; K += 8)
-      cq_gtile_mma_tn(acc, p.Rt + cq_tile(K, I) * 1024, p.Rt + cq_tile(K, J) * 1024);
-    cq_fold8(acc, red);
-    const double* gij = p.Gt + cq_tile(I, J) * 1024;
-    for (int e = threadIdx.x; e < 1024; e += 256) {
-      const double sum = ((red[0][e] + red[1][e]) + red[2][e]) + red[3][e];
-      Ts[(e & 31) * 33 + (e >> 5)] = __ldcg(gij + e) - sum;  // Ts[k][n] row-major
-    }
-    __syncthreads();
-    // R(I, J) = Rinv_II^T T: warp w computes fragment (mt, nt) = (w / 4, w % 4)
+  for (int q = 0; q < p.nbs; ++q) {
+    const double* src = p.Gt + cq_tile(p.to + q, J) * 1024;
+    for (int e = threadIdx.x; e < 1024; e += 256) Tc[q * 1056 + (e >> 5) * 33 + (e & 31)] = __ldcg(src + e);
+  }
+  __syncthreads();
+  for (int q = 0; q < p.nbs; ++q) {
+    const int I = p.to + q;
+    double* T = Tc + q * 1056;
+    // R(I, J) = Rinv_II^T T (in place after every warp has read T)
+    const int mt = warp >> 2, nt = warp & 3;
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
     {
-      const int mt = warp >> 2, nt = warp & 3;
       const double* ri = p.Rinv + (int64_t)I * 1024;
-      double q[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int k = ks * 4 + tq;
-        const double a0 = __ldcg(ri + (mt * 16 + g) * 32 + k);       // Rinv[k][m]
-        const double a1 = __ldcg(ri + (mt * 16 + 8 + g) * 32 + k);
-        const double b0 = Ts[k * 33 + nt * 8 + g];
-        cq_dmma(q, a0, a1, b0);
-      }
-      double* out = p.Rt + cq_tile(I, J) * 1024;
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int r = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-        out[c * 32 + r] = q[h];
+        cq_dmma(r, __ldcg(ri + (mt * 16 + g) * 32 + k), __ldcg(ri + (mt * 16 + 8 + g) * 32 + k),
+                T[(nt * 8 + g) * 33 + k]);
       }
     }
-    __syncthreads();  // R(I, J) visible to the next tile row of this column
+    __syncthreads();
+    double* out = p.Rt + cq_tile(I, J) * 1024;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int rr = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+      T[c * 33 + rr] = r[h];
+      out[c * 32 + rr] = r[h];
+    }
+    __syncthreads();  // R(I, J) in T
+    // T(I', J) -= R(I, I')^T R(I, J): I' = I+1 by all 8 warps (one fragment
+    // each), then the rest one block per warp
+    auto update = [&](int qq, int mt0, int nmt, int nt0, int nnt) {
+      const double* A = p.Rt + cq_tile(I, p.to + qq) * 1024;  // R(I, I')
+      double acc[2][4][4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][b2][c] = 0.0;
+#pragma unroll
+      for (int m2 = 0; m2 < 2; ++m2) {
+        if (m2 >= nmt) break;
+        double af[8][2], bfr[8][4];
+        cq_frag_load_tn(A, mt0 + m2, nt0, nnt, af, T, bfr);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            if (q4 < nnt) cq_dmma(acc[m2][q4], af[ks][0], af[ks][1], bfr[ks][q4]);
+      }
+      double* Tq = Tc + qq * 1056;
+#pragma unroll
+      for (int m2 = 0; m2 < 2; ++m2) {
+        if (m2 >= nmt) break;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          if (q4 >= nnt) break;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int rr = (mt0 + m2) * 16 + g + (h >= 2 ? 8 : 0), c = (nt0 + q4) * 8 + 2 * tq + (h & 1);
+            Tq[c * 33 + rr] -= acc[m2][q4][h];
+          }
+        }
+      }
+    };
+    if (q + 1 < p.nbs) update(q + 1, warp >> 2, 1, warp & 3, 1);
+    for (int qq = q + 2 + warp; qq < p.nbs; qq += 8) update(qq, 0, 2, 0, 4);
+    __syncthreads();
   }
 }
 
@@ -1527,7 +1577,9 @@ int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, do
     const int rest = nb - to - nbs;
     if (rest == 0) break;
     TriParams tp{Gt, Rt, Rinv, to, nbs, nb};
-    SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), 0, st, true, tp));
+    const size_t tsm = (size_t)nbs * 1056 * sizeof(double);
+    SKL_CUDA(raise_smem_limit(cqr_trirow_kernel, tsm));
+    SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), tsm, st, true, tp));
     SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2)), dim3(256), 0, st,
                       true, tp));
   }
