@@ -1008,21 +1008,30 @@ __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_rl_kernel(const TrsmParam
     tsm[c * CQ_QLD + r] = (c < p.N && gr < d) ? __ldg(cq_col(p.X, c) + gr) : 0.0;
   }
   __syncthreads();
-  double bf[8][4];
+  double bf[8][4], bi[8];
+  // Rinv_JJ fragments of the next block column, loaded one step ahead
+  auto fetch_rinv = [&](int J) {
+    if (warp < 4 && J < p.nb) {
+      const double* rinv = p.Rinv + (int64_t)J * 1024;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
+    }
+  };
+  fetch_rinv(0);
   for (int J = 0; J < p.nb; ++J) {
     // this warp's first update tile of the step: loads in flight now
     const int L0 = J + 1 + warp;
     if (L0 < p.nb) cq_trsm_fetch_r(p.Rt + cq_tile(J, L0) * 1024, bf);
     double qa[4] = {0.0, 0.0, 0.0, 0.0};
     if (warp < 4) {
-      const double* rinv = p.Rinv + (int64_t)J * 1024;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int k = J * 32 + ks * 4 + tq;
         const double a0 = tsm[k * CQ_QLD + g], a1 = tsm[k * CQ_QLD + g + 8];
-        cq_dmma(qa, a0, a1, __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq));
+        cq_dmma(qa, a0, a1, bi[ks]);
       }
     }
+    fetch_rinv(J + 1);
     __syncthreads();  // every read of T_J done
     if (warp < 4) {
 #pragma unroll
