@@ -8,3 +8,7 @@ timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/
 timeout 1200 python tools/bench_configs.py > gpurun_out/r02_configs.jsonl 2> gpurun_out/r02_configs.err; echo cfg rc=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/r02_bench_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-solve --no-e2e --no-parity > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
+SKL_PROF_WARM_S=0.01 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r02_cqr_launches.csv python tools/prof_qr.py 2048 256 2 cholqr > /dev/null 2>&1; echo ncu2 rc=$?
+SKL_PROF_WARM_S=0.01 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r02_cqr_big_launches.csv python tools/prof_qr.py 8192 1024 1 cholqr > /dev/null 2>&1; echo ncu3 rc=$?

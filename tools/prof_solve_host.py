@@ -11,16 +11,18 @@ import torch  # noqa: E402
 import paper_2409_14309_b200 as E  # noqa: E402
 from paper_2409_14309_b200 import workloads as W  # noqa: E402
 
-c = W.config(2, kind="countsketch")
+c = W.config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 A, b, _ = W.make_problem(c, backend="torch")
-prob = E.LeastSquaresProblem(E.DenseMatrix(A), E.Vector(b))
-spec, opts = E.SketchSpec("countsketch", 1, seed=W.SEED), E.SolverOptions(d_factor=c.d / c.n)
+A = E.SparseMatrix.from_scipy(A) if c.gen == "csr" else E.DenseMatrix(A)
+prob = E.LeastSquaresProblem(A, E.Vector(b))
+spec, opts = E.SketchSpec(c.kind, 1, seed=W.SEED), E.SolverOptions(d_factor=c.d / c.n)
 for _ in range(5):
     E.solve(prob, "saa", spec, opts)
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 pr.enable()
-for _ in range(200):
+for _ in range(50):
     E.solve(prob, "saa", spec, opts)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(14)
+pstats.Stats(pr).sort_stats("cumtime").print_stats(14)

@@ -26,4 +26,8 @@ torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     E.solve(prob, "saa", spec, opts)
     torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
+rows = [(e.key, e.device_time_total, e.count) for e in prof.key_averages() if e.device_time_total > 0]
+tot = sum(r[1] for r in rows)
+for k, t, n in sorted(rows, key=lambda r: -r[1])[:25]:
+    print(f"{t / 1e3:9.3f} ms  x{n:<3d} {k[:70]}")
+print(f"{tot / 1e3:9.3f} ms  total device time (PDL-chained kernels include their early start)")
