@@ -857,6 +857,13 @@ struct TrsmParams {
   const double* Rinv;
   double* Q;
   int64_t ldq;
+  const double* Rf;   // R's tiles in B-fragment order (cqr_rfrag_kernel)
+  const double* Rfi;  // the diagonal tiles' inverses, same order
+  // block-row solve of the blocked Cholesky (GT): X = G(to.., J0..)^T, R and
+  // Rinv tiles offset by `to`, the result R(to.., J0..) written as tiles
+  const double* G;
+  double* Rout;
+  int to, J0;
 };
 
 // Q (rows r0 .. r0+15) = X R^{-1}: for each block column J,
@@ -888,6 +895,55 @@ __device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8
   for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(rk + (nt * 8 + g) * 32 + ks * 4 + tq);
+}
+
+// R tiles re-laid in the order the DMMA B fragments consume them: for each
+// tile, 16 rows of 32 double2 (q = ks * 2 + np holds bf[ks][2np], bf[ks][2np+1]
+// of every lane), so a warp's fetch of a tile is 16 fully used 512-byte loads
+// instead of 32 loads touching 8 separate 128-byte lines each -- the TRSM
+// streams all of R once per 16-row block, and the scattered loads made it
+// bound by the L1 wavefront rate rather than by the fp64 tensor pipe.
+// Blocks [0, nbs (nbs + 1) / 2): the upper tiles of the diagonal block that
+// starts at tile `to`; the next nbs blocks: its diagonal tiles' inverses.
+__global__ void __launch_bounds__(256) cqr_rfrag_kernel(const double* __restrict__ Rt,
+                                                        const double* __restrict__ Rinv,
+                                                        double* __restrict__ Rf,
+                                                        double* __restrict__ Rfi, int to, int nbs) {
+  pdl_enter();
+  const int t = blockIdx.x, ntl = nbs * (nbs + 1) / 2;
+  const double* src;
+  double* dst;
+  if (t < ntl) {
+    int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while ((J + 1) * (J + 2) / 2 <= t) ++J;
+    while (J * (J + 1) / 2 > t) --J;
+    const int64_t base = cq_tile(to + t - J * (J + 1) / 2, to + J) * 1024;
+    src = Rt + base;
+    dst = Rf + base;
+  } else {
+    const int64_t base = (int64_t)(to + t - ntl) * 1024;
+    src = Rinv + base;
+    dst = Rfi + base;
+  }
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    const int o = threadIdx.x + q4 * 256;
+    const int pr = o >> 1, lane = pr & 31, q = pr >> 5;
+    const int ks = q >> 1, nt = 2 * (q & 1) + (o & 1), g = lane >> 2, tq = lane & 3;
+    dst[o] = __ldg(src + (nt * 8 + g) * 32 + ks * 4 + tq);
+  }
+}
+
+__device__ __forceinline__ void cq_trsm_fetch_rf(const double* rf, double (&bf)[8][4]) {
+  const double2* f = reinterpret_cast<const double2*>(rf) + (threadIdx.x & 31);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int np = 0; np < 2; ++np) {
+      const double2 v = __ldg(f + (ks * 2 + np) * 32);
+      bf[ks][2 * np] = v.x;
+      bf[ks][2 * np + 1] = v.y;
+    }
 }
 
 // QS: earlier Q blocks kept in shared memory (nb <= 16); else read back
@@ -987,98 +1043,158 @@ __global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p
   }
 }
 
-// Right-looking TRSM: the CTA's 16 rows of X live in shared memory as T;
-// for each block column J, Q_J = T_J Rinv_JJ (warps 0-3, 8 columns each),
-// then every later block takes T_L -= Q_J R(J, L) (warp w: L = J+1+w,
-// J+9+w, ...; the tile loads of a warp's first L are issued before Q_J is
-// formed).  The dependent chain per block column is one 16 x 32 x 32
-// product; the bulk of the work (16 N^2 / 2 FMA per CTA) runs at the fp64
-// tensor rate.
-__global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_rl_kernel(const TrsmParams p) {
-  extern __shared__ double tsm[];  // T[c * CQ_QLD + r], c < nb * 32; becomes Q
-  pdl_enter();
+// Right-looking TRSM as a dataflow over the CTA's 8 warps: the CTA's 16 rows
+// of X live in shared memory as T (block columns T_0 .. T_{nb-1}); warp w
+// owns the block columns L = w (mod 8) and alone applies every update
+// T_L -= Q_J R(J, L) to them, in order J = 0, 1, ...; right after the last
+// one (J = L - 1) it forms Q_L = T_L Rinv_LL in place and releases it through
+// an mbarrier.  The dependent chain per block column is one 16 x 32 x 32
+// update plus one 16 x 32 x 32 product in one warp, with no CTA-wide barrier:
+// the other warps keep streaming their updates (one R tile per 32 DMMA, the
+// next tile's fragments in flight).  GT: the block-row solve of the blocked
+// Cholesky, X = G(to.., J0..)^T and the result written as R tiles.
+// Q_L = T_L Rinv_LL (bi), stored over T_L and to the output, then released.
+template <bool GT>
+__device__ __forceinline__ void cq_df_form_q(const TrsmParams& p, double* tsm, int L, int Jt, int rb,
+                                             int64_t r0, const double (&bi)[8][4], uint64_t* bar) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  __syncwarp();  // the warp's updates of T_L visible to all its lanes
+  double qa[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) qa[a][b] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int k = L * 32 + ks * 4 + tq;
+    const double a0 = tsm[k * CQ_QLD + g], a1 = tsm[k * CQ_QLD + g + 8];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) cq_dmma(qa[nt], a0, a1, bi[ks][nt]);
+  }
+  __syncwarp();  // every lane's reads of T_L done
+  double* out = GT ? p.Rout + cq_tile(p.to + L, Jt) * 1024 : nullptr;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+      tsm[(L * 32 + c) * CQ_QLD + r] = qa[nt][h];
+      if (GT) {
+        out[(rb + r) * 32 + c] = qa[nt][h];
+      } else {
+        const int64_t gc = (int64_t)L * 32 + c, gr = r0 + r;
+        if (gc < p.N && gr < p.X.d) p.Q[gc * p.ldq + gr] = qa[nt][h];
+      }
+    }
+  mbar_arrive(bar);
+}
+
+// T_L -= Q_J R(J, L), R(J, L) in bf; the fragments of my next tile (L + 8)
+// are fetched into bn while the product issues.
+__device__ __forceinline__ void cq_df_update(const TrsmParams& p, double* tsm, int J, int L,
+                                             const double (&qf0)[8], const double (&qf1)[8],
+                                             const double (&bf)[8][4], double (&bn)[8][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qf0[ks], qf1[ks], bf[ks][nt]);
+  if (L + CQ_TRSM_WARPS < p.nb)
+    cq_trsm_fetch_rf(p.Rf + cq_tile(p.to + J, p.to + L + CQ_TRSM_WARPS) * 1024, bn);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
+      tsm[(L * 32 + c) * CQ_QLD + r] -= acc[nt][h];
+    }
+}
+
+__device__ __forceinline__ void cq_copy_frags(double (&dst)[8][4], const double (&src)[8][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) dst[ks][nt] = src[ks][nt];
+}
+
+template <bool GT>
+__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmParams p) {
+  extern __shared__ __align__(16) double tsm[];  // T[c * CQ_QLD + r]; becomes Q
+  __shared__ __align__(8) uint64_t qbar[CQ_MAXNB_BIG];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
   const int64_t d = p.X.d;
-  const int ncol = p.nb * 32;
-  // T = X (16 rows x nb*32 columns, zero past N and d)
-  for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
-    const int r = e & 15, c = e >> 4;
-    const int64_t gr = r0 + r;
-    tsm[c * CQ_QLD + r] = (c < p.N && gr < d) ? __ldg(cq_col(p.X, c) + gr) : 0.0;
-  }
-  __syncthreads();
-  double bf[8][4], bi[8];
-  // Rinv_JJ fragments of the next block column, loaded one step ahead
-  auto fetch_rinv = [&](int J) {
-    if (warp < 4 && J < p.nb) {
-      const double* rinv = p.Rinv + (int64_t)J * 1024;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
+  const int nb = p.nb, ncol = nb * 32;
+  const int Jt = p.J0 + (int)(r0 >> 5), rb = (int)(r0 & 31);
+  if (threadIdx.x < nb) mbar_init(&qbar[threadIdx.x], 32);
+  pdl_enter();
+  // T = X: every 8-byte copy in flight at once (zero-filled past N and d)
+  if (GT) {  // X(r, c) = G(c, r): 16 contiguous rows of 32 in each tile
+    for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
+      const int ci = e & 31, r = (e >> 5) & 15, cI = e >> 9;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       smem_u32(tsm + (cI * 32 + ci) * CQ_QLD + r)),
+                   "l"(p.G + cq_tile(p.to + cI, Jt) * 1024 + (rb + r) * 32 + ci)
+                   : "memory");
     }
-  };
-  fetch_rinv(0);
-  for (int J = 0; J < p.nb; ++J) {
-    // this warp's first update tile of the step: loads in flight now
-    const int L0 = J + 1 + warp;
-    if (L0 < p.nb) cq_trsm_fetch_r(p.Rt + cq_tile(J, L0) * 1024, bf);
-    double qa[4] = {0.0, 0.0, 0.0, 0.0};
-    if (warp < 4) {
+  } else {
+    for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
+      const int r = e & 15, c = e >> 4;
+      const int64_t gr = r0 + r;
+      const bool ok = c < p.N && gr < d;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       smem_u32(tsm + c * CQ_QLD + r)),
+                   "l"(ok ? cq_col(p.X, c) + gr : p.X.A), "r"(ok ? 8 : 0)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    double bi[8][4];
+    cq_trsm_fetch_rf(p.Rfi + (int64_t)p.to * 1024, bi);
+    cq_df_form_q<GT>(p, tsm, 0, Jt, rb, r0, bi, &qbar[0]);
+  }
+  for (int J = 0; J + 1 < nb; ++J) {
+    const int L0 = J + 1 + ((warp - (J + 1)) % 8 + 8) % 8;  // my first block column > J
+    if (L0 >= nb) break;
+    double bf[8][4];
+    cq_trsm_fetch_rf(p.Rf + cq_tile(p.to + J, p.to + L0) * 1024, bf);
+    double qf0[8], qf1[8];
+    int L = L0;
+    if (L0 == J + 1) {  // T_{J+1} becomes final here: the next link of the chain first
+      double bi[8][4], bn[8][4];
+      cq_trsm_fetch_rf(p.Rfi + (int64_t)(p.to + L0) * 1024, bi);
+      mbar_wait(&qbar[J], 0);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int k = J * 32 + ks * 4 + tq;
-        const double a0 = tsm[k * CQ_QLD + g], a1 = tsm[k * CQ_QLD + g + 8];
-        cq_dmma(qa, a0, a1, bi[ks]);
+        qf0[ks] = tsm[k * CQ_QLD + g];
+        qf1[ks] = tsm[k * CQ_QLD + g + 8];
+      }
+      cq_df_update(p, tsm, J, L, qf0, qf1, bf, bn);
+      cq_df_form_q<GT>(p, tsm, L, Jt, rb, r0, bi, &qbar[L]);
+      cq_copy_frags(bf, bn);
+      L += CQ_TRSM_WARPS;
+    } else {
+      mbar_wait(&qbar[J], 0);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k = J * 32 + ks * 4 + tq;
+        qf0[ks] = tsm[k * CQ_QLD + g];
+        qf1[ks] = tsm[k * CQ_QLD + g + 8];
       }
     }
-    fetch_rinv(J + 1);
-    __syncthreads();  // every read of T_J done
-    if (warp < 4) {
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
-        const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
-        tsm[(J * 32 + c) * CQ_QLD + r] = qa[h];
-        if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
-      }
-    }
-    __syncthreads();  // Q_J visible
-    // T_L -= Q_J R(J, L), L > J
-    double qf0[8], qf1[8];
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int k = J * 32 + ks * 4 + tq;
-      qf0[ks] = tsm[k * CQ_QLD + g];
-      qf1[ks] = tsm[k * CQ_QLD + g + 8];
-    }
-    for (int L = L0; L < p.nb; L += CQ_TRSM_WARPS) {
+    for (; L < nb; L += CQ_TRSM_WARPS) {
       double bn[8][4];
-      const int Ln = L + CQ_TRSM_WARPS;
-      if (Ln < p.nb) cq_trsm_fetch_r(p.Rt + cq_tile(J, Ln) * 1024, bn);
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qf0[ks], qf1[ks], bf[ks][nt]);
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-          tsm[(L * 32 + c) * CQ_QLD + r] -= acc[nt][h];
-        }
-      if (Ln < p.nb) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = bn[ks][nt];
-      }
+      cq_df_update(p, tsm, J, L, qf0, qf1, bf, bn);
+      cq_copy_frags(bf, bn);
     }
-    __syncthreads();  // T_{J+1} final before the next step reads it
   }
 }
 
@@ -1471,7 +1587,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1502,6 +1618,8 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oRi = take((size_t)nb * 1024 * 8);
   w.oFro = take(8);
   w.oRef = take(4);
+  w.oRf = take(nt * 1024 * 8);
+  w.oRfi = take((size_t)nb * 1024 * 8);
   w.bytes = off;
   return w;
 }
@@ -1577,8 +1695,9 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
 // diagonal block, block-row solve, trailing SYRK).  `shift_coef` only on the
 // single-cluster path (the blocked path shifts beforehand).
 int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
-                int* flag, bool pdl, cudaStream_t st) {
+                int* flag, double* Rf, double* Rfi, bool pdl, cudaStream_t st) {
   if (nb <= CQ_MAXNB) return cq_chol(Gt, nb, N, shift_coef, Rt, Rinv, flag, pdl, st);
+  static const bool old_rowsolve = env_flag("SKL_CQR_TRIROW");  // A/B knob
   for (int to = 0; to < nb; to += CQ_MAXNB) {
     const int nbs = std::min(CQ_MAXNB, nb - to);
     int rc = cq_chol(Gt, nbs, N, 0.0, Rt, Rinv, flag, pdl, st, to);
@@ -1586,9 +1705,22 @@ int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, do
     const int rest = nb - to - nbs;
     if (rest == 0) break;
     TriParams tp{Gt, Rt, Rinv, to, nbs, nb};
-    const size_t tsm = (size_t)nbs * 1056 * sizeof(double);
-    SKL_CUDA(raise_smem_limit(cqr_trirow_kernel, tsm));
-    SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), tsm, st, true, tp));
+    if (old_rowsolve) {
+      const size_t tsm = (size_t)nbs * 1056 * sizeof(double);
+      SKL_CUDA(raise_smem_limit(cqr_trirow_kernel, tsm));
+      SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), tsm, st, true, tp));
+    } else {
+      // R(to.., J0..) = R11^{-T} G(to.., J0..), i.e. its transpose is the
+      // right-looking TRSM of G(to.., J0..)^T by R11 (16 rows per CTA)
+      const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
+      SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
+      SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs)), dim3(256), 0,
+                        st, true, (const double*)Rt, (const double*)Rinv, Rf, Rfi, to, nbs));
+      const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
+      TrsmParams sp{none, (int64_t)nbs * 32, nbs, Rt, Rinv, nullptr, 0, Rf, Rfi, Gt, Rt, to, to + nbs};
+      SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS)),
+                        dim3(CQ_TRSM_NT), tsm, st, true, sp));
+    }
     SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2)), dim3(256), 0, st,
                       true, tp));
   }
@@ -1596,7 +1728,7 @@ int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, do
 }
 
 int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* Rinv, double* Q,
-            int64_t ldq, bool pdl, cudaStream_t st) {
+            int64_t ldq, double* Rf, double* Rfi, bool pdl, cudaStream_t st) {
   static std::once_flag attr_set[64];
   const size_t smem_max = (size_t)CQ_MAXNB_BIG * 32 * CQ_QLD * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
@@ -1605,7 +1737,7 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* 
     return SKL_OK;
   });
   if (arc) return arc;
-  TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq};
+  TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq, Rf, Rfi, nullptr, nullptr, 0, 0};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
   // (cqr_trsm_kernel<false>, reading earlier Q blocks back from L2 instead
   // of shared memory, measured no faster at 8192 x 1025: the kernel holds
@@ -1617,12 +1749,14 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* 
   } else {
     static std::once_flag rl_set[64];
     const int rc = once_per_device(rl_set, [&]() -> int {
-      SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_df_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_max));
       return SKL_OK;
     });
     if (rc) return rc;
-    SKL_CUDA(launch_k(cqr_trsm_rl_kernel, dim3(grid), dim3(CQ_TRSM_NT),
+    SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
+                      pdl, Rt, Rinv, Rf, Rfi, 0, nb));
+    SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
                       (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
   }
   return SKL_OK;
@@ -1695,10 +1829,12 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
         break;
       }
     }
-    if ((rc = cq_chol_any(G1, nb, N, big ? 0.0 : shift, R1, I1, flag, true, st))) break;
-    if ((rc = cq_trsm(M, N, nb, R1, I1, Q, ldq, true, st))) break;
+    double* Rf = (double*)P(w.oRf);
+    double* Rfi = (double*)P(w.oRfi);
+    if ((rc = cq_chol_any(G1, nb, N, big ? 0.0 : shift, R1, I1, flag, Rf, Rfi, true, st))) break;
+    if ((rc = cq_trsm(M, N, nb, R1, I1, Q, ldq, Rf, Rfi, true, st))) break;
     if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st))) break;
-    if ((rc = cq_chol_any(G2, nb, N, 0.0, R2, I2, flag, true, st))) break;
+    if ((rc = cq_chol_any(G2, nb, N, 0.0, R2, I2, flag, Rf, Rfi, true, st))) break;
     double* Rt = (double*)P(w.oRt);
     double* Ri = (double*)P(w.oRi);
     ProdParams pp{R1, R2, I1, I2, Rt, Ri};

@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_cholqr.py -q -x 2>&1 | tail -2
+timeout 300 python tools/time_cholqr.py 800x200 2048x256 8192x1024 2>&1 | tail -3
+SKL_NO_PDL=1 timeout 300 python tools/prof_cqr_kernels.py 8192 1024 2>&1 | tail -16
+SKL_NO_PDL=1 timeout 300 python tools/prof_cqr_kernels.py 2048 256 2>&1 | tail -12
