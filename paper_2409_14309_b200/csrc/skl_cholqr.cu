@@ -636,9 +636,8 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
 // ------------------------------------------- Cholesky beyond 16 block columns
 // N > 512: right-looking over super-blocks of up to 16 tiles.  For the
 // super-block [to, to + nbs): the cluster kernel factors its diagonal block,
-// cqr_trirow_kernel solves the block row R(I, J) = R_II^{-T} (G(I, J) -
-// sum_{to <= K < I} R(K, I)^T R(K, J)) for every later tile column J (one CTA
-// per column, the tile rows in order), cqr_syrk_kernel applies
+// the block row R(to.., J) = R11^{-T} G(to.., J) of every later tile column
+// J is the TRSM of G^T by R11 (cqr_trsm_df_kernel<true>), cqr_syrk_kernel applies
 // G(I, J) -= sum_K R(K, I)^T R(K, J) to the trailing tiles.  The shift of
 // the first factorisation is applied once beforehand (cqr_shift_kernel),
 // because the trailing updates change the later diagonal tiles.
@@ -692,103 +691,6 @@ struct TriParams {
   const double* Rinv; // inverses of R's diagonal tiles
   int to, nbs, nb;
 };
-
-// One CTA per later tile column J: the column's nbs blocks T(I, J) sit in
-// shared memory (stride 33); step I solves R(I, J) = Rinv_II^T T(I, J)
-// (warp w: fragment (w / 4, w % 4)), then the warps update every later block
-// T(I', J) -= R(I, I')^T R(I, J) (I' = I+1 first, split over 4 warps by
-// fragment quarters; the others one block per warp) -- the dependent chain
-// per step is one small product, the rest runs beside it.
-__device__ __forceinline__ void cq_frag_load_tn(const double* A, int mt, int nt0, int nnt,
-                                                double (&af)[8][2], const double* B,
-                                                double (&bfr)[8][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) af[ks][h] = __ldcg(A + (mt * 16 + h * 8 + g) * 32 + ks * 4 + tq);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      bfr[ks][q] = q < nnt ? B[((nt0 + q) * 8 + g) * 33 + ks * 4 + tq] : 0.0;
-  }
-}
-
-__global__ void __launch_bounds__(256) cqr_trirow_kernel(const TriParams p) {
-  extern __shared__ double Tc[];  // [nbs][32 * 33]: T(I, J) column-major, stride 33
-  pdl_enter();
-  const int J = p.to + p.nbs + blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  for (int q = 0; q < p.nbs; ++q) {
-    const double* src = p.Gt + cq_tile(p.to + q, J) * 1024;
-    for (int e = threadIdx.x; e < 1024; e += 256) Tc[q * 1056 + (e >> 5) * 33 + (e & 31)] = __ldcg(src + e);
-  }
-  __syncthreads();
-  for (int q = 0; q < p.nbs; ++q) {
-    const int I = p.to + q;
-    double* T = Tc + q * 1056;
-    // R(I, J) = Rinv_II^T T (in place after every warp has read T)
-    const int mt = warp >> 2, nt = warp & 3;
-    double r[4] = {0.0, 0.0, 0.0, 0.0};
-    {
-      const double* ri = p.Rinv + (int64_t)I * 1024;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int k = ks * 4 + tq;
-        cq_dmma(r, __ldcg(ri + (mt * 16 + g) * 32 + k), __ldcg(ri + (mt * 16 + 8 + g) * 32 + k),
-                T[(nt * 8 + g) * 33 + k]);
-      }
-    }
-    __syncthreads();
-    double* out = p.Rt + cq_tile(I, J) * 1024;
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int rr = mt * 16 + g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-      T[c * 33 + rr] = r[h];
-      out[c * 32 + rr] = r[h];
-    }
-    __syncthreads();  // R(I, J) in T
-    // T(I', J) -= R(I, I')^T R(I, J): I' = I+1 by all 8 warps (one fragment
-    // each), then the rest one block per warp
-    auto update = [&](int qq, int mt0, int nmt, int nt0, int nnt) {
-      const double* A = p.Rt + cq_tile(I, p.to + qq) * 1024;  // R(I, I')
-      double acc[2][4][4];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 4; ++b2)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[a][b2][c] = 0.0;
-#pragma unroll
-      for (int m2 = 0; m2 < 2; ++m2) {
-        if (m2 >= nmt) break;
-        double af[8][2], bfr[8][4];
-        cq_frag_load_tn(A, mt0 + m2, nt0, nnt, af, T, bfr);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            if (q4 < nnt) cq_dmma(acc[m2][q4], af[ks][0], af[ks][1], bfr[ks][q4]);
-      }
-      double* Tq = Tc + qq * 1056;
-#pragma unroll
-      for (int m2 = 0; m2 < 2; ++m2) {
-        if (m2 >= nmt) break;
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          if (q4 >= nnt) break;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int rr = (mt0 + m2) * 16 + g + (h >= 2 ? 8 : 0), c = (nt0 + q4) * 8 + 2 * tq + (h & 1);
-            Tq[c * 33 + rr] -= acc[m2][q4][h];
-          }
-        }
-      }
-    };
-    if (q + 1 < p.nbs) update(q + 1, warp >> 2, 1, warp & 3, 1);
-    for (int qq = q + 2 + warp; qq < p.nbs; qq += 8) update(qq, 0, 2, 0, 4);
-    __syncthreads();
-  }
-}
 
 __global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p) {
   __shared__ double red[4][1024];
@@ -1059,18 +961,24 @@ __device__ __forceinline__ void cq_df_form_q(const TrsmParams& p, double* tsm, i
                                              int64_t r0, const double (&bi)[8][4], uint64_t* bar) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   __syncwarp();  // the warp's updates of T_L visible to all its lanes
-  double qa[4][4];
+  double qa[2][4][4];  // ks halves: half the dependent DMMA depth
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) qa[a][b] = 0.0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) qa[s2][a][b] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int k = L * 32 + ks * 4 + tq;
     const double a0 = tsm[k * CQ_QLD + g], a1 = tsm[k * CQ_QLD + g + 8];
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) cq_dmma(qa[nt], a0, a1, bi[ks][nt]);
+    for (int nt = 0; nt < 4; ++nt) cq_dmma(qa[ks >> 2][nt], a0, a1, bi[ks][nt]);
   }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) qa[0][a][b] += qa[1][a][b];
   __syncwarp();  // every lane's reads of T_L done
   double* out = GT ? p.Rout + cq_tile(p.to + L, Jt) * 1024 : nullptr;
 #pragma unroll
@@ -1078,40 +986,46 @@ __device__ __forceinline__ void cq_df_form_q(const TrsmParams& p, double* tsm, i
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-      tsm[(L * 32 + c) * CQ_QLD + r] = qa[nt][h];
+      tsm[(L * 32 + c) * CQ_QLD + r] = qa[0][nt][h];
       if (GT) {
-        out[(rb + r) * 32 + c] = qa[nt][h];
+        out[(rb + r) * 32 + c] = qa[0][nt][h];
       } else {
         const int64_t gc = (int64_t)L * 32 + c, gr = r0 + r;
-        if (gc < p.N && gr < p.X.d) p.Q[gc * p.ldq + gr] = qa[nt][h];
+        if (gc < p.N && gr < p.X.d) p.Q[gc * p.ldq + gr] = qa[0][nt][h];
       }
     }
   mbar_arrive(bar);
 }
 
-// T_L -= Q_J R(J, L), R(J, L) in bf; the fragments of my next tile (L + 8)
-// are fetched into bn while the product issues.
+// T_L -= Q_J R(J, L), R(J, L) in bf.  CHAIN (the link that makes T_L final):
+// two accumulator sets over ks halves (half the dependent DMMA depth), no
+// prefetch; else the fragments of my next tile (L + 8) are fetched into bn
+// before the product issues.
+template <bool CHAIN>
 __device__ __forceinline__ void cq_df_update(const TrsmParams& p, double* tsm, int J, int L,
                                              const double (&qf0)[8], const double (&qf1)[8],
                                              const double (&bf)[8][4], double (&bn)[8][4]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  double acc[4][4];
+  if (!CHAIN && L + CQ_TRSM_WARPS < p.nb)
+    cq_trsm_fetch_rf(p.Rf + cq_tile(p.to + J, p.to + L + CQ_TRSM_WARPS) * 1024, bn);
+  constexpr int NS = CHAIN ? 2 : 1;
+  double acc[NS][4][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int s2 = 0; s2 < NS; ++s2)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[s2][a][b] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qf0[ks], qf1[ks], bf[ks][nt]);
-  if (L + CQ_TRSM_WARPS < p.nb)
-    cq_trsm_fetch_rf(p.Rf + cq_tile(p.to + J, p.to + L + CQ_TRSM_WARPS) * 1024, bn);
+    for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[CHAIN ? ks >> 2 : 0][nt], qf0[ks], qf1[ks], bf[ks][nt]);
 #pragma unroll
   for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-      tsm[(L * 32 + c) * CQ_QLD + r] -= acc[nt][h];
+      tsm[(L * 32 + c) * CQ_QLD + r] -= CHAIN ? acc[0][nt][h] + acc[NS - 1][nt][h] : acc[0][nt][h];
     }
 }
 
@@ -1168,7 +1082,7 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
     double qf0[8], qf1[8];
     int L = L0;
     if (L0 == J + 1) {  // T_{J+1} becomes final here: the next link of the chain first
-      double bi[8][4], bn[8][4];
+      double bi[8][4];
       cq_trsm_fetch_rf(p.Rfi + (int64_t)(p.to + L0) * 1024, bi);
       mbar_wait(&qbar[J], 0);
 #pragma unroll
@@ -1177,10 +1091,10 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
         qf0[ks] = tsm[k * CQ_QLD + g];
         qf1[ks] = tsm[k * CQ_QLD + g + 8];
       }
-      cq_df_update(p, tsm, J, L, qf0, qf1, bf, bn);
+      cq_df_update<true>(p, tsm, J, L, qf0, qf1, bf, bf);
       cq_df_form_q<GT>(p, tsm, L, Jt, rb, r0, bi, &qbar[L]);
-      cq_copy_frags(bf, bn);
       L += CQ_TRSM_WARPS;
+      if (L < nb) cq_trsm_fetch_rf(p.Rf + cq_tile(p.to + J, p.to + L) * 1024, bf);
     } else {
       mbar_wait(&qbar[J], 0);
 #pragma unroll
@@ -1192,7 +1106,7 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
     }
     for (; L < nb; L += CQ_TRSM_WARPS) {
       double bn[8][4];
-      cq_df_update(p, tsm, J, L, qf0, qf1, bf, bn);
+      cq_df_update<false>(p, tsm, J, L, qf0, qf1, bf, bn);
       cq_copy_frags(bf, bn);
     }
   }
@@ -1697,7 +1611,6 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
 int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
                 int* flag, double* Rf, double* Rfi, bool pdl, cudaStream_t st) {
   if (nb <= CQ_MAXNB) return cq_chol(Gt, nb, N, shift_coef, Rt, Rinv, flag, pdl, st);
-  static const bool old_rowsolve = env_flag("SKL_CQR_TRIROW");  // A/B knob
   for (int to = 0; to < nb; to += CQ_MAXNB) {
     const int nbs = std::min(CQ_MAXNB, nb - to);
     int rc = cq_chol(Gt, nbs, N, 0.0, Rt, Rinv, flag, pdl, st, to);
@@ -1705,22 +1618,16 @@ int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, do
     const int rest = nb - to - nbs;
     if (rest == 0) break;
     TriParams tp{Gt, Rt, Rinv, to, nbs, nb};
-    if (old_rowsolve) {
-      const size_t tsm = (size_t)nbs * 1056 * sizeof(double);
-      SKL_CUDA(raise_smem_limit(cqr_trirow_kernel, tsm));
-      SKL_CUDA(launch_k(cqr_trirow_kernel, dim3((unsigned)rest), dim3(256), tsm, st, true, tp));
-    } else {
-      // R(to.., J0..) = R11^{-T} G(to.., J0..), i.e. its transpose is the
-      // right-looking TRSM of G(to.., J0..)^T by R11 (16 rows per CTA)
-      const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
-      SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
-      SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs)), dim3(256), 0,
-                        st, true, (const double*)Rt, (const double*)Rinv, Rf, Rfi, to, nbs));
-      const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
-      TrsmParams sp{none, (int64_t)nbs * 32, nbs, Rt, Rinv, nullptr, 0, Rf, Rfi, Gt, Rt, to, to + nbs};
-      SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS)),
-                        dim3(CQ_TRSM_NT), tsm, st, true, sp));
-    }
+    // R(to.., J0..) = R11^{-T} G(to.., J0..): its transpose is the TRSM of
+    // G(to.., J0..)^T by R11 (16 rows per CTA)
+    const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
+    SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
+    SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs)), dim3(256), 0,
+                      st, true, (const double*)Rt, (const double*)Rinv, Rf, Rfi, to, nbs));
+    const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
+    TrsmParams sp{none, (int64_t)nbs * 32, nbs, Rt, Rinv, nullptr, 0, Rf, Rfi, Gt, Rt, to, to + nbs};
+    SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS)),
+                      dim3(CQ_TRSM_NT), tsm, st, true, sp));
     SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2)), dim3(256), 0, st,
                       true, tp));
   }
