@@ -47,8 +47,9 @@
 //                     apply the rank-32 update to the rest of their column
 //                     (DMMA, R(K, I) read over DSMEM).  Two split cluster
 //                     barriers per step.
-//   cqr_trsm_kernel   Q = M R^{-1}, 16 rows per CTA, block-column sweep with
-//                     the inverted diagonal blocks.
+//   cqr_trsm_df_kernel  Q = M R^{-1}, 16 rows per CTA, right-looking as a
+//                     dataflow over the warps (see the kernel); the blocked
+//                     Cholesky's block-row solves run through it too.
 //   cqr_solve_*       rank check, y, the triangular solves (one CTA), the
 //                     residual and SA^T r (multi-CTA GEMVs).
 #include <cuda_runtime.h>
@@ -91,6 +92,12 @@ struct CqCols {
   int64_t n;  // columns taken from A
   int64_t d;  // rows
 };
+// The second factorisation is skipped when the Gram of Q1 is the identity
+// to first order (cqr_gram_kernel's E mode): max |G2 - I| <= tau.
+__device__ __forceinline__ bool cq_skipped(const unsigned long long* skip, double tau) {
+  return skip != nullptr && __longlong_as_double((long long)*skip) <= tau;
+}
+
 __device__ __forceinline__ const double* cq_col(const CqCols& X, int64_t c) {
   return c < X.n ? X.A + c * X.lda : X.b;
 }
@@ -155,6 +162,13 @@ struct GramParams {
   double* part;       // [P][SEG][1024]
   double* Gt;         // [ntiles][1024]
   unsigned* cnt;      // [ntiles], zero on entry, left zero
+  double* Gt2;        // optional second copy of the Gram (unshifted variant)
+  // E mode (Gram of Q1): E = G - I; emax = max |E| over the first N rows and
+  // columns, R2 = I + up(E) and the inverses of its diagonal tiles I - up(E)
+  // (the Cholesky factor of I + E and its inverse to first order)
+  unsigned long long* emax;
+  double* R2t;
+  double* R2inv;
 };
 
 __device__ __forceinline__ uint32_t cq_unit_lo(const GramParams& p, uint32_t c) { return p.U * c / p.P; }
@@ -205,6 +219,31 @@ __device__ __forceinline__ void cq_gram_mma(double (&acc)[2][4][4], const double
 // N - 1 instead (the Cholesky ignores those Gram entries).  Every segment
 // leaves a partial tile; the last CTA to finish a tile folds the partials
 // of the CTAs that cover it in CTA order (deterministic).
+__device__ __forceinline__ void cq_gram_e(const GramParams& p, int t, const double (&v)[8]) {
+  __shared__ double mred[4];
+  int I, J;
+  cq_tile_ij(t, I, J);
+  double m = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = threadIdx.x + i * 128, r = e & 31, c = e >> 5;
+    const int64_t gi = (int64_t)I * 32 + r, gj = (int64_t)J * 32 + c;
+    const bool valid = gi < p.N && gj < p.N;
+    const double E = v[i] - (gi == gj ? 1.0 : 0.0);
+    if (valid) m = isfinite(E) ? fmax(m, fabs(E)) : INFINITY;
+    const double F = !valid ? 0.0 : (I < J || r < c) ? E : (r == c ? 0.5 * E : 0.0);
+    p.R2t[(int64_t)t * 1024 + e] = (gi == gj ? 1.0 : 0.0) + F;
+    if (I == J) p.R2inv[(int64_t)I * 1024 + e] = (r == c ? 1.0 : 0.0) - F;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    atomicMax(p.emax, (unsigned long long)__double_as_longlong(
+                          fmax(fmax(mred[0], mred[1]), fmax(mred[2], mred[3]))));
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
   pdl_enter();
@@ -290,6 +329,10 @@ __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) p.Gt[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
+      if (p.Gt2 != nullptr)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p.Gt2[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
+      if (p.emax != nullptr) cq_gram_e(p, t, v);
       if (threadIdx.x == 0) p.cnt[t] = 0u;
     }
     __syncthreads();  // red reused by the next segment
@@ -307,6 +350,11 @@ struct CholParams {
   double* Rinv;        // inverses of R's diagonal tiles [nb][1024]
   int* flag;           // set on a non-positive / non-finite pivot
   int to;              // tile offset: this cluster factors diagonal block [to, to + nb)
+  // blockIdx.y = 1: the unshifted variant (Gt + vs_g, Rt + vs_r, Rinv + vs_i,
+  // flag + 1, no shift), factored beside the shifted one
+  int64_t vs_g, vs_r, vs_i;
+  const unsigned long long* skip;  // second factorisation: skipped (cq_skipped)
+  double tau;
 };
 
 #ifdef CQ_FACTOR_CLOCKS
@@ -534,7 +582,15 @@ __device__ __forceinline__ void cq_push(const double* blk, int from, int nb, dou
                      mapa_u32(smem_u32(&mbar[buf]), (uint32_t)dst));
 }
 
-__global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParams p) {
+__global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParams p0) {
+  CholParams p = p0;
+  if (blockIdx.y) {
+    p.Gt += p.vs_g;
+    p.Rt += p.vs_r;
+    p.Rinv += p.vs_i;
+    p.flag += 1;
+    p.shift_coef = 0.0;
+  }
   // tiles (I, J) of my block column, I = 0..J, then 32 doubles (1/sqrt of
   // my pivots) right after my diagonal tile
   extern __shared__ __align__(16) double csm[];
@@ -555,6 +611,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
     if (J > 1) mbar_arrive_expect_tx(&mbar[1], CQ_PUSH_BYTES);
   }
   pdl_enter();
+  if (cq_skipped(p.skip, p.tau)) return;  // every CTA of the cluster alike
   CQ_PROBE(0);
   // my column's Gram tiles, all copies in flight at once (8-byte cp.async;
   // past N: zero-filled, identity on the diagonal below)
@@ -690,11 +747,20 @@ struct TriParams {
   double* Rt;         // R tiles (diagonal block [to, to+nbs) factored)
   const double* Rinv; // inverses of R's diagonal tiles
   int to, nbs, nb;
+  int64_t vs_g, vs_r;  // blockIdx.y = 1: the unshifted variant's buffers
+  const unsigned long long* skip;
+  double tau;
 };
 
-__global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p) {
+__global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p0) {
   __shared__ double red[4][1024];
+  TriParams p = p0;
+  if (blockIdx.y) {
+    p.Gt += p.vs_g;
+    p.Rt += p.vs_r;
+  }
   pdl_enter();
+  if (cq_skipped(p.skip, p.tau)) return;
   int jj = (int)((sqrtf(8.0f * blockIdx.x + 1.0f) - 1.0f) * 0.5f);
   while ((jj + 1) * (jj + 2) / 2 <= (int)blockIdx.x) ++jj;
   while (jj * (jj + 1) / 2 > (int)blockIdx.x) --jj;
@@ -766,38 +832,13 @@ struct TrsmParams {
   const double* G;
   double* Rout;
   int to, J0;
+  int64_t vs_g, vs_r, vs_i;  // GT, blockIdx.y = 1: the unshifted variant (G, Rout and Rf, Rfi)
+  const unsigned long long* skip;
+  double tau;
 };
 
-// Q (rows r0 .. r0+15) = X R^{-1}: for each block column J,
-//   T = X_J - sum_{K<J} Q_K R(K, J)   (K split over the 8 warps)
-//   Q_J = T Rinv_JJ                    (warps 0-3: 8 columns each)
 constexpr int CQ_TRSM_WARPS = 8;
 constexpr int CQ_TRSM_NT = CQ_TRSM_WARPS * 32;
-
-__device__ __forceinline__ void cq_trsm_fetch_x(const TrsmParams& p, int J, int64_t r0,
-                                                double (&xv)[2], double (&bi)[8]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int e = threadIdx.x + q * CQ_TRSM_NT;
-    const int r = e & 15, c = e >> 4;
-    const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
-    xv[q] = (gc < p.N && gr < p.X.d) ? __ldg(cq_col(p.X, gc) + gr) : 0.0;
-  }
-  if (warp < 4) {
-    const double* rinv = p.Rinv + (int64_t)J * 1024;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) bi[ks] = __ldg(rinv + (warp * 8 + g) * 32 + ks * 4 + tq);
-  }
-}
-
-__device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = __ldg(rk + (nt * 8 + g) * 32 + ks * 4 + tq);
-}
 
 // R tiles re-laid in the order the DMMA B fragments consume them: for each
 // tile, 16 rows of 32 double2 (q = ks * 2 + np holds bf[ks][2np], bf[ks][2np+1]
@@ -807,11 +848,29 @@ __device__ __forceinline__ void cq_trsm_fetch_r(const double* rk, double (&bf)[8
 // bound by the L1 wavefront rate rather than by the fp64 tensor pipe.
 // Blocks [0, nbs (nbs + 1) / 2): the upper tiles of the diagonal block that
 // starts at tile `to`; the next nbs blocks: its diagonal tiles' inverses.
-__global__ void __launch_bounds__(256) cqr_rfrag_kernel(const double* __restrict__ Rt,
-                                                        const double* __restrict__ Rinv,
-                                                        double* __restrict__ Rf,
-                                                        double* __restrict__ Rfi, int to, int nbs) {
+// Variants: the source is variant *sel (after the pick) or blockIdx.y, the
+// destination variant blockIdx.y (buffers of variant 1 at + vs_r / + vs_i).
+struct FragParams {
+  const double* Rt;
+  const double* Rinv;
+  double* Rf;
+  double* Rfi;
+  int to, nbs;
+  int64_t vs_r, vs_i;
+  const int* sel;
+  const unsigned long long* skip;
+  double tau;
+};
+
+__global__ void __launch_bounds__(256) cqr_rfrag_kernel(const FragParams fp) {
   pdl_enter();
+  if (cq_skipped(fp.skip, fp.tau)) return;
+  const int vsrc = fp.sel != nullptr ? (*fp.sel != 0) : (int)blockIdx.y, vdst = (int)blockIdx.y;
+  const double* Rt = fp.Rt + vsrc * fp.vs_r;
+  const double* Rinv = fp.Rinv + vsrc * fp.vs_i;
+  double* Rf = fp.Rf + vdst * fp.vs_r;
+  double* Rfi = fp.Rfi + vdst * fp.vs_i;
+  const int to = fp.to, nbs = fp.nbs;
   const int t = blockIdx.x, ntl = nbs * (nbs + 1) / 2;
   const double* src;
   double* dst;
@@ -848,113 +907,6 @@ __device__ __forceinline__ void cq_trsm_fetch_rf(const double* rf, double (&bf)[
     }
 }
 
-// QS: earlier Q blocks kept in shared memory (nb <= 16); else read back
-// from the global Q (L2) -- small shared memory, several CTAs per SM.
-template <bool QS>
-__global__ void __launch_bounds__(CQ_TRSM_NT) cqr_trsm_kernel(const TrsmParams p) {
-  extern __shared__ double qsm[];  // Qs[c * CQ_QLD + r], c < nb * 32 (QS only)
-  __shared__ double red[CQ_TRSM_WARPS][16 * 33];
-  __shared__ double Ts[16 * 33];
-  pdl_enter();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
-  const int64_t d = p.X.d;
-  double* Qs = qsm;
-  double xv[2], bi[8];
-  double bf[8][4], bn[8][4];
-  cq_trsm_fetch_x(p, 0, r0, xv, bi);
-  for (int J = 0; J < p.nb; ++J) {
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    // sum_{K < J, K = warp mod 8} Q_K R(K, J): the next tile's loads are in
-    // flight while the current one is multiplied (the first tile was
-    // fetched during the previous block column)
-    int K = warp;
-    while (K < J) {
-      const int Kn = K + CQ_TRSM_WARPS;
-      if (Kn < J) cq_trsm_fetch_r(p.Rt + cq_tile(Kn, J) * 1024, bn);
-      double qa0[8], qa1[8];
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int k = K * 32 + ks * 4 + tq;
-        if (QS) {
-          qa0[ks] = Qs[k * CQ_QLD + g];
-          qa1[ks] = Qs[k * CQ_QLD + g + 8];
-        } else {  // rows past d were never written: zero
-          qa0[ks] = r0 + g < d ? __ldcg(p.Q + (int64_t)k * p.ldq + r0 + g) : 0.0;
-          qa1[ks] = r0 + g + 8 < d ? __ldcg(p.Q + (int64_t)k * p.ldq + r0 + g + 8) : 0.0;
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[nt], qa0[ks], qa1[ks], bf[ks][nt]);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) bf[ks][nt] = bn[ks][nt];
-      K = Kn;
-    }
-    if (warp < J) {
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int r = g + (h >= 2 ? 8 : 0), c = nt * 8 + 2 * tq + (h & 1);
-          red[warp][r * 33 + c] = acc[nt][h];
-        }
-    }
-    __syncthreads();
-    const int nw = min(J, CQ_TRSM_WARPS);  // warps holding partial sums
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = threadIdx.x + q * CQ_TRSM_NT;
-      const int r = e & 15, c = e >> 4;
-      const int o = r * 33 + c;
-      double sacc = 0.0;
-      for (int w = 0; w < nw; ++w) sacc += red[w][o];
-      Ts[o] = xv[q] - sacc;
-    }
-    __syncthreads();
-    double qa[4] = {0.0, 0.0, 0.0, 0.0};
-    if (warp < 4) {
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const double a0 = Ts[g * 33 + ks * 4 + tq], a1 = Ts[(g + 8) * 33 + ks * 4 + tq];
-        cq_dmma(qa, a0, a1, bi[ks]);
-      }
-    }
-    if (J + 1 < p.nb) {
-      cq_trsm_fetch_x(p, J + 1, r0, xv, bi);
-      if (warp < J + 1) cq_trsm_fetch_r(p.Rt + cq_tile(warp, J + 1) * 1024, bf);
-    }
-    if (warp < 4) {
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int r = g + (h >= 2 ? 8 : 0), c = warp * 8 + 2 * tq + (h & 1);
-        const int64_t gc = (int64_t)J * 32 + c, gr = r0 + r;
-        if (QS) Qs[(J * 32 + c) * CQ_QLD + r] = qa[h];
-        // (read-back path: only tiles K < J <= nb - 1 are read, all below N)
-        if (gc < p.N && gr < d) p.Q[gc * p.ldq + gr] = qa[h];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Right-looking TRSM as a dataflow over the CTA's 8 warps: the CTA's 16 rows
-// of X live in shared memory as T (block columns T_0 .. T_{nb-1}); warp w
-// owns the block columns L = w (mod 8) and alone applies every update
-// T_L -= Q_J R(J, L) to them, in order J = 0, 1, ...; right after the last
-// one (J = L - 1) it forms Q_L = T_L Rinv_LL in place and releases it through
-// an mbarrier.  The dependent chain per block column is one 16 x 32 x 32
-// update plus one 16 x 32 x 32 product in one warp, with no CTA-wide barrier:
-// the other warps keep streaming their updates (one R tile per 32 DMMA, the
-// next tile's fragments in flight).  GT: the block-row solve of the blocked
-// Cholesky, X = G(to.., J0..)^T and the result written as R tiles.
 // Q_L = T_L Rinv_LL (bi), stored over T_L and to the output, then released.
 template <bool GT>
 __device__ __forceinline__ void cq_df_form_q(const TrsmParams& p, double* tsm, int L, int Jt, int rb,
@@ -1037,9 +989,16 @@ __device__ __forceinline__ void cq_copy_frags(double (&dst)[8][4], const double 
 }
 
 template <bool GT>
-__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmParams p) {
+__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmParams p0) {
   extern __shared__ __align__(16) double tsm[];  // T[c * CQ_QLD + r]; becomes Q
   __shared__ __align__(8) uint64_t qbar[CQ_MAXNB_BIG];
+  TrsmParams p = p0;
+  if (GT && blockIdx.y) {
+    p.G += p.vs_g;
+    p.Rout += p.vs_r;
+    p.Rf += p.vs_r;
+    p.Rfi += p.vs_i;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
   const int64_t d = p.X.d;
@@ -1047,6 +1006,7 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
   const int Jt = p.J0 + (int)(r0 >> 5), rb = (int)(r0 & 31);
   if (threadIdx.x < nb) mbar_init(&qbar[threadIdx.x], 32);
   pdl_enter();
+  if (cq_skipped(p.skip, p.tau)) return;
   // T = X: every 8-byte copy in flight at once (zero-filled past N and d)
   if (GT) {  // X(r, c) = G(c, r): 16 contiguous rows of 32 in each tile
     for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
@@ -1112,6 +1072,46 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
   }
 }
 
+// After the first factorisation: take the unshifted variant (*sel = 1) when
+// it did not break down and its R's diagonal over the n columns of SA spans
+// less than CQ_REFINE_RATIO (kappa small: the unshifted CholeskyQR leaves Q1
+// orthonormal to ~kappa^2 u, so the second Gram is I to first order and its
+// factorisation can be skipped); the shifted variant otherwise.  The flag
+// then describes the chosen variant.  One CTA.
+__global__ void __launch_bounds__(1024) cqr_pick_kernel(const double* R1u, int64_t n, int* flag,
+                                                        int* sel) {
+  __shared__ double red[2][32];
+  pdl_enter();
+  double lo = INFINITY, hi = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    const double v = R1u[cq_tile((int)(i >> 5), (int)(i >> 5)) * 1024 + (i & 31) * 33];
+    const bool ok = v > 0.0 && v < INFINITY;
+    lo = ok ? fmin(lo, v) : -1.0;
+    hi = ok ? fmax(hi, v) : INFINITY;
+    if (!ok) break;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = lo;
+    red[1][w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 32; ++k) {
+      lo = fmin(lo, red[0][k]);
+      hi = fmax(hi, red[1][k]);
+    }
+    const int s2 = (flag[1] == 0 && lo > 0.0 && hi < CQ_REFINE_RATIO * lo) ? 1 : 0;
+    *sel = s2;
+    if (s2) flag[0] = 0;
+  }
+}
+
 // ----------------------------------------------------------------- solves
 // R = R2 R1 (upper, tile layout) and the inverses of its diagonal tiles
 // (R_II^{-1} = R1_II^{-1} R2_II^{-1}).  One CTA per upper tile, the K terms
@@ -1123,6 +1123,8 @@ struct ProdParams {
   const double* R2inv;
   double* Rt;
   double* Rinv;
+  const int* sel;        // R1 of the unshifted variant (+ vs_r, + vs_i) when *sel
+  int64_t vs_r, vs_i;
 };
 
 // acc += A B for 32 x 32 global tiles (column-major, ld 32), one warp.
@@ -1147,9 +1149,14 @@ __device__ __forceinline__ void cq_gtile_mma(double (&acc)[2][4][4], const doubl
       for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], af[ks][mt][0], af[ks][mt][1], bf[ks][nt]);
 }
 
-__global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p) {
+__global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p0) {
   __shared__ double red[4][1024];
   pdl_enter();
+  ProdParams p = p0;
+  if (p.sel != nullptr && *p.sel) {
+    p.R1t += p.vs_r;
+    p.R1inv += p.vs_i;
+  }
   const int t = blockIdx.x;
   int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
   while ((J + 1) * (J + 2) / 2 <= t) ++J;
@@ -1501,7 +1508,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi, oEmax;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1514,16 +1521,17 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   };
   const size_t nt = (size_t)nb * (nb + 1) / 2;
   const int64_t ldq = (d + 1) / 2 * 2;
-  w.oG1 = take(nt * 1024 * 8);
+  // G1, R1, I1, Rf, Rfi: two variants (shifted, unshifted) back to back
+  w.oG1 = take(2 * nt * 1024 * 8);
   w.oG2 = take(nt * 1024 * 8);
   w.oPart = take((size_t)nslots * 1024 * 8);
   w.oCnt = take(nt * 4);
-  w.oR1 = take(nt * 1024 * 8);
+  w.oR1 = take(2 * nt * 1024 * 8);
   w.oR2 = take(nt * 1024 * 8);
-  w.oI1 = take((size_t)nb * 1024 * 8);
+  w.oI1 = take(2 * (size_t)nb * 1024 * 8);
   w.oI2 = take((size_t)nb * 1024 * 8);
   w.oQ = take((size_t)ldq * N * 8);
-  w.oFlag = take(4);
+  w.oFlag = take(16);  // flag (chosen variant), flag of the unshifted variant, sel
   w.oR = take((size_t)d * 8);
   w.oG = take((size_t)N * 8);
   w.oBad = take(8);
@@ -1532,8 +1540,9 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oRi = take((size_t)nb * 1024 * 8);
   w.oFro = take(8);
   w.oRef = take(4);
-  w.oRf = take(nt * 1024 * 8);
-  w.oRfi = take((size_t)nb * 1024 * 8);
+  w.oRf = take(2 * nt * 1024 * 8);
+  w.oRfi = take(2 * (size_t)nb * 1024 * 8);
+  w.oEmax = take(8);
   w.bytes = off;
   return w;
 }
@@ -1558,15 +1567,22 @@ CqGramGeom cq_gram_geom(int64_t d, int nt) {
   return g;
 }
 
+struct GramOut {
+  double* Gt2 = nullptr;
+  unsigned long long* emax = nullptr;
+  double* R2t = nullptr;
+  double* R2inv = nullptr;
+};
+
 int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsigned* cnt,
-            bool pdl, cudaStream_t st) {
+            bool pdl, cudaStream_t st, const GramOut& go = GramOut()) {
   const int nt = nb * (nb + 1) / 2;
   const CqGramGeom gg = cq_gram_geom(X.d, nt);
   SKL_REQUIRE((uint64_t)gg.U * (gg.P + 1) < (1ULL << 32), SKL_ERR_SPEC, "cqr_gram: %lld rows too many",
               (long long)X.d);
   const bool vec = ((uintptr_t)X.A % 16 == 0) && (X.lda % 2 == 0) &&
                    (X.b == nullptr || (uintptr_t)X.b % 16 == 0);
-  GramParams gp{X, N, gg.nchunk, gg.U, gg.P, gg.SEG, part, Gt, cnt};
+  GramParams gp{X, N, gg.nchunk, gg.U, gg.P, gg.SEG, part, Gt, cnt, go.Gt2, go.emax, go.R2t, go.R2inv};
   if (vec)
     SKL_CUDA(launch_k(cqr_gram_kernel<true>, dim3(gg.P), dim3(128), 0, st, pdl, gp));
   else
@@ -1574,8 +1590,24 @@ int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsign
   return SKL_OK;
 }
 
-int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
-            int* flag, bool pdl, cudaStream_t st, int to = 0) {
+// One Cholesky chain: nv = 2 factors the unshifted variant beside the shifted
+// one (its buffers at + vs_*, its flag at flag + 1); skip: the second
+// factorisation's kernels return at once when cq_skipped.
+struct CqChain {
+  double* Gt;
+  double* Rt;
+  double* Rinv;
+  int* flag;
+  double* Rf;
+  double* Rfi;
+  int nv = 1;
+  int64_t vs_g = 0, vs_r = 0, vs_i = 0;
+  const unsigned long long* skip = nullptr;
+  double tau = 0.0;
+};
+
+int cq_chol(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pdl, cudaStream_t st,
+            int to = 0) {
   static std::once_flag attr_set[64];
   const size_t smem_max = ((size_t)CQ_MAXNB * CQ_TILE + 32) * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
@@ -1585,9 +1617,10 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
     return SKL_OK;
   });
   if (arc) return arc;
-  CholParams cp{Gt, nb, N, shift_coef, Rt, Rinv, flag, to};
+  CholParams cp{ch.Gt, nb, N, shift_coef, ch.Rt, ch.Rinv, ch.flag, to,
+                ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, ch.tau};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nb);
+  cfg.gridDim = dim3((unsigned)nb, (unsigned)ch.nv);
   cfg.blockDim = dim3(CQ_CHOL_NT);
   cfg.dynamicSmemBytes = ((size_t)nb * CQ_TILE + 32) * sizeof(double);
   cfg.stream = st;
@@ -1608,64 +1641,56 @@ int cq_chol(const double* Gt, int nb, int64_t N, double shift_coef, double* Rt, 
 // else right-looking over 16-tile super-blocks (cluster kernel on the
 // diagonal block, block-row solve, trailing SYRK).  `shift_coef` only on the
 // single-cluster path (the blocked path shifts beforehand).
-int cq_chol_any(double* Gt, int nb, int64_t N, double shift_coef, double* Rt, double* Rinv,
-                int* flag, double* Rf, double* Rfi, bool pdl, cudaStream_t st) {
-  if (nb <= CQ_MAXNB) return cq_chol(Gt, nb, N, shift_coef, Rt, Rinv, flag, pdl, st);
+int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pdl,
+                cudaStream_t st) {
+  if (nb <= CQ_MAXNB) return cq_chol(ch, nb, N, shift_coef, pdl, st);
+  const dim3 v1(1, (unsigned)ch.nv);
   for (int to = 0; to < nb; to += CQ_MAXNB) {
     const int nbs = std::min(CQ_MAXNB, nb - to);
-    int rc = cq_chol(Gt, nbs, N, 0.0, Rt, Rinv, flag, pdl, st, to);
+    int rc = cq_chol(ch, nbs, N, 0.0, pdl, st, to);
     if (rc) return rc;
     const int rest = nb - to - nbs;
     if (rest == 0) break;
-    TriParams tp{Gt, Rt, Rinv, to, nbs, nb};
     // R(to.., J0..) = R11^{-T} G(to.., J0..): its transpose is the TRSM of
     // G(to.., J0..)^T by R11 (16 rows per CTA)
     const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
     SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
-    SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs)), dim3(256), 0,
-                      st, true, (const double*)Rt, (const double*)Rinv, Rf, Rfi, to, nbs));
+    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, nullptr,
+                        ch.skip, ch.tau};
+    SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs), ch.nv),
+                      dim3(256), 0, st, true, fp));
     const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
-    TrsmParams sp{none, (int64_t)nbs * 32, nbs, Rt, Rinv, nullptr, 0, Rf, Rfi, Gt, Rt, to, to + nbs};
-    SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS)),
+    TrsmParams sp{none, (int64_t)nbs * 32, nbs, ch.Rt, ch.Rinv, nullptr, 0, ch.Rf, ch.Rfi,
+                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, ch.tau};
+    SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS), ch.nv),
                       dim3(CQ_TRSM_NT), tsm, st, true, sp));
-    SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2)), dim3(256), 0, st,
-                      true, tp));
+    TriParams tp{ch.Gt, ch.Rt, ch.Rinv, to, nbs, nb, ch.vs_g, ch.vs_r, ch.skip, ch.tau};
+    SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2), ch.nv), dim3(256), 0,
+                      st, true, tp));
   }
+  (void)v1;
   return SKL_OK;
 }
 
-int cq_trsm(const CqCols& X, int64_t N, int nb, const double* Rt, const double* Rinv, double* Q,
-            int64_t ldq, double* Rf, double* Rfi, bool pdl, cudaStream_t st) {
+int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* sel, double* Q,
+            int64_t ldq, bool pdl, cudaStream_t st) {
   static std::once_flag attr_set[64];
   const size_t smem_max = (size_t)CQ_MAXNB_BIG * 32 * CQ_QLD * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
-    SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_max));
+    SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_df_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     return SKL_OK;
   });
   if (arc) return arc;
-  TrsmParams tp{X, N, nb, Rt, Rinv, Q, ldq, Rf, Rfi, nullptr, nullptr, 0, 0};
+  // R1 (the picked variant) and its diagonal inverses in fragment order
+  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, ch.vs_r, ch.vs_i, sel, nullptr, 0.0};
+  SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
+                    pdl, fp));
+  TrsmParams tp{X, N, nb, ch.Rt, ch.Rinv, Q, ldq, ch.Rf, ch.Rfi, nullptr, nullptr, 0, 0,
+                0, 0, 0, nullptr, 0.0};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
-  // (cqr_trsm_kernel<false>, reading earlier Q blocks back from L2 instead
-  // of shared memory, measured no faster at 8192 x 1025: the kernel holds
-  // one CTA per SM through its registers either way)
-  static const bool left_looking = env_flag("SKL_CQR_TRSM_LL");  // A/B knob
-  if (left_looking) {
-    SKL_CUDA(launch_k(cqr_trsm_kernel<true>, dim3(grid), dim3(CQ_TRSM_NT),
-                      (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
-  } else {
-    static std::once_flag rl_set[64];
-    const int rc = once_per_device(rl_set, [&]() -> int {
-      SKL_CUDA(cudaFuncSetAttribute(cqr_trsm_df_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem_max));
-      return SKL_OK;
-    });
-    if (rc) return rc;
-    SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
-                      pdl, Rt, Rinv, Rf, Rfi, 0, nb));
-    SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
-                      (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
-  }
+  SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
+                    (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
   return SKL_OK;
 }
 
@@ -1715,7 +1740,8 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   int rc = SKL_OK;
   do {
     cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nt * 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 16, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P(w.oEmax), 0, 8, st);
     if (e != cudaSuccess) {
       set_error("cqr_solve: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
@@ -1727,7 +1753,15 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     const double shift = 11.0 * ((double)d * N + (double)N * (N + 1)) * u;
     const bool big = nb > CQ_MAXNB;
     double* fro2 = (double*)P(w.oFro);
-    if ((rc = cq_gram(M, N, nb, part, G1, cnt, false, st))) break;
+    // the unshifted variant is factored beside the shifted one (SKL_CQR_SINGLE=1:
+    // shifted only, A/B knob); well-conditioned systems then skip the second
+    // factorisation
+    static const bool single = env_flag("SKL_CQR_SINGLE");
+    const bool dual = !single;
+    const int64_t vsT = (int64_t)nt * 1024, vsI = (int64_t)nb * 1024;
+    GramOut g1;
+    if (big && dual) g1.Gt2 = G1 + vsT;
+    if ((rc = cq_gram(M, N, nb, part, G1, cnt, false, st, g1))) break;
     if (big) {  // shift once, before the super-block updates change the diagonal
       if ((e = launch_k(cqr_shift_kernel, dim3(1), dim3(1024), 0, st, true, G1, N, n, shift,
                         fro2)) != cudaSuccess) {
@@ -1738,13 +1772,37 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     }
     double* Rf = (double*)P(w.oRf);
     double* Rfi = (double*)P(w.oRfi);
-    if ((rc = cq_chol_any(G1, nb, N, big ? 0.0 : shift, R1, I1, flag, Rf, Rfi, true, st))) break;
-    if ((rc = cq_trsm(M, N, nb, R1, I1, Q, ldq, Rf, Rfi, true, st))) break;
-    if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st))) break;
-    if ((rc = cq_chol_any(G2, nb, N, 0.0, R2, I2, flag, Rf, Rfi, true, st))) break;
+    CqChain c1{G1, R1, I1, flag, Rf, Rfi};
+    c1.nv = dual ? 2 : 1;
+    c1.vs_g = big ? vsT : 0;
+    c1.vs_r = vsT;
+    c1.vs_i = vsI;
+    if ((rc = cq_chol_any(c1, nb, N, big ? 0.0 : shift, true, st))) break;
+    int* sel = dual ? flag + 2 : nullptr;
+    if (dual && (e = launch_k(cqr_pick_kernel, dim3(1), dim3(1024), 0, st, true,
+                              (const double*)(R1 + vsT), n, flag, sel)) != cudaSuccess) {
+      set_error("cqr_solve: %s", cudaGetErrorString(e));
+      rc = SKL_ERR_CUDA;
+      break;
+    }
+    if ((rc = cq_trsm(M, N, nb, c1, sel, Q, ldq, true, st))) break;
+    unsigned long long* emax = (unsigned long long*)P(w.oEmax);
+    GramOut g2;
+    if (dual) {
+      g2.emax = emax;
+      g2.R2t = R2;
+      g2.R2inv = I2;
+    }
+    if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st, g2))) break;
+    CqChain c2{G2, R2, I2, flag, Rf, Rfi};
+    if (dual) {  // first order exact to 0.1 u: N max|E|^2 <= 0.1 u
+      c2.skip = emax;
+      c2.tau = std::sqrt(0.1 * u / (double)N);
+    }
+    if ((rc = cq_chol_any(c2, nb, N, 0.0, true, st))) break;
     double* Rt = (double*)P(w.oRt);
     double* Ri = (double*)P(w.oRi);
-    ProdParams pp{R1, R2, I1, I2, Rt, Ri};
+    ProdParams pp{R1, R2, I1, I2, Rt, Ri, sel, vsT, vsI};
     int* refine = (int*)P(w.oRef);
     SolveParams sp{refine, big ? fro2 : nullptr, G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad),
                    (double*)P(w.oBadV)};

@@ -165,3 +165,31 @@ def test_solve_many_rank_deficient_member_raises_like_solve():
     with pytest.raises(SingularFactorError) as many:
         E.solve_many([good, bad, good], "saa", spec)
     assert str(one.value) == str(many.value)
+
+
+# The unshifted variant is factored beside the shifted one and taken when its
+# R's diagonal spans < 1e3 (then the second Gram is I to first order and its
+# factorisation is skipped); these cover both sides of that pick, on the
+# single-cluster and the blocked (N > 512) Cholesky.
+@pytest.mark.parametrize("d,n", [(2048, 256), (3000, 700)])
+@pytest.mark.parametrize("kappa", [1e2, 1e3, 1e5, 1e8])
+def test_cholqr_variant_pick_accuracy(d, n, kappa):
+    SA, Sb = system(d, n, kappa=kappa, seed=int(kappa) % 97 + n)
+    x, fell_back = cqr(SA, Sb)
+    assert not fell_back
+    want = oracle_x(SA, Sb)
+    rs, rw = np.linalg.norm(SA @ x - Sb), np.linalg.norm(SA @ want - Sb)
+    assert rs <= rw * (1 + 1e-10)
+    assert np.linalg.norm(x - want) / np.linalg.norm(want) <= max(1e-13, 50 * kappa * 1.1e-16)
+
+
+@pytest.mark.parametrize("d,n", [(1000, 100), (2048, 600)])
+def test_cholqr_consistent_system(d, n):
+    # Sb in the range of SA: the augmented column's pivot is ~0, the
+    # unshifted variant breaks down there and the shifted one is taken
+    rng = np.random.default_rng(d + n)
+    SA = np.asfortranarray(rng.standard_normal((d, n)))
+    x0 = rng.standard_normal(n)
+    Sb = SA @ x0
+    x, _ = cqr(SA, Sb)
+    assert np.linalg.norm(x - x0) / np.linalg.norm(x0) <= 1e-12
