@@ -92,11 +92,10 @@ struct CqCols {
   int64_t n;  // columns taken from A
   int64_t d;  // rows
 };
-// The second factorisation is skipped when the Gram of Q1 is the identity
-// to first order (cqr_gram_kernel's E mode): max |G2 - I| <= tau.
-__device__ __forceinline__ bool cq_skipped(const unsigned long long* skip, double tau) {
-  return skip != nullptr && __longlong_as_double((long long)*skip) <= tau;
-}
+// The CholeskyQR2 kernels after the pick (TRSM, second Gram, second
+// factorisation) return at once when *stop: the unshifted first factor was
+// picked and the solve is the semi-normal one (cqr_pick_kernel).
+__device__ __forceinline__ bool cq_stopped(const int* stop) { return stop != nullptr && *stop != 0; }
 
 __device__ __forceinline__ const double* cq_col(const CqCols& X, int64_t c) {
   return c < X.n ? X.A + c * X.lda : X.b;
@@ -163,12 +162,7 @@ struct GramParams {
   double* Gt;         // [ntiles][1024]
   unsigned* cnt;      // [ntiles], zero on entry, left zero
   double* Gt2;        // optional second copy of the Gram (unshifted variant)
-  // E mode (Gram of Q1): E = G - I; emax = max |E| over the first N rows and
-  // columns, R2 = I + up(E) and the inverses of its diagonal tiles I - up(E)
-  // (the Cholesky factor of I + E and its inverse to first order)
-  unsigned long long* emax;
-  double* R2t;
-  double* R2inv;
+  const int* skip;    // cq_stopped: return at once
 };
 
 __device__ __forceinline__ uint32_t cq_unit_lo(const GramParams& p, uint32_t c) { return p.U * c / p.P; }
@@ -219,34 +213,10 @@ __device__ __forceinline__ void cq_gram_mma(double (&acc)[2][4][4], const double
 // N - 1 instead (the Cholesky ignores those Gram entries).  Every segment
 // leaves a partial tile; the last CTA to finish a tile folds the partials
 // of the CTAs that cover it in CTA order (deterministic).
-__device__ __forceinline__ void cq_gram_e(const GramParams& p, int t, const double (&v)[8]) {
-  __shared__ double mred[4];
-  int I, J;
-  cq_tile_ij(t, I, J);
-  double m = 0.0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int e = threadIdx.x + i * 128, r = e & 31, c = e >> 5;
-    const int64_t gi = (int64_t)I * 32 + r, gj = (int64_t)J * 32 + c;
-    const bool valid = gi < p.N && gj < p.N;
-    const double E = v[i] - (gi == gj ? 1.0 : 0.0);
-    if (valid) m = isfinite(E) ? fmax(m, fabs(E)) : INFINITY;
-    const double F = !valid ? 0.0 : (I < J || r < c) ? E : (r == c ? 0.5 * E : 0.0);
-    p.R2t[(int64_t)t * 1024 + e] = (gi == gj ? 1.0 : 0.0) + F;
-    if (I == J) p.R2inv[(int64_t)I * 1024 + e] = (r == c ? 1.0 : 0.0) - F;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    atomicMax(p.emax, (unsigned long long)__double_as_longlong(
-                          fmax(fmax(mred[0], mred[1]), fmax(mred[2], mred[3]))));
-}
-
 template <bool VEC>
 __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
   pdl_enter();
+  if (cq_stopped(p.skip)) return;
   __shared__ double red[4][1024];
   __shared__ int is_last;
   const uint32_t c = blockIdx.x;
@@ -332,7 +302,6 @@ __global__ void __launch_bounds__(128) cqr_gram_kernel(const GramParams p) {
       if (p.Gt2 != nullptr)
 #pragma unroll
         for (int i = 0; i < 8; ++i) p.Gt2[(int64_t)t * 1024 + threadIdx.x + i * 128] = v[i];
-      if (p.emax != nullptr) cq_gram_e(p, t, v);
       if (threadIdx.x == 0) p.cnt[t] = 0u;
     }
     __syncthreads();  // red reused by the next segment
@@ -353,8 +322,7 @@ struct CholParams {
   // blockIdx.y = 1: the unshifted variant (Gt + vs_g, Rt + vs_r, Rinv + vs_i,
   // flag + 1, no shift), factored beside the shifted one
   int64_t vs_g, vs_r, vs_i;
-  const unsigned long long* skip;  // second factorisation: skipped (cq_skipped)
-  double tau;
+  const int* skip;  // second factorisation: not run (cq_stopped)
 };
 
 #ifdef CQ_FACTOR_CLOCKS
@@ -611,7 +579,7 @@ __global__ void __launch_bounds__(CQ_CHOL_NT, 1) cqr_chol_kernel(const CholParam
     if (J > 1) mbar_arrive_expect_tx(&mbar[1], CQ_PUSH_BYTES);
   }
   pdl_enter();
-  if (cq_skipped(p.skip, p.tau)) return;  // every CTA of the cluster alike
+  if (cq_stopped(p.skip)) return;  // every CTA of the cluster alike
   CQ_PROBE(0);
   // my column's Gram tiles, all copies in flight at once (8-byte cp.async;
   // past N: zero-filled, identity on the diagonal below)
@@ -748,8 +716,7 @@ struct TriParams {
   const double* Rinv; // inverses of R's diagonal tiles
   int to, nbs, nb;
   int64_t vs_g, vs_r;  // blockIdx.y = 1: the unshifted variant's buffers
-  const unsigned long long* skip;
-  double tau;
+  const int* skip;
 };
 
 __global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p0) {
@@ -760,7 +727,7 @@ __global__ void __launch_bounds__(256) cqr_syrk_kernel(const TriParams p0) {
     p.Rt += p.vs_r;
   }
   pdl_enter();
-  if (cq_skipped(p.skip, p.tau)) return;
+  if (cq_stopped(p.skip)) return;
   int jj = (int)((sqrtf(8.0f * blockIdx.x + 1.0f) - 1.0f) * 0.5f);
   while ((jj + 1) * (jj + 2) / 2 <= (int)blockIdx.x) ++jj;
   while (jj * (jj + 1) / 2 > (int)blockIdx.x) --jj;
@@ -833,8 +800,7 @@ struct TrsmParams {
   double* Rout;
   int to, J0;
   int64_t vs_g, vs_r, vs_i;  // GT, blockIdx.y = 1: the unshifted variant (G, Rout and Rf, Rfi)
-  const unsigned long long* skip;
-  double tau;
+  const int* skip;           // cq_stopped: return at once
 };
 
 constexpr int CQ_TRSM_WARPS = 8;
@@ -848,8 +814,7 @@ constexpr int CQ_TRSM_NT = CQ_TRSM_WARPS * 32;
 // bound by the L1 wavefront rate rather than by the fp64 tensor pipe.
 // Blocks [0, nbs (nbs + 1) / 2): the upper tiles of the diagonal block that
 // starts at tile `to`; the next nbs blocks: its diagonal tiles' inverses.
-// Variants: the source is variant *sel (after the pick) or blockIdx.y, the
-// destination variant blockIdx.y (buffers of variant 1 at + vs_r / + vs_i).
+// Variant blockIdx.y (buffers of variant 1 at + vs_r / + vs_i).
 struct FragParams {
   const double* Rt;
   const double* Rinv;
@@ -857,19 +822,17 @@ struct FragParams {
   double* Rfi;
   int to, nbs;
   int64_t vs_r, vs_i;
-  const int* sel;
-  const unsigned long long* skip;
-  double tau;
+  const int* skip;  // cq_stopped: return at once
 };
 
 __global__ void __launch_bounds__(256) cqr_rfrag_kernel(const FragParams fp) {
   pdl_enter();
-  if (cq_skipped(fp.skip, fp.tau)) return;
-  const int vsrc = fp.sel != nullptr ? (*fp.sel != 0) : (int)blockIdx.y, vdst = (int)blockIdx.y;
-  const double* Rt = fp.Rt + vsrc * fp.vs_r;
-  const double* Rinv = fp.Rinv + vsrc * fp.vs_i;
-  double* Rf = fp.Rf + vdst * fp.vs_r;
-  double* Rfi = fp.Rfi + vdst * fp.vs_i;
+  if (cq_stopped(fp.skip)) return;
+  const int v = (int)blockIdx.y;
+  const double* Rt = fp.Rt + v * fp.vs_r;
+  const double* Rinv = fp.Rinv + v * fp.vs_i;
+  double* Rf = fp.Rf + v * fp.vs_r;
+  double* Rfi = fp.Rfi + v * fp.vs_i;
   const int to = fp.to, nbs = fp.nbs;
   const int t = blockIdx.x, ntl = nbs * (nbs + 1) / 2;
   const double* src;
@@ -1006,7 +969,7 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
   const int Jt = p.J0 + (int)(r0 >> 5), rb = (int)(r0 & 31);
   if (threadIdx.x < nb) mbar_init(&qbar[threadIdx.x], 32);
   pdl_enter();
-  if (cq_skipped(p.skip, p.tau)) return;
+  if (cq_stopped(p.skip)) return;
   // T = X: every 8-byte copy in flight at once (zero-filled past N and d)
   if (GT) {  // X(r, c) = G(c, r): 16 contiguous rows of 32 in each tile
     for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
@@ -1074,10 +1037,12 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
 
 // After the first factorisation: take the unshifted variant (*sel = 1) when
 // it did not break down and its R's diagonal over the n columns of SA spans
-// less than CQ_REFINE_RATIO (kappa small: the unshifted CholeskyQR leaves Q1
-// orthonormal to ~kappa^2 u, so the second Gram is I to first order and its
-// factorisation can be skipped); the shifted variant otherwise.  The flag
-// then describes the chosen variant.  One CTA.
+// less than CQ_REFINE_RATIO.  Its R1 is then the Cholesky factor of the
+// normal equations of a well-conditioned SA, x = R1^{-1} R1^{-T} SA^T Sb is
+// within ~kappa^2 u, and one corrected semi-normal step brings it to ~kappa u
+// (the error contracts by ~kappa^2 u per step): the CholeskyQR2 kernels after
+// this one return at once.  The shifted variant (CholeskyQR2) otherwise.  The
+// flag then describes the chosen variant.  One CTA.
 __global__ void __launch_bounds__(1024) cqr_pick_kernel(const double* R1u, int64_t n, int* flag,
                                                         int* sel) {
   __shared__ double red[2][32];
@@ -1152,16 +1117,19 @@ __device__ __forceinline__ void cq_gtile_mma(double (&acc)[2][4][4], const doubl
 __global__ void __launch_bounds__(256) cqr_rprod_kernel(const ProdParams p0) {
   __shared__ double red[4][1024];
   pdl_enter();
-  ProdParams p = p0;
-  if (p.sel != nullptr && *p.sel) {
-    p.R1t += p.vs_r;
-    p.R1inv += p.vs_i;
-  }
+  const ProdParams& p = p0;
   const int t = blockIdx.x;
   int J = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
   while ((J + 1) * (J + 2) / 2 <= t) ++J;
   while (J * (J + 1) / 2 > t) --J;
   const int I = t - J * (J + 1) / 2;
+  if (p.sel != nullptr && *p.sel) {  // semi-normal solve: R = R1 of the unshifted variant
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      p.Rt[(int64_t)t * 1024 + e] = p.R1t[p.vs_r + (int64_t)t * 1024 + e];
+      if (I == J) p.Rinv[(int64_t)I * 1024 + e] = p.R1inv[p.vs_i + (int64_t)I * 1024 + e];
+    }
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   double acc[2][4][4];
   auto zero = [&]() {
@@ -1217,6 +1185,7 @@ struct SolveParams {
   const double* g;     // SA^T r (solve_b input)
   int64_t* bad_col;
   double* bad_val;
+  const int* sel;      // semi-normal solve on R1 (cqr_pick_kernel): always refined
 };
 
 constexpr int CQ_SOLVE_ROWS = 512;             // one thread per row (n <= 511)
@@ -1422,7 +1391,7 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
       mn = fmin(mn, ext[1][w]);
     }
     const bool broke = *p.flag != 0 || !(mx <= CQ_DIAG_RATIO_MAX * mn);
-    *p.refine = (mx <= CQ_REFINE_RATIO * mn) ? 0 : 1;
+    *p.refine = (mx <= CQ_REFINE_RATIO * mn && !cq_stopped(p.sel)) ? 0 : 1;
     const long long fb = first_bad == ~0ull ? -1 : (long long)first_bad;
     *p.bad_col = broke ? -2 : fb;
     *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
@@ -1431,20 +1400,47 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
   for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] = ys[i];
 }
 
-// x += R^{-1} R^{-T} g
+// x += R^{-1} R^{-T} g.  On the semi-normal path the correction must have
+// contracted (||dx|| <= 1e-6 ||x||, kappa^2 u well below one); otherwise the
+// solve is handed to the Householder factorisation (bad_col = -2).
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
   pdl_enter();
   if (*p.refine == 0) return;
   __shared__ double ys[CQ_MAXNB_BIG * 32];
   __shared__ double xb[32];
-  
+  __shared__ double red[2][CQ_SOLVE_NT / 32];
   const int64_t n = p.n;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) ys[i] = p.g[i];
   __syncthreads();
   cq_fwdsolve_t(p.Rt, p.Rinv, n, ys, xb);
   cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
-  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] += ys[i];
+  double dx2 = 0.0, x2 = 0.0;
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) {
+    const double xi = p.x[i] + ys[i];
+    p.x[i] = xi;
+    dx2 += ys[i] * ys[i];
+    x2 += xi * xi;
+  }
+  if (!cq_stopped(p.sel)) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dx2 += __shfl_xor_sync(0xffffffffu, dx2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = dx2;
+    red[1][warp] = x2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    if (!(a <= 1e-12 * b) && *p.bad_col == -1) *p.bad_col = -2;
+  }
 }
 
 // r = b - A x, rows split over CTAs: 64 rows x 4 column quarters per CTA.
@@ -1508,7 +1504,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi, oEmax;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1542,7 +1538,6 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oRef = take(4);
   w.oRf = take(2 * nt * 1024 * 8);
   w.oRfi = take(2 * (size_t)nb * 1024 * 8);
-  w.oEmax = take(8);
   w.bytes = off;
   return w;
 }
@@ -1569,9 +1564,7 @@ CqGramGeom cq_gram_geom(int64_t d, int nt) {
 
 struct GramOut {
   double* Gt2 = nullptr;
-  unsigned long long* emax = nullptr;
-  double* R2t = nullptr;
-  double* R2inv = nullptr;
+  const int* skip = nullptr;
 };
 
 int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsigned* cnt,
@@ -1582,7 +1575,7 @@ int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsign
               (long long)X.d);
   const bool vec = ((uintptr_t)X.A % 16 == 0) && (X.lda % 2 == 0) &&
                    (X.b == nullptr || (uintptr_t)X.b % 16 == 0);
-  GramParams gp{X, N, gg.nchunk, gg.U, gg.P, gg.SEG, part, Gt, cnt, go.Gt2, go.emax, go.R2t, go.R2inv};
+  GramParams gp{X, N, gg.nchunk, gg.U, gg.P, gg.SEG, part, Gt, cnt, go.Gt2, go.skip};
   if (vec)
     SKL_CUDA(launch_k(cqr_gram_kernel<true>, dim3(gg.P), dim3(128), 0, st, pdl, gp));
   else
@@ -1591,8 +1584,8 @@ int cq_gram(const CqCols& X, int64_t N, int nb, double* part, double* Gt, unsign
 }
 
 // One Cholesky chain: nv = 2 factors the unshifted variant beside the shifted
-// one (its buffers at + vs_*, its flag at flag + 1); skip: the second
-// factorisation's kernels return at once when cq_skipped.
+// one (its buffers at + vs_*, its flag at flag + 1); skip: the chain's
+// kernels return at once when cq_stopped.
 struct CqChain {
   double* Gt;
   double* Rt;
@@ -1602,8 +1595,7 @@ struct CqChain {
   double* Rfi;
   int nv = 1;
   int64_t vs_g = 0, vs_r = 0, vs_i = 0;
-  const unsigned long long* skip = nullptr;
-  double tau = 0.0;
+  const int* skip = nullptr;
 };
 
 int cq_chol(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pdl, cudaStream_t st,
@@ -1618,7 +1610,7 @@ int cq_chol(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pdl, c
   });
   if (arc) return arc;
   CholParams cp{ch.Gt, nb, N, shift_coef, ch.Rt, ch.Rinv, ch.flag, to,
-                ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, ch.tau};
+                ch.vs_g, ch.vs_r, ch.vs_i, ch.skip};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nb, (unsigned)ch.nv);
   cfg.blockDim = dim3(CQ_CHOL_NT);
@@ -1655,16 +1647,15 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
     // G(to.., J0..)^T by R11 (16 rows per CTA)
     const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
     SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
-    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, nullptr,
-                        ch.skip, ch.tau};
+    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, ch.skip};
     SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs), ch.nv),
                       dim3(256), 0, st, true, fp));
     const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
     TrsmParams sp{none, (int64_t)nbs * 32, nbs, ch.Rt, ch.Rinv, nullptr, 0, ch.Rf, ch.Rfi,
-                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, ch.tau};
+                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip};
     SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS), ch.nv),
                       dim3(CQ_TRSM_NT), tsm, st, true, sp));
-    TriParams tp{ch.Gt, ch.Rt, ch.Rinv, to, nbs, nb, ch.vs_g, ch.vs_r, ch.skip, ch.tau};
+    TriParams tp{ch.Gt, ch.Rt, ch.Rinv, to, nbs, nb, ch.vs_g, ch.vs_r, ch.skip};
     SKL_CUDA(launch_k(cqr_syrk_kernel, dim3((unsigned)(rest * (rest + 1) / 2), ch.nv), dim3(256), 0,
                       st, true, tp));
   }
@@ -1672,7 +1663,7 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
   return SKL_OK;
 }
 
-int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* sel, double* Q,
+int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* stop, double* Q,
             int64_t ldq, bool pdl, cudaStream_t st) {
   static std::once_flag attr_set[64];
   const size_t smem_max = (size_t)CQ_MAXNB_BIG * 32 * CQ_QLD * sizeof(double);
@@ -1682,12 +1673,12 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* se
     return SKL_OK;
   });
   if (arc) return arc;
-  // R1 (the picked variant) and its diagonal inverses in fragment order
-  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, ch.vs_r, ch.vs_i, sel, nullptr, 0.0};
+  // R1 (the shifted variant) and its diagonal inverses in fragment order
+  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, 0, 0, stop};
   SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
                     pdl, fp));
   TrsmParams tp{X, N, nb, ch.Rt, ch.Rinv, Q, ldq, ch.Rf, ch.Rfi, nullptr, nullptr, 0, 0,
-                0, 0, 0, nullptr, 0.0};
+                0, 0, 0, stop};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
   SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
                     (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
@@ -1741,7 +1732,6 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   do {
     cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nt * 4, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 16, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(P(w.oEmax), 0, 8, st);
     if (e != cudaSuccess) {
       set_error("cqr_solve: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
@@ -1754,8 +1744,9 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     const bool big = nb > CQ_MAXNB;
     double* fro2 = (double*)P(w.oFro);
     // the unshifted variant is factored beside the shifted one (SKL_CQR_SINGLE=1:
-    // shifted only, A/B knob); well-conditioned systems then skip the second
-    // factorisation
+    // shifted only, A/B knob); when it is picked (well-conditioned SA) the
+    // CholeskyQR2 kernels after the pick return at once and the solve is the
+    // corrected semi-normal one on R1
     static const bool single = env_flag("SKL_CQR_SINGLE");
     const bool dual = !single;
     const int64_t vsT = (int64_t)nt * 1024, vsI = (int64_t)nb * 1024;
@@ -1786,26 +1777,18 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
       break;
     }
     if ((rc = cq_trsm(M, N, nb, c1, sel, Q, ldq, true, st))) break;
-    unsigned long long* emax = (unsigned long long*)P(w.oEmax);
     GramOut g2;
-    if (dual) {
-      g2.emax = emax;
-      g2.R2t = R2;
-      g2.R2inv = I2;
-    }
+    g2.skip = sel;
     if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st, g2))) break;
     CqChain c2{G2, R2, I2, flag, Rf, Rfi};
-    if (dual) {  // first order exact to 0.1 u: N max|E|^2 <= 0.1 u
-      c2.skip = emax;
-      c2.tau = std::sqrt(0.1 * u / (double)N);
-    }
+    c2.skip = sel;
     if ((rc = cq_chol_any(c2, nb, N, 0.0, true, st))) break;
     double* Rt = (double*)P(w.oRt);
     double* Ri = (double*)P(w.oRi);
     ProdParams pp{R1, R2, I1, I2, Rt, Ri, sel, vsT, vsI};
     int* refine = (int*)P(w.oRef);
     SolveParams sp{refine, big ? fro2 : nullptr, G1, Rt, Ri, n, flag, x, g, (int64_t*)P(w.oBad),
-                   (double*)P(w.oBadV)};
+                   (double*)P(w.oBadV), sel};
     const size_t ysm = (size_t)N * sizeof(double);
 #define CQ_LAUNCH(call)                                                          \
   if ((e = (call)) != cudaSuccess) {                                             \
