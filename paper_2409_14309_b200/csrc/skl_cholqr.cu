@@ -801,6 +801,10 @@ struct TrsmParams {
   int to, J0;
   int64_t vs_g, vs_r, vs_i;  // GT, blockIdx.y = 1: the unshifted variant (G, Rout and Rf, Rfi)
   const int* skip;           // cq_stopped: return at once
+  // X = I (the rows r0.. of the identity): Q = R^{-1}, rows r0.. (block
+  // columns before r0's start out and stay zero); run only when *need
+  int ident;
+  const int* need;
 };
 
 constexpr int CQ_TRSM_WARPS = 8;
@@ -823,11 +827,12 @@ struct FragParams {
   int to, nbs;
   int64_t vs_r, vs_i;
   const int* skip;  // cq_stopped: return at once
+  const int* need;  // run only when *need
 };
 
 __global__ void __launch_bounds__(256) cqr_rfrag_kernel(const FragParams fp) {
   pdl_enter();
-  if (cq_stopped(fp.skip)) return;
+  if (cq_stopped(fp.skip) || (fp.need != nullptr && *fp.need == 0)) return;
   const int v = (int)blockIdx.y;
   const double* Rt = fp.Rt + v * fp.vs_r;
   const double* Rinv = fp.Rinv + v * fp.vs_i;
@@ -969,9 +974,13 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
   const int Jt = p.J0 + (int)(r0 >> 5), rb = (int)(r0 & 31);
   if (threadIdx.x < nb) mbar_init(&qbar[threadIdx.x], 32);
   pdl_enter();
-  if (cq_stopped(p.skip)) return;
+  if (cq_stopped(p.skip) || (p.need != nullptr && *p.need == 0)) return;
+  const int Js = (!GT && p.ident) ? (int)(r0 >> 5) : 0;  // first nonzero block column
   // T = X: every 8-byte copy in flight at once (zero-filled past N and d)
-  if (GT) {  // X(r, c) = G(c, r): 16 contiguous rows of 32 in each tile
+  if (!GT && p.ident) {
+    for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT)
+      tsm[(e >> 4) * CQ_QLD + (e & 15)] = (r0 + (e & 15) == (e >> 4)) ? 1.0 : 0.0;
+  } else if (GT) {  // X(r, c) = G(c, r): 16 contiguous rows of 32 in each tile
     for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
       const int ci = e & 31, r = (e >> 5) & 15, cI = e >> 9;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
@@ -992,12 +1001,12 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
   }
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
+  if (warp == Js % CQ_TRSM_WARPS) {
     double bi[8][4];
-    cq_trsm_fetch_rf(p.Rfi + (int64_t)p.to * 1024, bi);
-    cq_df_form_q<GT>(p, tsm, 0, Jt, rb, r0, bi, &qbar[0]);
+    cq_trsm_fetch_rf(p.Rfi + (int64_t)(p.to + Js) * 1024, bi);
+    cq_df_form_q<GT>(p, tsm, Js, Jt, rb, r0, bi, &qbar[Js]);
   }
-  for (int J = 0; J + 1 < nb; ++J) {
+  for (int J = Js; J + 1 < nb; ++J) {
     const int L0 = J + 1 + ((warp - (J + 1)) % 8 + 8) % 8;  // my first block column > J
     if (L0 >= nb) break;
     double bf[8][4];
@@ -1182,12 +1191,13 @@ struct SolveParams {
   int64_t n;           // R[:n,:n]; column n = Q^T Sb
   const int* flag;
   double* x;
-  const double* g;     // SA^T r (solve_b input)
+  double* g;           // SA^T r (solve_b input); r12 on the semi-normal path
   int64_t* bad_col;
   double* bad_val;
   const int* sel;      // semi-normal solve on R1 (cqr_pick_kernel): always refined
 };
 
+constexpr int CQ_RS_GROUPS = 16;               // column groups of the GEMV kernels
 constexpr int CQ_SOLVE_ROWS = 512;             // one thread per row (n <= 511)
 constexpr int CQ_SOLVE_NT = CQ_SOLVE_ROWS + 32;  // + the diagonal-block warp
 
@@ -1396,84 +1406,182 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
     *p.bad_col = broke ? -2 : fb;
     *p.bad_val = (!broke && fb >= 0) ? cq_rt(p.Rt, fb, fb) : 0.0;
   }
+  if (cq_stopped(p.sel)) {  // semi-normal path: x = R^{-1} r12 by the explicit inverse
+    for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.g[i] = ys[i];
+    return;
+  }
   cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
   for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] = ys[i];
 }
 
-// x += R^{-1} R^{-T} g.  On the semi-normal path the correction must have
-// contracted (||dx|| <= 1e-6 ||x||, kappa^2 u well below one); otherwise the
-// solve is handed to the Householder factorisation (bad_col = -2).
+// x += R^{-1} R^{-T} g (CholeskyQR2 path; the semi-normal path applies the
+// explicit inverse instead: cqr_trmv*_kernel, cqr_sne_finish_kernel).
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
   pdl_enter();
-  if (*p.refine == 0) return;
+  if (*p.refine == 0 || cq_stopped(p.sel)) return;
   __shared__ double ys[CQ_MAXNB_BIG * 32];
   __shared__ double xb[32];
-  __shared__ double red[2][CQ_SOLVE_NT / 32];
   const int64_t n = p.n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) ys[i] = p.g[i];
   __syncthreads();
   cq_fwdsolve_t(p.Rt, p.Rinv, n, ys, xb);
   cq_backsolve(p.Rt, p.Rinv, n, ys, xb);
-  double dx2 = 0.0, x2 = 0.0;
-  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) {
-    const double xi = p.x[i] + ys[i];
-    p.x[i] = xi;
-    dx2 += ys[i] * ys[i];
-    x2 += xi * xi;
+  for (int64_t i = tid; i < n; i += CQ_SOLVE_NT) p.x[i] += ys[i];
+}
+
+// Semi-normal path, with Ri = R^{-1} (upper, column-major, ld even, only
+// j >= i ever read: the rest of the buffer is stale).
+// out = Ri[:n, :n] y: 64 rows per CTA (a row pair per lane) x 16 column groups
+// over the columns right of the block's first row, folded in fixed order.
+__global__ void __launch_bounds__(CQ_RS_GROUPS * 32) cqr_trmv_kernel(const double* Ri, int64_t ld,
+                                                                   int64_t n, const double* y,
+                                                                   double* out, const int* need) {
+  extern __shared__ double ysm[];  // n
+  __shared__ double part[CQ_RS_GROUPS][64];
+  pdl_enter();
+  if (*need == 0) return;
+  for (int64_t c = threadIdx.x; c < n; c += CQ_RS_GROUPS * 32) ysm[c] = y[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t cb = (int64_t)blockIdx.x * 64, i0 = cb + 2 * lane;
+  const int64_t c0 = cb + (n - cb) * grp / CQ_RS_GROUPS, c1 = cb + (n - cb) * (grp + 1) / CQ_RS_GROUPS;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t c = c0; c < c1; ++c) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(Ri + c * ld + i0));
+    s0 = fma(c >= i0 ? v.x : 0.0, ysm[c], s0);
+    s1 = fma(c >= i0 + 1 ? v.y : 0.0, ysm[c], s1);
   }
-  if (!cq_stopped(p.sel)) return;
+  part[grp][2 * lane] = s0;
+  part[grp][2 * lane + 1] = s1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int64_t i = cb + threadIdx.x;
+    double t = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < CQ_RS_GROUPS; ++g2) t += part[g2][threadIdx.x];
+    if (i < n) out[i] = t;
+  }
+}
+
+// out = Ri[:n, :n]^T y: one warp per column j (rows 0..j, a row pair per lane;
+// y 16-byte aligned with one readable entry past n - 1).
+__global__ void __launch_bounds__(256) cqr_trmv_t_kernel(const double* Ri, int64_t ld, int64_t n,
+                                                         const double* y, double* out,
+                                                         const int* need) {
+  pdl_enter();
+  if (*need == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= n) return;
+  const double* col = Ri + j * ld;
+  double t0 = 0.0, t1 = 0.0;
+  for (int64_t i = 2 * lane; i <= j; i += 64) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(col + i));
+    const double2 w = __ldcg(reinterpret_cast<const double2*>(y + i));
+    t0 = fma(v.x, w.x, t0);
+    if (i + 1 <= j) t1 = fma(v.y, w.y, t1);
+  }
+  double t = t0 + t1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) out[j] = t;
+}
+
+// x += dx; the correction must have contracted (||dx|| <= 1e-6 ||x||, kappa^2
+// u well below one), else the solve is handed to the Householder
+// factorisation (bad_col = -2).  One CTA.
+__global__ void __launch_bounds__(1024) cqr_sne_finish_kernel(double* x, const double* dx, int64_t n,
+                                                              int64_t* bad_col, const int* need) {
+  __shared__ double red[2][32];
+  pdl_enter();
+  if (*need == 0) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    const double xi = x[i] + dx[i];
+    x[i] = xi;
+    a += dx[i] * dx[i];
+    b += xi * xi;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    dx2 += __shfl_xor_sync(0xffffffffu, dx2, o);
-    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
   }
-  if (lane == 0) {
-    red[0][warp] = dx2;
-    red[1][warp] = x2;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
   }
   __syncthreads();
-  if (tid == 0) {
-    double a = 0.0, b = 0.0;
-    for (int w = 0; w < CQ_SOLVE_NT / 32; ++w) {
+  if (threadIdx.x == 0) {
+    a = 0.0;
+    b = 0.0;
+    for (int w = 0; w < 32; ++w) {
       a += red[0][w];
       b += red[1][w];
     }
-    if (!(a <= 1e-12 * b) && *p.bad_col == -1) *p.bad_col = -2;
+    if (!(a <= 1e-12 * b) && *bad_col == -1) *bad_col = -2;
   }
 }
 
-// r = b - A x, rows split over CTAs: 64 rows x 4 column quarters per CTA.
-__global__ void __launch_bounds__(256) cqr_resid_kernel(const double* A, int64_t lda,
-                                                        const double* b, int64_t d, int64_t n,
-                                                        const double* x, double* r,
-                                                        const int* refine) {
+// r = b - A x: 64 rows per CTA (16-byte loads, a row pair per lane) x 16
+// column groups (one warp each, eight column loads in flight), the 16
+// partials of a row folded in fixed order.
+template <bool VEC>
+__global__ void __launch_bounds__(CQ_RS_GROUPS * 32) cqr_resid_kernel(const double* A, int64_t lda,
+                                                                    const double* b, int64_t d,
+                                                                    int64_t n, const double* x,
+                                                                    double* r, const int* refine) {
   extern __shared__ double xs[];  // n
-  __shared__ double part[4][64];
+  __shared__ double part[CQ_RS_GROUPS][64];
   pdl_enter();
   if (*refine == 0) return;
-  for (int64_t c = threadIdx.x; c < n; c += 256) xs[c] = x[c];
+  for (int64_t c = threadIdx.x; c < n; c += CQ_RS_GROUPS * 32) xs[c] = x[c];
   __syncthreads();
-  const int rl = threadIdx.x & 63, qc = threadIdx.x >> 6;
-  const int64_t i = (int64_t)blockIdx.x * 64 + rl;
-  const int64_t c0 = n * qc / 4, c1 = n * (qc + 1) / 4;
-  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-  if (i < d) {
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * 64 + 2 * lane;
+  const int64_t c0 = n * grp / CQ_RS_GROUPS, c1 = n * (grp + 1) / CQ_RS_GROUPS;
+  double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+  if (VEC && i0 + 1 < d) {
     int64_t c = c0;
-    for (; c + 3 < c1; c += 4) {
-      t0 = fma(A[c * lda + i], xs[c], t0);
-      t1 = fma(A[(c + 1) * lda + i], xs[c + 1], t1);
-      t2 = fma(A[(c + 2) * lda + i], xs[c + 2], t2);
-      t3 = fma(A[(c + 3) * lda + i], xs[c + 3], t3);
+    for (; c + 8 <= c1; c += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(reinterpret_cast<const double2*>(A + (c + k) * lda + i0));
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        s0 = fma(v[k].x, xs[c + k], s0);
+        s1 = fma(v[k].y, xs[c + k], s1);
+        u0 = fma(v[k + 1].x, xs[c + k + 1], u0);
+        u1 = fma(v[k + 1].y, xs[c + k + 1], u1);
+      }
     }
-    for (; c < c1; ++c) t0 = fma(A[c * lda + i], xs[c], t0);
+    for (; c < c1; ++c) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(A + c * lda + i0));
+      s0 = fma(v.x, xs[c], s0);
+      s1 = fma(v.y, xs[c], s1);
+    }
+  } else {
+    for (int64_t c = c0; c < c1; ++c) {
+      if (i0 < d) s0 = fma(A[c * lda + i0], xs[c], s0);
+      if (i0 + 1 < d) s1 = fma(A[c * lda + i0 + 1], xs[c], s1);
+    }
   }
-  part[qc][rl] = (t0 + t1) + (t2 + t3);
+  part[grp][2 * lane] = s0 + u0;
+  part[grp][2 * lane + 1] = s1 + u1;
   __syncthreads();
-  if (qc == 0 && i < d) r[i] = b[i] - (((part[0][rl] + part[1][rl]) + part[2][rl]) + part[3][rl]);
+  if (threadIdx.x < 64) {
+    const int64_t i = (int64_t)blockIdx.x * 64 + threadIdx.x;
+    double t = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < CQ_RS_GROUPS; ++g2) t += part[g2][threadIdx.x];
+    if (i < d) r[i] = b[i] - t;
+  }
 }
 
-// g = A^T r, one warp per column (fixed shuffle tree).
+// g = A^T r, one warp per column (16-byte loads, eight in flight; fixed
+// shuffle tree).
+template <bool VEC>
 __global__ void __launch_bounds__(256) cqr_gemv_t_kernel(const double* A, int64_t lda, int64_t d,
                                                          int64_t n, const double* r, double* g,
                                                          const int* refine) {
@@ -1483,14 +1591,30 @@ __global__ void __launch_bounds__(256) cqr_gemv_t_kernel(const double* A, int64_
   const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= n) return;
   const double* col = A + c * lda;
-  double t0 = 0.0, t1 = 0.0;
-  int64_t i = lane;
-  for (; i + 32 < d; i += 64) {
-    t0 = fma(col[i], r[i], t0);
-    t1 = fma(col[i + 32], r[i + 32], t1);
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+  int64_t i = 2 * lane;
+  if (VEC) {
+    for (; i + 7 * 64 + 1 < d; i += 8 * 64) {
+      double2 v[8], w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        v[k] = __ldcs(reinterpret_cast<const double2*>(col + i + k * 64));
+        w[k] = __ldcg(reinterpret_cast<const double2*>(r + i + k * 64));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        t0 = fma(v[k].x, w[k].x, t0);
+        t1 = fma(v[k].y, w[k].y, t1);
+        t2 = fma(v[k + 1].x, w[k + 1].x, t2);
+        t3 = fma(v[k + 1].y, w[k + 1].y, t3);
+      }
+    }
   }
-  if (i < d) t0 = fma(col[i], r[i], t0);
-  double t = t0 + t1;
+  for (; i < d; i += 64) {
+    t0 = fma(col[i], r[i], t0);
+    if (i + 1 < d) t1 = fma(col[i + 1], r[i + 1], t1);
+  }
+  double t = (t0 + t1) + (t2 + t3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) g[c] = t;
@@ -1504,7 +1628,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi, oY;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1526,7 +1650,8 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oR2 = take(nt * 1024 * 8);
   w.oI1 = take(2 * (size_t)nb * 1024 * 8);
   w.oI2 = take((size_t)nb * 1024 * 8);
-  w.oQ = take((size_t)ldq * N * 8);
+  // Q1; on the semi-normal path R^{-1} (ld nb * 32; GEMV row pairs read up to 64 past it)
+  w.oQ = take(((size_t)std::max<int64_t>(ldq, (int64_t)nb * 32) * N + 64) * 8);
   w.oFlag = take(16);  // flag (chosen variant), flag of the unshifted variant, sel
   w.oR = take((size_t)d * 8);
   w.oG = take((size_t)N * 8);
@@ -1538,6 +1663,7 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oRef = take(4);
   w.oRf = take(2 * nt * 1024 * 8);
   w.oRfi = take(2 * (size_t)nb * 1024 * 8);
+  w.oY = take((size_t)N * 8);
   w.bytes = off;
   return w;
 }
@@ -1647,12 +1773,12 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
     // G(to.., J0..)^T by R11 (16 rows per CTA)
     const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
     SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
-    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, ch.skip};
+    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, ch.skip, nullptr};
     SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs), ch.nv),
                       dim3(256), 0, st, true, fp));
     const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
     TrsmParams sp{none, (int64_t)nbs * 32, nbs, ch.Rt, ch.Rinv, nullptr, 0, ch.Rf, ch.Rfi,
-                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip};
+                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, 0, nullptr};
     SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS), ch.nv),
                       dim3(CQ_TRSM_NT), tsm, st, true, sp));
     TriParams tp{ch.Gt, ch.Rt, ch.Rinv, to, nbs, nb, ch.vs_g, ch.vs_r, ch.skip};
@@ -1674,11 +1800,11 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* st
   });
   if (arc) return arc;
   // R1 (the shifted variant) and its diagonal inverses in fragment order
-  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, 0, 0, stop};
+  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, 0, 0, stop, nullptr};
   SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
                     pdl, fp));
   TrsmParams tp{X, N, nb, ch.Rt, ch.Rinv, Q, ldq, ch.Rf, ch.Rfi, nullptr, nullptr, 0, 0,
-                0, 0, 0, stop};
+                0, 0, 0, stop, 0, nullptr};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
   SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
                     (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
@@ -1798,12 +1924,40 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   }
     CQ_LAUNCH(launch_k(cqr_rprod_kernel, dim3((unsigned)nt), dim3(256), 0, st, true, pp));
     CQ_LAUNCH(launch_k(cqr_solve_a_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
+    // semi-normal path: R^{-1} explicitly (the dataflow TRSM on the identity,
+    // into the unused Q buffer), then x = R^{-1} r12 (r12 left in g by solve_a)
+    const int64_t ldi = (int64_t)nb * 32;
+    if (dual) {
+      const FragParams fp{Rt, Ri, Rf, Rfi, 0, nb, 0, 0, nullptr, sel};
+      CQ_LAUNCH(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nt + nb)), dim3(256), 0, st, true, fp));
+      const CqCols idc{nullptr, 0, nullptr, 0, N};
+      TrsmParams ip{idc, N, nb, Rt, Ri, Q, ldi, Rf, Rfi, nullptr, nullptr, 0, 0, 0, 0, 0,
+                    nullptr, 1, sel};
+      CQ_LAUNCH(launch_k(cqr_trsm_df_kernel<false>, dim3((unsigned)(2 * nb)), dim3(CQ_TRSM_NT),
+                         (size_t)nb * 32 * CQ_QLD * sizeof(double), st, true, ip));
+      CQ_LAUNCH(launch_k(cqr_trmv_kernel, dim3((unsigned)((n + 63) / 64)), dim3(CQ_RS_GROUPS * 32),
+                         (size_t)n * sizeof(double), st, true, (const double*)Q, ldi, n,
+                         (const double*)g, x, (const int*)sel));
+    }
     // corrected semi-normal step: r = Sb - SA x, g = SA^T r, x += R^{-1} R^{-T} g
-    CQ_LAUNCH(launch_k(cqr_resid_kernel, dim3((unsigned)((d + 63) / 64)), dim3(256), ysm, st, true,
-                       SA, ldsa, Sb, d, n, (const double*)x, r, (const int*)refine));
-    CQ_LAUNCH(launch_k(cqr_gemv_t_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true,
-                       SA, ldsa, d, n, (const double*)r, g, (const int*)refine));
+    const bool vec = ((uintptr_t)SA % 16 == 0) && (ldsa % 2 == 0);
+    CQ_LAUNCH(launch_k(vec ? cqr_resid_kernel<true> : cqr_resid_kernel<false>,
+                       dim3((unsigned)((d + 63) / 64)), dim3(CQ_RS_GROUPS * 32), ysm, st, true, SA,
+                       ldsa, Sb, d, n, (const double*)x, r, (const int*)refine));
+    CQ_LAUNCH(launch_k(vec ? cqr_gemv_t_kernel<true> : cqr_gemv_t_kernel<false>,
+                       dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true, SA, ldsa, d, n,
+                       (const double*)r, g, (const int*)refine));
     CQ_LAUNCH(launch_k(cqr_solve_b_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
+    if (dual) {  // dx = R^{-1} R^{-T} g, x += dx
+      double* dx = (double*)P(w.oY);
+      CQ_LAUNCH(launch_k(cqr_trmv_t_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true,
+                         (const double*)Q, ldi, n, (const double*)g, r, (const int*)sel));
+      CQ_LAUNCH(launch_k(cqr_trmv_kernel, dim3((unsigned)((n + 63) / 64)), dim3(CQ_RS_GROUPS * 32),
+                         (size_t)n * sizeof(double), st, true, (const double*)Q, ldi, n,
+                         (const double*)r, dx, (const int*)sel));
+      CQ_LAUNCH(launch_k(cqr_sne_finish_kernel, dim3(1), dim3(1024), 0, st, true, x,
+                         (const double*)dx, n, (int64_t*)P(w.oBad), (const int*)sel));
+    }
 #undef CQ_LAUNCH
     e = cudaMemcpyAsync(bad_col, P(w.oBad), 8, cudaMemcpyDefault, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(bad_val, P(w.oBadV), 8, cudaMemcpyDefault, st);
