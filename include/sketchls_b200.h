@@ -396,15 +396,20 @@ int skl_qr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t
                        int64_t* bad_col, double* bad_val, void* stream);
 
 /* ---------------------------------------------------------------------
- * Reduced solve of sketch-and-apply by shifted CholeskyQR2 (device): the
- * same R (diag > 0, unique) and x as skl_qr_solve to rounding, with one
- * corrected semi-normal refinement step; the rank check of linalg.py:186-191
- * on diag(R).  Replaces the numpy QR + solve_triangular of solvers.py:309
- * for systems with n + 1 <= 512 < d (skl_cqr_supported).  Asynchronous like
+ * Reduced solve of sketch-and-apply (device): the least-squares minimiser
+ * x of ||SA x - Sb|| as skl_qr_solve gives it, to rounding (~kappa u).  A
+ * well-conditioned SA (the unshifted Cholesky factor of [SA Sb]^T [SA Sb]
+ * holds and its diagonal spans < 1e3) is solved by the corrected semi-normal
+ * equations on that factor; otherwise by shifted CholeskyQR2 (R with
+ * diag > 0, unique) plus one corrected semi-normal step -- picked on the
+ * device.  The rank check of linalg.py:186-191 on diag(R).  Replaces the
+ * numpy QR + solve_triangular of solvers.py:309 for systems with
+ * n + 1 <= 1056 < d (skl_cqr_supported).  Asynchronous like
  * skl_qr_solve_async: *bad_col (pinned host or device) receives -1 when x
  * is valid, the first rank-deficient column, or -2 when a Cholesky pivot
- * broke down; in both failure cases the caller re-solves with skl_qr_solve
- * (Householder), which produces the reference's error message.
+ * broke down or the refinement did not contract; in both failure cases the
+ * caller re-solves with skl_qr_solve (Householder), which produces the
+ * reference's error message.
  * ------------------------------------------------------------------- */
 int skl_cqr_supported(int64_t d, int64_t n);
 int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double* Sb, int64_t d, int64_t n,

@@ -1,30 +1,39 @@
-// Reduced solve of the sketch-and-apply path by shifted CholeskyQR2 with one
-// step of corrected semi-normal refinement.
+// Reduced solve of the sketch-and-apply path: Cholesky-based, two paths
+// picked on the device, each with one corrected semi-normal step.
 //
 // Reference: /root/reference/pkg/src/sketchls/solvers.py:296-320 and
 // linalg.py:166-192, 214-218 -- x = R^{-1} Q^T Sb from the economy QR of SA
 // (numpy/LAPACK Householder), diag(R) >= 0, rank check
 // |R[c,c]| < 1e-14 ||SA||_F.  The R factor with a positive diagonal is
 // unique, so any backward-stable QR gives the reference's R and x to
-// rounding; this file computes it with far fewer dependent steps than a
-// column-by-column Householder sweep (skl_qr_blocked.cu: 257 dependent
-// column steps across a thread-block cluster for config 2's 2048 x 257):
+// rounding, and x is the least-squares minimiser either way; this file
+// computes it with far fewer dependent steps than a column-by-column
+// Householder sweep (skl_qr_blocked.cu: 257 dependent column steps across a
+// thread-block cluster for config 2's 2048 x 257):
 //
 //   M  = [SA | Sb]                     (d x N, N = n + 1, never copied)
 //   G1 = M^T M                          gram kernel, fp64 tensor cores (DMMA)
-//   R1 = chol(G1 + s I)                 cluster Cholesky, s = 11 (dN + N(N+1)) u ||M||_F^2
-//   Q1 = M R1^{-1}                      row-block TRSM (DMMA)
-//   G2 = Q1^T Q1, R2 = chol(G2)         (shifted CholeskyQR2: Fukaya, Kannan,
-//   R  = R2 R1                           Nakatsukasa, Yamamoto, Yanagisawa 2020)
-//   x  = R[:n,:n]^{-1} R[:n, n]         (the augmented column carries Q^T Sb)
-//   x += R^{-1} R^{-T} SA^T (Sb - SA x) (one corrected semi-normal step)
+//   R1s = chol(G1 + s I)                cluster Cholesky, s = 11 (dN + N(N+1)) u ||M||_F^2,
+//   R1u = chol(G1)                      and the unshifted variant in a second cluster
+//   pick (cqr_pick_kernel): R1u held and its diagonal spans < 1e3 ->
+//     semi-normal path: R1u^{-1} explicitly (dataflow TRSM on I),
+//       x = R11^{-1} r12 (normal equations, ~kappa^2 u), one corrected
+//       semi-normal step (~kappa u; Householder hand-over if it does not contract)
+//   else shifted CholeskyQR2 (Fukaya, Kannan, Nakatsukasa, Yamamoto,
+//   Yanagisawa 2020):
+//     Q1 = M R1s^{-1}                   row-block dataflow TRSM (DMMA)
+//     G2 = Q1^T Q1, R2 = chol(G2), R = R2 R1s
+//     x  = R[:n,:n]^{-1} R[:n, n]       (the augmented column carries Q^T Sb)
+//     x += R^{-1} R^{-T} SA^T (Sb - SA x) when R's diagonal spans > 1e3
+//   The kernels of the path not taken return at once on the pick's flag.
 //
 // The refinement step brings the x error on config 2 (kappa = 1e8) to the
 // spread of two Householder QRs of the same system (measured in numpy on the
 // full-size sketched system: 4-6e-9 vs the Householder spread of 3-6e-9).
-// A non-positive or non-finite Cholesky pivot (numerically rank deficient
-// or kappa beyond ~1e15) sets a flag; the caller then falls back to the
-// Householder factorisation, which also produces the reference's error.
+// A non-positive or non-finite Cholesky pivot of the chosen variant
+// (numerically rank deficient or kappa beyond ~1e15) sets a flag; the caller
+// then falls back to the Householder factorisation, which also produces the
+// reference's error.
 //
 // Layouts: Gram, R and the diagonal-block inverses of R are kept as 32 x 32
 // column-major tiles ("tile layout"), upper tiles (I <= J) packed column by
@@ -1813,7 +1822,7 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* st
 
 }  // namespace
 
-// Sizes the CholeskyQR path covers: N = n + 1 <= 512 and at least one row
+// Sizes the CholeskyQR path covers: N = n + 1 <= 1056 and at least one row
 // more than N (a square augmented system is rank deficient by construction).
 extern "C" int skl_cqr_supported(int64_t d, int64_t n) {
   const int64_t N = n + 1;
@@ -1831,7 +1840,7 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   SKL_REQUIRE(SA && Sb && x && bad_col && bad_val && ldsa >= d, SKL_ERR_INVALID,
               "cqr_solve: bad arguments");
   SKL_REQUIRE(skl_cqr_supported(d, n), SKL_ERR_SPEC,
-              "cqr_solve: %lld x %lld outside the CholeskyQR path (n + 1 <= 512 < d)",
+              "cqr_solve: %lld x %lld outside the CholeskyQR path (n + 1 <= 1056 < d)",
               (long long)d, (long long)n);
   const int64_t N = n + 1;
   const int nb = (int)((N + 31) / 32);

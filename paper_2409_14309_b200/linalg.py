@@ -290,7 +290,7 @@ _CQR_OFF = os.environ.get("SKL_QR_HOUSEHOLDER", "") not in ("", "0")
 
 def cholqr_enabled(d: int, n: int) -> bool:
     """Whether the reduced solve of a d x n sketched system takes the
-    CholeskyQR2 path (skl_cqr_solve_async): n + 1 <= 512 < d, unless
+    Cholesky-based path (skl_cqr_solve_async): n + 1 <= 1056 < d, unless
     SKL_QR_HOUSEHOLDER=1 forces the Householder factorisation (A/B knob,
     read at import)."""
     return not _CQR_OFF and bool(_native.lib().skl_cqr_supported(d, n))
@@ -301,9 +301,11 @@ def qr_solve_device_async(SA, ldsa: int, Sb, d: int, n: int, flags=None):
     returns (x, check) where check() -- to be called once the stream has
     been synchronised (e.g. by the residual pass) -- returns None when x is
     valid, or a replacement x, or raises the SingularFactorError
-    skl_qr_solve would have.  Sketched systems with n + 1 <= 512 < d go
-    through the CholeskyQR2 kernels (csrc/skl_cholqr.cu); when one of their
-    Cholesky pivots breaks down or their rank check fires, check() re-solves
+    skl_qr_solve would have.  Sketched systems with n + 1 <= 1056 < d go
+    through the Cholesky-based kernels (csrc/skl_cholqr.cu: a semi-normal
+    solve for a well-conditioned SA, shifted CholeskyQR2 otherwise, picked
+    on the device); when a Cholesky pivot breaks down, the refinement does
+    not contract or the rank check fires, check() re-solves
     with the Householder factorisation, which decides (and words the error
     exactly as linalg.py:186-191).  The flags land in a pinned per-thread
     buffer."""

@@ -193,3 +193,39 @@ def test_cholqr_consistent_system(d, n):
     Sb = SA @ x0
     x, _ = cqr(SA, Sb)
     assert np.linalg.norm(x - x0) / np.linalg.norm(x0) <= 1e-12
+
+
+def test_semi_normal_path_is_deterministic():
+    for d, n in [(2048, 256), (3000, 700)]:
+        SA, Sb = system(d, n, kappa=10.0, seed=d)
+        a, _ = cqr(SA, Sb)
+        for _ in range(2):
+            b, _ = cqr(SA, Sb)
+            assert np.array_equal(a, b)
+
+
+def test_shifted_only_knob_matches_oracle(tmp_path):
+    # SKL_CQR_SINGLE=1 (A/B knob, read once per process): shifted CholeskyQR2
+    # for every system, the well-conditioned ones included
+    import subprocess
+    import textwrap
+    script = tmp_path / "single.py"
+    script.write_text(textwrap.dedent(f"""
+        import sys
+        sys.path.insert(0, {str(ROOT)!r})
+        sys.path.insert(0, {str(Path(__file__).resolve().parent)!r})
+        import numpy as np
+        from test_gpu_cholqr import system, cqr, oracle_x
+        for d, n in [(2048, 256), (3000, 700)]:
+            SA, Sb = system(d, n, kappa=10.0, seed=d + n)
+            x, fb = cqr(SA, Sb)
+            want = oracle_x(SA, Sb)
+            err = np.linalg.norm(x - want) / np.linalg.norm(want)
+            assert not fb and err <= 1e-13, (d, n, err)
+        print("ok")
+    """))
+    import os
+    env = dict(os.environ, SKL_CQR_SINGLE="1")
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

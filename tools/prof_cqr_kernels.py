@@ -1,7 +1,8 @@
 """Warm per-kernel times of the CholeskyQR2 reduced solve (torch.profiler,
 CUDA activity), averaged over `reps` solves of a d x n system.  Run with
 SKL_NO_PDL=1: with programmatic dependent launch a kernel's recorded span
-starts while its predecessor still runs.  Usage: prof_cqr_kernels.py d n [reps]"""
+starts while its predecessor still runs.  Usage: prof_cqr_kernels.py d n [reps] [kappa]
+(kappa: log-spaced singular values, e.g. 1e8 = config 2; default a Gaussian SA)."""
 import sys
 from pathlib import Path
 
@@ -14,7 +15,14 @@ from paper_2409_14309_b200.linalg import reduced_solve_device  # noqa: E402
 
 d, n = int(sys.argv[1]), int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
-M = torch.randn((n, d), dtype=torch.float64, device="cuda").t()
+kappa = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
+if kappa > 0:
+    U, _ = torch.linalg.qr(torch.randn((d, n), dtype=torch.float64, device="cuda"))
+    V, _ = torch.linalg.qr(torch.randn((n, n), dtype=torch.float64, device="cuda"))
+    sv = torch.logspace(0, -torch.log10(torch.tensor(kappa)).item(), n, dtype=torch.float64, device="cuda")
+    M = ((U * sv) @ V.t()).t().contiguous().t()
+else:
+    M = torch.randn((n, d), dtype=torch.float64, device="cuda").t()
 y = torch.randn((d,), dtype=torch.float64, device="cuda")
 for _ in range(20):
     reduced_solve_device(M, d, y, d, n)
