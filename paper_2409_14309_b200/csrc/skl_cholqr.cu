@@ -827,6 +827,48 @@ constexpr int CQ_TRSM_NT = CQ_TRSM_WARPS * 32;
 // bound by the L1 wavefront rate rather than by the fp64 tensor pipe.
 // Blocks [0, nbs (nbs + 1) / 2): the upper tiles of the diagonal block that
 // starts at tile `to`; the next nbs blocks: its diagonal tiles' inverses.
+// The pick after the first factorisation: take the unshifted variant (1)
+// when it did not break down and its R's diagonal over the n columns of SA
+// spans less than CQ_REFINE_RATIO.  Its R1 is then the Cholesky factor of
+// the normal equations of a well-conditioned SA, x = R1^{-1} R1^{-T} SA^T Sb
+// is within ~kappa^2 u, and one corrected semi-normal step brings it to
+// ~kappa u (the error contracts by ~kappa^2 u per step): the CholeskyQR2
+// kernels after the pick return at once.  The shifted variant (0,
+// CholeskyQR2) otherwise.  Block-wide (every CTA of the kernel that makes
+// it reaches the same answer); the result in every thread.
+__device__ __noinline__ int cq_pick(const double* R1u, int64_t n, const int* flag) {
+  __shared__ double red[2][32];
+  __shared__ int res;
+  double lo = INFINITY, hi = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = R1u[cq_tile((int)(i >> 5), (int)(i >> 5)) * 1024 + (i & 31) * 33];
+    const bool ok = v > 0.0 && v < INFINITY;
+    lo = ok ? fmin(lo, v) : -1.0;
+    hi = ok ? fmax(hi, v) : INFINITY;
+    if (!ok) break;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = lo;
+    red[1][w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      lo = fmin(lo, red[0][k]);
+      hi = fmax(hi, red[1][k]);
+    }
+    res = (flag[1] == 0 && lo > 0.0 && hi < CQ_REFINE_RATIO * lo) ? 1 : 0;
+  }
+  __syncthreads();
+  return res;
+}
+
 // Variant blockIdx.y (buffers of variant 1 at + vs_r / + vs_i).
 struct FragParams {
   const double* Rt;
@@ -837,16 +879,30 @@ struct FragParams {
   int64_t vs_r, vs_i;
   const int* skip;  // cq_stopped: return at once
   const int* need;  // run only when *need
+  // pick != nullptr (after the first factorisation): every CTA makes the
+  // pick (cq_pick, R1u's diagonal = Rt + vs_r), takes that variant as the
+  // source, and CTA 0 records it (pick[2]; pick[0] = 0 when the unshifted
+  // variant is taken: the flag then describes the chosen variant)
+  int* pick;
+  int64_t n;
 };
 
 __global__ void __launch_bounds__(256) cqr_rfrag_kernel(const FragParams fp) {
   pdl_enter();
   if (cq_stopped(fp.skip) || (fp.need != nullptr && *fp.need == 0)) return;
-  const int v = (int)blockIdx.y;
-  const double* Rt = fp.Rt + v * fp.vs_r;
-  const double* Rinv = fp.Rinv + v * fp.vs_i;
-  double* Rf = fp.Rf + v * fp.vs_r;
-  double* Rfi = fp.Rfi + v * fp.vs_i;
+  int vs = (int)blockIdx.y;
+  const int vd = (int)blockIdx.y;
+  if (fp.pick != nullptr) {
+    vs = cq_pick(fp.Rt + fp.vs_r, fp.n, fp.pick);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      fp.pick[2] = vs;
+      if (vs) fp.pick[0] = 0;
+    }
+  }
+  const double* Rt = fp.Rt + vs * fp.vs_r;
+  const double* Rinv = fp.Rinv + vs * fp.vs_i;
+  double* Rf = fp.Rf + vd * fp.vs_r;
+  double* Rfi = fp.Rfi + vd * fp.vs_i;
   const int to = fp.to, nbs = fp.nbs;
   const int t = blockIdx.x, ntl = nbs * (nbs + 1) / 2;
   const double* src;
@@ -1050,48 +1106,6 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
       cq_df_update<false>(p, tsm, J, L, qf0, qf1, bf, bn);
       cq_copy_frags(bf, bn);
     }
-  }
-}
-
-// After the first factorisation: take the unshifted variant (*sel = 1) when
-// it did not break down and its R's diagonal over the n columns of SA spans
-// less than CQ_REFINE_RATIO.  Its R1 is then the Cholesky factor of the
-// normal equations of a well-conditioned SA, x = R1^{-1} R1^{-T} SA^T Sb is
-// within ~kappa^2 u, and one corrected semi-normal step brings it to ~kappa u
-// (the error contracts by ~kappa^2 u per step): the CholeskyQR2 kernels after
-// this one return at once.  The shifted variant (CholeskyQR2) otherwise.  The
-// flag then describes the chosen variant.  One CTA.
-__global__ void __launch_bounds__(1024) cqr_pick_kernel(const double* R1u, int64_t n, int* flag,
-                                                        int* sel) {
-  __shared__ double red[2][32];
-  pdl_enter();
-  double lo = INFINITY, hi = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) {
-    const double v = R1u[cq_tile((int)(i >> 5), (int)(i >> 5)) * 1024 + (i & 31) * 33];
-    const bool ok = v > 0.0 && v < INFINITY;
-    lo = ok ? fmin(lo, v) : -1.0;
-    hi = ok ? fmax(hi, v) : INFINITY;
-    if (!ok) break;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    red[0][w] = lo;
-    red[1][w] = hi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < 32; ++k) {
-      lo = fmin(lo, red[0][k]);
-      hi = fmax(hi, red[1][k]);
-    }
-    const int s2 = (flag[1] == 0 && lo > 0.0 && hi < CQ_REFINE_RATIO * lo) ? 1 : 0;
-    *sel = s2;
-    if (s2) flag[0] = 0;
   }
 }
 
@@ -1424,7 +1438,7 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_a_kernel(const SolvePar
 }
 
 // x += R^{-1} R^{-T} g (CholeskyQR2 path; the semi-normal path applies the
-// explicit inverse instead: cqr_trmv*_kernel, cqr_sne_finish_kernel).
+// explicit inverse instead: cqr_trmv_t_kernel, cqr_trmv_kernel).
 __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolveParams p) {
   pdl_enter();
   if (*p.refine == 0 || cq_stopped(p.sel)) return;
@@ -1443,11 +1457,25 @@ __global__ void __launch_bounds__(CQ_SOLVE_NT) cqr_solve_b_kernel(const SolvePar
 // j >= i ever read: the rest of the buffer is stale).
 // out = Ri[:n, :n] y: 64 rows per CTA (a row pair per lane) x 16 column groups
 // over the columns right of the block's first row, folded in fixed order.
+// Finishing form (xacc != nullptr): x += out instead, and the correction
+// must have contracted (||dx|| <= 1e-6 ||x||, kappa^2 u well below one) --
+// per-CTA sums, the last CTA folds them in CTA order -- else the solve is
+// handed to the Householder factorisation (bad_col = -2).
+struct TrmvFinish {
+  double* xacc;
+  int64_t* bad_col;
+  unsigned* ticket;  // zero on entry, left zero
+  double* part;      // [2 * CTAs]
+};
+
 __global__ void __launch_bounds__(CQ_RS_GROUPS * 32) cqr_trmv_kernel(const double* Ri, int64_t ld,
                                                                    int64_t n, const double* y,
-                                                                   double* out, const int* need) {
+                                                                   double* out, const int* need,
+                                                                   const TrmvFinish fin) {
   extern __shared__ double ysm[];  // n
   __shared__ double part[CQ_RS_GROUPS][64];
+  __shared__ double ab[2][2];
+  __shared__ int is_last;
   pdl_enter();
   if (*need == 0) return;
   for (int64_t c = threadIdx.x; c < n; c += CQ_RS_GROUPS * 32) ysm[c] = y[c];
@@ -1455,21 +1483,72 @@ __global__ void __launch_bounds__(CQ_RS_GROUPS * 32) cqr_trmv_kernel(const doubl
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t cb = (int64_t)blockIdx.x * 64, i0 = cb + 2 * lane;
   const int64_t c0 = cb + (n - cb) * grp / CQ_RS_GROUPS, c1 = cb + (n - cb) * (grp + 1) / CQ_RS_GROUPS;
-  double s0 = 0.0, s1 = 0.0;
-  for (int64_t c = c0; c < c1; ++c) {
+  double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+  int64_t c = c0;
+  for (; c + 8 <= c1; c += 8) {  // eight column loads in flight
+    double2 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(reinterpret_cast<const double2*>(Ri + (c + k) * ld + i0));
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      s0 = fma(c + k >= i0 ? v[k].x : 0.0, ysm[c + k], s0);
+      s1 = fma(c + k >= i0 + 1 ? v[k].y : 0.0, ysm[c + k], s1);
+      u0 = fma(c + k + 1 >= i0 ? v[k + 1].x : 0.0, ysm[c + k + 1], u0);
+      u1 = fma(c + k + 1 >= i0 + 1 ? v[k + 1].y : 0.0, ysm[c + k + 1], u1);
+    }
+  }
+  for (; c < c1; ++c) {
     const double2 v = __ldcg(reinterpret_cast<const double2*>(Ri + c * ld + i0));
     s0 = fma(c >= i0 ? v.x : 0.0, ysm[c], s0);
     s1 = fma(c >= i0 + 1 ? v.y : 0.0, ysm[c], s1);
   }
-  part[grp][2 * lane] = s0;
-  part[grp][2 * lane + 1] = s1;
+  part[grp][2 * lane] = s0 + u0;
+  part[grp][2 * lane + 1] = s1 + u1;
   __syncthreads();
   if (threadIdx.x < 64) {
     const int64_t i = cb + threadIdx.x;
     double t = 0.0;
 #pragma unroll
     for (int g2 = 0; g2 < CQ_RS_GROUPS; ++g2) t += part[g2][threadIdx.x];
-    if (i < n) out[i] = t;
+    if (fin.xacc == nullptr) {
+      if (i < n) out[i] = t;
+    } else {
+      double a = 0.0, b = 0.0;
+      if (i < n) {
+        const double xi = fin.xacc[i] + t;
+        fin.xacc[i] = xi;
+        a = t * t;
+        b = xi * xi;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (lane == 0) {
+        ab[threadIdx.x >> 5][0] = a;
+        ab[threadIdx.x >> 5][1] = b;
+      }
+    }
+  }
+  if (fin.xacc == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fin.part[2 * blockIdx.x] = ab[0][0] + ab[1][0];
+    fin.part[2 * blockIdx.x + 1] = ab[0][1] + ab[1][1];
+    __threadfence();
+    is_last = atomicAdd(fin.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double a = 0.0, b = 0.0;
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      a += __ldcg(fin.part + 2 * q);
+      b += __ldcg(fin.part + 2 * q + 1);
+    }
+    if (!(a <= 1e-12 * b) && *fin.bad_col == -1) *fin.bad_col = -2;
+    *fin.ticket = 0u;
   }
 }
 
@@ -1485,7 +1564,21 @@ __global__ void __launch_bounds__(256) cqr_trmv_t_kernel(const double* Ri, int64
   if (j >= n) return;
   const double* col = Ri + j * ld;
   double t0 = 0.0, t1 = 0.0;
-  for (int64_t i = 2 * lane; i <= j; i += 64) {
+  int64_t i = 2 * lane;
+  for (; i + 3 * 64 <= j; i += 4 * 64) {  // four row pairs in flight, all within rows <= j
+    double2 v[4], w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = __ldcg(reinterpret_cast<const double2*>(col + i + k * 64));
+      w[k] = __ldcg(reinterpret_cast<const double2*>(y + i + k * 64));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      t0 = fma(v[k].x, w[k].x, t0);
+      t1 = (i + k * 64 + 1 <= j) ? fma(v[k].y, w[k].y, t1) : t1;
+    }
+  }
+  for (; i <= j; i += 64) {
     const double2 v = __ldcg(reinterpret_cast<const double2*>(col + i));
     const double2 w = __ldcg(reinterpret_cast<const double2*>(y + i));
     t0 = fma(v.x, w.x, t0);
@@ -1495,42 +1588,6 @@ __global__ void __launch_bounds__(256) cqr_trmv_t_kernel(const double* Ri, int64
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) out[j] = t;
-}
-
-// x += dx; the correction must have contracted (||dx|| <= 1e-6 ||x||, kappa^2
-// u well below one), else the solve is handed to the Householder
-// factorisation (bad_col = -2).  One CTA.
-__global__ void __launch_bounds__(1024) cqr_sne_finish_kernel(double* x, const double* dx, int64_t n,
-                                                              int64_t* bad_col, const int* need) {
-  __shared__ double red[2][32];
-  pdl_enter();
-  if (*need == 0) return;
-  double a = 0.0, b = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) {
-    const double xi = x[i] + dx[i];
-    x[i] = xi;
-    a += dx[i] * dx[i];
-    b += xi * xi;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = a;
-    red[1][threadIdx.x >> 5] = b;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    a = 0.0;
-    b = 0.0;
-    for (int w = 0; w < 32; ++w) {
-      a += red[0][w];
-      b += red[1][w];
-    }
-    if (!(a <= 1e-12 * b) && *bad_col == -1) *bad_col = -2;
-  }
 }
 
 // r = b - A x: 64 rows per CTA (16-byte loads, a row pair per lane) x 16
@@ -1637,7 +1694,7 @@ namespace {
 
 struct CqWork {
   size_t bytes = 0;
-  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oFlag, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi, oY;
+  size_t oG1, oG2, oPart, oCnt, oR1, oR2, oI1, oI2, oQ, oR, oG, oBad, oBadV, oRt, oRi, oFro, oRef, oRf, oRfi, oY;
 };
 
 CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
@@ -1654,14 +1711,13 @@ CqWork cq_layout(int64_t d, int64_t N, int nb, int nslots) {
   w.oG1 = take(2 * nt * 1024 * 8);
   w.oG2 = take(nt * 1024 * 8);
   w.oPart = take((size_t)nslots * 1024 * 8);
-  w.oCnt = take(nt * 4);
+  w.oCnt = take(nt * 4 + 16);  // tile counters, then the flags (one memset)
   w.oR1 = take(2 * nt * 1024 * 8);
   w.oR2 = take(nt * 1024 * 8);
   w.oI1 = take(2 * (size_t)nb * 1024 * 8);
   w.oI2 = take((size_t)nb * 1024 * 8);
   // Q1; on the semi-normal path R^{-1} (ld nb * 32; GEMV row pairs read up to 64 past it)
   w.oQ = take(((size_t)std::max<int64_t>(ldq, (int64_t)nb * 32) * N + 64) * 8);
-  w.oFlag = take(16);  // flag (chosen variant), flag of the unshifted variant, sel
   w.oR = take((size_t)d * 8);
   w.oG = take((size_t)N * 8);
   w.oBad = take(8);
@@ -1782,7 +1838,8 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
     // G(to.., J0..)^T by R11 (16 rows per CTA)
     const size_t tsm = (size_t)nbs * 32 * CQ_QLD * sizeof(double);
     SKL_CUDA(raise_smem_limit(cqr_trsm_df_kernel<true>, tsm));
-    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, ch.skip, nullptr};
+    const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, to, nbs, ch.vs_r, ch.vs_i, ch.skip, nullptr,
+                        nullptr, 0};
     SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nbs * (nbs + 1) / 2 + nbs), ch.nv),
                       dim3(256), 0, st, true, fp));
     const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
@@ -1798,8 +1855,9 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
   return SKL_OK;
 }
 
-int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* stop, double* Q,
+int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, int* pick, double* Q,
             int64_t ldq, bool pdl, cudaStream_t st) {
+  const int* stop = pick != nullptr ? pick + 2 : nullptr;
   static std::once_flag attr_set[64];
   const size_t smem_max = (size_t)CQ_MAXNB_BIG * 32 * CQ_QLD * sizeof(double);
   const int arc = once_per_device(attr_set, [&]() -> int {
@@ -1808,8 +1866,10 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, const int* st
     return SKL_OK;
   });
   if (arc) return arc;
-  // R1 (the shifted variant) and its diagonal inverses in fragment order
-  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, 0, 0, stop, nullptr};
+  // the pick, then R1 of the picked variant and its diagonal inverses in
+  // fragment order (for this TRSM, or for R1u^{-1} on the semi-normal path)
+  const FragParams fp{ch.Rt, ch.Rinv, ch.Rf, ch.Rfi, 0, nb, ch.vs_r, ch.vs_i, nullptr, nullptr,
+                      pick, X.n};
   SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
                     pdl, fp));
   TrsmParams tp{X, N, nb, ch.Rt, ch.Rinv, Q, ldq, ch.Rf, ch.Rfi, nullptr, nullptr, 0, 0,
@@ -1860,13 +1920,13 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
   double* I1 = (double*)P(w.oI1);
   double* I2 = (double*)P(w.oI2);
   double* Q = (double*)P(w.oQ);
-  int* flag = (int*)P(w.oFlag);
+  // flag of the chosen variant, flag of the unshifted variant, sel, ticket
+  int* flag = (int*)P(w.oCnt) + nt;
   double* r = (double*)P(w.oR);
   double* g = (double*)P(w.oG);
   int rc = SKL_OK;
   do {
-    cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nt * 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 16, st);
+    cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nt * 4 + 16, st);
     if (e != cudaSuccess) {
       set_error("cqr_solve: %s", cudaGetErrorString(e));
       rc = SKL_ERR_CUDA;
@@ -1905,13 +1965,7 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     c1.vs_i = vsI;
     if ((rc = cq_chol_any(c1, nb, N, big ? 0.0 : shift, true, st))) break;
     int* sel = dual ? flag + 2 : nullptr;
-    if (dual && (e = launch_k(cqr_pick_kernel, dim3(1), dim3(1024), 0, st, true,
-                              (const double*)(R1 + vsT), n, flag, sel)) != cudaSuccess) {
-      set_error("cqr_solve: %s", cudaGetErrorString(e));
-      rc = SKL_ERR_CUDA;
-      break;
-    }
-    if ((rc = cq_trsm(M, N, nb, c1, sel, Q, ldq, true, st))) break;
+    if ((rc = cq_trsm(M, N, nb, c1, dual ? flag : nullptr, Q, ldq, true, st))) break;
     GramOut g2;
     g2.skip = sel;
     if ((rc = cq_gram(Q1, N, nb, part, G2, cnt, true, st, g2))) break;
@@ -1937,8 +1991,6 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     // into the unused Q buffer), then x = R^{-1} r12 (r12 left in g by solve_a)
     const int64_t ldi = (int64_t)nb * 32;
     if (dual) {
-      const FragParams fp{Rt, Ri, Rf, Rfi, 0, nb, 0, 0, nullptr, sel};
-      CQ_LAUNCH(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nt + nb)), dim3(256), 0, st, true, fp));
       const CqCols idc{nullptr, 0, nullptr, 0, N};
       TrsmParams ip{idc, N, nb, Rt, Ri, Q, ldi, Rf, Rfi, nullptr, nullptr, 0, 0, 0, 0, 0,
                     nullptr, 1, sel};
@@ -1946,7 +1998,7 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
                          (size_t)nb * 32 * CQ_QLD * sizeof(double), st, true, ip));
       CQ_LAUNCH(launch_k(cqr_trmv_kernel, dim3((unsigned)((n + 63) / 64)), dim3(CQ_RS_GROUPS * 32),
                          (size_t)n * sizeof(double), st, true, (const double*)Q, ldi, n,
-                         (const double*)g, x, (const int*)sel));
+                         (const double*)g, x, (const int*)sel, TrmvFinish{}));
     }
     // corrected semi-normal step: r = Sb - SA x, g = SA^T r, x += R^{-1} R^{-T} g
     const bool vec = ((uintptr_t)SA % 16 == 0) && (ldsa % 2 == 0);
@@ -1957,15 +2009,13 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
                        dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true, SA, ldsa, d, n,
                        (const double*)r, g, (const int*)refine));
     CQ_LAUNCH(launch_k(cqr_solve_b_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
-    if (dual) {  // dx = R^{-1} R^{-T} g, x += dx
-      double* dx = (double*)P(w.oY);
+    if (dual) {  // x += R^{-1} R^{-T} g, with the contraction check
       CQ_LAUNCH(launch_k(cqr_trmv_t_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true,
                          (const double*)Q, ldi, n, (const double*)g, r, (const int*)sel));
+      const TrmvFinish fin{x, (int64_t*)P(w.oBad), (unsigned*)(flag + 3), (double*)P(w.oY)};
       CQ_LAUNCH(launch_k(cqr_trmv_kernel, dim3((unsigned)((n + 63) / 64)), dim3(CQ_RS_GROUPS * 32),
                          (size_t)n * sizeof(double), st, true, (const double*)Q, ldi, n,
-                         (const double*)r, dx, (const int*)sel));
-      CQ_LAUNCH(launch_k(cqr_sne_finish_kernel, dim3(1), dim3(1024), 0, st, true, x,
-                         (const double*)dx, n, (int64_t*)P(w.oBad), (const int*)sel));
+                         (const double*)r, (double*)nullptr, (const int*)sel, fin));
     }
 #undef CQ_LAUNCH
     e = cudaMemcpyAsync(bad_col, P(w.oBad), 8, cudaMemcpyDefault, st);
