@@ -1828,8 +1828,13 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
                 cudaStream_t st) {
   if (nb <= CQ_MAXNB) return cq_chol(ch, nb, N, shift_coef, pdl, st);
   const dim3 v1(1, (unsigned)ch.nv);
-  for (int to = 0; to < nb; to += CQ_MAXNB) {
-    const int nbs = std::min(CQ_MAXNB, nb - to);
+  // equal super-blocks (33 tiles: 11 + 11 + 11, not 16 + 16 + 1): the
+  // block-row solves' chains are one step per tile of their super-block
+  static const int sb_env = env_int("SKL_CQR_SB", 0);  // A/B knob: fixed super-block size
+  const int nsb = (nb + CQ_MAXNB - 1) / CQ_MAXNB;
+  const int sb = sb_env > 0 ? std::min(sb_env, CQ_MAXNB) : (nb + nsb - 1) / nsb;
+  for (int to = 0; to < nb; to += sb) {
+    const int nbs = std::min(sb, nb - to);
     int rc = cq_chol(ch, nbs, N, 0.0, pdl, st, to);
     if (rc) return rc;
     const int rest = nb - to - nbs;
