@@ -814,6 +814,9 @@ struct TrsmParams {
   // columns before r0's start out and stay zero); run only when *need
   int ident;
   const int* need;
+  // X from the rows of R's tile layout: X(r, c) = R(r, to * 32 + c) (the
+  // off-diagonal block of the 2 x 2 split of R^{-1}); nullptr: X as above
+  const double* XR;
 };
 
 constexpr int CQ_TRSM_WARPS = 8;
@@ -1022,7 +1025,7 @@ __device__ __forceinline__ void cq_copy_frags(double (&dst)[8][4], const double 
 }
 
 template <bool GT>
-__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmParams p0) {
+__device__ __forceinline__ void cq_df_body(const TrsmParams& p0, int blk) {
   extern __shared__ __align__(16) double tsm[];  // T[c * CQ_QLD + r]; becomes Q
   __shared__ __align__(8) uint64_t qbar[CQ_MAXNB_BIG];
   TrsmParams p = p0;
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
     p.Rfi += p.vs_i;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.x * CQ_TRSM_ROWS;
+  const int64_t r0 = (int64_t)blk * CQ_TRSM_ROWS;
   const int64_t d = p.X.d;
   const int nb = p.nb, ncol = nb * 32;
   const int Jt = p.J0 + (int)(r0 >> 5), rb = (int)(r0 & 31);
@@ -1051,6 +1054,14 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                        smem_u32(tsm + (cI * 32 + ci) * CQ_QLD + r)),
                    "l"(p.G + cq_tile(p.to + cI, Jt) * 1024 + (rb + r) * 32 + ci)
+                   : "memory");
+    }
+  } else if (p.XR != nullptr) {  // X(r, c) = R(r0 + r, to * 32 + c): 16 contiguous doubles per column
+    for (int e = threadIdx.x; e < ncol * CQ_TRSM_ROWS; e += CQ_TRSM_NT) {
+      const int r = e & 15, c = e >> 4;
+      const int64_t gr = r0 + r;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(tsm + c * CQ_QLD + r)),
+                   "l"(p.XR + cq_tile((int)(gr >> 5), p.to + (c >> 5)) * 1024 + (c & 31) * 32 + (gr & 31))
                    : "memory");
     }
   } else {
@@ -1107,6 +1118,76 @@ __global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmPa
       cq_copy_frags(bf, bn);
     }
   }
+}
+
+template <bool GT>
+__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_kernel(const TrsmParams p) {
+  cq_df_body<GT>(p, (int)blockIdx.x);
+}
+
+// Up to three independent TRSMs in one launch (CTA ranges [cta0[k],
+// cta0[k+1])): the 2 x 2 split of R^{-1} -- A^{-1} and C^{-1} of the two
+// diagonal blocks, and W = B C^{-1} for the off-diagonal block B -- whose
+// chains then run side by side, each at most half as long as R^{-1}'s.
+struct TrsmBatch {
+  TrsmParams p[3];
+  int cta0[4];
+};
+
+__global__ void __launch_bounds__(CQ_TRSM_NT, 1) cqr_trsm_df_batch_kernel(const TrsmBatch b) {
+  const int x = (int)blockIdx.x;
+  const int k = x < b.cta0[1] ? 0 : (x < b.cta0[2] ? 1 : 2);
+  cq_df_body<false>(b.p[k], x - b.cta0[k]);
+}
+
+// The off-diagonal block of R^{-1} = [[A^{-1}, -A^{-1} B C^{-1}], [0, C^{-1}]]:
+// out = -Ai W with Ai = A^{-1} (h x h tiles, upper; dense column-major at
+// ld) and W = B C^{-1} (ld ldw).  One CTA per 32 x 32 output tile, the K
+// tiles I..h-1 split over the 8 warps and folded in fixed order.
+__device__ __forceinline__ void cq_dtile_mma(double (&acc)[2][4][4], const double* X, int64_t ldx,
+                                             const double* Y, int64_t ldy) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    double af[2][2], bf[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) af[mt][h2] = __ldcg(X + (int64_t)(ks * 4 + tq) * ldx + mt * 16 + h2 * 8 + g);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = __ldcg(Y + (int64_t)(nt * 8 + g) * ldy + ks * 4 + tq);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) cq_dmma(acc[mt][nt], af[mt][0], af[mt][1], bf[nt]);
+  }
+}
+
+__global__ void __launch_bounds__(256) cqr_rinv_offdiag_kernel(double* Ri, int64_t ld, int h, int nc,
+                                                               int64_t ncols, const double* W,
+                                                               int64_t ldw, const int* need) {
+  __shared__ double red[4][1024];
+  pdl_enter();
+  if (*need == 0) return;
+  const int I = (int)blockIdx.x % h, J = (int)blockIdx.x / h;  // output tile (I, h + J)
+  const int warp = threadIdx.x >> 5;
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b2][c] = 0.0;
+  for (int K = I + warp; K < h; K += 8)
+    cq_dtile_mma(acc, Ri + (int64_t)K * 32 * ld + I * 32, ld, W + (int64_t)J * 32 * ldw + K * 32, ldw);
+  cq_fold8(acc, red);
+  for (int e = threadIdx.x; e < 1024; e += 256) {
+    const int r = e & 31, c = e >> 5;
+    const int64_t gc = (int64_t)(h + J) * 32 + c;
+    if (gc < ncols)
+      Ri[gc * ld + I * 32 + r] = -(((red[0][e] + red[1][e]) + red[2][e]) + red[3][e]);
+  }
+  (void)nc;
 }
 
 // ----------------------------------------------------------------- solves
@@ -1849,7 +1930,8 @@ int cq_chol_any(const CqChain& ch, int nb, int64_t N, double shift_coef, bool pd
                       dim3(256), 0, st, true, fp));
     const CqCols none{nullptr, 0, nullptr, 0, (int64_t)rest * 32};
     TrsmParams sp{none, (int64_t)nbs * 32, nbs, ch.Rt, ch.Rinv, nullptr, 0, ch.Rf, ch.Rfi,
-                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, 0, nullptr};
+                  ch.Gt, ch.Rt, to, to + nbs, ch.vs_g, ch.vs_r, ch.vs_i, ch.skip, 0, nullptr,
+                  nullptr};
     SKL_CUDA(launch_k(cqr_trsm_df_kernel<true>, dim3((unsigned)(rest * 32 / CQ_TRSM_ROWS), ch.nv),
                       dim3(CQ_TRSM_NT), tsm, st, true, sp));
     TriParams tp{ch.Gt, ch.Rt, ch.Rinv, to, nbs, nb, ch.vs_g, ch.vs_r, ch.skip};
@@ -1878,7 +1960,7 @@ int cq_trsm(const CqCols& X, int64_t N, int nb, const CqChain& ch, int* pick, do
   SKL_CUDA(launch_k(cqr_rfrag_kernel, dim3((unsigned)(nb * (nb + 1) / 2 + nb)), dim3(256), 0, st,
                     pdl, fp));
   TrsmParams tp{X, N, nb, ch.Rt, ch.Rinv, Q, ldq, ch.Rf, ch.Rfi, nullptr, nullptr, 0, 0,
-                0, 0, 0, stop, 0, nullptr};
+                0, 0, 0, stop, 0, nullptr, nullptr};
   const unsigned grid = (unsigned)((X.d + CQ_TRSM_ROWS - 1) / CQ_TRSM_ROWS);
   SKL_CUDA(launch_k(cqr_trsm_df_kernel<false>, dim3(grid), dim3(CQ_TRSM_NT),
                     (size_t)nb * 32 * CQ_QLD * sizeof(double), st, pdl, tp));
@@ -1996,11 +2078,41 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
     // into the unused Q buffer), then x = R^{-1} r12 (r12 left in g by solve_a)
     const int64_t ldi = (int64_t)nb * 32;
     if (dual) {
-      const CqCols idc{nullptr, 0, nullptr, 0, N};
-      TrsmParams ip{idc, N, nb, Rt, Ri, Q, ldi, Rf, Rfi, nullptr, nullptr, 0, 0, 0, 0, 0,
-                    nullptr, 1, sel};
-      CQ_LAUNCH(launch_k(cqr_trsm_df_kernel<false>, dim3((unsigned)(2 * nb)), dim3(CQ_TRSM_NT),
-                         (size_t)nb * 32 * CQ_QLD * sizeof(double), st, true, ip));
+      if (nb < 8) {
+        const CqCols idc{nullptr, 0, nullptr, 0, N};
+        TrsmParams ip{idc, N, nb, Rt, Ri, Q, ldi, Rf, Rfi, nullptr, nullptr, 0, 0, 0, 0, 0,
+                      nullptr, 1, sel, nullptr};
+        CQ_LAUNCH(launch_k(cqr_trsm_df_kernel<false>, dim3((unsigned)(2 * nb)), dim3(CQ_TRSM_NT),
+                           (size_t)nb * 32 * CQ_QLD * sizeof(double), st, true, ip));
+      } else {
+        // 2 x 2 split R = [[A, B], [0, C]] at tile h: A^{-1}, C^{-1} and
+        // W = B C^{-1} side by side in one launch, then -A^{-1} W
+        const int h = nb / 2, hc = nb - h;
+        const int64_t hr = (int64_t)h * 32;
+        double* Wb = G2;  // free on this path
+        TrsmBatch tb{};
+        tb.p[0] = TrsmParams{CqCols{nullptr, 0, nullptr, 0, hr}, hr, h, Rt, Ri, Q, ldi, Rf, Rfi,
+                             nullptr, nullptr, 0, 0, 0, 0, 0, nullptr, 1, sel, nullptr};
+        tb.p[1] = TrsmParams{CqCols{nullptr, 0, nullptr, 0, N - hr}, N - hr, hc, Rt, Ri,
+                             Q + hr * ldi + hr, ldi, Rf, Rfi, nullptr, nullptr, h, 0, 0, 0, 0,
+                             nullptr, 1, sel, nullptr};
+        tb.p[2] = TrsmParams{CqCols{nullptr, 0, nullptr, 0, hr}, N - hr, hc, Rt, Ri, Wb, hr, Rf,
+                             Rfi, nullptr, nullptr, h, 0, 0, 0, 0, nullptr, 0, sel, Rt};
+        tb.cta0[0] = 0;
+        tb.cta0[1] = 2 * h;
+        tb.cta0[2] = 2 * h + 2 * hc;
+        tb.cta0[3] = 4 * h + 2 * hc;
+        const size_t bsm = (size_t)hc * 32 * CQ_QLD * sizeof(double);
+        if ((e = raise_smem_limit(cqr_trsm_df_batch_kernel, bsm)) != cudaSuccess) {
+          set_error("cqr_solve: %s", cudaGetErrorString(e));
+          rc = SKL_ERR_CUDA;
+          break;
+        }
+        CQ_LAUNCH(launch_k(cqr_trsm_df_batch_kernel, dim3((unsigned)tb.cta0[3]), dim3(CQ_TRSM_NT),
+                           bsm, st, true, tb));
+        CQ_LAUNCH(launch_k(cqr_rinv_offdiag_kernel, dim3((unsigned)(h * hc)), dim3(256), 0, st, true,
+                           Q, ldi, h, hc, N, (const double*)Wb, hr, (const int*)sel));
+      }
       CQ_LAUNCH(launch_k(cqr_trmv_kernel, dim3((unsigned)((n + 63) / 64)), dim3(CQ_RS_GROUPS * 32),
                          (size_t)n * sizeof(double), st, true, (const double*)Q, ldi, n,
                          (const double*)g, x, (const int*)sel, TrmvFinish{}));
