@@ -1726,45 +1726,53 @@ __global__ void __launch_bounds__(CQ_RS_GROUPS * 32) cqr_resid_kernel(const doub
   }
 }
 
-// g = A^T r, one warp per column (16-byte loads, eight in flight; fixed
-// shuffle tree).
+// g = A^T r: two warps per column (one per half of the rows: 16 warps per
+// CTA for the loads in flight), 16-byte loads, eight in flight; fixed
+// shuffle tree, halves added in order.
 template <bool VEC>
-__global__ void __launch_bounds__(256) cqr_gemv_t_kernel(const double* A, int64_t lda, int64_t d,
+__global__ void __launch_bounds__(512) cqr_gemv_t_kernel(const double* A, int64_t lda, int64_t d,
                                                          int64_t n, const double* r, double* g,
                                                          const int* refine) {
+  __shared__ double half1[8];
   pdl_enter();
   if (*refine == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= n) return;
-  const double* col = A + c * lda;
-  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-  int64_t i = 2 * lane;
-  if (VEC) {
-    for (; i + 7 * 64 + 1 < d; i += 8 * 64) {
-      double2 v[8], w[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, hf = w >> 3;
+  const int64_t c = (int64_t)blockIdx.x * 8 + (w & 7);
+  const int64_t dh = (d / 2 + 63) / 64 * 64;  // first half: rows [0, dh), a multiple of 64
+  const int64_t lo = hf ? dh : 0, hi = hf ? d : min(dh, d);
+  double t = 0.0;
+  if (c < n) {
+    const double* col = A + c * lda;
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    int64_t i = lo + 2 * lane;
+    if (VEC) {
+      for (; i + 7 * 64 + 1 < hi; i += 8 * 64) {
+        double2 v[8], u[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        v[k] = __ldcs(reinterpret_cast<const double2*>(col + i + k * 64));
-        w[k] = __ldcg(reinterpret_cast<const double2*>(r + i + k * 64));
-      }
+        for (int k = 0; k < 8; ++k) {
+          v[k] = __ldcs(reinterpret_cast<const double2*>(col + i + k * 64));
+          u[k] = __ldcg(reinterpret_cast<const double2*>(r + i + k * 64));
+        }
 #pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        t0 = fma(v[k].x, w[k].x, t0);
-        t1 = fma(v[k].y, w[k].y, t1);
-        t2 = fma(v[k + 1].x, w[k + 1].x, t2);
-        t3 = fma(v[k + 1].y, w[k + 1].y, t3);
+        for (int k = 0; k < 8; k += 2) {
+          t0 = fma(v[k].x, u[k].x, t0);
+          t1 = fma(v[k].y, u[k].y, t1);
+          t2 = fma(v[k + 1].x, u[k + 1].x, t2);
+          t3 = fma(v[k + 1].y, u[k + 1].y, t3);
+        }
       }
     }
-  }
-  for (; i < d; i += 64) {
-    t0 = fma(col[i], r[i], t0);
-    if (i + 1 < d) t1 = fma(col[i + 1], r[i + 1], t1);
-  }
-  double t = (t0 + t1) + (t2 + t3);
+    for (; i < hi; i += 64) {
+      t0 = fma(col[i], r[i], t0);
+      if (i + 1 < hi) t1 = fma(col[i + 1], r[i + 1], t1);
+    }
+    t = (t0 + t1) + (t2 + t3);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (lane == 0) g[c] = t;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  if (hf && lane == 0) half1[w & 7] = t;
+  __syncthreads();
+  if (!hf && lane == 0 && c < n) g[c] = t + half1[w & 7];
 }
 
 }  // namespace skl
@@ -2123,7 +2131,7 @@ extern "C" int skl_cqr_solve_async(const double* SA, int64_t ldsa, const double*
                        dim3((unsigned)((d + 63) / 64)), dim3(CQ_RS_GROUPS * 32), ysm, st, true, SA,
                        ldsa, Sb, d, n, (const double*)x, r, (const int*)refine));
     CQ_LAUNCH(launch_k(vec ? cqr_gemv_t_kernel<true> : cqr_gemv_t_kernel<false>,
-                       dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, true, SA, ldsa, d, n,
+                       dim3((unsigned)((n + 7) / 8)), dim3(512), 0, st, true, SA, ldsa, d, n,
                        (const double*)r, g, (const int*)refine));
     CQ_LAUNCH(launch_k(cqr_solve_b_kernel, dim3(1), dim3(CQ_SOLVE_NT), 0, st, true, sp));
     if (dual) {  // x += R^{-1} R^{-T} g, with the contraction check
