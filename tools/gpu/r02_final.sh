@@ -12,3 +12,6 @@ SKL_PROF_WARM_S=0.01 timeout 300 ncu --metrics gpu__time_duration.sum --clock-co
   --log-file gpurun_out/r02_cqr_launches.csv python tools/prof_qr.py 2048 256 2 cholqr > /dev/null 2>&1; echo ncu2 rc=$?
 SKL_PROF_WARM_S=0.01 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/r02_cqr_big_launches.csv python tools/prof_qr.py 8192 1024 1 cholqr > /dev/null 2>&1; echo ncu3 rc=$?
+timeout 300 python tools/time_cholqr.py 800x200 2048x256 2048x511 8192x511 2048x600 8192x1024 > gpurun_out/r02_time_cholqr.jsonl 2>&1; echo tc rc=$?
+SKL_NO_PDL=1 timeout 300 python tools/prof_cqr_kernels.py 8192 1024 10 > gpurun_out/r02_cqr_kernels_8192.txt 2>&1
+SKL_NO_PDL=1 timeout 300 python tools/prof_cqr_kernels.py 2048 256 20 1e8 > gpurun_out/r02_cqr_kernels_2048_k1e8.txt 2>&1
