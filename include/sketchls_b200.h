@@ -286,6 +286,14 @@ int skl_lsqr_fused_dev(const double* A, int64_t m, int64_t n, int64_t lda, const
 int skl_lsqr_step_dev(const double* R, int64_t ldr, int64_t n, const double* Rinv,
                       const double* z, double* v, double* v_raw, double* y, double* w, double* x,
                       double* state, void* stream);
+/* R^{-1} of the n x n upper-triangular R in full (n <= 256; Ri: n * n
+ * doubles, column-major, zero below the diagonal; device), once per
+ * preconditioned solve, and skl_lsqr_step_dev with both triangular solves
+ * as products with it. */
+int skl_lsqr_rinv_full(const double* R, int64_t ldr, int64_t n, double* Ri, void* stream);
+int skl_lsqr_step_full_dev(const double* Ri, int64_t n, const double* z, double* v,
+                           double* v_raw, double* y, double* w, double* x, double* state,
+                           void* stream);
 /* CSR operands: u_out = s (A y) - alpha u_in, *norm2 = ||u_out||^2 (rows
  * folded in stored order); and u_n = u_raw / beta, z = A^T u_n from the
  * CSC form of A (colptr int64 n+1, rowidx int32 ascending within a column,

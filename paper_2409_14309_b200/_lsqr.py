@@ -120,6 +120,13 @@ def _lsqr_device_driven(op, ws, fwork, n, Rp, ldr, Rinv, alfa, beta, atol, btol,
     The recurrence performs the host loop's IEEE operations in the same
     order, so iterates, iteration counts and stopping rule are the same."""
     P = _native.ptr
+    # R^{-1} in full once (n <= 256): the step's two triangular solves become
+    # products with it (SKL_LSQR_BLOCK_SOLVES=1 keeps the blocked solves)
+    RF = None
+    if Rp is not None and Rinv is not None and n <= 256 and not os.environ.get(
+            "SKL_LSQR_BLOCK_SOLVES"):
+        RF = device_f64((n * n,))
+        _native.call("skl_lsqr_rinv_full", Rp, ldr, n, P(RF), st)
     nst = int(_native.lib().skl_lsqr_state_size())
     state = torch.zeros(nst, dtype=torch.float64, device="cuda")
     init = torch.zeros(nst, dtype=torch.float64)
@@ -139,8 +146,12 @@ def _lsqr_device_driven(op, ws, fwork, n, Rp, ldr, Rinv, alfa, beta, atol, btol,
     itn = istop = 0
     while itn < max_iter:
         itn += 1
-        _native.call("skl_lsqr_step_dev", Rp, ldr, n, P(Rinv), P(ws.z), P(ws.v), P(ws.v_raw),
-                     P(ws.y), P(ws.w), P(ws.x), P(state), st)
+        if RF is not None:
+            _native.call("skl_lsqr_step_full_dev", P(RF), n, P(ws.z), P(ws.v), P(ws.v_raw),
+                         P(ws.y), P(ws.w), P(ws.x), P(state), st)
+        else:
+            _native.call("skl_lsqr_step_dev", Rp, ldr, n, P(Rinv), P(ws.z), P(ws.v), P(ws.v_raw),
+                         P(ws.y), P(ws.w), P(ws.x), P(state), st)
         rep.copy_(state, non_blocking=True)
         done.record()
         r_prev, r_out = r_out, r_prev

@@ -105,6 +105,9 @@ SIGNATURES: dict[str, tuple] = {
         c_int, [c_ptr, c_i64, c_i64, c_ptr, ctypes.c_double, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_lsqr_trsv_n": (c_int, [c_ptr, c_i64, c_i64, ctypes.c_double, c_ptr, c_ptr, c_ptr]),
     "skl_lsqr_rinv_blocks": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
+    "skl_lsqr_rinv_full": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
+    "skl_lsqr_step_full_dev": (
+        c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "skl_lsqr_state_size": (c_i64, []),
     "skl_lsqr_fused_dev": (
         c_int,

@@ -1091,6 +1091,87 @@ __device__ __forceinline__ void ls_recur(double* st) {
 }
 __global__ void lsqr_recur_kernel(double* st) { ls_recur(st); }
 
+// Full inverse of the n x n upper-triangular R (n <= 256), column-major with
+// ld n, zeros below the diagonal: one warp per column j, back substitution
+// right-looking over R's columns (z_i = t_i / R_ii, then t_l -= R_li z_i for
+// l < i: a coalesced column read per step; lane holds t_l for l = lane +
+// 32 q).  Once per preconditioned solve: R does not change across LSQR
+// iterations, and the step's two triangular solves become products with
+// R^{-1} (lq_gemv_full_*).
+constexpr int LQ_FULL_MAX = 256;
+
+__global__ void __launch_bounds__(256) lsqr_rinv_full_kernel(const double* __restrict__ R,
+                                                             int64_t ldr, int n,
+                                                             double* __restrict__ Ri) {
+  const int lane = threadIdx.x & 31;
+  const int j = (int)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= n) return;
+  double t[LQ_FULL_MAX / 32];
+#pragma unroll
+  for (int q = 0; q < LQ_FULL_MAX / 32; ++q) t[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+  double* col = Ri + (int64_t)j * n;
+  for (int i = j + 1 + lane; i < n; i += 32) col[i] = 0.0;
+  for (int i = j; i >= 0; --i) {
+    double ti = 0.0;
+#pragma unroll
+    for (int q = 0; q < LQ_FULL_MAX / 32; ++q)
+      if (q == (i >> 5)) ti = t[q];
+    const double zi = __shfl_sync(0xffffffffu, ti, i & 31) / R[(int64_t)i * ldr + i];
+    if (lane == (i & 31)) col[i] = zi;
+    const double* ri = R + (int64_t)i * ldr;
+#pragma unroll
+    for (int q = 0; q < LQ_FULL_MAX / 32; ++q) {
+      const int l = lane + 32 * q;
+      if (l < i) t[q] = fma(-ri[l], zi, t[q]);
+    }
+  }
+}
+
+// xs <- R^{-T} xs with RF = R^{-1} (column-major, ld n): out_j = sum_{i <= j}
+// RF[i + j n] xs_i, warp w the columns j = w (mod warps), lanes split i.
+__device__ void lq_gemv_full_t(const double* __restrict__ RF, int n, double* xs, double* tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nw) {
+    const double* col = RF + (int64_t)j * n;
+    double a = 0.0;
+    for (int i = lane; i <= j; i += 32) a = fma(col[i], xs[i], a);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) tmp[j] = a;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = tmp[i];
+  __syncthreads();
+}
+
+// xs <- R^{-1} xs: out_i = sum_{j >= i} RF[i + j n] xs_j, a thread per (row,
+// half of the columns), halves added in order.
+__device__ void lq_gemv_full_n(const double* __restrict__ RF, int n, double* xs, double* tmp) {
+  const int nh = blockDim.x / 2;
+  const int i = threadIdx.x % nh, hf = threadIdx.x / nh;
+  const int jm = (n + 1) / 2;
+  double a = 0.0;
+  if (i < n) {
+    const int j0 = hf ? max(jm, i) : i, j1 = hf ? n : jm;
+    int j = j0;
+    for (; j + 4 <= j1; j += 4) {
+      const double r0 = RF[(int64_t)j * n + i], r1 = RF[(int64_t)(j + 1) * n + i];
+      const double r2 = RF[(int64_t)(j + 2) * n + i], r3 = RF[(int64_t)(j + 3) * n + i];
+      a = fma(r0, xs[j], a);
+      a = fma(r1, xs[j + 1], a);
+      a = fma(r2, xs[j + 2], a);
+      a = fma(r3, xs[j + 3], a);
+    }
+    for (; j < j1; ++j) a = fma(RF[(int64_t)j * n + i], xs[j], a);
+  }
+  if (hf && i < n) tmp[i] = a;
+  __syncthreads();
+  if (!hf && i < n) a += tmp[i];
+  __syncthreads();
+  if (!hf && i < n) xs[i] = a;
+  __syncthreads();
+}
+
 // The whole device step after a pass in one CTA (what lsqr_trsv_t_kernel,
 // lsqr_trsv_n_kernel, lsqr_recur_kernel and lsqr_xw_kernel do in four
 // launches, with the same operations in the same order: bitwise the same
@@ -1100,7 +1181,7 @@ __global__ void lsqr_recur_kernel(double* st) { ls_recur(st); }
 __global__ void __launch_bounds__(LT_NT) lsqr_step_kernel(
     const double* __restrict__ R, int64_t ldr, int n, const double* __restrict__ Rinv,
     const double* __restrict__ z, double* v, double* v_raw, double* y, double* w, double* x,
-    double* st) {
+    double* st, const double* __restrict__ RF) {
   pdl_enter();
   extern __shared__ double xs[];
   __shared__ double red[32];
@@ -1110,7 +1191,10 @@ __global__ void __launch_bounds__(LT_NT) lsqr_step_kernel(
     // v_raw = R^-T z - beta v, ||v_raw||^2 -> LS_ALFA2
     for (int i = tid; i < n; i += LT_NT) xs[i] = z[i];
     __syncthreads();
-    if (R) lq_solve_t(R, ldr, n, xs, Rinv);
+    if (RF)
+      lq_gemv_full_t(RF, n, xs, xs + n);
+    else if (R)
+      lq_solve_t(R, ldr, n, xs, Rinv);
     double ss = 0.0;
     for (int i = tid; i < n; i += LT_NT) {
       const double vv = xs[i] - beta * v[i];
@@ -1129,7 +1213,10 @@ __global__ void __launch_bounds__(LT_NT) lsqr_step_kernel(
       xs[i] = vn;
     }
     __syncthreads();
-    if (R) lq_solve_n(R, ldr, n, xs, Rinv);
+    if (RF)
+      lq_gemv_full_n(RF, n, xs, xs + n);
+    else if (R)
+      lq_solve_n(R, ldr, n, xs, Rinv);
     for (int i = tid; i < n; i += LT_NT) y[i] = xs[i];
   }
   __syncthreads();
@@ -1165,7 +1252,34 @@ extern "C" int skl_lsqr_step_dev(const double* R, int64_t ldr, int64_t n, const 
   if (smem > 48 * 1024) SKL_CUDA(raise_smem_limit(lsqr_step_kernel, smem));
   // the pass is the kernel right before this one on the stream
   SKL_CUDA(launch_k(lsqr_step_kernel, dim3(1), dim3(LT_NT), smem, (cudaStream_t)stream, true, R,
-                    ldr, (int)n, Rinv, z, v, v_raw, y, w, x, state));
+                    ldr, (int)n, Rinv, z, v, v_raw, y, w, x, state, (const double*)nullptr));
+  return SKL_OK;
+}
+
+// R^{-1} in full (n <= 256; Ri: n * n doubles, device), once per solve.
+extern "C" int skl_lsqr_rinv_full(const double* R, int64_t ldr, int64_t n, double* Ri,
+                                  void* stream) {
+  clear_error();
+  SKL_REQUIRE(R && Ri && n >= 1 && n <= LQ_FULL_MAX && ldr >= n, SKL_ERR_INVALID,
+              "lsqr_rinv_full: bad arguments (n <= %d)", LQ_FULL_MAX);
+  lsqr_rinv_full_kernel<<<(unsigned)((n + 7) / 8), 256, 0, (cudaStream_t)stream>>>(R, ldr, (int)n,
+                                                                                   Ri);
+  SKL_CUDA_LAUNCH();
+  return SKL_OK;
+}
+
+// skl_lsqr_step_dev with both triangular solves as products with the full
+// R^{-1} (skl_lsqr_rinv_full).
+extern "C" int skl_lsqr_step_full_dev(const double* Ri, int64_t n, const double* z, double* v,
+                                      double* v_raw, double* y, double* w, double* x,
+                                      double* state, void* stream) {
+  clear_error();
+  SKL_REQUIRE(Ri && z && v && v_raw && y && w && x && state && n >= 1 && n <= LQ_FULL_MAX,
+              SKL_ERR_INVALID, "lsqr_step_full_dev: bad arguments");
+  const size_t smem = 2 * (size_t)n * sizeof(double);
+  SKL_CUDA(launch_k(lsqr_step_kernel, dim3(1), dim3(LT_NT), smem, (cudaStream_t)stream, true,
+                    (const double*)nullptr, (int64_t)n, (int)n, (const double*)nullptr, z, v, v_raw,
+                    y, w, x, state, Ri));
   return SKL_OK;
 }
 

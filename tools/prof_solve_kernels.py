@@ -1,4 +1,4 @@
-"""Kernel-level breakdown of one warm SAA solve() for a BASELINE config
+"""Kernel-level breakdown of one warm solve() (method argv[2], default saa) for a BASELINE config
 (torch.profiler CUDA activity: every kernel and copy of the solve)."""
 import sys
 from pathlib import Path
@@ -11,6 +11,7 @@ import paper_2409_14309_b200 as E  # noqa: E402
 from paper_2409_14309_b200 import workloads as W  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+method = sys.argv[2] if len(sys.argv) > 2 else "saa"
 c = W.config(cfg)
 A, b, _ = W.make_problem(c, backend="torch")
 if c.gen == "csr":
@@ -21,10 +22,10 @@ prob = E.LeastSquaresProblem(A=A, b=E.Vector(b))
 spec = E.SketchSpec(c.kind, 1, seed=W.SEED)
 opts = E.SolverOptions(d_factor=c.d / c.n)
 for _ in range(2):
-    E.solve(prob, "saa", spec, opts)
+    E.solve(prob, method, spec, opts)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    E.solve(prob, "saa", spec, opts)
+    E.solve(prob, method, spec, opts)
     torch.cuda.synchronize()
 rows = [(e.key, e.device_time_total, e.count) for e in prof.key_averages() if e.device_time_total > 0]
 tot = sum(r[1] for r in rows)
