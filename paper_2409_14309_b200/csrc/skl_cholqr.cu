@@ -1359,7 +1359,8 @@ __device__ void cq_backsolve(const double* Rt, const double* Rinv, int64_t n, do
         t1 = fma(c[j + 1], xb[j + 1], t1);
       }
     }
-    // rows 512 .. 1055 (n > 512): a second row per thread, loaded at use
+    // rows 512 .. 1023 (n > 512): a second row per thread, loaded at use
+    // (rows past 1023 lie in the last block only, so no update reaches them)
     const int64_t i2 = tid + CQ_SOLVE_ROWS;
     double s2 = 0.0;
     if (tid < CQ_SOLVE_ROWS && i2 < lo) {
@@ -1430,11 +1431,13 @@ __device__ void cq_fwdsolve_t(const double* Rt, const double* Rinv, int64_t n, d
         t1 = fma(c[j + 1], zb[j + 1], t1);
       }
     }
-    const int64_t i2 = tid + CQ_SOLVE_ROWS;  // rows 512 .. 1055
+    // rows 512 .. 1023 and 1024 .. 1055 (n > 512, n > 1024): a second and a
+    // third row per thread, loaded at use
+    const int64_t i2 = tid + CQ_SOLVE_ROWS, i3 = tid + 2 * CQ_SOLVE_ROWS;
     const bool mine2 = tid < CQ_SOLVE_ROWS && i2 >= lo + 32 && i2 < n;
-    double s2 = 0.0;
-    if (mine2) {
-      const double2* rc = reinterpret_cast<const double2*>(Rt + cq_tile(b, (int)(i2 >> 5)) * 1024 + (i2 & 31) * 32);
+    const bool mine3 = tid < CQ_SOLVE_ROWS && i3 >= lo + 32 && i3 < n;
+    auto row_dot = [&](int64_t i) {
+      const double2* rc = reinterpret_cast<const double2*>(Rt + cq_tile(b, (int)(i >> 5)) * 1024 + (i & 31) * 32);
       double u0 = 0.0, u1 = 0.0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -1442,11 +1445,14 @@ __device__ void cq_fwdsolve_t(const double* Rt, const double* Rinv, int64_t n, d
         u0 = fma(v.x, zb[2 * j], u0);
         u1 = fma(v.y, zb[2 * j + 1], u1);
       }
-      s2 = u0 + u1;
-    }
+      return u0 + u1;
+    };
+    const double s2 = mine2 ? row_dot(i2) : 0.0;
+    const double s3 = mine3 ? row_dot(i3) : 0.0;
     if (b + 1 < nbn) cq_fs_fetch(Rt, Rinv, b + 1, n, c);
     if (mine) ys[tid] -= t0 + t1;
     if (mine2) ys[i2] -= s2;
+    if (mine3) ys[i3] -= s3;
     __syncthreads();
   }
 }

@@ -183,6 +183,19 @@ def test_cholqr_variant_pick_accuracy(d, n, kappa):
     assert np.linalg.norm(x - want) / np.linalg.norm(want) <= max(1e-13, 50 * kappa * 1.1e-16)
 
 
+@pytest.mark.parametrize("d,n", [(2456, 1030), (4096, 1055)])
+def test_shifted_path_rows_past_1024(d, n):
+    # n > 1024 on the shifted path: the forward solve with R^T updates rows
+    # 1024.. with a third row per thread (once missing: x off by 5e-7 at
+    # kappa = 1e6, 4e-4 at 5e7)
+    for kappa in (1e6, 5e7):
+        SA, Sb = system(d, n, kappa=kappa, seed=7 + n)
+        x, fell_back = cqr(SA, Sb)
+        assert not fell_back
+        want = oracle_x(SA, Sb)
+        assert np.linalg.norm(x - want) / np.linalg.norm(want) <= 50 * kappa * 1.1e-16
+
+
 @pytest.mark.parametrize("d,n", [(1000, 100), (2048, 600)])
 def test_cholqr_consistent_system(d, n):
     # Sb in the range of SA: the augmented column's pivot is ~0, the
@@ -229,3 +242,21 @@ def test_shifted_only_knob_matches_oracle(tmp_path):
     out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_reduced_solve_randomised_shapes_and_conditioning():
+    # seeded sweep over both paths and every split of the kernels: block
+    # counts 1..33 (the single-cluster / blocked Cholesky boundary at 16, the
+    # 2 x 2 split of R^{-1} from 8 block columns), ragged N, kappa 1..1e9
+    rng = np.random.default_rng(2409)
+    for _ in range(24):
+        n = int(rng.integers(1, 1055))
+        d = int(n + 1 + rng.integers(1, 3 * n + 64))
+        kappa = float(10 ** rng.uniform(0, 9))
+        SA, Sb = system(d, n, kappa=kappa, seed=int(rng.integers(1 << 30)))
+        x, _ = cqr(SA, Sb)
+        want = oracle_x(SA, Sb)
+        rs, rw = np.linalg.norm(SA @ x - Sb), np.linalg.norm(SA @ want - Sb)
+        assert rs <= rw * (1 + 1e-9), (d, n, kappa, rs, rw)
+        err = np.linalg.norm(x - want) / np.linalg.norm(want)
+        assert err <= max(1e-12, 100 * kappa * 1.1e-16), (d, n, kappa, err)
