@@ -30,8 +30,8 @@ constexpr int CSR_B = 8;   // buckets (warps) per CTA
 // One round = 32 consecutive source rows of a bucket (lane l: row base + l).
 struct CsrRound {
   int64_t p0;     // first nonzero of my row
-  int64_t start;  // exclusive scan of the rows' nonzero counts (flattened index)
-  int64_t total;  // nonzeros of the round
+  int start;      // exclusive scan of the rows' nonzero counts (flattened index)
+  int total;      // nonzeros of the round (< 2^31: n < 2^26 is checked at launch)
   double s;       // my row's sign (x scale)
 };
 
@@ -45,11 +45,11 @@ struct CsrSlot {
 __device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t sg, double scale) {
   CsrRound r;
   const int lane = threadIdx.x & 31;
-  const int64_t cnt = np1 - np0;
-  int64_t incl = cnt;
+  const int cnt = (int)(np1 - np0);  // 32-bit scan: one SHFL per step
+  int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
   r.p0 = np0;
@@ -62,16 +62,16 @@ __device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t s
 // Issue the loads of flattened nonzero f of round r (owner lane = the
 // largest l with start_l <= f; among equal starts, i.e. empty rows, the
 // largest index).  The values are consumed a round later.
-__device__ __forceinline__ CsrSlot csr_fetch(const CsrRound& r, int64_t f,
+__device__ __forceinline__ CsrSlot csr_fetch(const CsrRound& r, int f,
                                              const int64_t* __restrict__ indices,
                                              const double* __restrict__ values) {
   int lo = 0;
 #pragma unroll
   for (int step = 16; step > 0; step >>= 1) {
-    const int64_t st = __shfl_sync(0xffffffffu, r.start, min(lo + step, 31));
+    const int st = __shfl_sync(0xffffffffu, r.start, min(lo + step, 31));
     if (lo + step <= 31 && st <= f) lo += step;
   }
-  const int64_t st_o = __shfl_sync(0xffffffffu, r.start, lo);
+  const int st_o = __shfl_sync(0xffffffffu, r.start, lo);
   const int64_t p0_o = __shfl_sync(0xffffffffu, r.p0, lo);
   CsrSlot sl;
   sl.s = __shfl_sync(0xffffffffu, r.s, lo);
@@ -83,6 +83,15 @@ __device__ __forceinline__ CsrSlot csr_fetch(const CsrRound& r, int64_t f,
     sl.c = indices[p];
     sl.v = values[p];
   }
+  return sl;
+}
+
+__device__ __forceinline__ CsrSlot csr_empty() {
+  CsrSlot sl;
+  sl.c = -1;
+  sl.v = 0.0;
+  sl.s = 0.0;
+  sl.ok = false;
   return sl;
 }
 
@@ -147,21 +156,23 @@ __global__ void __launch_bounds__(CSR_B * 32)
     extent(brow_at(r_beg), r_beg);
     CsrRound cur = csr_round(np0, np1, nsg, scale);
     CsrSlot a = csr_fetch(cur, lane, indices, values);
-    CsrSlot b = csr_fetch(cur, 32 + lane, indices, values);
+    CsrSlot b = cur.total > 32 ? csr_fetch(cur, 32 + lane, indices, values) : csr_empty();
     extent(brow_at(r_beg + 32), r_beg + 32);
     int32_t nj = brow_at(r_beg + 64);
     for (int64_t base = r_beg; base < r_end; base += 32) {
       // round r+1: extents arrived last iteration -> scan, issue its nonzeros
       const CsrRound nxt = csr_round(np0, np1, nsg, scale);
       const CsrSlot na = csr_fetch(nxt, lane, indices, values);
-      const CsrSlot nb = csr_fetch(nxt, 32 + lane, indices, values);
+      // the second flattened pass only when the round has > 32 nonzeros
+    // (warp-uniform; about half the rounds at ~1 nonzero per row)
+    const CsrSlot nb = nxt.total > 32 ? csr_fetch(nxt, 32 + lane, indices, values) : csr_empty();
       // round r+2 extents, round r+3 rows
       extent(nj, base + 64);
       nj = brow_at(base + 96);
       // commit round r
       csr_commit(a, my, c0, cw);
-      csr_commit(b, my, c0, cw);
-      for (int64_t f0 = 64; f0 < cur.total; f0 += 32)  // rare: > 64 nonzeros in 32 rows
+      if (cur.total > 32) csr_commit(b, my, c0, cw);
+      for (int f0 = 64; f0 < cur.total; f0 += 32)  // rare: > 64 nonzeros in 32 rows
         csr_commit(csr_fetch(cur, f0 + lane, indices, values), my, c0, cw);
       cur = nxt;
       a = na;
@@ -206,9 +217,13 @@ static int csr_launch(const int64_t* indptr, const int64_t* indices, const doubl
   SKL_REQUIRE(indptr && bucket_rows && bucket_ptr && signs && SA && m >= 1 && n >= 1 && d >= 1 &&
                   ldsa >= d,
               SKL_ERR_SHAPE, "countsketch_csr: bad arguments");
+  SKL_REQUIRE(n < (int64_t(1) << 26), SKL_ERR_SHAPE,
+              "countsketch_csr: n = %lld columns exceeds the 2^26 limit", (long long)n);
   // shared tile budget: up to 192 KiB
   const int64_t max_cw = (192 * 1024) / (CSR_B * 8) - 1;
-  const int64_t Cw = std::min<int64_t>(n, max_cw);
+  int64_t Cw = std::min<int64_t>(n, max_cw);
+  static const int64_t cw_knob = env_int("SKL_CSR_CW", 0);  // A/B knob: narrower column tiles
+  if (cw_knob >= 8) Cw = std::min<int64_t>(Cw, cw_knob);
   const size_t smem = (size_t)(Cw + 1) * CSR_B * sizeof(double);
   SKL_CUDA(raise_smem_limit(countsketch_csr_kernel, smem));
   dim3 grid((unsigned)((d + CSR_B - 1) / CSR_B), (unsigned)((n + Cw - 1) / Cw));
