@@ -29,10 +29,10 @@ constexpr int CSR_B = 8;   // buckets (warps) per CTA
 
 // One round = 32 consecutive source rows of a bucket (lane l: row base + l).
 struct CsrRound {
-  int64_t p0;     // first nonzero of my row
+  int64_t q;      // first nonzero of my row minus start (nonzero f sits at q + f)
   int start;      // exclusive scan of the rows' nonzero counts (flattened index)
   int total;      // nonzeros of the round (< 2^31: n < 2^26 is checked at launch)
-  double s;       // my row's sign (x scale)
+  int sg;         // my row's sign (+-1; 0 for a row past the bucket)
 };
 
 // A prefetched nonzero of a round's flattened order: column, value, row sign.
@@ -42,7 +42,7 @@ struct CsrSlot {
   bool ok;
 };
 
-__device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t sg, double scale) {
+__device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t sg) {
   CsrRound r;
   const int lane = threadIdx.x & 31;
   const int cnt = (int)(np1 - np0);  // 32-bit scan: one SHFL per step
@@ -52,10 +52,10 @@ __device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t s
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  r.p0 = np0;
   r.start = incl - cnt;
+  r.q = np0 - r.start;
   r.total = __shfl_sync(0xffffffffu, incl, 31);
-  r.s = (double)sg * scale;  // +-1 (CountSketch) or +-fl(1/sqrt(s)) (sparse sign)
+  r.sg = sg;
   return r;
 }
 
@@ -64,22 +64,23 @@ __device__ __forceinline__ CsrRound csr_round(int64_t np0, int64_t np1, int8_t s
 // largest index).  The values are consumed a round later.
 __device__ __forceinline__ CsrSlot csr_fetch(const CsrRound& r, int f,
                                              const int64_t* __restrict__ indices,
-                                             const double* __restrict__ values) {
+                                             const double* __restrict__ values, double scale) {
   int lo = 0;
 #pragma unroll
   for (int step = 16; step > 0; step >>= 1) {
     const int st = __shfl_sync(0xffffffffu, r.start, min(lo + step, 31));
     if (lo + step <= 31 && st <= f) lo += step;
   }
-  const int st_o = __shfl_sync(0xffffffffu, r.start, lo);
-  const int64_t p0_o = __shfl_sync(0xffffffffu, r.p0, lo);
+  const int64_t q_o = __shfl_sync(0xffffffffu, r.q, lo);
   CsrSlot sl;
-  sl.s = __shfl_sync(0xffffffffu, r.s, lo);
+  // +-1 (CountSketch) or +-fl(1/sqrt(s)) (sparse sign): the same product as
+  // forming the signed scale per row
+  sl.s = (double)__shfl_sync(0xffffffffu, r.sg, lo) * scale;
   sl.ok = f < r.total;
   sl.c = -1;
   sl.v = 0.0;
   if (sl.ok) {
-    const int64_t p = p0_o + (f - st_o);
+    const int64_t p = q_o + f;
     sl.c = indices[p];
     sl.v = values[p];
   }
@@ -154,18 +155,18 @@ __global__ void __launch_bounds__(CSR_B * 32)
     // prologue: round 0 extents (dependent), round 0 nonzeros, round 1
     // extents, round 2 rows
     extent(brow_at(r_beg), r_beg);
-    CsrRound cur = csr_round(np0, np1, nsg, scale);
-    CsrSlot a = csr_fetch(cur, lane, indices, values);
-    CsrSlot b = cur.total > 32 ? csr_fetch(cur, 32 + lane, indices, values) : csr_empty();
+    CsrRound cur = csr_round(np0, np1, nsg);
+    CsrSlot a = csr_fetch(cur, lane, indices, values, scale);
+    CsrSlot b = cur.total > 32 ? csr_fetch(cur, 32 + lane, indices, values, scale) : csr_empty();
     extent(brow_at(r_beg + 32), r_beg + 32);
     int32_t nj = brow_at(r_beg + 64);
     for (int64_t base = r_beg; base < r_end; base += 32) {
       // round r+1: extents arrived last iteration -> scan, issue its nonzeros
-      const CsrRound nxt = csr_round(np0, np1, nsg, scale);
-      const CsrSlot na = csr_fetch(nxt, lane, indices, values);
+      const CsrRound nxt = csr_round(np0, np1, nsg);
+      const CsrSlot na = csr_fetch(nxt, lane, indices, values, scale);
       // the second flattened pass only when the round has > 32 nonzeros
     // (warp-uniform; about half the rounds at ~1 nonzero per row)
-    const CsrSlot nb = nxt.total > 32 ? csr_fetch(nxt, 32 + lane, indices, values) : csr_empty();
+      const CsrSlot nb = nxt.total > 32 ? csr_fetch(nxt, 32 + lane, indices, values, scale) : csr_empty();
       // round r+2 extents, round r+3 rows
       extent(nj, base + 64);
       nj = brow_at(base + 96);
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(CSR_B * 32)
       csr_commit(a, my, c0, cw);
       if (cur.total > 32) csr_commit(b, my, c0, cw);
       for (int f0 = 64; f0 < cur.total; f0 += 32)  // rare: > 64 nonzeros in 32 rows
-        csr_commit(csr_fetch(cur, f0 + lane, indices, values), my, c0, cw);
+        csr_commit(csr_fetch(cur, f0 + lane, indices, values, scale), my, c0, cw);
       cur = nxt;
       a = na;
       b = nb;
